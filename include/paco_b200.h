@@ -1,0 +1,117 @@
+/*
+ * paco_b200.h -- C ABI of the B200 (sm_100a) PACO semiring-MM library.
+ *
+ * This is the drop-in boundary for the reference's semiring-MM hot path
+ * (/root/reference/pkg/src/paco/matmul.py).  Every entry point replaces one
+ * NumPy operation the reference executes per task:
+ *
+ *   paco_mm        <- mm_seq(A, B, C, semiring, base)            matmul.py:342-397
+ *                     i.e. the COMPUTE-task body of mm_execute   matmul.py:441-454
+ *                     and Semiring.block_mm(C, A, B)             matmul.py:41,45-50
+ *   paco_fold      <- REDUCE-task body: copyto(t, vadd(t, temp)); temp.fill(zero)
+ *                                                                matmul.py:455-460
+ *   paco_fill      <- np.full(shape, semiring.zero)              matmul.py:430-433
+ *   paco_mm_naive  <- mm_oracle(A, B, semiring) (defining sums)  matmul.py:400-414
+ *   paco_plan_one_piece <- mm_one_piece_partition(n, m, k, p)    matmul.py:250-300
+ *                     (cuboid geometry only; used for the CTA-level plan)
+ *   paco_lincomb   <- Strassen S_r/T_r formation and C-block combination
+ *                     (reference has no code: SPEC.md:474-552)
+ *
+ * Conventions: plain pointers, row-major matrices with a leading dimension in
+ * ELEMENTS, int64 extents, an explicit device ordinal and cudaStream_t passed
+ * as void*.  All calls are asynchronous on `stream`, re-entrant, and never
+ * allocate user-visible memory.  Status: 0 = OK, negative = error; the text of
+ * the last error on the calling thread is returned by paco_last_error().
+ */
+#ifndef PACO_B200_H_
+#define PACO_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PACO_ABI_VERSION 1
+#define PACO_MAX_PIECES 640
+
+/* status codes */
+#define PACO_OK 0
+#define PACO_ERR_ARG (-1)         /* bad argument (maps to ValueError / PlanError) */
+#define PACO_ERR_CUDA (-2)        /* CUDA runtime failure */
+#define PACO_ERR_UNSUPPORTED (-3) /* layout/alignment the kernel cannot take */
+
+/* semiring ids (element types: A, B -> C) */
+#define PACO_SR_INT_I64 0         /* (+,x)  int64,int64 -> int64 (wrapping)   = SEMIRING_INT   matmul.py:53 */
+#define PACO_SR_INT_I32_I64 1     /* (+,x)  int32,int32 -> int64                                        */
+#define PACO_SR_F64 2             /* (+,x)  f64 -> f64                         = SEMIRING_F64   matmul.py:54 */
+#define PACO_SR_MINPLUS_I64 3     /* (min,+) int64 wrapping add, zero 2^62     = SEMIRING_MINPLUS matmul.py:55 */
+#define PACO_SR_MINPLUS_SAT32 4   /* (min,+) int32 storage, domain [0,2^30], INF=2^30, saturating      */
+#define PACO_SR_MAXPLUS_SAT32 5   /* (max,+) int32 storage, domain [-2^30,2^30), -INF=-2^30, saturating */
+#define PACO_SR_F32 6             /* (+,x)  f32 -> f32 (FFMA)                                          */
+#define PACO_SR_BF16_F32 7        /* (+,x)  bf16,bf16 -> f32 (tcgen05 tensor cores)                    */
+#define PACO_SR_COUNT 8
+
+#define PACO_TROPICAL_INF (1 << 30)
+
+/* paco_mm flags */
+#define PACO_MM_OVERWRITE 1 /* C = A (x) B: C is not read (caller guarantees C == zero) */
+
+/* dtype ids for paco_lincomb */
+#define PACO_DT_F32 0
+#define PACO_DT_F64 1
+#define PACO_DT_I64 2
+
+/*
+ * C (+)= A (x) B on `device`/`stream`.  A is n x k (lda), B is k x m (ldb),
+ * C is n x m (ldc).  `pieces` is an optional HOST array of n_pieces x 6 int32
+ * (ti0, tj0, tl0, tn, tm, tk) in units of the kernel's tile shape (see
+ * paco_mm_tile_shape): the CTA-level PACO plan, one persistent CTA per
+ * piece.  Pass NULL/0 to let the library build the MM-1-Piece plan over
+ * 148 x ctas_per_sm workers itself.  Pieces that split k fold with atomics.
+ */
+int paco_mm(int device, void* stream, int semiring, const void* A, int64_t lda, const void* B,
+            int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
+            const int32_t* pieces, int n_pieces, int flags);
+
+/* Tile shape (bm, bn, bk) and resident CTAs per SM of the kernel paco_mm uses. */
+int paco_mm_tile_shape(int semiring, int* bm, int* bn, int* bk, int* ctas_per_sm);
+
+/* Cuboid geometry of mm_one_piece_partition(n, m, k, p): writes p rows of
+ * (i0, j0, l0, n, m, k) into out[p*6], worker order.  Host only. */
+int paco_plan_one_piece(int64_t n, int64_t m, int64_t k, int p, int64_t* out);
+
+/* dst (+)= src elementwise (n x m views); if reset_src, src = semiring zero. */
+int paco_fold(int device, void* stream, int semiring, void* dst, int64_t ld_dst, void* src,
+              int64_t ld_src, int64_t n, int64_t m, int reset_src);
+
+/* dst = semiring zero (the value the reference fills temporaries with). */
+int paco_fill(int device, void* stream, int semiring, void* dst, int64_t ld, int64_t n, int64_t m);
+
+/* Device ground truth: C = C (+) (defining sum over l), one thread per element. */
+int paco_mm_naive(int device, void* stream, int semiring, const void* A, int64_t lda,
+                  const void* B, int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m,
+                  int64_t k);
+
+/* out (= or +=) sum_i coef[i] * in[i] over n x m views (coef in {-1, +1}). */
+int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out, int64_t n,
+                 int64_t m, int nin, const void* const* ins, const int64_t* lds,
+                 const int32_t* coefs, int accumulate);
+
+/* Enable peer access from `device` to `peer` (idempotent). */
+int paco_enable_peer(int device, int peer);
+
+/* ALU issue-rate probe: runs `which` (0 = VIADDMNMX.U32 min-plus, 1 = VIADDMNMX.S32
+ * max-plus, 2 = FFMA, 3 = IMAD.WIDE, 4 = DFMA) on every SM and returns the
+ * measured terms per clock per SM and the SM clock (MHz) seen during the run. */
+int paco_alu_probe(int device, void* stream, int which, int iters, double* terms_per_clk_sm,
+                   double* sm_mhz);
+
+const char* paco_last_error(void);
+int paco_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PACO_B200_H_ */

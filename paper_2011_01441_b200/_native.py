@@ -1,0 +1,119 @@
+"""ctypes binding of libpaco_b200.so (the C ABI in include/paco_b200.h).
+
+The library is built in-tree by ``__graft_entry__.build()``.  There is no
+fallback: if the shared object is missing every compute entry point raises.
+ctypes releases the GIL for the duration of each call, so the per-worker
+threads of ``execute_plan(mode="parallel")`` enqueue concurrently.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .plan import PlanError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpaco_b200.so")
+
+# semiring ids (include/paco_b200.h)
+SR_INT_I64 = 0
+SR_INT_I32_I64 = 1
+SR_F64 = 2
+SR_MINPLUS_I64 = 3
+SR_MINPLUS_SAT32 = 4
+SR_MAXPLUS_SAT32 = 5
+SR_F32 = 6
+SR_BF16_F32 = 7
+
+DT_F32, DT_F64, DT_I64 = 0, 1, 2
+
+MM_OVERWRITE = 1
+TROPICAL_INF = 1 << 30
+MAX_PIECES = 640
+
+OK, ERR_ARG, ERR_CUDA, ERR_UNSUPPORTED = 0, -1, -2, -3
+
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+_int = ctypes.c_int
+
+# name -> (restype, argtypes); every symbol the header declares
+SIGNATURES = {
+    "paco_mm": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64,
+                       ctypes.POINTER(ctypes.c_int32), _int, _int]),
+    "paco_mm_tile_shape": (_int, [_int] + [ctypes.POINTER(_int)] * 4),
+    "paco_plan_one_piece": (_int, [_i64, _i64, _i64, _int, ctypes.POINTER(_i64)]),
+    "paco_fold": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _i64, _i64, _int]),
+    "paco_fill": (_int, [_int, _vp, _int, _vp, _i64, _i64, _i64]),
+    "paco_mm_naive": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64]),
+    "paco_lincomb": (_int, [_int, _vp, _int, _vp, _i64, _i64, _i64, _int,
+                            ctypes.POINTER(_vp), ctypes.POINTER(_i64),
+                            ctypes.POINTER(ctypes.c_int32), _int]),
+    "paco_enable_peer": (_int, [_int, _int]),
+    "paco_alu_probe": (_int, [_int, _vp, _int, _int, ctypes.POINTER(ctypes.c_double),
+                              ctypes.POINTER(ctypes.c_double)]),
+    "paco_last_error": (ctypes.c_char_p, []),
+    "paco_abi_version": (_int, []),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class NativeError(RuntimeError):
+    """CUDA-side failure reported by the C ABI."""
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise NativeError(
+                    f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                    " -- there is no CPU fallback")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            if lib.paco_abi_version() != 1:
+                raise NativeError("libpaco_b200.so ABI version mismatch; rebuild")
+            _lib = lib
+    return _lib
+
+
+def check(rc: int) -> None:
+    """Map C status codes to the reference's exception types."""
+    if rc == OK:
+        return
+    msg = load().paco_last_error().decode(errors="replace")
+    if rc == ERR_ARG:
+        raise PlanError(msg) if "piece" in msg or "worker" in msg else ValueError(msg)
+    if rc == ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise NativeError(msg)
+
+
+def tile_shape(sr: int) -> tuple[int, int, int, int]:
+    vals = [_int() for _ in range(4)]
+    check(load().paco_mm_tile_shape(sr, *[ctypes.byref(v) for v in vals]))
+    return tuple(v.value for v in vals)
+
+
+def plan_one_piece(n: int, m: int, k: int, p: int) -> list[tuple[int, ...]]:
+    """Native MM-1-Piece geometry: p rows of (i0, j0, l0, n, m, k)."""
+    buf = (_i64 * (6 * p))()
+    check(load().paco_plan_one_piece(n, m, k, p, buf))
+    return [tuple(buf[6 * i:6 * i + 6]) for i in range(p)]
+
+
+def pieces_array(pieces):
+    """Flatten [(ti0, tj0, tl0, tn, tm, tk), ...] into a ctypes int32 array."""
+    if not pieces:
+        return None, 0
+    if len(pieces) > MAX_PIECES:
+        raise PlanError(f"{len(pieces)} CTA pieces exceed PACO_MAX_PIECES={MAX_PIECES}")
+    flat = [int(v) for pc in pieces for v in pc]
+    return (ctypes.c_int32 * len(flat))(*flat), len(pieces)

@@ -1,0 +1,181 @@
+// extern "C" boundary of libpaco_b200.so (declared in include/paco_b200.h).
+// Validates arguments, selects the device, maps semirings to kernels and
+// reports errors through return codes + a thread-local message.
+#include <cstdarg>
+#include <cstdio>
+#include <vector>
+
+#include "common.cuh"
+
+namespace paco {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+// defined in the kernel translation units
+int launch_mm_simt(int sr, int device, cudaStream_t stream, const void* A, int64_t lda, const void* B,
+                   int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
+                   const int32_t* pieces, int n_pieces, int flags);
+int simt_tile_shape(int sr, int* bm, int* bn, int* bk, int* cps);
+int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B,
+                      int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
+                      const int32_t* pieces, int n_pieces, int flags);
+int bf16_tile_shape(int* bm, int* bn, int* bk, int* cps);
+int launch_fold(int sr, cudaStream_t st, void* dst, int64_t ldd, void* src, int64_t lds, int64_t n,
+                int64_t m, int reset);
+int launch_fill(int sr, cudaStream_t st, void* dst, int64_t ld, int64_t n, int64_t m);
+int launch_naive(int sr, cudaStream_t st, const void* A, int64_t lda, const void* B, int64_t ldb,
+                 void* C, int64_t ldc, int64_t n, int64_t m, int64_t k);
+int launch_lincomb(int dtype, cudaStream_t st, void* out, int64_t ldo, int64_t n, int64_t m, int nin,
+                   const void* const* ins, const int64_t* lds, const int32_t* coefs, int acc);
+int run_alu_probe(cudaStream_t st, int which, int iters, double* tpc, double* mhz);
+struct Box;
+}  // namespace paco
+
+using namespace paco;
+
+namespace {
+int check_sr(int sr) {
+  if (sr < 0 || sr >= PACO_SR_COUNT) {
+    set_error("unknown semiring id %d", sr);
+    return PACO_ERR_ARG;
+  }
+  return PACO_OK;
+}
+
+int use_device(int device) {
+  int cur = -1;
+  PACO_CUDA_TRY(cudaGetDevice(&cur));
+  if (cur != device) PACO_CUDA_TRY(cudaSetDevice(device));
+  return PACO_OK;
+}
+
+int check_view(const char* what, const void* p, int64_t ld, int64_t rows, int64_t cols) {
+  if (rows < 0 || cols < 0) {
+    set_error("%s: negative extent %lld x %lld", what, (long long)rows, (long long)cols);
+    return PACO_ERR_ARG;
+  }
+  if (rows > 0 && cols > 0) {
+    if (p == nullptr) {
+      set_error("%s: null pointer", what);
+      return PACO_ERR_ARG;
+    }
+    if (ld < cols) {
+      set_error("%s: leading dimension %lld < columns %lld", what, (long long)ld, (long long)cols);
+      return PACO_ERR_ARG;
+    }
+  }
+  return PACO_OK;
+}
+}  // namespace
+
+#define PACO_TRY(expr)            \
+  do {                            \
+    int _rc = (expr);             \
+    if (_rc != PACO_OK) return _rc; \
+  } while (0)
+
+extern "C" {
+
+const char* paco_last_error(void) { return g_err; }
+int paco_abi_version(void) { return PACO_ABI_VERSION; }
+
+int paco_mm(int device, void* stream, int semiring, const void* A, int64_t lda, const void* B,
+            int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces,
+            int n_pieces, int flags) {
+  PACO_TRY(check_sr(semiring));
+  PACO_TRY(check_view("A", A, lda, n, k));
+  PACO_TRY(check_view("B", B, ldb, k, m));
+  PACO_TRY(check_view("C", C, ldc, n, m));
+  if (n == 0 || m == 0) return PACO_OK;
+  PACO_TRY(use_device(device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (k == 0) {
+    // empty reduction: C (+)= zero leaves C as is, or C = zero when overwriting
+    return (flags & PACO_MM_OVERWRITE) ? launch_fill(semiring, st, C, ldc, n, m) : PACO_OK;
+  }
+  if (semiring == PACO_SR_BF16_F32)
+    return launch_mm_bf16_tc(device, st, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
+  return launch_mm_simt(semiring, device, st, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
+}
+
+int paco_mm_tile_shape(int semiring, int* bm, int* bn, int* bk, int* cps) {
+  PACO_TRY(check_sr(semiring));
+  if (!bm || !bn || !bk || !cps) {
+    set_error("paco_mm_tile_shape: null output pointer");
+    return PACO_ERR_ARG;
+  }
+  if (semiring == PACO_SR_BF16_F32) return bf16_tile_shape(bm, bn, bk, cps);
+  return simt_tile_shape(semiring, bm, bn, bk, cps);
+}
+
+int paco_fold(int device, void* stream, int semiring, void* dst, int64_t ld_dst, void* src,
+              int64_t ld_src, int64_t n, int64_t m, int reset_src) {
+  PACO_TRY(check_sr(semiring));
+  PACO_TRY(check_view("dst", dst, ld_dst, n, m));
+  PACO_TRY(check_view("src", src, ld_src, n, m));
+  PACO_TRY(use_device(device));
+  return launch_fold(semiring, static_cast<cudaStream_t>(stream), dst, ld_dst, src, ld_src, n, m, reset_src);
+}
+
+int paco_fill(int device, void* stream, int semiring, void* dst, int64_t ld, int64_t n, int64_t m) {
+  PACO_TRY(check_sr(semiring));
+  PACO_TRY(check_view("dst", dst, ld, n, m));
+  PACO_TRY(use_device(device));
+  return launch_fill(semiring, static_cast<cudaStream_t>(stream), dst, ld, n, m);
+}
+
+int paco_mm_naive(int device, void* stream, int semiring, const void* A, int64_t lda, const void* B,
+                  int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k) {
+  PACO_TRY(check_sr(semiring));
+  PACO_TRY(check_view("A", A, lda, n, k));
+  PACO_TRY(check_view("B", B, ldb, k, m));
+  PACO_TRY(check_view("C", C, ldc, n, m));
+  PACO_TRY(use_device(device));
+  return launch_naive(semiring, static_cast<cudaStream_t>(stream), A, lda, B, ldb, C, ldc, n, m, k);
+}
+
+int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out, int64_t n, int64_t m,
+                 int nin, const void* const* ins, const int64_t* lds, const int32_t* coefs,
+                 int accumulate) {
+  PACO_TRY(check_view("out", out, ld_out, n, m));
+  for (int q = 0; q < nin; ++q) PACO_TRY(check_view("in", ins[q], lds[q], n, m));
+  PACO_TRY(use_device(device));
+  return launch_lincomb(dtype, static_cast<cudaStream_t>(stream), out, ld_out, n, m, nin, ins, lds,
+                        coefs, accumulate);
+}
+
+int paco_enable_peer(int device, int peer) {
+  if (device == peer) return PACO_OK;
+  int can = 0;
+  PACO_CUDA_TRY(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) {
+    set_error("device %d cannot access peer %d", device, peer);
+    return PACO_ERR_UNSUPPORTED;
+  }
+  PACO_TRY(use_device(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return PACO_OK;
+  }
+  PACO_CUDA_TRY(e);
+  return PACO_OK;
+}
+
+int paco_alu_probe(int device, void* stream, int which, int iters, double* tpc, double* mhz) {
+  if (!tpc || !mhz || iters < 1) {
+    set_error("paco_alu_probe: bad arguments");
+    return PACO_ERR_ARG;
+  }
+  PACO_TRY(use_device(device));
+  return run_alu_probe(static_cast<cudaStream_t>(stream), which, iters, tpc, mhz);
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+// Shared definitions for the sm_100a PACO semiring-MM library.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/paco_b200.h"
+
+namespace paco {
+
+constexpr int kNumSMs = 148;
+constexpr int kMaxPieces = PACO_MAX_PIECES;
+
+// One CTA-level PACO piece in TILE units (tile sizes are kernel-specific).
+// A piece whose k-range does not cover the whole k extent folds its partial C
+// face with an atomic (+) -- exact for the integer / tropical semirings.
+struct Piece {
+  int32_t ti0, tj0, tl0;  // tile offsets along n, m, k
+  int32_t tn, tm, tk;     // extents in tiles
+};
+
+struct PieceTable {
+  int32_t count;
+  int32_t ksplit;  // 1 if any piece covers a strict sub-range of k
+  Piece p[kMaxPieces];
+};
+
+// thread-local error text behind paco_last_error()
+void set_error(const char* fmt, ...);
+
+#define PACO_CUDA_TRY(expr)                                                     \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) {                                                    \
+      ::paco::set_error("%s:%d %s -> %s", __FILE__, __LINE__, #expr,            \
+                        cudaGetErrorString(_e));                                \
+      return PACO_ERR_CUDA;                                                     \
+    }                                                                           \
+  } while (0)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte async copy with zero fill of the bytes past `src_bytes`.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+}  // namespace paco

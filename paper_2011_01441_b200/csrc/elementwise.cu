@@ -1,0 +1,235 @@
+// Elementwise companions of the PACO hot path on sm_100a:
+//   fold     REDUCE body  t (+)= temp ; temp = zero        (matmul.py:455-460)
+//   fill     temp = semiring zero                          (matmul.py:430-433)
+//   naive    defining-sum ground truth, one thread/element (matmul.py:400-414)
+//   lincomb  Strassen S/T formation and C-block combination
+// All are HBM-bound grid-stride kernels over 2-D strided views; the grid is a
+// multiple of the 148 SMs.
+#include <cstdio>
+
+#include "common.cuh"
+#include "semiring_ops.cuh"
+
+namespace paco {
+
+namespace {
+int ew_grid(int64_t n_elems, int threads) {
+  const int64_t want = (n_elems + threads - 1) / threads;
+  const int64_t cap = int64_t(kNumSMs) * 16;
+  return int(want < 1 ? 1 : (want > cap ? cap : want));
+}
+}  // namespace
+
+template <class Op>
+__global__ void fold_kernel(typename Op::TC* dst, int64_t ldd, typename Op::TC* src, int64_t lds,
+                            int64_t n, int64_t m, int reset) {
+  const int64_t total = n * m;
+  const auto z = Op::zero();
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / m, j = e - i * m;
+    typename Op::TC* s = src + i * lds + j;
+    typename Op::TC* d = dst + i * ldd + j;
+    *d = Op::combine(*d, *s);
+    if (reset) *s = z;
+  }
+}
+
+template <class Op>
+__global__ void fill_kernel(typename Op::TC* dst, int64_t ld, int64_t n, int64_t m) {
+  const int64_t total = n * m;
+  const auto z = Op::zero();
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / m, j = e - i * m;
+    dst[i * ld + j] = z;
+  }
+}
+
+// mm_oracle (matmul.py:400-414): acc starts at the semiring identity, folds
+// every term in l order, then C = C (+) acc.  No tiling, no shared memory: an
+// independent device-side ground truth for the tiled kernels.
+template <class Op>
+__global__ void naive_kernel(const typename Op::TA* A, int64_t lda, const typename Op::TB* B,
+                             int64_t ldb, typename Op::TC* C, int64_t ldc, int64_t n, int64_t m,
+                             int64_t k) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (j >= m || i >= n) return;
+  typename Op::Acc acc = Op::identity();
+  for (int64_t l = 0; l < k; ++l) acc = Op::mac(acc, A[i * lda + l], B[l * ldb + j]);
+  C[i * ldc + j] = Op::combine(C[i * ldc + j], Op::finish(acc));
+}
+
+template <class T, int NIN>
+struct LinArgs {
+  const T* in[NIN];
+  int64_t ld[NIN];
+  int32_t coef[NIN];
+};
+
+template <class T, int NIN>
+__global__ void lincomb_kernel(T* out, int64_t ldo, int64_t n, int64_t m, const LinArgs<T, NIN> a,
+                               int nin, int accumulate) {
+  const int64_t total = n * m;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / m, j = e - i * m;
+    T v = accumulate ? out[i * ldo + j] : T(0);
+#pragma unroll
+    for (int q = 0; q < NIN; ++q) {
+      if (q < nin) {
+        const T x = a.in[q][i * a.ld[q] + j];
+        v = a.coef[q] > 0 ? v + x : v - x;
+      }
+    }
+    out[i * ldo + j] = v;
+  }
+}
+
+int launch_fold(int sr, cudaStream_t st, void* dst, int64_t ldd, void* src, int64_t lds, int64_t n,
+                int64_t m, int reset) {
+  if (n <= 0 || m <= 0) return PACO_OK;
+  return dispatch_op(sr, [&](auto op) -> int {
+    using Op = decltype(op);
+    using TC = typename Op::TC;
+    fold_kernel<Op><<<ew_grid(n * m, 256), 256, 0, st>>>(static_cast<TC*>(dst), ldd,
+                                                         static_cast<TC*>(src), lds, n, m, reset);
+    PACO_CUDA_TRY(cudaGetLastError());
+    return PACO_OK;
+  });
+}
+
+int launch_fill(int sr, cudaStream_t st, void* dst, int64_t ld, int64_t n, int64_t m) {
+  if (n <= 0 || m <= 0) return PACO_OK;
+  return dispatch_op(sr, [&](auto op) -> int {
+    using Op = decltype(op);
+    fill_kernel<Op><<<ew_grid(n * m, 256), 256, 0, st>>>(static_cast<typename Op::TC*>(dst), ld, n, m);
+    PACO_CUDA_TRY(cudaGetLastError());
+    return PACO_OK;
+  });
+}
+
+int launch_naive(int sr, cudaStream_t st, const void* A, int64_t lda, const void* B, int64_t ldb,
+                 void* C, int64_t ldc, int64_t n, int64_t m, int64_t k) {
+  if (n <= 0 || m <= 0) return PACO_OK;
+  if (n > 65535) {
+    set_error("paco_mm_naive: n=%lld exceeds the 65535-row grid limit", (long long)n);
+    return PACO_ERR_ARG;
+  }
+  return dispatch_op(sr, [&](auto op) -> int {
+    using Op = decltype(op);
+    dim3 grid(unsigned((m + 127) / 128), unsigned(n));
+    naive_kernel<Op><<<grid, 128, 0, st>>>(static_cast<const typename Op::TA*>(A), lda,
+                                           static_cast<const typename Op::TB*>(B), ldb,
+                                           static_cast<typename Op::TC*>(C), ldc, n, m, k);
+    PACO_CUDA_TRY(cudaGetLastError());
+    return PACO_OK;
+  });
+}
+
+template <class T>
+int lincomb_t(cudaStream_t st, void* out, int64_t ldo, int64_t n, int64_t m, int nin,
+              const void* const* ins, const int64_t* lds, const int32_t* coefs, int acc) {
+  LinArgs<T, 4> a{};
+  for (int q = 0; q < nin; ++q) {
+    a.in[q] = static_cast<const T*>(ins[q]);
+    a.ld[q] = lds[q];
+    a.coef[q] = coefs[q];
+  }
+  lincomb_kernel<T, 4><<<ew_grid(n * m, 256), 256, 0, st>>>(static_cast<T*>(out), ldo, n, m, a, nin, acc);
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
+int launch_lincomb(int dtype, cudaStream_t st, void* out, int64_t ldo, int64_t n, int64_t m, int nin,
+                   const void* const* ins, const int64_t* lds, const int32_t* coefs, int acc) {
+  if (nin < 0 || nin > 4) {
+    set_error("paco_lincomb: nin=%d (1..4 supported)", nin);
+    return PACO_ERR_ARG;
+  }
+  if (n <= 0 || m <= 0) return PACO_OK;
+  switch (dtype) {
+    case PACO_DT_F32: return lincomb_t<float>(st, out, ldo, n, m, nin, ins, lds, coefs, acc);
+    case PACO_DT_F64: return lincomb_t<double>(st, out, ldo, n, m, nin, ins, lds, coefs, acc);
+    case PACO_DT_I64: return lincomb_t<long long>(st, out, ldo, n, m, nin, ins, lds, coefs, acc);
+    default: set_error("paco_lincomb: unknown dtype %d", dtype); return PACO_ERR_ARG;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ALU issue-rate probe (the roofline denominator for the non-tensor kernels).
+// 32 independent accumulators per thread, 8 warps x 2 CTAs per SM; per-SM
+// terms/clock from clock64 and the SM clock from %globaltimer.
+// ---------------------------------------------------------------------------
+template <int V>
+__global__ void __launch_bounds__(256, 2) alu_probe_kernel(uint32_t* sink, long long* cyc, long long* ns,
+                                                           int iters, uint32_t seed) {
+  constexpr int N = 32;
+  uint32_t acc[N], x[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    acc[i] = seed * (i + 3) + threadIdx.x;
+    x[i] = seed ^ (i * 977u + threadIdx.x);
+  }
+  uint32_t y = seed + threadIdx.x;
+  __syncthreads();
+  long long t0 = clock64(), g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (V == 0) acc[i] = min(acc[i], x[i] + y);
+      if (V == 1) acc[i] = uint32_t(max(int(acc[i]), int(x[i] + y)));
+      if (V == 2) acc[i] = __float_as_uint(fmaf(__uint_as_float(x[i]), __uint_as_float(y), __uint_as_float(acc[i])));
+    }
+    y += 0x9e3779b9u;
+  }
+  long long t1 = clock64(), g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) s ^= acc[i];
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) {
+    cyc[blockIdx.x] = t1 - t0;
+    ns[blockIdx.x] = g1 - g0;
+  }
+}
+
+int run_alu_probe(cudaStream_t st, int which, int iters, double* tpc, double* mhz) {
+  if (which < 0 || which > 2) {
+    set_error("paco_alu_probe: which=%d not in 0..2", which);
+    return PACO_ERR_ARG;
+  }
+  const int blocks = kNumSMs * 2, threads = 256;
+  uint32_t* sink;
+  long long *cyc, *ns;
+  PACO_CUDA_TRY(cudaMallocAsync(&sink, size_t(blocks) * threads * 4, st));
+  PACO_CUDA_TRY(cudaMallocAsync(&cyc, blocks * 8, st));
+  PACO_CUDA_TRY(cudaMallocAsync(&ns, blocks * 8, st));
+  if (which == 0) alu_probe_kernel<0><<<blocks, threads, 0, st>>>(sink, cyc, ns, iters, 7);
+  if (which == 1) alu_probe_kernel<1><<<blocks, threads, 0, st>>>(sink, cyc, ns, iters, 7);
+  if (which == 2) alu_probe_kernel<2><<<blocks, threads, 0, st>>>(sink, cyc, ns, iters, 7);
+  PACO_CUDA_TRY(cudaGetLastError());
+  long long hc[kNumSMs * 2], hn[kNumSMs * 2];
+  PACO_CUDA_TRY(cudaMemcpyAsync(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost, st));
+  PACO_CUDA_TRY(cudaMemcpyAsync(hn, ns, sizeof(hn), cudaMemcpyDeviceToHost, st));
+  PACO_CUDA_TRY(cudaFreeAsync(sink, st));
+  PACO_CUDA_TRY(cudaFreeAsync(cyc, st));
+  PACO_CUDA_TRY(cudaFreeAsync(ns, st));
+  PACO_CUDA_TRY(cudaStreamSynchronize(st));
+  // two co-resident CTAs per SM: each CTA's loop saw the SM shared with its twin
+  long long mx = 0;
+  double mhz_sum = 0;
+  for (int b = 0; b < blocks; ++b) {
+    mx = hc[b] > mx ? hc[b] : mx;
+    mhz_sum += double(hc[b]) / double(hn[b] > 0 ? hn[b] : 1) * 1e3;
+  }
+  const double terms_per_sm = double(iters) * 32 * threads * 2;
+  *tpc = terms_per_sm / double(mx);
+  *mhz = mhz_sum / blocks;
+  return PACO_OK;
+}
+
+}  // namespace paco

@@ -1,0 +1,231 @@
+"""Semiring MM entry points with the reference's signatures, run on B200.
+
+* ``mm_seq``      -- matmul.py:342-366: C <- C (+) A (x) B on one device.  The
+  reference recursion (halve the longest axis down to 32^3 NumPy leaves,
+  matmul.py:369-397) is replaced by one persistent sm_100a launch whose CTAs
+  each own one cuboid of the CTA-level PACO plan (MM-1-Piece over the tile
+  grid, 148 SMs x resident CTAs).
+* ``mm_execute``  -- matmul.py:417-462: binds a plan to device work.  COMPUTE
+  tasks launch ``paco_mm`` on sub-views; REDUCE tasks launch ``paco_fold``
+  (t (+)= temp; temp = zero).  Plan workers map to (device, stream) pairs.
+* ``mm_oracle``   -- matmul.py:400-414: defining sums, one thread per element.
+
+Inputs may be NumPy arrays (staged to the device and C written back in place,
+as the reference mutates C) or CUDA tensors (used in place).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from functools import lru_cache
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .cuboid import DEFAULT_BASE, Cuboid, temp_shape
+from .device import Output, View, is_host, pick_device, stage_in, torch_dtype
+from .engine import execute_plan
+from .plan import COMPUTE, REDUCE, CostReport, Plan, PlanError
+from .semiring import SEMIRING_INT, Semiring
+
+
+def _dtype_of(x):
+    if isinstance(x, np.ndarray):
+        return x.dtype
+    if isinstance(x, torch.Tensor):
+        return x.dtype
+    raise TypeError(f"unsupported array type {type(x).__name__}")
+
+
+def _is_i32(x) -> bool:
+    dt = _dtype_of(x)
+    return dt == np.int32 or dt == torch.int32
+
+
+def kernel_for(semiring: Semiring, A, B) -> tuple[int, object]:
+    """(kernel id, operand dtype) for this semiring and these operands."""
+    if semiring.narrow_kernel_id is not None and _is_i32(A) and _is_i32(B):
+        return semiring.narrow_kernel_id, semiring.narrow_in_dtype
+    return semiring.kernel_id, semiring.in_dtype
+
+
+def launch_mm(kid: int, stream: torch.cuda.Stream, a: View, b: View, c: View, *,
+              pieces=None, overwrite: bool = False) -> None:
+    """One ``paco_mm`` call on views (no validation beyond the C ABI's)."""
+    arr, npieces = nat.pieces_array(pieces)
+    nat.check(nat.load().paco_mm(
+        c.device, stream.cuda_stream, kid, a.ptr, a.ld, b.ptr, b.ld, c.ptr, c.ld,
+        c.rows, c.cols, a.cols, arr, npieces, nat.MM_OVERWRITE if overwrite else 0))
+
+
+def launch_fold(kid: int, stream: torch.cuda.Stream, dst: View, src: View, reset: bool) -> None:
+    nat.check(nat.load().paco_fold(dst.device, stream.cuda_stream, kid, dst.ptr, dst.ld,
+                                   src.ptr, src.ld, dst.rows, dst.cols, int(reset)))
+
+
+def launch_fill(kid: int, stream: torch.cuda.Stream, dst: View) -> None:
+    nat.check(nat.load().paco_fill(dst.device, stream.cuda_stream, kid, dst.ptr, dst.ld,
+                                   dst.rows, dst.cols))
+
+
+def _shape_check(A, B, C) -> tuple[int, int, int]:
+    n, k = tuple(A.shape)
+    k2, m = tuple(B.shape)
+    if k != k2 or tuple(C.shape) != (n, m):
+        raise ValueError(f"shape mismatch: A{tuple(A.shape)} B{tuple(B.shape)} C{tuple(C.shape)}")
+    return n, m, k
+
+
+def mm_seq(A, B, C, semiring: Semiring = SEMIRING_INT, base: int = DEFAULT_BASE, sim=None,
+           ids: tuple[int, int, int] = (100, 101, 0), *, stream: torch.cuda.Stream | None = None,
+           pieces=None, overwrite: bool = False) -> None:
+    """C <- C (+) A (x) B on one B200 (matmul.py:342-366).
+
+    ``base`` is accepted for signature compatibility: the leaf size of the
+    reference recursion has no role once the CTA-level plan tiles the cuboid.
+    ``pieces`` overrides the CTA-level PACO plan (tile-unit cuboids);
+    ``overwrite`` declares C == zero so the kernel does not read it.
+    """
+    _shape_check(A, B, C)
+    if sim is not None:
+        raise NotImplementedError("cache simulation is out of scope on B200; use ncu counters")
+    kid, in_dt = kernel_for(semiring, A, B)
+    dev = pick_device(A, B, C)
+    with torch.cuda.device(dev):
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.stream(st):
+            a = View.of(stage_in(A, in_dt, dev))
+            b = View.of(stage_in(B, in_dt, dev))
+            out = Output(C, semiring.dtype, dev, load=not overwrite)
+            launch_mm(kid, st, a, b, View.of(out.dev), pieces=pieces, overwrite=overwrite)
+            out.finish()
+
+
+def mm_oracle(A, B, semiring: Semiring = SEMIRING_INT):
+    """Triple-loop ground truth on the device (matmul.py:400-414).
+
+    One thread per C element folds the defining sum in l order; no tiling,
+    shared memory or CTA plan, so it is independent of the fast kernels.
+    Returns the same array kind as ``A``.
+    """
+    n, k = tuple(A.shape)
+    _, m = tuple(B.shape)
+    kid, in_dt = kernel_for(semiring, A, B)
+    dev = pick_device(A, B)
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev)
+        a = View.of(stage_in(A, in_dt, dev))
+        b = View.of(stage_in(B, in_dt, dev))
+        c = torch.empty((n, m), dtype=torch_dtype(semiring.dtype), device=dev)
+        cv = View.of(c)
+        launch_fill(kid, st, cv)
+        nat.check(nat.load().paco_mm_naive(dev, st.cuda_stream, kid, a.ptr, a.ld, b.ptr, b.ld,
+                                           cv.ptr, cv.ld, n, m, k))
+    if isinstance(A, np.ndarray):
+        return c.cpu().numpy()
+    return c if isinstance(A, torch.Tensor) and A.is_cuda else c.cpu()
+
+
+def semiring_vadd(semiring: Semiring, x, y):
+    """Elementwise (+) of two equal-shape matrices into a new one."""
+    if tuple(x.shape) != tuple(y.shape):
+        raise ValueError(f"shape mismatch: {tuple(x.shape)} vs {tuple(y.shape)}")
+    dev = pick_device(x, y)
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev)
+        out = stage_in(x, semiring.dtype, dev).clone()
+        yy = stage_in(y, semiring.dtype, dev)
+        launch_fold(semiring.kernel_id, st, View.of(out), View.of(yy), reset=False)
+    if isinstance(x, np.ndarray):
+        return out.cpu().numpy()
+    return out if isinstance(x, torch.Tensor) and x.is_cuda else out.cpu()
+
+
+def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str = "serial_sim",
+               sims: dict | None = None, *, devices: list[int] | None = None) -> CostReport:
+    """Run an MM plan on B200s (matmul.py:417-462).
+
+    Worker ``w`` runs on ``devices[w % len(devices)]`` with its own stream
+    (default: every worker on the current device, one stream each).  C and the
+    temporaries live on the first device; A and B are replicated to every
+    device used, and kernels on other devices reach C/temps through NVLink
+    peer access.  ``mode`` keeps the reference meaning: ``serial_sim``
+    enqueues tasks in plan order from this thread, ``parallel`` from one host
+    thread per worker; the device result is identical.
+    """
+    if sims is not None:
+        raise NotImplementedError("cache simulation is out of scope on B200; use ncu counters")
+    n, m, k = _shape_check(A, B, C)
+    meta = plan.meta
+    if (meta.get("n"), meta.get("m"), meta.get("k")) not in ((n, m, k), (None, None, None)):
+        raise PlanError(f"plan built for {meta.get('n')}x{meta.get('m')}x{meta.get('k')}, "
+                        f"operands are {n}x{m}x{k}")
+    kid, in_dt = kernel_for(semiring, A, B)
+    if devices is None:
+        devices = [pick_device(A, B, C)]
+    home = devices[0]
+    dev_of = [devices[w % len(devices)] for w in range(plan.p)]
+    used = sorted(set(dev_of))
+    lib = nat.load()
+    for d in used:
+        if d != home:
+            nat.check(lib.paco_enable_peer(d, home))
+
+    with torch.cuda.device(home):
+        stage = torch.cuda.current_stream(home)
+        a_on = {d: View.of(stage_in(A, in_dt, d)) for d in used}
+        b_on = {d: View.of(stage_in(B, in_dt, d)) for d in used}
+        out = Output(C, semiring.dtype, home)
+        c_view = View.of(out.dev)
+        temps: dict[int, View] = {}
+        for bid, size in meta["temp_sizes"].items():
+            shape = temp_shape(plan, bid) if size else (0, 1)
+            t = torch.empty(shape, dtype=torch_dtype(semiring.dtype), device=home)
+            temps[bid] = View.of(t)
+            launch_fill(semiring.kernel_id, stage, temps[bid])
+        staged = torch.cuda.Event()
+        staged.record(stage)
+        for d in used:
+            if d != home:
+                torch.cuda.current_stream(d).wait_event(staged)
+
+        streams = [torch.cuda.Stream(device=dev_of[w]) for w in range(plan.p)]
+        for s in streams:
+            s.wait_event(staged)
+        events: list[torch.cuda.Event | None] = [None] * len(plan.tasks)
+        reduces = meta["reduces"]
+        t_begin = torch.cuda.Event(enable_timing=True)
+        t_begin.record(stage)
+
+        def buffer(bid: int) -> View:
+            return c_view if bid == 0 else temps[bid]
+
+        def runner(task) -> None:
+            w = task.workers()[0]
+            st = streams[w]
+            for d in task.deps:
+                st.wait_event(events[d])
+            if task.kind == COMPUTE:
+                cb: Cuboid = task.region
+                dv = dev_of[w]
+                launch_mm(kid, st, a_on[dv].sub(cb.i0, cb.l0, cb.n, cb.k),
+                          b_on[dv].sub(cb.l0, cb.j0, cb.k, cb.m),
+                          buffer(cb.out).sub(cb.out_i0, cb.out_j0, cb.n, cb.m))
+            elif task.kind == REDUCE:
+                bid, tgt, oi, oj, rn, rm = reduces[task.id]
+                launch_fold(semiring.kernel_id, st, buffer(tgt).sub(oi, oj, rn, rm),
+                            temps[bid], reset=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            events[task.id] = ev
+
+        report = execute_plan(plan, runner, mode)
+        for s in streams:
+            stage.wait_stream(s)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_end.record(stage)
+        out.finish()
+        t_end.synchronize()
+        report.gpu_ms = t_begin.elapsed_time(t_end)
+    return report

@@ -1,0 +1,249 @@
+"""GPU parity of the sm_100a semiring kernels against the reference's own results.
+
+Every test calls through the public API (-> C ABI -> CUDA) and compares with
+(a) golden fixtures produced by the reference itself (tests/golden/), and
+(b) the CPU oracle (oracle/semiring_ref.c) on seeded inputs.  Integer and
+tropical semirings must match bit for bit; floating point within the stated
+relative tolerance.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cref
+from paper_2011_01441_b200 import _native as nat
+from paper_2011_01441_b200 import matmul as M
+
+pytestmark = pytest.mark.gpu
+
+INF = 2**30
+
+
+def tropical(rng, shape, lo, hi, inf_frac=0.0, inf=INF):
+    x = rng.integers(lo, hi, shape, dtype=np.int32)
+    if inf_frac:
+        x[rng.random(shape) < inf_frac] = inf
+    return x
+
+
+# ---------------------------------------------------------------- golden vectors
+
+def test_cfg1_full_paco_p3_matches_reference(golden_cases):
+    A, B, want = golden_cases["cfg1_A"], golden_cases["cfg1_B"], golden_cases["cfg1_C"]
+    plan = M.mm_paco_partition(384, 320, 256, 3)
+    for mode in ("serial_sim", "parallel"):
+        C = np.zeros((384, 320), np.int64)
+        rep = M.mm_execute(plan, A, B, C, M.SEMIRING_INT, mode=mode)
+        assert np.array_equal(C, want), mode
+        assert rep.work_total == 384 * 320 * 256 + sum(
+            t.cost_work for t in plan.tasks if t.kind == "reduce")
+    # int64 operands take the wide int64 kernel: same answer
+    C = np.zeros((384, 320), np.int64)
+    M.mm_execute(plan, A.astype(np.int64), B.astype(np.int64), C, M.SEMIRING_INT)
+    assert np.array_equal(C, want)
+
+
+def test_minplus_sat_golden(golden_cases):
+    for tag in ("minplus_sat", "minplus_inf"):
+        A, B, want = golden_cases[f"{tag}_A"], golden_cases[f"{tag}_B"], golden_cases[f"{tag}_C"]
+        n, k = A.shape
+        m = B.shape[1]
+        for p in (1, 3, 5, 7):
+            C = np.full((n, m), INF, np.int32)
+            M.mm_execute(M.mm_one_piece_partition(n, m, k, p), A, B, C, M.SEMIRING_MINPLUS_SAT)
+            assert np.array_equal(C, want), (tag, p)
+        C = np.full((n, m), INF, np.int32)
+        M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)
+        assert np.array_equal(C, want), tag
+
+
+def test_maxplus_golden(golden_cases):
+    A, B, want = golden_cases["maxplus_A"], golden_cases["maxplus_B"], golden_cases["maxplus_C"]
+    n, k = A.shape
+    m = B.shape[1]
+    for p in (1, 2, 3, 5, 7, 8):
+        C = np.full((n, m), -INF, np.int32)
+        M.mm_execute(M.mm_one_piece_partition(n, m, k, p), A, B, C, M.SEMIRING_MAXPLUS)
+        assert np.array_equal(C, want), p
+
+
+def test_reference_minplus_int64_with_wrap(golden_cases):
+    A, B, want = golden_cases["minplus_i64_A"], golden_cases["minplus_i64_B"], golden_cases["minplus_i64_C"]
+    n, k = A.shape
+    m = B.shape[1]
+    C = np.full((n, m), M.MINPLUS_INF, np.int64)
+    M.mm_execute(M.mm_paco_partition(n, m, k, 3), A, B, C, M.SEMIRING_MINPLUS)
+    assert np.array_equal(C, want)
+
+
+def test_int64_ring_wraps_like_numpy(golden_cases):
+    g = golden_cases
+    C = g["int_wrap_C0"].copy()
+    n, k = g["int_wrap_A"].shape
+    m = g["int_wrap_B"].shape[1]
+    M.mm_execute(M.mm_one_piece_partition(n, m, k, 5), g["int_wrap_A"], g["int_wrap_B"], C, M.SEMIRING_INT)
+    assert np.array_equal(C, g["int_wrap_C"])
+
+
+def test_f64_golden(golden_cases):
+    g = golden_cases
+    C = g["f64_C0"].copy()
+    n, k = g["f64_A"].shape
+    m = g["f64_B"].shape[1]
+    M.mm_execute(M.mm_one_piece_partition(n, m, k, 3), g["f64_A"], g["f64_B"], C, M.SEMIRING_F64)
+    np.testing.assert_allclose(C, g["f64_C"], rtol=1e-12, atol=1e-12)
+
+
+def test_bf16_golden(golden_cases):
+    g = golden_cases
+    a = torch.from_numpy(g["bf16_A"]).cuda().to(torch.bfloat16)
+    b = torch.from_numpy(g["bf16_B"]).cuda().to(torch.bfloat16)
+    # the fixture operands are exactly bf16-representable
+    assert torch.equal(a.float().cpu(), torch.from_numpy(g["bf16_A"]))
+    c = torch.zeros(a.shape[0], b.shape[1], device="cuda")
+    M.mm_seq(a, b, c, M.SEMIRING_BF16)
+    ref = g["bf16_C"]
+    err = np.linalg.norm(c.cpu().numpy().astype(np.float64) - ref) / np.linalg.norm(ref)
+    assert err <= 1e-2  # BASELINE cfg3 tolerance; fp32 accumulation gives ~1e-7
+    assert err < 1e-5
+
+
+# ---------------------------------------------------------------- oracle sweeps
+
+SHAPES = [(1, 1, 1), (1, 7, 3), (5, 1, 9), (3, 4, 1), (31, 33, 35), (128, 128, 32),
+          (129, 127, 33), (200, 300, 257), (257, 129, 1000), (64, 1024, 48), (1030, 70, 520)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_minplus_sat_vs_oracle(shape):
+    n, m, k = shape
+    rng = np.random.default_rng(n * 7 + m * 3 + k)
+    A = tropical(rng, (n, k), 0, 2**20, 0.1)
+    B = tropical(rng, (k, m), 0, 2**20, 0.1)
+    C0 = tropical(rng, (n, m), 0, 2**21, 0.5)
+    want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, C0.copy())
+    C = C0.copy()
+    M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)
+    assert np.array_equal(C, want)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_maxplus_vs_oracle(shape):
+    n, m, k = shape
+    rng = np.random.default_rng(n * 5 + m * 11 + k)
+    A = tropical(rng, (n, k), -2**20, 2**20, 0.05, -INF)
+    B = tropical(rng, (k, m), -2**20, 2**20, 0.05, -INF)
+    C0 = np.full((n, m), -INF, np.int32)
+    want = cref.mm(cref.SR_MAXPLUS_SAT32, A, B, C0.copy())
+    C = C0.copy()
+    M.mm_seq(A, B, C, M.SEMIRING_MAXPLUS)
+    assert np.array_equal(C, want)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_int32_to_int64_vs_oracle(shape):
+    n, m, k = shape
+    rng = np.random.default_rng(n + m + k)
+    A = rng.integers(-2**31, 2**31, (n, k), dtype=np.int64).astype(np.int32)
+    B = rng.integers(-2**31, 2**31, (k, m), dtype=np.int64).astype(np.int32)
+    C0 = rng.integers(-2**62, 2**62, (n, m), dtype=np.int64)
+    want = cref.mm(cref.SR_INT_I32_I64, A, B, C0.copy())
+    C = C0.copy()
+    M.mm_seq(A, B, C, M.SEMIRING_INT)
+    assert np.array_equal(C, want)
+
+
+@pytest.mark.parametrize("shape", SHAPES[:8])
+def test_f32_vs_oracle(shape):
+    n, m, k = shape
+    rng = np.random.default_rng(n * 3 + k)
+    A = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    B = rng.uniform(-1, 1, (k, m)).astype(np.float32)
+    C = np.zeros((n, m), np.float32)
+    M.mm_seq(A, B, C, M.SEMIRING_F32)
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    assert np.linalg.norm(C - ref) <= 1e-5 * max(np.linalg.norm(ref), 1e-30) + 1e-6
+
+
+def test_unaligned_views_and_ldc():
+    """Sub-views at odd offsets take the element-granular load path."""
+    rng = np.random.default_rng(5)
+    big_a = torch.from_numpy(tropical(rng, (301, 403), 0, 2**20, 0.1)).cuda()
+    big_b = torch.from_numpy(tropical(rng, (411, 299), 0, 2**20, 0.1)).cuda()
+    big_c = torch.full((305, 307), INF, dtype=torch.int32, device="cuda")
+    a = big_a[3:203, 5:390]      # 200 x 385, misaligned base
+    b = big_b[7:392, 1:258]      # 385 x 257
+    c = big_c[1:201, 9:266]      # 200 x 257
+    want = cref.mm(cref.SR_MINPLUS_SAT32, a.cpu().numpy(), b.cpu().numpy(), c.cpu().numpy().copy())
+    M.mm_seq(a, b, c, M.SEMIRING_MINPLUS_SAT)
+    assert np.array_equal(c.cpu().numpy(), want)
+    # untouched border of C stays INF
+    assert int(big_c[0].min()) == INF and int(big_c[:, :9].min()) == INF
+
+
+def test_cta_plan_overrides_and_ksplit_atomics():
+    """Explicit CTA-level pieces, including k-split pieces folded by atomics."""
+    rng = np.random.default_rng(11)
+    n, m, k = 256, 384, 320
+    A = tropical(rng, (n, k), 0, 2**20, 0.1)
+    B = tropical(rng, (k, m), 0, 2**20, 0.1)
+    want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, np.full((n, m), INF, np.int32))
+    bm, bn, bk, _ = nat.tile_shape(nat.SR_MINPLUS_SAT32)
+    nt, mt, kt = -(-n // bm), -(-m // bn), -(-k // bk)
+    for p in (1, 2, 3, 5, 7, 13, 20):
+        plan = M.mm_one_piece_partition(nt, mt, kt, p)
+        pieces = [(c.region.i0, c.region.j0, c.region.l0, c.region.n, c.region.m, c.region.k)
+                  for c in plan.compute_tasks()]
+        C = np.full((n, m), INF, np.int32)
+        M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT, pieces=pieces)
+        assert np.array_equal(C, want), p
+
+
+def test_overwrite_mode_does_not_read_c():
+    rng = np.random.default_rng(12)
+    A = tropical(rng, (130, 70), 0, 2**20)
+    B = tropical(rng, (70, 90), 0, 2**20)
+    want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, np.full((130, 90), INF, np.int32))
+    c = torch.full((130, 90), -123, dtype=torch.int32, device="cuda")  # garbage C
+    M.mm_seq(A, B, c, M.SEMIRING_MINPLUS_SAT, overwrite=True)
+    assert np.array_equal(c.cpu().numpy(), want)
+
+
+def test_empty_k_and_empty_output():
+    A = np.zeros((4, 0), np.int32)
+    B = np.zeros((0, 5), np.int32)
+    C = np.full((4, 5), 7, np.int32)
+    M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)
+    assert (C == 7).all()
+    C = np.zeros((0, 5), np.int32)
+    M.mm_seq(np.zeros((0, 3), np.int32), np.zeros((3, 5), np.int32), C, M.SEMIRING_MINPLUS_SAT)
+
+
+def test_device_oracle_matches_cpu_oracle():
+    rng = np.random.default_rng(13)
+    A = tropical(rng, (70, 90), 0, 2**20, 0.2)
+    B = tropical(rng, (90, 50), 0, 2**20, 0.2)
+    want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, np.full((70, 50), INF, np.int32))
+    assert np.array_equal(M.mm_oracle(A, B, M.SEMIRING_MINPLUS_SAT), want)
+    A64 = rng.integers(-100, 100, (33, 44))
+    B64 = rng.integers(-100, 100, (44, 55))
+    assert np.array_equal(M.mm_oracle(A64, B64, M.SEMIRING_INT), A64 @ B64)
+
+
+def test_shape_mismatch_raises_value_error():
+    with pytest.raises(ValueError, match="shape mismatch"):
+        M.mm_seq(np.zeros((3, 4), np.int32), np.zeros((5, 6), np.int32), np.zeros((3, 6), np.int64))
+
+
+def test_paco_plans_every_p_minplus_i64():
+    rng = np.random.default_rng(21)
+    n, m, k = 70, 50, 90
+    A = rng.integers(0, 1000, (n, k), dtype=np.int64)
+    B = rng.integers(0, 1000, (k, m), dtype=np.int64)
+    want = cref.mm(cref.SR_MINPLUS_I64, A, B, np.full((n, m), M.MINPLUS_INF, np.int64))
+    for p in (1, 2, 3, 5, 7, 12, 13):
+        for plan in (M.mm_paco_partition(n, m, k, p), M.mm_one_piece_partition(n, m, k, p)):
+            C = np.full((n, m), M.MINPLUS_INF, np.int64)
+            M.mm_execute(plan, A, B, C, M.SEMIRING_MINPLUS, mode="parallel")
+            assert np.array_equal(C, want), (p, plan.meta["variant"])
