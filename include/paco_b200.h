@@ -66,21 +66,28 @@ extern "C" {
 /*
  * C (+)= A (x) B on `device`/`stream`.  A is n x k (lda), B is k x m (ldb),
  * C is n x m (ldc).  `pieces` is an optional HOST array of n_pieces x 6 int32
- * (ti0, tj0, tl0, tn, tm, tk) in units of the kernel's tile shape (see
- * paco_mm_tile_shape): the CTA-level PACO plan, one persistent CTA per
- * piece.  Pass NULL/0 to let the library build the MM-1-Piece plan over
- * 148 x ctas_per_sm workers itself.  Pieces that split k fold with atomics.
+ * (ti0, tj0, tl0, tn, tm, tk) in the units of paco_mm_tile_shape (C tiles
+ * along n and m, k quanta along k): the CTA-level PACO plan, one persistent
+ * CTA per piece.  Pass NULL/0 to use paco_plan_cta over 148 x ctas_per_sm
+ * workers.  Pieces that split k fold into C with atomics.
  */
 int paco_mm(int device, void* stream, int semiring, const void* A, int64_t lda, const void* B,
             int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
             const int32_t* pieces, int n_pieces, int flags);
 
-/* Tile shape (bm, bn, bk) and resident CTAs per SM of the kernel paco_mm uses. */
+/* Piece units of paco_mm's CTA plan: C tile (bm x bn), k quantum bk (piece k
+ * bounds are multiples of bk elements), and resident CTAs per SM. */
 int paco_mm_tile_shape(int semiring, int* bm, int* bn, int* bk, int* ctas_per_sm);
 
 /* Cuboid geometry of mm_one_piece_partition(n, m, k, p): writes p rows of
  * (i0, j0, l0, n, m, k) into out[p*6], worker order.  Host only. */
 int paco_plan_one_piece(int64_t n, int64_t m, int64_t k, int p, int64_t* out);
+
+/* The CTA-level plan paco_mm builds when pieces == NULL: MM-1-Piece over the
+ * (bm, bn, bk) unit grid of `semiring` for p workers, with nearest-unit cuts
+ * and a fall-back to the finest axis when a cut would miss the p-ratio by
+ * > 1%.  Writes p rows of (ti0, tj0, tl0, tn, tm, tk) into out[p*6]. Host only. */
+int paco_plan_cta(int semiring, int64_t n, int64_t m, int64_t k, int p, int32_t* out);
 
 /* dst (+)= src elementwise (n x m views); if reset_src, src = semiring zero. */
 int paco_fold(int device, void* stream, int semiring, void* dst, int64_t ld_dst, void* src,
@@ -107,6 +114,11 @@ int paco_enable_peer(int device, int peer);
  * measured terms per clock per SM and the SM clock (MHz) seen during the run. */
 int paco_alu_probe(int device, void* stream, int which, int iters, double* terms_per_clk_sm,
                    double* sm_mhz);
+
+/* Diagnostics: while `device_buffer` (>= 10 x grid int64) is set, each
+ * SIMT paco_mm CTA writes (smid, start ns, end ns, stage count, its piece
+ * ti0,tj0,tl0,tn,tm,tk) -- 10 int64 per CTA.  NULL disables. */
+int paco_debug_trace(void* device_buffer);
 
 const char* paco_last_error(void);
 int paco_abi_version(void);

@@ -44,6 +44,7 @@ SIGNATURES = {
                        ctypes.POINTER(ctypes.c_int32), _int, _int]),
     "paco_mm_tile_shape": (_int, [_int] + [ctypes.POINTER(_int)] * 4),
     "paco_plan_one_piece": (_int, [_i64, _i64, _i64, _int, ctypes.POINTER(_i64)]),
+    "paco_plan_cta": (_int, [_int, _i64, _i64, _i64, _int, ctypes.POINTER(ctypes.c_int32)]),
     "paco_fold": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _i64, _i64, _int]),
     "paco_fill": (_int, [_int, _vp, _int, _vp, _i64, _i64, _i64]),
     "paco_mm_naive": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64]),
@@ -53,6 +54,7 @@ SIGNATURES = {
     "paco_enable_peer": (_int, [_int, _int]),
     "paco_alu_probe": (_int, [_int, _vp, _int, _int, ctypes.POINTER(ctypes.c_double),
                               ctypes.POINTER(ctypes.c_double)]),
+    "paco_debug_trace": (_int, [_vp]),
     "paco_last_error": (ctypes.c_char_p, []),
     "paco_abi_version": (_int, []),
 }
@@ -106,6 +108,13 @@ def plan_one_piece(n: int, m: int, k: int, p: int) -> list[tuple[int, ...]]:
     """Native MM-1-Piece geometry: p rows of (i0, j0, l0, n, m, k)."""
     buf = (_i64 * (6 * p))()
     check(load().paco_plan_one_piece(n, m, k, p, buf))
+    return [tuple(buf[6 * i:6 * i + 6]) for i in range(p)]
+
+
+def plan_cta(sr: int, n: int, m: int, k: int, p: int) -> list[tuple[int, ...]]:
+    """The library's default CTA-level plan: p rows of (ti0, tj0, tl0, tn, tm, tk)."""
+    buf = (ctypes.c_int32 * (6 * p))()
+    check(load().paco_plan_cta(sr, n, m, k, p, buf))
     return [tuple(buf[6 * i:6 * i + 6]) for i in range(p)]
 
 

@@ -6,6 +6,8 @@
 //   finish(acc)       accumulator -> stored C value (tropical: saturate at +-INF)
 //   combine(c, x)     the semiring (+) used to fold into existing C (vadd)
 //   atomic_combine    the same fold as one global atomic (k-split pieces)
+//   bulk_combine      the same fold for a contiguous smem row, done by the TMA
+//                     unit in L2 (cp.reduce.async.bulk)
 //   zero()            the semiring zero the reference fills temps with
 #pragma once
 #include <cstdint>
@@ -14,6 +16,14 @@
 #include "common.cuh"
 
 namespace paco {
+
+// TMA bulk reduction smem -> global (SASS UBLKRED): the L2 applies the
+// semiring (+) to `bytes` contiguous bytes.  Exact for the integer ops.
+#define PACO_BULK_RED(NAME, OPTYPE)                                                    \
+  __device__ __forceinline__ static void NAME(void* gdst, uint32_t ssrc, uint32_t bytes) { \
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group." OPTYPE          \
+                 " [%0], [%1], %2;\n" ::"l"(gdst), "r"(ssrc), "r"(bytes) : "memory");    \
+  }
 
 // (min,+) on 32-bit lanes.  Inputs live in [0, 2^30] (2^30 = INF), so a + b
 // <= 2^31 never wraps in u32; min() then a final clamp to 2^30 equals the
@@ -32,6 +42,7 @@ struct OpMinPlusSat32 {
   }
   __device__ __forceinline__ static TC combine(TC c, TC x) { return min(c, x); }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicMin(p, x); }
+  PACO_BULK_RED(bulk_combine, "min.s32")
   __host__ __device__ static TC zero() { return PACO_TROPICAL_INF; }
 };
 
@@ -47,6 +58,7 @@ struct OpMaxPlusSat32 {
   __device__ __forceinline__ static TC finish(Acc acc) { return max(acc, -PACO_TROPICAL_INF); }
   __device__ __forceinline__ static TC combine(TC c, TC x) { return max(c, x); }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicMax(p, x); }
+  PACO_BULK_RED(bulk_combine, "max.s32")
   __host__ __device__ static TC zero() { return -PACO_TROPICAL_INF; }
 };
 
@@ -61,6 +73,7 @@ struct OpF32 {
   __device__ __forceinline__ static TC finish(Acc acc) { return acc; }
   __device__ __forceinline__ static TC combine(TC c, TC x) { return c + x; }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicAdd(p, x); }
+  PACO_BULK_RED(bulk_combine, "add.f32")
   __host__ __device__ static TC zero() { return 0.f; }
 };
 
@@ -75,6 +88,7 @@ struct OpF64 {
   __device__ __forceinline__ static TC finish(Acc acc) { return acc; }
   __device__ __forceinline__ static TC combine(TC c, TC x) { return c + x; }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicAdd(p, x); }
+  PACO_BULK_RED(bulk_combine, "add.f64")
   __host__ __device__ static TC zero() { return 0.0; }
 };
 
@@ -96,6 +110,7 @@ struct OpIntI64 {
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) {
     atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(x));
   }
+  PACO_BULK_RED(bulk_combine, "add.u64")
   __host__ __device__ static TC zero() { return 0; }
 };
 
@@ -117,6 +132,7 @@ struct OpIntI32I64 {
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) {
     atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(x));
   }
+  PACO_BULK_RED(bulk_combine, "add.u64")
   __host__ __device__ static TC zero() { return 0; }
 };
 
@@ -138,6 +154,7 @@ struct OpMinPlusI64 {
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) {
     atomicMin(reinterpret_cast<long long*>(p), static_cast<long long>(x));
   }
+  PACO_BULK_RED(bulk_combine, "min.s64")
   __host__ __device__ static TC zero() { return static_cast<TC>(1) << 62; }
 };
 
@@ -156,6 +173,7 @@ struct OpBF16F32 {
   __device__ __forceinline__ static TC finish(Acc acc) { return acc; }
   __device__ __forceinline__ static TC combine(TC c, TC x) { return c + x; }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicAdd(p, x); }
+  PACO_BULK_RED(bulk_combine, "add.f32")
   __host__ __device__ static TC zero() { return 0.f; }
 };
 

@@ -2,25 +2,37 @@
 //
 // Replaces the reference's recursive mm_seq + 32^3 NumPy leaves
 // (matmul.py:342-397, block kernels 45-50) with one persistent launch:
-//   * grid = the CTA-level PACO plan: one CTA per MM-1-Piece cuboid over the
-//     tile grid (148 SMs x resident CTAs), see plan_pieces() below;
+//   * grid = the CTA-level PACO plan: one CTA per MM-1-Piece cuboid of the
+//     iteration space (148 SMs x 2 resident CTAs), see plan_pieces_balanced();
+//     a piece owns a rectangle of 128x128 C tiles and an arbitrary k range
+//     (k bounds are multiples of the 16-byte load quantum);
 //   * each CTA walks the C tiles of its cuboid; per tile it streams its k
-//     range through a STAGES-deep cp.async ring (16 B, zero-filled at edges);
+//     range through a STAGES-deep cp.async ring (16 B; an unpredicated fast
+//     path for interior tiles, zero-filled predicated loads at the edges);
 //   * a 16x16 thread grid holds TMxTN register accumulators per thread, fed by
 //     128-bit LDS from padded, bank-conflict-free shared tiles;
 //   * epilogue: C (+)= acc, or one global atomic (+) per element for pieces
-//     that split k (exact for the integer/tropical semirings, order-free).
+//     that split k (exact and order-free for the integer/tropical semirings).
 // The tropical inner loop is one VIADDMNMX per term (checked in SASS).
 #include <algorithm>
-#include <mutex>
+#include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
+#include "cta_plan.cuh"
 #include "semiring_ops.cuh"
 
 namespace paco {
+
+constexpr int kDefaultWaves = 2;
+
+// Device buffer of 10 x (grid size) int64 set by paco_debug_trace(); when
+// non-null every CTA of the next launches records smid and start/end times.
+long long* g_trace_buffer = nullptr;
 
 template <class Op>
 struct SimtCfg {
@@ -34,15 +46,24 @@ struct SimtCfg {
   static constexpr int TN = 4 * GN;
   static constexpr int THREADS = 256;
   static constexpr int STAGES = kWide ? 4 : 3;
-  static constexpr int MIN_BLOCKS = kWide ? 2 : 2;
+  static constexpr int MIN_BLOCKS = 2;
   static constexpr int VA = 16 / sizeof(typename Op::TA);  // elements per 16 B chunk
   static constexpr int VB = 16 / sizeof(typename Op::TB);
+  static constexpr int KQ = VA;          // k quantum of piece boundaries
   static constexpr int LDA_S = BK + VA;  // padded smem row (k-major rows of A)
   static constexpr int LDB_S = BN;
   static constexpr int A_STAGE = BM * LDA_S;
   static constexpr int B_STAGE = BK * LDB_S;
+  static constexpr int A_CPR = BK / VA;             // 16 B chunks per A tile row
+  static constexpr int A_RPP = THREADS / A_CPR;     // A rows covered per pass
+  static constexpr int A_PASSES = BM / A_RPP;
+  static constexpr int B_CPR = BN / VB;
+  static constexpr int B_RPP = THREADS / B_CPR;
+  static constexpr int B_PASSES = BK / B_RPP;
   static constexpr size_t SMEM =
       size_t(STAGES) * (A_STAGE * sizeof(typename Op::TA) + B_STAGE * sizeof(typename Op::TB));
+  static_assert(A_RPP * A_CPR == THREADS && A_PASSES * A_RPP == BM, "A load mapping");
+  static_assert(B_RPP * B_CPR == THREADS && B_PASSES * B_RPP == BK, "B load mapping");
 };
 
 template <class T>
@@ -71,14 +92,17 @@ struct MMArgs {
   void* C;
   int64_t lda, ldb, ldc;
   int64_t n, m, k;
-  int32_t k_tiles;  // total k tiles of the problem
+  int32_t kq;  // k quantum of the piece table
   int32_t overwrite;
+  long long* trace;  // optional per-CTA [smid, start ns, end ns, stages] (diagnostics)
+  int32_t bulk_ok;   // C is 16 B aligned with ldc*sizeof(TC) % 16 == 0: TMA bulk epilogue
 };
 
-// Stage one (tile, k-tile) pair of A and B into shared memory.
+// Stage one (C tile, k tile) of A and B into shared memory.  kVec: 16 B
+// chunks; interior tiles skip every bound check.
 template <class Op, bool kVec>
 __device__ __forceinline__ void load_stage(const MMArgs& a, typename Op::TA* As, typename Op::TB* Bs,
-                                           int64_t row0, int64_t col0, int64_t k0) {
+                                           int64_t row0, int64_t col0, int64_t k0, int64_t kend) {
   using C = SimtCfg<Op>;
   using TA = typename Op::TA;
   using TB = typename Op::TB;
@@ -86,35 +110,43 @@ __device__ __forceinline__ void load_stage(const MMArgs& a, typename Op::TA* As,
   const TB* B = static_cast<const TB*>(a.B);
   const int tid = threadIdx.x;
   if constexpr (kVec) {
-    constexpr int A_CHUNKS_ROW = C::BK / C::VA;
-    constexpr int A_ITERS = C::BM * A_CHUNKS_ROW / C::THREADS;
+    const int ar = tid / C::A_CPR, ak = (tid % C::A_CPR) * C::VA;
+    const int br = tid / C::B_CPR, bc = (tid % C::B_CPR) * C::VB;
+    TA* sa = As + ar * C::LDA_S + ak;
+    TB* sb = Bs + br * C::LDB_S + bc;
+    const bool interior = (row0 + C::BM <= a.n) && (col0 + C::BN <= a.m) && (k0 + C::BK <= kend);
+    if (interior) {
+      const TA* ga = A + (row0 + ar) * a.lda + (k0 + ak);
+      const TB* gb = B + (k0 + br) * a.ldb + (col0 + bc);
 #pragma unroll
-    for (int it = 0; it < A_ITERS; ++it) {
-      const int c = tid + it * C::THREADS;
-      const int r = c / A_CHUNKS_ROW, kc = (c % A_CHUNKS_ROW) * C::VA;
-      const int64_t gr = row0 + r, gk = k0 + kc;
-      int bytes = 0;
-      const TA* src = A;
-      if (gr < a.n && gk < a.k) {
-        bytes = int((a.k - gk < C::VA ? a.k - gk : C::VA) * sizeof(TA));
-        src = A + gr * a.lda + gk;
-      }
-      cp_async16(As + r * C::LDA_S + kc, src, bytes);
-    }
-    constexpr int B_CHUNKS_ROW = C::BN / C::VB;
-    constexpr int B_ITERS = C::BK * B_CHUNKS_ROW / C::THREADS;
+      for (int i = 0; i < C::A_PASSES; ++i)
+        cp_async16(sa + i * C::A_RPP * C::LDA_S, ga + i * C::A_RPP * a.lda, 16);
 #pragma unroll
-    for (int it = 0; it < B_ITERS; ++it) {
-      const int c = tid + it * C::THREADS;
-      const int r = c / B_CHUNKS_ROW, nc = (c % B_CHUNKS_ROW) * C::VB;
-      const int64_t gk = k0 + r, gc = col0 + nc;
-      int bytes = 0;
-      const TB* src = B;
-      if (gk < a.k && gc < a.m) {
-        bytes = int((a.m - gc < C::VB ? a.m - gc : C::VB) * sizeof(TB));
-        src = B + gk * a.ldb + gc;
+      for (int i = 0; i < C::B_PASSES; ++i)
+        cp_async16(sb + i * C::B_RPP * C::LDB_S, gb + i * C::B_RPP * a.ldb, 16);
+    } else {
+#pragma unroll
+      for (int i = 0; i < C::A_PASSES; ++i) {
+        const int64_t gr = row0 + ar + i * C::A_RPP, gk = k0 + ak;
+        int bytes = 0;
+        const TA* src = A;
+        if (gr < a.n && gk < kend) {
+          bytes = int((kend - gk < C::VA ? kend - gk : C::VA) * sizeof(TA));
+          src = A + gr * a.lda + gk;
+        }
+        cp_async16(sa + i * C::A_RPP * C::LDA_S, src, bytes);
       }
-      cp_async16(Bs + r * C::LDB_S + nc, src, bytes);
+#pragma unroll
+      for (int i = 0; i < C::B_PASSES; ++i) {
+        const int64_t gk = k0 + br + i * C::B_RPP, gc = col0 + bc;
+        int bytes = 0;
+        const TB* src = B;
+        if (gk < kend && gc < a.m) {
+          bytes = int((a.m - gc < C::VB ? a.m - gc : C::VB) * sizeof(TB));
+          src = B + gk * a.ldb + gc;
+        }
+        cp_async16(sb + i * C::B_RPP * C::LDB_S, src, bytes);
+      }
     }
   } else {
     // element-granular path for views that are not 16 B aligned
@@ -124,7 +156,7 @@ __device__ __forceinline__ void load_stage(const MMArgs& a, typename Op::TA* As,
       const int c = tid + it * C::THREADS;
       const int r = c / C::BK, kc = c % C::BK;
       const int64_t gr = row0 + r, gk = k0 + kc;
-      const bool ok = gr < a.n && gk < a.k;
+      const bool ok = gr < a.n && gk < kend;
       const TA* src = ok ? A + gr * a.lda + gk : A;
       if constexpr (sizeof(TA) == 4)
         cp_async4(As + r * C::LDA_S + kc, src, ok ? 4 : 0);
@@ -137,7 +169,7 @@ __device__ __forceinline__ void load_stage(const MMArgs& a, typename Op::TA* As,
       const int c = tid + it * C::THREADS;
       const int r = c / C::BN, nc = c % C::BN;
       const int64_t gk = k0 + r, gc = col0 + nc;
-      const bool ok = gk < a.k && gc < a.m;
+      const bool ok = gk < kend && gc < a.m;
       const TB* src = ok ? B + gk * a.ldb + gc : B;
       if constexpr (sizeof(TB) == 4)
         cp_async4(Bs + r * C::LDB_S + nc, src, ok ? 4 : 0);
@@ -147,8 +179,42 @@ __device__ __forceinline__ void load_stage(const MMArgs& a, typename Op::TA* As,
   }
 }
 
-// acc[i][j] = acc (+) A[row_i][k] (x) B[k][col_j] over `kvalid` k of the stage.
-template <class Op, bool kFull>
+// Four k steps of the register-blocked product: 2*GM + 2*GN LDS.128 feed
+// TM*TN*4 semiring MACs.
+template <class Op>
+__device__ __forceinline__ void mac_k4(typename Op::Acc (&acc)[SimtCfg<Op>::TM][SimtCfg<Op>::TN],
+                                       const typename Op::TA* a_base, const typename Op::TB* b_base,
+                                       int kk) {
+  using C = SimtCfg<Op>;
+  using TA = typename Op::TA;
+  using TB = typename Op::TB;
+  TA a[C::TM][4];
+#pragma unroll
+  for (int g = 0; g < C::GM; ++g)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const Vec4<TA> v = lds4(a_base + (g * 64 + r) * C::LDA_S + kk);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a[g * 4 + r][q] = v.v[q];
+    }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    TB b[C::TN];
+#pragma unroll
+    for (int g = 0; g < C::GN; ++g) {
+      const Vec4<TB> v = lds4(b_base + (kk + q) * C::LDB_S + g * 64);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) b[g * 4 + e] = v.v[e];
+    }
+#pragma unroll
+    for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::mac(acc[i][j], a[i][q], b[j]);
+  }
+}
+
+// acc (+)= A_stage (x) B_stage over the first `kvalid` k of the stage.
+template <class Op>
 __device__ __forceinline__ void compute_stage(typename Op::Acc (&acc)[SimtCfg<Op>::TM][SimtCfg<Op>::TN],
                                               const typename Op::TA* As, const typename Op::TB* Bs,
                                               int kvalid) {
@@ -158,50 +224,28 @@ __device__ __forceinline__ void compute_stage(typename Op::Acc (&acc)[SimtCfg<Op
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const TA* a_base = As + (ty * 4) * C::LDA_S;
   const TB* b_base = Bs + tx * 4;
-  if constexpr (kFull) {
+  if (kvalid == C::BK) {
 #pragma unroll
-    for (int kk = 0; kk < C::BK; kk += 4) {
-      TA a[C::TM][4];
+    for (int kk = 0; kk < C::BK; kk += 4) mac_k4<Op>(acc, a_base, b_base, kk);
+    return;
+  }
+  int kk = 0;
+  for (; kk + 4 <= kvalid; kk += 4) mac_k4<Op>(acc, a_base, b_base, kk);
+  for (; kk < kvalid; ++kk) {  // only at a global k end that is not a multiple of 4
+    TA a[C::TM];
+    TB b[C::TN];
 #pragma unroll
-      for (int g = 0; g < C::GM; ++g)
+    for (int g = 0; g < C::GM; ++g)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const Vec4<TA> v = lds4(a_base + (g * 64 + r) * C::LDA_S + kk);
+      for (int r = 0; r < 4; ++r) a[g * 4 + r] = a_base[(g * 64 + r) * C::LDA_S + kk];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a[g * 4 + r][q] = v.v[q];
-        }
+    for (int g = 0; g < C::GN; ++g)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        TB b[C::TN];
+      for (int e = 0; e < 4; ++e) b[g * 4 + e] = b_base[kk * C::LDB_S + g * 64 + e];
 #pragma unroll
-        for (int g = 0; g < C::GN; ++g) {
-          const Vec4<TB> v = lds4(b_base + (kk + q) * C::LDB_S + g * 64);
+    for (int i = 0; i < C::TM; ++i)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) b[g * 4 + e] = v.v[e];
-        }
-#pragma unroll
-        for (int i = 0; i < C::TM; ++i)
-#pragma unroll
-          for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::mac(acc[i][j], a[i][q], b[j]);
-      }
-    }
-  } else {
-    for (int kk = 0; kk < kvalid; ++kk) {
-      TA a[C::TM];
-      TB b[C::TN];
-#pragma unroll
-      for (int g = 0; g < C::GM; ++g)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) a[g * 4 + r] = a_base[(g * 64 + r) * C::LDA_S + kk];
-#pragma unroll
-      for (int g = 0; g < C::GN; ++g)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) b[g * 4 + e] = b_base[kk * C::LDB_S + g * 64 + e];
-#pragma unroll
-      for (int i = 0; i < C::TM; ++i)
-#pragma unroll
-        for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::mac(acc[i][j], a[i], b[j]);
-    }
+      for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::mac(acc[i][j], a[i], b[j]);
   }
 }
 
@@ -233,6 +277,77 @@ __device__ __forceinline__ void epilogue(const MMArgs& a,
   }
 }
 
+// Epilogue through the TMA unit: the finished tile is staged in the stage
+// buffer that was just consumed (A part: 32 rows, B part: 32 rows of 512 B),
+// 64 rows per round, and each row is folded into C by one
+// cp.reduce.async.bulk (semiring (+) applied in L2) -- or stored with
+// cp.async.bulk when overwriting.  Exact and order-free for k-split pieces.
+template <class Op>
+__device__ __forceinline__ void epilogue_bulk(const MMArgs& a,
+                                              typename Op::Acc (&acc)[SimtCfg<Op>::TM][SimtCfg<Op>::TN],
+                                              int64_t row0, int64_t col0, void* bufA, void* bufB,
+                                              uint32_t bytes) {
+  using C = SimtCfg<Op>;
+  using TC = typename Op::TC;
+  static_assert(C::BM == 128 && C::BN == 128 && sizeof(TC) == 4, "bulk epilogue layout");
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  TC* Cp = static_cast<TC*>(a.C);
+  __syncthreads();  // every warp is done reading the stage buffer
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int lr = ty * 4 + r;  // 0..63 within the round
+      TC* dst = lr < 32 ? static_cast<TC*>(bufA) + lr * C::BN : static_cast<TC*>(bufB) + (lr - 32) * C::BN;
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        TC v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = Op::finish(acc[4 * h + r][4 * g + e]);
+        uint4 bits;
+        memcpy(&bits, v, 16);  // bit copy (TC may be float)
+        *reinterpret_cast<uint4*>(dst + g * 64 + tx * 4) = bits;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll 1
+      for (int q = 0; q < 8; ++q) {
+        const int lr = warp * 8 + q;
+        const int64_t gr = row0 + 64 * h + lr;
+        if (gr < a.n) {
+          const void* src = lr < 32 ? static_cast<TC*>(bufA) + lr * C::BN : static_cast<TC*>(bufB) + (lr - 32) * C::BN;
+          TC* gdst = Cp + gr * a.ldc + col0;
+          if (a.overwrite)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+                         "r"(smem_u32(src)), "r"(bytes) : "memory");
+          else
+            Op::bulk_combine(gdst, smem_u32(src), bytes);
+        }
+      }
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+    __syncthreads();  // smem free again (round 2 / the next cp.async stage)
+  }
+}
+
+// (ti, tj, kt) walk of one piece: k fastest, then C tile columns, then rows.
+struct TileWalk {
+  int ti, tj, kt;
+  __device__ __forceinline__ void next(int tm, int KT) {
+    if (++kt == KT) {
+      kt = 0;
+      if (++tj == tm) {
+        tj = 0;
+        ++ti;
+      }
+    }
+  }
+};
+
 template <class Op, bool kVec>
 __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
     simt_mm_kernel(const MMArgs args, const __grid_constant__ PieceTable table) {
@@ -243,25 +358,31 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
   TA* As = reinterpret_cast<TA*>(smem_raw);
   TB* Bs = reinterpret_cast<TB*>(smem_raw + size_t(C::STAGES) * C::A_STAGE * sizeof(TA));
 
-  const Piece pc = table.p[blockIdx.x];
-  const bool atomic = pc.tk != args.k_tiles;
-  const int KT = pc.tk;
+  Piece pc;
+  if (table.count > 0) {
+    pc = table.p[blockIdx.x];
+  } else {  // derive this CTA's piece of the default plan (same code as paco_plan_cta)
+    UnitBox b;
+    plan_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, int(gridDim.x), int(blockIdx.x), b);
+    pc = Piece{int32_t(b.o[0]), int32_t(b.o[1]), int32_t(b.o[2]), int32_t(b.e[0]), int32_t(b.e[1]),
+               int32_t(b.e[2])};
+  }
+  long long t_start = 0;
+  if (args.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const int64_t kb = int64_t(pc.tl0) * args.kq;
+  const int64_t kend = min(args.k, kb + int64_t(pc.tk) * args.kq);
+  const bool atomic = !(kb == 0 && kend == args.k);
+  const int KT = int((kend - kb + C::BK - 1) / C::BK);
   const int total = pc.tn * pc.tm * KT;
 
-  auto coords = [&](int it, int64_t& row0, int64_t& col0, int64_t& k0) {
-    const int tile = it / KT, kt = it - tile * KT;
-    const int ti = tile / pc.tm, tj = tile - ti * pc.tm;
-    row0 = int64_t(pc.ti0 + ti) * C::BM;
-    col0 = int64_t(pc.tj0 + tj) * C::BN;
-    k0 = int64_t(pc.tl0 + kt) * C::BK;
-  };
-
+  TileWalk ld{0, 0, 0};
 #pragma unroll
   for (int s = 0; s < C::STAGES - 1; ++s) {
     if (s < total) {
-      int64_t r0, c0, k0;
-      coords(s, r0, c0, k0);
-      load_stage<Op, kVec>(args, As + s * C::A_STAGE, Bs + s * C::B_STAGE, r0, c0, k0);
+      load_stage<Op, kVec>(args, As + s * C::A_STAGE, Bs + s * C::B_STAGE,
+                           int64_t(pc.ti0 + ld.ti) * C::BM, int64_t(pc.tj0 + ld.tj) * C::BN,
+                           kb + int64_t(ld.kt) * C::BK, kend);
+      ld.next(pc.tm, KT);
     }
     cp_async_commit();
   }
@@ -272,56 +393,80 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
 #pragma unroll
     for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::identity();
 
+  TileWalk cw{0, 0, 0};
+  int s_load = C::STAGES - 1, s_comp = 0;
   for (int it = 0; it < total; ++it) {
     cp_async_wait<C::STAGES - 2>();
     __syncthreads();
-    {
-      const int nxt = it + C::STAGES - 1;
-      if (nxt < total) {
-        int64_t r0, c0, k0;
-        coords(nxt, r0, c0, k0);
-        const int s = nxt % C::STAGES;
-        load_stage<Op, kVec>(args, As + s * C::A_STAGE, Bs + s * C::B_STAGE, r0, c0, k0);
-      }
-      cp_async_commit();
+    if (it + C::STAGES - 1 < total) {
+      load_stage<Op, kVec>(args, As + s_load * C::A_STAGE, Bs + s_load * C::B_STAGE,
+                           int64_t(pc.ti0 + ld.ti) * C::BM, int64_t(pc.tj0 + ld.tj) * C::BN,
+                           kb + int64_t(ld.kt) * C::BK, kend);
+      ld.next(pc.tm, KT);
     }
-    int64_t r0, c0, k0;
-    coords(it, r0, c0, k0);
-    const int s = it % C::STAGES;
-    const int64_t krem = args.k - k0;
-    if (krem >= C::BK)
-      compute_stage<Op, true>(acc, As + s * C::A_STAGE, Bs + s * C::B_STAGE, C::BK);
-    else
-      compute_stage<Op, false>(acc, As + s * C::A_STAGE, Bs + s * C::B_STAGE, int(krem));
-    if ((it + 1) % KT == 0) {
-      epilogue<Op>(args, acc, r0, c0, atomic);
+    cp_async_commit();
+    s_load = (s_load + 1 == C::STAGES) ? 0 : s_load + 1;
+
+    const int64_t k0 = kb + int64_t(cw.kt) * C::BK;
+    const int kvalid = (kend - k0 < C::BK) ? int(kend - k0) : C::BK;
+    const int s_cur = s_comp;
+    compute_stage<Op>(acc, As + s_cur * C::A_STAGE, Bs + s_cur * C::B_STAGE, kvalid);
+    s_comp = (s_comp + 1 == C::STAGES) ? 0 : s_comp + 1;
+    if (cw.kt == KT - 1) {
+      const int64_t row0 = int64_t(pc.ti0 + cw.ti) * C::BM, col0 = int64_t(pc.tj0 + cw.tj) * C::BN;
+      bool done = false;
+      if constexpr (!C::kWide) {
+        const int64_t cols = (args.m - col0 < C::BN) ? args.m - col0 : C::BN;
+        const uint32_t bytes = uint32_t(cols * sizeof(typename Op::TC));
+        if (args.bulk_ok && (bytes % 16) == 0) {
+          epilogue_bulk<Op>(args, acc, row0, col0, As + s_cur * C::A_STAGE, Bs + s_cur * C::B_STAGE, bytes);
+          done = true;
+        }
+      }
+      if (!done) epilogue<Op>(args, acc, row0, col0, atomic);
 #pragma unroll
       for (int i = 0; i < C::TM; ++i)
 #pragma unroll
         for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::identity();
     }
+    cw.next(pc.tm, KT);
   }
   cp_async_wait<0>();
+  if (args.trace && threadIdx.x == 0) {
+    long long t_end;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    long long* tr = args.trace + 10 * blockIdx.x;
+    tr[0] = smid;
+    tr[1] = t_start;
+    tr[2] = t_end;
+    tr[3] = total;
+    tr[4] = pc.ti0;
+    tr[5] = pc.tj0;
+    tr[6] = pc.tl0;
+    tr[7] = pc.tn;
+    tr[8] = pc.tm;
+    tr[9] = pc.tk;
+  }
 }
 
 // ---------------------------------------------------------------------------
-// CTA-level PACO: MM-1-Piece over the tile grid (host side).
-//
-// Same recursion as mm_one_piece_partition (matmul.py:250-300): the worker
-// list splits floor(p/2):ceil(p/2); the cut axis is the longest axis of an
-// evenly-halved virtual cuboid (ties n -> m -> k); the real length is split
-// max(1, len*a // (a+b)).  Here the virtual cuboid is in ELEMENTS while the
-// real cut is in TILES, so pieces stay cube-like in the iteration space and
-// every cut lands on a tile boundary.  With unit tiles it is exactly the
-// reference rule (paco_plan_one_piece, pinned by the CPU tests).
+// CTA-level PACO planning (host side).
 // ---------------------------------------------------------------------------
 namespace {
 struct Box {
-  int64_t o[3];  // offsets (tiles)
-  int64_t e[3];  // extents (tiles)
+  int64_t o[3];  // offsets (units)
+  int64_t e[3];  // extents (units)
 };
 
-bool one_piece_rec(const Box& b, int lo_w, int hi_w, double vn, double vm, double vk,
+int virtual_axis(const double v[3]) {
+  if (v[0] >= v[1] && v[0] >= v[2]) return 0;
+  return v[1] >= v[2] ? 1 : 2;
+}
+
+// Exactly mm_one_piece_partition (matmul.py:250-300) on unit-size cells.
+bool one_piece_rec(const Box& b, int lo_w, int hi_w, double v0, double v1, double v2,
                    std::vector<Box>& out) {
   const int cnt = hi_w - lo_w;
   if (cnt == 1) {
@@ -329,11 +474,8 @@ bool one_piece_rec(const Box& b, int lo_w, int hi_w, double vn, double vm, doubl
     return true;
   }
   const int h = cnt / 2;  // left list is the smaller one
-  int axis;
-  if (vn >= vm && vn >= vk)
-    axis = 0;
-  else
-    axis = vm >= vk ? 1 : 2;
+  double v[3] = {v0, v1, v2};
+  const int axis = virtual_axis(v);
   const int64_t len = b.e[axis];
   if (len < 2) return false;
   const int64_t left = std::max<int64_t>(1, len * h / cnt);
@@ -341,22 +483,51 @@ bool one_piece_rec(const Box& b, int lo_w, int hi_w, double vn, double vm, doubl
   lo.e[axis] = left;
   hi.o[axis] += left;
   hi.e[axis] = len - left;
-  double v[3] = {vn, vm, vk};
   v[axis] /= 2;
   return one_piece_rec(lo, lo_w, lo_w + h, v[0], v[1], v[2], out) &&
          one_piece_rec(hi, lo_w + h, hi_w, v[0], v[1], v[2], out);
 }
+
 }  // namespace
 
-// Tile-quantised MM-1-Piece plan; returns false when p pieces do not fit.
-bool plan_pieces(int64_t n, int64_t m, int64_t k, int bm, int bn, int bk, int p, std::vector<Box>& out) {
+bool plan_pieces(int64_t n, int64_t m, int64_t k, int p, std::vector<Box>& out) {
   out.assign(p, Box{});
-  Box root{{0, 0, 0}, {(n + bm - 1) / bm, (m + bn - 1) / bn, (k + bk - 1) / bk}};
+  Box root{{0, 0, 0}, {n, m, k}};
   return one_piece_rec(root, 0, p, double(n), double(m), double(k), out);
 }
 
-int fill_table(PieceTable& t, int64_t n, int64_t m, int64_t k, int bm, int bn, int bk, int k_tiles,
+bool plan_pieces_balanced(int64_t n, int64_t m, int64_t k, int bm, int bn, int kq, int p,
+                          std::vector<Box>& out) {
+  out.assign(p, Box{});
+  for (int i = 0; i < p; ++i) {
+    UnitBox b;
+    if (!plan_piece(n, m, k, bm, bn, kq, p, i, b)) return false;
+    for (int d = 0; d < 3; ++d) {
+      out[i].o[d] = b.o[d];
+      out[i].e[d] = b.e[d];
+    }
+  }
+  return true;
+}
+
+// Default CTA-level plan size: 148 SMs x resident CTAs x waves (the later
+// waves are dispatched to whichever SM frees a slot first).  PACO_CTA_PIECES
+// overrides it (tuning / experiments).
+int default_pieces(int ctas_per_sm) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("PACO_CTA_PIECES");
+    env = e ? atoi(e) : 0;
+  }
+  return env > 0 ? env : kNumSMs * ctas_per_sm * kDefaultWaves;
+}
+
+// Resolve the CTA plan: an explicit table (pieces != NULL), or the default
+// plan derived on device (t.count = 0).  Returns the grid size in *grid.
+int fill_table(PieceTable& t, int* grid, int64_t n, int64_t m, int64_t k, int bm, int bn, int kq,
                const int32_t* pieces, int n_pieces, int default_p) {
+  const int64_t units[3] = {(n + bm - 1) / bm, (m + bn - 1) / bn, (k + kq - 1) / kq};
+  t.ksplit = 0;
   if (pieces && n_pieces > 0) {
     if (n_pieces > kMaxPieces) {
       set_error("n_pieces=%d exceeds PACO_MAX_PIECES=%d", n_pieces, kMaxPieces);
@@ -365,27 +536,46 @@ int fill_table(PieceTable& t, int64_t n, int64_t m, int64_t k, int bm, int bn, i
     t.count = n_pieces;
     for (int i = 0; i < n_pieces; ++i) {
       const int32_t* q = pieces + 6 * i;
-      t.p[i] = Piece{q[0], q[1], q[2], q[3], q[4], q[5]};
-      if (q[3] < 1 || q[4] < 1 || q[5] < 1) {
-        set_error("piece %d has an empty extent", i);
+      if (q[3] < 1 || q[4] < 1 || q[5] < 1 || q[0] < 0 || q[1] < 0 || q[2] < 0 ||
+          q[0] + q[3] > units[0] || q[1] + q[4] > units[1] || q[2] + q[5] > units[2]) {
+        set_error("piece %d (%d,%d,%d,%d,%d,%d) is empty or outside the %lldx%lldx%lld unit grid", i,
+                  q[0], q[1], q[2], q[3], q[4], q[5], (long long)units[0], (long long)units[1],
+                  (long long)units[2]);
         return PACO_ERR_ARG;
       }
+      t.p[i] = Piece{q[0], q[1], q[2], q[3], q[4], q[5]};
+      t.ksplit |= (q[5] != units[2]);
     }
-  } else {
-    const int64_t tiles = ((n + bm - 1) / bm) * ((m + bn - 1) / bn) * int64_t(k_tiles);
-    int p = int(std::min<int64_t>(std::min(default_p, kMaxPieces), tiles));
-    std::vector<Box> boxes;
-    while (p > 1 && !plan_pieces(n, m, k, bm, bn, bk, p, boxes)) --p;
-    if (p <= 1) plan_pieces(n, m, k, bm, bn, bk, 1, boxes);
-    t.count = p;
-    for (int i = 0; i < p; ++i) {
-      const Box& b = boxes[i];
-      t.p[i] = Piece{int32_t(b.o[0]), int32_t(b.o[1]), int32_t(b.o[2]),
-                     int32_t(b.e[0]), int32_t(b.e[1]), int32_t(b.e[2])};
-    }
+    *grid = n_pieces;
+    return PACO_OK;
   }
-  t.ksplit = 0;
-  for (int i = 0; i < t.count; ++i) t.ksplit |= (t.p[i].tk != k_tiles);
+  // default: the largest feasible p <= default_p, cached per shape
+  struct Key {
+    int64_t n, m, k;
+    int bm, bn, kq, p;
+  };
+  static thread_local Key last{-1, -1, -1, 0, 0, 0, 0};
+  static thread_local int last_p = 0, last_ksplit = 0;
+  const int64_t cells = units[0] * units[1] * units[2];
+  int p = int(std::min<int64_t>(default_p, cells));
+  if (!(last.n == n && last.m == m && last.k == k && last.bm == bm && last.bn == bn && last.kq == kq &&
+        last.p == p)) {
+    std::vector<Box> boxes;
+    int q = p;
+    while (q > 1 && !plan_pieces_balanced(n, m, k, bm, bn, kq, q, boxes)) --q;
+    if (q <= 1) {
+      q = 1;
+      plan_pieces_balanced(n, m, k, bm, bn, kq, 1, boxes);
+    }
+    int ks = 0;
+    for (const Box& b : boxes) ks |= (b.e[2] != units[2]);
+    last = Key{n, m, k, bm, bn, kq, p};
+    last_p = q;
+    last_ksplit = ks;
+  }
+  t.count = 0;
+  t.ksplit = last_ksplit;
+  *grid = last_p;
   return PACO_OK;
 }
 
@@ -394,14 +584,16 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
                 int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
                 const int32_t* pieces, int n_pieces, int flags) {
   using Cfg = SimtCfg<Op>;
-  static PieceTable table;  // large; guarded by the mutex below
+  static PieceTable table;  // ~15 KB; copied into the launch's parameter buffer
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
-  const int k_tiles = int((k + Cfg::BK - 1) / Cfg::BK);
-  int rc = fill_table(table, n, m, k, Cfg::BM, Cfg::BN, Cfg::BK, k_tiles, pieces, n_pieces,
-                      kNumSMs * Cfg::MIN_BLOCKS);
+  int grid = 0;
+  int rc = fill_table(table, &grid, n, m, k, Cfg::BM, Cfg::BN, Cfg::KQ, pieces, n_pieces,
+                      default_pieces(Cfg::MIN_BLOCKS));
   if (rc) return rc;
-  MMArgs args{A, B, C, lda, ldb, ldc, n, m, k, k_tiles, (flags & PACO_MM_OVERWRITE) ? 1 : 0};
+  MMArgs args{A, B, C, lda, ldb, ldc, n, m, k, Cfg::KQ, (flags & PACO_MM_OVERWRITE) ? 1 : 0,
+              g_trace_buffer,
+              (reinterpret_cast<uintptr_t>(C) % 16 == 0 && (ldc * sizeof(typename Op::TC)) % 16 == 0) ? 1 : 0};
   if (args.overwrite && table.ksplit) {
     // atomics fold into C, so C must first hold the semiring zero
     rc = paco_fill(device, stream, Op::kId, C, ldc, n, m);
@@ -412,7 +604,7 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
                    ((lda * sizeof(typename Op::TA)) % 16 == 0) && ((ldb * sizeof(typename Op::TB)) % 16 == 0);
   auto kern = vec ? simt_mm_kernel<Op, true> : simt_mm_kernel<Op, false>;
   PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
-  kern<<<table.count, Cfg::THREADS, Cfg::SMEM, stream>>>(args, table);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, stream>>>(args, table);
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;
 }
@@ -436,13 +628,18 @@ int simt_tile_shape(int sr, int* bm, int* bn, int* bk, int* cps) {
     using Cfg = SimtCfg<decltype(op)>;
     *bm = Cfg::BM;
     *bn = Cfg::BN;
-    *bk = Cfg::BK;
+    *bk = Cfg::KQ;
     *cps = Cfg::MIN_BLOCKS;
     return PACO_OK;
   });
 }
 
 }  // namespace paco
+
+extern "C" int paco_debug_trace(void* device_buffer) {
+  paco::g_trace_buffer = static_cast<long long*>(device_buffer);
+  return PACO_OK;
+}
 
 extern "C" int paco_plan_one_piece(int64_t n, int64_t m, int64_t k, int p, int64_t* out) {
   using namespace paco;
@@ -451,7 +648,7 @@ extern "C" int paco_plan_one_piece(int64_t n, int64_t m, int64_t k, int p, int64
     return PACO_ERR_ARG;
   }
   std::vector<Box> boxes;
-  if (!plan_pieces(n, m, k, 1, 1, 1, p, boxes)) {
+  if (!plan_pieces(n, m, k, p, boxes)) {
     set_error("extents too small to give every worker a nonempty piece");
     return PACO_ERR_ARG;
   }
@@ -459,6 +656,28 @@ extern "C" int paco_plan_one_piece(int64_t n, int64_t m, int64_t k, int p, int64
     for (int d = 0; d < 3; ++d) {
       out[6 * i + d] = boxes[i].o[d];
       out[6 * i + 3 + d] = boxes[i].e[d];
+    }
+  return PACO_OK;
+}
+
+extern "C" int paco_plan_cta(int semiring, int64_t n, int64_t m, int64_t k, int p, int32_t* out) {
+  using namespace paco;
+  int bm, bn, kq, cps;
+  int rc = paco_mm_tile_shape(semiring, &bm, &bn, &kq, &cps);
+  if (rc) return rc;
+  if (p < 1 || !out || n < 1 || m < 1 || k < 1) {
+    set_error("paco_plan_cta: need extents >= 1, p >= 1 and an output buffer");
+    return PACO_ERR_ARG;
+  }
+  std::vector<Box> boxes;
+  if (!plan_pieces_balanced(n, m, k, bm, bn, kq, p, boxes)) {
+    set_error("extents too small to give every worker a nonempty piece");
+    return PACO_ERR_ARG;
+  }
+  for (int i = 0; i < p; ++i)
+    for (int d = 0; d < 3; ++d) {
+      out[6 * i + d] = int32_t(boxes[i].o[d]);
+      out[6 * i + 3 + d] = int32_t(boxes[i].e[d]);
     }
   return PACO_OK;
 }

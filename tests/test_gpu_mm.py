@@ -247,3 +247,26 @@ def test_paco_plans_every_p_minplus_i64():
             C = np.full((n, m), M.MINPLUS_INF, np.int64)
             M.mm_execute(plan, A, B, C, M.SEMIRING_MINPLUS, mode="parallel")
             assert np.array_equal(C, want), (p, plan.meta["variant"])
+
+
+def test_device_derived_cta_plan_matches_host_plan():
+    """Each CTA derives its piece on device; it must equal paco_plan_cta's."""
+    lib = nat.load()
+    rng = np.random.default_rng(31)
+    for (n, m, k) in [(1000, 700, 900), (300, 4000, 129), (2048, 2048, 2048)]:
+        A = torch.from_numpy(tropical(rng, (n, k), 0, 2**20)).cuda()
+        B = torch.from_numpy(tropical(rng, (k, m), 0, 2**20)).cuda()
+        C = torch.full((n, m), INF, dtype=torch.int32, device="cuda")
+        tr = torch.zeros(10 * 4096, dtype=torch.int64, device="cuda")
+        nat.check(lib.paco_debug_trace(tr.data_ptr()))
+        try:
+            M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)
+            torch.cuda.synchronize()
+        finally:
+            nat.check(lib.paco_debug_trace(None))
+        t = tr.view(-1, 10).cpu().numpy()
+        t = t[t[:, 2] > 0]
+        host = nat.plan_cta(nat.SR_MINPLUS_SAT32, n, m, k, len(t))
+        assert [tuple(r) for r in t[:, 4:10]] == [tuple(h) for h in host]
+        want = cref.mm(cref.SR_MINPLUS_SAT32, A.cpu().numpy(), B.cpu().numpy(), np.full((n, m), INF, np.int32))
+        assert np.array_equal(C.cpu().numpy(), want)

@@ -213,3 +213,23 @@ def test_native_one_piece_matches_reference_rule():
             want = [(t.region.i0, t.region.j0, t.region.l0, t.region.n, t.region.m, t.region.k)
                     for t in plan.compute_tasks()]
             assert nat.plan_one_piece(n, m, k, p) == want, (n, m, k, p)
+
+
+def test_cta_plan_balance_and_cover():
+    """Default CTA-level plan: tiles the unit grid exactly and stays within 3% of V/p."""
+    for (n, m, k) in [(8192, 8192, 8192), (16384, 16384, 16384), (9363, 8192, 8192),
+                      (7021, 10923, 8192), (4096, 4096, 4096), (65536, 1024, 256)]:
+        bm, bn, kq, cps = nat.tile_shape(nat.SR_MINPLUS_SAT32)
+        p = 148 * cps
+        pieces = nat.plan_cta(nat.SR_MINPLUS_SAT32, n, m, k, p)
+        units = (-(-n // bm), -(-m // bn), -(-k // kq))
+        vols = np.array([pc[3] * pc[4] * pc[5] for pc in pieces], dtype=float)
+        assert vols.sum() == units[0] * units[1] * units[2]
+        assert vols.max() / vols.mean() < 1.05, (n, m, k, vols.max() / vols.mean())
+        if (n, m, k) == (8192, 8192, 8192):
+            assert vols.max() / vols.mean() < 1.015
+    small = nat.plan_cta(nat.SR_MINPLUS_SAT32, 300, 260, 515, 7)
+    cover = np.zeros((3, 3, 129), np.int32)
+    for a, b, c, dn, dm, dk in small:
+        cover[a:a + dn, b:b + dm, c:c + dk] += 1
+    assert (cover == 1).all()
