@@ -28,7 +28,8 @@
 
 namespace paco {
 
-constexpr int kDefaultWaves = 2;
+// 8192^3 (min,+) with 1/2/3/4/5/8 waves of 296: 37.5/35.2/34.6/34.3/35.1/35.6 ms
+constexpr int kDefaultWaves = 4;
 
 // Device buffer of 10 x (grid size) int64 set by paco_debug_trace(); when
 // non-null every CTA of the next launches records smid and start/end times.
