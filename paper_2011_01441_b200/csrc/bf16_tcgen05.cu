@@ -2,10 +2,11 @@
 //
 // Replaces SEMIRING_F64.block_mm / _int_block (matmul.py:45-46,54) for the
 // dense bf16 case.  One persistent CTA per SM, warp-specialised:
-//   warp 0      TMA producer: A tile [128 x 64] and B^T tile [256 x 64] per
-//               k block (128B-swizzled, K-major) into a 4-stage smem ring;
-//               when K fits the ring (K <= 256) B^T stays resident across
-//               consecutive tiles of the same column block;
+//   warp 0      TMA producer: A tile [128 x 64] (K-major) and B tile
+//               [64 x 256] (N-major, as the caller stores it) per k block,
+//               128B-swizzled, into a 4-stage smem ring; when K fits the ring
+//               (K <= 256) B stays resident across consecutive tiles of the
+//               same column block;
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma.kind::f16
 //               (M=128, N=256, K=16) into a double-buffered TMEM accumulator
 //               (2 x 256 fp32 columns) and commits to mbarriers;
@@ -15,9 +16,7 @@
 // The CTA-level plan is the 1-D MM-1-Piece split of the column-block-major
 // tile sequence over the 148 CTAs (floor(p/2):ceil(p/2) halving of a 1-D
 // range == contiguous ranges of floor/ceil(T/p) tiles), which keeps each
-// CTA on one B^T column block.
-// B (k x m, row-major) is first transposed to B^T (m x k) in a library
-// workspace so both operands are K-major (the canonical UMMA SW128 layout).
+// CTA on one B column block.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -46,8 +45,9 @@ constexpr int SMEM_TOTAL = SMEM_BAR + 256;
 constexpr int SMEM_ALLOC = SMEM_TOTAL + 1024;  // runtime 1024-B alignment slack
 constexpr uint32_t TMEM_COLS = 512;
 
-// instruction descriptor: F32 accumulate, BF16 A/B, K-major both, N=256, M=128
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
+// instruction descriptor: F32 accumulate, BF16 A/B, A K-major, B MN-major
+// (bit 16), N=256, M=128
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(BN >> 3) << 17) |
                             (uint32_t(BM >> 4) << 24);
 
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
@@ -57,6 +57,19 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
   d |= uint64_t((saddr >> 4) & 0x3FFF);
   d |= uint64_t(1) << 16;
   d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
+
+// MN-major (N contiguous), 128B swizzle, canonical ((8,n),(8,k)):((1,LBO),(8,SBO))
+// in 16 B units: 64 N-elements per 128 B row, rows = k; 8-row (1024 B) atoms
+// step along k by SBO; 64-wide N chunks (one TMA box of BK rows each) step by LBO.
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((BK * 128) >> 4) << 16;  // LBO: next 64-wide N chunk
+  d |= uint64_t(1024 >> 4) << 32;        // SBO: next 8 k-rows
   d |= uint64_t(1) << 46;
   d |= uint64_t(2) << 61;
   return d;
@@ -125,6 +138,7 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 struct TcArgs {
   int64_t n, m, k;   // C is n x m
   int32_t a_col0;    // column offset of A inside its aligned tensor map
+  int32_t b_col0;    // column offset of B inside its aligned tensor map
   int32_t c_col0;    // column offset of C inside its aligned tensor map
   int32_t overwrite;
   int32_t tiles_rb;  // row blocks
@@ -187,7 +201,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           mbar_expect_tx(&full[s], keep_b ? A_BYTES : A_BYTES + B_BYTES);
           tma_load_2d(smem + SMEM_A + s * A_BYTES, &map_a, &full[s], args.a_col0 + kb * BK, rb * BM);
-          if (!keep_b) tma_load_2d(smem + SMEM_B + s * B_BYTES, &map_b, &full[s], kb * BK, nb * BN);
+          if (!keep_b) {
+            // B is k x m row-major (N contiguous): 4 boxes of [64 k rows][64 n]
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(smem + SMEM_B + s * B_BYTES + j * (BK * 128), &map_b, &full[s],
+                          args.b_col0 + nb * BN + 64 * j, kb * BK);
+          }
         }
         resident_nb = can_keep_b ? nb : -1;
       }
@@ -208,11 +228,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(&full[s], (it / STAGES) & 1);
           tc_fence_after();
           const uint64_t ad = smem_desc_sw128(smem_u32(smem + SMEM_A + s * A_BYTES));
-          const uint64_t bd = smem_desc_sw128(smem_u32(smem + SMEM_B + s * B_BYTES));
+          const uint64_t bd = smem_desc_mn_sw128(smem_u32(smem + SMEM_B + s * B_BYTES));
 #pragma unroll
           for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-            // advance 32 B (16 bf16) inside the 128 B swizzle row: +2 in 16 B units
-            umma_bf16(d_tmem, ad + uint64_t(2 * kk), bd + uint64_t(2 * kk), (kb | kk) != 0);
+            // A (K-major): +32 B inside the 128 B swizzle row = +2 units;
+            // B (MN-major): +16 k rows = 2 atoms of 1024 B = +128 units
+            umma_bf16(d_tmem, ad + uint64_t(2 * kk), bd + uint64_t(128 * kk), (kb | kk) != 0);
           }
           umma_commit(&empty[s]);  // stage is free once these MMAs complete
         }
@@ -285,22 +306,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(TMEM_COLS));
 }
 
-// B (k x m row-major, bf16) -> B^T (m x ldt) so the MMA sees a K-major B.
-__global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ B, int64_t ldb,
-                                      __nv_bfloat16* __restrict__ Bt, int64_t ldt, int64_t k, int64_t m) {
-  __shared__ __nv_bfloat16 tile[32][33];
-  const int64_t l0 = int64_t(blockIdx.y) * 32, j0 = int64_t(blockIdx.x) * 32;
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int64_t l = l0 + r, j = j0 + threadIdx.x;
-    tile[r][threadIdx.x] = (l < k && j < m) ? B[l * ldb + j] : __float2bfloat16(0.f);
-  }
-  __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int64_t j = j0 + r, l = l0 + threadIdx.x;
-    if (j < m && l < ldt) Bt[j * ldt + l] = (l < k) ? tile[threadIdx.x][r] : __float2bfloat16(0.f);
-  }
-}
-
 }  // namespace tc
 
 namespace {
@@ -328,8 +333,8 @@ int make_map(CUtensorMap* map, CUtensorMapDataType dt, int elsize, const void* p
   }
   const uintptr_t p = reinterpret_cast<uintptr_t>(ptr);
   const uintptr_t base = p & ~uintptr_t(15);
-  if ((p - base) % elsize != 0 || (ld * elsize) % 16 != 0) {
-    set_error("tcgen05 path needs element-aligned views with 16-byte row pitch (ld*%d %% 16 == 0)", elsize);
+  if ((p - base) % elsize != 0 || (ld * elsize) % 16 != 0) {  // callers repack first
+    set_error("internal: tensor map needs a 16-byte row pitch (ld*%d %% 16 == 0)", elsize);
     return PACO_ERR_UNSUPPORTED;
   }
   *col_off = int32_t((p - base) / elsize);
@@ -348,29 +353,33 @@ int make_map(CUtensorMap* map, CUtensorMapDataType dt, int elsize, const void* p
   return PACO_OK;
 }
 
-// Per-device workspace for B^T (grown on demand, never shrunk).
-struct Workspace {
+// Per-device scratch for operands whose row pitch is not a multiple of 16 B
+// (TMA needs it): they are repacked with a padded pitch.  Grown on demand.
+struct Scratch {
   void* ptr = nullptr;
   size_t bytes = 0;
 };
-std::mutex g_ws_mu;
-Workspace g_ws[64];
+std::mutex g_scratch_mu;
+Scratch g_scratch[64][3];
 
-int workspace(int device, size_t bytes, cudaStream_t st, void** out) {
-  std::lock_guard<std::mutex> lock(g_ws_mu);
-  Workspace& w = g_ws[device & 63];
+int scratch(int device, int slot, size_t bytes, cudaStream_t st, void** out) {
+  std::lock_guard<std::mutex> lock(g_scratch_mu);
+  Scratch& w = g_scratch[device & 63][slot];
   if (w.bytes < bytes) {
     if (w.ptr) {
       PACO_CUDA_TRY(cudaStreamSynchronize(st));
       PACO_CUDA_TRY(cudaFree(w.ptr));
-      w.ptr = nullptr;
-      w.bytes = 0;
+      w = Scratch{};
     }
     PACO_CUDA_TRY(cudaMalloc(&w.ptr, bytes));
     w.bytes = bytes;
   }
   *out = w.ptr;
   return PACO_OK;
+}
+
+bool pitch_ok(const void* p, int64_t ld, int elsize) {
+  return (reinterpret_cast<uintptr_t>(p) % elsize == 0) && (ld * elsize) % 16 == 0;
 }
 }  // namespace
 
@@ -385,27 +394,47 @@ int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t ld
     set_error("tcgen05 bf16 path: extents must fit int32");
     return PACO_ERR_ARG;
   }
-  // B^T workspace, K padded to a multiple of 8 (16-byte rows for TMA)
-  const int64_t ldt = (k + 7) / 8 * 8;
-  void* bt = nullptr;
-  int rc = workspace(device, size_t(m) * ldt * 2, stream, &bt);
-  if (rc) return rc;
-  {
-    dim3 grid(unsigned((m + 31) / 32), unsigned((ldt + 31) / 32)), block(32, 8);
-    tc::transpose_bf16_kernel<<<grid, block, 0, stream>>>(static_cast<const __nv_bfloat16*>(B), ldb,
-                                                          static_cast<__nv_bfloat16*>(bt), ldt, k, m);
-    PACO_CUDA_TRY(cudaGetLastError());
-  }
   CUtensorMap ma, mb, mc;
+  int rc;
   int32_t a_off = 0, b_off = 0, c_off = 0;
+  // operands with a row pitch TMA cannot take are repacked into padded scratch
+  if (!pitch_ok(A, lda, 2)) {
+    const int64_t ld2 = (k + 7) / 8 * 8;
+    void* p;
+    if ((rc = scratch(device, 0, size_t(n) * ld2 * 2, stream, &p))) return rc;
+    PACO_CUDA_TRY(cudaMemcpy2DAsync(p, ld2 * 2, A, lda * 2, k * 2, n, cudaMemcpyDeviceToDevice, stream));
+    A = p;
+    lda = ld2;
+  }
+  if (!pitch_ok(B, ldb, 2)) {
+    const int64_t ld2 = (m + 7) / 8 * 8;
+    void* p;
+    if ((rc = scratch(device, 1, size_t(k) * ld2 * 2, stream, &p))) return rc;
+    PACO_CUDA_TRY(cudaMemcpy2DAsync(p, ld2 * 2, B, ldb * 2, m * 2, k, cudaMemcpyDeviceToDevice, stream));
+    B = p;
+    ldb = ld2;
+  }
+  void* c_user = nullptr;
+  int64_t ldc_user = ldc;
+  if (!pitch_ok(C, ldc, 4)) {
+    const int64_t ld2 = (m + 3) / 4 * 4;
+    void* p;
+    if ((rc = scratch(device, 2, size_t(n) * ld2 * 4, stream, &p))) return rc;
+    if (!(flags & PACO_MM_OVERWRITE))
+      PACO_CUDA_TRY(cudaMemcpy2DAsync(p, ld2 * 4, C, ldc * 4, m * 4, n, cudaMemcpyDeviceToDevice, stream));
+    c_user = C;
+    C = p;
+    ldc = ld2;
+  }
   if ((rc = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, A, n, k, lda, tc::BK, tc::BM, &a_off))) return rc;
-  if ((rc = make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, bt, m, k, ldt, tc::BK, tc::BN, &b_off))) return rc;
+  if ((rc = make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, k, m, ldb, 64, tc::BK, &b_off))) return rc;
   if ((rc = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, n, m, ldc, 32, 32, &c_off))) return rc;
   tc::TcArgs args;
   args.n = n;
   args.m = m;
   args.k = k;
   args.a_col0 = a_off;
+  args.b_col0 = b_off;
   args.c_col0 = c_off;
   args.overwrite = (flags & PACO_MM_OVERWRITE) ? 1 : 0;
   args.tiles_rb = int32_t((n + tc::BM - 1) / tc::BM);
@@ -416,6 +445,8 @@ int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t ld
   PACO_CUDA_TRY(cudaFuncSetAttribute(tc::bf16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC));
   tc::bf16_tc_kernel<<<grid, tc::THREADS, tc::SMEM_ALLOC, stream>>>(ma, mb, mc, args);
   PACO_CUDA_TRY(cudaGetLastError());
+  if (c_user)
+    PACO_CUDA_TRY(cudaMemcpy2DAsync(c_user, ldc_user * 4, C, ldc * 4, m * 4, n, cudaMemcpyDeviceToDevice, stream));
   return PACO_OK;
 }
 

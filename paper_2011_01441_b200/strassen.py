@@ -1,0 +1,405 @@
+"""PACO-Strassen on B200 (the reference specifies it but ships no code).
+
+Follows SPEC.md:474-552 and the identities of PAPER.md:1839-1852:
+
+* ``strassen_seq(A, B, n, base=64)`` -- C = A x B with Strassen's 7-way
+  recursion down to ``base`` (B_str), then classic semiring MM leaves
+  (``mm_seq`` -> the sm_100a kernels with the CTA-level PACO plan).  S_r/T_r
+  formation and the C-block combination are ``paco_lincomb`` launches.
+  Non-power-of-two n is zero-padded.
+* ``strassen_paco_partition(n, p, base)`` -- pruned BFS of the arity-7 tree
+  (core.py:149-222 with arity 7); every internal node gets a FORM task (its
+  S/T additions, charged to the workers of its subtree, before its children)
+  and a COMBINE task (its C-block additions, after all seven children).
+* ``strassen_const_pieces_partition(n, p, cfg)`` -- the same, but after
+  ``cfg.gamma`` super-rounds every still-unassigned node is dealt out
+  round-robin (Corollary strassen-const-pieces).
+* ``strassen_execute(plan, A, B)`` -- runs a plan on the GPU(s): workers map
+  to (device, stream); returns C.
+
+Ring: float32 (FFMA leaves), float64 (DFMA leaves) or int64 (exact).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .device import View, pick_device, stage_in
+from .engine import execute_plan
+from .mm import launch_mm
+from .plan import COMPUTE, MERGE, Plan, PlanError, Task, pruned_bfs_assign
+
+DEFAULT_STRASSEN_BASE = 64
+
+# S_r, T_r and C-block formulas, 1-indexed as in PAPER.md:1839-1852:
+# (coefficient, quadrant "rc") of A for S_r, of B for T_r; (coefficient, r) of M for C blocks.
+S_TERMS = {1: ((1, "00"), (1, "11")), 2: ((1, "10"), (1, "11")), 3: ((1, "00"),), 4: ((1, "11"),),
+           5: ((1, "00"), (1, "01")), 6: ((1, "10"), (-1, "00")), 7: ((1, "01"), (-1, "11"))}
+T_TERMS = {1: ((1, "00"), (1, "11")), 2: ((1, "00"),), 3: ((1, "01"), (-1, "11")),
+           4: ((1, "10"), (-1, "00")), 5: ((1, "11"),), 6: ((1, "00"), (1, "01")),
+           7: ((1, "10"), (1, "11"))}
+C_TERMS = {"00": ((1, 1), (1, 4), (-1, 5), (1, 7)), "01": ((1, 3), (1, 5)),
+           "10": ((1, 2), (1, 4)), "11": ((1, 1), (1, 3), (-1, 2), (1, 6))}
+
+_RING = {  # torch dtype -> (leaf kernel id, lincomb dtype id)
+    torch.float32: (nat.SR_F32, nat.DT_F32),
+    torch.float64: (nat.SR_F64, nat.DT_F64),
+    torch.int64: (nat.SR_INT_I64, nat.DT_I64),
+}
+
+
+@dataclass(frozen=True)
+class SuperRoundCfg:
+    """Cap on assignment super-rounds for Strassen-Const-Pieces."""
+
+    gamma: int = 8
+
+    def __post_init__(self):
+        if self.gamma < 1:
+            raise PlanError(f"gamma must be >= 1, got {self.gamma}")
+
+
+class StrassenNode:
+    """One multiplication of the 7-way tree: ``path`` = sequence of r in 1..7."""
+
+    __slots__ = ("path", "size", "kids", "task_id")
+
+    def __init__(self, path: tuple[int, ...], size: int):
+        self.path = path
+        self.size = size
+        self.kids: list[StrassenNode] = []
+        self.task_id: int | None = None
+
+    @property
+    def depth(self) -> int:
+        return len(self.path)
+
+    @property
+    def volume(self) -> int:
+        """Strassen work of the node: 7^log2(size) (= size^log2 7) leaf-size units."""
+        return 7 ** int(round(math.log2(self.size))) if self.size >= 1 else 0
+
+    def __str__(self) -> str:
+        return "strassen[depth=%d,path=%s,n=%d]" % (self.depth, ".".join(map(str, self.path)) or "-",
+                                                   self.size)
+
+
+def _padded(n: int) -> int:
+    if n < 1:
+        raise PlanError("n must be >= 1")
+    return 1 << (n - 1).bit_length()
+
+
+def _expand(node: StrassenNode) -> list[StrassenNode]:
+    node.kids = [StrassenNode(node.path + (r,), node.size // 2) for r in range(1, 8)]
+    return node.kids
+
+
+def _assemble(root: StrassenNode, assigned: list[Task], p: int, n: int, base: int, variant: str) -> Plan:
+    """Topological task list: FORM(internal, BFS) -> COMPUTE(assigned) -> COMBINE(reverse BFS)."""
+    internal: list[StrassenNode] = []
+    frontier = [root]
+    while frontier:
+        nxt = []
+        for nd in frontier:
+            if nd.kids:
+                internal.append(nd)
+                nxt.extend(nd.kids)
+        frontier = nxt
+    owner = {id(t.region): t.worker for t in assigned}
+
+    workers_of: dict[int, tuple[int, ...]] = {}
+
+    def subtree(nd: StrassenNode) -> tuple[int, ...]:
+        key = id(nd)
+        if key not in workers_of:
+            if key in owner:
+                workers_of[key] = (owner[key],)
+            else:
+                workers_of[key] = tuple(sorted({w for k in nd.kids for w in subtree(k)}))
+        return workers_of[key]
+
+    def pack(ws):
+        return ws[0] if len(ws) == 1 else ws
+
+    tasks: list[Task] = []
+    form_id: dict[int, int] = {}
+    parent_of: dict[int, StrassenNode] = {id(k): nd for nd in internal for k in nd.kids}
+    for nd in internal:
+        par = parent_of.get(id(nd))
+        half = (nd.size // 2) ** 2
+        t = Task(id=len(tasks), kind=MERGE, region=f"form[{nd}]", worker=pack(subtree(nd)),
+                 deps=(form_id[id(par)],) if par is not None else (), cost_work=10 * half)
+        form_id[id(nd)] = t.id
+        tasks.append(t)
+    done_id: dict[int, int] = {}
+    for a in assigned:
+        nd = a.region
+        par = parent_of.get(id(nd))
+        t = Task(id=len(tasks), kind=COMPUTE, region=nd, worker=a.worker,
+                 deps=(form_id[id(par)],) if par is not None else (), cost_work=nd.volume, label=a.label)
+        nd.task_id = t.id
+        done_id[id(nd)] = t.id
+        tasks.append(t)
+    for nd in reversed(internal):
+        half = (nd.size // 2) ** 2
+        t = Task(id=len(tasks), kind=MERGE, region=f"combine[{nd}]", worker=pack(subtree(nd)),
+                 deps=tuple(sorted(done_id[id(k)] for k in nd.kids)), cost_work=8 * half)
+        done_id[id(nd)] = t.id
+        tasks.append(t)
+    temp = sum(21 * (nd.size // 2) ** 2 for nd in internal)
+    meta = {"algo": "strassen", "variant": variant, "n": n, "n_padded": root.size, "base": base,
+            "internal": len(internal), "leaves": len(assigned), "temp_peak": temp,
+            "tree": root}
+    return Plan(tasks=tasks, p=p, meta=meta)
+
+
+def strassen_paco_partition(n: int, p: int, base: int = DEFAULT_STRASSEN_BASE) -> Plan:
+    """PACO-Strassen: pruned BFS of the 7-way tree."""
+    size = _padded(n)
+    root = StrassenNode((), size)
+    bfs = pruned_bfs_assign(root, 7, _expand, lambda nd: nd.size <= base, p,
+                            cost=lambda nd: nd.volume)
+    return _assemble(root, bfs.tasks, p, n, base, "paco")
+
+
+def strassen_const_pieces_partition(n: int, p: int, cfg: SuperRoundCfg = SuperRoundCfg(),
+                                    base: int = DEFAULT_STRASSEN_BASE) -> Plan:
+    """Strassen-Const-Pieces: pruned BFS capped at ``cfg.gamma`` super-rounds.
+
+    A super-round ends when at least one batch fired at the current depth and
+    fewer than p nodes survive; after the gamma-th, every
+    surviving node is assigned round-robin in one final batch.
+    """
+    if p < 1:
+        raise PlanError(f"need at least one worker, got p={p}")
+    size = _padded(n)
+    root = StrassenNode((), size)
+    assigned: list[Task] = []
+    cursor, label, rounds = 0, 0, 0
+
+    def deal(nodes):
+        nonlocal cursor, label
+        label += 1
+        for nd in nodes:
+            assigned.append(Task(len(assigned), COMPUTE, nd, cursor, (), nd.volume, label))
+            cursor = (cursor + 1) % p
+
+    frontier = [root]
+    while frontier:
+        fired = False
+        while len(frontier) >= p:
+            deal(frontier[:p])
+            frontier = frontier[p:]
+            fired = True
+        if not frontier:
+            break
+        if fired:
+            rounds += 1
+            if rounds >= cfg.gamma:
+                deal(frontier)
+                break
+        if all(nd.size <= base for nd in frontier):
+            deal(frontier)
+            break
+        nxt = []
+        for nd in frontier:
+            nxt.extend([nd] if nd.size <= base else _expand(nd))
+        frontier = nxt
+    return _assemble(root, assigned, p, n, base, f"const-pieces(gamma={cfg.gamma})")
+
+
+# ---------------------------------------------------------------- device side
+
+def _quad(v: View, q: str) -> View:
+    h = v.rows // 2
+    r, c = int(q[0]), int(q[1])
+    return v.sub(r * h, c * h, h, h)
+
+
+def _lincomb(dt: int, stream, out: View, terms, accumulate: bool = False) -> None:
+    nin = len(terms)
+    ins = (ctypes.c_void_p * nin)(*[t[1].ptr for t in terms])
+    lds = (ctypes.c_int64 * nin)(*[t[1].ld for t in terms])
+    coefs = (ctypes.c_int32 * nin)(*[t[0] for t in terms])
+    nat.check(nat.load().paco_lincomb(out.device, stream.cuda_stream, dt, out.ptr, out.ld, out.rows,
+                                      out.cols, nin, ins, lds, coefs, int(accumulate)))
+
+
+class _Workspace:
+    """S/T/M buffers of one internal node: 7 of each, (size/2)^2, on one device."""
+
+    def __init__(self, size: int, dtype: torch.dtype, device: int):
+        h = size // 2
+        self.S = [View.of(torch.empty((h, h), dtype=dtype, device=device)) for _ in range(7)]
+        self.T = [View.of(torch.empty((h, h), dtype=dtype, device=device)) for _ in range(7)]
+        self.M = [View.of(torch.empty((h, h), dtype=dtype, device=device)) for _ in range(7)]
+
+
+def _form(ws: _Workspace, A: View, B: View, dt: int, stream) -> None:
+    for r in range(1, 8):
+        _lincomb(dt, stream, ws.S[r - 1], [(c, _quad(A, q)) for c, q in S_TERMS[r]])
+        _lincomb(dt, stream, ws.T[r - 1], [(c, _quad(B, q)) for c, q in T_TERMS[r]])
+
+
+def _combine(ws: _Workspace, C: View, dt: int, stream) -> None:
+    for q, terms in C_TERMS.items():
+        _lincomb(dt, stream, _quad(C, q), [(c, ws.M[r - 1]) for c, r in terms])
+
+
+def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stream) -> None:
+    """C = A x B (square, power-of-two size) on one device, depth-first."""
+    kid, dt = _RING[dtype]
+    if C.rows <= base or C.rows % 2:
+        launch_mm(kid, stream, A, B, C, overwrite=True)
+        return
+    ws = _Workspace(C.rows, dtype, C.device)
+    _form(ws, A, B, dt, stream)
+    for r in range(7):
+        _strassen_dev(ws.S[r], ws.T[r], ws.M[r], base, dtype, stream)
+    _combine(ws, C, dt, stream)
+
+
+def _ring_dtype(A, B) -> torch.dtype:
+    dts = set()
+    for x in (A, B):
+        dts.add(x.dtype if isinstance(x, torch.Tensor) else {
+            np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+            np.dtype(np.int64): torch.int64, np.dtype(np.int32): torch.int64}[np.dtype(x.dtype)])
+    if dts == {torch.float32}:
+        return torch.float32
+    if torch.float64 in dts or torch.float32 in dts:
+        return torch.float64
+    return torch.int64
+
+
+def _staged_square(X, size: int, dtype: torch.dtype, dev: int) -> torch.Tensor:
+    t = stage_in(X, dtype, dev)
+    if t.shape[0] == size and t.shape[1] == size:
+        return t
+    out = torch.zeros((size, size), dtype=dtype, device=dev)
+    out[:t.shape[0], :t.shape[1]] = t
+    return out
+
+
+def strassen_seq(A, B, n: int | None = None, base: int = DEFAULT_STRASSEN_BASE, *,
+                 stream: torch.cuda.Stream | None = None):
+    """C = A x B by Strassen down to ``base``, then classic MM.
+
+    A, B: n x n NumPy arrays or CUDA tensors (float32 / float64 / int64 ring).
+    Returns C of A's kind.
+    """
+    n = n if n is not None else A.shape[0]
+    if tuple(A.shape) != (n, n) or tuple(B.shape) != (n, n):
+        raise ValueError(f"shape mismatch: A{tuple(A.shape)} B{tuple(B.shape)} n={n}")
+    dtype = _ring_dtype(A, B)
+    dev = pick_device(A, B)
+    size = _padded(n)
+    with torch.cuda.device(dev):
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.stream(st):
+            a = _staged_square(A, size, dtype, dev)
+            b = _staged_square(B, size, dtype, dev)
+            c = torch.empty((size, size), dtype=dtype, device=dev)
+            _strassen_dev(View.of(a), View.of(b), View.of(c), base, dtype, st)
+            c = c[:n, :n]
+    if isinstance(A, np.ndarray):
+        return c.cpu().numpy()
+    return c if isinstance(A, torch.Tensor) and A.is_cuda else c.cpu()
+
+
+def strassen_execute(plan: Plan, A, B, mode: str = "serial_sim", *, devices: list[int] | None = None,
+                     with_report: bool = False):
+    """Run a Strassen plan; returns C = A x B (and the
+    CostReport -- work, makespan, temp_space_peak -- when ``with_report``).
+
+    Workers map to ``devices[w % len(devices)]`` with one stream each.  S/T/M
+    buffers live on the first device; FORM/COMBINE tasks run on their first
+    worker, COMPUTE tasks run ``strassen_seq`` of their node into the
+    parent's M slot.
+    """
+    meta = plan.meta
+    if meta.get("algo") != "strassen":
+        raise PlanError("not a Strassen plan")
+    n, size, base = meta["n"], meta["n_padded"], meta["base"]
+    if tuple(A.shape) != (n, n) or tuple(B.shape) != (n, n):
+        raise ValueError(f"shape mismatch: A{tuple(A.shape)} B{tuple(B.shape)} n={n}")
+    dtype = _ring_dtype(A, B)
+    kid, dt = _RING[dtype]
+    if devices is None:
+        devices = [pick_device(A, B)]
+    home = devices[0]
+    dev_of = [devices[w % len(devices)] for w in range(plan.p)]
+    for d in sorted(set(dev_of)):
+        if d != home:
+            nat.check(nat.load().paco_enable_peer(d, home))
+    root: StrassenNode = meta["tree"]
+    with torch.cuda.device(home):
+        stage = torch.cuda.current_stream(home)
+        a = _staged_square(A, size, dtype, home)
+        b = _staged_square(B, size, dtype, home)
+        c = torch.empty((size, size), dtype=dtype, device=home)
+        # operand / output views of every node, and workspaces of internal nodes
+        ops: dict[int, tuple[View, View, View]] = {id(root): (View.of(a), View.of(b), View.of(c))}
+        wss: dict[int, _Workspace] = {}
+        stack = [root]
+        while stack:
+            nd = stack.pop()
+            if nd.kids:
+                ws = _Workspace(nd.size, dtype, home)
+                wss[id(nd)] = ws
+                for r, kid_nd in enumerate(nd.kids):
+                    ops[id(kid_nd)] = (ws.S[r], ws.T[r], ws.M[r])
+                    stack.append(kid_nd)
+        staged = torch.cuda.Event()
+        staged.record(stage)
+        streams = [torch.cuda.Stream(device=dev_of[w]) for w in range(plan.p)]
+        for s in streams:
+            s.wait_event(staged)
+        events: list = [None] * len(plan.tasks)
+        by_name = {}
+        stack = [root]
+        while stack:
+            nd = stack.pop()
+            by_name[str(nd)] = nd
+            stack.extend(nd.kids)
+
+        def runner(task: Task) -> None:
+            w = task.workers()[0]
+            st = streams[w]
+            for d in task.deps:
+                st.wait_event(events[d])
+            with torch.cuda.device(dev_of[w]):
+                if task.kind == COMPUTE:
+                    nd = task.region
+                    A_n, B_n, C_n = ops[id(nd)]
+                    with torch.cuda.stream(st):
+                        _strassen_dev(A_n, B_n, C_n, base, dtype, st)
+                else:
+                    what, name = task.region.split("[", 1)
+                    nd = by_name[name[:-1]]
+                    A_n, B_n, C_n = ops[id(nd)]
+                    if what == "form":
+                        _form(wss[id(nd)], A_n, B_n, dt, st)
+                    else:
+                        _combine(wss[id(nd)], C_n, dt, st)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            events[task.id] = ev
+
+        report = execute_plan(plan, runner, mode)
+        for s in streams:
+            stage.wait_stream(s)
+        out = c[:n, :n]
+        torch.cuda.current_stream(home).synchronize()
+    if isinstance(A, np.ndarray):
+        out = out.cpu().numpy()
+    elif not (isinstance(A, torch.Tensor) and A.is_cuda):
+        out = out.cpu()
+    return (out, report) if with_report else out

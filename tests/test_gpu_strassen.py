@@ -1,0 +1,71 @@
+"""GPU parity of PACO-Strassen against the CPU restatement.
+
+Integer ring: exact equality with the NumPy product / oracle Strassen.
+float32: relative Frobenius error <= 1e-4 against the float64 oracle Strassen
+(BASELINE cfg5 tolerance), at reduced size and at the full n=16384.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import paco_numpy as PN
+from paper_2011_01441_b200 import strassen as S
+
+pytestmark = pytest.mark.gpu
+
+
+def test_known_answers():
+    assert S.strassen_seq(np.array([[3]], np.int64), np.array([[-4]], np.int64), 1).tolist() == [[-12]]
+    rng = np.random.default_rng(1)
+    B4 = rng.integers(-9, 10, (4, 4)).astype(np.int64)
+    assert np.array_equal(S.strassen_seq(np.eye(4, dtype=np.int64), B4, 4, base=1), B4)
+    A8, B8 = rng.integers(-9, 10, (8, 8)).astype(np.int64), rng.integers(-9, 10, (8, 8)).astype(np.int64)
+    assert np.array_equal(S.strassen_seq(A8, B8, 8, base=1), A8 @ B8)
+
+
+@pytest.mark.parametrize("n,base", [(16, 2), (64, 8), (100, 16), (256, 32), (256, 64)])
+def test_integer_ring_exact(n, base):
+    rng = np.random.default_rng(n + base)
+    A = rng.integers(-50, 50, (n, n)).astype(np.int64)
+    B = rng.integers(-50, 50, (n, n)).astype(np.int64)
+    assert np.array_equal(S.strassen_seq(A, B, n, base=base), A @ B)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 7, 10, 13])
+def test_execute_plans_integer_exact(p):
+    rng = np.random.default_rng(p)
+    n = 256
+    A = rng.integers(-30, 30, (n, n)).astype(np.int64)
+    B = rng.integers(-30, 30, (n, n)).astype(np.int64)
+    for plan in (S.strassen_paco_partition(n, p, base=16),
+                 S.strassen_const_pieces_partition(n, p, S.SuperRoundCfg(2), base=16)):
+        for mode in ("serial_sim", "parallel"):
+            C = S.strassen_execute(plan, A, B, mode)
+            assert np.array_equal(C, A @ B), (p, mode, plan.meta["variant"])
+
+
+def test_f32_two_levels_vs_oracle():
+    rng = np.random.default_rng(1005)
+    n = 2048
+    A = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    B = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    C = S.strassen_seq(A, B, n, base=n // 4)
+    ref = PN.strassen(A.astype(np.float64), B.astype(np.float64), 2)
+    err = np.linalg.norm(C.astype(np.float64) - ref) / np.linalg.norm(ref)
+    assert err <= 1e-4, err
+
+
+def test_cfg5_full_size_vs_oracle():
+    """BASELINE cfg5: n=16384, 2 levels (49 leaves of 4096^3), fp32, rel Frobenius <= 1e-4."""
+    rng = np.random.default_rng(1005)
+    n = 16384
+    A = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    B = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    c = S.strassen_seq(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), n, base=n // 4)
+    C = c.cpu().numpy()
+    del c
+    torch.cuda.empty_cache()
+    ref = PN.strassen(A.astype(np.float64), B.astype(np.float64), 2)
+    err = np.linalg.norm(C.astype(np.float64) - ref) / np.linalg.norm(ref)
+    assert err <= 1e-4, err
