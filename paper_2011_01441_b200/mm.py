@@ -87,19 +87,78 @@ def mm_seq(A, B, C, semiring: Semiring = SEMIRING_INT, base: int = DEFAULT_BASE,
     ``pieces`` overrides the CTA-level PACO plan (tile-unit cuboids);
     ``overwrite`` declares C == zero so the kernel does not read it.
     """
-    _shape_check(A, B, C)
+    n, m, k = _shape_check(A, B, C)
     if sim is not None:
         raise NotImplementedError("cache simulation is out of scope on B200; use ncu counters")
     kid, in_dt = kernel_for(semiring, A, B)
     dev = pick_device(A, B, C)
     with torch.cuda.device(dev):
         st = stream if stream is not None else torch.cuda.current_stream(dev)
+        if pieces is None and _pinned_host(A, in_dt) and _pinned_host(B, in_dt) \
+                and _pinned_host(C, semiring.dtype) and n >= 2 * _PIPE_MIN_ROWS:
+            _pipelined_host_mm(A, B, C, kid, semiring, dev, st, overwrite)
+            return
         with torch.cuda.stream(st):
             a = View.of(stage_in(A, in_dt, dev))
             b = View.of(stage_in(B, in_dt, dev))
             out = Output(C, semiring.dtype, dev, load=not overwrite)
             launch_mm(kid, st, a, b, View.of(out.dev), pieces=pieces, overwrite=overwrite)
             out.finish()
+
+
+_PIPE_MIN_ROWS = 512
+
+
+def _pinned_host(x, dtype) -> bool:
+    return (isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.is_contiguous()
+            and x.dtype == torch_dtype(dtype))
+
+
+def _pipelined_host_mm(A, B, C, kid: int, semiring: Semiring, dev: int, st, overwrite: bool) -> None:
+    """Host (pinned) operands: overlap H2D, compute and D2H by row blocks.
+
+    B goes up first (every row block needs all of it); then row block i of
+    A (and of C unless overwriting) is copied on an H2D stream, multiplied on
+    ``st`` as soon as it lands, and its C rows stream back on a D2H stream
+    while block i+1 computes.  The reference mutates C synchronously, so this
+    returns only after the last D2H completes.
+    """
+    n, k = tuple(A.shape)
+    m = B.shape[1]
+    nblk = max(2, min(8, n // _PIPE_MIN_ROWS))
+    edges = [((n * i // nblk) // 128) * 128 for i in range(nblk)] + [n]
+    h2d = torch.cuda.Stream(device=dev)
+    d2h = torch.cuda.Stream(device=dev)
+    h2d.wait_stream(st)
+    a_d = torch.empty((n, k), dtype=A.dtype, device=dev)
+    b_d = torch.empty((k, m), dtype=B.dtype, device=dev)
+    c_d = torch.empty((n, m), dtype=C.dtype, device=dev)
+    for t in (a_d, b_d, c_d):
+        t.record_stream(h2d)
+        t.record_stream(d2h)
+    av, bv, cv = View.of(a_d), View.of(b_d), View.of(c_d)
+    landed = []
+    with torch.cuda.stream(h2d):
+        b_d.copy_(B, non_blocking=True)
+        for r0, r1 in zip(edges[:-1], edges[1:]):
+            a_d[r0:r1].copy_(A[r0:r1], non_blocking=True)
+            if not overwrite:
+                c_d[r0:r1].copy_(C[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+            landed.append(ev)
+    for (r0, r1), ev in zip(zip(edges[:-1], edges[1:]), landed):
+        if r1 <= r0:
+            continue
+        st.wait_event(ev)
+        launch_mm(kid, st, av.sub(r0, 0, r1 - r0, k), bv, cv.sub(r0, 0, r1 - r0, m), overwrite=overwrite)
+        done = torch.cuda.Event()
+        done.record(st)
+        d2h.wait_event(done)
+        with torch.cuda.stream(d2h):
+            C[r0:r1].copy_(c_d[r0:r1], non_blocking=True)
+    st.wait_stream(d2h)
+    d2h.synchronize()
 
 
 def mm_oracle(A, B, semiring: Semiring = SEMIRING_INT):

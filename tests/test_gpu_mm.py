@@ -270,3 +270,20 @@ def test_device_derived_cta_plan_matches_host_plan():
         assert [tuple(r) for r in t[:, 4:10]] == [tuple(h) for h in host]
         want = cref.mm(cref.SR_MINPLUS_SAT32, A.cpu().numpy(), B.cpu().numpy(), np.full((n, m), INF, np.int32))
         assert np.array_equal(C.cpu().numpy(), want)
+
+
+def test_pinned_host_pipeline_matches_oracle():
+    """Pinned host operands take the overlapped H2D/compute/D2H path."""
+    rng = np.random.default_rng(41)
+    n, m, k = 1500, 700, 333
+    A = torch.from_numpy(tropical(rng, (n, k), 0, 2**20, 0.1)).pin_memory()
+    B = torch.from_numpy(tropical(rng, (k, m), 0, 2**20, 0.1)).pin_memory()
+    C0 = tropical(rng, (n, m), 0, 2**21, 0.3)
+    C = torch.from_numpy(C0.copy()).pin_memory()
+    M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)
+    want = cref.mm(cref.SR_MINPLUS_SAT32, A.numpy(), B.numpy(), C0.copy())
+    assert np.array_equal(C.numpy(), want)
+    C2 = torch.full((n, m), 12345, dtype=torch.int32).pin_memory()
+    M.mm_seq(A, B, C2, M.SEMIRING_MINPLUS_SAT, overwrite=True)
+    want2 = cref.mm(cref.SR_MINPLUS_SAT32, A.numpy(), B.numpy(), np.full((n, m), INF, np.int32))
+    assert np.array_equal(C2.numpy(), want2)
