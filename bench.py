@@ -115,7 +115,7 @@ def alu_peak(device):
     return tpc.value, mhz.value
 
 
-def cpu_baseline(rows_per_proc=16):
+def cpu_baseline(rows_per_proc=48):
     out = subprocess.run([sys.executable, "-m", "oracle.cpu_baseline", "--cfg", "2",
                           "--rows-per-proc", str(rows_per_proc)], cwd=ROOT, capture_output=True,
                          text=True, timeout=900)
@@ -157,7 +157,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--ref-rows", type=int, default=16, help="rows of A per host process (reference arm)")
+    ap.add_argument("--ref-rows", type=int, default=48, help="rows of A per host process (reference arm)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
