@@ -115,10 +115,10 @@ def alu_peak(device):
     return tpc.value, mhz.value
 
 
-def cpu_baseline(rows_per_proc=48):
+def cpu_baseline(rows_per_proc=48, repeat=1):
     out = subprocess.run([sys.executable, "-m", "oracle.cpu_baseline", "--cfg", "2",
-                          "--rows-per-proc", str(rows_per_proc)], cwd=ROOT, capture_output=True,
-                         text=True, timeout=900)
+                          "--rows-per-proc", str(rows_per_proc), "--repeat", str(repeat)], cwd=ROOT,
+                         capture_output=True, text=True, timeout=1800)
     if out.returncode != 0:
         return {"value": None, "unit": "Gop/s", "cores": None, "kind": "port",
                 "sample": "failed: " + out.stderr.strip()[-200:]}
@@ -129,12 +129,8 @@ def run_reference(args, rank, world):
     """--impl reference: the reference CPU algorithm on the host cores."""
     if rank != 0:
         return
-    vals = []
-    last = None
-    for i in range(args.warmup + args.steps):
-        last = cpu_baseline(rows_per_proc=args.ref_rows)
-        if i >= args.warmup:
-            vals.append(last["value"])
+    last = cpu_baseline(rows_per_proc=args.ref_rows, repeat=args.warmup + args.steps)
+    vals = (last.get("values") or [last["value"]])[args.warmup:] or [last["value"]]
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gop/s", "n_gpus": world,

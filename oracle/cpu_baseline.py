@@ -67,20 +67,26 @@ def _work(args):
     return time.perf_counter() - t0
 
 
-def measure(cfg: int, rows_per_proc: int, procs: int | None = None) -> dict:
+def measure(cfg: int, rows_per_proc: int, procs: int | None = None, repeat: int = 1) -> dict:
     procs = procs or len(os.sched_getaffinity(0))
     A, B, kind = cfg_inputs(cfg, rows_per_proc * procs)
     _G.update(A=A, B=B, kind=kind)
     slabs = [(i * rows_per_proc, (i + 1) * rows_per_proc) for i in range(procs)]
     ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(procs) as pool:
-        per = pool.map(_work, slabs)
-    wall = time.perf_counter() - t0
     n_rows = rows_per_proc * procs
     ops = 2.0 * n_rows * B.shape[1] * B.shape[0]
+    values, walls, per = [], [], [0.0]
+    with ctx.Pool(procs) as pool:
+        for _ in range(repeat):
+            t0 = time.perf_counter()
+            per = pool.map(_work, slabs)
+            wall = time.perf_counter() - t0
+            walls.append(wall)
+            values.append(ops / wall / 1e9)
+    wall = walls[-1]
     return {
-        "value": ops / wall / 1e9,
+        "value": values[-1],
+        "values": values,
         "unit": "Gop/s",
         "cores": procs,
         "kind": "port",
@@ -97,5 +103,6 @@ if __name__ == "__main__":
     ap.add_argument("--cfg", type=int, default=2)
     ap.add_argument("--rows-per-proc", type=int, default=32)
     ap.add_argument("--procs", type=int, default=None)
+    ap.add_argument("--repeat", type=int, default=1)
     a = ap.parse_args()
-    print(json.dumps(measure(a.cfg, a.rows_per_proc, a.procs)))
+    print(json.dumps(measure(a.cfg, a.rows_per_proc, a.procs, a.repeat)))
