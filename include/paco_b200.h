@@ -51,7 +51,8 @@ extern "C" {
 #define PACO_SR_MAXPLUS_SAT32 5   /* (max,+) int32 storage, domain [-2^30,2^30), -INF=-2^30, saturating */
 #define PACO_SR_F32 6             /* (+,x)  f32 -> f32 (FFMA)                                          */
 #define PACO_SR_BF16_F32 7        /* (+,x)  bf16,bf16 -> f32 (tcgen05 tensor cores)                    */
-#define PACO_SR_COUNT 8
+#define PACO_SR_F32_TC 8          /* (+,x)  f32 -> f32 as 3xTF32 on tcgen05 (hi/lo split, ~fp32 accuracy) */
+#define PACO_SR_COUNT 9
 
 #define PACO_TROPICAL_INF (1 << 30)
 

@@ -25,6 +25,8 @@ SR_MINPLUS_SAT32 = 4
 SR_MAXPLUS_SAT32 = 5
 SR_F32 = 6
 SR_BF16_F32 = 7
+SR_F32_TC = 8
+SR_COUNT = 9
 
 DT_F32, DT_F64, DT_I64 = 0, 1, 2
 

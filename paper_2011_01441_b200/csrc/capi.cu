@@ -26,7 +26,10 @@ int simt_tile_shape(int sr, int* bm, int* bn, int* bk, int* cps);
 int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B,
                       int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
                       const int32_t* pieces, int n_pieces, int flags);
-int bf16_tile_shape(int* bm, int* bn, int* bk, int* cps);
+int launch_mm_f32_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B,
+                     int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
+                     const int32_t* pieces, int n_pieces, int flags);
+int tc_tile_shape(int semiring, int* bm, int* bn, int* bk, int* cps);
 int launch_fold(int sr, cudaStream_t st, void* dst, int64_t ldd, void* src, int64_t lds, int64_t n,
                 int64_t m, int reset);
 int launch_fill(int sr, cudaStream_t st, void* dst, int64_t ld, int64_t n, int64_t m);
@@ -102,6 +105,8 @@ int paco_mm(int device, void* stream, int semiring, const void* A, int64_t lda, 
   }
   if (semiring == PACO_SR_BF16_F32)
     return launch_mm_bf16_tc(device, st, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
+  if (semiring == PACO_SR_F32_TC)
+    return launch_mm_f32_tc(device, st, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
   return launch_mm_simt(semiring, device, st, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
 }
 
@@ -111,7 +116,7 @@ int paco_mm_tile_shape(int semiring, int* bm, int* bn, int* bk, int* cps) {
     set_error("paco_mm_tile_shape: null output pointer");
     return PACO_ERR_ARG;
   }
-  if (semiring == PACO_SR_BF16_F32) return bf16_tile_shape(bm, bn, bk, cps);
+  if (semiring == PACO_SR_BF16_F32 || semiring == PACO_SR_F32_TC) return tc_tile_shape(semiring, bm, bn, bk, cps);
   return simt_tile_shape(semiring, bm, bn, bk, cps);
 }
 

@@ -187,7 +187,8 @@ int dispatch_op(int sr, F&& f) {
     case PACO_SR_MINPLUS_I64: return f(OpMinPlusI64{});
     case PACO_SR_MINPLUS_SAT32: return f(OpMinPlusSat32{});
     case PACO_SR_MAXPLUS_SAT32: return f(OpMaxPlusSat32{});
-    case PACO_SR_F32: return f(OpF32{});
+    case PACO_SR_F32:
+    case PACO_SR_F32_TC: return f(OpF32{});
     case PACO_SR_BF16_F32: return f(OpBF16F32{});
     default: set_error("unknown semiring id %d", sr); return PACO_ERR_ARG;
   }

@@ -1,7 +1,8 @@
-// bf16 x bf16 -> fp32 (+,x) MM on the 5th-generation tensor cores (cfg3).
+// (+,x) MM on the 5th-generation tensor cores: bf16 x bf16 -> fp32 (cfg3) and
+// fp32 x fp32 -> fp32 as 3xTF32 (Strassen leaves, cfg5).
 //
 // Replaces SEMIRING_F64.block_mm / _int_block (matmul.py:45-46,54) for the
-// dense bf16 case.  One persistent CTA per SM, warp-specialised:
+// dense floating-point case.  One persistent CTA per SM, warp-specialised:
 //   warp 0      TMA producer: A tile [128 x 64] (K-major) and B tile
 //               [64 x 256] (N-major, as the caller stores it) per k block,
 //               128B-swizzled, into a 4-stage smem ring; when K fits the ring
@@ -17,11 +18,20 @@
 // tile sequence over the 148 CTAs (floor(p/2):ceil(p/2) halving of a 1-D
 // range == contiguous ranges of floor/ceil(T/p) tiles), which keeps each
 // CTA on one B column block.
+//
+// 3xTF32: every fp32 operand x is split (by split_tf32_kernel) into
+// hi = x with the low 13 mantissa bits cleared (exactly representable in tf32)
+// and lo = x - hi (exact in fp32); C += Ahi*Bhi + Ahi*Blo + Alo*Bhi with
+// kind::tf32 MMAs accumulating in fp32 TMEM -- ~fp32 accuracy (the dropped
+// Alo*Blo term is < 2^-20 relative) at tensor-core rate.  The split writes B
+// transposed (K-major): kind::tf32 with an MN-major B descriptor returned
+// zeros on this toolchain/hardware, K-major both sides is exact.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -31,24 +41,43 @@ namespace paco {
 
 namespace tc {
 
-constexpr int BM = 128, BN = 256, BK = 64, UMMA_K = 16;
-constexpr int STAGES = 4;
-constexpr int THREADS = 192;  // 6 warps
-constexpr int A_BYTES = BM * BK * 2;        // 16 KB
-constexpr int B_BYTES = BN * BK * 2;        // 32 KB
+constexpr int BM = 128;
+constexpr int THREADS = 192;                // 6 warps
 constexpr int EPI_BUF = 32 * 32 * 4;        // 4 KB: 32 rows x 32 fp32 (128 B)
-constexpr int SMEM_A = 0;
-constexpr int SMEM_B = SMEM_A + STAGES * A_BYTES;
-constexpr int SMEM_EPI = SMEM_B + STAGES * B_BYTES;
-constexpr int SMEM_BAR = SMEM_EPI + 4 * 2 * EPI_BUF;
-constexpr int SMEM_TOTAL = SMEM_BAR + 256;
-constexpr int SMEM_ALLOC = SMEM_TOTAL + 1024;  // runtime 1024-B alignment slack
-constexpr uint32_t TMEM_COLS = 512;
 
-// instruction descriptor: F32 accumulate, BF16 A/B, A K-major, B MN-major
-// (bit 16), N=256, M=128
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(BN >> 3) << 17) |
-                            (uint32_t(BM >> 4) << 24);
+// bf16 inputs, one MMA pass; N=256 tiles, 64-deep k blocks (128 B rows).
+struct KindBF16 {
+  static constexpr int BN = 256, BK = 64, UMMA_K = 16, STAGES = 4, ELEM = 2, NOPS = 1, PASSES = 1;
+  static constexpr bool B_KMAJOR = false;
+  // F32 accumulate, BF16 A/B (format 1), A K-major, B MN-major (bit 16)
+  static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                                    (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+  static constexpr CUtensorMapDataType DT = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+};
+// fp32 inputs as 3xTF32 (hi/lo operand tiles), N=128 tiles, 32-deep k blocks.
+struct KindTF32x3 {
+  static constexpr int BN = 128, BK = 32, UMMA_K = 8, STAGES = 3, ELEM = 4, NOPS = 2, PASSES = 3;
+  static constexpr bool B_KMAJOR = true;  // B^T tiles (the split writes B transposed)
+  // F32 accumulate, TF32 A/B (format 2), both K-major
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+  static constexpr CUtensorMapDataType DT = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+};
+
+template <class K>
+struct Layout {
+  static constexpr int BOX_N = 128 / K::ELEM;                 // elements per 128 B row
+  static constexpr int A_BYTES = BM * K::BK * K::ELEM;        // one operand tile
+  static constexpr int B_BYTES = K::BN * K::BK * K::ELEM;
+  static constexpr int STAGE_BYTES = K::NOPS * (A_BYTES + B_BYTES);
+  static constexpr int SMEM_EPI = K::STAGES * STAGE_BYTES;
+  static constexpr int SMEM_BAR = SMEM_EPI + 4 * 2 * EPI_BUF;
+  static constexpr int SMEM_ALLOC = SMEM_BAR + 256 + 1024;    // + runtime 1024-B alignment slack
+  static constexpr uint32_t TMEM_COLS = 2 * K::BN;            // double-buffered accumulator
+  static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
+  __device__ static int a_off(int stage, int op) { return stage * STAGE_BYTES + op * A_BYTES; }
+  __device__ static int b_off(int stage, int op) { return stage * STAGE_BYTES + K::NOPS * A_BYTES + op * B_BYTES; }
+};
 
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
   // K-major, 128B swizzle: rows of 128 B, 8-row groups 1024 B apart (SBO),
@@ -63,12 +92,12 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
 }
 
 // MN-major (N contiguous), 128B swizzle, canonical ((8,n),(8,k)):((1,LBO),(8,SBO))
-// in 16 B units: 64 N-elements per 128 B row, rows = k; 8-row (1024 B) atoms
-// step along k by SBO; 64-wide N chunks (one TMA box of BK rows each) step by LBO.
-__device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t saddr) {
+// in 16 B units: 128 B of N per row, rows = k; 8-row (1024 B) atoms step along
+// k by SBO; 128-byte-wide N chunks (one TMA box of BK rows each) step by LBO.
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(uint32_t saddr, int bk) {
   uint64_t d = 0;
   d |= uint64_t((saddr >> 4) & 0x3FFF);
-  d |= uint64_t((BK * 128) >> 4) << 16;  // LBO: next 64-wide N chunk
+  d |= uint64_t((bk * 128) >> 4) << 16;  // LBO: next 128-byte-wide N chunk (one TMA box)
   d |= uint64_t(1024 >> 4) << 32;        // SBO: next 8 k-rows
   d |= uint64_t(1) << 46;
   d |= uint64_t(2) << 61;
@@ -123,12 +152,20 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
-      : "memory");
+template <class K>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  if constexpr (K::ELEM == 2)
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(K::IDESC), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(K::IDESC), "r"(accumulate)
+        : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
@@ -146,12 +183,17 @@ struct TcArgs {
   int32_t kblocks;
 };
 
-__global__ void __launch_bounds__(THREADS, 1)
-    bf16_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ CUtensorMap map_c, const TcArgs args) {
+struct TcMaps {
+  CUtensorMap a[2], b[2], c;  // operand maps (hi/lo for 3xTF32) and the output map
+};
+
+template <class K>
+__global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
+  using L = Layout<K>;
+  constexpr int STAGES = K::STAGES, BN = K::BN, BK = K::BK;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::SMEM_BAR);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -173,13 +215,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&tempty[a], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_c)) : "memory");
+    for (int o = 0; o < K::NOPS; ++o) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.a[o])) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.b[o])) : "memory");
+    }
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.c)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
+                 "r"(L::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
   }
   tc_fence_before();
@@ -199,14 +243,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-          mbar_expect_tx(&full[s], keep_b ? A_BYTES : A_BYTES + B_BYTES);
-          tma_load_2d(smem + SMEM_A + s * A_BYTES, &map_a, &full[s], args.a_col0 + kb * BK, rb * BM);
-          if (!keep_b) {
-            // B is k x m row-major (N contiguous): 4 boxes of [64 k rows][64 n]
+          mbar_expect_tx(&full[s], K::NOPS * (keep_b ? L::A_BYTES : L::A_BYTES + L::B_BYTES));
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(smem + SMEM_B + s * B_BYTES + j * (BK * 128), &map_b, &full[s],
-                          args.b_col0 + nb * BN + 64 * j, kb * BK);
+          for (int o = 0; o < K::NOPS; ++o) {
+            tma_load_2d(smem + L::a_off(s, o), &maps.a[o], &full[s], args.a_col0 + kb * BK, rb * BM);
+            if (!keep_b) {
+              if constexpr (K::B_KMAJOR) {
+                // B^T (m x k, K contiguous): one box of [BN rows][BK k]
+                tma_load_2d(smem + L::b_off(s, o), &maps.b[o], &full[s], args.b_col0 + kb * BK, nb * BN);
+              } else {
+                // B is k x m row-major (N contiguous): boxes of [BK k rows][128 B of n]
+#pragma unroll
+                for (int j = 0; j < BN / L::BOX_N; ++j)
+                  tma_load_2d(smem + L::b_off(s, o) + j * (BK * 128), &maps.b[o], &full[s],
+                              args.b_col0 + nb * BN + L::BOX_N * j, kb * BK);
+              }
+            }
           }
         }
         resident_nb = can_keep_b ? nb : -1;
@@ -227,13 +279,25 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
           tc_fence_after();
-          const uint64_t ad = smem_desc_sw128(smem_u32(smem + SMEM_A + s * A_BYTES));
-          const uint64_t bd = smem_desc_mn_sw128(smem_u32(smem + SMEM_B + s * B_BYTES));
+          uint64_t ad[K::NOPS], bd[K::NOPS];
 #pragma unroll
-          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-            // A (K-major): +32 B inside the 128 B swizzle row = +2 units;
-            // B (MN-major): +16 k rows = 2 atoms of 1024 B = +128 units
-            umma_bf16(d_tmem, ad + uint64_t(2 * kk), bd + uint64_t(128 * kk), (kb | kk) != 0);
+          for (int o = 0; o < K::NOPS; ++o) {
+            ad[o] = smem_desc_sw128(smem_u32(smem + L::a_off(s, o)));
+            bd[o] = K::B_KMAJOR ? smem_desc_sw128(smem_u32(smem + L::b_off(s, o)))
+                                : smem_desc_mn_sw128(smem_u32(smem + L::b_off(s, o)), BK);
+          }
+#pragma unroll
+          for (int kk = 0; kk < BK / K::UMMA_K; ++kk) {
+            // A (K-major): +UMMA_K*ELEM = 32 B inside the 128 B swizzle row = +2 units;
+            // B (MN-major): +UMMA_K k rows of 128 B = +8*UMMA_K units
+            const uint64_t a_adv = uint64_t(2 * kk);
+            const uint64_t b_adv = K::B_KMAJOR ? uint64_t(2 * kk) : uint64_t(8 * K::UMMA_K * kk);
+#pragma unroll
+            for (int ps = 0; ps < K::PASSES; ++ps) {
+              // passes: hi*hi, hi*lo, lo*hi (3xTF32); a single pass for bf16
+              const int ao = ps == 2 ? 1 : 0, bo = ps == 1 ? 1 : 0;
+              umma<K>(d_tmem, ad[ao] + a_adv, bd[bo] + b_adv, (kb | kk | ps) != 0);
+            }
           }
           umma_commit(&empty[s]);  // stage is free once these MMAs complete
         }
@@ -243,7 +307,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {
     // ---------------- epilogue warps ----------------
     const int q = warp % 4;  // TMEM lane quadrant this warp may access
-    unsigned char* stage0 = smem + SMEM_EPI + q * 2 * EPI_BUF;
+    unsigned char* stage0 = smem + L::SMEM_EPI + q * 2 * EPI_BUF;
     int tile = 0;
     uint32_t nstore = 0;
     for (int64_t t = t_begin; t < t_end; ++t, ++tile) {
@@ -287,9 +351,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
           if (row0 < args.n) {
             if (args.overwrite)
-              tma_store_2d(&map_c, buf, args.c_col0 + col0, row0);
+              tma_store_2d(&maps.c, buf, args.c_col0 + col0, row0);
             else
-              tma_reduce_add_2d(&map_c, buf, args.c_col0 + col0, row0);
+              tma_reduce_add_2d(&maps.c, buf, args.c_col0 + col0, row0);
           }
           asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         }
@@ -303,7 +367,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(L::TMEM_COLS));
 }
 
 }  // namespace tc
@@ -360,7 +424,7 @@ struct Scratch {
   size_t bytes = 0;
 };
 std::mutex g_scratch_mu;
-Scratch g_scratch[64][3];
+Scratch g_scratch[64][8];
 
 int scratch(int device, int slot, size_t bytes, cudaStream_t st, void** out) {
   std::lock_guard<std::mutex> lock(g_scratch_mu);
@@ -383,36 +447,120 @@ bool pitch_ok(const void* p, int64_t ld, int elsize) {
 }
 }  // namespace
 
-int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B, int64_t ldb,
-                      void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces,
-                      int n_pieces, int flags) {
+namespace tc {
+// x -> (hi, lo) with hi = x & ~0x1FFF (a tf32 value), lo = x - hi (exact).
+// Packed outputs with a 16-byte row pitch `ldo`; kT writes them transposed
+// (cols x rows) through a 32x32 smem tile so both sides stay coalesced.
+template <bool kT>
+__global__ void split_tf32_kernel(const float* __restrict__ x, int64_t ldx, float* __restrict__ hi,
+                                  float* __restrict__ lo, int64_t ldo, int64_t rows, int64_t cols) {
+  __shared__ float th[32][33], tl[32][33];
+  const int64_t r0 = int64_t(blockIdx.y) * 32, c0 = int64_t(blockIdx.x) * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t i = r0 + dy, j = c0 + threadIdx.x;
+    float v = (i < rows && j < cols) ? x[i * ldx + j] : 0.f;
+    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    if (!kT) {
+      if (i < rows && j < cols) {
+        hi[i * ldo + j] = h;
+        lo[i * ldo + j] = v - h;
+      }
+    } else {
+      th[dy][threadIdx.x] = h;
+      tl[dy][threadIdx.x] = v - h;
+    }
+  }
+  if (kT) {
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+      const int64_t j = c0 + dy, i = r0 + threadIdx.x;  // output row j (a column of x)
+      if (j < cols && i < rows) {
+        hi[j * ldo + i] = th[threadIdx.x][dy];
+        lo[j * ldo + i] = tl[threadIdx.x][dy];
+      }
+    }
+  }
+}
+}  // namespace tc
+
+namespace {
+// Repack an operand whose row pitch TMA cannot take into padded scratch.
+int repack(int device, int slot, const void** p, int64_t* ld, int64_t rows, int64_t cols, int elsize,
+           cudaStream_t st) {
+  if (pitch_ok(*p, *ld, elsize)) return PACO_OK;
+  const int64_t q = 16 / elsize, ld2 = (cols + q - 1) / q * q;
+  void* dst;
+  int rc = scratch(device, slot, size_t(rows) * ld2 * elsize, st, &dst);
+  if (rc) return rc;
+  PACO_CUDA_TRY(cudaMemcpy2DAsync(dst, ld2 * elsize, *p, *ld * elsize, cols * elsize, rows,
+                                  cudaMemcpyDeviceToDevice, st));
+  *p = dst;
+  *ld = ld2;
+  return PACO_OK;
+}
+
+// fp32 operand -> packed hi/lo tf32 pair in scratch slots (slot, slot+1);
+// `transpose` stores them as (cols x rows), i.e. K-major for a B operand.
+int split_operand(int device, int slot, const void* x, int64_t ldx, int64_t rows, int64_t cols,
+                  bool transpose, cudaStream_t st, const void** hi, const void** lo, int64_t* ld) {
+  const int64_t orows = transpose ? cols : rows, ocols = transpose ? rows : cols;
+  const int64_t ld2 = (ocols + 3) / 4 * 4;
+  void *h, *l;
+  int rc = scratch(device, slot, size_t(orows) * ld2 * 4, st, &h);
+  if (rc) return rc;
+  if ((rc = scratch(device, slot + 1, size_t(orows) * ld2 * 4, st, &l))) return rc;
+  dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32)), block(32, 8);
+  if (transpose)
+    tc::split_tf32_kernel<true><<<grid, block, 0, st>>>(static_cast<const float*>(x), ldx, static_cast<float*>(h),
+                                                        static_cast<float*>(l), ld2, rows, cols);
+  else
+    tc::split_tf32_kernel<false><<<grid, block, 0, st>>>(static_cast<const float*>(x), ldx, static_cast<float*>(h),
+                                                         static_cast<float*>(l), ld2, rows, cols);
+  PACO_CUDA_TRY(cudaGetLastError());
+  *hi = h;
+  *lo = l;
+  *ld = ld2;
+  return PACO_OK;
+}
+}  // namespace
+
+template <class K>
+int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B, int64_t ldb,
+              void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces, int n_pieces,
+              int flags) {
+  using L = tc::Layout<K>;
   if (pieces && n_pieces > 0) {
-    set_error("the tcgen05 bf16 kernel takes its own CTA plan (pass pieces=NULL)");
+    set_error("the tcgen05 kernels take their own CTA plan (pass pieces=NULL)");
     return PACO_ERR_UNSUPPORTED;
   }
   if (n > INT32_MAX || m > INT32_MAX || k > INT32_MAX) {
-    set_error("tcgen05 bf16 path: extents must fit int32");
+    set_error("tcgen05 path: extents must fit int32");
     return PACO_ERR_ARG;
   }
-  CUtensorMap ma, mb, mc;
   int rc;
-  int32_t a_off = 0, b_off = 0, c_off = 0;
-  // operands with a row pitch TMA cannot take are repacked into padded scratch
-  if (!pitch_ok(A, lda, 2)) {
-    const int64_t ld2 = (k + 7) / 8 * 8;
-    void* p;
-    if ((rc = scratch(device, 0, size_t(n) * ld2 * 2, stream, &p))) return rc;
-    PACO_CUDA_TRY(cudaMemcpy2DAsync(p, ld2 * 2, A, lda * 2, k * 2, n, cudaMemcpyDeviceToDevice, stream));
-    A = p;
-    lda = ld2;
-  }
-  if (!pitch_ok(B, ldb, 2)) {
-    const int64_t ld2 = (m + 7) / 8 * 8;
-    void* p;
-    if ((rc = scratch(device, 1, size_t(k) * ld2 * 2, stream, &p))) return rc;
-    PACO_CUDA_TRY(cudaMemcpy2DAsync(p, ld2 * 2, B, ldb * 2, m * 2, k, cudaMemcpyDeviceToDevice, stream));
-    B = p;
-    ldb = ld2;
+  tc::TcMaps maps;
+  int32_t a_off = 0, b_off = 0, c_off = 0, t_off = 0;
+  if constexpr (K::NOPS == 1) {
+    // bf16: operands with a row pitch TMA cannot take are repacked first
+    if ((rc = repack(device, 0, &A, &lda, n, k, K::ELEM, stream))) return rc;
+    if ((rc = repack(device, 1, &B, &ldb, k, m, K::ELEM, stream))) return rc;
+    if ((rc = make_map(&maps.a[0], K::DT, K::ELEM, A, n, k, lda, K::BK, tc::BM, &a_off))) return rc;
+    if ((rc = make_map(&maps.b[0], K::DT, K::ELEM, B, k, m, ldb, L::BOX_N, K::BK, &b_off))) return rc;
+  } else {
+    // 3xTF32: split both operands into packed hi/lo pairs (scratch slots 3..6)
+    const void *ah, *al, *bh, *bl;
+    int64_t lda2, ldb2;
+    if ((rc = split_operand(device, 3, A, lda, n, k, false, stream, &ah, &al, &lda2))) return rc;
+    if ((rc = split_operand(device, 5, B, ldb, k, m, K::B_KMAJOR, stream, &bh, &bl, &ldb2))) return rc;
+    if ((rc = make_map(&maps.a[0], K::DT, K::ELEM, ah, n, k, lda2, K::BK, tc::BM, &a_off))) return rc;
+    if ((rc = make_map(&maps.a[1], K::DT, K::ELEM, al, n, k, lda2, K::BK, tc::BM, &t_off))) return rc;
+    if constexpr (K::B_KMAJOR) {
+      if ((rc = make_map(&maps.b[0], K::DT, K::ELEM, bh, m, k, ldb2, K::BK, K::BN, &b_off))) return rc;
+      if ((rc = make_map(&maps.b[1], K::DT, K::ELEM, bl, m, k, ldb2, K::BK, K::BN, &t_off))) return rc;
+    } else {
+      if ((rc = make_map(&maps.b[0], K::DT, K::ELEM, bh, k, m, ldb2, L::BOX_N, K::BK, &b_off))) return rc;
+      if ((rc = make_map(&maps.b[1], K::DT, K::ELEM, bl, k, m, ldb2, L::BOX_N, K::BK, &t_off))) return rc;
+    }
   }
   void* c_user = nullptr;
   int64_t ldc_user = ldc;
@@ -426,9 +574,7 @@ int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t ld
     C = p;
     ldc = ld2;
   }
-  if ((rc = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, A, n, k, lda, tc::BK, tc::BM, &a_off))) return rc;
-  if ((rc = make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, k, m, ldb, 64, tc::BK, &b_off))) return rc;
-  if ((rc = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, n, m, ldc, 32, 32, &c_off))) return rc;
+  if ((rc = make_map(&maps.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, n, m, ldc, 32, 32, &c_off))) return rc;
   tc::TcArgs args;
   args.n = n;
   args.m = m;
@@ -438,22 +584,35 @@ int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t ld
   args.c_col0 = c_off;
   args.overwrite = (flags & PACO_MM_OVERWRITE) ? 1 : 0;
   args.tiles_rb = int32_t((n + tc::BM - 1) / tc::BM);
-  args.tiles_nb = int32_t((m + tc::BN - 1) / tc::BN);
-  args.kblocks = int32_t((k + tc::BK - 1) / tc::BK);
+  args.tiles_nb = int32_t((m + K::BN - 1) / K::BN);
+  args.kblocks = int32_t((k + K::BK - 1) / K::BK);
   const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb;
   const int grid = int(tiles < kNumSMs ? tiles : kNumSMs);
-  PACO_CUDA_TRY(cudaFuncSetAttribute(tc::bf16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC));
-  tc::bf16_tc_kernel<<<grid, tc::THREADS, tc::SMEM_ALLOC, stream>>>(ma, mb, mc, args);
+  auto kern = tc::tc_gemm_kernel<K>;
+  PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
+  kern<<<grid, tc::THREADS, L::SMEM_ALLOC, stream>>>(maps, args);
   PACO_CUDA_TRY(cudaGetLastError());
   if (c_user)
     PACO_CUDA_TRY(cudaMemcpy2DAsync(c_user, ldc_user * 4, C, ldc * 4, m * 4, n, cudaMemcpyDeviceToDevice, stream));
   return PACO_OK;
 }
 
-int bf16_tile_shape(int* bm, int* bn, int* bk, int* cps) {
+int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B, int64_t ldb,
+                      void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces,
+                      int n_pieces, int flags) {
+  return launch_tc<tc::KindBF16>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
+}
+
+int launch_mm_f32_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B, int64_t ldb,
+                     void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces,
+                     int n_pieces, int flags) {
+  return launch_tc<tc::KindTF32x3>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
+}
+
+int tc_tile_shape(int semiring, int* bm, int* bn, int* bk, int* cps) {
   *bm = tc::BM;
-  *bn = tc::BN;
-  *bk = tc::BK;
+  *bn = semiring == PACO_SR_BF16_F32 ? tc::KindBF16::BN : tc::KindTF32x3::BN;
+  *bk = semiring == PACO_SR_BF16_F32 ? tc::KindBF16::BK : tc::KindTF32x3::BK;
   *cps = 1;
   return PACO_OK;
 }

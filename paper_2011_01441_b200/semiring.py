@@ -20,7 +20,9 @@ B200-native additions for the BASELINE configs:
 * ``SEMIRING_MAXPLUS``   (max,+) on int32 lanes, domain [-2^30, 2^30),
   -INF = -2^30, saturating (cfg4).  Equals ``-minplus(-A, -B)`` of the
   reference on that domain.
-* ``SEMIRING_F32``       float32 (+,x) with FFMA (Strassen leaves, cfg5).
+* ``SEMIRING_F32``       float32 (+,x) on the tensor cores as 3xTF32 (hi/lo split,
+  ~fp32 accuracy; Strassen leaves, cfg5).  ``SEMIRING_F32_SIMT`` is the FFMA
+  (CUDA-core) kernel of the same semiring.
 * ``SEMIRING_BF16``      bf16 inputs, float32 accumulate and C, tcgen05 (cfg3).
 """
 
@@ -71,10 +73,11 @@ SEMIRING_MINPLUS = Semiring("minplus", np.int64, MINPLUS_INF, nat.SR_MINPLUS_I64
 
 SEMIRING_MINPLUS_SAT = Semiring("minplus_sat", np.int32, np.int32(TROPICAL_INF), nat.SR_MINPLUS_SAT32)
 SEMIRING_MAXPLUS = Semiring("maxplus", np.int32, np.int32(-TROPICAL_INF), nat.SR_MAXPLUS_SAT32)
-SEMIRING_F32 = Semiring("f32", np.float32, np.float32(0.0), nat.SR_F32)
+SEMIRING_F32 = Semiring("f32", np.float32, np.float32(0.0), nat.SR_F32_TC)
+SEMIRING_F32_SIMT = Semiring("f32_simt", np.float32, np.float32(0.0), nat.SR_F32)
 SEMIRING_BF16 = Semiring("bf16", np.float32, np.float32(0.0), nat.SR_BF16_F32, in_dtype="bfloat16")
 
 # reference registry (matmul.py:57) plus the B200 additions
 SEMIRINGS = {s.name: s for s in (SEMIRING_INT, SEMIRING_F64, SEMIRING_MINPLUS)}
 ALL_SEMIRINGS = dict(SEMIRINGS, **{s.name: s for s in (
-    SEMIRING_MINPLUS_SAT, SEMIRING_MAXPLUS, SEMIRING_F32, SEMIRING_BF16)})
+    SEMIRING_MINPLUS_SAT, SEMIRING_MAXPLUS, SEMIRING_F32, SEMIRING_F32_SIMT, SEMIRING_BF16)})

@@ -17,7 +17,7 @@ Follows SPEC.md:474-552 and the identities of PAPER.md:1839-1852:
 * ``strassen_execute(plan, A, B)`` -- runs a plan on the GPU(s): workers map
   to (device, stream); returns C.
 
-Ring: float32 (FFMA leaves), float64 (DFMA leaves) or int64 (exact).
+Ring: float32 (3xTF32 tcgen05 leaves), float64 (DFMA leaves) or int64 (exact).
 """
 
 from __future__ import annotations
@@ -48,7 +48,7 @@ C_TERMS = {"00": ((1, 1), (1, 4), (-1, 5), (1, 7)), "01": ((1, 3), (1, 5)),
            "10": ((1, 2), (1, 4)), "11": ((1, 1), (1, 3), (-1, 2), (1, 6))}
 
 _RING = {  # torch dtype -> (leaf kernel id, lincomb dtype id)
-    torch.float32: (nat.SR_F32, nat.DT_F32),
+    torch.float32: (nat.SR_F32_TC, nat.DT_F32),   # 3xTF32 tensor-core leaves
     torch.float64: (nat.SR_F64, nat.DT_F64),
     torch.int64: (nat.SR_INT_I64, nat.DT_I64),
 }

@@ -28,7 +28,7 @@ def test_all_header_symbols_exported_and_bound():
 
 
 def test_tile_shapes():
-    for sr in range(8):
+    for sr in range(nat.SR_COUNT):
         bm, bn, bk, cps = nat.tile_shape(sr)
         assert bm > 0 and bn > 0 and bk > 0 and cps >= 1
 

@@ -154,16 +154,19 @@ def test_int32_to_int64_vs_oracle(shape):
     assert np.array_equal(C, want)
 
 
-@pytest.mark.parametrize("shape", SHAPES[:8])
-def test_f32_vs_oracle(shape):
+@pytest.mark.parametrize("shape", SHAPES[:8] + [(1000, 513, 777)])
+@pytest.mark.parametrize("sr", ["tc", "simt"])
+def test_f32_vs_oracle(shape, sr):
+    """float32 (+,x): 3xTF32 tensor cores and FFMA, relative Frobenius <= 1e-5 vs f64."""
     n, m, k = shape
     rng = np.random.default_rng(n * 3 + k)
     A = rng.uniform(-1, 1, (n, k)).astype(np.float32)
     B = rng.uniform(-1, 1, (k, m)).astype(np.float32)
-    C = np.zeros((n, m), np.float32)
-    M.mm_seq(A, B, C, M.SEMIRING_F32)
-    ref = A.astype(np.float64) @ B.astype(np.float64)
-    assert np.linalg.norm(C - ref) <= 1e-5 * max(np.linalg.norm(ref), 1e-30) + 1e-6
+    C0 = rng.uniform(-1, 1, (n, m)).astype(np.float32)
+    C = C0.copy()
+    M.mm_seq(A, B, C, M.SEMIRING_F32 if sr == "tc" else M.SEMIRING_F32_SIMT)
+    ref = A.astype(np.float64) @ B.astype(np.float64) + C0
+    assert np.linalg.norm(C - ref) <= 1e-5 * np.linalg.norm(ref)
 
 
 def test_unaligned_views_and_ldc():
