@@ -107,6 +107,11 @@ int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out,
                  int64_t m, int nin, const void* const* ins, const int64_t* lds,
                  const int32_t* coefs, int accumulate);
 
+/* Asynchronous 2-D copy (host<->device or device<->device; pitches and width in
+ * BYTES): the staging primitive of the overlapped host pipeline. */
+int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                int64_t width, int64_t rows);
+
 /* Enable peer access from `device` to `peer` (idempotent). */
 int paco_enable_peer(int device, int peer);
 

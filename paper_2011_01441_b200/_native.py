@@ -53,6 +53,7 @@ SIGNATURES = {
     "paco_lincomb": (_int, [_int, _vp, _int, _vp, _i64, _i64, _i64, _int,
                             ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                             ctypes.POINTER(ctypes.c_int32), _int]),
+    "paco_copy2d": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_enable_peer": (_int, [_int, _int]),
     "paco_alu_probe": (_int, [_int, _vp, _int, _int, ctypes.POINTER(ctypes.c_double),
                               ctypes.POINTER(ctypes.c_double)]),

@@ -156,6 +156,19 @@ int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out,
                         coefs, accumulate);
 }
 
+int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                int64_t width, int64_t rows) {
+  if (rows <= 0 || width <= 0) return PACO_OK;
+  if (!dst || !src || dpitch < width || spitch < width) {
+    set_error("paco_copy2d: bad pointers or pitches");
+    return PACO_ERR_ARG;
+  }
+  PACO_TRY(use_device(device));
+  PACO_CUDA_TRY(cudaMemcpy2DAsync(dst, size_t(dpitch), src, size_t(spitch), size_t(width), size_t(rows),
+                                  cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return PACO_OK;
+}
+
 int paco_enable_peer(int device, int peer) {
   if (device == peer) return PACO_OK;
   int can = 0;

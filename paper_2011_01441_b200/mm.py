@@ -16,8 +16,7 @@ as the reference mutates C) or CUDA tensors (used in place).
 
 from __future__ import annotations
 
-import ctypes
-from functools import lru_cache
+import os
 
 import numpy as np
 import torch
@@ -107,6 +106,7 @@ def mm_seq(A, B, C, semiring: Semiring = SEMIRING_INT, base: int = DEFAULT_BASE,
 
 
 _PIPE_MIN_ROWS = 512
+_PIPE_GRID = tuple(int(x) for x in os.environ.get("PACO_PIPE_GRID", "4,2").split(","))  # measured best of 4x4/8x1/4x2/2x4/8x2 for 8192^3
 
 
 def _pinned_host(x, dtype) -> bool:
@@ -114,19 +114,34 @@ def _pinned_host(x, dtype) -> bool:
             and x.dtype == torch_dtype(dtype))
 
 
-def _pipelined_host_mm(A, B, C, kid: int, semiring: Semiring, dev: int, st, overwrite: bool) -> None:
-    """Host (pinned) operands: overlap H2D, compute and D2H by row blocks.
+def _copy2d(stream, dst: torch.Tensor, dr0: int, dc0: int, src: torch.Tensor, sr0: int, sc0: int,
+            rows: int, cols: int) -> None:
+    """Async 2-D block copy between row-major tensors (host pinned <-> device)."""
+    es = dst.element_size()
+    nat.check(nat.load().paco_copy2d(
+        dst.device.index if dst.is_cuda else src.device.index, stream.cuda_stream,
+        dst.data_ptr() + (dr0 * dst.stride(0) + dc0) * es, dst.stride(0) * es,
+        src.data_ptr() + (sr0 * src.stride(0) + sc0) * es, src.stride(0) * es, cols * es, rows))
 
-    B goes up first (every row block needs all of it); then row block i of
-    A (and of C unless overwriting) is copied on an H2D stream, multiplied on
-    ``st`` as soon as it lands, and its C rows stream back on a D2H stream
-    while block i+1 computes.  The reference mutates C synchronously, so this
-    returns only after the last D2H completes.
+
+def _pipelined_host_mm(A, B, C, kid: int, semiring: Semiring, dev: int, st, overwrite: bool) -> None:
+    """Host (pinned) operands: overlap H2D, compute and D2H over a 2-D block grid.
+
+    C is cut into R row blocks x J column blocks.  The H2D stream uploads B's
+    column block j (needed by every row block), the row blocks of A on the
+    first pass, and C's block (unless overwriting); the compute stream runs
+    block (i, j) as soon as its inputs landed; the D2H stream returns C(i, j)
+    while later blocks compute.  So only the first block's inputs and the last
+    block's output are exposed.  The reference mutates C synchronously, so this
+    returns after the last D2H.
     """
     n, k = tuple(A.shape)
     m = B.shape[1]
-    nblk = max(2, min(8, n // _PIPE_MIN_ROWS))
-    edges = [((n * i // nblk) // 128) * 128 for i in range(nblk)] + [n]
+    R, J = _PIPE_GRID
+    R = max(1, min(R, n // _PIPE_MIN_ROWS))
+    J = max(1, min(J, m // _PIPE_MIN_ROWS))
+    redges = [((n * i // R) // 128) * 128 for i in range(R)] + [n]
+    cedges = [((m * j // J) // 128) * 128 for j in range(J)] + [m]
     h2d = torch.cuda.Stream(device=dev)
     d2h = torch.cuda.Stream(device=dev)
     h2d.wait_stream(st)
@@ -137,26 +152,30 @@ def _pipelined_host_mm(A, B, C, kid: int, semiring: Semiring, dev: int, st, over
         t.record_stream(h2d)
         t.record_stream(d2h)
     av, bv, cv = View.of(a_d), View.of(b_d), View.of(c_d)
-    landed = []
-    with torch.cuda.stream(h2d):
-        b_d.copy_(B, non_blocking=True)
-        for r0, r1 in zip(edges[:-1], edges[1:]):
-            a_d[r0:r1].copy_(A[r0:r1], non_blocking=True)
-            if not overwrite:
-                c_d[r0:r1].copy_(C[r0:r1], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(h2d)
-            landed.append(ev)
-    for (r0, r1), ev in zip(zip(edges[:-1], edges[1:]), landed):
-        if r1 <= r0:
+    blocks = [(i, j) for j in range(J) for i in range(R)]
+    landed = {}
+    for (i, j) in blocks:
+        r0, r1, c0, c1 = redges[i], redges[i + 1], cedges[j], cedges[j + 1]
+        if i == 0:
+            _copy2d(h2d, b_d, 0, c0, B, 0, c0, k, c1 - c0)
+        if j == 0:
+            _copy2d(h2d, a_d, r0, 0, A, r0, 0, r1 - r0, k)
+        if not overwrite:
+            _copy2d(h2d, c_d, r0, c0, C, r0, c0, r1 - r0, c1 - c0)
+        ev = torch.cuda.Event()
+        ev.record(h2d)
+        landed[(i, j)] = ev
+    for (i, j) in blocks:
+        r0, r1, c0, c1 = redges[i], redges[i + 1], cedges[j], cedges[j + 1]
+        if r1 <= r0 or c1 <= c0:
             continue
-        st.wait_event(ev)
-        launch_mm(kid, st, av.sub(r0, 0, r1 - r0, k), bv, cv.sub(r0, 0, r1 - r0, m), overwrite=overwrite)
+        st.wait_event(landed[(i, j)])
+        launch_mm(kid, st, av.sub(r0, 0, r1 - r0, k), bv.sub(0, c0, k, c1 - c0),
+                  cv.sub(r0, c0, r1 - r0, c1 - c0), overwrite=overwrite)
         done = torch.cuda.Event()
         done.record(st)
         d2h.wait_event(done)
-        with torch.cuda.stream(d2h):
-            C[r0:r1].copy_(c_d[r0:r1], non_blocking=True)
+        _copy2d(d2h, C, r0, c0, c_d, r0, c0, r1 - r0, c1 - c0)
     st.wait_stream(d2h)
     d2h.synchronize()
 
