@@ -181,6 +181,7 @@ struct TcArgs {
   int32_t tiles_rb;  // row blocks
   int32_t tiles_nb;  // column blocks
   int32_t kblocks;
+  int32_t ablate;    // diagnostics: 1 = no C stores, 2 = no MMAs, 4 = no smem staging
 };
 
 struct TcMaps {
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
             for (int ps = 0; ps < K::PASSES; ++ps) {
               // passes: hi*hi, hi*lo, lo*hi (3xTF32); a single pass for bf16
               const int ao = ps == 2 ? 1 : 0, bo = ps == 1 ? 1 : 0;
-              umma<K>(d_tmem, ad[ao] + a_adv, bd[bo] + b_adv, (kb | kk | ps) != 0);
+              if (!(args.ablate & 2)) umma<K>(d_tmem, ad[ao] + a_adv, bd[bo] + b_adv, (kb | kk | ps) != 0);
             }
           }
           umma_commit(&empty[s]);  // stage is free once these MMAs complete
@@ -341,15 +342,17 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
         __syncwarp();
         // 128B-swizzled [32 rows][32 fp32] staging: 16 B chunk j of row r at (j ^ r%8)
+        if (!(args.ablate & 4)) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint4 w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) * 16)) = w;
+          for (int j = 0; j < 8; ++j) {
+            uint4 w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) * 16)) = w;
+          }
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         }
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          if (row0 < args.n) {
+          if (row0 < args.n && !(args.ablate & 1)) {
             if (args.overwrite)
               tma_store_2d(&maps.c, buf, args.c_col0 + col0, row0);
             else
@@ -586,6 +589,10 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
   args.tiles_rb = int32_t((n + tc::BM - 1) / tc::BM);
   args.tiles_nb = int32_t((m + K::BN - 1) / K::BN);
   args.kblocks = int32_t((k + K::BK - 1) / K::BK);
+  {
+    static const int ablate = getenv("PACO_TC_ABLATE") ? atoi(getenv("PACO_TC_ABLATE")) : 0;
+    args.ablate = ablate;
+  }
   const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb;
   const int grid = int(tiles < kNumSMs ? tiles : kNumSMs);
   auto kern = tc::tc_gemm_kernel<K>;
