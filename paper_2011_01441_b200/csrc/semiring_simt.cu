@@ -35,19 +35,24 @@ constexpr int kDefaultWaves = 4;
 // non-null every CTA of the next launches records smid and start/end times.
 long long* g_trace_buffer = nullptr;
 
+#ifndef PACO_SIMT_NSPAN
+#define PACO_SIMT_NSPAN 1  // 32-bit ops: C tile width in units of 128 columns (2 = 128x256 tiles,
+                           // 1 CTA/SM: measured 34.7 vs 34.4 ms on 8192^3 min-plus -- kept at 1)
+#endif
+
 template <class Op>
 struct SimtCfg {
   static constexpr bool kWide = sizeof(typename Op::Acc) == 8;
   static constexpr int BM = kWide ? 64 : 128;
-  static constexpr int BN = kWide ? 64 : 128;
+  static constexpr int BN = kWide ? 64 : 128 * PACO_SIMT_NSPAN;
   static constexpr int BK = kWide ? 16 : 32;
   static constexpr int GM = BM / 64;  // 4-row groups per thread along m
   static constexpr int GN = BN / 64;
   static constexpr int TM = 4 * GM;
   static constexpr int TN = 4 * GN;
   static constexpr int THREADS = 256;
-  static constexpr int STAGES = kWide ? 4 : 3;
-  static constexpr int MIN_BLOCKS = 2;
+  static constexpr int STAGES = kWide ? 4 : (PACO_SIMT_NSPAN > 1 ? 4 : 3);
+  static constexpr int MIN_BLOCKS = (!kWide && PACO_SIMT_NSPAN > 1) ? 1 : 2;
   static constexpr int VA = 16 / sizeof(typename Op::TA);  // elements per 16 B chunk
   static constexpr int VB = 16 / sizeof(typename Op::TB);
   static constexpr int KQ = VA;          // k quantum of piece boundaries
@@ -290,36 +295,46 @@ __device__ __forceinline__ void epilogue_bulk(const MMArgs& a,
                                               uint32_t bytes) {
   using C = SimtCfg<Op>;
   using TC = typename Op::TC;
-  static_assert(C::BM == 128 && C::BN == 128 && sizeof(TC) == 4, "bulk epilogue layout");
+  static_assert(C::BM == 128 && sizeof(TC) == 4, "bulk epilogue layout");
+  // rows per round: the B stage buffer holds BK = 32 rows of the C tile; the
+  // padded A buffer adds 32 more when the tile is 128 wide
+  constexpr int RPR = (C::A_STAGE >= 32 * C::BN) ? 64 : 32;
+  constexpr int ROUNDS = C::BM / RPR;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   TC* Cp = static_cast<TC*>(a.C);
+  auto row_buf = [&](int lr) -> TC* {
+    return lr < 32 ? static_cast<TC*>(bufB) + lr * C::BN : static_cast<TC*>(bufA) + (lr - 32) * C::BN;
+  };
   __syncthreads();  // every warp is done reading the stage buffer
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < ROUNDS; ++h) {
+    const int g = (h * RPR) / 64;                    // the thread's 64-row group in this round
+    const int lr0 = 64 * g + ty * 4 - RPR * h;      // first local row of this thread
+    if (lr0 >= 0 && lr0 < RPR) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int lr = ty * 4 + r;  // 0..63 within the round
-      TC* dst = lr < 32 ? static_cast<TC*>(bufA) + lr * C::BN : static_cast<TC*>(bufB) + (lr - 32) * C::BN;
+      for (int r = 0; r < 4; ++r) {
+        TC* dst = row_buf(lr0 + r);
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        TC v[4];
+        for (int gn = 0; gn < C::GN; ++gn) {
+          TC v[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) v[e] = Op::finish(acc[4 * h + r][4 * g + e]);
-        uint4 bits;
-        memcpy(&bits, v, 16);  // bit copy (TC may be float)
-        *reinterpret_cast<uint4*>(dst + g * 64 + tx * 4) = bits;
+          for (int e = 0; e < 4; ++e) v[e] = Op::finish(acc[4 * g + r][4 * gn + e]);
+          uint4 bits;
+          memcpy(&bits, v, 16);  // bit copy (TC may be float)
+          *reinterpret_cast<uint4*>(dst + gn * 64 + tx * 4) = bits;
+        }
       }
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
     if (lane == 0) {
 #pragma unroll 1
-      for (int q = 0; q < 8; ++q) {
-        const int lr = warp * 8 + q;
-        const int64_t gr = row0 + 64 * h + lr;
+      for (int q = 0; q < RPR / 8; ++q) {
+        const int lr = warp * (RPR / 8) + q;
+        const int64_t gr = row0 + RPR * h + lr;
         if (gr < a.n) {
-          const void* src = lr < 32 ? static_cast<TC*>(bufA) + lr * C::BN : static_cast<TC*>(bufB) + (lr - 32) * C::BN;
+          const void* src = row_buf(lr);
           TC* gdst = Cp + gr * a.ldc + col0;
           if (a.overwrite)
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
@@ -331,7 +346,7 @@ __device__ __forceinline__ void epilogue_bulk(const MMArgs& a,
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
-    __syncthreads();  // smem free again (round 2 / the next cp.async stage)
+    __syncthreads();  // smem free again (next round / the next cp.async stage)
   }
 }
 
