@@ -106,6 +106,18 @@ def make_inputs(device):
     return A_h, B_h
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "r1_minplus_ncu.json")
+    try:
+        k = json.load(open(path))["kernels"][0]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = sum(float(k[m]["value"]) * scale[k[m]["unit"]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        return tot, os.path.relpath(path, ROOT)
+    except Exception:
+        return None, None
+
+
 def alu_peak(device):
     """VIADDMNMX.U32 issue rate measured live (terms/clk/SM) -> Top/s at a given clock."""
     from paper_2011_01441_b200 import _native as nat
@@ -264,6 +276,7 @@ def main():
 
     if rank == 0:
         peak_max = 2 * tpc * 148 * 1965.0 / 1e6  # Top/s at the 1965 MHz max SM clock
+        traffic, traffic_src = ncu_traffic()
         achieved = OPS_PER_STEP / (kern_ms * 1e-3) / 1e12 if kern_ms else value / world / 1e3
         line = {
             "metric": METRIC, "value": value, "unit": "Gop/s", "n_gpus": world, "steps": args.steps,
@@ -279,7 +292,8 @@ def main():
                          "peak_source": (f"live VIADDMNMX.U32 probe: {tpc:.2f} terms/clk/SM x 2 op x 148 SM "
                                          f"x 1965 MHz max clock (probe ran at {probe_mhz:.0f} MHz)"),
                          "peak_at_run_clock": (2 * tpc * 148 * clocks["sm_mhz"] / 1e6) if clocks.get("sm_mhz") else None,
-                         "traffic": None, "algorithmic_bytes": ALG_BYTES},
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes": ALG_BYTES},
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
