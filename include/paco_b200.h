@@ -58,6 +58,10 @@ extern "C" {
 
 /* paco_mm flags */
 #define PACO_MM_OVERWRITE 1 /* C = A (x) B: C is not read (caller guarantees C == zero) */
+#define PACO_MM_ATOMIC 2    /* fold every C element atomically (semiring (+) in L2): other
+                               launches may fold into the same C concurrently (fused k-cut
+                               folds of a PACO plan) */
+#define PACO_MM_REMOTE 4    /* C is peer memory (NVLink): fold with element atomics, not TMA */
 
 /* dtype ids for paco_lincomb */
 #define PACO_DT_F32 0
@@ -111,6 +115,15 @@ int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out,
  * BYTES): the staging primitive of the overlapped host pipeline. */
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,
                 int64_t width, int64_t rows);
+
+/* Device memory for buffers shared across processes (CUDA IPC) -- the only
+ * allocation the library makes on a caller's behalf. */
+int paco_device_alloc(int device, size_t bytes, void** ptr);
+int paco_device_free(int device, void* ptr);
+/* CUDA IPC: export a paco_device_alloc'd pointer (64-byte handle), map a peer's. */
+int paco_ipc_handle(int device, void* ptr, void* handle64);
+int paco_ipc_open(int device, const void* handle64, void** ptr);
+int paco_ipc_close(int device, void* ptr);
 
 /* Enable peer access from `device` to `peer` (idempotent). */
 int paco_enable_peer(int device, int peer);

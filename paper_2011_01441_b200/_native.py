@@ -31,6 +31,8 @@ SR_COUNT = 9
 DT_F32, DT_F64, DT_I64 = 0, 1, 2
 
 MM_OVERWRITE = 1
+MM_ATOMIC = 2
+MM_REMOTE = 4
 TROPICAL_INF = 1 << 30
 MAX_PIECES = 640
 
@@ -54,6 +56,11 @@ SIGNATURES = {
                             ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                             ctypes.POINTER(ctypes.c_int32), _int]),
     "paco_copy2d": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
+    "paco_device_alloc": (_int, [_int, ctypes.c_size_t, ctypes.POINTER(_vp)]),
+    "paco_device_free": (_int, [_int, _vp]),
+    "paco_ipc_handle": (_int, [_int, _vp, _vp]),
+    "paco_ipc_open": (_int, [_int, _vp, ctypes.POINTER(_vp)]),
+    "paco_ipc_close": (_int, [_int, _vp]),
     "paco_enable_peer": (_int, [_int, _int]),
     "paco_alu_probe": (_int, [_int, _vp, _int, _int, ctypes.POINTER(ctypes.c_double),
                               ctypes.POINTER(ctypes.c_double)]),

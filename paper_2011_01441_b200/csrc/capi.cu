@@ -3,6 +3,7 @@
 // reports errors through return codes + a thread-local message.
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -166,6 +167,45 @@ int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void*
   PACO_TRY(use_device(device));
   PACO_CUDA_TRY(cudaMemcpy2DAsync(dst, size_t(dpitch), src, size_t(spitch), size_t(width), size_t(rows),
                                   cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return PACO_OK;
+}
+
+int paco_device_alloc(int device, size_t bytes, void** ptr) {
+  if (!ptr) {
+    set_error("paco_device_alloc: null output");
+    return PACO_ERR_ARG;
+  }
+  PACO_TRY(use_device(device));
+  PACO_CUDA_TRY(cudaMalloc(ptr, bytes));
+  return PACO_OK;
+}
+
+int paco_device_free(int device, void* ptr) {
+  PACO_TRY(use_device(device));
+  PACO_CUDA_TRY(cudaFree(ptr));
+  return PACO_OK;
+}
+
+int paco_ipc_handle(int device, void* ptr, void* handle64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  PACO_TRY(use_device(device));
+  cudaIpcMemHandle_t h;
+  PACO_CUDA_TRY(cudaIpcGetMemHandle(&h, ptr));
+  memcpy(handle64, &h, sizeof(h));
+  return PACO_OK;
+}
+
+int paco_ipc_open(int device, const void* handle64, void** ptr) {
+  PACO_TRY(use_device(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  PACO_CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return PACO_OK;
+}
+
+int paco_ipc_close(int device, void* ptr) {
+  PACO_TRY(use_device(device));
+  PACO_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
   return PACO_OK;
 }
 

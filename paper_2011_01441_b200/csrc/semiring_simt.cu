@@ -102,6 +102,7 @@ struct MMArgs {
   int32_t overwrite;
   long long* trace;  // optional per-CTA [smid, start ns, end ns, stages] (diagnostics)
   int32_t bulk_ok;   // C is 16 B aligned with ldc*sizeof(TC) % 16 == 0: TMA bulk epilogue
+  int32_t all_atomic;  // every piece folds atomically (other kernels fold into the same C)
 };
 
 // Stage one (C tile, k tile) of A and B into shared memory.  kVec: 16 B
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
   if (args.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int64_t kb = int64_t(pc.tl0) * args.kq;
   const int64_t kend = min(args.k, kb + int64_t(pc.tk) * args.kq);
-  const bool atomic = !(kb == 0 && kend == args.k);
+  const bool atomic = args.all_atomic || !(kb == 0 && kend == args.k);
   const int KT = int((kend - kb + C::BK - 1) / C::BK);
   const int total = pc.tn * pc.tm * KT;
 
@@ -609,7 +610,13 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
   if (rc) return rc;
   MMArgs args{A, B, C, lda, ldb, ldc, n, m, k, Cfg::KQ, (flags & PACO_MM_OVERWRITE) ? 1 : 0,
               g_trace_buffer,
-              (reinterpret_cast<uintptr_t>(C) % 16 == 0 && (ldc * sizeof(typename Op::TC)) % 16 == 0) ? 1 : 0};
+              (reinterpret_cast<uintptr_t>(C) % 16 == 0 && (ldc * sizeof(typename Op::TC)) % 16 == 0 &&
+               !(flags & PACO_MM_REMOTE)) ? 1 : 0,
+              (flags & (PACO_MM_ATOMIC | PACO_MM_REMOTE)) ? 1 : 0};
+  if (args.overwrite && (flags & (PACO_MM_ATOMIC | PACO_MM_REMOTE))) {
+    set_error("PACO_MM_OVERWRITE cannot be combined with atomic / remote folding");
+    return PACO_ERR_ARG;
+  }
   if (args.overwrite && table.ksplit) {
     // atomics fold into C, so C must first hold the semiring zero
     rc = paco_fill(device, stream, Op::kId, C, ldc, n, m);

@@ -540,6 +540,15 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
     set_error("tcgen05 path: extents must fit int32");
     return PACO_ERR_ARG;
   }
+  if ((flags & PACO_MM_REMOTE) || ((flags & PACO_MM_ATOMIC) && !pitch_ok(C, ldc, 4))) {
+    // the TMA reduce-add epilogue is atomic, but only on local C with a TMA-able pitch
+    set_error("tcgen05 path: atomic folding needs a local C with a 16-byte row pitch");
+    return PACO_ERR_UNSUPPORTED;
+  }
+  if ((flags & PACO_MM_ATOMIC) && (flags & PACO_MM_OVERWRITE)) {
+    set_error("PACO_MM_OVERWRITE cannot be combined with atomic folding");
+    return PACO_ERR_ARG;
+  }
   int rc;
   tc::TcMaps maps;
   int32_t a_off = 0, b_off = 0, c_off = 0, t_off = 0;

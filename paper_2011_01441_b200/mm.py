@@ -50,12 +50,15 @@ def kernel_for(semiring: Semiring, A, B) -> tuple[int, object]:
 
 
 def launch_mm(kid: int, stream: torch.cuda.Stream, a: View, b: View, c: View, *,
-              pieces=None, overwrite: bool = False) -> None:
-    """One ``paco_mm`` call on views (no validation beyond the C ABI's)."""
+              pieces=None, overwrite: bool = False, flags: int = 0, device: int | None = None) -> None:
+    """One ``paco_mm`` call on views (no validation beyond the C ABI's).
+
+    ``device`` is the GPU that runs the kernel (default: C's device; differs
+    when C is peer memory, with ``flags`` carrying MM_REMOTE)."""
     arr, npieces = nat.pieces_array(pieces)
     nat.check(nat.load().paco_mm(
-        c.device, stream.cuda_stream, kid, a.ptr, a.ld, b.ptr, b.ld, c.ptr, c.ld,
-        c.rows, c.cols, a.cols, arr, npieces, nat.MM_OVERWRITE if overwrite else 0))
+        c.device if device is None else device, stream.cuda_stream, kid, a.ptr, a.ld, b.ptr, b.ld,
+        c.ptr, c.ld, c.rows, c.cols, a.cols, arr, npieces, flags | (nat.MM_OVERWRITE if overwrite else 0)))
 
 
 def launch_fold(kid: int, stream: torch.cuda.Stream, dst: View, src: View, reset: bool) -> None:
@@ -220,8 +223,35 @@ def semiring_vadd(semiring: Semiring, x, y):
     return out if isinstance(x, torch.Tensor) and x.is_cuda else out.cpu()
 
 
+def fold_destinations(plan: Plan) -> dict[int, tuple[int, int, int]]:
+    """Where each temporary finally lands: temp id -> (buffer 0, row offset, col offset).
+
+    A REDUCE folds temp ``b`` into ``(out, oi, oj)`` (matmul.py:455-460); chains of
+    nested k-cuts compose, ending in the caller's C (buffer 0).
+    """
+    via = {spec[0]: (spec[1], spec[2], spec[3]) for spec in plan.meta["reduces"].values()}
+    dest: dict[int, tuple[int, int, int]] = {}
+
+    def resolve(bid: int) -> tuple[int, int, int]:
+        if bid == 0:
+            return (0, 0, 0)
+        if bid not in dest:
+            tgt, oi, oj = via[bid]
+            fb, fi, fj = resolve(tgt)
+            dest[bid] = (fb, fi + oi, fj + oj)
+        return dest[bid]
+
+    for bid in plan.meta["temp_sizes"]:
+        resolve(bid)
+    return dest
+
+
+_TC_KERNELS = (nat.SR_BF16_F32, nat.SR_F32_TC)
+
+
 def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str = "serial_sim",
-               sims: dict | None = None, *, devices: list[int] | None = None) -> CostReport:
+               sims: dict | None = None, *, devices: list[int] | None = None,
+               fused_folds: bool | None = None) -> CostReport:
     """Run an MM plan on B200s (matmul.py:417-462).
 
     Worker ``w`` runs on ``devices[w % len(devices)]`` with its own stream
@@ -245,6 +275,13 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
     home = devices[0]
     dev_of = [devices[w % len(devices)] for w in range(plan.p)]
     used = sorted(set(dev_of))
+    has_reduces = bool(meta["reduces"])
+    if fused_folds is None:
+        fused_folds = semiring.dtype.kind in "iu" if hasattr(semiring.dtype, "kind") else False
+    if kid in _TC_KERNELS and any(d != home for d in used):
+        fused_folds = False  # the tensor-core epilogue folds atomically only into local C
+    fused_folds = fused_folds and has_reduces
+    fold_dest = fold_destinations(plan) if fused_folds else {}
     lib = nat.load()
     for d in used:
         if d != home:
@@ -257,7 +294,7 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
         out = Output(C, semiring.dtype, home)
         c_view = View.of(out.dev)
         temps: dict[int, View] = {}
-        for bid, size in meta["temp_sizes"].items():
+        for bid, size in ([] if fused_folds else meta["temp_sizes"].items()):
             shape = temp_shape(plan, bid) if size else (0, 1)
             t = torch.empty(shape, dtype=torch_dtype(semiring.dtype), device=home)
             temps[bid] = View.of(t)
@@ -287,10 +324,16 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
             if task.kind == COMPUTE:
                 cb: Cuboid = task.region
                 dv = dev_of[w]
+                if fused_folds:
+                    fb, fi, fj = fold_dest.get(cb.out, (0, 0, 0))
+                    out = c_view.sub(fi + cb.out_i0, fj + cb.out_j0, cb.n, cb.m)
+                    flags = nat.MM_ATOMIC | (nat.MM_REMOTE if dv != home else 0)
+                else:
+                    out = buffer(cb.out).sub(cb.out_i0, cb.out_j0, cb.n, cb.m)
+                    flags = 0
                 launch_mm(kid, st, a_on[dv].sub(cb.i0, cb.l0, cb.n, cb.k),
-                          b_on[dv].sub(cb.l0, cb.j0, cb.k, cb.m),
-                          buffer(cb.out).sub(cb.out_i0, cb.out_j0, cb.n, cb.m))
-            elif task.kind == REDUCE:
+                          b_on[dv].sub(cb.l0, cb.j0, cb.k, cb.m), out, flags=flags, device=dv)
+            elif task.kind == REDUCE and not fused_folds:
                 bid, tgt, oi, oj, rn, rm = reduces[task.id]
                 launch_fold(semiring.kernel_id, st, buffer(tgt).sub(oi, oj, rn, rm),
                             temps[bid], reset=True)

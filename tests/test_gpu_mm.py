@@ -290,3 +290,30 @@ def test_pinned_host_pipeline_matches_oracle():
     M.mm_seq(A, B, C2, M.SEMIRING_MINPLUS_SAT, overwrite=True)
     want2 = cref.mm(cref.SR_MINPLUS_SAT32, A.numpy(), B.numpy(), np.full((n, m), INF, np.int32))
     assert np.array_equal(C2.numpy(), want2)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_fused_and_explicit_folds_agree(fused):
+    """k-cut plans: epilogue-fused folds (no temps) and explicit REDUCE folds give the reference C."""
+    rng = np.random.default_rng(51)
+    n, m, k = 150, 130, 700                      # k-heavy: every plan below cuts k
+    A = tropical(rng, (n, k), 0, 2**20, 0.1)
+    B = tropical(rng, (k, m), 0, 2**20, 0.1)
+    C0 = tropical(rng, (n, m), 0, 2**21, 0.5)
+    want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, C0.copy())
+    for p in (2, 3, 5, 7, 8):
+        for plan in (M.mm_one_piece_partition(n, m, k, p), M.mm_paco_partition(n, m, k, p, base=64)):
+            assert plan.meta["reduces"], (p, plan.meta["variant"])
+            C = C0.copy()
+            M.mm_execute(plan, A, B, C, M.SEMIRING_MINPLUS_SAT, mode="parallel", fused_folds=fused)
+            assert np.array_equal(C, want), (p, plan.meta["variant"], fused)
+    # int64 ring (wide kernel, element atomics) and f64 (order-free within tolerance)
+    A64 = rng.integers(-1000, 1000, (n, k)).astype(np.int64)
+    B64 = rng.integers(-1000, 1000, (k, m)).astype(np.int64)
+    C = np.zeros((n, m), np.int64)
+    M.mm_execute(M.mm_paco_partition(n, m, k, 5, base=64), A64, B64, C, M.SEMIRING_INT, fused_folds=fused)
+    assert np.array_equal(C, A64 @ B64)
+    Af, Bf = rng.standard_normal((n, k)), rng.standard_normal((k, m))
+    C = np.zeros((n, m))
+    M.mm_execute(M.mm_one_piece_partition(n, m, k, 7), Af, Bf, C, M.SEMIRING_F64, fused_folds=fused)
+    np.testing.assert_allclose(C, Af @ Bf, rtol=1e-11, atol=1e-9)
