@@ -6,7 +6,9 @@ One step = one full C (+)= A (x) B over the 8192^3 iteration cuboid, inputs
 resident in HBM: the GPU-level PACO plan (mm_one_piece_partition over N ranks,
 matmul.py:250-300) gives each rank one cuboid; inside each rank the CTA-level
 plan (MM-1-Piece over the tile grid, 148 SMs x 2 CTAs) drives one persistent
-sm_100a launch; k-cut folds (N >= 5) are NCCL MIN reductions.  The timed region
+sm_100a launch; k-cut folds (N >= 5) are fused into the kernels (upper-k ranks
+fold straight into the owner's C over CUDA IPC / NVLink; --fold nccl uses NCCL
+MIN reductions instead).  The timed region
 is bracketed by barrier + synchronize, timed with CUDA events and max'ed over
 ranks.  A, B (256 MiB each) exceed the 126 MB L2, so no flush is needed.
 
@@ -167,6 +169,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-rows", type=int, default=48, help="rows of A per host process (reference arm)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fold", default="fused", choices=["fused", "nccl"],
+                    help="N>1: k-cut folds fused into the kernels over IPC, or NCCL reductions")
     args = ap.parse_args()
 
     world = env_int("WORLD_SIZE", 1)
@@ -181,14 +185,18 @@ def main():
     from paper_2011_01441_b200 import _native as nat
     from paper_2011_01441_b200 import matmul as M
     from paper_2011_01441_b200.device import View
-    from paper_2011_01441_b200.distributed import CudaOps, DistributedMM
+    from paper_2011_01441_b200.distributed import CudaOps, DistributedMM, FusedDistributedMM
     from paper_2011_01441_b200.mm import launch_mm
 
-    torch.cuda.set_device(local)
-    dev = local
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PACO_BENCH_BACKEND", "nccl")  # gloo: N ranks on fewer GPUs (testing)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
 
     A_h, B_h = make_inputs(dev)
     A = A_h.to(dev)
@@ -205,6 +213,18 @@ def main():
             launch_mm(kid, st, a, b, c)
         launches_per_step = 1
         plan_desc = "1 GPU, CTA-level MM-1-Piece over 296 pieces (148 SMs x 2)"
+    elif args.fold == "fused":
+        plan = M.mm_one_piece_partition(N, N, N, world)
+        ex = FusedDistributedMM(plan, sr, kid, dev)
+        nred = sum(1 for t in plan.tasks if t.kind == "reduce")
+
+        def step():
+            ex.run(A, B)
+        launches_per_step = 1 + len(ex.launches)
+        plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}); its {nred} k-cut folds "
+                     f"are fused into the kernels (upper-k ranks fold their tiles into the owner's C "
+                     f"over CUDA IPC/NVLink, {'TMA bulk' if ex.remote_bulk else 'element'} atomics); "
+                     "CTA-level MM-1-Piece inside each rank")
     else:
         plan = M.mm_one_piece_partition(N, N, N, world)
         ex = DistributedMM(plan, sr, CudaOps(sr, kid, st))

@@ -32,12 +32,13 @@ def torch_dtype(dt) -> torch.dtype:
 
 @dataclass
 class View:
-    tensor: torch.Tensor  # keeps the storage alive
+    tensor: torch.Tensor | None  # keeps the storage alive (None: raw device memory)
     ptr: int
     ld: int
     rows: int
     cols: int
     device: int
+    itemsize: int = 0
 
     @classmethod
     def of(cls, t: torch.Tensor) -> "View":
@@ -48,16 +49,23 @@ class View:
         if t.numel() > 0 and t.shape[1] > 1 and t.stride(1) != 1:
             raise ValueError("View needs unit column stride")
         ld = t.stride(0) if t.shape[0] > 1 else max(t.shape[1], 1)
-        return cls(t, t.data_ptr(), max(ld, t.shape[1]), t.shape[0], t.shape[1], t.device.index)
+        return cls(t, t.data_ptr(), max(ld, t.shape[1]), t.shape[0], t.shape[1], t.device.index,
+                   t.element_size())
+
+    @classmethod
+    def raw(cls, ptr: int, rows: int, cols: int, itemsize: int, device: int, ld: int | None = None) -> "View":
+        """A view of device memory not owned by PyTorch (e.g. CUDA IPC-mapped peer memory)."""
+        return cls(None, ptr, ld if ld is not None else cols, rows, cols, device, itemsize)
 
     @property
     def elsize(self) -> int:
-        return self.tensor.element_size()
+        return self.itemsize or self.tensor.element_size()
 
     def sub(self, i0: int, j0: int, n: int, m: int) -> "View":
         if i0 < 0 or j0 < 0 or i0 + n > self.rows or j0 + m > self.cols:
             raise ValueError(f"sub-view [{i0}:{i0 + n}, {j0}:{j0 + m}] outside {self.rows}x{self.cols}")
-        return View(self.tensor, self.ptr + (i0 * self.ld + j0) * self.elsize, self.ld, n, m, self.device)
+        return View(self.tensor, self.ptr + (i0 * self.ld + j0) * self.elsize, self.ld, n, m, self.device,
+                    self.elsize)
 
 
 def is_host(x) -> bool:

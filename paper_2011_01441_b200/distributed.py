@@ -175,3 +175,178 @@ class DistributedMM:
     def gather(self, C_local: torch.Tensor, dst: int = 0) -> None:
         """Assemble the full C on ``dst``: one (+)-reduce of the holder copies."""
         dist.reduce(C_local, dst=dst, op=self.op)
+
+
+def fused_launches(plan: Plan, rank: int):
+    """Owner map and this rank's kernel launches for fused folds.
+
+    Owners: the out=0 COMPUTE rectangles (they partition C) with their worker.
+    Launches: every COMPUTE task of ``rank`` whose final C rectangle (temps
+    resolved through the REDUCE chain, ``mm.fold_destinations``) is cut along
+    the owner rectangles it overlaps: (A rows/cols, B rows/cols, owner, C rect).
+    """
+    from .mm import fold_destinations
+
+    owners = []
+    for t in plan.tasks:
+        if t.kind == COMPUTE and t.region.out == 0:
+            c = t.region
+            owners.append(((c.out_i0, c.out_j0, c.n, c.m), t.worker))
+    dest = fold_destinations(plan)
+    launches = []
+    for t in plan.tasks:
+        if t.kind != COMPUTE or t.worker != rank:
+            continue
+        c = t.region
+        _, fi, fj = dest.get(c.out, (0, 0, 0))
+        D = (fi + c.out_i0, fj + c.out_j0, c.n, c.m)
+        for rect, owner in owners:
+            x = _rect_intersect(D, rect)
+            if x is None:
+                continue
+            di, dj = x[0] - D[0], x[1] - D[1]
+            launches.append(((c.i0 + di, c.l0, x[2], c.k), (c.l0, c.j0 + dj, c.k, x[3]), owner, x))
+    return owners, launches
+
+
+def _rect_intersect(a, b):
+    i0, j0 = max(a[0], b[0]), max(a[1], b[1])
+    i1, j1 = min(a[0] + a[2], b[0] + b[2]), min(a[1] + a[3], b[1] + b[3])
+    return (i0, j0, i1 - i0, j1 - j0) if i1 > i0 and j1 > j0 else None
+
+
+class FusedDistributedMM:
+    """One process per GPU with the k-cut folds fused into the kernels.
+
+    Every C element is owned by the rank whose out=0 COMPUTE task covers it
+    (those rectangles partition C).  Each rank's C lives in IPC-shareable
+    device memory; a task whose output is a temporary writes its tiles
+    straight to their final place in the owners' C -- over NVLink for remote
+    owners (element atomics, ``PACO_MM_REMOTE``), locally with the TMA bulk
+    reduction -- so the plan's REDUCE tasks vanish: no temporaries, no fold
+    pass, no NCCL call on the data path.  Remote folds use the TMA bulk
+    reduction too when a start-up probe shows it lands correctly in peer
+    memory (``remote_bulk``).  Construct on every rank (it exchanges IPC
+    handles with ``all_gather_object``).
+    """
+
+    def __init__(self, plan: Plan, semiring, kernel_id: int, device: int, *, group=None):
+        import ctypes
+
+        import numpy as np
+
+        from . import _native as nat
+        from .device import View, torch_dtype
+        from .mm import fold_destinations
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if plan.p != self.world:
+            raise PlanError(f"plan built for p={plan.p}, world size is {self.world}")
+        plan.validate()
+        self.plan, self.semiring, self.kid, self.device, self.group = plan, semiring, kernel_id, device, group
+        self.n, self.m = plan.meta["n"], plan.meta["m"]
+        self.tdtype = torch_dtype(semiring.dtype)
+        self.itemsize = np.dtype(semiring.dtype).itemsize
+        self.op = _REDUCE_OPS[semiring.name]
+        self.nat = nat
+        lib = nat.load()
+        ptr = ctypes.c_void_p()
+        nat.check(lib.paco_device_alloc(device, self.n * self.m * self.itemsize, ctypes.byref(ptr)))
+        self.own_ptr = ptr.value
+        handle = ctypes.create_string_buffer(64)
+        nat.check(lib.paco_ipc_handle(device, self.own_ptr, handle))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw, group=group)
+        self.ptrs = []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.ptrs.append(self.own_ptr)
+                continue
+            p = ctypes.c_void_p()
+            nat.check(lib.paco_ipc_open(device, ctypes.create_string_buffer(h, 64), ctypes.byref(p)))
+            self.ptrs.append(p.value)
+        self.views = [View.raw(p, self.n, self.m, self.itemsize, device) for p in self.ptrs]
+        owners, self.launches = fused_launches(plan, self.rank)
+        self.owned = [rect for rect, w in owners if w == self.rank]
+        self.remote_bulk = self._probe_remote_bulk()
+
+    def _probe_remote_bulk(self) -> bool:
+        """Can the TMA bulk-reduce epilogue fold into a peer's IPC-mapped C?
+
+        Each rank folds a small known product into the next rank's buffer with
+        the bulk epilogue, every owner checks what landed against a local
+        computation, and the fused path uses bulk remote folds only if all
+        ranks agree; otherwise remote folds use element atomics (MM_REMOTE).
+        """
+        from .device import View
+        from .mm import launch_fill, launch_mm
+
+        if self.world == 1 or self.n < 128 or self.m < 128:
+            return False
+        dev = self.device
+        st = torch.cuda.current_stream(dev)
+        g = torch.Generator(device="cpu").manual_seed(1234)
+        a = torch.randint(0, 1000, (128, 8), generator=g, dtype=torch.int32).to(dev)
+        b = torch.randint(0, 1000, (8, 128), generator=g, dtype=torch.int32).to(dev)
+        probe_sr = self.nat.SR_MINPLUS_SAT32
+        mine = View.raw(self.own_ptr, 128, 128, 4, dev, ld=self.m * self.itemsize // 4)
+        launch_fill(probe_sr, st, mine)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=self.group)
+        peer = (self.rank + 1) % self.world
+        pv = View.raw(self.ptrs[peer], 128, 128, 4, dev, ld=self.m * self.itemsize // 4)
+        ok = True
+        try:
+            launch_mm(probe_sr, st, View.of(a), View.of(b), pv, flags=self.nat.MM_ATOMIC, device=dev)
+            torch.cuda.synchronize(dev)
+        except Exception:
+            ok = False
+        dist.barrier(group=self.group)
+        ref = torch.full((128, 128), 2**30, dtype=torch.int32, device=dev)
+        launch_mm(probe_sr, st, View.of(a), View.of(b), View.of(ref))
+        got = torch.empty((128, 128), dtype=torch.int32, device=dev)
+        from .mm import _copy2d_raw
+        _copy2d_raw(dev, got, self.own_ptr, self.m * self.itemsize)
+        torch.cuda.synchronize(dev)
+        ok = ok and bool(torch.equal(got, ref))
+        flags = [None] * self.world
+        dist.all_gather_object(flags, ok, group=self.group)
+        return all(flags)
+
+    def run(self, A: torch.Tensor, B: torch.Tensor, C_init: torch.Tensor | None = None) -> None:
+        from .device import View
+        from .mm import launch_fill, launch_fold, launch_mm
+
+        st = torch.cuda.current_stream(self.device)
+        mine = self.views[self.rank]
+        launch_fill(self.semiring.kernel_id, st, mine)
+        if C_init is not None:
+            ci = View.of(C_init)
+            for (i0, j0, n, m) in self.owned:
+                launch_fold(self.semiring.kernel_id, st, mine.sub(i0, j0, n, m), ci.sub(i0, j0, n, m), False)
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)          # every owner's C is initialised
+        av, bv = View.of(A), View.of(B)
+        for (ai, al, an, ak), (bl, bj, bk, bm), owner, (ci, cj, cn, cm) in self.launches:
+            remote = owner != self.rank and not self.remote_bulk
+            flags = self.nat.MM_ATOMIC | (self.nat.MM_REMOTE if remote else 0)
+            launch_mm(self.kid, st, av.sub(ai, al, an, ak), bv.sub(bl, bj, bk, bm),
+                      self.views[owner].sub(ci, cj, cn, cm), flags=flags, device=self.device)
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)          # every remote fold has landed
+
+    def gather(self, out: torch.Tensor, dst: int = 0) -> None:
+        """Copy this rank's C into ``out`` and reduce the owners' pieces onto ``dst``."""
+        from .mm import _copy2d_raw
+
+        _copy2d_raw(self.device, out, self.own_ptr, self.m * self.itemsize)
+        dist.reduce(out, dst=dst, op=self.op, group=self.group)
+
+    def close(self) -> None:
+        lib = self.nat.load()
+        for r, p in enumerate(self.ptrs):
+            if r != self.rank:
+                lib.paco_ipc_close(self.device, p)
+        lib.paco_device_free(self.device, self.own_ptr)
+        self.ptrs = []

@@ -127,6 +127,14 @@ def _copy2d(stream, dst: torch.Tensor, dr0: int, dc0: int, src: torch.Tensor, sr
         src.data_ptr() + (sr0 * src.stride(0) + sc0) * es, src.stride(0) * es, cols * es, rows))
 
 
+def _copy2d_raw(device: int, out: torch.Tensor, src_ptr: int, src_pitch: int) -> None:
+    """out (contiguous, on ``device``) <- rows of raw device memory at src_ptr."""
+    st = torch.cuda.current_stream(device)
+    es = out.element_size()
+    nat.check(nat.load().paco_copy2d(device, st.cuda_stream, out.data_ptr(), out.stride(0) * es, src_ptr,
+                                     src_pitch, out.shape[1] * es, out.shape[0]))
+
+
 def _pipelined_host_mm(A, B, C, kid: int, semiring: Semiring, dev: int, st, overwrite: bool) -> None:
     """Host (pinned) operands: overlap H2D, compute and D2H over a 2-D block grid.
 

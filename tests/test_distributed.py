@@ -124,3 +124,25 @@ def test_distributed_matches_oracle(world):
     results = sorted(q.get(timeout=5) for _ in cases)
     assert all(ok for _, ok, _ in results), results
     assert any(nred > 0 for _, _, nred in results)
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 7, 8])
+def test_fused_launches_cover_iteration_space_once(p):
+    """Fused folds: all ranks' launches tile the (i, j, l) cuboid exactly once, and
+    every launch writes inside one owner's rectangle of C."""
+    from paper_2011_01441_b200.distributed import fused_launches
+    rng = np.random.default_rng(p)
+    for _ in range(6):
+        n, m, k = (int(x) for x in rng.integers(8, 60, 3))
+        for plan in (M.mm_one_piece_partition(n, m, k * 4, p), M.mm_paco_partition(n, m, k, p, base=6)):
+            cover = np.zeros((plan.meta["n"], plan.meta["m"], plan.meta["k"]), np.int32)
+            for r in range(p):
+                owners, launches = fused_launches(plan, r)
+                for (ai, al, an, ak), (bl, bj, bk, bm), owner, (ci, cj, cn, cm) in launches:
+                    assert (an, bm) == (cn, cm) and ak == bk and al == bl
+                    assert ci == ai and cj == bj  # C[i, j] gets A row i and B column j
+                    cover[ai:ai + an, bj:bj + bm, al:al + ak] += 1
+                    owner_rects = [o for o in owners if o[1] == owner]
+                    assert any(o[0][0] <= ci and o[0][1] <= cj and ci + cn <= o[0][0] + o[0][2]
+                               and cj + cm <= o[0][1] + o[0][3] for o in owner_rects)
+            assert (cover == 1).all()
