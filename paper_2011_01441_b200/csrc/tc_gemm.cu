@@ -5,13 +5,11 @@
 // dense floating-point case.  One persistent CTA per SM, warp-specialised:
 //   warp 0      TMA producer: A tile [128 x 64] (K-major) and B tile
 //               [64 x 256] (N-major, as the caller stores it) per k block,
-//               128B-swizzled, into a 4-stage smem ring; when K fits the ring
-//               (K <= 256) B stays resident across consecutive tiles of the
-//               same column block;
+//               128B-swizzled, into a 3-stage smem ring;
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma.kind::f16
 //               (M=128, N=256, K=16) into a double-buffered TMEM accumulator
 //               (2 x 256 fp32 columns) and commits to mbarriers;
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> swizzled smem
+//   warps 2..   epilogue: tcgen05.ld 32x32b.x32 -> registers -> swizzled smem
 //               staging -> TMA tensor store (C = AB) or TMA reduce-add
 //               (C += AB), overlapping the next tile's MMAs.
 // The CTA-level plan is the 1-D MM-1-Piece split of the column-block-major
@@ -42,12 +40,15 @@ namespace paco {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int THREADS = 192;                // 6 warps
+// warp 0: TMA producer, warp 1: MMA issuer, warps 2..: epilogue (Kind::EPI_WARPS)
 constexpr int EPI_BUF = 32 * 32 * 4;        // 4 KB: 32 rows x 32 fp32 (128 B)
 
 // bf16 inputs, one MMA pass; N=256 tiles, 64-deep k blocks (128 B rows).
 struct KindBF16 {
-  static constexpr int BN = 256, BK = 64, UMMA_K = 16, STAGES = 4, ELEM = 2, NOPS = 1, PASSES = 1;
+  static constexpr int BN = 256, BK = 64, UMMA_K = 16, STAGES = 3, ELEM = 2, NOPS = 1, PASSES = 1;
+  // 3 stages of 48 KB; 8 epilogue warps (2 per TMEM lane quadrant, half the
+  // columns each): the epilogue -- not the MMAs -- bounds this HBM-bound kernel
+  static constexpr int RING_BYTES = 160 * 1024, EPI_WARPS = 8;
   static constexpr bool B_KMAJOR = false;
   // F32 accumulate, BF16 A/B (format 1), A K-major, B MN-major (bit 16)
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
@@ -57,6 +58,7 @@ struct KindBF16 {
 // fp32 inputs as 3xTF32 (hi/lo operand tiles), N=128 tiles, 32-deep k blocks.
 struct KindTF32x3 {
   static constexpr int BN = 128, BK = 32, UMMA_K = 8, STAGES = 3, ELEM = 4, NOPS = 2, PASSES = 3;
+  static constexpr int RING_BYTES = 3 * 64 * 1024, EPI_WARPS = 4;
   static constexpr bool B_KMAJOR = true;  // B^T tiles (the split writes B transposed)
   // F32 accumulate, TF32 A/B (format 2), both K-major
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
@@ -70,9 +72,11 @@ struct Layout {
   static constexpr int A_BYTES = BM * K::BK * K::ELEM;        // one operand tile
   static constexpr int B_BYTES = K::BN * K::BK * K::ELEM;
   static constexpr int STAGE_BYTES = K::NOPS * (A_BYTES + B_BYTES);
-  static constexpr int SMEM_EPI = K::STAGES * STAGE_BYTES;
-  static constexpr int SMEM_BAR = SMEM_EPI + 4 * 2 * EPI_BUF;
-  static constexpr int SMEM_ALLOC = SMEM_BAR + 256 + 1024;    // + runtime 1024-B alignment slack
+  static constexpr int SMEM_EPI = K::RING_BYTES;
+  static constexpr int SMEM_BAR = SMEM_EPI + K::EPI_WARPS * 2 * EPI_BUF;
+  static constexpr int THREADS = 64 + 32 * K::EPI_WARPS;
+  static_assert(K::STAGES * STAGE_BYTES <= K::RING_BYTES, "stage ring");
+  static constexpr int SMEM_ALLOC = SMEM_BAR + 512 + 1024;    // + runtime 1024-B alignment slack
   static constexpr uint32_t TMEM_COLS = 2 * K::BN;            // double-buffered accumulator
   static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
   __device__ static int a_off(int stage, int op) { return stage * STAGE_BYTES + op * A_BYTES; }
@@ -184,27 +188,45 @@ struct TcArgs {
   int32_t ablate;    // diagnostics: 1 = no C stores, 2 = no MMAs, 4 = no smem staging
 };
 
+// CTA-level plan: contiguous ranges of the column-block-major tile sequence
+// (the 1-D MM-1-Piece split: floor/ceil(T/p) tiles per CTA), so consecutive
+// tiles of a CTA share their B column block and concurrent CTAs share A rows.
+struct TileRange {
+  int64_t begin, count;
+};
+
+__device__ __forceinline__ TileRange cta_tiles(const TcArgs& a) {
+  const int64_t G = gridDim.x, c = blockIdx.x;
+  const int64_t T = int64_t(a.tiles_rb) * a.tiles_nb;
+  const int64_t b = T * c / G, e = T * (c + 1) / G;
+  return TileRange{b, e - b};
+}
+
+__device__ __forceinline__ void tile_coords(const TcArgs& a, const TileRange& r, int64_t i, int& nb, int& rb) {
+  const int64_t t = r.begin + i;
+  nb = int(t / a.tiles_rb);
+  rb = int(t % a.tiles_rb);
+}
+
 struct TcMaps {
   CUtensorMap a[2], b[2], c;  // operand maps (hi/lo for 3xTF32) and the output map
 };
 
 template <class K>
-__global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
+__global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
   using L = Layout<K>;
   constexpr int STAGES = K::STAGES, BN = K::BN, BK = K::BK;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int MAXR = 16;  // barrier slots for the stage / A ring
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::SMEM_BAR);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* empty = full + MAXR;
+  uint64_t* tfull = empty + MAXR;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-  // CTA-level plan: contiguous range of the column-block-major tile sequence
-  const int64_t T = int64_t(args.tiles_rb) * args.tiles_nb;
-  const int64_t t_begin = T * blockIdx.x / gridDim.x, t_end = T * (blockIdx.x + 1) / gridDim.x;
+  const TileRange tr = cta_tiles(args);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -213,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], K::EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     for (int o = 0; o < K::NOPS; ++o) {
@@ -235,20 +257,18 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      const bool can_keep_b = args.kblocks == STAGES;
-      int resident_nb = -1;
-      uint32_t it = 0;
-      for (int64_t t = t_begin; t < t_end; ++t) {
-        const int nb = int(t / args.tiles_rb), rb = int(t % args.tiles_rb);
-        const bool keep_b = can_keep_b && nb == resident_nb;
-        for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-          mbar_expect_tx(&full[s], K::NOPS * (keep_b ? L::A_BYTES : L::A_BYTES + L::B_BYTES));
+      {
+        uint32_t it = 0;
+        for (int64_t i = 0; i < tr.count; ++i) {
+          int nb, rb;
+          tile_coords(args, tr, i, nb, rb);
+          for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+            mbar_expect_tx(&full[s], K::NOPS * (L::A_BYTES + L::B_BYTES));
 #pragma unroll
-          for (int o = 0; o < K::NOPS; ++o) {
-            tma_load_2d(smem + L::a_off(s, o), &maps.a[o], &full[s], args.a_col0 + kb * BK, rb * BM);
-            if (!keep_b) {
+            for (int o = 0; o < K::NOPS; ++o) {
+              tma_load_2d(smem + L::a_off(s, o), &maps.a[o], &full[s], args.a_col0 + kb * BK, rb * BM);
               if constexpr (K::B_KMAJOR) {
                 // B^T (m x k, K contiguous): one box of [BN rows][BK k]
                 tma_load_2d(smem + L::b_off(s, o), &maps.b[o], &full[s], args.b_col0 + kb * BK, nb * BN);
@@ -262,7 +282,6 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
             }
           }
         }
-        resident_nb = can_keep_b ? nb : -1;
       }
     }
   } else if (warp == 1) {
@@ -270,7 +289,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
       // ---------------- MMA issuer ----------------
       uint32_t it = 0;
       int tile = 0;
-      for (int64_t t = t_begin; t < t_end; ++t, ++tile) {
+      for (int64_t i = 0; i < tr.count; ++i, ++tile) {
         const int a = tile & 1;
         const uint32_t use = uint32_t(tile >> 1);
         mbar_wait(&tempty[a], (use & 1) ^ 1);
@@ -283,9 +302,9 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
           uint64_t ad[K::NOPS], bd[K::NOPS];
 #pragma unroll
           for (int o = 0; o < K::NOPS; ++o) {
-            ad[o] = smem_desc_sw128(smem_u32(smem + L::a_off(s, o)));
-            bd[o] = K::B_KMAJOR ? smem_desc_sw128(smem_u32(smem + L::b_off(s, o)))
-                                : smem_desc_mn_sw128(smem_u32(smem + L::b_off(s, o)), BK);
+            const int aoff = L::a_off(s, o), boff = L::b_off(s, o);
+            ad[o] = smem_desc_sw128(smem_u32(smem + aoff));
+            bd[o] = K::B_KMAJOR ? smem_desc_sw128(smem_u32(smem + boff)) : smem_desc_mn_sw128(smem_u32(smem + boff), BK);
           }
 #pragma unroll
           for (int kk = 0; kk < BK / K::UMMA_K; ++kk) {
@@ -307,60 +326,75 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     }
   } else {
     // ---------------- epilogue warps ----------------
+    // Each warp drains its TMEM lane quadrant for PER 32-column chunks of the
+    // tile, two chunks per tcgen05.ld (32x32b.x64): stage both into
+    // 128B-swizzled [32 rows][32 fp32] buffers, one proxy fence, two TMA
+    // stores (C = AB) or TMA reduce-adds (C += AB).
     const int q = warp % 4;  // TMEM lane quadrant this warp may access
-    unsigned char* stage0 = smem + L::SMEM_EPI + q * 2 * EPI_BUF;
+    const int ew = warp - 2;  // epilogue warp index
+    constexpr int CHUNKS = BN / 32, PER = CHUNKS * 4 / K::EPI_WARPS;  // chunks per warp
+    static_assert(PER % 2 == 0, "chunk pairs");
+    const int c_lo = (ew / 4) * PER;
+    unsigned char* stage0 = smem + L::SMEM_EPI + ew * 2 * EPI_BUF;
     int tile = 0;
-    uint32_t nstore = 0;
-    for (int64_t t = t_begin; t < t_end; ++t, ++tile) {
-      const int nb = int(t / args.tiles_rb), rb = int(t % args.tiles_rb);
+    for (int64_t i = 0; i < tr.count; ++i, ++tile) {
+      int nb, rb;
+      tile_coords(args, tr, i, nb, rb);
       const int a = tile & 1;
       const uint32_t use = uint32_t(tile >> 1);
       mbar_wait(&tfull[a], use & 1);
       tc_fence_after();
       const int row0 = rb * BM + 32 * q;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
+      for (int c = c_lo; c < c_lo + PER; c += 2) {
+        uint32_t v[64];
         const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(a * BN + 32 * c);
+#define PACO_R8(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), "=r"(v[i + 5]), \
+                   "=r"(v[i + 6]), "=r"(v[i + 7])
         asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-            "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, "
+            "%34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, "
+            "%54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];\n"
+            : PACO_R8(0), PACO_R8(8), PACO_R8(16), PACO_R8(24), PACO_R8(32), PACO_R8(40), PACO_R8(48), PACO_R8(56)
             : "r"(taddr));
+#undef PACO_R8
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (c == BN / 32 - 1) {
+        if (c + 2 == c_lo + PER) {
           // all of this warp's TMEM reads for the tile are done: release the buffer
           tc_fence_before();
           if (lane == 0) mbar_arrive(&tempty[a]);
         }
         const int col0 = nb * BN + 32 * c;
         if (col0 >= args.m) continue;  // warp-uniform: nothing left to store
-        unsigned char* buf = stage0 + (nstore & 1) * EPI_BUF;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        const bool second = col0 + 32 < args.m;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
         __syncwarp();
-        // 128B-swizzled [32 rows][32 fp32] staging: 16 B chunk j of row r at (j ^ r%8)
         if (!(args.ablate & 4)) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uint4 w = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            *reinterpret_cast<uint4*>(buf + lane * 128 + ((j ^ (lane & 7)) * 16)) = w;
-          }
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint4 w = make_uint4(v[32 * h + 4 * j], v[32 * h + 4 * j + 1], v[32 * h + 4 * j + 2],
+                                         v[32 * h + 4 * j + 3]);
+              *reinterpret_cast<uint4*>(stage0 + h * EPI_BUF + lane * 128 + ((j ^ (lane & 7)) * 16)) = w;
+            }
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         }
         __syncwarp();
         if (lane == 0) {
           if (row0 < args.n && !(args.ablate & 1)) {
-            if (args.overwrite)
-              tma_store_2d(&maps.c, buf, args.c_col0 + col0, row0);
-            else
-              tma_reduce_add_2d(&maps.c, buf, args.c_col0 + col0, row0);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (h == 1 && !second) break;
+              if (args.overwrite)
+                tma_store_2d(&maps.c, stage0 + h * EPI_BUF, args.c_col0 + col0 + 32 * h, row0);
+              else
+                tma_reduce_add_2d(&maps.c, stage0 + h * EPI_BUF, args.c_col0 + col0 + 32 * h, row0);
+            }
           }
           asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         }
-        ++nstore;
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
@@ -606,7 +640,7 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
   const int grid = int(tiles < kNumSMs ? tiles : kNumSMs);
   auto kern = tc::tc_gemm_kernel<K>;
   PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
-  kern<<<grid, tc::THREADS, L::SMEM_ALLOC, stream>>>(maps, args);
+  kern<<<grid, L::THREADS, L::SMEM_ALLOC, stream>>>(maps, args);
   PACO_CUDA_TRY(cudaGetLastError());
   if (c_user)
     PACO_CUDA_TRY(cudaMemcpy2DAsync(c_user, ldc_user * 4, C, ldc * 4, m * 4, n, cudaMemcpyDeviceToDevice, stream));
