@@ -14,7 +14,7 @@ import threading
 
 from .plan import PlanError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpaco_b200.so")
+LIB_PATH = os.environ.get("PACO_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpaco_b200.so")
 
 # semiring ids (include/paco_b200.h)
 SR_INT_I64 = 0

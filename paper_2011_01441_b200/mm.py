@@ -358,3 +358,23 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
         t_end.synchronize()
         report.gpu_ms = t_begin.elapsed_time(t_end)
     return report
+
+
+def measured_weights(devices: list[int], which: int = 0, iters: int = 20000) -> tuple[float, ...]:
+    """Per-GPU throughput weights for ``mm_hetero_partition``.
+
+    Runs the ALU issue-rate probe (``paco_alu_probe``: 0 = VIADDMNMX tropical
+    term, 2 = FFMA) on every device and returns terms/clk/SM x the SM clock it
+    ran at -- power-capped or thermally throttled GPUs get proportionally
+    smaller cuboids.
+    """
+    out = []
+    lib = nat.load()
+    for d in devices:
+        import ctypes
+
+        tpc, mhz = ctypes.c_double(), ctypes.c_double()
+        with torch.cuda.device(d):
+            nat.check(lib.paco_alu_probe(d, None, which, iters, ctypes.byref(tpc), ctypes.byref(mhz)))
+        out.append(tpc.value * mhz.value)
+    return tuple(out)

@@ -317,3 +317,18 @@ def test_fused_and_explicit_folds_agree(fused):
     C = np.zeros((n, m))
     M.mm_execute(M.mm_one_piece_partition(n, m, k, 7), Af, Bf, C, M.SEMIRING_F64, fused_folds=fused)
     np.testing.assert_allclose(C, Af @ Bf, rtol=1e-11, atol=1e-9)
+
+
+def test_hetero_plan_from_measured_weights():
+    """Throughput-weighted one-piece plan (matmul.py:303-339) driven by the live ALU probe."""
+    w = M.measured_weights([0, 0, 0])
+    assert len(w) == 3 and all(x > 0 for x in w)
+    rng = np.random.default_rng(61)
+    n, m, k = 300, 200, 260
+    A = tropical(rng, (n, k), 0, 2**20, 0.1)
+    B = tropical(rng, (k, m), 0, 2**20, 0.1)
+    want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, np.full((n, m), INF, np.int32))
+    for weights in (w, (3.0, 1.0, 1.0), (1.0, 2.0)):
+        C = np.full((n, m), INF, np.int32)
+        M.mm_execute(M.mm_hetero_partition(n, m, k, weights), A, B, C, M.SEMIRING_MINPLUS_SAT, mode="parallel")
+        assert np.array_equal(C, want), weights
