@@ -62,6 +62,8 @@ extern "C" {
                                launches may fold into the same C concurrently (fused k-cut
                                folds of a PACO plan) */
 #define PACO_MM_REMOTE 4    /* C is peer memory (NVLink): fold with element atomics, not TMA */
+#define PACO_MM_PACO_PLAN 8 /* pieces == NULL: CTAs take the balanced PACO plan (paco_plan_cta over
+                               148 x ctas_per_sm x 4 workers) instead of the tile grid (paco_cta_grid) */
 
 /* dtype ids for paco_lincomb */
 #define PACO_DT_F32 0
@@ -72,9 +74,10 @@ extern "C" {
  * C (+)= A (x) B on `device`/`stream`.  A is n x k (lda), B is k x m (ldb),
  * C is n x m (ldc).  `pieces` is an optional HOST array of n_pieces x 6 int32
  * (ti0, tj0, tl0, tn, tm, tk) in the units of paco_mm_tile_shape (C tiles
- * along n and m, k quanta along k): the CTA-level PACO plan, one persistent
- * CTA per piece.  Pass NULL/0 to use paco_plan_cta over 148 x ctas_per_sm
- * workers.  Pieces that split k fold into C with atomics.
+ * along n and m, k quanta along k): an explicit CTA-level plan, one CTA per
+ * piece.  Pass NULL/0 for the default: the tile grid of paco_cta_grid (or,
+ * with PACO_MM_PACO_PLAN, paco_plan_cta's balanced PACO plan).  Pieces that
+ * split k fold into C with the semiring (+) in L2 (TMA bulk reduce).
  */
 int paco_mm(int device, void* stream, int semiring, const void* A, int64_t lda, const void* B,
             int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
@@ -88,7 +91,14 @@ int paco_mm_tile_shape(int semiring, int* bm, int* bn, int* bk, int* ctas_per_sm
  * (i0, j0, l0, n, m, k) into out[p*6], worker order.  Host only. */
 int paco_plan_one_piece(int64_t n, int64_t m, int64_t k, int p, int64_t* out);
 
-/* The CTA-level plan paco_mm builds when pieces == NULL: MM-1-Piece over the
+/* The default CTA-level plan of paco_mm for the SIMT semirings: one CTA per C
+ * tile and k quantum range, the k extent split `*ksplit` ways (CTA idx ->
+ * tile idx / ksplit in row-major tile order, k part idx % ksplit), `*ctas`
+ * CTAs in all.  ksplit minimises ceil(tiles * s / 148) * (k / s + 96): whole
+ * SM-waves of pieces, each charged a fixed per-visit cost.  Host only. */
+int paco_cta_grid(int semiring, int64_t n, int64_t m, int64_t k, int* ksplit, int64_t* ctas);
+
+/* The CTA-level plan paco_mm builds with PACO_MM_PACO_PLAN: MM-1-Piece over the
  * (bm, bn, bk) unit grid of `semiring` for p workers, with nearest-unit cuts
  * and a fall-back to the finest axis when a cut would miss the p-ratio by
  * > 1%.  Writes p rows of (ti0, tj0, tl0, tn, tm, tk) into out[p*6]. Host only. */

@@ -33,6 +33,7 @@ DT_F32, DT_F64, DT_I64 = 0, 1, 2
 MM_OVERWRITE = 1
 MM_ATOMIC = 2
 MM_REMOTE = 4
+MM_PACO_PLAN = 8
 TROPICAL_INF = 1 << 30
 MAX_PIECES = 640
 
@@ -49,6 +50,7 @@ SIGNATURES = {
     "paco_mm_tile_shape": (_int, [_int] + [ctypes.POINTER(_int)] * 4),
     "paco_plan_one_piece": (_int, [_i64, _i64, _i64, _int, ctypes.POINTER(_i64)]),
     "paco_plan_cta": (_int, [_int, _i64, _i64, _i64, _int, ctypes.POINTER(ctypes.c_int32)]),
+    "paco_cta_grid": (_int, [_int, _i64, _i64, _i64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_i64)]),
     "paco_fold": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _i64, _i64, _int]),
     "paco_fill": (_int, [_int, _vp, _int, _vp, _i64, _i64, _i64]),
     "paco_mm_naive": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64]),
@@ -119,6 +121,26 @@ def plan_one_piece(n: int, m: int, k: int, p: int) -> list[tuple[int, ...]]:
     buf = (_i64 * (6 * p))()
     check(load().paco_plan_one_piece(n, m, k, p, buf))
     return [tuple(buf[6 * i:6 * i + 6]) for i in range(p)]
+
+
+def cta_grid(sr: int, n: int, m: int, k: int) -> tuple[int, int]:
+    """(k split, CTA count) of paco_mm's default tile-grid plan."""
+    s, ctas = ctypes.c_int(), _i64()
+    check(load().paco_cta_grid(sr, n, m, k, ctypes.byref(s), ctypes.byref(ctas)))
+    return s.value, ctas.value
+
+
+def grid_pieces(sr: int, n: int, m: int, k: int) -> list[tuple[int, ...]]:
+    """The default tile-grid plan as (ti0, tj0, tl0, tn, tm, tk) rows, CTA order."""
+    bm, bn, kq, _ = tile_shape(sr)
+    s, ctas = cta_grid(sr, n, m, k)
+    tm_, ku = -(-m // bn), -(-k // kq)
+    out = []
+    for idx in range(ctas):
+        tile, part = divmod(idx, s)
+        l0 = part * ku // s
+        out.append((tile // tm_, tile % tm_, l0, 1, 1, (part + 1) * ku // s - l0))
+    return out
 
 
 def plan_cta(sr: int, n: int, m: int, k: int, p: int) -> list[tuple[int, ...]]:

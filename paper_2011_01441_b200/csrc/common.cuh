@@ -21,6 +21,7 @@ struct Piece {
 struct PieceTable {
   int32_t count;
   int32_t ksplit;  // 1 if any piece covers a strict sub-range of k
+  int32_t grid_s;  // count == 0: 0 = PACO plan derived per CTA; s > 0 = tile grid, k split s ways
   Piece p[kMaxPieces];
 };
 

@@ -68,10 +68,14 @@ __host__ __device__ inline UnitBox plan_root(int64_t n, int64_t m, int64_t k, in
 }
 
 // Piece of worker `idx` among p; false if the plan is infeasible on its path.
+//
+// kw scales the virtual k length: 1 is the reference's rule; kw < 1 makes the
+// descent cut the C tile grid before k (a k cut costs the piece a fold of its
+// C block and splits each tile's k loop into more, shorter visits).
 __host__ __device__ inline bool plan_piece(int64_t n, int64_t m, int64_t k, int bm, int bn, int kq,
-                                           int p, int idx, UnitBox& out) {
+                                           int p, int idx, UnitBox& out, double kw = 1.0) {
   UnitBox b = plan_root(n, m, k, bm, bn, kq);
-  double v[3] = {double(n), double(m), double(k)};
+  double v[3] = {double(n), double(m), double(k) * kw};
   int lo = 0, hi = p;
   while (hi - lo > 1) {
     const int cnt = hi - lo, h = cnt / 2;
@@ -89,6 +93,19 @@ __host__ __device__ inline bool plan_piece(int64_t n, int64_t m, int64_t k, int 
   }
   out = b;
   return true;
+}
+
+// Tile-grid plan: piece idx = (C tile idx / s, k part idx % s); the k units
+// split as evenly as possible.
+__host__ __device__ inline void plan_grid_piece(int64_t n, int64_t m, int64_t k, int bm, int bn, int kq,
+                                                int s, int idx, UnitBox& out) {
+  const UnitBox r = plan_root(n, m, k, bm, bn, kq);
+  const int64_t tile = idx / s, part = idx % s;
+  out.o[0] = tile / r.e[1];
+  out.o[1] = tile % r.e[1];
+  out.e[0] = out.e[1] = 1;
+  out.o[2] = part * r.e[2] / s;
+  out.e[2] = (part + 1) * r.e[2] / s - out.o[2];
 }
 
 }  // namespace paco

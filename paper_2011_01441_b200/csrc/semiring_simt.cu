@@ -30,6 +30,9 @@ namespace paco {
 
 // 8192^3 (min,+) with 1/2/3/4/5/8 waves of 296: 37.5/35.2/34.6/34.3/35.1/35.6 ms
 constexpr int kDefaultWaves = 4;
+constexpr double kDefaultKw = 1.0;
+constexpr int kMaxKSplit = 64;
+constexpr double kVisitK = 96.0;  // per-visit cost in k elements
 
 // Device buffer of 10 x (grid size) int64 set by paco_debug_trace(); when
 // non-null every CTA of the next launches records smid and start/end times.
@@ -103,6 +106,7 @@ struct MMArgs {
   long long* trace;  // optional per-CTA [smid, start ns, end ns, stages] (diagnostics)
   int32_t bulk_ok;   // C is 16 B aligned with ldc*sizeof(TC) % 16 == 0: TMA bulk epilogue
   int32_t all_atomic;  // every piece folds atomically (other kernels fold into the same C)
+  double kw;           // virtual k weight of the CTA plan (cta_plan.cuh)
 };
 
 // Stage one (C tile, k tile) of A and B into shared memory.  kVec: 16 B
@@ -380,7 +384,10 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
     pc = table.p[blockIdx.x];
   } else {  // derive this CTA's piece of the default plan (same code as paco_plan_cta)
     UnitBox b;
-    plan_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, int(gridDim.x), int(blockIdx.x), b);
+    if (table.grid_s > 0)
+      plan_grid_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, table.grid_s, int(blockIdx.x), b);
+    else
+      plan_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, int(gridDim.x), int(blockIdx.x), b, args.kw);
     pc = Piece{int32_t(b.o[0]), int32_t(b.o[1]), int32_t(b.o[2]), int32_t(b.e[0]), int32_t(b.e[1]),
                int32_t(b.e[2])};
   }
@@ -513,12 +520,22 @@ bool plan_pieces(int64_t n, int64_t m, int64_t k, int p, std::vector<Box>& out) 
   return one_piece_rec(root, 0, p, double(n), double(m), double(k), out);
 }
 
+// Virtual k weight of the default CTA plan; PACO_CTA_KW overrides it.
+double plan_kw() {
+  static double kw = -1.0;
+  if (kw < 0.0) {
+    const char* e = getenv("PACO_CTA_KW");
+    kw = e ? atof(e) : kDefaultKw;
+  }
+  return kw;
+}
+
 bool plan_pieces_balanced(int64_t n, int64_t m, int64_t k, int bm, int bn, int kq, int p,
                           std::vector<Box>& out) {
   out.assign(p, Box{});
   for (int i = 0; i < p; ++i) {
     UnitBox b;
-    if (!plan_piece(n, m, k, bm, bn, kq, p, i, b)) return false;
+    if (!plan_piece(n, m, k, bm, bn, kq, p, i, b, plan_kw())) return false;
     for (int d = 0; d < 3; ++d) {
       out[i].o[d] = b.o[d];
       out[i].e[d] = b.e[d];
@@ -541,10 +558,42 @@ int default_pieces(int ctas_per_sm) {
 
 // Resolve the CTA plan: an explicit table (pieces != NULL), or the default
 // plan derived on device (t.count = 0).  Returns the grid size in *grid.
+// k split of the default tile-grid plan: whole SM-waves of equal pieces
+// (ceil(tiles*s/148)), each piece k/s of work plus a fixed per-visit cost
+// (ring fill, epilogue, fold) worth kVisitK k elements of MACs.  Measured on B200:
+// lone CTAs run an SM at nearly full ALU rate, so only SM-level waves count.
+// PACO_CTA_KSPLIT overrides s.
+int grid_ksplit(const int64_t units[3], int kq, int64_t* ctas) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("PACO_CTA_KSPLIT");
+    env = e ? atoi(e) : 0;
+  }
+  const int64_t tiles = units[0] * units[1];
+  const int64_t smax = units[2] < kMaxKSplit ? units[2] : kMaxKSplit;
+  int64_t best = 1;
+  if (env > 0) {
+    best = env < smax ? env : smax;
+  } else {
+    double best_cost = 1e300;
+    for (int64_t s = 1; s <= smax; ++s) {
+      const double waves = double((tiles * s + kNumSMs - 1) / kNumSMs);
+      const double cost = waves * (double(units[2] * kq) / double(s) + kVisitK);
+      if (cost < best_cost * (1.0 - 1e-9)) {
+        best_cost = cost;
+        best = s;
+      }
+    }
+  }
+  *ctas = tiles * best;
+  return int(best);
+}
+
 int fill_table(PieceTable& t, int* grid, int64_t n, int64_t m, int64_t k, int bm, int bn, int kq,
-               const int32_t* pieces, int n_pieces, int default_p) {
+               const int32_t* pieces, int n_pieces, int default_p, int flags) {
   const int64_t units[3] = {(n + bm - 1) / bm, (m + bn - 1) / bn, (k + kq - 1) / kq};
   t.ksplit = 0;
+  t.grid_s = 0;
   if (pieces && n_pieces > 0) {
     if (n_pieces > kMaxPieces) {
       set_error("n_pieces=%d exceeds PACO_MAX_PIECES=%d", n_pieces, kMaxPieces);
@@ -564,6 +613,14 @@ int fill_table(PieceTable& t, int* grid, int64_t n, int64_t m, int64_t k, int bm
       t.ksplit |= (q[5] != units[2]);
     }
     *grid = n_pieces;
+    return PACO_OK;
+  }
+  if (!(flags & PACO_MM_PACO_PLAN)) {
+    int64_t ctas = 0;
+    t.count = 0;
+    t.grid_s = grid_ksplit(units, kq, &ctas);
+    t.ksplit = t.grid_s > 1;
+    *grid = int(ctas);
     return PACO_OK;
   }
   // default: the largest feasible p <= default_p, cached per shape
@@ -606,13 +663,13 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
   std::lock_guard<std::mutex> lock(mu);
   int grid = 0;
   int rc = fill_table(table, &grid, n, m, k, Cfg::BM, Cfg::BN, Cfg::KQ, pieces, n_pieces,
-                      default_pieces(Cfg::MIN_BLOCKS));
+                      default_pieces(Cfg::MIN_BLOCKS), flags);
   if (rc) return rc;
   MMArgs args{A, B, C, lda, ldb, ldc, n, m, k, Cfg::KQ, (flags & PACO_MM_OVERWRITE) ? 1 : 0,
               g_trace_buffer,
               (reinterpret_cast<uintptr_t>(C) % 16 == 0 && (ldc * sizeof(typename Op::TC)) % 16 == 0 &&
                !(flags & PACO_MM_REMOTE)) ? 1 : 0,
-              (flags & (PACO_MM_ATOMIC | PACO_MM_REMOTE)) ? 1 : 0};
+              (flags & (PACO_MM_ATOMIC | PACO_MM_REMOTE)) ? 1 : 0, plan_kw()};
   if (args.overwrite && (flags & (PACO_MM_ATOMIC | PACO_MM_REMOTE))) {
     set_error("PACO_MM_OVERWRITE cannot be combined with atomic / remote folding");
     return PACO_ERR_ARG;
@@ -680,6 +737,20 @@ extern "C" int paco_plan_one_piece(int64_t n, int64_t m, int64_t k, int p, int64
       out[6 * i + d] = boxes[i].o[d];
       out[6 * i + 3 + d] = boxes[i].e[d];
     }
+  return PACO_OK;
+}
+
+extern "C" int paco_cta_grid(int semiring, int64_t n, int64_t m, int64_t k, int* ksplit, int64_t* ctas) {
+  using namespace paco;
+  int bm, bn, kq, cps;
+  int rc = paco_mm_tile_shape(semiring, &bm, &bn, &kq, &cps);
+  if (rc) return rc;
+  if (n < 1 || m < 1 || k < 1 || !ksplit || !ctas) {
+    set_error("paco_cta_grid: need extents >= 1 and output pointers");
+    return PACO_ERR_ARG;
+  }
+  const int64_t units[3] = {(n + bm - 1) / bm, (m + bn - 1) / bn, (k + kq - 1) / kq};
+  *ksplit = grid_ksplit(units, kq, ctas);
   return PACO_OK;
 }
 

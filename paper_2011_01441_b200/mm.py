@@ -98,7 +98,11 @@ def mm_seq(A, B, C, semiring: Semiring = SEMIRING_INT, base: int = DEFAULT_BASE,
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         if pieces is None and _pinned_host(A, in_dt) and _pinned_host(B, in_dt) \
                 and _pinned_host(C, semiring.dtype) and n >= 2 * _PIPE_MIN_ROWS:
-            _pipelined_host_mm(A, B, C, kid, semiring, dev, st, overwrite)
+            mode = _PIPE_MODE or ("k" if k >= 4 * _PIPE_MIN_K else "grid")
+            if mode == "k":
+                _kphased_host_mm(A, B, C, kid, dev, st, overwrite)
+            else:
+                _pipelined_host_mm(A, B, C, kid, semiring, dev, st, overwrite)
             return
         with torch.cuda.stream(st):
             a = View.of(stage_in(A, in_dt, dev))
@@ -110,6 +114,11 @@ def mm_seq(A, B, C, semiring: Semiring = SEMIRING_INT, base: int = DEFAULT_BASE,
 
 _PIPE_MIN_ROWS = 512
 _PIPE_GRID = tuple(int(x) for x in os.environ.get("PACO_PIPE_GRID", "4,2").split(","))  # measured best of 4x4/8x1/4x2/2x4/8x2 for 8192^3
+_PIPE_MODE = os.environ.get("PACO_PIPE_MODE", "")          # "k" | "grid" | "" (auto)
+_PIPE_MIN_K = 512
+# k-phased schedule: first k chunk, growth factor, chunk cap, share of k in the
+# row-blocked last phase, and its number of row blocks
+_KP = tuple(float(x) for x in os.environ.get("PACO_PIPE_KP", "256,2,2048,0.25,8").split(","))
 
 
 def _pinned_host(x, dtype) -> bool:
@@ -187,6 +196,90 @@ def _pipelined_host_mm(A, B, C, kid: int, semiring: Semiring, dev: int, st, over
         done.record(st)
         d2h.wait_event(done)
         _copy2d(d2h, C, r0, c0, c_d, r0, c0, r1 - r0, c1 - c0)
+    st.wait_stream(d2h)
+    d2h.synchronize()
+
+
+def _kphased_edges(k: int) -> tuple[list[int], int]:
+    """k-chunk edges of the front phase (geometric growth from a small first
+    chunk, capped) and the start of the row-blocked last phase."""
+    first, growth, cap, share, _ = _KP
+    align = 128
+    last = min(k - align, max(align, -(-int(k * share) // align) * align))
+    front = k - last
+    edges, pos, w = [0], 0, int(first)
+    while pos < front:
+        step = min(max(align, (w // align) * align), int(cap), front - pos)
+        if front - pos - step < max(align, step // 2):
+            step = front - pos
+        pos += step
+        edges.append(pos)
+        w = int(w * growth)
+    return edges, front
+
+
+def _kphased_host_mm(A, B, C, kid: int, dev: int, st, overwrite: bool) -> None:
+    """Host (pinned) operands with a long k: overlap H2D, compute and D2H by
+    cutting k first, rows last.
+
+    Front phase: k chunks [l0, l1) of geometrically growing width; the H2D
+    stream uploads A[:, l0:l1] and B[l0:l1, :] and the compute stream runs the
+    whole C (+)= A[:, l0:l1] (x) B[l0:l1, :] as soon as they land (the first
+    chunk overwrites; C's upload queues behind every chunk's, hidden by the
+    front phase's compute, and is folded in with one (+) pass).  Last phase: the final k chunk row block by
+    row block, each block's rows of C returned by the D2H stream while the next
+    block computes.  So only the small first chunk's upload and the last row
+    block's download are exposed, versus a whole A row block + B column block
+    + C block for the 2-D grid (``_pipelined_host_mm``).  The semiring's (+)
+    is associative and commutative, so the result is the one-shot product
+    (integer/tropical bit-identical; float within its summation tolerance).
+    """
+    n, k = tuple(A.shape)
+    m = B.shape[1]
+    edges, front = _kphased_edges(k)
+    R = max(1, min(int(_KP[4]), n // _PIPE_MIN_ROWS))
+    redges = [((n * i // R) // 128) * 128 for i in range(R)] + [n]
+    h2d = torch.cuda.Stream(device=dev)
+    d2h = torch.cuda.Stream(device=dev)
+    h2d.wait_stream(st)
+    a_d = torch.empty((n, k), dtype=A.dtype, device=dev)
+    b_d = torch.empty((k, m), dtype=B.dtype, device=dev)
+    c_d = torch.empty((n, m), dtype=C.dtype, device=dev)
+    c_in = None if overwrite else torch.empty((n, m), dtype=C.dtype, device=dev)
+    for t in (a_d, b_d, c_d, c_in):
+        if t is not None:
+            t.record_stream(h2d)
+            t.record_stream(d2h)
+    av, bv, cv = View.of(a_d), View.of(b_d), View.of(c_d)
+    spans = list(zip(edges[:-1], edges[1:])) + [(front, k)]
+    landed, c_landed = [], None
+    for idx, (l0, l1) in enumerate(spans):
+        _copy2d(h2d, a_d, 0, l0, A, 0, l0, n, l1 - l0)
+        _copy2d(h2d, b_d, l0, 0, B, l0, 0, l1 - l0, m)
+        ev = torch.cuda.Event()
+        ev.record(h2d)
+        landed.append(ev)
+        if c_in is not None and idx == len(spans) - 1:
+            _copy2d(h2d, c_in, 0, 0, C, 0, 0, n, m)
+            c_landed = torch.cuda.Event()
+            c_landed.record(h2d)
+    for idx, (l0, l1) in enumerate(spans[:-1]):
+        st.wait_event(landed[idx])
+        launch_mm(kid, st, av.sub(0, l0, n, l1 - l0), bv.sub(l0, 0, l1 - l0, m), cv, overwrite=idx == 0)
+    if c_landed is not None:
+        st.wait_event(c_landed)
+        launch_fold(kid, st, cv, View.of(c_in), reset=False)
+    st.wait_event(landed[-1])
+    for i in range(R):
+        r0, r1 = redges[i], redges[i + 1]
+        if r1 <= r0:
+            continue
+        launch_mm(kid, st, av.sub(r0, front, r1 - r0, k - front), bv.sub(front, 0, k - front, m),
+                  cv.sub(r0, 0, r1 - r0, m))
+        done = torch.cuda.Event()
+        done.record(st)
+        d2h.wait_event(done)
+        _copy2d(d2h, C, r0, 0, c_d, r0, 0, r1 - r0, m)
     st.wait_stream(d2h)
     d2h.synchronize()
 

@@ -14,6 +14,8 @@ import torch
 from oracle import cref
 from paper_2011_01441_b200 import _native as nat
 from paper_2011_01441_b200 import matmul as M
+from paper_2011_01441_b200.device import View
+from paper_2011_01441_b200.mm import launch_mm
 
 pytestmark = pytest.mark.gpu
 
@@ -252,24 +254,28 @@ def test_paco_plans_every_p_minplus_i64():
             assert np.array_equal(C, want), (p, plan.meta["variant"])
 
 
-def test_device_derived_cta_plan_matches_host_plan():
-    """Each CTA derives its piece on device; it must equal paco_plan_cta's."""
+@pytest.mark.parametrize("paco_plan", [False, True])
+def test_device_derived_cta_plan_matches_host_plan(paco_plan):
+    """Each CTA derives its piece on device; it must equal the host's plan
+    (tile grid: paco_cta_grid; PACO_MM_PACO_PLAN: paco_plan_cta)."""
     lib = nat.load()
     rng = np.random.default_rng(31)
-    for (n, m, k) in [(1000, 700, 900), (300, 4000, 129), (2048, 2048, 2048)]:
+    for (n, m, k) in [(1000, 700, 900), (300, 4000, 129), (2048, 2048, 2048), (200, 150, 3000)]:
         A = torch.from_numpy(tropical(rng, (n, k), 0, 2**20)).cuda()
         B = torch.from_numpy(tropical(rng, (k, m), 0, 2**20)).cuda()
         C = torch.full((n, m), INF, dtype=torch.int32, device="cuda")
-        tr = torch.zeros(10 * 4096, dtype=torch.int64, device="cuda")
+        tr = torch.zeros(10 * 8192, dtype=torch.int64, device="cuda")
         nat.check(lib.paco_debug_trace(tr.data_ptr()))
         try:
-            M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)
+            launch_mm(nat.SR_MINPLUS_SAT32, torch.cuda.current_stream(), View.of(A), View.of(B), View.of(C),
+                        flags=nat.MM_PACO_PLAN if paco_plan else 0)
             torch.cuda.synchronize()
         finally:
             nat.check(lib.paco_debug_trace(None))
         t = tr.view(-1, 10).cpu().numpy()
         t = t[t[:, 2] > 0]
-        host = nat.plan_cta(nat.SR_MINPLUS_SAT32, n, m, k, len(t))
+        host = (nat.plan_cta(nat.SR_MINPLUS_SAT32, n, m, k, len(t)) if paco_plan
+                else nat.grid_pieces(nat.SR_MINPLUS_SAT32, n, m, k))
         assert [tuple(r) for r in t[:, 4:10]] == [tuple(h) for h in host]
         want = cref.mm(cref.SR_MINPLUS_SAT32, A.cpu().numpy(), B.cpu().numpy(), np.full((n, m), INF, np.int32))
         assert np.array_equal(C.cpu().numpy(), want)
@@ -290,6 +296,53 @@ def test_pinned_host_pipeline_matches_oracle():
     M.mm_seq(A, B, C2, M.SEMIRING_MINPLUS_SAT, overwrite=True)
     want2 = cref.mm(cref.SR_MINPLUS_SAT32, A.numpy(), B.numpy(), np.full((n, m), INF, np.int32))
     assert np.array_equal(C2.numpy(), want2)
+
+
+@pytest.mark.parametrize("sr", ["minplus", "maxplus", "int", "f32", "bf16"])
+@pytest.mark.parametrize("overwrite", [False, True])
+def test_pinned_k_phased_pipeline(sr, overwrite):
+    """Long-k pinned operands take the k-first / rows-last pipeline; same C as the oracle."""
+    from paper_2011_01441_b200 import mm as MMmod
+    rng = np.random.default_rng(43)
+    n, m, k = 1100, 650, 2600
+    assert MMmod._kphased_edges(k)[1] < k
+    if sr in ("minplus", "maxplus"):
+        lo, hi = (0, 2**20) if sr == "minplus" else (-2**20, 2**20)
+        A = tropical(rng, (n, k), lo, hi, 0.1 if sr == "minplus" else 0.0)
+        B = tropical(rng, (k, m), lo, hi, 0.1 if sr == "minplus" else 0.0)
+        C0 = tropical(rng, (n, m), lo, 2**21, 0.3 if sr == "minplus" else 0.0)
+        sem, cid = ((M.SEMIRING_MINPLUS_SAT, cref.SR_MINPLUS_SAT32) if sr == "minplus"
+                    else (M.SEMIRING_MAXPLUS, cref.SR_MAXPLUS_SAT32))
+        zero = INF if sr == "minplus" else -INF
+    elif sr == "int":
+        A = rng.integers(-50, 50, (n, k)).astype(np.int64)
+        B = rng.integers(-50, 50, (k, m)).astype(np.int64)
+        C0 = rng.integers(-1000, 1000, (n, m)).astype(np.int64)
+        sem, cid, zero = M.SEMIRING_INT, cref.SR_INT_I64, 0
+    else:
+        A = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+        B = rng.uniform(-1, 1, (k, m)).astype(np.float32)
+        if sr == "bf16":
+            A = torch.from_numpy(A).to(torch.bfloat16).float().numpy()
+            B = torch.from_numpy(B).to(torch.bfloat16).float().numpy()
+        C0 = rng.uniform(-1, 1, (n, m)).astype(np.float32)
+        sem, zero = (M.SEMIRING_F32 if sr == "f32" else M.SEMIRING_BF16), 0.0
+    if overwrite:
+        C0 = np.full((n, m), zero, C0.dtype)
+    Ah, Bh = torch.from_numpy(A), torch.from_numpy(B)
+    if sr == "bf16":
+        Ah, Bh = Ah.to(torch.bfloat16), Bh.to(torch.bfloat16)
+    Ah, Bh = Ah.pin_memory(), Bh.pin_memory()
+    C = torch.full(C0.shape, 7, dtype=torch.from_numpy(C0).dtype).pin_memory() if overwrite \
+        else torch.from_numpy(C0.copy()).pin_memory()
+    M.mm_seq(Ah, Bh, C, sem, overwrite=overwrite)
+    if sr in ("f32", "bf16"):
+        want = C0.astype(np.float64) + A.astype(np.float64) @ B.astype(np.float64)
+        err = np.linalg.norm(C.numpy() - want) / np.linalg.norm(want)
+        assert err <= (1e-5 if sr == "f32" else 1e-5), err   # exact-bf16 inputs, f32 accumulation
+    else:
+        want = cref.mm(cid, A, B, C0.copy())
+        assert np.array_equal(C.numpy(), want)
 
 
 @pytest.mark.parametrize("fused", [True, False])

@@ -233,3 +233,18 @@ def test_cta_plan_balance_and_cover():
     for a, b, c, dn, dm, dk in small:
         cover[a:a + dn, b:b + dm, c:c + dk] += 1
     assert (cover == 1).all()
+
+
+def test_cta_grid_plan_tiles_iteration_space_once():
+    """Default tile-grid plan: every (C tile, k quantum) cell covered exactly once."""
+    for sr in (nat.SR_MINPLUS_SAT32, nat.SR_INT_I64):
+        bm, bn, kq, _ = nat.tile_shape(sr)
+        for (n, m, k) in [(300, 260, 515), (1000, 700, 9000), (129, 4000, 64), (1, 1, 1), (200, 150, 3000)]:
+            s, ctas = nat.cta_grid(sr, n, m, k)
+            units = (-(-n // bm), -(-m // bn), -(-k // kq))
+            assert ctas == units[0] * units[1] * s and 1 <= s <= units[2]
+            cover = np.zeros(units, np.int32)
+            for a, b, c, dn, dm, dk in nat.grid_pieces(sr, n, m, k):
+                assert dk >= 1
+                cover[a:a + dn, b:b + dm, c:c + dk] += 1
+            assert (cover == 1).all()

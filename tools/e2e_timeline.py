@@ -14,14 +14,16 @@ for _ in range(2):
     M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)
 # instrument: monkeypatch launch_mm and _copy2d to record events
 rec = []
-orig_launch, orig_copy = MM.launch_mm, MM._copy2d
+orig_launch, orig_copy, orig_fold = MM.launch_mm, MM._copy2d, MM.launch_fold
 def ev(stream):
     e = torch.cuda.Event(enable_timing=True); e.record(stream); return e
 def launch(kid, st, a, b, c, **kw):
-    e0 = ev(st); orig_launch(kid, st, a, b, c, **kw); rec.append(("kernel %dx%d" % (c.rows, c.cols), e0, ev(st)))
+    e0 = ev(st); orig_launch(kid, st, a, b, c, **kw); rec.append(("kernel %dx%dx%d" % (c.rows, c.cols, a.cols), e0, ev(st)))
 def copy(st, dst, *args):
     e0 = ev(st); orig_copy(st, dst, *args); rec.append(("%s %dx%d" % ("H2D" if dst.is_cuda else "D2H", args[-2], args[-1]), e0, ev(st)))
-MM.launch_mm, MM._copy2d = launch, copy
+def fold(kid, st, dst, src, reset):
+    e0 = ev(st); orig_fold(kid, st, dst, src, reset); rec.append(("fold", e0, ev(st)))
+MM.launch_mm, MM._copy2d, MM.launch_fold = launch, copy, fold
 start = ev(torch.cuda.current_stream())
 M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)
 end = ev(torch.cuda.current_stream()); end.synchronize()
