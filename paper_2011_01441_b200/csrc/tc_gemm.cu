@@ -18,10 +18,11 @@
 // CTA on one B column block.
 //
 // 3xTF32: every fp32 operand x is split (by split_tf32_kernel) into
-// hi = x with the low 13 mantissa bits cleared (exactly representable in tf32)
-// and lo = x - hi (exact in fp32); C += Ahi*Bhi + Ahi*Blo + Alo*Bhi with
-// kind::tf32 MMAs accumulating in fp32 TMEM -- ~fp32 accuracy (the dropped
-// Alo*Blo term is < 2^-20 relative) at tensor-core rate.  The split writes B
+// hi = tf32_rn(x) and lo = tf32_rn(x - hi) (|x - hi - lo| <= 2^-22 |x|; a
+// truncated split leaves lo's low bits to the MMA's truncation: 20x the
+// error); C += Ahi*Bhi + Ahi*Blo + Alo*Bhi with kind::tf32 MMAs accumulating
+// in fp32 TMEM -- ~fp32 accuracy (the dropped Alo*Blo term is < 2^-22
+// relative) at tensor-core rate.  The split writes B
 // transposed (K-major): kind::tf32 with an MN-major B descriptor returned
 // zeros on this toolchain/hardware, K-major both sides is exact.
 #include <cuda.h>
@@ -454,28 +455,34 @@ int make_map(CUtensorMap* map, CUtensorMapDataType dt, int elsize, const void* p
   return PACO_OK;
 }
 
-// Per-device scratch for operands whose row pitch is not a multiple of 16 B
-// (TMA needs it): they are repacked with a padded pitch.  Grown on demand.
+// Scratch for split / repacked operands: stream-ordered allocations from the
+// device's default memory pool (kept cached: release threshold = max), freed
+// on the launch stream after the kernel.  Concurrent launches on different
+// streams (mm_execute workers, Strassen leaves) each get their own buffers.
 struct Scratch {
-  void* ptr = nullptr;
-  size_t bytes = 0;
-};
-std::mutex g_scratch_mu;
-Scratch g_scratch[64][8];
-
-int scratch(int device, int slot, size_t bytes, cudaStream_t st, void** out) {
-  std::lock_guard<std::mutex> lock(g_scratch_mu);
-  Scratch& w = g_scratch[device & 63][slot];
-  if (w.bytes < bytes) {
-    if (w.ptr) {
-      PACO_CUDA_TRY(cudaStreamSynchronize(st));
-      PACO_CUDA_TRY(cudaFree(w.ptr));
-      w = Scratch{};
-    }
-    PACO_CUDA_TRY(cudaMalloc(&w.ptr, bytes));
-    w.bytes = bytes;
+  cudaStream_t st = nullptr;
+  std::vector<void*> bufs;
+  ~Scratch() {
+    for (void* p : bufs) cudaFreeAsync(p, st);
   }
-  *out = w.ptr;
+};
+
+int scratch(int device, Scratch& sc, size_t bytes, cudaStream_t st, void** out) {
+  static std::mutex mu;
+  static bool pool_ready[64] = {};
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pool_ready[device & 63]) {
+      cudaMemPool_t pool;
+      PACO_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = UINT64_MAX;
+      PACO_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+      pool_ready[device & 63] = true;
+    }
+  }
+  sc.st = st;
+  PACO_CUDA_TRY(cudaMallocAsync(out, bytes, st));
+  sc.bufs.push_back(*out);
   return PACO_OK;
 }
 
@@ -485,9 +492,15 @@ bool pitch_ok(const void* p, int64_t ld, int elsize) {
 }  // namespace
 
 namespace tc {
-// x -> (hi, lo) with hi = x & ~0x1FFF (a tf32 value), lo = x - hi (exact).
-// Packed outputs with a 16-byte row pitch `ldo`; kT writes them transposed
+// x -> (hi, lo) = (tf32_rn(x), tf32_rn(x - hi)).  Packed outputs with a 16-byte row pitch `ldo`; kT writes them transposed
 // (cols x rows) through a 32x32 smem tile so both sides stay coalesced.
+// Round to the nearest tf32 (10 mantissa bits; the result's low 13 bits are 0).
+__device__ __forceinline__ float round_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 template <bool kT>
 __global__ void split_tf32_kernel(const float* __restrict__ x, int64_t ldx, float* __restrict__ hi,
                                   float* __restrict__ lo, int64_t ldo, int64_t rows, int64_t cols) {
@@ -496,15 +509,16 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, int64_t ldx, floa
   for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
     const int64_t i = r0 + dy, j = c0 + threadIdx.x;
     float v = (i < rows && j < cols) ? x[i * ldx + j] : 0.f;
-    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    const float h = round_tf32(v);
+    const float l = round_tf32(v - h);  // the MMA would truncate an unrounded lo
     if (!kT) {
       if (i < rows && j < cols) {
         hi[i * ldo + j] = h;
-        lo[i * ldo + j] = v - h;
+        lo[i * ldo + j] = l;
       }
     } else {
       th[dy][threadIdx.x] = h;
-      tl[dy][threadIdx.x] = v - h;
+      tl[dy][threadIdx.x] = l;
     }
   }
   if (kT) {
@@ -522,12 +536,12 @@ __global__ void split_tf32_kernel(const float* __restrict__ x, int64_t ldx, floa
 
 namespace {
 // Repack an operand whose row pitch TMA cannot take into padded scratch.
-int repack(int device, int slot, const void** p, int64_t* ld, int64_t rows, int64_t cols, int elsize,
+int repack(int device, Scratch& sc, const void** p, int64_t* ld, int64_t rows, int64_t cols, int elsize,
            cudaStream_t st) {
   if (pitch_ok(*p, *ld, elsize)) return PACO_OK;
   const int64_t q = 16 / elsize, ld2 = (cols + q - 1) / q * q;
   void* dst;
-  int rc = scratch(device, slot, size_t(rows) * ld2 * elsize, st, &dst);
+  int rc = scratch(device, sc, size_t(rows) * ld2 * elsize, st, &dst);
   if (rc) return rc;
   PACO_CUDA_TRY(cudaMemcpy2DAsync(dst, ld2 * elsize, *p, *ld * elsize, cols * elsize, rows,
                                   cudaMemcpyDeviceToDevice, st));
@@ -536,16 +550,16 @@ int repack(int device, int slot, const void** p, int64_t* ld, int64_t rows, int6
   return PACO_OK;
 }
 
-// fp32 operand -> packed hi/lo tf32 pair in scratch slots (slot, slot+1);
+// fp32 operand -> packed hi/lo tf32 pair in scratch;
 // `transpose` stores them as (cols x rows), i.e. K-major for a B operand.
-int split_operand(int device, int slot, const void* x, int64_t ldx, int64_t rows, int64_t cols,
+int split_operand(int device, Scratch& sc, const void* x, int64_t ldx, int64_t rows, int64_t cols,
                   bool transpose, cudaStream_t st, const void** hi, const void** lo, int64_t* ld) {
   const int64_t orows = transpose ? cols : rows, ocols = transpose ? rows : cols;
   const int64_t ld2 = (ocols + 3) / 4 * 4;
   void *h, *l;
-  int rc = scratch(device, slot, size_t(orows) * ld2 * 4, st, &h);
+  int rc = scratch(device, sc, size_t(orows) * ld2 * 4, st, &h);
   if (rc) return rc;
-  if ((rc = scratch(device, slot + 1, size_t(orows) * ld2 * 4, st, &l))) return rc;
+  if ((rc = scratch(device, sc, size_t(orows) * ld2 * 4, st, &l))) return rc;
   dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32)), block(32, 8);
   if (transpose)
     tc::split_tf32_kernel<true><<<grid, block, 0, st>>>(static_cast<const float*>(x), ldx, static_cast<float*>(h),
@@ -584,20 +598,21 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
     return PACO_ERR_ARG;
   }
   int rc;
+  Scratch sc;  // freed (stream-ordered) when this call returns
   tc::TcMaps maps;
   int32_t a_off = 0, b_off = 0, c_off = 0, t_off = 0;
   if constexpr (K::NOPS == 1) {
     // bf16: operands with a row pitch TMA cannot take are repacked first
-    if ((rc = repack(device, 0, &A, &lda, n, k, K::ELEM, stream))) return rc;
-    if ((rc = repack(device, 1, &B, &ldb, k, m, K::ELEM, stream))) return rc;
+    if ((rc = repack(device, sc, &A, &lda, n, k, K::ELEM, stream))) return rc;
+    if ((rc = repack(device, sc, &B, &ldb, k, m, K::ELEM, stream))) return rc;
     if ((rc = make_map(&maps.a[0], K::DT, K::ELEM, A, n, k, lda, K::BK, tc::BM, &a_off))) return rc;
     if ((rc = make_map(&maps.b[0], K::DT, K::ELEM, B, k, m, ldb, L::BOX_N, K::BK, &b_off))) return rc;
   } else {
-    // 3xTF32: split both operands into packed hi/lo pairs (scratch slots 3..6)
+    // 3xTF32: split both operands into packed hi/lo pairs
     const void *ah, *al, *bh, *bl;
     int64_t lda2, ldb2;
-    if ((rc = split_operand(device, 3, A, lda, n, k, false, stream, &ah, &al, &lda2))) return rc;
-    if ((rc = split_operand(device, 5, B, ldb, k, m, K::B_KMAJOR, stream, &bh, &bl, &ldb2))) return rc;
+    if ((rc = split_operand(device, sc, A, lda, n, k, false, stream, &ah, &al, &lda2))) return rc;
+    if ((rc = split_operand(device, sc, B, ldb, k, m, K::B_KMAJOR, stream, &bh, &bl, &ldb2))) return rc;
     if ((rc = make_map(&maps.a[0], K::DT, K::ELEM, ah, n, k, lda2, K::BK, tc::BM, &a_off))) return rc;
     if ((rc = make_map(&maps.a[1], K::DT, K::ELEM, al, n, k, lda2, K::BK, tc::BM, &t_off))) return rc;
     if constexpr (K::B_KMAJOR) {
@@ -613,7 +628,7 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
   if (!pitch_ok(C, ldc, 4)) {
     const int64_t ld2 = (m + 3) / 4 * 4;
     void* p;
-    if ((rc = scratch(device, 2, size_t(n) * ld2 * 4, stream, &p))) return rc;
+    if ((rc = scratch(device, sc, size_t(n) * ld2 * 4, stream, &p))) return rc;
     if (!(flags & PACO_MM_OVERWRITE))
       PACO_CUDA_TRY(cudaMemcpy2DAsync(p, ld2 * 4, C, ldc * 4, m * 4, n, cudaMemcpyDeviceToDevice, stream));
     c_user = C;

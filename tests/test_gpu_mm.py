@@ -385,3 +385,30 @@ def test_hetero_plan_from_measured_weights():
         C = np.full((n, m), INF, np.int32)
         M.mm_execute(M.mm_hetero_partition(n, m, k, weights), A, B, C, M.SEMIRING_MINPLUS_SAT, mode="parallel")
         assert np.array_equal(C, want), weights
+
+
+@pytest.mark.parametrize("sr", ["f32", "bf16"])
+def test_tensor_core_plans_on_concurrent_streams(sr):
+    """Plan workers launch the tcgen05 kernels concurrently on their own streams;
+    each launch's split/repack scratch is its own (regression: a shared
+    per-device scratch raced under mode='parallel')."""
+    rng = np.random.default_rng(77)
+    n, m, k = 200, 150, 300
+    A = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    B = rng.uniform(-1, 1, (k, m)).astype(np.float32)
+    if sr == "bf16":
+        a = torch.from_numpy(A).cuda().to(torch.bfloat16)
+        b = torch.from_numpy(B).cuda().to(torch.bfloat16)
+        A, B = a.float().cpu().numpy(), b.float().cpu().numpy()
+        sem = M.SEMIRING_BF16
+    else:
+        a, b = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        sem = M.SEMIRING_F32
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    for p in (3, 5, 7):
+        for plan in (M.mm_paco_partition(n, m, k, p, base=16), M.mm_one_piece_partition(n, m, k, p)):
+            for _ in range(3):
+                C = torch.zeros((n, m), device="cuda")
+                M.mm_execute(plan, a, b, C, sem, mode="parallel")
+                got = C.cpu().numpy().astype(np.float64)
+                assert np.linalg.norm(got - ref) <= 1e-5 * np.linalg.norm(ref), (p, plan.meta["variant"])
