@@ -25,6 +25,9 @@ struct PieceTable {
   Piece p[kMaxPieces];
 };
 
+// paco_debug_trace()'s device buffer (diagnostics; null when off)
+extern long long* g_trace_buffer;
+
 // thread-local error text behind paco_last_error()
 void set_error(const char* fmt, ...);
 

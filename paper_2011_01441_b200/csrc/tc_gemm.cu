@@ -3,19 +3,18 @@
 //
 // Replaces SEMIRING_F64.block_mm / _int_block (matmul.py:45-46,54) for the
 // dense floating-point case.  One persistent CTA per SM, warp-specialised:
-//   warp 0      TMA producer: A tile [128 x 64] (K-major) and B tile
-//               [64 x 256] (N-major, as the caller stores it) per k block,
-//               128B-swizzled, into a 3-stage smem ring;
+//   warp 0      TMA producer: claims tiles from a global counter (dynamic
+//               schedule, see claim_tile) and loads A tiles [128 x 64]
+//               (K-major) and B tiles [64 x 256] (N-major, as the caller
+//               stores it), 128B-swizzled, into a smem ring; with K <= 256
+//               (cfg3) the CTA's whole B column block stays resident and only
+//               A streams;
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma.kind::f16
 //               (M=128, N=256, K=16) into a double-buffered TMEM accumulator
 //               (2 x 256 fp32 columns) and commits to mbarriers;
-//   warps 2..   epilogue: tcgen05.ld 32x32b.x32 -> registers -> swizzled smem
+//   warps 2..   epilogue: tcgen05.ld 32x32b.x64 -> registers -> swizzled smem
 //               staging -> TMA tensor store (C = AB) or TMA reduce-add
 //               (C += AB), overlapping the next tile's MMAs.
-// The CTA-level plan is the 1-D MM-1-Piece split of the column-block-major
-// tile sequence over the 148 CTAs (floor(p/2):ceil(p/2) halving of a 1-D
-// range == contiguous ranges of floor/ceil(T/p) tiles), which keeps each
-// CTA on one B column block.
 //
 // 3xTF32: every fp32 operand x is split (by split_tf32_kernel) into
 // hi = tf32_rn(x) and lo = tf32_rn(x - hi) (|x - hi - lo| <= 2^-22 |x|; a
@@ -40,31 +39,49 @@ namespace paco {
 
 namespace tc {
 
+#define PACO_TC_ARGS(...) __VA_ARGS__
 constexpr int BM = 128;
 // warp 0: TMA producer, warp 1: MMA issuer, warps 2..: epilogue (Kind::EPI_WARPS)
-constexpr int EPI_BUF = 32 * 32 * 4;        // 4 KB: 32 rows x 32 fp32 (128 B)
 
-// bf16 inputs, one MMA pass; N=256 tiles, 64-deep k blocks (128 B rows).
-struct KindBF16 {
-  static constexpr int BN = 256, BK = 64, UMMA_K = 16, STAGES = 3, ELEM = 2, NOPS = 1, PASSES = 1;
-  // 3 stages of 48 KB; 8 epilogue warps (2 per TMEM lane quadrant, half the
-  // columns each): the epilogue -- not the MMAs -- bounds this HBM-bound kernel
-  static constexpr int RING_BYTES = 160 * 1024, EPI_WARPS = 8;
-  static constexpr bool B_KMAJOR = false;
+// bf16 inputs, one MMA pass; N=256 tiles, 64-deep k blocks (128 B rows);
+// ST stages of 48 KB, EW epilogue warps (EW = 8: 2 per TMEM lane quadrant,
+// half the columns each) with EB staging buffers each.
+template <int ST, int EB, int EW, int EC = 32>
+struct KindBF16T {
+  static constexpr int BN = 256, BK = 64, UMMA_K = 16, STAGES = ST, ELEM = 2, NOPS = 1, PASSES = 1;
+  static constexpr int RING_BYTES = ST * 48 * 1024, EPI_WARPS = EW, EPI_BUFS = EB, KB_MAX = 0, EPI_COLS = EC;
+  static constexpr bool B_KMAJOR = false, B_RES = false;
   // F32 accumulate, BF16 A/B (format 1), A K-major, B MN-major (bit 16)
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
   static constexpr CUtensorMapDataType DT = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
 };
+using KindBF16 = KindBF16T<3, 2, 8>;
 // fp32 inputs as 3xTF32 (hi/lo operand tiles), N=128 tiles, 32-deep k blocks.
 struct KindTF32x3 {
   static constexpr int BN = 128, BK = 32, UMMA_K = 8, STAGES = 3, ELEM = 4, NOPS = 2, PASSES = 3;
-  static constexpr int RING_BYTES = 3 * 64 * 1024, EPI_WARPS = 4;
-  static constexpr bool B_KMAJOR = true;  // B^T tiles (the split writes B transposed)
+  static constexpr int RING_BYTES = 3 * 64 * 1024, EPI_WARPS = 4, EPI_BUFS = 2, KB_MAX = 0, EPI_COLS = 32;
+  static constexpr bool B_KMAJOR = true, B_RES = false;  // B^T tiles (the split writes B transposed)
   // F32 accumulate, TF32 A/B (format 2), both K-major
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
   static constexpr CUtensorMapDataType DT = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+};
+
+// bf16 with K <= KB_MAX * BK: the CTA's whole B column block (K x 256, 128 KB)
+// stays resident in shared memory across its consecutive tiles of that block,
+// so per tile only A (64 KB) is loaded -- the streaming kind re-reads B's
+// 128 KB from L2 for every 128 KB of C it writes, which puts cfg3 on the L2
+// throughput cap instead of HBM.  A ring of AST stages, EB staging buffers
+// per epilogue warp.
+template <int AST, int EB, int EW = 8, int EC = 32>
+struct KindBF16Res {
+  static constexpr int BN = 256, BK = 64, UMMA_K = 16, STAGES = AST, ELEM = 2, NOPS = 1, PASSES = 1;
+  static constexpr int KB_MAX = 4, EPI_WARPS = EW, EPI_BUFS = EB, EPI_COLS = EC;
+  static constexpr int RING_BYTES = KB_MAX * BN * BK * 2 + AST * 128 * BK * 2;
+  static constexpr bool B_KMAJOR = false, B_RES = true;
+  static constexpr uint32_t IDESC = KindBF16::IDESC;
+  static constexpr CUtensorMapDataType DT = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
 };
 
 template <class K>
@@ -72,16 +89,19 @@ struct Layout {
   static constexpr int BOX_N = 128 / K::ELEM;                 // elements per 128 B row
   static constexpr int A_BYTES = BM * K::BK * K::ELEM;        // one operand tile
   static constexpr int B_BYTES = K::BN * K::BK * K::ELEM;
-  static constexpr int STAGE_BYTES = K::NOPS * (A_BYTES + B_BYTES);
+  static constexpr int B_REGION = K::KB_MAX * B_BYTES;         // resident B (B_RES kinds)
+  static constexpr int STAGE_BYTES = K::B_RES ? A_BYTES : K::NOPS * (A_BYTES + B_BYTES);
   static constexpr int SMEM_EPI = K::RING_BYTES;
-  static constexpr int SMEM_BAR = SMEM_EPI + K::EPI_WARPS * 2 * EPI_BUF;
+  static constexpr int EPI_BUF = 32 * K::EPI_COLS * 4;        // one C store box: 32 rows x EPI_COLS fp32
+  static constexpr int SMEM_BAR = SMEM_EPI + K::EPI_WARPS * K::EPI_BUFS * EPI_BUF;
   static constexpr int THREADS = 64 + 32 * K::EPI_WARPS;
-  static_assert(K::STAGES * STAGE_BYTES <= K::RING_BYTES, "stage ring");
+  static_assert(B_REGION + K::STAGES * STAGE_BYTES <= K::RING_BYTES, "stage ring");
   static constexpr int SMEM_ALLOC = SMEM_BAR + 512 + 1024;    // + runtime 1024-B alignment slack
   static constexpr uint32_t TMEM_COLS = 2 * K::BN;            // double-buffered accumulator
   static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
-  __device__ static int a_off(int stage, int op) { return stage * STAGE_BYTES + op * A_BYTES; }
+  __device__ static int a_off(int stage, int op) { return B_REGION + stage * STAGE_BYTES + op * A_BYTES; }
   __device__ static int b_off(int stage, int op) { return stage * STAGE_BYTES + K::NOPS * A_BYTES + op * B_BYTES; }
+  __device__ static int b_res_off(int kb) { return kb * B_BYTES; }
 };
 
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
@@ -187,26 +207,38 @@ struct TcArgs {
   int32_t tiles_nb;  // column blocks
   int32_t kblocks;
   int32_t ablate;    // diagnostics: 1 = no C stores, 2 = no MMAs, 4 = no smem staging
+  long long* trace;  // diagnostics (paco_debug_trace): per CTA x 16 tiles x 6 globaltimer stamps
+  int32_t* sched;    // per-group tile counters (zeroed before the launch)
+  int32_t groups;    // CTA c serves group c % groups: column blocks g, g + groups, ...
 };
 
-// CTA-level plan: contiguous ranges of the column-block-major tile sequence
-// (the 1-D MM-1-Piece split: floor/ceil(T/p) tiles per CTA), so consecutive
-// tiles of a CTA share their B column block and concurrent CTAs share A rows.
-struct TileRange {
-  int64_t begin, count;
-};
-
-__device__ __forceinline__ TileRange cta_tiles(const TcArgs& a) {
-  const int64_t G = gridDim.x, c = blockIdx.x;
-  const int64_t T = int64_t(a.tiles_rb) * a.tiles_nb;
-  const int64_t b = T * c / G, e = T * (c + 1) / G;
-  return TileRange{b, e - b};
+__device__ __forceinline__ void tc_stamp(const TcArgs& a, int64_t tile, int field) {
+  if (a.trace && tile < 16) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[(int64_t(blockIdx.x) * 16 + tile) * 6 + field] = t;
+  }
 }
 
-__device__ __forceinline__ void tile_coords(const TcArgs& a, const TileRange& r, int64_t i, int& nb, int& rb) {
-  const int64_t t = r.begin + i;
-  nb = int(t / a.tiles_rb);
-  rb = int(t % a.tiles_rb);
+// CTA-level schedule: dynamic.  The producer of each CTA claims the next tile
+// of its group with an atomic counter and hands it to the MMA and epilogue
+// warps through a small smem queue, so CTAs that get less HBM/L2 bandwidth
+// simply take fewer tiles (a static split left the slowest CTA ~10 % behind
+// the median).  groups = 1 (streaming B): tiles in row-block-major order, so
+// the CTAs running at any moment write whole rows of C (HBM page locality)
+// and share A row blocks in L2.  groups > 1 (resident B): group g walks column
+// blocks g, g + groups, ... and inside one all row blocks, so a CTA never
+// reloads its B, and the groups advance through the row blocks in step.
+__device__ __forceinline__ int32_t claim_tile(const TcArgs& a) {
+  const int g = int(blockIdx.x % uint32_t(a.groups));
+  const int32_t t = atomicAdd(&a.sched[g], 1);
+  if (a.groups == 1) {  // row-block-major: concurrent CTAs write whole rows of C, share A rows
+    if (t >= a.tiles_rb * a.tiles_nb) return -1;
+    return (t % a.tiles_nb) * a.tiles_rb + t / a.tiles_nb;
+  }
+  const int32_t nb = g + (t / a.tiles_rb) * a.groups;
+  if (nb >= a.tiles_nb) return -1;
+  return nb * a.tiles_rb + t % a.tiles_rb;
 }
 
 struct TcMaps {
@@ -224,10 +256,15 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   uint64_t* empty = full + MAXR;
   uint64_t* tfull = empty + MAXR;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = tempty + 2;   // resident B landed (B_RES)
+  uint64_t* bempty = bfull + 1;   // MMAs reading the resident B completed (B_RES)
+  constexpr int QD = 4;           // tile queue depth
+  uint64_t* qfull = bempty + 1;   // tile id published by the producer
+  uint64_t* qempty = qfull + QD;  // ... and read by the MMA warp + every epilogue warp
+  int32_t* qid = reinterpret_cast<int32_t*>(qempty + QD);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qid + QD);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const TileRange tr = cta_tiles(args);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -237,6 +274,12 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], K::EPI_WARPS);
+    }
+    mbar_init(bfull, 1);
+    mbar_init(bempty, 1);
+    for (int j = 0; j < QD; ++j) {
+      mbar_init(&qfull[j], 1);
+      mbar_init(&qempty[j], 1 + K::EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     for (int o = 0; o < K::NOPS; ++o) {
@@ -259,13 +302,39 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       {
-        uint32_t it = 0;
-        for (int64_t i = 0; i < tr.count; ++i) {
-          int nb, rb;
-          tile_coords(args, tr, i, nb, rb);
+        uint32_t it = 0, bloads = 0;
+        int loaded_nb = -1;
+        for (int64_t i = 0;; ++i) {
+          const int32_t id = claim_tile(args);
+          const int qs = int(i % QD);
+          mbar_wait(&qempty[qs], (uint32_t(i / QD) & 1) ^ 1);
+          qid[qs] = id;
+          mbar_arrive(&qfull[qs]);
+          if (id < 0) break;
+          const int nb = id / args.tiles_rb, rb = id % args.tiles_rb;
+          if constexpr (K::B_RES) {
+            if (nb != loaded_nb) {  // (re)load the resident B column block
+              if (bloads > 0) mbar_wait(bempty, (bloads - 1) & 1);
+              mbar_expect_tx(bfull, uint32_t(args.kblocks) * L::B_BYTES);
+              for (int kb = 0; kb < args.kblocks; ++kb)
+#pragma unroll
+                for (int j = 0; j < BN / L::BOX_N; ++j)
+                  tma_load_2d(smem + L::b_res_off(kb) + j * (BK * 128), &maps.b[0], bfull,
+                              args.b_col0 + nb * BN + L::BOX_N * j, kb * BK);
+              loaded_nb = nb;
+              ++bloads;
+            }
+          }
           for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
             const int s = it % STAGES;
             mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+            if (kb == 0) tc_stamp(args, i, 0);
+            if (kb == args.kblocks - 1) tc_stamp(args, i, 1);
+            if constexpr (K::B_RES) {
+              mbar_expect_tx(&full[s], L::A_BYTES);
+              tma_load_2d(smem + L::a_off(s, 0), &maps.a[0], &full[s], args.a_col0 + kb * BK, rb * BM);
+              continue;
+            }
             mbar_expect_tx(&full[s], K::NOPS * (L::A_BYTES + L::B_BYTES));
 #pragma unroll
             for (int o = 0; o < K::NOPS; ++o) {
@@ -288,11 +357,25 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      uint32_t it = 0;
-      int tile = 0;
-      for (int64_t i = 0; i < tr.count; ++i, ++tile) {
+      uint32_t it = 0, buses = 0;
+      int tile = 0, cur_nb = -1;
+      for (int64_t i = 0;; ++i, ++tile) {
+        const int qs = int(i % QD);
+        mbar_wait(&qfull[qs], uint32_t(i / QD) & 1);
+        const int32_t id = qid[qs];
+        mbar_arrive(&qempty[qs]);
+        if (id < 0) break;
         const int a = tile & 1;
         const uint32_t use = uint32_t(tile >> 1);
+        if constexpr (K::B_RES) {
+          const int nb = id / args.tiles_rb;
+          if (nb != cur_nb) {
+            if (cur_nb >= 0) umma_commit(bempty);  // the old B is free once its MMAs complete
+            mbar_wait(bfull, buses & 1);
+            ++buses;
+            cur_nb = nb;
+          }
+        }
         mbar_wait(&tempty[a], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(a * BN);
@@ -300,10 +383,11 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
           const int s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
           tc_fence_after();
+          if (kb == 0) tc_stamp(args, i, 2);
           uint64_t ad[K::NOPS], bd[K::NOPS];
 #pragma unroll
           for (int o = 0; o < K::NOPS; ++o) {
-            const int aoff = L::a_off(s, o), boff = L::b_off(s, o);
+            const int aoff = L::a_off(s, o), boff = K::B_RES ? L::b_res_off(kb) : L::b_off(s, o);
             ad[o] = smem_desc_sw128(smem_u32(smem + aoff));
             bd[o] = K::B_KMAJOR ? smem_desc_sw128(smem_u32(smem + boff)) : smem_desc_mn_sw128(smem_u32(smem + boff), BK);
           }
@@ -322,6 +406,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
           }
           umma_commit(&empty[s]);  // stage is free once these MMAs complete
         }
+        tc_stamp(args, i, 3);
         umma_commit(&tfull[a]);    // accumulator ready for the epilogue
       }
     }
@@ -336,15 +421,21 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
     constexpr int CHUNKS = BN / 32, PER = CHUNKS * 4 / K::EPI_WARPS;  // chunks per warp
     static_assert(PER % 2 == 0, "chunk pairs");
     const int c_lo = (ew / 4) * PER;
-    unsigned char* stage0 = smem + L::SMEM_EPI + ew * 2 * EPI_BUF;
+    unsigned char* stage0 = smem + L::SMEM_EPI + ew * K::EPI_BUFS * L::EPI_BUF;
     int tile = 0;
-    for (int64_t i = 0; i < tr.count; ++i, ++tile) {
-      int nb, rb;
-      tile_coords(args, tr, i, nb, rb);
+    for (int64_t i = 0;; ++i, ++tile) {
+      const int qs = int(i % QD);
+      mbar_wait(&qfull[qs], uint32_t(i / QD) & 1);
+      const int32_t id = qid[qs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty[qs]);
+      if (id < 0) break;
+      const int nb = id / args.tiles_rb, rb = id % args.tiles_rb;
       const int a = tile & 1;
       const uint32_t use = uint32_t(tile >> 1);
       mbar_wait(&tfull[a], use & 1);
       tc_fence_after();
+      if (ew == 0 && lane == 0) tc_stamp(args, i, 4);
       const int row0 = rb * BM + 32 * q;
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + PER; c += 2) {
@@ -368,35 +459,41 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
         }
         const int col0 = nb * BN + 32 * c;
         if (col0 >= args.m) continue;  // warp-uniform: nothing left to store
-        const bool second = col0 + 32 < args.m;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-        __syncwarp();
-        if (!(args.ablate & 4)) {
+        // 64 columns in SUBS boxes of EPI_COLS; buffer h % EPI_BUFS
+        constexpr int EC = K::EPI_COLS, SUBS = 64 / EC;
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint4 w = make_uint4(v[32 * h + 4 * j], v[32 * h + 4 * j + 1], v[32 * h + 4 * j + 2],
-                                         v[32 * h + 4 * j + 3]);
-              *reinterpret_cast<uint4*>(stage0 + h * EPI_BUF + lane * 128 + ((j ^ (lane & 7)) * 16)) = w;
-            }
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        }
-        __syncwarp();
-        if (lane == 0) {
-          if (row0 < args.n && !(args.ablate & 1)) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (h == 1 && !second) break;
-              if (args.overwrite)
-                tma_store_2d(&maps.c, stage0 + h * EPI_BUF, args.c_col0 + col0 + 32 * h, row0);
-              else
-                tma_reduce_add_2d(&maps.c, stage0 + h * EPI_BUF, args.c_col0 + col0 + 32 * h, row0);
-            }
+        for (int h = 0; h < SUBS; ++h) {
+          if (col0 + EC * h >= args.m) break;
+          unsigned char* buf = stage0 + (h % K::EPI_BUFS) * L::EPI_BUF;
+          if (h % K::EPI_BUFS == 0) {  // the buffer(s) must be read out by earlier stores
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            __syncwarp();
           }
-          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          if (!(args.ablate & 4)) {
+            // swizzled [32 rows][EC fp32]: 16 B chunk j of row r at j ^ (r-bits of the
+            // 128B (EC = 32) / 64B (EC = 16) TMA swizzle pattern)
+#pragma unroll
+            for (int j = 0; j < EC / 4; ++j) {
+              const uint4 w = make_uint4(v[EC * h + 4 * j], v[EC * h + 4 * j + 1], v[EC * h + 4 * j + 2],
+                                         v[EC * h + 4 * j + 3]);
+              const int sw = EC == 32 ? (j ^ (lane & 7)) : (j ^ ((lane >> 1) & 3));
+              *reinterpret_cast<uint4*>(buf + lane * (EC * 4) + sw * 16) = w;
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          }
+          __syncwarp();
+          if (lane == 0) {
+            if (row0 < args.n && !(args.ablate & 1)) {
+              if (args.overwrite)
+                tma_store_2d(&maps.c, buf, args.c_col0 + col0 + EC * h, row0);
+              else
+                tma_reduce_add_2d(&maps.c, buf, args.c_col0 + col0 + EC * h, row0);
+            }
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          }
         }
       }
+      if (ew == 0 && lane == 0) tc_stamp(args, i, 5);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   }
@@ -427,7 +524,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
 // 2-D row-major tensor map over an aligned base; `col_off` returns how many
 // elements the view starts after that base (added to column coordinates).
 int make_map(CUtensorMap* map, CUtensorMapDataType dt, int elsize, const void* ptr, int64_t rows,
-             int64_t cols, int64_t ld, uint32_t box_cols, uint32_t box_rows, int32_t* col_off) {
+             int64_t cols, int64_t ld, uint32_t box_cols, uint32_t box_rows, int32_t* col_off,
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encoder();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled is unavailable from the driver");
@@ -445,7 +543,7 @@ int make_map(CUtensorMap* map, CUtensorMapDataType dt, int elsize, const void* p
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, dt, 2, reinterpret_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d) for %lldx%lld ld=%lld", int(r), (long long)rows,
@@ -635,7 +733,9 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
     C = p;
     ldc = ld2;
   }
-  if ((rc = make_map(&maps.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, n, m, ldc, 32, 32, &c_off))) return rc;
+  if ((rc = make_map(&maps.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, n, m, ldc, K::EPI_COLS, 32, &c_off,
+                     K::EPI_COLS == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
+    return rc;
   tc::TcArgs args;
   args.n = n;
   args.m = m;
@@ -650,9 +750,17 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
   {
     static const int ablate = getenv("PACO_TC_ABLATE") ? atoi(getenv("PACO_TC_ABLATE")) : 0;
     args.ablate = ablate;
+    args.trace = g_trace_buffer;
   }
   const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb;
   const int grid = int(tiles < kNumSMs ? tiles : kNumSMs);
+  args.groups = K::B_RES ? (args.tiles_nb < grid ? args.tiles_nb : grid) : 1;
+  {
+    void* counters;
+    if ((rc = scratch(device, sc, sizeof(int32_t) * args.groups, stream, &counters))) return rc;
+    PACO_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(int32_t) * args.groups, stream));
+    args.sched = static_cast<int32_t*>(counters);
+  }
   auto kern = tc::tc_gemm_kernel<K>;
   PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
   kern<<<grid, L::THREADS, L::SMEM_ALLOC, stream>>>(maps, args);
@@ -665,6 +773,20 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
 int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B, int64_t ldb,
                       void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces,
                       int n_pieces, int flags) {
+  // k <= 256 (cfg3): resident-B kind, 5-stage A ring, 8 epilogue warps staging
+  // 16-column boxes (measured best of 7 layouts, tools/tc_trace.py); PACO_TC_RESV
+  // selects the alternatives for experiments (-1 = streaming kind).
+  static const int resv = getenv("PACO_TC_RESV") ? atoi(getenv("PACO_TC_RESV")) : 7;
+#define PACO_TC_GO(KIND) return launch_tc<KIND>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags)
+  if (k <= 256 && resv >= 0) {
+    if (resv == 0) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<3, 1>));
+    if (resv == 1) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<4, 1>));
+    if (resv == 3) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16T<4, 1, 8>));
+    if (resv == 5) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16T<4, 2, 8, 16>));
+    if (resv == 6) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<4, 2, 8, 16>));
+    PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<5, 1, 8, 16>));
+  }
+#undef PACO_TC_GO
   return launch_tc<tc::KindBF16>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
 }
 
