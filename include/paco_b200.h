@@ -121,6 +121,22 @@ int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out,
                  int64_t m, int nin, const void* const* ins, const int64_t* lds,
                  const int32_t* coefs, int accumulate);
 
+/* Strassen leaf operands for the 3xTF32 tensor-core MM, with the S/T sum
+ * fused in (replaces a lincomb + split pair): x = sum_i
+ * coef[i] * in[i] over rows x cols fp32 views (nin 1..4, coef +1/-1) is
+ * written as hi = tf32_rn(x), lo = tf32_rn(x - hi), row pitch ldo elements,
+ * transposed (cols x rows) when `transpose` (the K-major B^T operand). */
+int paco_tf32_split(int device, void* stream, int nin, const void* const* ins, const int64_t* lds,
+                    const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* lo,
+                    int64_t ldo);
+
+/* C (+)= A x B as 3xTF32 on tcgen05 from pre-split operands: A_hi/A_lo n x k
+ * (lda), B^T_hi/B^T_lo m x k (ldb) -- paco_tf32_split outputs; row pitches
+ * must be multiples of 16 bytes.  flags as paco_mm. */
+int paco_mm_tf32x3(int device, void* stream, const void* a_hi, const void* a_lo, int64_t lda,
+                   const void* bt_hi, const void* bt_lo, int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m,
+                   int64_t k, int flags);
+
 /* Asynchronous 2-D copy (host<->device or device<->device; pitches and width in
  * BYTES): the staging primitive of the overlapped host pipeline. */
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,

@@ -31,6 +31,12 @@ int launch_mm_f32_tc(int device, cudaStream_t stream, const void* A, int64_t lda
                      int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
                      const int32_t* pieces, int n_pieces, int flags);
 int tc_tile_shape(int semiring, int* bm, int* bn, int* bk, int* cps);
+int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, const void* ah, const void* al, int64_t lda,
+                              const void* bth, const void* btl, int64_t ldb, void* C, int64_t ldc, int64_t n,
+                              int64_t m, int64_t k, int flags);
+int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,
+                      const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* lo,
+                      int64_t ldo);
 int launch_fold(int sr, cudaStream_t st, void* dst, int64_t ldd, void* src, int64_t lds, int64_t n,
                 int64_t m, int reset);
 int launch_fill(int sr, cudaStream_t st, void* dst, int64_t ld, int64_t n, int64_t m);
@@ -155,6 +161,38 @@ int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out,
   PACO_TRY(use_device(device));
   return launch_lincomb(dtype, static_cast<cudaStream_t>(stream), out, ld_out, n, m, nin, ins, lds,
                         coefs, accumulate);
+}
+
+int paco_tf32_split(int device, void* stream, int nin, const void* const* ins, const int64_t* lds,
+                    const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* lo,
+                    int64_t ldo) {
+  if (rows <= 0 || cols <= 0) return PACO_OK;
+  if (!ins || !lds || !coefs || nin < 1 || nin > 4) {
+    set_error("paco_tf32_split: need 1..4 inputs with pitches and coefficients");
+    return PACO_ERR_ARG;
+  }
+  for (int q = 0; q < nin; ++q) PACO_TRY(check_view("in", ins[q], lds[q], rows, cols));
+  PACO_TRY(use_device(device));
+  return launch_tf32_split(static_cast<cudaStream_t>(stream), nin, ins, lds, coefs, rows, cols, transpose, hi,
+                           lo, ldo);
+}
+
+int paco_mm_tf32x3(int device, void* stream, const void* a_hi, const void* a_lo, int64_t lda,
+                   const void* bt_hi, const void* bt_lo, int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m,
+                   int64_t k, int flags) {
+  if (n <= 0 || m <= 0) return PACO_OK;
+  PACO_TRY(check_view("C", C, ldc, n, m));
+  if (k > 0) {
+    PACO_TRY(check_view("A_hi", a_hi, lda, n, k));
+    PACO_TRY(check_view("A_lo", a_lo, lda, n, k));
+    PACO_TRY(check_view("Bt_hi", bt_hi, ldb, m, k));
+    PACO_TRY(check_view("Bt_lo", bt_lo, ldb, m, k));
+  }
+  PACO_TRY(use_device(device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (k <= 0)
+    return (flags & PACO_MM_OVERWRITE) ? launch_fill(PACO_SR_F32_TC, st, C, ldc, n, m) : PACO_OK;
+  return launch_mm_tf32x3_presplit(device, st, a_hi, a_lo, lda, bt_hi, bt_lo, ldb, C, ldc, n, m, k, flags);
 }
 
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,

@@ -67,6 +67,8 @@ struct KindTF32x3 {
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
   static constexpr CUtensorMapDataType DT = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
 };
+// (MN-major B -- bit 16 of the descriptor -- is what the bf16 kind uses; with
+// kind::tf32 it returned all-zero products here, hence the transposed split.)
 
 // bf16 with K <= KB_MAX * BK: the CTA's whole B column block (K x 256, 128 KB)
 // stays resident in shared memory across its consecutive tiles of that block,
@@ -599,34 +601,130 @@ __device__ __forceinline__ float round_tf32(float x) {
   return __uint_as_float(r);
 }
 
-template <bool kT>
-__global__ void split_tf32_kernel(const float* __restrict__ x, int64_t ldx, float* __restrict__ hi,
-                                  float* __restrict__ lo, int64_t ldo, int64_t rows, int64_t cols) {
-  __shared__ float th[32][33], tl[32][33];
-  const int64_t r0 = int64_t(blockIdx.y) * 32, c0 = int64_t(blockIdx.x) * 32;
-  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
-    const int64_t i = r0 + dy, j = c0 + threadIdx.x;
-    float v = (i < rows && j < cols) ? x[i * ldx + j] : 0.f;
-    const float h = round_tf32(v);
-    const float l = round_tf32(v - h);  // the MMA would truncate an unrounded lo
-    if (!kT) {
-      if (i < rows && j < cols) {
-        hi[i * ldo + j] = h;
-        lo[i * ldo + j] = l;
+// Up to four signed input views summed (Strassen S/T formation, PAPER.md:
+// 1839-1852) and split; nin = 1, coef = +1 is the plain split.
+struct SplitIn {
+  const float* p[4];
+  int64_t ld[4];
+  int32_t coef[4];
+  int32_t nin;
+};
+
+__device__ __forceinline__ float lc_value(const SplitIn& in, int64_t i, int64_t j) {
+  float v = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (q < in.nin) {
+      const float x = in.p[q][i * in.ld[q] + j];
+      v = in.coef[q] > 0 ? v + x : v - x;
+    }
+  return v;
+}
+
+// Transposed output (cols x rows) through a 64x64 smem tile: 16-byte loads
+// along the input rows, 16-byte stores along the output rows (the K-major
+// B^T the 3xTF32 MMAs read).  kVec: every view 16 B aligned, cols % 4 == 0.
+template <bool kVec>
+__global__ void __launch_bounds__(256) split_tf32_t_kernel(const SplitIn in, float* __restrict__ hi,
+                                                           float* __restrict__ lo, int64_t ldo, int64_t rows,
+                                                           int64_t cols) {
+  __shared__ float th[64][65], tl[64][65];
+  const int64_t r0 = int64_t(blockIdx.y) * 64, c0 = int64_t(blockIdx.x) * 64;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int r = ty + 16 * p;
+    const int64_t i = r0 + r, j = c0 + 4 * tx;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (i < rows) {
+      if (kVec && j + 3 < cols) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < in.nin) {
+            const float4 x = *reinterpret_cast<const float4*>(in.p[q] + i * in.ld[q] + j);
+            const float sg = in.coef[q] > 0 ? 1.f : -1.f;
+            v[0] += sg * x.x;
+            v[1] += sg * x.y;
+            v[2] += sg * x.z;
+            v[3] += sg * x.w;
+          }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = j + e < cols ? lc_value(in, i, j + e) : 0.f;
       }
-    } else {
-      th[dy][threadIdx.x] = h;
-      tl[dy][threadIdx.x] = l;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float h = round_tf32(v[e]);
+      th[r][4 * tx + e] = h;
+      tl[r][4 * tx + e] = round_tf32(v[e] - h);  // the MMA would truncate an unrounded lo
     }
   }
-  if (kT) {
-    __syncthreads();
-    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
-      const int64_t j = c0 + dy, i = r0 + threadIdx.x;  // output row j (a column of x)
-      if (j < cols && i < rows) {
-        hi[j * ldo + i] = th[threadIdx.x][dy];
-        lo[j * ldo + i] = tl[threadIdx.x][dy];
-      }
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int c = ty + 16 * p;                 // output row j = c0 + c (a column of x)
+    const int64_t j = c0 + c, i = r0 + 4 * tx;  // 4 consecutive output columns (rows of x)
+    if (j >= cols) continue;
+    const float4 h = make_float4(th[4 * tx][c], th[4 * tx + 1][c], th[4 * tx + 2][c], th[4 * tx + 3][c]);
+    const float4 l = make_float4(tl[4 * tx][c], tl[4 * tx + 1][c], tl[4 * tx + 2][c], tl[4 * tx + 3][c]);
+    if (kVec && i + 3 < rows) {
+      *reinterpret_cast<float4*>(hi + j * ldo + i) = h;
+      *reinterpret_cast<float4*>(lo + j * ldo + i) = l;
+    } else {
+      const float hv[4] = {h.x, h.y, h.z, h.w}, lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (i + e < rows) {
+          hi[j * ldo + i + e] = hv[e];
+          lo[j * ldo + i + e] = lv[e];
+        }
+    }
+  }
+}
+
+// Row-major output, 4 consecutive elements per thread (16 B accesses when
+// every view is 16 B aligned: vec), rows strided over the grid's y.
+template <bool kVec>
+__global__ void split_tf32_n_kernel(const SplitIn in, float* __restrict__ hi, float* __restrict__ lo,
+                                    int64_t ldo, int64_t rows, int64_t cols) {
+  const int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (j >= cols) return;
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    float v[4];
+    if (kVec) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < in.nin) {
+          const float4 x = *reinterpret_cast<const float4*>(in.p[q] + i * in.ld[q] + j);
+          const float s = in.coef[q] > 0 ? 1.f : -1.f;
+          v[0] += s * x.x;
+          v[1] += s * x.y;
+          v[2] += s * x.z;
+          v[3] += s * x.w;
+        }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = j + e < cols ? lc_value(in, i, j + e) : 0.f;
+    }
+    float h[4], l[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      h[e] = round_tf32(v[e]);
+      l[e] = round_tf32(v[e] - h[e]);
+    }
+    if (kVec) {
+      *reinterpret_cast<float4*>(hi + i * ldo + j) = make_float4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<float4*>(lo + i * ldo + j) = make_float4(l[0], l[1], l[2], l[3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (j + e < cols) {
+          hi[i * ldo + j + e] = h[e];
+          lo[i * ldo + j + e] = l[e];
+        }
     }
   }
 }
@@ -648,8 +746,37 @@ int repack(int device, Scratch& sc, const void** p, int64_t* ld, int64_t rows, i
   return PACO_OK;
 }
 
-// fp32 operand -> packed hi/lo tf32 pair in scratch;
-// `transpose` stores them as (cols x rows), i.e. K-major for a B operand.
+// x = sum coef_q in_q (rows x cols) -> hi/lo tf32 pair with row pitch ldo
+// (elements), transposed (cols x rows) if `transpose`.
+int launch_split(const tc::SplitIn& in, int64_t rows, int64_t cols, bool transpose, float* h, float* l,
+                 int64_t ldo, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return PACO_OK;
+  bool vec = (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(h) % 16 == 0) &&
+             (reinterpret_cast<uintptr_t>(l) % 16 == 0);
+  for (int q = 0; q < in.nin; ++q)
+    vec = vec && (in.ld[q] % 4 == 0) && (reinterpret_cast<uintptr_t>(in.p[q]) % 16 == 0);
+  if (transpose) {
+    dim3 grid(unsigned((cols + 63) / 64), unsigned((rows + 63) / 64));
+    if (vec)
+      tc::split_tf32_t_kernel<true><<<grid, 256, 0, st>>>(in, h, l, ldo, rows, cols);
+    else
+      tc::split_tf32_t_kernel<false><<<grid, 256, 0, st>>>(in, h, l, ldo, rows, cols);
+  } else {
+    vec = vec && (cols % 4 == 0);
+    const int64_t xblocks = (cols / 4 + 1 + 127) / 128;
+    const int64_t yblocks = rows < 65535 ? rows : 65535;
+    dim3 grid(unsigned(xblocks), unsigned(yblocks > 2368 / xblocks + 1 ? 2368 / xblocks + 1 : yblocks));
+    if (vec)
+      tc::split_tf32_n_kernel<true><<<grid, 128, 0, st>>>(in, h, l, ldo, rows, cols);
+    else
+      tc::split_tf32_n_kernel<false><<<grid, 128, 0, st>>>(in, h, l, ldo, rows, cols);
+  }
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
+// fp32 operand -> packed hi/lo tf32 pair in scratch; `transpose` stores them
+// as (cols x rows), i.e. K-major for a B operand.
 int split_operand(int device, Scratch& sc, const void* x, int64_t ldx, int64_t rows, int64_t cols,
                   bool transpose, cudaStream_t st, const void** hi, const void** lo, int64_t* ld) {
   const int64_t orows = transpose ? cols : rows, ocols = transpose ? rows : cols;
@@ -658,14 +785,13 @@ int split_operand(int device, Scratch& sc, const void* x, int64_t ldx, int64_t r
   int rc = scratch(device, sc, size_t(orows) * ld2 * 4, st, &h);
   if (rc) return rc;
   if ((rc = scratch(device, sc, size_t(orows) * ld2 * 4, st, &l))) return rc;
-  dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32)), block(32, 8);
-  if (transpose)
-    tc::split_tf32_kernel<true><<<grid, block, 0, st>>>(static_cast<const float*>(x), ldx, static_cast<float*>(h),
-                                                        static_cast<float*>(l), ld2, rows, cols);
-  else
-    tc::split_tf32_kernel<false><<<grid, block, 0, st>>>(static_cast<const float*>(x), ldx, static_cast<float*>(h),
-                                                         static_cast<float*>(l), ld2, rows, cols);
-  PACO_CUDA_TRY(cudaGetLastError());
+  tc::SplitIn in{};
+  in.p[0] = static_cast<const float*>(x);
+  in.ld[0] = ldx;
+  in.coef[0] = 1;
+  in.nin = 1;
+  if ((rc = launch_split(in, rows, cols, transpose, static_cast<float*>(h), static_cast<float*>(l), ld2, st)))
+    return rc;
   *hi = h;
   *lo = l;
   *ld = ld2;
@@ -673,10 +799,16 @@ int split_operand(int device, Scratch& sc, const void* x, int64_t ldx, int64_t r
 }
 }  // namespace
 
+// 3xTF32 operands already split (paco_tf32_split): A hi/lo n x k, B^T hi/lo m x k.
+struct Presplit {
+  const void *ah, *al, *bh, *bl;
+  int64_t lda, ldb;
+};
+
 template <class K>
 int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B, int64_t ldb,
               void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces, int n_pieces,
-              int flags) {
+              int flags, const Presplit* pre = nullptr) {
   using L = tc::Layout<K>;
   if (pieces && n_pieces > 0) {
     set_error("the tcgen05 kernels take their own CTA plan (pass pieces=NULL)");
@@ -709,8 +841,20 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
     // 3xTF32: split both operands into packed hi/lo pairs
     const void *ah, *al, *bh, *bl;
     int64_t lda2, ldb2;
-    if ((rc = split_operand(device, sc, A, lda, n, k, false, stream, &ah, &al, &lda2))) return rc;
-    if ((rc = split_operand(device, sc, B, ldb, k, m, K::B_KMAJOR, stream, &bh, &bl, &ldb2))) return rc;
+    if (pre) {
+      if (!K::B_KMAJOR) {
+        set_error("internal: pre-split B operands are K-major");
+        return PACO_ERR_UNSUPPORTED;
+      }
+      ah = pre->ah, al = pre->al, bh = pre->bh, bl = pre->bl, lda2 = pre->lda, ldb2 = pre->ldb;
+      if (!pitch_ok(ah, lda2, 4) || !pitch_ok(al, lda2, 4) || !pitch_ok(bh, ldb2, 4) || !pitch_ok(bl, ldb2, 4)) {
+        set_error("paco_mm_tf32x3: operand row pitches must be multiples of 16 bytes");
+        return PACO_ERR_UNSUPPORTED;
+      }
+    } else {
+      if ((rc = split_operand(device, sc, A, lda, n, k, false, stream, &ah, &al, &lda2))) return rc;
+      if ((rc = split_operand(device, sc, B, ldb, k, m, K::B_KMAJOR, stream, &bh, &bl, &ldb2))) return rc;
+    }
     if ((rc = make_map(&maps.a[0], K::DT, K::ELEM, ah, n, k, lda2, K::BK, tc::BM, &a_off))) return rc;
     if ((rc = make_map(&maps.a[1], K::DT, K::ELEM, al, n, k, lda2, K::BK, tc::BM, &t_off))) return rc;
     if constexpr (K::B_KMAJOR) {
@@ -794,6 +938,36 @@ int launch_mm_f32_tc(int device, cudaStream_t stream, const void* A, int64_t lda
                      void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces,
                      int n_pieces, int flags) {
   return launch_tc<tc::KindTF32x3>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
+}
+
+int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, const void* ah, const void* al, int64_t lda,
+                              const void* bth, const void* btl, int64_t ldb, void* C, int64_t ldc, int64_t n,
+                              int64_t m, int64_t k, int flags) {
+  const Presplit pre{ah, al, bth, btl, lda, ldb};
+  return launch_tc<tc::KindTF32x3>(device, stream, nullptr, 0, nullptr, 0, C, ldc, n, m, k, nullptr, 0, flags,
+                                   &pre);
+}
+
+int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,
+                      const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* lo,
+                      int64_t ldo) {
+  if (nin < 1 || nin > 4) {
+    set_error("paco_tf32_split: nin=%d (1..4 supported)", nin);
+    return PACO_ERR_ARG;
+  }
+  if (!hi || !lo || ldo < (transpose ? rows : cols)) {
+    set_error("paco_tf32_split: bad outputs or pitch");
+    return PACO_ERR_ARG;
+  }
+  tc::SplitIn in{};
+  for (int q = 0; q < nin; ++q) {
+    in.p[q] = static_cast<const float*>(ins[q]);
+    in.ld[q] = lds[q];
+    in.coef[q] = coefs[q] >= 0 ? 1 : -1;
+  }
+  in.nin = nin;
+  return launch_split(in, rows, cols, transpose != 0, static_cast<float*>(hi), static_cast<float*>(lo), ldo,
+                      stream);
 }
 
 int tc_tile_shape(int semiring, int* bm, int* bn, int* bk, int* cps) {

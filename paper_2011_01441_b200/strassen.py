@@ -232,25 +232,71 @@ def _lincomb(dt: int, stream, out: View, terms, accumulate: bool = False) -> Non
                                       out.cols, nin, ins, lds, coefs, int(accumulate)))
 
 
-class _Workspace:
-    """S/T/M buffers of one internal node: 7 of each, (size/2)^2, on one device."""
+def _single(terms) -> str | None:
+    """The quadrant of a one-term, +1 formula (S3 = A00, T2 = B00, ...): used as a view."""
+    return terms[0][1] if len(terms) == 1 and terms[0][0] == 1 else None
 
-    def __init__(self, size: int, dtype: torch.dtype, device: int):
+
+class _Workspace:
+    """S/T/M buffers of one internal node: 7 of each, (size/2)^2, on one device.
+
+    One-term formulas (S3, S4, T2, T5) are views of the operand quadrants,
+    not copies.  ``leaf_split`` nodes (3xTF32 children) keep no S/T at all:
+    their operands are formed straight into split tf32 pairs."""
+
+    def __init__(self, size: int, dtype: torch.dtype, device: int, A: View, B: View, leaf_split: bool = False):
         h = size // 2
-        self.S = [View.of(torch.empty((h, h), dtype=dtype, device=device)) for _ in range(7)]
-        self.T = [View.of(torch.empty((h, h), dtype=dtype, device=device)) for _ in range(7)]
-        self.M = [View.of(torch.empty((h, h), dtype=dtype, device=device)) for _ in range(7)]
+
+        def buf():
+            return View.of(torch.empty((h, h), dtype=dtype, device=device))
+
+        self.S = [None if leaf_split else (_quad(A, q) if (q := _single(S_TERMS[r])) else buf())
+                  for r in range(1, 8)]
+        self.T = [None if leaf_split else (_quad(B, q) if (q := _single(T_TERMS[r])) else buf())
+                  for r in range(1, 8)]
+        self.M = [buf() for _ in range(7)]
 
 
 def _form(ws: _Workspace, A: View, B: View, dt: int, stream) -> None:
     for r in range(1, 8):
-        _lincomb(dt, stream, ws.S[r - 1], [(c, _quad(A, q)) for c, q in S_TERMS[r]])
-        _lincomb(dt, stream, ws.T[r - 1], [(c, _quad(B, q)) for c, q in T_TERMS[r]])
+        if not _single(S_TERMS[r]):
+            _lincomb(dt, stream, ws.S[r - 1], [(c, _quad(A, q)) for c, q in S_TERMS[r]])
+        if not _single(T_TERMS[r]):
+            _lincomb(dt, stream, ws.T[r - 1], [(c, _quad(B, q)) for c, q in T_TERMS[r]])
 
 
 def _combine(ws: _Workspace, C: View, dt: int, stream) -> None:
     for q, terms in C_TERMS.items():
         _lincomb(dt, stream, _quad(C, q), [(c, ws.M[r - 1]) for c, r in terms])
+
+
+def _split(stream, terms, src: View, hi: torch.Tensor, lo: torch.Tensor, transpose: bool) -> None:
+    views = [_quad(src, q) for _, q in terms]
+    nin = len(views)
+    ins = (ctypes.c_void_p * nin)(*[v.ptr for v in views])
+    lds = (ctypes.c_int64 * nin)(*[v.ld for v in views])
+    coefs = (ctypes.c_int32 * nin)(*[c for c, _ in terms])
+    h = views[0].rows
+    nat.check(nat.load().paco_tf32_split(src.device, stream.cuda_stream, nin, ins, lds, coefs, h, h,
+                                         int(transpose), hi.data_ptr(), lo.data_ptr(), hi.stride(0)))
+
+
+def _leaf_level_tf32(A: View, B: View, C: View, stream) -> None:
+    """A node whose seven children are 3xTF32 leaves: each S_r / T_r is formed
+    directly as its split tf32 pair (A-side row-major, B-side transposed), so
+    the sums never round-trip through HBM as fp32; then M_r = S_r T_r on
+    tcgen05 (paco_mm_tf32x3) and the C blocks are combined as usual."""
+    h = C.rows // 2
+    ws = _Workspace(C.rows, torch.float32, C.device, A, B, leaf_split=True)
+    ah, al, bh, bl = (torch.empty((h, h), dtype=torch.float32, device=C.device) for _ in range(4))
+    lib = nat.load()
+    for r in range(1, 8):  # one stream: the operand buffers are reused in order
+        _split(stream, S_TERMS[r], A, ah, al, transpose=False)
+        _split(stream, T_TERMS[r], B, bh, bl, transpose=True)
+        M = ws.M[r - 1]
+        nat.check(lib.paco_mm_tf32x3(C.device, stream.cuda_stream, ah.data_ptr(), al.data_ptr(), h,
+                                     bh.data_ptr(), bl.data_ptr(), h, M.ptr, M.ld, h, h, h, nat.MM_OVERWRITE))
+    _combine(ws, C, nat.DT_F32, stream)
 
 
 def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stream) -> None:
@@ -259,7 +305,11 @@ def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stre
     if C.rows <= base or C.rows % 2:
         launch_mm(kid, stream, A, B, C, overwrite=True)
         return
-    ws = _Workspace(C.rows, dtype, C.device)
+    h = C.rows // 2
+    if kid == nat.SR_F32_TC and (h <= base or h % 2) and h % 4 == 0:
+        _leaf_level_tf32(A, B, C, stream)
+        return
+    ws = _Workspace(C.rows, dtype, C.device, A, B)
     _form(ws, A, B, dt, stream)
     for r in range(7):
         _strassen_dev(ws.S[r], ws.T[r], ws.M[r], base, dtype, stream)
@@ -352,7 +402,7 @@ def strassen_execute(plan: Plan, A, B, mode: str = "serial_sim", *, devices: lis
         while stack:
             nd = stack.pop()
             if nd.kids:
-                ws = _Workspace(nd.size, dtype, home)
+                ws = _Workspace(nd.size, dtype, home, *ops[id(nd)][:2])
                 wss[id(nd)] = ws
                 for r, kid_nd in enumerate(nd.kids):
                     ops[id(kid_nd)] = (ws.S[r], ws.T[r], ws.M[r])

@@ -69,3 +69,47 @@ def test_cfg5_full_size_vs_oracle():
     ref = PN.strassen(A.astype(np.float64), B.astype(np.float64), 2)
     err = np.linalg.norm(C.astype(np.float64) - ref) / np.linalg.norm(ref)
     assert err <= 1e-4, err
+
+
+@pytest.mark.parametrize("transpose", [False, True])
+def test_tf32_split_fused_sum_and_presplit_mm(transpose):
+    """paco_tf32_split forms x = sum(+-in) as a tf32 (hi, lo) pair (hi has 13
+    zero low mantissa bits, |x - hi - lo| <= 2^-21 |x|), optionally transposed;
+    paco_mm_tf32x3 on pre-split operands equals the 3xTF32 paco_mm."""
+    import ctypes
+    from paper_2011_01441_b200 import _native as nat
+    lib = nat.load()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    rows, cols = 300, 260   # ragged: exercises the scalar edges of the vector kernels
+    X = [torch.rand(rows + 5, cols + 8, device="cuda", generator=g) * 2 - 1 for _ in range(2)]
+    views = [x[2:2 + rows, 4:4 + cols] for x in X]
+    want = (views[0] - views[1]).double()
+    orow, ocol = (cols, rows) if transpose else (rows, cols)
+    ldo = (ocol + 3) // 4 * 4
+    hi = torch.empty(orow, ldo, device="cuda"); lo = torch.empty(orow, ldo, device="cuda")
+    ins = (ctypes.c_void_p * 2)(*[v.data_ptr() for v in views])
+    lds = (ctypes.c_int64 * 2)(*[v.stride(0) for v in views])
+    coefs = (ctypes.c_int32 * 2)(1, -1)
+    nat.check(lib.paco_tf32_split(0, None, 2, ins, lds, coefs, rows, cols, int(transpose),
+                                  hi.data_ptr(), lo.data_ptr(), ldo))
+    torch.cuda.synchronize()
+    h, l = hi[:, :ocol], lo[:, :ocol]
+    if transpose:
+        h, l = h.t(), l.t()
+    assert int((h.contiguous().view(torch.int32) & 0x1FFF).abs().max()) == 0
+    err = (h.double() + l.double() - want).abs()
+    assert float((err - want.abs() * 2.0**-21).max()) <= 0
+    # pre-split MM: C = S x T with S = X0 - X1 (n x k), T^T given transposed
+    n, k, m = rows, cols, 200
+    Y = torch.rand(k, m, device="cuda", generator=g) * 2 - 1
+    ah = torch.empty(n, (k + 3) // 4 * 4, device="cuda"); al = torch.empty_like(ah)
+    nat.check(lib.paco_tf32_split(0, None, 2, ins, lds, coefs, n, k, 0, ah.data_ptr(), al.data_ptr(), ah.stride(0)))
+    bth = torch.empty(m, (k + 3) // 4 * 4, device="cuda"); btl = torch.empty_like(bth)
+    yin = (ctypes.c_void_p * 1)(Y.data_ptr()); yld = (ctypes.c_int64 * 1)(Y.stride(0)); one = (ctypes.c_int32 * 1)(1)
+    nat.check(lib.paco_tf32_split(0, None, 1, yin, yld, one, k, m, 1, bth.data_ptr(), btl.data_ptr(), bth.stride(0)))
+    C = torch.zeros(n, m, device="cuda")
+    nat.check(lib.paco_mm_tf32x3(0, None, ah.data_ptr(), al.data_ptr(), ah.stride(0), bth.data_ptr(),
+                                 btl.data_ptr(), bth.stride(0), C.data_ptr(), C.stride(0), n, m, k, nat.MM_OVERWRITE))
+    torch.cuda.synchronize()
+    ref = want @ Y.double()
+    assert float((C.double() - ref).norm() / ref.norm()) < 1e-5
