@@ -130,12 +130,14 @@ int paco_tf32_split(int device, void* stream, int nin, const void* const* ins, c
                     const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* lo,
                     int64_t ldo);
 
-/* C (+)= A x B as 3xTF32 on tcgen05 from pre-split operands: A_hi/A_lo n x k
- * (lda), B^T_hi/B^T_lo m x k (ldb) -- paco_tf32_split outputs; row pitches
- * must be multiples of 16 bytes.  flags as paco_mm. */
-int paco_mm_tf32x3(int device, void* stream, const void* a_hi, const void* a_lo, int64_t lda,
-                   const void* bt_hi, const void* bt_lo, int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m,
-                   int64_t k, int flags);
+/* C[q] (+)= A[q] x B[q], q < count (1..8), as 3xTF32 on tcgen05 from pre-split
+ * operands -- one launch whose tiles of all `count` same-shape products share
+ * one dynamic queue (Strassen's seven leaf products of a node).  A_hi/A_lo
+ * n x k (lda), B^T_hi/B^T_lo m x k (ldb) -- paco_tf32_split outputs; C n x m
+ * (ldc); row pitches must be multiples of 16 bytes.  flags as paco_mm. */
+int paco_mm_tf32x3(int device, void* stream, int count, const void* const* a_hi, const void* const* a_lo,
+                   int64_t lda, const void* const* bt_hi, const void* const* bt_lo, int64_t ldb, void* const* C,
+                   int64_t ldc, int64_t n, int64_t m, int64_t k, int flags);
 
 /* Asynchronous 2-D copy (host<->device or device<->device; pitches and width in
  * BYTES): the staging primitive of the overlapped host pipeline. */

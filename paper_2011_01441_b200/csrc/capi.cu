@@ -31,9 +31,10 @@ int launch_mm_f32_tc(int device, cudaStream_t stream, const void* A, int64_t lda
                      int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
                      const int32_t* pieces, int n_pieces, int flags);
 int tc_tile_shape(int semiring, int* bm, int* bn, int* bk, int* cps);
-int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, const void* ah, const void* al, int64_t lda,
-                              const void* bth, const void* btl, int64_t ldb, void* C, int64_t ldc, int64_t n,
-                              int64_t m, int64_t k, int flags);
+int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, int count, const void* const* ah,
+                              const void* const* al, int64_t lda, const void* const* bth, const void* const* btl,
+                              int64_t ldb, void* const* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
+                              int flags);
 int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,
                       const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* lo,
                       int64_t ldo);
@@ -177,22 +178,31 @@ int paco_tf32_split(int device, void* stream, int nin, const void* const* ins, c
                            lo, ldo);
 }
 
-int paco_mm_tf32x3(int device, void* stream, const void* a_hi, const void* a_lo, int64_t lda,
-                   const void* bt_hi, const void* bt_lo, int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m,
-                   int64_t k, int flags) {
+int paco_mm_tf32x3(int device, void* stream, int count, const void* const* a_hi, const void* const* a_lo,
+                   int64_t lda, const void* const* bt_hi, const void* const* bt_lo, int64_t ldb, void* const* C,
+                   int64_t ldc, int64_t n, int64_t m, int64_t k, int flags) {
+  if (count < 1 || !a_hi || !a_lo || !bt_hi || !bt_lo || !C) {
+    set_error("paco_mm_tf32x3: need count >= 1 and pointer arrays");
+    return PACO_ERR_ARG;
+  }
   if (n <= 0 || m <= 0) return PACO_OK;
-  PACO_TRY(check_view("C", C, ldc, n, m));
-  if (k > 0) {
-    PACO_TRY(check_view("A_hi", a_hi, lda, n, k));
-    PACO_TRY(check_view("A_lo", a_lo, lda, n, k));
-    PACO_TRY(check_view("Bt_hi", bt_hi, ldb, m, k));
-    PACO_TRY(check_view("Bt_lo", bt_lo, ldb, m, k));
+  for (int q = 0; q < count; ++q) {
+    PACO_TRY(check_view("C", C[q], ldc, n, m));
+    if (k > 0) {
+      PACO_TRY(check_view("A_hi", a_hi[q], lda, n, k));
+      PACO_TRY(check_view("A_lo", a_lo[q], lda, n, k));
+      PACO_TRY(check_view("Bt_hi", bt_hi[q], ldb, m, k));
+      PACO_TRY(check_view("Bt_lo", bt_lo[q], ldb, m, k));
+    }
   }
   PACO_TRY(use_device(device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (k <= 0)
-    return (flags & PACO_MM_OVERWRITE) ? launch_fill(PACO_SR_F32_TC, st, C, ldc, n, m) : PACO_OK;
-  return launch_mm_tf32x3_presplit(device, st, a_hi, a_lo, lda, bt_hi, bt_lo, ldb, C, ldc, n, m, k, flags);
+  if (k <= 0) {
+    if (flags & PACO_MM_OVERWRITE)
+      for (int q = 0; q < count; ++q) PACO_TRY(launch_fill(PACO_SR_F32_TC, st, C[q], ldc, n, m));
+    return PACO_OK;
+  }
+  return launch_mm_tf32x3_presplit(device, st, count, a_hi, a_lo, lda, bt_hi, bt_lo, ldb, C, ldc, n, m, k, flags);
 }
 
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,

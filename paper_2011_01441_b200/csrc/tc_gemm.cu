@@ -58,15 +58,18 @@ struct KindBF16T {
 };
 using KindBF16 = KindBF16T<3, 2, 8>;
 // fp32 inputs as 3xTF32 (hi/lo operand tiles), N=128 tiles, 32-deep k blocks.
-struct KindTF32x3 {
-  static constexpr int BN = 128, BK = 32, UMMA_K = 8, STAGES = 3, ELEM = 4, NOPS = 2, PASSES = 3;
-  static constexpr int RING_BYTES = 3 * 64 * 1024, EPI_WARPS = 4, EPI_BUFS = 2, KB_MAX = 0, EPI_COLS = 32;
+template <int BN_, int ST>
+struct KindTF32x3T {
+  static constexpr int BN = BN_, BK = 32, UMMA_K = 8, STAGES = ST, ELEM = 4, NOPS = 2, PASSES = 3;
+  static constexpr int RING_BYTES = ST * 2 * (128 + BN_) * BK * 4, EPI_WARPS = 4, EPI_BUFS = 2, KB_MAX = 0,
+                       EPI_COLS = 32;
   static constexpr bool B_KMAJOR = true, B_RES = false;  // B^T tiles (the split writes B transposed)
   // F32 accumulate, TF32 A/B (format 2), both K-major
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
   static constexpr CUtensorMapDataType DT = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
 };
+using KindTF32x3 = KindTF32x3T<128, 3>;
 // (MN-major B -- bit 16 of the descriptor -- is what the bf16 kind uses; with
 // kind::tf32 it returned all-zero products here, hence the transposed split.)
 
@@ -200,10 +203,8 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 }
 
 struct TcArgs {
-  int64_t n, m, k;   // C is n x m
-  int32_t a_col0;    // column offset of A inside its aligned tensor map
-  int32_t b_col0;    // column offset of B inside its aligned tensor map
-  int32_t c_col0;    // column offset of C inside its aligned tensor map
+  int64_t n, m, k;   // every problem's C is n x m
+  int32_t count;     // problems in the batch (same shape; tiles of all share one queue)
   int32_t overwrite;
   int32_t tiles_rb;  // row blocks
   int32_t tiles_nb;  // column blocks
@@ -231,20 +232,31 @@ __device__ __forceinline__ void tc_stamp(const TcArgs& a, int64_t tile, int fiel
 // and share A row blocks in L2.  groups > 1 (resident B): group g walks column
 // blocks g, g + groups, ... and inside one all row blocks, so a CTA never
 // reloads its B, and the groups advance through the row blocks in step.
+// A batch (count > 1, groups = 1) puts every problem's tiles in one queue:
+// id = problem * tiles_rb * tiles_nb + nb * tiles_rb + rb.
 __device__ __forceinline__ int32_t claim_tile(const TcArgs& a) {
   const int g = int(blockIdx.x % uint32_t(a.groups));
   const int32_t t = atomicAdd(&a.sched[g], 1);
   if (a.groups == 1) {  // row-block-major: concurrent CTAs write whole rows of C, share A rows
-    if (t >= a.tiles_rb * a.tiles_nb) return -1;
-    return (t % a.tiles_nb) * a.tiles_rb + t / a.tiles_nb;
+    const int32_t tpp = a.tiles_rb * a.tiles_nb;
+    if (t >= tpp * a.count) return -1;
+    const int32_t u = t % tpp;
+    return (t / tpp) * tpp + (u % a.tiles_nb) * a.tiles_rb + u / a.tiles_nb;
   }
   const int32_t nb = g + (t / a.tiles_rb) * a.groups;
   if (nb >= a.tiles_nb) return -1;
   return nb * a.tiles_rb + t % a.tiles_rb;
 }
 
+// One problem: operand maps (hi/lo for 3xTF32), the output map, and the column
+// offset of each view inside its 16-byte aligned map base.
+struct TcProb {
+  CUtensorMap a[2], b[2], c;
+  int32_t a_col0[2], b_col0[2], c_col0;
+};
+constexpr int kMaxBatch = 8;
 struct TcMaps {
-  CUtensorMap a[2], b[2], c;  // operand maps (hi/lo for 3xTF32) and the output map
+  TcProb p[kMaxBatch];
 };
 
 template <class K>
@@ -284,11 +296,13 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
       mbar_init(&qempty[j], 1 + K::EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    for (int o = 0; o < K::NOPS; ++o) {
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.a[o])) : "memory");
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.b[o])) : "memory");
+    for (int q = 0; q < args.count; ++q) {
+      for (int o = 0; o < K::NOPS; ++o) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.p[q].a[o])) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.p[q].b[o])) : "memory");
+      }
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.p[q].c)) : "memory");
     }
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.c)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
@@ -313,7 +327,9 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
           qid[qs] = id;
           mbar_arrive(&qfull[qs]);
           if (id < 0) break;
-          const int nb = id / args.tiles_rb, rb = id % args.tiles_rb;
+          const int tpp = args.tiles_rb * args.tiles_nb, lid = id % tpp;
+          const int nb = lid / args.tiles_rb, rb = lid % args.tiles_rb;
+          const TcProb& P = maps.p[id / tpp];
           if constexpr (K::B_RES) {
             if (nb != loaded_nb) {  // (re)load the resident B column block
               if (bloads > 0) mbar_wait(bempty, (bloads - 1) & 1);
@@ -321,8 +337,8 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
               for (int kb = 0; kb < args.kblocks; ++kb)
 #pragma unroll
                 for (int j = 0; j < BN / L::BOX_N; ++j)
-                  tma_load_2d(smem + L::b_res_off(kb) + j * (BK * 128), &maps.b[0], bfull,
-                              args.b_col0 + nb * BN + L::BOX_N * j, kb * BK);
+                  tma_load_2d(smem + L::b_res_off(kb) + j * (BK * 128), &P.b[0], bfull,
+                              P.b_col0[0] + nb * BN + L::BOX_N * j, kb * BK);
               loaded_nb = nb;
               ++bloads;
             }
@@ -334,22 +350,22 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
             if (kb == args.kblocks - 1) tc_stamp(args, i, 1);
             if constexpr (K::B_RES) {
               mbar_expect_tx(&full[s], L::A_BYTES);
-              tma_load_2d(smem + L::a_off(s, 0), &maps.a[0], &full[s], args.a_col0 + kb * BK, rb * BM);
+              tma_load_2d(smem + L::a_off(s, 0), &P.a[0], &full[s], P.a_col0[0] + kb * BK, rb * BM);
               continue;
             }
             mbar_expect_tx(&full[s], K::NOPS * (L::A_BYTES + L::B_BYTES));
 #pragma unroll
             for (int o = 0; o < K::NOPS; ++o) {
-              tma_load_2d(smem + L::a_off(s, o), &maps.a[o], &full[s], args.a_col0 + kb * BK, rb * BM);
+              tma_load_2d(smem + L::a_off(s, o), &P.a[o], &full[s], P.a_col0[o] + kb * BK, rb * BM);
               if constexpr (K::B_KMAJOR) {
                 // B^T (m x k, K contiguous): one box of [BN rows][BK k]
-                tma_load_2d(smem + L::b_off(s, o), &maps.b[o], &full[s], args.b_col0 + kb * BK, nb * BN);
+                tma_load_2d(smem + L::b_off(s, o), &P.b[o], &full[s], P.b_col0[o] + kb * BK, nb * BN);
               } else {
                 // B is k x m row-major (N contiguous): boxes of [BK k rows][128 B of n]
 #pragma unroll
                 for (int j = 0; j < BN / L::BOX_N; ++j)
-                  tma_load_2d(smem + L::b_off(s, o) + j * (BK * 128), &maps.b[o], &full[s],
-                              args.b_col0 + nb * BN + L::BOX_N * j, kb * BK);
+                  tma_load_2d(smem + L::b_off(s, o) + j * (BK * 128), &P.b[o], &full[s],
+                              P.b_col0[o] + nb * BN + L::BOX_N * j, kb * BK);
               }
             }
           }
@@ -369,7 +385,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
         if (id < 0) break;
         const int a = tile & 1;
         const uint32_t use = uint32_t(tile >> 1);
-        if constexpr (K::B_RES) {
+        if constexpr (K::B_RES) {  // count == 1
           const int nb = id / args.tiles_rb;
           if (nb != cur_nb) {
             if (cur_nb >= 0) umma_commit(bempty);  // the old B is free once its MMAs complete
@@ -432,7 +448,9 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
       __syncwarp();
       if (lane == 0) mbar_arrive(&qempty[qs]);
       if (id < 0) break;
-      const int nb = id / args.tiles_rb, rb = id % args.tiles_rb;
+      const int tpp = args.tiles_rb * args.tiles_nb, lid = id % tpp;
+      const int nb = lid / args.tiles_rb, rb = lid % args.tiles_rb;
+      const TcProb& P = maps.p[id / tpp];
       const int a = tile & 1;
       const uint32_t use = uint32_t(tile >> 1);
       mbar_wait(&tfull[a], use & 1);
@@ -487,9 +505,9 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
           if (lane == 0) {
             if (row0 < args.n && !(args.ablate & 1)) {
               if (args.overwrite)
-                tma_store_2d(&maps.c, buf, args.c_col0 + col0 + EC * h, row0);
+                tma_store_2d(&P.c, buf, P.c_col0 + col0 + EC * h, row0);
               else
-                tma_reduce_add_2d(&maps.c, buf, args.c_col0 + col0 + EC * h, row0);
+                tma_reduce_add_2d(&P.c, buf, P.c_col0 + col0 + EC * h, row0);
             }
             asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
           }
@@ -799,17 +817,65 @@ int split_operand(int device, Scratch& sc, const void* x, int64_t ldx, int64_t r
 }
 }  // namespace
 
-// 3xTF32 operands already split (paco_tf32_split): A hi/lo n x k, B^T hi/lo m x k.
+// 3xTF32 operands already split (paco_tf32_split): A hi/lo n x k, B^T hi/lo m x k,
+// one entry per problem of a batch.
 struct Presplit {
   const void *ah, *al, *bh, *bl;
-  int64_t lda, ldb;
+  void* c;
 };
 
+// Operand maps of one problem.  Plain calls split (3xTF32) or repack (bf16
+// with a pitch TMA cannot take) into stream-ordered scratch first.
 template <class K>
-int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B, int64_t ldb,
-              void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces, int n_pieces,
-              int flags, const Presplit* pre = nullptr) {
+int build_operands(int device, Scratch& sc, cudaStream_t stream, const void* A, int64_t lda, const void* B,
+                   int64_t ldb, int64_t n, int64_t m, int64_t k, const Presplit* pre, int64_t pre_lda,
+                   int64_t pre_ldb, tc::TcProb& P) {
   using L = tc::Layout<K>;
+  int rc;
+  if constexpr (K::NOPS == 1) {
+    if ((rc = repack(device, sc, &A, &lda, n, k, K::ELEM, stream))) return rc;
+    if ((rc = repack(device, sc, &B, &ldb, k, m, K::ELEM, stream))) return rc;
+    if ((rc = make_map(&P.a[0], K::DT, K::ELEM, A, n, k, lda, K::BK, tc::BM, &P.a_col0[0]))) return rc;
+    if ((rc = make_map(&P.b[0], K::DT, K::ELEM, B, k, m, ldb, L::BOX_N, K::BK, &P.b_col0[0]))) return rc;
+  } else {
+    const void *ah, *al, *bh, *bl;
+    int64_t lda2, ldb2;
+    if (pre) {
+      if (!K::B_KMAJOR) {
+        set_error("internal: pre-split B operands are K-major");
+        return PACO_ERR_UNSUPPORTED;
+      }
+      ah = pre->ah, al = pre->al, bh = pre->bh, bl = pre->bl, lda2 = pre_lda, ldb2 = pre_ldb;
+      if (!pitch_ok(ah, lda2, 4) || !pitch_ok(al, lda2, 4) || !pitch_ok(bh, ldb2, 4) || !pitch_ok(bl, ldb2, 4)) {
+        set_error("paco_mm_tf32x3: operand row pitches must be multiples of 16 bytes");
+        return PACO_ERR_UNSUPPORTED;
+      }
+    } else {
+      if ((rc = split_operand(device, sc, A, lda, n, k, false, stream, &ah, &al, &lda2))) return rc;
+      if ((rc = split_operand(device, sc, B, ldb, k, m, K::B_KMAJOR, stream, &bh, &bl, &ldb2))) return rc;
+    }
+    if ((rc = make_map(&P.a[0], K::DT, K::ELEM, ah, n, k, lda2, K::BK, tc::BM, &P.a_col0[0]))) return rc;
+    if ((rc = make_map(&P.a[1], K::DT, K::ELEM, al, n, k, lda2, K::BK, tc::BM, &P.a_col0[1]))) return rc;
+    if constexpr (K::B_KMAJOR) {
+      if ((rc = make_map(&P.b[0], K::DT, K::ELEM, bh, m, k, ldb2, K::BK, K::BN, &P.b_col0[0]))) return rc;
+      if ((rc = make_map(&P.b[1], K::DT, K::ELEM, bl, m, k, ldb2, K::BK, K::BN, &P.b_col0[1]))) return rc;
+    } else {
+      if ((rc = make_map(&P.b[0], K::DT, K::ELEM, bh, k, m, ldb2, L::BOX_N, K::BK, &P.b_col0[0]))) return rc;
+      if ((rc = make_map(&P.b[1], K::DT, K::ELEM, bl, k, m, ldb2, L::BOX_N, K::BK, &P.b_col0[1]))) return rc;
+    }
+  }
+  return PACO_OK;
+}
+
+template <class K>
+int build_output(tc::TcProb& P, void* C, int64_t ldc, int64_t n, int64_t m) {
+  return make_map(&P.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, n, m, ldc, K::EPI_COLS, 32, &P.c_col0,
+                  K::EPI_COLS == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+template <class K>
+int check_tc_call(void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces, int n_pieces,
+                  int flags) {
   if (pieces && n_pieces > 0) {
     set_error("the tcgen05 kernels take their own CTA plan (pass pieces=NULL)");
     return PACO_ERR_UNSUPPORTED;
@@ -827,44 +893,59 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
     set_error("PACO_MM_OVERWRITE cannot be combined with atomic folding");
     return PACO_ERR_ARG;
   }
+  return PACO_OK;
+}
+
+template <class K>
+int run_tc(int device, Scratch& sc, cudaStream_t stream, const tc::TcMaps& maps, int count, int64_t n, int64_t m,
+           int64_t k, int flags) {
+  using L = tc::Layout<K>;
   int rc;
-  Scratch sc;  // freed (stream-ordered) when this call returns
-  tc::TcMaps maps;
-  int32_t a_off = 0, b_off = 0, c_off = 0, t_off = 0;
-  if constexpr (K::NOPS == 1) {
-    // bf16: operands with a row pitch TMA cannot take are repacked first
-    if ((rc = repack(device, sc, &A, &lda, n, k, K::ELEM, stream))) return rc;
-    if ((rc = repack(device, sc, &B, &ldb, k, m, K::ELEM, stream))) return rc;
-    if ((rc = make_map(&maps.a[0], K::DT, K::ELEM, A, n, k, lda, K::BK, tc::BM, &a_off))) return rc;
-    if ((rc = make_map(&maps.b[0], K::DT, K::ELEM, B, k, m, ldb, L::BOX_N, K::BK, &b_off))) return rc;
-  } else {
-    // 3xTF32: split both operands into packed hi/lo pairs
-    const void *ah, *al, *bh, *bl;
-    int64_t lda2, ldb2;
-    if (pre) {
-      if (!K::B_KMAJOR) {
-        set_error("internal: pre-split B operands are K-major");
-        return PACO_ERR_UNSUPPORTED;
-      }
-      ah = pre->ah, al = pre->al, bh = pre->bh, bl = pre->bl, lda2 = pre->lda, ldb2 = pre->ldb;
-      if (!pitch_ok(ah, lda2, 4) || !pitch_ok(al, lda2, 4) || !pitch_ok(bh, ldb2, 4) || !pitch_ok(bl, ldb2, 4)) {
-        set_error("paco_mm_tf32x3: operand row pitches must be multiples of 16 bytes");
-        return PACO_ERR_UNSUPPORTED;
-      }
-    } else {
-      if ((rc = split_operand(device, sc, A, lda, n, k, false, stream, &ah, &al, &lda2))) return rc;
-      if ((rc = split_operand(device, sc, B, ldb, k, m, K::B_KMAJOR, stream, &bh, &bl, &ldb2))) return rc;
-    }
-    if ((rc = make_map(&maps.a[0], K::DT, K::ELEM, ah, n, k, lda2, K::BK, tc::BM, &a_off))) return rc;
-    if ((rc = make_map(&maps.a[1], K::DT, K::ELEM, al, n, k, lda2, K::BK, tc::BM, &t_off))) return rc;
-    if constexpr (K::B_KMAJOR) {
-      if ((rc = make_map(&maps.b[0], K::DT, K::ELEM, bh, m, k, ldb2, K::BK, K::BN, &b_off))) return rc;
-      if ((rc = make_map(&maps.b[1], K::DT, K::ELEM, bl, m, k, ldb2, K::BK, K::BN, &t_off))) return rc;
-    } else {
-      if ((rc = make_map(&maps.b[0], K::DT, K::ELEM, bh, k, m, ldb2, L::BOX_N, K::BK, &b_off))) return rc;
-      if ((rc = make_map(&maps.b[1], K::DT, K::ELEM, bl, k, m, ldb2, L::BOX_N, K::BK, &t_off))) return rc;
-    }
+  tc::TcArgs args;
+  args.n = n;
+  args.m = m;
+  args.k = k;
+  args.count = count;
+  args.overwrite = (flags & PACO_MM_OVERWRITE) ? 1 : 0;
+  args.tiles_rb = int32_t((n + tc::BM - 1) / tc::BM);
+  args.tiles_nb = int32_t((m + K::BN - 1) / K::BN);
+  args.kblocks = int32_t((k + K::BK - 1) / K::BK);
+  {
+    static const int ablate = getenv("PACO_TC_ABLATE") ? atoi(getenv("PACO_TC_ABLATE")) : 0;
+    args.ablate = ablate;
+    args.trace = g_trace_buffer;
   }
+  const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb * count;
+  if (tiles > INT32_MAX) {
+    set_error("tcgen05 path: too many tiles");
+    return PACO_ERR_ARG;
+  }
+  const int grid = int(tiles < kNumSMs ? tiles : kNumSMs);
+  args.groups = (K::B_RES && count == 1) ? (args.tiles_nb < grid ? args.tiles_nb : grid) : 1;
+  {
+    void* counters;
+    if ((rc = scratch(device, sc, sizeof(int32_t) * args.groups, stream, &counters))) return rc;
+    PACO_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(int32_t) * args.groups, stream));
+    args.sched = static_cast<int32_t*>(counters);
+  }
+  auto kern = tc::tc_gemm_kernel<K>;
+  PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
+  kern<<<grid, L::THREADS, L::SMEM_ALLOC, stream>>>(maps, args);
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
+template <class K>
+int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B, int64_t ldb,
+              void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces, int n_pieces,
+              int flags) {
+  int rc;
+  if ((rc = check_tc_call<K>(C, ldc, n, m, k, pieces, n_pieces, flags))) return rc;
+  Scratch sc;  // freed (stream-ordered) when this call returns
+  static tc::TcMaps maps;  // ~5.6 KB, copied into the launch's parameter buffer
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if ((rc = build_operands<K>(device, sc, stream, A, lda, B, ldb, n, m, k, nullptr, 0, 0, maps.p[0]))) return rc;
   void* c_user = nullptr;
   int64_t ldc_user = ldc;
   if (!pitch_ok(C, ldc, 4)) {
@@ -877,41 +958,50 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
     C = p;
     ldc = ld2;
   }
-  if ((rc = make_map(&maps.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, n, m, ldc, K::EPI_COLS, 32, &c_off,
-                     K::EPI_COLS == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)))
-    return rc;
-  tc::TcArgs args;
-  args.n = n;
-  args.m = m;
-  args.k = k;
-  args.a_col0 = a_off;
-  args.b_col0 = b_off;
-  args.c_col0 = c_off;
-  args.overwrite = (flags & PACO_MM_OVERWRITE) ? 1 : 0;
-  args.tiles_rb = int32_t((n + tc::BM - 1) / tc::BM);
-  args.tiles_nb = int32_t((m + K::BN - 1) / K::BN);
-  args.kblocks = int32_t((k + K::BK - 1) / K::BK);
-  {
-    static const int ablate = getenv("PACO_TC_ABLATE") ? atoi(getenv("PACO_TC_ABLATE")) : 0;
-    args.ablate = ablate;
-    args.trace = g_trace_buffer;
-  }
-  const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb;
-  const int grid = int(tiles < kNumSMs ? tiles : kNumSMs);
-  args.groups = K::B_RES ? (args.tiles_nb < grid ? args.tiles_nb : grid) : 1;
-  {
-    void* counters;
-    if ((rc = scratch(device, sc, sizeof(int32_t) * args.groups, stream, &counters))) return rc;
-    PACO_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(int32_t) * args.groups, stream));
-    args.sched = static_cast<int32_t*>(counters);
-  }
-  auto kern = tc::tc_gemm_kernel<K>;
-  PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
-  kern<<<grid, L::THREADS, L::SMEM_ALLOC, stream>>>(maps, args);
-  PACO_CUDA_TRY(cudaGetLastError());
+  if ((rc = build_output<K>(maps.p[0], C, ldc, n, m))) return rc;
+  if ((rc = run_tc<K>(device, sc, stream, maps, 1, n, m, k, flags))) return rc;
   if (c_user)
     PACO_CUDA_TRY(cudaMemcpy2DAsync(c_user, ldc_user * 4, C, ldc * 4, m * 4, n, cudaMemcpyDeviceToDevice, stream));
   return PACO_OK;
+}
+
+// A batch of same-shape 3xTF32 problems from pre-split operands, one launch
+// (one tile queue): Strassen's seven leaf products of a node.
+template <class K>
+int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* pre, int64_t lda, int64_t ldb,
+                    int64_t ldc, int64_t n, int64_t m, int64_t k, int flags) {
+  int rc;
+  if (count < 1 || count > tc::kMaxBatch) {
+    set_error("paco_mm_tf32x3: count=%d (1..%d)", count, tc::kMaxBatch);
+    return PACO_ERR_ARG;
+  }
+  for (int q = 0; q < count; ++q) {
+    if ((rc = check_tc_call<K>(pre[q].c, ldc, n, m, k, nullptr, 0, flags))) return rc;
+    if (!pitch_ok(pre[q].c, ldc, 4)) {
+      set_error("paco_mm_tf32x3: C row pitch must be a multiple of 16 bytes");
+      return PACO_ERR_UNSUPPORTED;
+    }
+  }
+  Scratch sc;
+  static tc::TcMaps maps;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int q = 0; q < count; ++q) {
+    if ((rc = build_operands<K>(device, sc, stream, nullptr, 0, nullptr, 0, n, m, k, &pre[q], lda, ldb, maps.p[q])))
+      return rc;
+    if ((rc = build_output<K>(maps.p[q], pre[q].c, ldc, n, m))) return rc;
+  }
+  return run_tc<K>(device, sc, stream, maps, count, n, m, k, flags);
+}
+
+// 3xTF32 tile width: N = 256 halves the B-operand traffic per output (the
+// kernel is L2-bandwidth bound at N = 128: 48 flop per loaded byte) but only
+// pays when the batch has enough tiles for the 148 SMs (4096^3 alone: 512
+// tiles = 3.5 per SM).  PACO_TF32_V=0/1 forces 128/256.
+bool tf32_wide(int64_t n, int64_t m, int count) {
+  static const int v = getenv("PACO_TF32_V") ? atoi(getenv("PACO_TF32_V")) : -1;
+  if (v >= 0) return v == 1;
+  return ((n + 127) / 128) * ((m + 255) / 256) * count >= 6 * kNumSMs;
 }
 
 int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B, int64_t ldb,
@@ -937,15 +1027,25 @@ int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t ld
 int launch_mm_f32_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const void* B, int64_t ldb,
                      void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces,
                      int n_pieces, int flags) {
+  if (tf32_wide(n, m, 1))
+    return launch_tc<tc::KindTF32x3T<256, 2>>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces,
+                                              flags);
   return launch_tc<tc::KindTF32x3>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
 }
 
-int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, const void* ah, const void* al, int64_t lda,
-                              const void* bth, const void* btl, int64_t ldb, void* C, int64_t ldc, int64_t n,
-                              int64_t m, int64_t k, int flags) {
-  const Presplit pre{ah, al, bth, btl, lda, ldb};
-  return launch_tc<tc::KindTF32x3>(device, stream, nullptr, 0, nullptr, 0, C, ldc, n, m, k, nullptr, 0, flags,
-                                   &pre);
+int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, int count, const void* const* ah,
+                              const void* const* al, int64_t lda, const void* const* bth, const void* const* btl,
+                              int64_t ldb, void* const* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
+                              int flags) {
+  Presplit pre[tc::kMaxBatch];
+  if (count < 1 || count > tc::kMaxBatch) {
+    set_error("paco_mm_tf32x3: count=%d (1..%d)", count, tc::kMaxBatch);
+    return PACO_ERR_ARG;
+  }
+  for (int q = 0; q < count; ++q) pre[q] = Presplit{ah[q], al[q], bth[q], btl[q], C[q]};
+  if (tf32_wide(n, m, count))
+    return launch_tc_batch<tc::KindTF32x3T<256, 2>>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags);
+  return launch_tc_batch<tc::KindTF32x3>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags);
 }
 
 int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,

@@ -284,18 +284,28 @@ def _split(stream, terms, src: View, hi: torch.Tensor, lo: torch.Tensor, transpo
 def _leaf_level_tf32(A: View, B: View, C: View, stream) -> None:
     """A node whose seven children are 3xTF32 leaves: each S_r / T_r is formed
     directly as its split tf32 pair (A-side row-major, B-side transposed), so
-    the sums never round-trip through HBM as fp32; then M_r = S_r T_r on
-    tcgen05 (paco_mm_tf32x3) and the C blocks are combined as usual."""
+    the sums never round-trip through HBM as fp32; then all seven products
+    M_r = S_r T_r run as ONE batched tcgen05 launch (paco_mm_tf32x3, count 7:
+    their tiles share one dynamic queue, so 7 x tiles fill the 148 SMs where
+    one product's tiles alone quantise badly), and the C blocks are combined."""
     h = C.rows // 2
     ws = _Workspace(C.rows, torch.float32, C.device, A, B, leaf_split=True)
-    ah, al, bh, bl = (torch.empty((h, h), dtype=torch.float32, device=C.device) for _ in range(4))
-    lib = nat.load()
-    for r in range(1, 8):  # one stream: the operand buffers are reused in order
+    ops = [[torch.empty((h, h), dtype=torch.float32, device=C.device) for _ in range(4)] for _ in range(7)]
+    for r in range(1, 8):
+        ah, al, bh, bl = ops[r - 1]
         _split(stream, S_TERMS[r], A, ah, al, transpose=False)
         _split(stream, T_TERMS[r], B, bh, bl, transpose=True)
-        M = ws.M[r - 1]
-        nat.check(lib.paco_mm_tf32x3(C.device, stream.cuda_stream, ah.data_ptr(), al.data_ptr(), h,
-                                     bh.data_ptr(), bl.data_ptr(), h, M.ptr, M.ld, h, h, h, nat.MM_OVERWRITE))
+
+    def arr(vals):
+        return (ctypes.c_void_p * 7)(*vals)
+
+    nat.check(nat.load().paco_mm_tf32x3(
+        C.device, stream.cuda_stream, 7, arr([o[0].data_ptr() for o in ops]), arr([o[1].data_ptr() for o in ops]), h,
+        arr([o[2].data_ptr() for o in ops]), arr([o[3].data_ptr() for o in ops]), h,
+        arr([M.ptr for M in ws.M]), ws.M[0].ld, h, h, h, nat.MM_OVERWRITE))
+    for o in ops:
+        for t in o:
+            t.record_stream(stream)
     _combine(ws, C, nat.DT_F32, stream)
 
 

@@ -107,9 +107,15 @@ def test_tf32_split_fused_sum_and_presplit_mm(transpose):
     bth = torch.empty(m, (k + 3) // 4 * 4, device="cuda"); btl = torch.empty_like(bth)
     yin = (ctypes.c_void_p * 1)(Y.data_ptr()); yld = (ctypes.c_int64 * 1)(Y.stride(0)); one = (ctypes.c_int32 * 1)(1)
     nat.check(lib.paco_tf32_split(0, None, 1, yin, yld, one, k, m, 1, bth.data_ptr(), btl.data_ptr(), bth.stride(0)))
-    C = torch.zeros(n, m, device="cuda")
-    nat.check(lib.paco_mm_tf32x3(0, None, ah.data_ptr(), al.data_ptr(), ah.stride(0), bth.data_ptr(),
-                                 btl.data_ptr(), bth.stride(0), C.data_ptr(), C.stride(0), n, m, k, nat.MM_OVERWRITE))
+    # a batch of 3: the same product into three C's (one tile queue), C[1] accumulating
+    Cs = [torch.zeros(n, m, device="cuda") for _ in range(3)]
+    Cs[1].fill_(1.0)
+    arr = lambda xs: (ctypes.c_void_p * 3)(*xs)
+    nat.check(lib.paco_mm_tf32x3(0, None, 3, arr([ah.data_ptr()] * 3), arr([al.data_ptr()] * 3), ah.stride(0),
+                                 arr([bth.data_ptr()] * 3), arr([btl.data_ptr()] * 3), bth.stride(0),
+                                 arr([c.data_ptr() for c in Cs]), Cs[0].stride(0), n, m, k, 0))
     torch.cuda.synchronize()
     ref = want @ Y.double()
-    assert float((C.double() - ref).norm() / ref.norm()) < 1e-5
+    for q, C in enumerate(Cs):
+        got = C.double() - (1.0 if q == 1 else 0.0)
+        assert float((got - ref).norm() / ref.norm()) < 1e-5, q
