@@ -141,6 +141,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// Relaxed: no release fence, so an in-flight global atomic (the producer's
+// tile claim) does not stall it; the TMA's complete_tx orders the data.
+__device__ __forceinline__ void mbar_expect_tx_relaxed(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -215,6 +221,7 @@ struct TcArgs {
   int32_t groups;    // CTA c serves group c % groups: column blocks g, g + groups, ...
 };
 
+// slot 15 of each CTA: (entry, after setup, exit)
 __device__ __forceinline__ void tc_stamp(const TcArgs& a, int64_t tile, int field) {
   if (a.trace && tile < 16) {
     long long t;
@@ -234,9 +241,10 @@ __device__ __forceinline__ void tc_stamp(const TcArgs& a, int64_t tile, int fiel
 // reloads its B, and the groups advance through the row blocks in step.
 // A batch (count > 1, groups = 1) puts every problem's tiles in one queue:
 // id = problem * tiles_rb * tiles_nb + nb * tiles_rb + rb.
-__device__ __forceinline__ int32_t claim_tile(const TcArgs& a) {
-  const int g = int(blockIdx.x % uint32_t(a.groups));
-  const int32_t t = atomicAdd(&a.sched[g], 1);
+// The first tile of every CTA is static (its rank in its group) so 148
+// simultaneous atomics on one counter do not delay the start (~2 us measured);
+// later claims are atomics, issued one tile ahead by the producer.
+__device__ __forceinline__ int32_t tile_of(const TcArgs& a, int g, int32_t t) {
   if (a.groups == 1) {  // row-block-major: concurrent CTAs write whole rows of C, share A rows
     const int32_t tpp = a.tiles_rb * a.tiles_nb;
     if (t >= tpp * a.count) return -1;
@@ -246,6 +254,13 @@ __device__ __forceinline__ int32_t claim_tile(const TcArgs& a) {
   const int32_t nb = g + (t / a.tiles_rb) * a.groups;
   if (nb >= a.tiles_nb) return -1;
   return nb * a.tiles_rb + t % a.tiles_rb;
+}
+
+__device__ __forceinline__ int32_t claim_tile(const TcArgs& a, bool first) {
+  const int g = int(blockIdx.x % uint32_t(a.groups));
+  const int32_t in_group = int32_t((gridDim.x - g + a.groups - 1) / a.groups);
+  const int32_t t = first ? int32_t(blockIdx.x / a.groups) : in_group + atomicAdd(&a.sched[g], 1);
+  return tile_of(a, g, t);
 }
 
 // One problem: operand maps (hi/lo for 3xTF32), the output map, and the column
@@ -270,8 +285,8 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   uint64_t* empty = full + MAXR;
   uint64_t* tfull = empty + MAXR;
   uint64_t* tempty = tfull + 2;
-  uint64_t* bfull = tempty + 2;   // resident B landed (B_RES)
-  uint64_t* bempty = bfull + 1;   // MMAs reading the resident B completed (B_RES)
+  uint64_t* bfull = tempty + 2;   // resident B k block landed (B_RES; one per k block)
+  uint64_t* bempty = bfull + 4;   // MMAs reading the resident B completed (B_RES)
   constexpr int QD = 4;           // tile queue depth
   uint64_t* qfull = bempty + 1;   // tile id published by the producer
   uint64_t* qempty = qfull + QD;  // ... and read by the MMA warp + every epilogue warp
@@ -279,6 +294,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qid + QD);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) tc_stamp(args, 15, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -289,7 +305,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], K::EPI_WARPS);
     }
-    mbar_init(bfull, 1);
+    for (int kb = 0; kb < 4; ++kb) mbar_init(&bfull[kb], 1);
     mbar_init(bempty, 1);
     for (int j = 0; j < QD; ++j) {
       mbar_init(&qfull[j], 1);
@@ -313,6 +329,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) tc_stamp(args, 15, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -320,40 +337,45 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
       {
         uint32_t it = 0, bloads = 0;
         int loaded_nb = -1;
+        int32_t next = claim_tile(args, true);
         for (int64_t i = 0;; ++i) {
-          const int32_t id = claim_tile(args);
+          const int32_t id = next;
+          if (i == 0) tc_stamp(args, 15, 3);
           const int qs = int(i % QD);
           mbar_wait(&qempty[qs], (uint32_t(i / QD) & 1) ^ 1);
           qid[qs] = id;
           mbar_arrive(&qfull[qs]);
           if (id < 0) break;
+          next = claim_tile(args, false);  // one tile ahead; only the next publish (release) waits for it
           const int tpp = args.tiles_rb * args.tiles_nb, lid = id % tpp;
           const int nb = lid / args.tiles_rb, rb = lid % args.tiles_rb;
           const TcProb& P = maps.p[id / tpp];
           if constexpr (K::B_RES) {
             if (nb != loaded_nb) {  // (re)load the resident B column block
               if (bloads > 0) mbar_wait(bempty, (bloads - 1) & 1);
-              mbar_expect_tx(bfull, uint32_t(args.kblocks) * L::B_BYTES);
-              for (int kb = 0; kb < args.kblocks; ++kb)
+              for (int kb = 0; kb < args.kblocks; ++kb) {  // per k block: the first MMA starts early
+                mbar_expect_tx_relaxed(&bfull[kb], L::B_BYTES);
 #pragma unroll
                 for (int j = 0; j < BN / L::BOX_N; ++j)
-                  tma_load_2d(smem + L::b_res_off(kb) + j * (BK * 128), &P.b[0], bfull,
+                  tma_load_2d(smem + L::b_res_off(kb) + j * (BK * 128), &P.b[0], &bfull[kb],
                               P.b_col0[0] + nb * BN + L::BOX_N * j, kb * BK);
+              }
               loaded_nb = nb;
               ++bloads;
+              if (i == 0) tc_stamp(args, 15, 4);
             }
           }
           for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
             const int s = it % STAGES;
             mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-            if (kb == 0) tc_stamp(args, i, 0);
-            if (kb == args.kblocks - 1) tc_stamp(args, i, 1);
+            if (kb == 0 && i < 15) tc_stamp(args, i, 0);
+            if (kb == args.kblocks - 1 && i < 15) tc_stamp(args, i, 1);
             if constexpr (K::B_RES) {
-              mbar_expect_tx(&full[s], L::A_BYTES);
+              mbar_expect_tx_relaxed(&full[s], L::A_BYTES);
               tma_load_2d(smem + L::a_off(s, 0), &P.a[0], &full[s], P.a_col0[0] + kb * BK, rb * BM);
               continue;
             }
-            mbar_expect_tx(&full[s], K::NOPS * (L::A_BYTES + L::B_BYTES));
+            mbar_expect_tx_relaxed(&full[s], K::NOPS * (L::A_BYTES + L::B_BYTES));
 #pragma unroll
             for (int o = 0; o < K::NOPS; ++o) {
               tma_load_2d(smem + L::a_off(s, o), &P.a[o], &full[s], P.a_col0[o] + kb * BK, rb * BM);
@@ -377,6 +399,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
       // ---------------- MMA issuer ----------------
       uint32_t it = 0, buses = 0;
       int tile = 0, cur_nb = -1;
+      bool new_b = false;  // first tile on a freshly loaded B: wait per k block
       for (int64_t i = 0;; ++i, ++tile) {
         const int qs = int(i % QD);
         mbar_wait(&qfull[qs], uint32_t(i / QD) & 1);
@@ -389,7 +412,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
           const int nb = id / args.tiles_rb;
           if (nb != cur_nb) {
             if (cur_nb >= 0) umma_commit(bempty);  // the old B is free once its MMAs complete
-            mbar_wait(bfull, buses & 1);
+            new_b = true;
             ++buses;
             cur_nb = nb;
           }
@@ -399,9 +422,10 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
         const uint32_t d_tmem = tmem_base + uint32_t(a * BN);
         for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
           const int s = it % STAGES;
+          if (K::B_RES && new_b) mbar_wait(&bfull[kb], (buses - 1) & 1);
           mbar_wait(&full[s], (it / STAGES) & 1);
           tc_fence_after();
-          if (kb == 0) tc_stamp(args, i, 2);
+          if (kb == 0 && i < 15) tc_stamp(args, i, 2);
           uint64_t ad[K::NOPS], bd[K::NOPS];
 #pragma unroll
           for (int o = 0; o < K::NOPS; ++o) {
@@ -424,8 +448,9 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
           }
           umma_commit(&empty[s]);  // stage is free once these MMAs complete
         }
-        tc_stamp(args, i, 3);
+        if (i < 15) tc_stamp(args, i, 3);
         umma_commit(&tfull[a]);    // accumulator ready for the epilogue
+        new_b = false;
       }
     }
   } else {
@@ -455,7 +480,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
       const uint32_t use = uint32_t(tile >> 1);
       mbar_wait(&tfull[a], use & 1);
       tc_fence_after();
-      if (ew == 0 && lane == 0) tc_stamp(args, i, 4);
+      if (ew == 0 && lane == 0 && i < 15) tc_stamp(args, i, 4);
       const int row0 = rb * BM + 32 * q;
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + PER; c += 2) {
@@ -513,7 +538,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
           }
         }
       }
-      if (ew == 0 && lane == 0) tc_stamp(args, i, 5);
+      if (ew == 0 && lane == 0 && i < 15) tc_stamp(args, i, 5);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   }
@@ -523,6 +548,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   tc_fence_after();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(L::TMEM_COLS));
+  if (threadIdx.x == 0) tc_stamp(args, 15, 2);
 }
 
 }  // namespace tc

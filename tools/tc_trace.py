@@ -25,10 +25,17 @@ nat.check(lib.paco_debug_trace(None))
 t = tr.view(148, 16, 6).cpu().numpy().astype(np.float64)
 t0 = t[t > 0].min()
 t = np.where(t > 0, (t - t0) / 1e3, np.nan)   # us
+life = t[:, 15, :6]
+print("producer: first claim done median %.2f, resident B issued median %.2f us"
+      % (np.nanmedian(life[:, 3]), np.nanmedian(life[:, 4])))
+t = t[:, :15]
+print("CTA entry: min %.2f max %.2f | setup done: median %.2f | exit: min %.2f median %.2f max %.2f us"
+      % (np.nanmin(life[:, 0]), np.nanmax(life[:, 0]), np.nanmedian(life[:, 1]), np.nanmin(life[:, 2]),
+         np.nanmedian(life[:, 2]), np.nanmax(life[:, 2])))
 print("fields: P0 first-load  P1 last-load  M0 stage-ready  M1 mma-issued  E0 acc-ready  E1 stores-issued (us)")
 for cta in (0, 1, 74, 147):
     print(f"CTA {cta}")
-    for i in range(16):
+    for i in range(15):
         if np.isnan(t[cta, i]).all():
             continue
         print("  tile %2d " % i + " ".join("%7.2f" % x for x in t[cta, i]))
