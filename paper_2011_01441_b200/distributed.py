@@ -225,8 +225,8 @@ class FusedDistributedMM:
     owners (element atomics, ``PACO_MM_REMOTE``), locally with the TMA bulk
     reduction -- so the plan's REDUCE tasks vanish: no temporaries, no fold
     pass, no NCCL call on the data path.  Remote folds use the TMA bulk
-    reduction too when a start-up probe shows it lands correctly in peer
-    memory (``remote_bulk``).  Construct on every rank (it exchanges IPC
+    reduction too when ``PACO_REMOTE_BULK=1`` and a start-up probe shows it
+    lands correctly in peer memory (``remote_bulk``).  Construct on every rank (it exchanges IPC
     handles with ``all_gather_object``).
     """
 
@@ -282,6 +282,12 @@ class FusedDistributedMM:
         from .device import View
         from .mm import launch_fill, launch_mm
 
+        import os
+        # Off unless asked for: a TMA bulk reduction that the fabric rejected
+        # would leave a sticky CUDA error, and element atomics over NVLink are
+        # always legal for peer-mapped memory.
+        if os.environ.get("PACO_REMOTE_BULK", "0") != "1":
+            return False
         if self.world == 1 or self.n < 128 or self.m < 128:
             return False
         dev = self.device

@@ -36,8 +36,8 @@ def _inputs(n, m, k, seed):
     return A, B, C
 
 
-def _worker(rank, world, port, cases, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+def _worker(rank, world, port, cases, q, remote_bulk="0"):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PACO_REMOTE_BULK=remote_bulk)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     from paper_2011_01441_b200 import _native as nat
@@ -72,13 +72,15 @@ def _worker(rank, world, port, cases, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_fused_ipc_distributed_matches_oracle(world):
+@pytest.mark.parametrize("world,remote_bulk", [(2, "0"), (3, "0"), (2, "1")])
+def test_fused_ipc_distributed_matches_oracle(world, remote_bulk):
+    """Remote folds as element atomics (default) and, with PACO_REMOTE_BULK=1,
+    as TMA bulk reductions into the peer's IPC mapping (probed first)."""
     cases = [("one_piece", 96, 80, 700), ("one_piece", 200, 150, 260), ("paco", 130, 90, 333)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q, remote_bulk)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -87,4 +89,5 @@ def test_fused_ipc_distributed_matches_oracle(world):
     res = sorted(q.get(timeout=5) for _ in cases)
     assert all(r[1] for r in res), res
     assert any(r[2] > 0 for r in res)
-    print("remote bulk folds:", [r[3] for r in res])
+    # the probe needs a C of >= 128 x 128: only the 200 x 150 case can use bulk folds
+    assert [r[3] for r in res] == [False, remote_bulk == "1", False], res
