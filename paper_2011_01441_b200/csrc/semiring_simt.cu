@@ -30,6 +30,10 @@ namespace paco {
 
 // 8192^3 (min,+) with 1/2/3/4/5/8 waves of 296: 37.5/35.2/34.6/34.3/35.1/35.6 ms
 constexpr int kDefaultWaves = 4;
+#ifndef PACO_SIMT_MBAR
+#define PACO_SIMT_MBAR 1
+#endif
+constexpr bool kMbarPipe = PACO_SIMT_MBAR != 0;  // split arrive/wait stage ring (vs __syncthreads)
 constexpr double kDefaultKw = 1.0;
 constexpr int kMaxKSplit = 64;
 constexpr double kVisitK = 96.0;  // per-visit cost in k elements
@@ -400,6 +404,77 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
   const int total = pc.tn * pc.tm * KT;
 
   TileWalk ld{0, 0, 0};
+  typename Op::Acc acc[C::TM][C::TN];
+#pragma unroll
+  for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::identity();
+  TileWalk cw{0, 0, 0};
+
+  if constexpr (kMbarPipe) {
+    // Split arrive/wait ring: full[s] completes when every thread's cp.async
+    // into stage s has landed (cp.async.mbarrier.arrive.noinc); empty[s]
+    // when every thread has finished reading it.  A stage is refilled one
+    // iteration after it was consumed, so the empty wait is almost never a
+    // stall -- unlike a __syncthreads per k step, which makes all 8 warps
+    // meet every stage.
+    __shared__ uint64_t full[C::STAGES], empty[C::STAGES];
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < C::STAGES; ++s) {
+        mbar_init_cta(&full[s], C::THREADS);
+        mbar_init_cta(&empty[s], C::THREADS);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < C::STAGES - 1; ++s) {
+      if (s < total) {
+        load_stage<Op, kVec>(args, As + s * C::A_STAGE, Bs + s * C::B_STAGE,
+                             int64_t(pc.ti0 + ld.ti) * C::BM, int64_t(pc.tj0 + ld.tj) * C::BN,
+                             kb + int64_t(ld.kt) * C::BK, kend);
+        cp_async_arrive_noinc(&full[s]);
+        ld.next(pc.tm, KT);
+      }
+    }
+    for (int it = 0; it < total; ++it) {
+      const int s = it % C::STAGES;
+      mbar_wait_cta(&full[s], uint32_t(it / C::STAGES) & 1);
+      const int64_t k0 = kb + int64_t(cw.kt) * C::BK;
+      const int kvalid = (kend - k0 < C::BK) ? int(kend - k0) : C::BK;
+      compute_stage<Op>(acc, As + s * C::A_STAGE, Bs + s * C::B_STAGE, kvalid);
+      if (cw.kt == KT - 1) {
+        const int64_t row0 = int64_t(pc.ti0 + cw.ti) * C::BM, col0 = int64_t(pc.tj0 + cw.tj) * C::BN;
+        bool done = false;
+        if constexpr (!C::kWide) {
+          const int64_t cols = (args.m - col0 < C::BN) ? args.m - col0 : C::BN;
+          const uint32_t bytes = uint32_t(cols * sizeof(typename Op::TC));
+          if (args.bulk_ok && (bytes % 16) == 0) {  // stages the tile in stage s (CTA-wide syncs)
+            epilogue_bulk<Op>(args, acc, row0, col0, As + s * C::A_STAGE, Bs + s * C::B_STAGE, bytes);
+            done = true;
+          }
+        }
+        if (!done) epilogue<Op>(args, acc, row0, col0, atomic);
+#pragma unroll
+        for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::identity();
+      }
+      cw.next(pc.tm, KT);
+      mbar_arrive_cta(&empty[s]);
+      const int nl = it + C::STAGES - 1;  // refill the stage consumed in the previous iteration
+      if (nl < total) {
+        const int sl = nl % C::STAGES;
+        mbar_wait_cta(&empty[sl], (uint32_t(nl / C::STAGES) & 1) ^ 1);
+        load_stage<Op, kVec>(args, As + sl * C::A_STAGE, Bs + sl * C::B_STAGE,
+                             int64_t(pc.ti0 + ld.ti) * C::BM, int64_t(pc.tj0 + ld.tj) * C::BN,
+                             kb + int64_t(ld.kt) * C::BK, kend);
+        cp_async_arrive_noinc(&full[sl]);
+        ld.next(pc.tm, KT);
+      }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  } else {
 #pragma unroll
   for (int s = 0; s < C::STAGES - 1; ++s) {
     if (s < total) {
@@ -411,13 +486,6 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
     cp_async_commit();
   }
 
-  typename Op::Acc acc[C::TM][C::TN];
-#pragma unroll
-  for (int i = 0; i < C::TM; ++i)
-#pragma unroll
-    for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::identity();
-
-  TileWalk cw{0, 0, 0};
   int s_load = C::STAGES - 1, s_comp = 0;
   for (int it = 0; it < total; ++it) {
     cp_async_wait<C::STAGES - 2>();
@@ -454,6 +522,7 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
         for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::identity();
     }
     cw.next(pc.tm, KT);
+  }
   }
   cp_async_wait<0>();
   if (args.trace && threadIdx.x == 0) {
