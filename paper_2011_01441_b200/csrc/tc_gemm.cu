@@ -50,6 +50,7 @@ template <int ST, int EB, int EW, int EC = 32>
 struct KindBF16T {
   static constexpr int BN = 256, BK = 64, UMMA_K = 16, STAGES = ST, ELEM = 2, NOPS = 1, PASSES = 1;
   static constexpr int RING_BYTES = ST * 48 * 1024, EPI_WARPS = EW, EPI_BUFS = EB, KB_MAX = 0, EPI_COLS = EC;
+  static constexpr int SWZ = 128;  // operand swizzle (bytes per K-major row)
   static constexpr bool B_KMAJOR = false, B_RES = false;
   // F32 accumulate, BF16 A/B (format 1), A K-major, B MN-major (bit 16)
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
@@ -58,11 +59,13 @@ struct KindBF16T {
 };
 using KindBF16 = KindBF16T<3, 2, 8>;
 // fp32 inputs as 3xTF32 (hi/lo operand tiles), N=128 tiles, 32-deep k blocks.
-template <int BN_, int ST>
+// BK_ = 32: 128-byte K-major rows (SWIZZLE_128B); BK_ = 16: 64-byte rows
+// (SWIZZLE_64B) -- half the bytes per stage, so twice the stages in the ring.
+template <int BN_, int ST, int BK_ = 32>
 struct KindTF32x3T {
-  static constexpr int BN = BN_, BK = 32, UMMA_K = 8, STAGES = ST, ELEM = 4, NOPS = 2, PASSES = 3;
+  static constexpr int BN = BN_, BK = BK_, UMMA_K = 8, STAGES = ST, ELEM = 4, NOPS = 2, PASSES = 3;
   static constexpr int RING_BYTES = ST * 2 * (128 + BN_) * BK * 4, EPI_WARPS = 4, EPI_BUFS = 2, KB_MAX = 0,
-                       EPI_COLS = 32;
+                       EPI_COLS = 32, SWZ = BK_ * 4;
   static constexpr bool B_KMAJOR = true, B_RES = false;  // B^T tiles (the split writes B transposed)
   // F32 accumulate, TF32 A/B (format 2), both K-major
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
@@ -70,6 +73,10 @@ struct KindTF32x3T {
   static constexpr CUtensorMapDataType DT = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
 };
 using KindTF32x3 = KindTF32x3T<128, 3>;
+// Wide: N = 256 tiles, 16-deep k blocks (64-byte rows, SWIZZLE_64B) so four
+// 48 KB stages fit beside the epilogue buffers -- measured best of
+// {<256,2,32>, <256,4,16>, <128,6,16>} on cfg5 (36.9 / 34.6 / 48.1 ms).
+using KindTF32x3W = KindTF32x3T<256, 4, 16>;
 // (MN-major B -- bit 16 of the descriptor -- is what the bf16 kind uses; with
 // kind::tf32 it returned all-zero products here, hence the transposed split.)
 
@@ -82,7 +89,7 @@ using KindTF32x3 = KindTF32x3T<128, 3>;
 template <int AST, int EB, int EW = 8, int EC = 32>
 struct KindBF16Res {
   static constexpr int BN = 256, BK = 64, UMMA_K = 16, STAGES = AST, ELEM = 2, NOPS = 1, PASSES = 1;
-  static constexpr int KB_MAX = 4, EPI_WARPS = EW, EPI_BUFS = EB, EPI_COLS = EC;
+  static constexpr int KB_MAX = 4, EPI_WARPS = EW, EPI_BUFS = EB, EPI_COLS = EC, SWZ = 128;
   static constexpr int RING_BYTES = KB_MAX * BN * BK * 2 + AST * 128 * BK * 2;
   static constexpr bool B_KMAJOR = false, B_RES = true;
   static constexpr uint32_t IDESC = KindBF16::IDESC;
@@ -108,6 +115,17 @@ struct Layout {
   __device__ static int b_off(int stage, int op) { return stage * STAGE_BYTES + K::NOPS * A_BYTES + op * B_BYTES; }
   __device__ static int b_res_off(int kb) { return kb * B_BYTES; }
 };
+
+// K-major, 64B swizzle: 64-byte rows, 8-row groups 512 B apart, layout type 4.
+__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(512 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;
+  return d;
+}
 
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
   // K-major, 128B swizzle: rows of 128 B, 8-row groups 1024 B apart (SBO),
@@ -430,8 +448,13 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
 #pragma unroll
           for (int o = 0; o < K::NOPS; ++o) {
             const int aoff = L::a_off(s, o), boff = K::B_RES ? L::b_res_off(kb) : L::b_off(s, o);
-            ad[o] = smem_desc_sw128(smem_u32(smem + aoff));
-            bd[o] = K::B_KMAJOR ? smem_desc_sw128(smem_u32(smem + boff)) : smem_desc_mn_sw128(smem_u32(smem + boff), BK);
+            if constexpr (K::SWZ == 64) {
+              ad[o] = smem_desc_sw64(smem_u32(smem + aoff));
+              bd[o] = smem_desc_sw64(smem_u32(smem + boff));  // B^T, K-major
+            } else {
+              ad[o] = smem_desc_sw128(smem_u32(smem + aoff));
+              bd[o] = K::B_KMAJOR ? smem_desc_sw128(smem_u32(smem + boff)) : smem_desc_mn_sw128(smem_u32(smem + boff), BK);
+            }
           }
 #pragma unroll
           for (int kk = 0; kk < BK / K::UMMA_K; ++kk) {
@@ -880,11 +903,12 @@ int build_operands(int device, Scratch& sc, cudaStream_t stream, const void* A, 
       if ((rc = split_operand(device, sc, A, lda, n, k, false, stream, &ah, &al, &lda2))) return rc;
       if ((rc = split_operand(device, sc, B, ldb, k, m, K::B_KMAJOR, stream, &bh, &bl, &ldb2))) return rc;
     }
-    if ((rc = make_map(&P.a[0], K::DT, K::ELEM, ah, n, k, lda2, K::BK, tc::BM, &P.a_col0[0]))) return rc;
-    if ((rc = make_map(&P.a[1], K::DT, K::ELEM, al, n, k, lda2, K::BK, tc::BM, &P.a_col0[1]))) return rc;
+    constexpr CUtensorMapSwizzle SW = K::SWZ == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+    if ((rc = make_map(&P.a[0], K::DT, K::ELEM, ah, n, k, lda2, K::BK, tc::BM, &P.a_col0[0], SW))) return rc;
+    if ((rc = make_map(&P.a[1], K::DT, K::ELEM, al, n, k, lda2, K::BK, tc::BM, &P.a_col0[1], SW))) return rc;
     if constexpr (K::B_KMAJOR) {
-      if ((rc = make_map(&P.b[0], K::DT, K::ELEM, bh, m, k, ldb2, K::BK, K::BN, &P.b_col0[0]))) return rc;
-      if ((rc = make_map(&P.b[1], K::DT, K::ELEM, bl, m, k, ldb2, K::BK, K::BN, &P.b_col0[1]))) return rc;
+      if ((rc = make_map(&P.b[0], K::DT, K::ELEM, bh, m, k, ldb2, K::BK, K::BN, &P.b_col0[0], SW))) return rc;
+      if ((rc = make_map(&P.b[1], K::DT, K::ELEM, bl, m, k, ldb2, K::BK, K::BN, &P.b_col0[1], SW))) return rc;
     } else {
       if ((rc = make_map(&P.b[0], K::DT, K::ELEM, bh, k, m, ldb2, L::BOX_N, K::BK, &P.b_col0[0]))) return rc;
       if ((rc = make_map(&P.b[1], K::DT, K::ELEM, bl, k, m, ldb2, L::BOX_N, K::BK, &P.b_col0[1]))) return rc;
@@ -1026,7 +1050,7 @@ int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* 
 // tiles = 3.5 per SM).  PACO_TF32_V=0/1 forces 128/256.
 bool tf32_wide(int64_t n, int64_t m, int count) {
   static const int v = getenv("PACO_TF32_V") ? atoi(getenv("PACO_TF32_V")) : -1;
-  if (v >= 0) return v == 1;
+  if (v >= 0) return v != 0;
   return ((n + 127) / 128) * ((m + 255) / 256) * count >= 6 * kNumSMs;
 }
 
@@ -1054,8 +1078,7 @@ int launch_mm_f32_tc(int device, cudaStream_t stream, const void* A, int64_t lda
                      void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces,
                      int n_pieces, int flags) {
   if (tf32_wide(n, m, 1))
-    return launch_tc<tc::KindTF32x3T<256, 2>>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces,
-                                              flags);
+    return launch_tc<tc::KindTF32x3W>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
   return launch_tc<tc::KindTF32x3>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
 }
 
@@ -1070,7 +1093,7 @@ int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, int count, const 
   }
   for (int q = 0; q < count; ++q) pre[q] = Presplit{ah[q], al[q], bth[q], btl[q], C[q]};
   if (tf32_wide(n, m, count))
-    return launch_tc_batch<tc::KindTF32x3T<256, 2>>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags);
+    return launch_tc_batch<tc::KindTF32x3W>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags);
   return launch_tc_batch<tc::KindTF32x3>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags);
 }
 
