@@ -192,7 +192,9 @@ def main():
     torch.cuda.set_device(dev)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = os.environ.get("PACO_BENCH_BACKEND", "nccl")  # gloo: N ranks on fewer GPUs (testing)
+        # NCCL needs one GPU per rank; with more ranks than GPUs (a test box) use gloo
+        backend = os.environ.get("PACO_BENCH_BACKEND",
+                                 "nccl" if torch.cuda.device_count() >= world else "gloo")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
