@@ -2,9 +2,11 @@
 
 * ``mm_seq``      -- matmul.py:342-366: C <- C (+) A (x) B on one device.  The
   reference recursion (halve the longest axis down to 32^3 NumPy leaves,
-  matmul.py:369-397) is replaced by one persistent sm_100a launch whose CTAs
-  each own one cuboid of the CTA-level PACO plan (MM-1-Piece over the tile
-  grid, 148 SMs x resident CTAs).
+  matmul.py:369-397) is replaced by one sm_100a launch whose CTAs each own a
+  piece of the CTA-level plan (default: one C tile per CTA with a cost-model
+  k split; the balanced PACO cuboid plan on request, PACO_MM_PACO_PLAN).
+  Pinned host operands are streamed through a k-first / rows-last
+  H2D-compute-D2H pipeline.
 * ``mm_execute``  -- matmul.py:417-462: binds a plan to device work.  COMPUTE
   tasks launch ``paco_mm`` on sub-views; REDUCE tasks launch ``paco_fold``
   (t (+)= temp; temp = zero).  Plan workers map to (device, stream) pairs.
@@ -86,7 +88,7 @@ def mm_seq(A, B, C, semiring: Semiring = SEMIRING_INT, base: int = DEFAULT_BASE,
 
     ``base`` is accepted for signature compatibility: the leaf size of the
     reference recursion has no role once the CTA-level plan tiles the cuboid.
-    ``pieces`` overrides the CTA-level PACO plan (tile-unit cuboids);
+    ``pieces`` overrides the CTA-level plan (tile-unit cuboids);
     ``overwrite`` declares C == zero so the kernel does not read it.
     """
     n, m, k = _shape_check(A, B, C)
@@ -118,7 +120,7 @@ _PIPE_MODE = os.environ.get("PACO_PIPE_MODE", "")          # "k" | "grid" | "" (
 _PIPE_MIN_K = 512
 # k-phased schedule: first k chunk, growth factor, chunk cap, share of k in the
 # row-blocked last phase, and its number of row blocks
-_KP = tuple(float(x) for x in os.environ.get("PACO_PIPE_KP", "256,2,2048,0.25,8").split(","))
+_KP = tuple(float(x) for x in os.environ.get("PACO_PIPE_KP", "128,2,2048,0.25,16").split(","))
 
 
 def _pinned_host(x, dtype) -> bool:
