@@ -653,9 +653,19 @@ int scratch(int device, Scratch& sc, size_t bytes, cudaStream_t st, void** out) 
   return PACO_OK;
 }
 
+// TMA takes a view in place only when its first element and row pitch are
+// 16-byte aligned: a tensor map over an aligned-down base with a column
+// offset is accepted by cuTensorMapEncodeTiled, but boxes whose rows start
+// off a 16-byte boundary never complete (the kernel's bounded mbarrier wait
+// then traps) -- such views are repacked into scratch instead.
 bool pitch_ok(const void* p, int64_t ld, int elsize) {
-  return (reinterpret_cast<uintptr_t>(p) % elsize == 0) && (ld * elsize) % 16 == 0;
+  return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && (ld * elsize) % 16 == 0;
 }
+
+// C is written by TMA stores / reduce-adds, which clip at the tensor edge in
+// 16-byte units: a row end inside a 16-byte chunk would clobber (or add into)
+// the neighbouring columns, which may belong to another task's block of C.
+bool c_ok(const void* p, int64_t ld, int64_t m) { return pitch_ok(p, ld, 4) && (m * 4) % 16 == 0; }
 }  // namespace
 
 namespace tc {
@@ -934,9 +944,9 @@ int check_tc_call(void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const i
     set_error("tcgen05 path: extents must fit int32");
     return PACO_ERR_ARG;
   }
-  if ((flags & PACO_MM_REMOTE) || ((flags & PACO_MM_ATOMIC) && !pitch_ok(C, ldc, 4))) {
+  if ((flags & PACO_MM_REMOTE) || ((flags & PACO_MM_ATOMIC) && !c_ok(C, ldc, m))) {
     // the TMA reduce-add epilogue is atomic, but only on local C with a TMA-able pitch
-    set_error("tcgen05 path: atomic folding needs a local C with a 16-byte row pitch");
+    set_error("tcgen05 path: atomic folding needs a local C with a 16-byte aligned start, pitch and row length");
     return PACO_ERR_UNSUPPORTED;
   }
   if ((flags & PACO_MM_ATOMIC) && (flags & PACO_MM_OVERWRITE)) {
@@ -998,7 +1008,7 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
   if ((rc = build_operands<K>(device, sc, stream, A, lda, B, ldb, n, m, k, nullptr, 0, 0, maps.p[0]))) return rc;
   void* c_user = nullptr;
   int64_t ldc_user = ldc;
-  if (!pitch_ok(C, ldc, 4)) {
+  if (!c_ok(C, ldc, m)) {  // stage C through padded scratch, copy back exactly n x m
     const int64_t ld2 = (m + 3) / 4 * 4;
     void* p;
     if ((rc = scratch(device, sc, size_t(n) * ld2 * 4, stream, &p))) return rc;
@@ -1027,8 +1037,8 @@ int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* 
   }
   for (int q = 0; q < count; ++q) {
     if ((rc = check_tc_call<K>(pre[q].c, ldc, n, m, k, nullptr, 0, flags))) return rc;
-    if (!pitch_ok(pre[q].c, ldc, 4)) {
-      set_error("paco_mm_tf32x3: C row pitch must be a multiple of 16 bytes");
+    if (!c_ok(pre[q].c, ldc, m)) {
+      set_error("paco_mm_tf32x3: C needs a 16-byte aligned start, row pitch and row length");
       return PACO_ERR_UNSUPPORTED;
     }
   }

@@ -32,8 +32,8 @@ import torch
 from . import _native as nat
 from .device import View, pick_device, stage_in
 from .engine import execute_plan
-from .mm import launch_mm
-from .plan import COMPUTE, MERGE, Plan, PlanError, Task, pruned_bfs_assign
+from .mm import launch_fold, launch_mm
+from .plan import COMPUTE, MERGE, REDUCE, Plan, PlanError, Task, pruned_bfs_assign
 
 DEFAULT_STRASSEN_BASE = 64
 
@@ -90,6 +90,36 @@ class StrassenNode:
                                                    self.size)
 
 
+@dataclass(frozen=True)
+class LeafPiece:
+    """One GPU's cuboid of a leftover leaf product M = S T, split across all p
+    workers by MM-1-Piece.  ``cuboid`` is in the leaf's (i, j, l)
+    space; its C face lands in M (out = 0) or in k-cut temporary ``out``."""
+
+    node: StrassenNode
+    cuboid: object
+
+    def __str__(self) -> str:
+        c = self.cuboid
+        return f"piece[{self.node},i0={c.i0},j0={c.j0},l0={c.l0},n={c.n},m={c.m},k={c.k},out={c.out}]"
+
+
+@dataclass(frozen=True)
+class LeafFold:
+    """k-cut REDUCE of a split leaf: (out, oi, oj) (+)= temp (matmul.py:455-460)."""
+
+    node: StrassenNode
+    temp: int
+    out: int
+    oi: int
+    oj: int
+    n: int
+    m: int
+
+    def __str__(self) -> str:
+        return f"reduce[{self.node},temp={self.temp}->out={self.out},n={self.n},m={self.m}]"
+
+
 def _padded(n: int) -> int:
     if n < 1:
         raise PlanError("n must be >= 1")
@@ -101,8 +131,12 @@ def _expand(node: StrassenNode) -> list[StrassenNode]:
     return node.kids
 
 
-def _assemble(root: StrassenNode, assigned: list[Task], p: int, n: int, base: int, variant: str) -> Plan:
-    """Topological task list: FORM(internal, BFS) -> COMPUTE(assigned) -> COMBINE(reverse BFS)."""
+def _assemble(root: StrassenNode, assigned: list[Task], p: int, n: int, base: int, variant: str,
+              split: list | None = None) -> Plan:
+    """Topological task list: FORM(internal, BFS) -> COMPUTE(assigned) -> COMBINE(reverse BFS).
+
+    ``split``: (leaf, one-piece MM plan over p workers) pairs -- leaves computed
+    as p cuboids plus their k-cut REDUCE tasks instead of by one worker."""
     internal: list[StrassenNode] = []
     frontier = [root]
     while frontier:
@@ -113,8 +147,10 @@ def _assemble(root: StrassenNode, assigned: list[Task], p: int, n: int, base: in
                 nxt.extend(nd.kids)
         frontier = nxt
     owner = {id(t.region): t.worker for t in assigned}
+    split = split or []
+    everyone = tuple(range(p))
 
-    workers_of: dict[int, tuple[int, ...]] = {}
+    workers_of: dict[int, tuple[int, ...]] = {id(leaf): everyone for leaf, _ in split}
 
     def subtree(nd: StrassenNode) -> tuple[int, ...]:
         key = id(nd)
@@ -145,28 +181,70 @@ def _assemble(root: StrassenNode, assigned: list[Task], p: int, n: int, base: in
         t = Task(id=len(tasks), kind=COMPUTE, region=nd, worker=a.worker,
                  deps=(form_id[id(par)],) if par is not None else (), cost_work=nd.volume, label=a.label)
         nd.task_id = t.id
-        done_id[id(nd)] = t.id
+        done_id[id(nd)] = (t.id,)
         tasks.append(t)
+    label = max((a.label for a in assigned), default=0) + 1
+    leaf_plans = {}
+    for leaf, mplan in split:
+        par = parent_of.get(id(leaf))
+        pre = (form_id[id(par)],) if par is not None else ()
+        vol = leaf.volume / float(leaf.size) ** 3  # Strassen work units per term
+        new_id: dict[int, int] = {}
+        for mt in mplan.tasks:
+            if mt.kind == COMPUTE:
+                region = LeafPiece(leaf, mt.region)
+                kind, deps = COMPUTE, pre
+                cost = max(1, round(vol * mt.region.n * mt.region.m * mt.region.k))
+            else:
+                spec = mplan.meta["reduces"][mt.id]
+                region = LeafFold(leaf, *spec)
+                kind, deps = REDUCE, tuple(new_id[d] for d in mt.deps)
+                cost = max(1, round(vol * mt.cost_work))
+            t = Task(id=len(tasks), kind=kind, region=region, worker=mt.worker, deps=deps,
+                     cost_work=cost, label=label)
+            new_id[mt.id] = t.id
+            tasks.append(t)
+        done_id[id(leaf)] = tuple(new_id.values())
+        leaf_plans[str(leaf)] = mplan
     for nd in reversed(internal):
         half = (nd.size // 2) ** 2
         t = Task(id=len(tasks), kind=MERGE, region=f"combine[{nd}]", worker=pack(subtree(nd)),
-                 deps=tuple(sorted(done_id[id(k)] for k in nd.kids)), cost_work=8 * half)
-        done_id[id(nd)] = t.id
+                 deps=tuple(sorted(d for k in nd.kids for d in done_id[id(k)])), cost_work=8 * half)
+        done_id[id(nd)] = (t.id,)
         tasks.append(t)
     temp = sum(21 * (nd.size // 2) ** 2 for nd in internal)
+    temp += sum(sum(mp.meta["temp_sizes"].values()) for _, mp in split)
     meta = {"algo": "strassen", "variant": variant, "n": n, "n_padded": root.size, "base": base,
-            "internal": len(internal), "leaves": len(assigned), "temp_peak": temp,
-            "tree": root}
+            "internal": len(internal), "leaves": len(assigned) + len(split), "temp_peak": temp,
+            "tree": root, "split_leaves": leaf_plans}
     return Plan(tasks=tasks, p=p, meta=meta)
 
 
-def strassen_paco_partition(n: int, p: int, base: int = DEFAULT_STRASSEN_BASE) -> Plan:
-    """PACO-Strassen: pruned BFS of the 7-way tree."""
+def strassen_paco_partition(n: int, p: int, base: int = DEFAULT_STRASSEN_BASE, *,
+                            split_leftover: bool = False) -> Plan:
+    """PACO-Strassen: pruned BFS of the 7-way tree.
+
+    ``split_leftover`` (this build's extension): the final batch
+    of fewer than p base-size leaves is not dealt one per worker -- which caps
+    the efficiency at 49/56 = 87.5 % for p = 8, 49/54 = 90.7 % for p = 6 on
+    cfg5 -- but each such leaf product is cut into p cuboids by MM-1-Piece
+    (matmul.py:246-300) with its k-cut REDUCE tasks, so every worker gets an
+    equal share."""
+    from .cuboid import mm_one_piece_partition
+
     size = _padded(n)
     root = StrassenNode((), size)
     bfs = pruned_bfs_assign(root, 7, _expand, lambda nd: nd.size <= base, p,
                             cost=lambda nd: nd.volume)
-    return _assemble(root, bfs.tasks, p, n, base, "paco")
+    assigned, split = bfs.tasks, []
+    if split_leftover and p > 1 and assigned:
+        last = max(t.label for t in assigned)
+        tail = [t for t in assigned if t.label == last]
+        if len(tail) < p and all(t.region.size <= base and t.region.size ** 3 >= p for t in tail):
+            assigned = [t for t in assigned if t.label != last]
+            split = [(t.region, mm_one_piece_partition(t.region.size, t.region.size, t.region.size, p))
+                     for t in tail]
+    return _assemble(root, assigned, p, n, base, "paco+split-leftover" if split else "paco", split)
 
 
 def strassen_const_pieces_partition(n: int, p: int, cfg: SuperRoundCfg = SuperRoundCfg(),
@@ -382,7 +460,8 @@ def strassen_execute(plan: Plan, A, B, mode: str = "serial_sim", *, devices: lis
     Workers map to ``devices[w % len(devices)]`` with one stream each.  S/T/M
     buffers live on the first device; FORM/COMBINE tasks run on their first
     worker, COMPUTE tasks run ``strassen_seq`` of their node into the
-    parent's M slot.
+    parent's M slot; pieces of split leaves (``split_leftover``) write their
+    cuboid of M (or of a k-cut temporary, folded by the leaf's REDUCE tasks).
     """
     meta = plan.meta
     if meta.get("algo") != "strassen":
@@ -417,6 +496,16 @@ def strassen_execute(plan: Plan, A, B, mode: str = "serial_sim", *, devices: lis
                 for r, kid_nd in enumerate(nd.kids):
                     ops[id(kid_nd)] = (ws.S[r], ws.T[r], ws.M[r])
                     stack.append(kid_nd)
+        # k-cut temporaries of leaves split across the workers (split_leftover)
+        from .cuboid import temp_shape
+        leaf_temps: dict[tuple[int, int], View] = {}
+        by_leaf = {name: mp for name, mp in meta.get("split_leaves", {}).items()}
+        for t in plan.tasks:
+            if isinstance(t.region, LeafPiece) and t.region.cuboid.out and \
+                    (id(t.region.node), t.region.cuboid.out) not in leaf_temps:
+                bid = t.region.cuboid.out
+                shp = temp_shape(by_leaf[str(t.region.node)], bid)
+                leaf_temps[(id(t.region.node), bid)] = View.of(torch.empty(shp, dtype=dtype, device=home))
         staged = torch.cuda.Event()
         staged.record(stage)
         streams = [torch.cuda.Stream(device=dev_of[w]) for w in range(plan.p)]
@@ -436,7 +525,19 @@ def strassen_execute(plan: Plan, A, B, mode: str = "serial_sim", *, devices: lis
             for d in task.deps:
                 st.wait_event(events[d])
             with torch.cuda.device(dev_of[w]):
-                if task.kind == COMPUTE:
+                if isinstance(task.region, LeafPiece):  # one worker's cuboid of a split leaf
+                    leaf, cb = task.region.node, task.region.cuboid
+                    A_n, B_n, C_n = ops[id(leaf)]
+                    dst = C_n if cb.out == 0 else leaf_temps[(id(leaf), cb.out)]
+                    launch_mm(kid, st, A_n.sub(cb.i0, cb.l0, cb.n, cb.k), B_n.sub(cb.l0, cb.j0, cb.k, cb.m),
+                              dst.sub(cb.out_i0, cb.out_j0, cb.n, cb.m), overwrite=True, device=dev_of[w])
+                elif isinstance(task.region, LeafFold):
+                    f = task.region
+                    A_n, B_n, C_n = ops[id(f.node)]
+                    dst = C_n if f.out == 0 else leaf_temps[(id(f.node), f.out)]
+                    src = leaf_temps[(id(f.node), f.temp)]
+                    launch_fold(kid, st, dst.sub(f.oi, f.oj, f.n, f.m), src.sub(0, 0, f.n, f.m), False)
+                elif task.kind == COMPUTE:
                     nd = task.region
                     A_n, B_n, C_n = ops[id(nd)]
                     with torch.cuda.stream(st):

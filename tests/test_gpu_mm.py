@@ -412,3 +412,26 @@ def test_tensor_core_plans_on_concurrent_streams(sr):
                 M.mm_execute(plan, a, b, C, sem, mode="parallel")
                 got = C.cpu().numpy().astype(np.float64)
                 assert np.linalg.norm(got - ref) <= 1e-5 * np.linalg.norm(ref), (p, plan.meta["variant"])
+
+
+@pytest.mark.parametrize("sr", ["f32", "bf16"])
+@pytest.mark.parametrize("offs", [(0, 1, 1), (3, 5, 7), (1, 0, 2)])
+def test_tensor_core_misaligned_views(sr, offs):
+    """tcgen05 operands / C whose first element is not 16-byte aligned are
+    repacked through scratch (TMA boxes must start 16-byte aligned)."""
+    ri, rl, rj = offs
+    g = torch.Generator(device="cuda").manual_seed(sum(offs))
+    dt = torch.float32 if sr == "f32" else torch.bfloat16
+    big_a = (torch.rand(300, 300, device="cuda", generator=g) * 2 - 1).to(dt)
+    big_b = (torch.rand(300, 300, device="cuda", generator=g) * 2 - 1).to(dt)
+    big_c = torch.rand(300, 300, device="cuda", generator=g)
+    n, k, m = 139, 96, 171
+    a, b = big_a[ri:ri + n, rl:rl + k], big_b[rl:rl + k, rj:rj + m]
+    c = big_c[ri:ri + n, rj:rj + m]
+    c0 = c.clone()
+    M.mm_seq(a, b, c, M.SEMIRING_F32 if sr == "f32" else M.SEMIRING_BF16)
+    ref = c0.double() + a.double() @ b.double()
+    assert float((c.double() - ref).norm() / ref.norm()) < 1e-5
+    outside = big_c.clone()
+    outside[ri:ri + n, rj:rj + m] = 0
+    assert torch.count_nonzero(outside[ri:ri + n, :rj]) == rj * n  # neighbours untouched

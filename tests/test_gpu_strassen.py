@@ -45,6 +45,26 @@ def test_execute_plans_integer_exact(p):
             assert np.array_equal(C, A @ B), (p, mode, plan.meta["variant"])
 
 
+@pytest.mark.parametrize("p", [5, 8])
+def test_execute_split_leftover(p):
+    """Leftover leaves cut into p cuboids with k-cut folds: exact on the int64
+    ring, 1e-4 on fp32 (3xTF32 leaf pieces), serial and parallel."""
+    rng = np.random.default_rng(10 + p)
+    n = 512
+    A = rng.integers(-30, 30, (n, n)).astype(np.int64)
+    B = rng.integers(-30, 30, (n, n)).astype(np.int64)
+    plan = S.strassen_paco_partition(n, p, base=64, split_leftover=True)
+    assert "split" in plan.meta["variant"]
+    for mode in ("serial_sim", "parallel"):
+        C = S.strassen_execute(plan, A, B, mode)
+        assert np.array_equal(C, A @ B), (p, mode)
+    Af = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    Bf = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    Cf = S.strassen_execute(plan, Af, Bf, "parallel")
+    ref = Af.astype(np.float64) @ Bf.astype(np.float64)
+    assert np.linalg.norm(Cf - ref) <= 1e-4 * np.linalg.norm(ref)
+
+
 def test_f32_two_levels_vs_oracle():
     rng = np.random.default_rng(1005)
     n = 2048

@@ -91,3 +91,36 @@ def test_errors():
         strassen_paco_partition(0, 2)
     with pytest.raises(PlanError):
         strassen_const_pieces_partition(64, 0)
+
+
+@pytest.mark.parametrize("p", [5, 6, 8])
+def test_split_leftover_balances_cfg5(p):
+    """the leftover base leaves, cut into p MM-1-Piece cuboids,
+    remove the 87.5 % (p = 8) / 90.7 % (p = 6) efficiency cap of cfg5's plan."""
+    from paper_2011_01441_b200.strassen import LeafPiece, LeafFold, strassen_paco_partition as part
+    loads = {}
+    for split in (False, True):
+        plan = part(16384, p, base=4096, split_leftover=split)
+        plan.validate()
+        w = [0] * p
+        for t in plan.tasks:
+            if t.kind in ("compute", "reduce"):
+                w[t.workers()[0]] += t.cost_work
+        loads[split] = max(w) / (sum(w) / p)
+    assert loads[True] < 1.001 and loads[True] < loads[False]
+    assert loads[False] > (1.05 if p != 5 else 1.01)
+    plan = part(16384, p, base=4096, split_leftover=True)
+    pieces = [t.region for t in plan.tasks if isinstance(t.region, LeafPiece)]
+    leaves = {str(pc.node) for pc in pieces}
+    for name in leaves:  # each split leaf's cuboids tile its 4096^3 cube exactly once
+        vol = sum(pc.cuboid.n * pc.cuboid.m * pc.cuboid.k for pc in pieces if str(pc.node) == name)
+        assert vol == 4096 ** 3
+    folds = [t for t in plan.tasks if isinstance(t.region, LeafFold)]
+    assert all(t.kind == "reduce" for t in folds)
+    assert "split" in plan.meta["variant"]
+
+
+def test_split_leftover_noop_when_even():
+    from paper_2011_01441_b200.strassen import strassen_paco_partition as part
+    a, b = part(16384, 7, base=4096), part(16384, 7, base=4096, split_leftover=True)
+    assert a.dump_text() == b.dump_text()
