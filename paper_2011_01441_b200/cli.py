@@ -134,14 +134,16 @@ def run_mm(n: int, m: int, k: int, p: int, *, variant: str = "paco", weights=Non
 
 
 def run_strassen(n: int, p: int, *, variant: str = "paco", gamma: int = 8, seed: int = 0,
-                 mode: str = "serial_sim", repeats: int = 3, devices=None) -> tuple[str, bool]:
+                 mode: str = "serial_sim", repeats: int = 3, devices=None, base: int | None = None,
+                 split_leftover: bool = False) -> tuple[str, bool]:
     if mode not in MODES:
         raise ValueError(f"unknown mode {mode!r}")
     t0 = time.perf_counter()
+    b = base if base is not None else S.DEFAULT_STRASSEN_BASE
     if variant == "paco":
-        plan = S.strassen_paco_partition(n, p)
+        plan = S.strassen_paco_partition(n, p, base=b, split_leftover=split_leftover)
     elif variant == "const-pieces":
-        plan = S.strassen_const_pieces_partition(n, p, S.SuperRoundCfg(gamma=gamma))
+        plan = S.strassen_const_pieces_partition(n, p, S.SuperRoundCfg(gamma=gamma), base=b)
     else:
         raise ValueError(f"unknown variant {variant!r}")
     plan_s = time.perf_counter() - t0
@@ -216,6 +218,9 @@ def main(argv=None) -> int:
     s.add_argument("--p", type=int, required=True)
     s.add_argument("--gamma", type=int, default=8)
     s.add_argument("--variant", default="paco", choices=["paco", "const-pieces"])
+    s.add_argument("--base", type=int, help="leaf size (default 64; cfg5 uses n/4)")
+    s.add_argument("--split-leftover", action="store_true",
+                   help="cut the last < p leaves into p MM-1-Piece cuboids (paco variant)")
     for x in (a, s):
         x.add_argument("--seed", type=int, default=0)
         x.add_argument("--mode", default="serial_sim", choices=MODES)
@@ -243,7 +248,8 @@ def main(argv=None) -> int:
                              repeats=args.repeats, devices=devices)
         else:
             row, ok = run_strassen(args.n, args.p, variant=args.variant, gamma=args.gamma, seed=args.seed,
-                                   mode=args.mode, repeats=args.repeats, devices=devices)
+                                   mode=args.mode, repeats=args.repeats, devices=devices, base=args.base,
+                                   split_leftover=args.split_leftover)
     except (PlanError, ValueError) as e:
         print(f"paco: error: {e}", file=sys.stderr)
         return 2

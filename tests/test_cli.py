@@ -43,6 +43,8 @@ def test_mm_and_strassen_rows_pass():
     for variant in ("paco", "const-pieces"):
         row, ok = cli.run_strassen(256, 7, variant=variant, gamma=1, mode="parallel")
         assert ok, row
+    row, ok = cli.run_strassen(512, 8, base=64, split_leftover=True, mode="parallel")
+    assert ok, row
     out = io.StringIO()
     assert cli.run_spec({"algo": "mm", "n": "64,96", "p": "1,2", "mode": "parallel"}, out)
     assert len(out.getvalue().strip().splitlines()) == 5
