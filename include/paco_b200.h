@@ -13,9 +13,19 @@
  *   paco_fill      <- np.full(shape, semiring.zero)              matmul.py:430-433
  *   paco_mm_naive  <- mm_oracle(A, B, semiring) (defining sums)  matmul.py:400-414
  *   paco_plan_one_piece <- mm_one_piece_partition(n, m, k, p)    matmul.py:250-300
- *                     (cuboid geometry only; used for the CTA-level plan)
+ *                     (cuboid geometry only)
+ *   paco_plan_cta / paco_cta_grid   the CTA-level plans paco_mm runs (this
+ *                     build's second PACO level: MM-1-Piece over tile units,
+ *                     or the default tile grid with a k split)
  *   paco_lincomb   <- Strassen S_r/T_r formation and C-block combination
  *                     (reference has no code: SPEC.md:474-552)
+ *   paco_tf32_split / paco_mm_tf32x3   the fp32 Strassen leaf level: S_r/T_r
+ *                     sums as tf32 hi/lo pairs + batched 3xTF32 products
+ *                     (SPEC.md:490-498 strassen_seq leaves)
+ *   paco_copy2d    <- the reference's implicit NumPy host residency: staging of
+ *                     host operands for mm_seq (matmul.py:342-366)
+ *   paco_device_alloc / paco_ipc_* / paco_enable_peer   multi-GPU plumbing for
+ *                     the parallel executor (core.py:301-326, one worker per GPU)
  *
  * Conventions: plain pointers, row-major matrices with a leading dimension in
  * ELEMENTS, int64 extents, an explicit device ordinal and cudaStream_t passed
