@@ -1,18 +1,23 @@
 // Register-blocked SIMT semiring MM for sm_100a (tropical / integer / fp32 / fp64).
 //
 // Replaces the reference's recursive mm_seq + 32^3 NumPy leaves
-// (matmul.py:342-397, block kernels 45-50) with one persistent launch:
-//   * grid = the CTA-level PACO plan: one CTA per MM-1-Piece cuboid of the
-//     iteration space (148 SMs x 2 resident CTAs), see plan_pieces_balanced();
-//     a piece owns a rectangle of 128x128 C tiles and an arbitrary k range
-//     (k bounds are multiples of the 16-byte load quantum);
-//   * each CTA walks the C tiles of its cuboid; per tile it streams its k
-//     range through a STAGES-deep cp.async ring (16 B; an unpredicated fast
-//     path for interior tiles, zero-filled predicated loads at the edges);
+// (matmul.py:342-397, block kernels 45-50) with one launch:
+//   * grid = the CTA-level plan.  Default: the tile grid -- one CTA per 128x128
+//     C tile and k range, the k extent split s ways by a cost model (whole
+//     SM-waves x per-visit cost, grid_ksplit); measured faster than the
+//     balanced PACO cuboid plan (MM-1-Piece over tile units,
+//     plan_pieces_balanced), which stays available (PACO_MM_PACO_PLAN) and
+//     for explicit piece tables;
+//   * each CTA walks the C tiles of its piece; per tile it streams its k range
+//     through a STAGES-deep cp.async ring (16 B; an unpredicated fast path for
+//     interior tiles, zero-filled predicated loads at the edges) synchronised
+//     by split arrive/wait mbarriers (full: copies landed, empty: stage read);
 //   * a 16x16 thread grid holds TMxTN register accumulators per thread, fed by
 //     128-bit LDS from padded, bank-conflict-free shared tiles;
-//   * epilogue: C (+)= acc, or one global atomic (+) per element for pieces
-//     that split k (exact and order-free for the integer/tropical semirings).
+//   * epilogue: C (+)= acc through TMA bulk copies / bulk reductions
+//     (cp.reduce.async.bulk min/max/add, exact and order-free for the
+//     integer/tropical semirings when pieces split k), or per-element stores /
+//     atomics at ragged edges.
 // The tropical inner loop is one VIADDMNMX per term (checked in SASS).
 #include <algorithm>
 #include <cmath>
