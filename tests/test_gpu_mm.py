@@ -223,6 +223,15 @@ def test_empty_k_and_empty_output():
     assert (C == 7).all()
     C = np.zeros((0, 5), np.int32)
     M.mm_seq(np.zeros((0, 3), np.int32), np.zeros((3, 5), np.int32), C, M.SEMIRING_MINPLUS_SAT)
+    for sem, dt in ((M.SEMIRING_F32, torch.float32), (M.SEMIRING_BF16, torch.bfloat16),
+                    (M.SEMIRING_INT, torch.int64), (M.SEMIRING_MAXPLUS, torch.int32)):
+        a = torch.zeros((6, 0), dtype=dt, device="cuda")
+        b = torch.zeros((0, 9), dtype=dt, device="cuda")
+        c = torch.full((6, 9), 3, dtype=torch.float32 if dt.is_floating_point else dt, device="cuda")
+        M.mm_seq(a, b, c, sem)
+        assert bool((c == 3).all()), sem.name
+        M.mm_seq(a, b, c, sem, overwrite=True)       # C = zero of the semiring
+        assert bool((c == sem.zero).all()), sem.name
 
 
 def test_device_oracle_matches_cpu_oracle():
