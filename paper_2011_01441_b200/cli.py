@@ -139,7 +139,9 @@ def run_strassen(n: int, p: int, *, variant: str = "paco", gamma: int = 8, seed:
     if mode not in MODES:
         raise ValueError(f"unknown mode {mode!r}")
     t0 = time.perf_counter()
-    b = base if base is not None else S.DEFAULT_STRASSEN_BASE
+    # GPU default: two Strassen levels (leaves of n/4, as cfg5) -- the API's
+    # reference default of 64 would launch 7^log2(n/64) tiny leaf products
+    b = base if base is not None else max(S.DEFAULT_STRASSEN_BASE, n // 4)
     if variant == "paco":
         plan = S.strassen_paco_partition(n, p, base=b, split_leftover=split_leftover)
     elif variant == "const-pieces":
@@ -185,7 +187,9 @@ def run_spec(spec: dict, out) -> bool:
                                  seed=seed, mode=mode, repeats=repeats)
             else:
                 row, ok = run_strassen(n, p, variant=spec.get("variant", "paco"),
-                                       gamma=int(spec.get("gamma", 8)), seed=seed, mode=mode, repeats=repeats)
+                                       gamma=int(spec.get("gamma", 8)), seed=seed, mode=mode, repeats=repeats,
+                                       base=int(spec["base"]) if "base" in spec else None,
+                                       split_leftover=spec.get("split_leftover", "0") in ("1", "true", "yes"))
             print(row, file=out, flush=True)
             all_ok &= ok
     return all_ok
@@ -218,7 +222,7 @@ def main(argv=None) -> int:
     s.add_argument("--p", type=int, required=True)
     s.add_argument("--gamma", type=int, default=8)
     s.add_argument("--variant", default="paco", choices=["paco", "const-pieces"])
-    s.add_argument("--base", type=int, help="leaf size (default 64; cfg5 uses n/4)")
+    s.add_argument("--base", type=int, help="leaf size (default max(64, n/4): two levels, as cfg5)")
     s.add_argument("--split-leftover", action="store_true",
                    help="cut the last < p leaves into p MM-1-Piece cuboids (paco variant)")
     for x in (a, s):
