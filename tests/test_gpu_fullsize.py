@@ -88,3 +88,40 @@ def test_cfg3_bf16_full_vs_f64():
     ref = a.double().cpu().numpy() @ b.double().cpu().numpy()
     err = np.linalg.norm(c.cpu().numpy().astype(np.float64) - ref) / np.linalg.norm(ref)
     assert err <= 1e-2 and err < 1e-5, err
+
+
+def test_c_beyond_2g_elements_minplus():
+    """Maximum-size indexing: a 49152 x 49152 int32 C (2.4e9 elements, 9.7 GB --
+    element offsets beyond 2^31) through the tile-grid plan and the PACO cuboid
+    plan; sampled rows (including the last) bit-exact vs the oracle."""
+    from paper_2011_01441_b200 import _native as nat
+    from paper_2011_01441_b200.device import View
+    from paper_2011_01441_b200.mm import launch_mm
+    rng = np.random.default_rng(77)
+    n, k = 49152, 160
+    A = rng.integers(0, 2**20, (n, k), dtype=np.int32)
+    B = rng.integers(0, 2**20, (k, n), dtype=np.int32)
+    a, b = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    rows = np.array([0, 1, 12345, 30000, n - 2, n - 1])
+    want = cref.mm_rows(cref.SR_MINPLUS_SAT32, A, B, np.full((len(rows), n), INF, np.int32), rows)
+    for flags in (0, nat.MM_PACO_PLAN):
+        c = torch.full((n, n), INF, dtype=torch.int32, device="cuda")
+        launch_mm(nat.SR_MINPLUS_SAT32, torch.cuda.current_stream(), View.of(a), View.of(b), View.of(c),
+                  flags=flags)
+        got = c[torch.from_numpy(rows).cuda()].cpu().numpy()
+        assert np.array_equal(got, want), flags
+        del c
+        torch.cuda.empty_cache()
+
+
+def test_c_beyond_2g_elements_bf16():
+    """The tcgen05 path at the same scale: 49152 x 49152 fp32 C from bf16 operands."""
+    n, k = 49152, 128
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(k, n, device="cuda", generator=g).to(torch.bfloat16)
+    c = torch.empty(n, n, device="cuda")
+    M.mm_seq(a, b, c, M.SEMIRING_BF16, overwrite=True)
+    rows = torch.tensor([0, 777, 40000, n - 1], device="cuda")
+    ref = a[rows].double() @ b.double()
+    assert float((c[rows].double() - ref).norm() / ref.norm()) < 1e-5
