@@ -528,34 +528,43 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
         const int col0 = nb * BN + 32 * c;
         if (col0 >= args.m) continue;  // warp-uniform: nothing left to store
         // 64 columns in SUBS boxes of EPI_COLS; buffer h % EPI_BUFS
-        constexpr int EC = K::EPI_COLS, SUBS = 64 / EC;
+        constexpr int EC = K::EPI_COLS, SUBS = 64 / EC, EB = K::EPI_BUFS;
+        // groups of EB boxes: wait for the buffers, stage EB boxes, ONE proxy
+        // fence, EB TMA stores (or reduce-adds), one bulk group
 #pragma unroll
-        for (int h = 0; h < SUBS; ++h) {
-          if (col0 + EC * h >= args.m) break;
-          unsigned char* buf = stage0 + (h % K::EPI_BUFS) * L::EPI_BUF;
-          if (h % K::EPI_BUFS == 0) {  // the buffer(s) must be read out by earlier stores
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-            __syncwarp();
-          }
+        for (int h0 = 0; h0 < SUBS; h0 += EB) {
+          if (col0 + EC * h0 >= args.m) break;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+          __syncwarp();
           if (!(args.ablate & 4)) {
-            // swizzled [32 rows][EC fp32]: 16 B chunk j of row r at j ^ (r-bits of the
-            // 128B (EC = 32) / 64B (EC = 16) TMA swizzle pattern)
 #pragma unroll
-            for (int j = 0; j < EC / 4; ++j) {
-              const uint4 w = make_uint4(v[EC * h + 4 * j], v[EC * h + 4 * j + 1], v[EC * h + 4 * j + 2],
-                                         v[EC * h + 4 * j + 3]);
-              const int sw = EC == 32 ? (j ^ (lane & 7)) : (j ^ ((lane >> 1) & 3));
-              *reinterpret_cast<uint4*>(buf + lane * (EC * 4) + sw * 16) = w;
+            for (int hh = 0; hh < EB; ++hh) {
+              const int h = h0 + hh;
+              unsigned char* buf = stage0 + hh * L::EPI_BUF;
+              // swizzled [32 rows][EC fp32]: 16 B chunk j of row r at j ^ (r-bits of the
+              // 128B (EC = 32) / 64B (EC = 16) TMA swizzle pattern)
+#pragma unroll
+              for (int j = 0; j < EC / 4; ++j) {
+                const uint4 w = make_uint4(v[EC * h + 4 * j], v[EC * h + 4 * j + 1], v[EC * h + 4 * j + 2],
+                                           v[EC * h + 4 * j + 3]);
+                const int sw = EC == 32 ? (j ^ (lane & 7)) : (j ^ ((lane >> 1) & 3));
+                *reinterpret_cast<uint4*>(buf + lane * (EC * 4) + sw * 16) = w;
+              }
             }
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           }
           __syncwarp();
           if (lane == 0) {
-            if (row0 < args.n && !(args.ablate & 1)) {
-              if (args.overwrite)
-                tma_store_2d(&P.c, buf, P.c_col0 + col0 + EC * h, row0);
-              else
-                tma_reduce_add_2d(&P.c, buf, P.c_col0 + col0 + EC * h, row0);
+#pragma unroll
+            for (int hh = 0; hh < EB; ++hh) {
+              const int h = h0 + hh;
+              if (row0 < args.n && !(args.ablate & 1) && col0 + EC * h < args.m) {
+                unsigned char* buf = stage0 + hh * L::EPI_BUF;
+                if (args.overwrite)
+                  tma_store_2d(&P.c, buf, P.c_col0 + col0 + EC * h, row0);
+                else
+                  tma_reduce_add_2d(&P.c, buf, P.c_col0 + col0 + EC * h, row0);
+              }
             }
             asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
           }
