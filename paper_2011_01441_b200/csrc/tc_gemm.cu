@@ -233,7 +233,7 @@ struct TcArgs {
   int32_t tiles_rb;  // row blocks
   int32_t tiles_nb;  // column blocks
   int32_t kblocks;
-  int32_t ablate;    // diagnostics: 1 = no C stores, 2 = no MMAs, 4 = no smem staging
+  int32_t ablate;    // diagnostics: 1 = no C stores, 2 = no MMAs, 4 = no smem staging, 8 = no A loads
   long long* trace;  // diagnostics (paco_debug_trace): per CTA x 16 tiles x 6 globaltimer stamps
   int32_t* sched;    // per-group tile counters (zeroed before the launch)
   int32_t groups;    // CTA c serves group c % groups: column blocks g, g + groups, ...
@@ -389,6 +389,10 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
             if (kb == 0 && i < 15) tc_stamp(args, i, 0);
             if (kb == args.kblocks - 1 && i < 15) tc_stamp(args, i, 1);
             if constexpr (K::B_RES) {
+              if (args.ablate & 8) {  // diagnostics: the stage "lands" with no bytes
+                mbar_arrive(&full[s]);
+                continue;
+              }
               mbar_expect_tx_relaxed(&full[s], L::A_BYTES);
               tma_load_2d(smem + L::a_off(s, 0), &P.a[0], &full[s], P.a_col0[0] + kb * BK, rb * BM);
               continue;
