@@ -1,3 +1,4 @@
+"""Dev timing: cuBLAS bf16->bf16 and bf16->f32 (out_dtype) on the cfg3 shape, and a 256 MB fill, in CUDA graphs."""
 import torch
 n, m, k = 65536, 1024, 256
 a = torch.randn(n, k, device="cuda").to(torch.bfloat16)

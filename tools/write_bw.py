@@ -1,3 +1,4 @@
+"""Write bandwidth of a plain fill and a copy (the HBM write ceiling the cfg3 epilogue is compared with)."""
 import torch
 for mb in (268, 1073):
     n = mb * 1024 * 1024 // 4
