@@ -93,6 +93,27 @@ int paco_mm(int device, void* stream, int semiring, const void* A, int64_t lda, 
             int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
             const int32_t* pieces, int n_pieces, int flags);
 
+/* One problem of a paco_mm_batch: C (+)= A (x) B on views (leading dimensions
+ * in elements); flags as paco_mm (PACO_MM_REMOTE not allowed). */
+typedef struct {
+  const void* A;
+  int64_t lda;
+  const void* B;
+  int64_t ldb;
+  void* C;
+  int64_t ldc;
+  int64_t n, m, k;
+  int32_t flags;
+} paco_mm_problem;
+
+#define PACO_MAX_BATCH 64
+
+/* Up to PACO_MAX_BATCH independent problems of one SIMT semiring as ONE launch
+ * (each gets its tile-grid CTA plan; CTA ranges are concatenated): e.g. all
+ * COMPUTE cuboids of a GPU-level PACO plan on one device, their k-cut folds
+ * fused (PACO_MM_ATOMIC), replacing one launch per task (matmul.py:441-454). */
+int paco_mm_batch(int device, void* stream, int semiring, int count, const paco_mm_problem* problems);
+
 /* Piece units of paco_mm's CTA plan: C tile (bm x bn), k quantum bk (piece k
  * bounds are multiples of bk elements), and resident CTAs per SM. */
 int paco_mm_tile_shape(int semiring, int* bm, int* bn, int* bk, int* ctas_per_sm);

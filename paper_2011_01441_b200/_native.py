@@ -57,6 +57,7 @@ SIGNATURES = {
     "paco_lincomb": (_int, [_int, _vp, _int, _vp, _i64, _i64, _i64, _int,
                             ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                             ctypes.POINTER(ctypes.c_int32), _int]),
+    "paco_mm_batch": (_int, [_int, _vp, _int, _int, ctypes.c_void_p]),
     "paco_tf32_split": (_int, [_int, _vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                                ctypes.POINTER(ctypes.c_int32), _i64, _i64, _int, _vp, _vp, _i64]),
     "paco_mm_tf32x3": (_int, [_int, _vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64,
@@ -126,6 +127,27 @@ def plan_one_piece(n: int, m: int, k: int, p: int) -> list[tuple[int, ...]]:
     buf = (_i64 * (6 * p))()
     check(load().paco_plan_one_piece(n, m, k, p, buf))
     return [tuple(buf[6 * i:6 * i + 6]) for i in range(p)]
+
+
+class MMProblem(ctypes.Structure):
+    """``paco_mm_problem`` of include/paco_b200.h."""
+
+    _fields_ = [("A", ctypes.c_void_p), ("lda", ctypes.c_int64), ("B", ctypes.c_void_p), ("ldb", ctypes.c_int64),
+                ("C", ctypes.c_void_p), ("ldc", ctypes.c_int64), ("n", ctypes.c_int64), ("m", ctypes.c_int64),
+                ("k", ctypes.c_int64), ("flags", ctypes.c_int32)]
+
+
+MAX_BATCH = 64
+
+
+def mm_batch(device: int, stream: int, sr: int, problems: list) -> None:
+    """One paco_mm_batch launch per MAX_BATCH problems; each problem is
+    (A_ptr, lda, B_ptr, ldb, C_ptr, ldc, n, m, k, flags)."""
+    lib = load()
+    for i in range(0, len(problems), MAX_BATCH):
+        chunk = problems[i:i + MAX_BATCH]
+        arr = (MMProblem * len(chunk))(*[MMProblem(*p) for p in chunk])
+        check(lib.paco_mm_batch(device, stream, sr, len(chunk), ctypes.cast(arr, ctypes.c_void_p)))
 
 
 def cta_grid(sr: int, n: int, m: int, k: int) -> tuple[int, int]:

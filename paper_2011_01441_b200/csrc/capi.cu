@@ -31,6 +31,7 @@ int launch_mm_f32_tc(int device, cudaStream_t stream, const void* A, int64_t lda
                      int64_t ldb, void* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
                      const int32_t* pieces, int n_pieces, int flags);
 int tc_tile_shape(int semiring, int* bm, int* bn, int* bk, int* cps);
+int launch_mm_simt_batch(int sr, int device, cudaStream_t stream, int count, const paco_mm_problem* problems);
 int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, int count, const void* const* ah,
                               const void* const* al, int64_t lda, const void* const* bth, const void* const* btl,
                               int64_t ldb, void* const* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
@@ -162,6 +163,32 @@ int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out,
   PACO_TRY(use_device(device));
   return launch_lincomb(dtype, static_cast<cudaStream_t>(stream), out, ld_out, n, m, nin, ins, lds,
                         coefs, accumulate);
+}
+
+int paco_mm_batch(int device, void* stream, int semiring, int count, const paco_mm_problem* problems) {
+  if (count < 0 || count > PACO_MAX_BATCH || (count > 0 && !problems)) {
+    set_error("paco_mm_batch: count=%d (0..%d) with a problem array", count, PACO_MAX_BATCH);
+    return PACO_ERR_ARG;
+  }
+  if (semiring < 0 || semiring >= PACO_SR_COUNT) {
+    set_error("unknown semiring id %d", semiring);
+    return PACO_ERR_ARG;
+  }
+  if (semiring == PACO_SR_BF16_F32 || semiring == PACO_SR_F32_TC) {
+    set_error("paco_mm_batch: SIMT semirings only (the tcgen05 kernels have their own batch entry)");
+    return PACO_ERR_UNSUPPORTED;
+  }
+  for (int q = 0; q < count; ++q) {
+    const paco_mm_problem& P = problems[q];
+    if (P.n <= 0 || P.m <= 0) continue;
+    PACO_TRY(check_view("C", P.C, P.ldc, P.n, P.m));
+    if (P.k > 0) {
+      PACO_TRY(check_view("A", P.A, P.lda, P.n, P.k));
+      PACO_TRY(check_view("B", P.B, P.ldb, P.k, P.m));
+    }
+  }
+  PACO_TRY(use_device(device));
+  return launch_mm_simt_batch(semiring, device, static_cast<cudaStream_t>(stream), count, problems);
 }
 
 int paco_tf32_split(int device, void* stream, int nin, const void* const* ins, const int64_t* lds,

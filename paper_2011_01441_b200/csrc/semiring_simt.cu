@@ -118,6 +118,13 @@ struct MMArgs {
   double kw;           // virtual k weight of the CTA plan (cta_plan.cuh)
 };
 
+struct BatchTable {
+  int32_t count;
+  int32_t grid_s[PACO_MAX_BATCH];
+  int64_t first[PACO_MAX_BATCH + 1];  // CTA prefix sums
+  MMArgs args[PACO_MAX_BATCH];
+};
+
 // Stage one (C tile, k tile) of A and B into shared memory.  kVec: 16 B
 // chunks; interior tiles skip every bound check.
 template <class Op, bool kVec>
@@ -378,9 +385,9 @@ struct TileWalk {
   }
 };
 
+// One CTA's piece of one problem: the whole pipeline (ring, MACs, epilogue).
 template <class Op, bool kVec>
-__global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
-    simt_mm_kernel(const MMArgs args, const __grid_constant__ PieceTable table) {
+__device__ __forceinline__ void simt_mm_body(const MMArgs& args, const Piece pc) {
   using C = SimtCfg<Op>;
   using TA = typename Op::TA;
   using TB = typename Op::TB;
@@ -388,18 +395,6 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
   TA* As = reinterpret_cast<TA*>(smem_raw);
   TB* Bs = reinterpret_cast<TB*>(smem_raw + size_t(C::STAGES) * C::A_STAGE * sizeof(TA));
 
-  Piece pc;
-  if (table.count > 0) {
-    pc = table.p[blockIdx.x];
-  } else {  // derive this CTA's piece of the default plan (same code as paco_plan_cta)
-    UnitBox b;
-    if (table.grid_s > 0)
-      plan_grid_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, table.grid_s, int(blockIdx.x), b);
-    else
-      plan_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, int(gridDim.x), int(blockIdx.x), b, args.kw);
-    pc = Piece{int32_t(b.o[0]), int32_t(b.o[1]), int32_t(b.o[2]), int32_t(b.e[0]), int32_t(b.e[1]),
-               int32_t(b.e[2])};
-  }
   long long t_start = 0;
   if (args.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int64_t kb = int64_t(pc.tl0) * args.kq;
@@ -547,6 +542,42 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
     tr[8] = pc.tm;
     tr[9] = pc.tk;
   }
+}
+
+template <class Op, bool kVec>
+__global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
+    simt_mm_kernel(const MMArgs args, const __grid_constant__ PieceTable table) {
+  using C = SimtCfg<Op>;
+  Piece pc;
+  if (table.count > 0) {
+    pc = table.p[blockIdx.x];
+  } else {  // derive this CTA's piece of the default plan (same code as paco_plan_cta)
+    UnitBox b;
+    if (table.grid_s > 0)
+      plan_grid_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, table.grid_s, int(blockIdx.x), b);
+    else
+      plan_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, int(gridDim.x), int(blockIdx.x), b, args.kw);
+    pc = Piece{int32_t(b.o[0]), int32_t(b.o[1]), int32_t(b.o[2]), int32_t(b.e[0]), int32_t(b.e[1]),
+               int32_t(b.e[2])};
+  }
+  simt_mm_body<Op, kVec>(args, pc);
+}
+
+// A batch of independent problems (e.g. every COMPUTE cuboid of a GPU-level
+// PACO plan on one device) as ONE launch: CTA ranges [first[q], first[q+1])
+// take problem q's tile-grid pieces (k split grid_s[q] ways).
+template <class Op, bool kVec>
+__global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
+    simt_mm_batch_kernel(const __grid_constant__ BatchTable bt) {
+  using C = SimtCfg<Op>;
+  int q = 0;
+  while (q + 1 < bt.count && int64_t(blockIdx.x) >= bt.first[q + 1]) ++q;
+  const MMArgs& args = bt.args[q];
+  UnitBox b;
+  plan_grid_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, bt.grid_s[q], int(blockIdx.x - bt.first[q]), b);
+  const Piece pc{int32_t(b.o[0]), int32_t(b.o[1]), int32_t(b.o[2]), int32_t(b.e[0]), int32_t(b.e[1]),
+                 int32_t(b.e[2])};
+  simt_mm_body<Op, kVec>(args, pc);
 }
 
 // ---------------------------------------------------------------------------
@@ -761,6 +792,80 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
   kern<<<grid, Cfg::THREADS, Cfg::SMEM, stream>>>(args, table);
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;
+}
+
+template <class Op>
+int launch_simt_batch(int device, cudaStream_t stream, int count, const paco_mm_problem* pr) {
+  using Cfg = SimtCfg<Op>;
+  static BatchTable bt;  // ~7.5 KB; copied into the launch's parameter buffer
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  bool vec = true;
+  int64_t total = 0;
+  int c = 0;
+  for (int q = 0; q < count; ++q) {
+    const paco_mm_problem& P = pr[q];
+    if (P.flags & PACO_MM_REMOTE) {
+      set_error("paco_mm_batch: PACO_MM_REMOTE is not supported in a batch");
+      return PACO_ERR_UNSUPPORTED;
+    }
+    if ((P.flags & PACO_MM_OVERWRITE) && (P.flags & PACO_MM_ATOMIC)) {
+      set_error("paco_mm_batch: problem %d combines OVERWRITE with ATOMIC", q);
+      return PACO_ERR_ARG;
+    }
+    if (P.n <= 0 || P.m <= 0) continue;
+    if (P.k <= 0) {
+      if (P.flags & PACO_MM_OVERWRITE) {
+        const int rc = paco_fill(device, stream, Op::kId, P.C, P.ldc, P.n, P.m);
+        if (rc) return rc;
+      }
+      continue;
+    }
+    const int64_t units[3] = {(P.n + Cfg::BM - 1) / Cfg::BM, (P.m + Cfg::BN - 1) / Cfg::BN,
+                              (P.k + Cfg::KQ - 1) / Cfg::KQ};
+    int64_t ctas = 0;
+    const int s = grid_ksplit(units, Cfg::KQ, &ctas);
+    MMArgs a{P.A, P.B, P.C, P.lda, P.ldb, P.ldc, P.n, P.m, P.k, Cfg::KQ, (P.flags & PACO_MM_OVERWRITE) ? 1 : 0,
+             g_trace_buffer,
+             (reinterpret_cast<uintptr_t>(P.C) % 16 == 0 && (P.ldc * sizeof(typename Op::TC)) % 16 == 0) ? 1 : 0,
+             (P.flags & PACO_MM_ATOMIC) ? 1 : 0, plan_kw()};
+    if (a.overwrite && s > 1) {  // k-split pieces fold into C: it must hold the semiring zero first
+      const int rc = paco_fill(device, stream, Op::kId, P.C, P.ldc, P.n, P.m);
+      if (rc) return rc;
+      a.overwrite = 0;
+    }
+    vec = vec && (reinterpret_cast<uintptr_t>(P.A) % 16 == 0) && (reinterpret_cast<uintptr_t>(P.B) % 16 == 0) &&
+          ((P.lda * sizeof(typename Op::TA)) % 16 == 0) && ((P.ldb * sizeof(typename Op::TB)) % 16 == 0);
+    bt.args[c] = a;
+    bt.grid_s[c] = s;
+    bt.first[c] = total;
+    total += ctas;
+    ++c;
+  }
+  bt.count = c;
+  bt.first[c] = total;
+  if (c == 0) return PACO_OK;
+  if (total > INT32_MAX) {
+    set_error("paco_mm_batch: %lld CTAs exceed the grid limit", (long long)total);
+    return PACO_ERR_ARG;
+  }
+  auto kern = vec ? simt_mm_batch_kernel<Op, true> : simt_mm_batch_kernel<Op, false>;
+  PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
+  kern<<<unsigned(total), Cfg::THREADS, Cfg::SMEM, stream>>>(bt);
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
+int launch_mm_simt_batch(int sr, int device, cudaStream_t stream, int count, const paco_mm_problem* problems) {
+  return dispatch_op(sr, [&](auto op) -> int {
+    using Op = decltype(op);
+    if constexpr (Op::kId == PACO_SR_BF16_F32) {
+      set_error("paco_mm_batch: bf16 goes through the tcgen05 kernel");
+      return PACO_ERR_UNSUPPORTED;
+    } else {
+      return launch_simt_batch<Op>(device, stream, count, problems);
+    }
+  });
 }
 
 int launch_mm_simt(int sr, int device, cudaStream_t stream, const void* A, int64_t lda, const void* B,

@@ -354,7 +354,7 @@ _TC_KERNELS = (nat.SR_BF16_F32, nat.SR_F32_TC)
 
 def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str = "serial_sim",
                sims: dict | None = None, *, devices: list[int] | None = None,
-               fused_folds: bool | None = None) -> CostReport:
+               fused_folds: bool | None = None, batch: bool | None = None) -> CostReport:
     """Run an MM plan on B200s (matmul.py:417-462).
 
     Worker ``w`` runs on ``devices[w % len(devices)]`` with its own stream
@@ -364,6 +364,12 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
     peer access.  ``mode`` keeps the reference meaning: ``serial_sim``
     enqueues tasks in plan order from this thread, ``parallel`` from one host
     thread per worker; the device result is identical.
+
+    ``batch`` (default: on when every worker is on one device, the semiring
+    runs on the SIMT kernel and the k-cut folds are fused): the plan's COMPUTE
+    cuboids become ONE ``paco_mm_batch`` launch -- the GPU-level PACO plan is
+    the CTA-level work list -- instead of one launch per task; any explicit
+    REDUCE folds follow in plan order.
     """
     if sims is not None:
         raise NotImplementedError("cache simulation is out of scope on B200; use ncu counters")
@@ -385,6 +391,11 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
         fused_folds = False  # the tensor-core epilogue folds atomically only into local C
     fused_folds = fused_folds and has_reduces
     fold_dest = fold_destinations(plan) if fused_folds else {}
+    if batch is None:
+        batch = len(used) == 1 and kid not in _TC_KERNELS and (fused_folds or not has_reduces)
+    batch = bool(batch) and len(used) == 1 and kid not in _TC_KERNELS
+    batched: list = []     # COMPUTE problems, launched together after the plan walk
+    deferred: list = []    # explicit REDUCE folds, run after the batch in plan order
     lib = nat.load()
     for d in used:
         if d != home:
@@ -422,8 +433,9 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
         def runner(task) -> None:
             w = task.workers()[0]
             st = streams[w]
-            for d in task.deps:
-                st.wait_event(events[d])
+            if not batch:  # batched: nothing is launched here, the order is applied after the walk
+                for d in task.deps:
+                    st.wait_event(events[d])
             if task.kind == COMPUTE:
                 cb: Cuboid = task.region
                 dv = dev_of[w]
@@ -434,10 +446,18 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
                 else:
                     out = buffer(cb.out).sub(cb.out_i0, cb.out_j0, cb.n, cb.m)
                     flags = 0
-                launch_mm(kid, st, a_on[dv].sub(cb.i0, cb.l0, cb.n, cb.k),
-                          b_on[dv].sub(cb.l0, cb.j0, cb.k, cb.m), out, flags=flags, device=dv)
+                av = a_on[dv].sub(cb.i0, cb.l0, cb.n, cb.k)
+                bv = b_on[dv].sub(cb.l0, cb.j0, cb.k, cb.m)
+                if batch:
+                    batched.append((task.id, (av.ptr, av.ld, bv.ptr, bv.ld, out.ptr, out.ld, cb.n, cb.m, cb.k,
+                                              flags)))
+                    return
+                launch_mm(kid, st, av, bv, out, flags=flags, device=dv)
             elif task.kind == REDUCE and not fused_folds:
                 bid, tgt, oi, oj, rn, rm = reduces[task.id]
+                if batch:
+                    deferred.append((task.id, buffer(tgt).sub(oi, oj, rn, rm), temps[bid]))
+                    return
                 launch_fold(semiring.kernel_id, st, buffer(tgt).sub(oi, oj, rn, rm),
                             temps[bid], reset=True)
             ev = torch.cuda.Event()
@@ -445,6 +465,10 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
             events[task.id] = ev
 
         report = execute_plan(plan, runner, mode)
+        if batch:  # the whole plan on one device: one launch, then the folds in plan order
+            nat.mm_batch(home, stage.cuda_stream, kid, [p for _, p in sorted(batched)])
+            for _, dst, src in sorted(deferred, key=lambda x: x[0]):
+                launch_fold(semiring.kernel_id, stage, dst, src, reset=True)
         for s in streams:
             stage.wait_stream(s)
         t_end = torch.cuda.Event(enable_timing=True)

@@ -444,3 +444,29 @@ def test_tensor_core_misaligned_views(sr, offs):
     outside = big_c.clone()
     outside[ri:ri + n, rj:rj + m] = 0
     assert torch.count_nonzero(outside[ri:ri + n, :rj]) == rj * n  # neighbours untouched
+
+
+@pytest.mark.parametrize("fused", [None, False])
+def test_plan_as_one_batched_launch(fused):
+    """mm_execute on one device runs the plan's COMPUTE cuboids as one
+    paco_mm_batch launch (explicit REDUCE folds after it): same C as per-task
+    launches and as the oracle, for one-piece and multi-piece plans."""
+    rng = np.random.default_rng(61)
+    n, m, k = 333, 290, 701
+    A = tropical(rng, (n, k), 0, 2**20, 0.1)
+    B = tropical(rng, (k, m), 0, 2**20, 0.1)
+    C0 = tropical(rng, (n, m), 0, 2**21, 0.3)
+    want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, C0.copy())
+    for p in (3, 5, 8, 13):
+        for plan in (M.mm_one_piece_partition(n, m, k, p), M.mm_paco_partition(n, m, k, p, base=32)):
+            for batch in (True, False):
+                C = C0.copy()
+                M.mm_execute(plan, A, B, C, M.SEMIRING_MINPLUS_SAT, mode="parallel", fused_folds=fused,
+                             batch=batch)
+                assert np.array_equal(C, want), (p, plan.meta["variant"], batch)
+    # int (+,x) with k-cuts, int32 operands -> int64
+    Ai = rng.integers(-100, 100, (n, k)).astype(np.int32)
+    Bi = rng.integers(-100, 100, (k, m)).astype(np.int32)
+    C = np.zeros((n, m), np.int64)
+    M.mm_execute(M.mm_paco_partition(n, m, k, 7, base=32), Ai, Bi, C, M.SEMIRING_INT, fused_folds=fused)
+    assert np.array_equal(C, Ai.astype(np.int64) @ Bi.astype(np.int64))

@@ -83,7 +83,8 @@ def main():
         ops = 2 * 384 * 320 * 256
         res["cfg1"] = {"ms_paco_p3_mm_execute": med, "gop_s": ops / med / 1e6,
                        "ms_single_launch": one, "gop_s_single_launch": ops / one / 1e6,
-                       "note": "latency-bound correctness config; mm_execute = 17 COMPUTE + 4 REDUCE tasks"}
+                       "note": "latency-bound correctness config; mm_execute: 17 COMPUTE cuboids as one paco_mm_batch "
+                               "launch, 4 REDUCEs fused into its epilogues; time is host-bound (plan walk)"}
 
     if 2 in only:  # cfg2: (min,+) 8192^3
         n = 8192
