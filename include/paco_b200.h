@@ -8,6 +8,8 @@
  *   paco_mm        <- mm_seq(A, B, C, semiring, base)            matmul.py:342-397
  *                     i.e. the COMPUTE-task body of mm_execute   matmul.py:441-454
  *                     and Semiring.block_mm(C, A, B)             matmul.py:41,45-50
+ *   paco_mm_batch  <- every COMPUTE task of one device's share of a plan at once
+ *                     (the runner loop of mm_execute, matmul.py:440-454)
  *   paco_fold      <- REDUCE-task body: copyto(t, vadd(t, temp)); temp.fill(zero)
  *                                                                matmul.py:455-460
  *   paco_fill      <- np.full(shape, semiring.zero)              matmul.py:430-433
