@@ -86,13 +86,15 @@ using KindTF32x3W = KindTF32x3T<256, 4, 16>;
 // 128 KB from L2 for every 128 KB of C it writes, which puts cfg3 on the L2
 // throughput cap instead of HBM.  A ring of AST stages, EB staging buffers
 // per epilogue warp.
-template <int AST, int EB, int EW = 8, int EC = 32>
+template <int AST, int EB, int EW = 8, int EC = 32, int BN_ = 256>
 struct KindBF16Res {
-  static constexpr int BN = 256, BK = 64, UMMA_K = 16, STAGES = AST, ELEM = 2, NOPS = 1, PASSES = 1;
+  static constexpr int BN = BN_, BK = 64, UMMA_K = 16, STAGES = AST, ELEM = 2, NOPS = 1, PASSES = 1;
   static constexpr int KB_MAX = 4, EPI_WARPS = EW, EPI_BUFS = EB, EPI_COLS = EC, SWZ = 128;
   static constexpr int RING_BYTES = KB_MAX * BN * BK * 2 + AST * 128 * BK * 2;
   static constexpr bool B_KMAJOR = false, B_RES = true;
-  static constexpr uint32_t IDESC = KindBF16::IDESC;
+  // F32 accumulate, BF16 A/B, A K-major, B MN-major, N = BN
+  static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                                    (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
   static constexpr CUtensorMapDataType DT = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
 };
 
@@ -994,7 +996,15 @@ int run_tc(int device, Scratch& sc, cudaStream_t stream, const tc::TcMaps& maps,
     return PACO_ERR_ARG;
   }
   const int grid = int(tiles < kNumSMs ? tiles : kNumSMs);
-  args.groups = (K::B_RES && count == 1) ? (args.tiles_nb < grid ? args.tiles_nb : grid) : 1;
+  // resident B: one group per column block, but only as many groups as divide
+  // the grid evenly (148 = 4 x 37), else the groups' CTA counts differ and the
+  // smaller groups finish last; a group then walks several column blocks.
+  args.groups = 1;
+  if (K::B_RES && count == 1) {
+    int g = args.tiles_nb < grid ? args.tiles_nb : grid;
+    while (g > 1 && grid % g) --g;
+    args.groups = g;
+  }
   {
     void* counters;
     if ((rc = scratch(device, sc, sizeof(int32_t) * args.groups, stream, &counters))) return rc;
@@ -1081,7 +1091,8 @@ int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t ld
                       void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces,
                       int n_pieces, int flags) {
   // k <= 256 (cfg3): resident-B kind, 5-stage A ring, 8 epilogue warps staging
-  // 16-column boxes (measured best of 7 layouts, tools/tc_trace.py); PACO_TC_RESV
+  // 16-column boxes (measured best of 10 layouts incl. N = 128 tiles with a
+  // 6-8 stage ring: 76-84 us vs 58; tools/tc_trace.py); PACO_TC_RESV
   // selects the alternatives for experiments (-1 = streaming kind).
   static const int resv = getenv("PACO_TC_RESV") ? atoi(getenv("PACO_TC_RESV")) : 7;
 #define PACO_TC_GO(KIND) return launch_tc<KIND>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags)
