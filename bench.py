@@ -214,7 +214,9 @@ def main():
         def step():
             launch_mm(kid, st, a, b, c)
         launches_per_step = 1
-        plan_desc = "1 GPU, CTA-level MM-1-Piece over 296 pieces (148 SMs x 2)"
+        ks, ctas = nat.cta_grid(kid, N, N, N)
+        plan_desc = (f"1 GPU, CTA-level tile grid: {ctas} CTAs of one 128x128 C tile, k split {ks} way(s) "
+                     "(cost-model choice over the PACO cuboid plan, DESIGN.md section 5)")
     elif args.fold == "fused":
         plan = M.mm_one_piece_partition(N, N, N, world)
         ex = FusedDistributedMM(plan, sr, kid, dev)
@@ -222,11 +224,13 @@ def main():
 
         def step():
             ex.run(A, B)
-        launches_per_step = 1 + len(ex.launches)
+        launches_per_step = 1 + len(ex.launches) + len(ex.incoming)
+        how = ("staged: local temporary -> one NVLink copy into the owner's staging slot -> owner fold"
+               if ex.fold_style == "stage" else
+               f"{'TMA bulk' if ex.remote_bulk else 'element'} atomics into the owner's C over NVLink")
         plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}); its {nred} k-cut folds "
-                     f"are fused into the kernels (upper-k ranks fold their tiles into the owner's C "
-                     f"over CUDA IPC/NVLink, {'TMA bulk' if ex.remote_bulk else 'element'} atomics); "
-                     "CTA-level MM-1-Piece inside each rank")
+                     f"need no REDUCE temporaries or NCCL call: local ones are fused into the kernels' epilogues, "
+                     f"remote ones {how} (CUDA IPC); tile-grid CTA plan inside each rank")
     else:
         plan = M.mm_one_piece_partition(N, N, N, world)
         ex = DistributedMM(plan, sr, CudaOps(sr, kid, st))
@@ -238,7 +242,7 @@ def main():
         launches_per_step = 2 + len(ex.temp_ids) + 3 * nred + len(ex.mine)
         plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}) "
                      f"({sum(1 for t in plan.tasks if t.kind == 'reduce')} k-cut NCCL MIN folds), "
-                     "CTA-level MM-1-Piece inside each rank")
+                     "tile-grid CTA plan inside each rank")
 
     def barrier():
         if world > 1:

@@ -230,8 +230,10 @@ class FusedDistributedMM:
     handles with ``all_gather_object``).
     """
 
-    def __init__(self, plan: Plan, semiring, kernel_id: int, device: int, *, group=None):
+    def __init__(self, plan: Plan, semiring, kernel_id: int, device: int, *, group=None,
+                 fold_style: str | None = None):
         import ctypes
+        import os
 
         import numpy as np
 
@@ -269,7 +271,64 @@ class FusedDistributedMM:
         self.views = [View.raw(p, self.n, self.m, self.itemsize, device) for p in self.ptrs]
         owners, self.launches = fused_launches(plan, self.rank)
         self.owned = [rect for rect, w in owners if w == self.rank]
-        self.remote_bulk = self._probe_remote_bulk()
+        # remote folds: "stage" = compute into a local temporary, one bulk copy
+        # into a staging slot in the owner's memory (IPC), the owner folds it
+        # after a barrier; "atomic" = the epilogue folds straight into the
+        # owner's C over NVLink (element atomics, or TMA bulk reductions with
+        # PACO_REMOTE_BULK=1).
+        self.fold_style = fold_style or os.environ.get("PACO_FOLD_STYLE", "stage")
+        if self.fold_style not in ("stage", "atomic"):
+            raise ValueError(f"fold_style must be 'stage' or 'atomic', got {self.fold_style!r}")
+        self.remote_bulk = self._probe_remote_bulk() if self.fold_style == "atomic" else False
+        self._setup_staging()
+
+    def _setup_staging(self) -> None:
+        """Staging slots: every rank's remote launches into this rank's C get a slot
+        in one IPC buffer here; senders keep a local temporary per remote launch."""
+        import ctypes
+
+        from .device import View
+
+        lib = self.nat.load()
+        self.incoming = []   # (rect, offset in elements) of slots others fill
+        self.outgoing = []   # per launch index: (slot offset at the owner) or None
+        self.temps = {}
+        self.stage_ptr = None
+        self.stage_ptrs = [None] * self.world
+        if self.fold_style != "stage" or self.world == 1:
+            return
+        slots = {}  # (src rank, launch index) -> offset at the owner
+        sizes = [0] * self.world
+        for r in range(self.world):
+            for j, (_, _, owner, rect) in enumerate(fused_launches(self.plan, r)[1]):
+                if owner == r:
+                    continue
+                slots[(r, j)] = sizes[owner]
+                if owner == self.rank:
+                    self.incoming.append((rect, sizes[owner]))
+                sizes[owner] += rect[2] * rect[3]
+        if sizes[self.rank]:
+            ptr = ctypes.c_void_p()
+            self.nat.check(lib.paco_device_alloc(self.device, sizes[self.rank] * self.itemsize, ctypes.byref(ptr)))
+            self.stage_ptr = ptr.value
+        handle = ctypes.create_string_buffer(64)
+        if self.stage_ptr is not None:
+            self.nat.check(lib.paco_ipc_handle(self.device, self.stage_ptr, handle))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw if self.stage_ptr is not None else None, group=self.group)
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.stage_ptrs[r] = self.stage_ptr
+            elif h is not None and any(o == r for _, _, o, _ in self.launches):
+                p = ctypes.c_void_p()
+                self.nat.check(lib.paco_ipc_open(self.device, ctypes.create_string_buffer(h, 64), ctypes.byref(p)))
+                self.stage_ptrs[r] = p.value
+        for j, (_, _, owner, rect) in enumerate(self.launches):
+            if owner == self.rank:
+                self.outgoing.append(None)
+                continue
+            self.outgoing.append(slots[(self.rank, j)])
+            self.temps[j] = torch.empty((rect[2], rect[3]), dtype=self.tdtype, device=self.device)
 
     def _probe_remote_bulk(self) -> bool:
         """Can the TMA bulk-reduce epilogue fold into a peer's IPC-mapped C?
@@ -334,13 +393,26 @@ class FusedDistributedMM:
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self.group)          # every owner's C is initialised
         av, bv = View.of(A), View.of(B)
-        for (ai, al, an, ak), (bl, bj, bk, bm), owner, (ci, cj, cn, cm) in self.launches:
+        es = self.itemsize
+        for j, ((ai, al, an, ak), (bl, bj, bk, bm), owner, (ci, cj, cn, cm)) in enumerate(self.launches):
+            a, b = av.sub(ai, al, an, ak), bv.sub(bl, bj, bk, bm)
+            if owner != self.rank and self.fold_style == "stage":
+                t = self.temps[j]
+                launch_mm(self.kid, st, a, b, View.of(t), overwrite=True, device=self.device)
+                slot = self.stage_ptrs[owner] + self.outgoing[j] * es
+                self.nat.check(self.nat.load().paco_copy2d(self.device, st.cuda_stream, slot, cm * es, t.data_ptr(),
+                                                           t.stride(0) * es, cm * es, cn))
+                continue
             remote = owner != self.rank and not self.remote_bulk
             flags = self.nat.MM_ATOMIC | (self.nat.MM_REMOTE if remote else 0)
-            launch_mm(self.kid, st, av.sub(ai, al, an, ak), bv.sub(bl, bj, bk, bm),
-                      self.views[owner].sub(ci, cj, cn, cm), flags=flags, device=self.device)
+            launch_mm(self.kid, st, a, b, self.views[owner].sub(ci, cj, cn, cm), flags=flags, device=self.device)
         torch.cuda.synchronize(self.device)
-        dist.barrier(group=self.group)          # every remote fold has landed
+        dist.barrier(group=self.group)          # every remote fold / staged block has landed
+        if self.incoming:
+            for (ci, cj, cn, cm), off in self.incoming:
+                src = View.raw(self.stage_ptr + off * es, cn, cm, es, self.device, ld=cm)
+                launch_fold(self.semiring.kernel_id, st, mine.sub(ci, cj, cn, cm), src, False)
+            torch.cuda.synchronize(self.device)
 
     def gather(self, out: torch.Tensor, dst: int = 0) -> None:
         """Copy this rank's C into ``out`` and reduce the owners' pieces onto ``dst``."""
@@ -354,5 +426,10 @@ class FusedDistributedMM:
         for r, p in enumerate(self.ptrs):
             if r != self.rank:
                 lib.paco_ipc_close(self.device, p)
+        for r, p in enumerate(self.stage_ptrs):
+            if p is not None and r != self.rank:
+                lib.paco_ipc_close(self.device, p)
+        if self.stage_ptr is not None:
+            lib.paco_device_free(self.device, self.stage_ptr)
         lib.paco_device_free(self.device, self.own_ptr)
-        self.ptrs = []
+        self.ptrs, self.stage_ptrs, self.stage_ptr = [], [None] * self.world, None

@@ -36,8 +36,9 @@ def _inputs(n, m, k, seed):
     return A, B, C
 
 
-def _worker(rank, world, port, cases, q, remote_bulk="0"):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PACO_REMOTE_BULK=remote_bulk)
+def _worker(rank, world, port, cases, q, remote_bulk="0", style="atomic"):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PACO_REMOTE_BULK=remote_bulk,
+                      PACO_FOLD_STYLE=style)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     from paper_2011_01441_b200 import _native as nat
@@ -72,15 +73,17 @@ def _worker(rank, world, port, cases, q, remote_bulk="0"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,remote_bulk", [(2, "0"), (3, "0"), (2, "1")])
-def test_fused_ipc_distributed_matches_oracle(world, remote_bulk):
-    """Remote folds as element atomics (default) and, with PACO_REMOTE_BULK=1,
-    as TMA bulk reductions into the peer's IPC mapping (probed first)."""
+@pytest.mark.parametrize("world,remote_bulk,style", [(2, "0", "stage"), (3, "0", "stage"), (2, "0", "atomic"),
+                                                     (3, "0", "atomic"), (2, "1", "atomic")])
+def test_fused_ipc_distributed_matches_oracle(world, remote_bulk, style):
+    """Remote folds staged (default: local temporary, one bulk copy into the
+    owner's staging slot, owner folds), as element atomics into the owner's C,
+    or, with PACO_REMOTE_BULK=1, as TMA bulk reductions into its IPC mapping."""
     cases = [("one_piece", 96, 80, 700), ("one_piece", 200, 150, 260), ("paco", 130, 90, 333)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q, remote_bulk)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q, remote_bulk, style)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
