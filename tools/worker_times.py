@@ -13,11 +13,15 @@ from paper_2011_01441_b200.mm import launch_mm, fold_destinations
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 ps = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "1,2,3,4,5,7,8").split(",")]
-sr, kid = M.SEMIRING_MAXPLUS, nat.SR_MAXPLUS_SAT32
+which = sys.argv[3] if len(sys.argv) > 3 else "maxplus"
 g = torch.Generator(device="cuda").manual_seed(1004)
-A = torch.randint(-2**20, 2**20, (n, n), device="cuda", dtype=torch.int32, generator=g)
-B = torch.randint(-2**20, 2**20, (n, n), device="cuda", dtype=torch.int32, generator=g)
-C = torch.full((n, n), -2**30, device="cuda", dtype=torch.int32)
+if which == "maxplus":
+    sr, kid, lo, zero = M.SEMIRING_MAXPLUS, nat.SR_MAXPLUS_SAT32, -2**20, -2**30
+else:
+    sr, kid, lo, zero = M.SEMIRING_MINPLUS_SAT, nat.SR_MINPLUS_SAT32, 0, 2**30
+A = torch.randint(lo, 2**20, (n, n), device="cuda", dtype=torch.int32, generator=g)
+B = torch.randint(lo, 2**20, (n, n), device="cuda", dtype=torch.int32, generator=g)
+C = torch.full((n, n), zero, device="cuda", dtype=torch.int32)
 a, b, c = View.of(A), View.of(B), View.of(C)
 st = torch.cuda.current_stream()
 
@@ -32,7 +36,7 @@ def timed(fn, reps=2):
     return best
 
 
-out = {"n": n, "semiring": "maxplus_sat32", "plans": []}
+out = {"n": n, "semiring": which + "_sat32", "plans": []}
 t1 = None
 for p in ps:
     plan = M.mm_one_piece_partition(n, n, n, p)
