@@ -127,7 +127,7 @@ int paco_plan_one_piece(int64_t n, int64_t m, int64_t k, int p, int64_t* out);
 /* The default CTA-level plan of paco_mm for the SIMT semirings: one CTA per C
  * tile and k quantum range, the k extent split `*ksplit` ways (CTA idx ->
  * tile idx / ksplit in row-major tile order, k part idx % ksplit), `*ctas`
- * CTAs in all.  ksplit minimises ceil(tiles * s / 148) * (k / s + 96): whole
+ * CTAs in all.  ksplit minimises ceil(tiles * s / 148) * (k / s + 64): whole
  * SM-waves of pieces, each charged a fixed per-visit cost.  Host only. */
 int paco_cta_grid(int semiring, int64_t n, int64_t m, int64_t k, int* ksplit, int64_t* ctas);
 

@@ -41,7 +41,7 @@ constexpr int kDefaultWaves = 4;
 constexpr bool kMbarPipe = PACO_SIMT_MBAR != 0;  // split arrive/wait stage ring (vs __syncthreads)
 constexpr double kDefaultKw = 1.0;
 constexpr int kMaxKSplit = 64;
-constexpr double kVisitK = 96.0;  // per-visit cost in k elements
+constexpr double kVisitK = 64.0;  // per-visit cost in k elements (re-fitted with the mbarrier ring)
 
 // Device buffer of 10 x (grid size) int64 set by paco_debug_trace(); when
 // non-null every CTA of the next launches records smid and start/end times.
