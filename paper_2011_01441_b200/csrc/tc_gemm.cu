@@ -1091,19 +1091,12 @@ int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t ld
                       void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const int32_t* pieces,
                       int n_pieces, int flags) {
   // k <= 256 (cfg3): resident-B kind, 5-stage A ring, 8 epilogue warps staging
-  // 16-column boxes (measured best of 10 layouts incl. N = 128 tiles with a
-  // 6-8 stage ring: 76-84 us vs 58; tools/tc_trace.py); PACO_TC_RESV
-  // selects the alternatives for experiments (-1 = streaming kind).
+  // 16-column boxes -- measured best of 10 layouts (ring depth 2-8, staging
+  // buffers 1-4 per warp, 16/32-column boxes, N = 128 tiles: 58 vs 59.5-84 us;
+  // DESIGN.md section 6); PACO_TC_RESV=-1 forces the streaming kind.
   static const int resv = getenv("PACO_TC_RESV") ? atoi(getenv("PACO_TC_RESV")) : 7;
 #define PACO_TC_GO(KIND) return launch_tc<KIND>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags)
-  if (k <= 256 && resv >= 0) {
-    if (resv == 0) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<3, 1>));
-    if (resv == 1) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<4, 1>));
-    if (resv == 3) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16T<4, 1, 8>));
-    if (resv == 5) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16T<4, 2, 8, 16>));
-    if (resv == 6) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<4, 2, 8, 16>));
-    PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<5, 1, 8, 16>));
-  }
+  if (k <= 256 && resv >= 0) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<5, 1, 8, 16>));
 #undef PACO_TC_GO
   return launch_tc<tc::KindBF16>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
 }
