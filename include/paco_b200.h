@@ -137,9 +137,13 @@ int paco_cta_grid(int semiring, int64_t n, int64_t m, int64_t k, int* ksplit, in
  * > 1%.  Writes p rows of (ti0, tj0, tl0, tn, tm, tk) into out[p*6]. Host only. */
 int paco_plan_cta(int semiring, int64_t n, int64_t m, int64_t k, int p, int32_t* out);
 
-/* dst (+)= src elementwise (n x m views); if reset_src, src = semiring zero. */
+/* dst (+)= src elementwise (n x m views).  flags: PACO_FOLD_RESET -- src = semiring
+ * zero afterwards (the REDUCE body); PACO_FOLD_ATOMIC -- one global atomic (+) per
+ * element, so other kernels may fold into dst concurrently (fused k-cut folds). */
+#define PACO_FOLD_RESET 1
+#define PACO_FOLD_ATOMIC 2
 int paco_fold(int device, void* stream, int semiring, void* dst, int64_t ld_dst, void* src,
-              int64_t ld_src, int64_t n, int64_t m, int reset_src);
+              int64_t ld_src, int64_t n, int64_t m, int flags);
 
 /* dst = semiring zero (the value the reference fills temporaries with). */
 int paco_fill(int device, void* stream, int semiring, void* dst, int64_t ld, int64_t n, int64_t m);

@@ -34,6 +34,8 @@ MM_OVERWRITE = 1
 MM_ATOMIC = 2
 MM_REMOTE = 4
 MM_PACO_PLAN = 8
+FOLD_RESET = 1
+FOLD_ATOMIC = 2
 TROPICAL_INF = 1 << 30
 MAX_PIECES = 640
 

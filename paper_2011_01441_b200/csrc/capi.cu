@@ -130,12 +130,16 @@ int paco_mm_tile_shape(int semiring, int* bm, int* bn, int* bk, int* cps) {
 }
 
 int paco_fold(int device, void* stream, int semiring, void* dst, int64_t ld_dst, void* src,
-              int64_t ld_src, int64_t n, int64_t m, int reset_src) {
+              int64_t ld_src, int64_t n, int64_t m, int flags) {
   PACO_TRY(check_sr(semiring));
+  if (flags & ~(PACO_FOLD_RESET | PACO_FOLD_ATOMIC)) {
+    set_error("paco_fold: unknown flags 0x%x", flags);
+    return PACO_ERR_ARG;
+  }
   PACO_TRY(check_view("dst", dst, ld_dst, n, m));
   PACO_TRY(check_view("src", src, ld_src, n, m));
   PACO_TRY(use_device(device));
-  return launch_fold(semiring, static_cast<cudaStream_t>(stream), dst, ld_dst, src, ld_src, n, m, reset_src);
+  return launch_fold(semiring, static_cast<cudaStream_t>(stream), dst, ld_dst, src, ld_src, n, m, flags);
 }
 
 int paco_fill(int device, void* stream, int semiring, void* dst, int64_t ld, int64_t n, int64_t m) {

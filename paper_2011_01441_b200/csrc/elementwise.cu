@@ -20,19 +20,22 @@ int ew_grid(int64_t n_elems, int threads) {
 }
 }  // namespace
 
+// flags: PACO_FOLD_RESET (src = zero afterwards), PACO_FOLD_ATOMIC (dst (+)= src
+// as one global atomic per element: safe while other kernels fold into dst).
 template <class Op>
 __global__ void fold_kernel(typename Op::TC* dst, int64_t ldd, typename Op::TC* src, int64_t lds,
-                            int64_t n, int64_t m, int reset) {
-  const int64_t total = n * m;
+                            int64_t n, int64_t m, int flags) {
   const auto z = Op::zero();
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / m, j = e - i * m;
-    typename Op::TC* s = src + i * lds + j;
-    typename Op::TC* d = dst + i * ldd + j;
-    *d = Op::combine(*d, *s);
-    if (reset) *s = z;
-  }
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < m; j += int64_t(gridDim.x) * blockDim.x) {
+      typename Op::TC* s = src + i * lds + j;
+      typename Op::TC* d = dst + i * ldd + j;
+      if (flags & PACO_FOLD_ATOMIC)
+        Op::atomic_combine(d, *s);
+      else
+        *d = Op::combine(*d, *s);
+      if (flags & PACO_FOLD_RESET) *s = z;
+    }
 }
 
 template <class Op>
@@ -112,13 +115,14 @@ __global__ void lincomb_kernel(T* out, int64_t ldo, int64_t n, int64_t m, const 
 }
 
 int launch_fold(int sr, cudaStream_t st, void* dst, int64_t ldd, void* src, int64_t lds, int64_t n,
-                int64_t m, int reset) {
+                int64_t m, int flags) {
   if (n <= 0 || m <= 0) return PACO_OK;
   return dispatch_op(sr, [&](auto op) -> int {
     using Op = decltype(op);
     using TC = typename Op::TC;
-    fold_kernel<Op><<<ew_grid(n * m, 256), 256, 0, st>>>(static_cast<TC*>(dst), ldd,
-                                                         static_cast<TC*>(src), lds, n, m, reset);
+    const int64_t xb = (m + 255) / 256, yb0 = n < 65535 ? n : 65535, ycap = 2368 / xb + 1;
+    const dim3 grid(unsigned(xb), unsigned(yb0 < ycap ? yb0 : ycap));
+    fold_kernel<Op><<<grid, 256, 0, st>>>(static_cast<TC*>(dst), ldd, static_cast<TC*>(src), lds, n, m, flags);
     PACO_CUDA_TRY(cudaGetLastError());
     return PACO_OK;
   });

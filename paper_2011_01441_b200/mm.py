@@ -63,9 +63,13 @@ def launch_mm(kid: int, stream: torch.cuda.Stream, a: View, b: View, c: View, *,
         c.ptr, c.ld, c.rows, c.cols, a.cols, arr, npieces, flags | (nat.MM_OVERWRITE if overwrite else 0)))
 
 
-def launch_fold(kid: int, stream: torch.cuda.Stream, dst: View, src: View, reset: bool) -> None:
+def launch_fold(kid: int, stream: torch.cuda.Stream, dst: View, src: View, reset: bool, *,
+                atomic: bool = False) -> None:
+    """dst (+)= src (paco_fold); ``reset``: src = zero afterwards; ``atomic``: per-element
+    atomics, safe while other kernels fold into dst."""
+    flags = (nat.FOLD_RESET if reset else 0) | (nat.FOLD_ATOMIC if atomic else 0)
     nat.check(nat.load().paco_fold(dst.device, stream.cuda_stream, kid, dst.ptr, dst.ld,
-                                   src.ptr, src.ld, dst.rows, dst.cols, int(reset)))
+                                   src.ptr, src.ld, dst.rows, dst.cols, flags))
 
 
 def launch_fill(kid: int, stream: torch.cuda.Stream, dst: View) -> None:
@@ -350,6 +354,7 @@ def fold_destinations(plan: Plan) -> dict[int, tuple[int, int, int]]:
 
 
 _TC_KERNELS = (nat.SR_BF16_F32, nat.SR_F32_TC)
+_STAGE_ALL = os.environ.get("PACO_MM_STAGE_ALL") == "1"  # test hook: every worker takes the remote path
 
 
 def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str = "serial_sim",
@@ -422,6 +427,9 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
         streams = [torch.cuda.Stream(device=dev_of[w]) for w in range(plan.p)]
         for s in streams:
             s.wait_event(staged)
+        fold_stream = torch.cuda.Stream(device=home)   # staged remote blocks fold here
+        fold_stream.wait_event(staged)
+        tdt = torch_dtype(semiring.dtype)
         events: list[torch.cuda.Event | None] = [None] * len(plan.tasks)
         reduces = meta["reduces"]
         t_begin = torch.cuda.Event(enable_timing=True)
@@ -442,7 +450,7 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
                 if fused_folds:
                     fb, fi, fj = fold_dest.get(cb.out, (0, 0, 0))
                     out = c_view.sub(fi + cb.out_i0, fj + cb.out_j0, cb.n, cb.m)
-                    flags = nat.MM_ATOMIC | (nat.MM_REMOTE if dv != home else 0)
+                    flags = nat.MM_ATOMIC
                 else:
                     out = buffer(cb.out).sub(cb.out_i0, cb.out_j0, cb.n, cb.m)
                     flags = 0
@@ -452,7 +460,29 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
                     batched.append((task.id, (av.ptr, av.ld, bv.ptr, bv.ld, out.ptr, out.ld, cb.n, cb.m, cb.k,
                                               flags)))
                     return
-                launch_mm(kid, st, av, bv, out, flags=flags, device=dv)
+                if dv != home or _STAGE_ALL:
+                    # a worker on another GPU computes its block locally (plain epilogue),
+                    # ships it over NVLink in one copy into a staging buffer on the home
+                    # GPU, and the block is folded into its destination there with
+                    # per-element atomics (a k-cut partner may fold into the same block)
+                    with torch.cuda.device(dv):
+                        loc = torch.empty((cb.n, cb.m), dtype=tdt, device=dv)
+                        loc.record_stream(st)
+                    launch_mm(kid, st, av, bv, View.of(loc), overwrite=True, device=dv)
+                    stg = torch.empty((cb.n, cb.m), dtype=tdt, device=home)
+                    stg.record_stream(st)
+                    stg.record_stream(fold_stream)
+                    _copy2d(st, stg, 0, 0, loc, 0, 0, cb.n, cb.m)
+                    shipped = torch.cuda.Event()
+                    shipped.record(st)
+                    fold_stream.wait_event(shipped)
+                    launch_fold(semiring.kernel_id, fold_stream, out, View.of(stg), False, atomic=True)
+                    ev = torch.cuda.Event()
+                    ev.record(fold_stream)
+                    events[task.id] = ev
+                    return
+                else:
+                    launch_mm(kid, st, av, bv, out, flags=flags, device=dv)
             elif task.kind == REDUCE and not fused_folds:
                 bid, tgt, oi, oj, rn, rm = reduces[task.id]
                 if batch:
@@ -471,6 +501,7 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
                 launch_fold(semiring.kernel_id, stage, dst, src, reset=True)
         for s in streams:
             stage.wait_stream(s)
+        stage.wait_stream(fold_stream)
         t_end = torch.cuda.Event(enable_timing=True)
         t_end.record(stage)
         out.finish()

@@ -1,0 +1,33 @@
+"""Helper of tests/test_gpu_mm.py::test_remote_worker_staging (run with
+PACO_MM_STAGE_ALL=1): every plan worker takes mm_execute's remote-GPU path
+(local block, one copy, staged atomic fold) on the single test GPU."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+from oracle import cref
+from paper_2011_01441_b200 import matmul as M
+
+rng = np.random.default_rng(71)
+n, m, k = 301, 257, 603
+A = rng.integers(0, 2**20, (n, k)).astype(np.int32)
+B = rng.integers(0, 2**20, (k, m)).astype(np.int32)
+C0 = rng.integers(0, 2**21, (n, m)).astype(np.int32)
+want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, C0.copy())
+for p in (3, 5, 8):
+    for plan in (M.mm_one_piece_partition(n, m, k, p), M.mm_paco_partition(n, m, k, p, base=32)):
+        for fused in (None, False):
+            for mode in ("serial_sim", "parallel"):
+                C = C0.copy()
+                M.mm_execute(plan, A, B, C, M.SEMIRING_MINPLUS_SAT, mode=mode, fused_folds=fused, batch=False)
+                assert np.array_equal(C, want), (p, plan.meta["variant"], fused, mode)
+Af = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+Bf = rng.uniform(-1, 1, (k, m)).astype(np.float32)
+ref = Af.astype(np.float64) @ Bf.astype(np.float64)
+for sem in (M.SEMIRING_F32, M.SEMIRING_F32_SIMT):
+    C = np.zeros((n, m), np.float32)
+    M.mm_execute(M.mm_paco_partition(n, m, k, 5, base=32), Af, Bf, C, sem, mode="parallel", batch=False)
+    assert np.linalg.norm(C - ref) <= 1e-5 * np.linalg.norm(ref), sem.name
+print("stage-all ok")
