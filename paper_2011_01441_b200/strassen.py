@@ -404,6 +404,36 @@ def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stre
     _combine(ws, C, dt, stream)
 
 
+_STAGE_ALL = __import__("os").environ.get("PACO_MM_STAGE_ALL") == "1"  # test hook (see mm.py)
+
+
+def _dtype_of_view(v: View) -> torch.dtype:
+    return {4: torch.float32, 8: torch.float64}[v.elsize] if v.tensor is None or v.tensor.is_floating_point() \
+        else v.tensor.dtype
+
+
+def _local(v: View, dev: int, st) -> torch.Tensor:
+    """A copy of (peer) view ``v`` in ``dev``'s memory, made on stream ``st``."""
+    t = _local_empty(v, dev, st)
+    es = t.element_size()
+    nat.check(nat.load().paco_copy2d(dev, st.cuda_stream, t.data_ptr(), t.stride(0) * es, v.ptr, v.ld * es,
+                                     v.cols * es, v.rows))
+    return t
+
+
+def _local_empty(v: View, dev: int, st) -> torch.Tensor:
+    with torch.cuda.device(dev):
+        t = torch.empty((v.rows, v.cols), dtype=_dtype_of_view(v), device=dev)
+    t.record_stream(st)
+    return t
+
+
+def _copy_back(dst: View, t: torch.Tensor, dev: int, st) -> None:
+    es = t.element_size()
+    nat.check(nat.load().paco_copy2d(dev, st.cuda_stream, dst.ptr, dst.ld * es, t.data_ptr(), t.stride(0) * es,
+                                     dst.cols * es, dst.rows))
+
+
 def _ring_dtype(A, B) -> torch.dtype:
     dts = set()
     for x in (A, B):
@@ -525,12 +555,20 @@ def strassen_execute(plan: Plan, A, B, mode: str = "serial_sim", *, devices: lis
             for d in task.deps:
                 st.wait_event(events[d])
             with torch.cuda.device(dev_of[w]):
+                dv = dev_of[w]
+                remote = dv != home or _STAGE_ALL
                 if isinstance(task.region, LeafPiece):  # one worker's cuboid of a split leaf
                     leaf, cb = task.region.node, task.region.cuboid
                     A_n, B_n, C_n = ops[id(leaf)]
                     dst = C_n if cb.out == 0 else leaf_temps[(id(leaf), cb.out)]
-                    launch_mm(kid, st, A_n.sub(cb.i0, cb.l0, cb.n, cb.k), B_n.sub(cb.l0, cb.j0, cb.k, cb.m),
-                              dst.sub(cb.out_i0, cb.out_j0, cb.n, cb.m), overwrite=True, device=dev_of[w])
+                    a_v, b_v = A_n.sub(cb.i0, cb.l0, cb.n, cb.k), B_n.sub(cb.l0, cb.j0, cb.k, cb.m)
+                    d_v = dst.sub(cb.out_i0, cb.out_j0, cb.n, cb.m)
+                    if remote:  # operands over NVLink into local memory, the block back in one copy
+                        a_l, b_l, c_l = _local(a_v, dv, st), _local(b_v, dv, st), _local_empty(d_v, dv, st)
+                        launch_mm(kid, st, View.of(a_l), View.of(b_l), View.of(c_l), overwrite=True, device=dv)
+                        _copy_back(d_v, c_l, dv, st)
+                    else:
+                        launch_mm(kid, st, a_v, b_v, d_v, overwrite=True, device=dv)
                 elif isinstance(task.region, LeafFold):
                     f = task.region
                     A_n, B_n, C_n = ops[id(f.node)]
@@ -541,7 +579,12 @@ def strassen_execute(plan: Plan, A, B, mode: str = "serial_sim", *, devices: lis
                     nd = task.region
                     A_n, B_n, C_n = ops[id(nd)]
                     with torch.cuda.stream(st):
-                        _strassen_dev(A_n, B_n, C_n, base, dtype, st)
+                        if remote:  # the node's operands to this GPU, its product back in one copy
+                            a_l, b_l, c_l = _local(A_n, dv, st), _local(B_n, dv, st), _local_empty(C_n, dv, st)
+                            _strassen_dev(View.of(a_l), View.of(b_l), View.of(c_l), base, dtype, st)
+                            _copy_back(C_n, c_l, dv, st)
+                        else:
+                            _strassen_dev(A_n, B_n, C_n, base, dtype, st)
                 else:
                     what, name = task.region.split("[", 1)
                     nd = by_name[name[:-1]]

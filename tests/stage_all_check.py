@@ -30,4 +30,18 @@ for sem in (M.SEMIRING_F32, M.SEMIRING_F32_SIMT):
     C = np.zeros((n, m), np.float32)
     M.mm_execute(M.mm_paco_partition(n, m, k, 5, base=32), Af, Bf, C, sem, mode="parallel", batch=False)
     assert np.linalg.norm(C - ref) <= 1e-5 * np.linalg.norm(ref), sem.name
+# Strassen plans: whole nodes and split-leaf pieces computed in "remote" local memory
+from paper_2011_01441_b200 import strassen as S
+ns = 256
+Ai = rng.integers(-30, 30, (ns, ns)).astype(np.int64)
+Bi = rng.integers(-30, 30, (ns, ns)).astype(np.int64)
+for plan in (S.strassen_paco_partition(ns, 5, base=32, split_leftover=True),
+             S.strassen_const_pieces_partition(ns, 6, S.SuperRoundCfg(2), base=32)):
+    for mode in ("serial_sim", "parallel"):
+        assert np.array_equal(S.strassen_execute(plan, Ai, Bi, mode), Ai @ Bi), (plan.meta["variant"], mode)
+Af2 = rng.uniform(-1, 1, (ns, ns)).astype(np.float32)
+Bf2 = rng.uniform(-1, 1, (ns, ns)).astype(np.float32)
+Cf2 = S.strassen_execute(S.strassen_paco_partition(ns, 8, base=32, split_leftover=True), Af2, Bf2, "parallel")
+ref2 = Af2.astype(np.float64) @ Bf2.astype(np.float64)
+assert np.linalg.norm(Cf2 - ref2) <= 1e-4 * np.linalg.norm(ref2)
 print("stage-all ok")
