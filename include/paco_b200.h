@@ -194,7 +194,7 @@ int paco_ipc_close(int device, void* ptr);
 int paco_enable_peer(int device, int peer);
 
 /* ALU issue-rate probe: runs `which` (0 = VIADDMNMX.U32 min-plus, 1 = VIADDMNMX.S32
- * max-plus, 2 = FFMA, 3 = IMAD.WIDE, 4 = DFMA) on every SM and returns the
+ * max-plus, 2 = FFMA, 3 = DFMA) on every SM and returns the
  * measured terms per clock per SM and the SM clock (MHz) seen during the run. */
 int paco_alu_probe(int device, void* stream, int which, int iters, double* terms_per_clk_sm,
                    double* sm_mhz);

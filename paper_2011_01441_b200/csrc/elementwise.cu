@@ -216,14 +216,23 @@ __global__ void __launch_bounds__(256, 2) alu_probe_kernel(uint32_t* sink, long 
   __syncthreads();
   long long t0 = clock64(), g0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  double dacc[V == 3 ? N : 1];
+#pragma unroll
+  for (int i = 0; i < (V == 3 ? N : 1); ++i) dacc[i] = double(acc[i]) * 1e-9;
+  const double dy = 1.0 + 1e-12 * double(y);
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       if (V == 0) acc[i] = min(acc[i], x[i] + y);
       if (V == 1) acc[i] = uint32_t(max(int(acc[i]), int(x[i] + y)));
       if (V == 2) acc[i] = __float_as_uint(fmaf(__uint_as_float(x[i]), __uint_as_float(y), __uint_as_float(acc[i])));
+      if (V == 3) dacc[i] = fma(dacc[i], dy, 1e-7);
     }
     y += 0x9e3779b9u;
+  }
+  if (V == 3) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] ^= uint32_t(__double_as_longlong(dacc[i]));
   }
   long long t1 = clock64(), g1;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
@@ -238,8 +247,8 @@ __global__ void __launch_bounds__(256, 2) alu_probe_kernel(uint32_t* sink, long 
 }
 
 int run_alu_probe(cudaStream_t st, int which, int iters, double* tpc, double* mhz) {
-  if (which < 0 || which > 2) {
-    set_error("paco_alu_probe: which=%d not in 0..2", which);
+  if (which < 0 || which > 3) {
+    set_error("paco_alu_probe: which=%d not in 0..3", which);
     return PACO_ERR_ARG;
   }
   const int blocks = kNumSMs * 2, threads = 256;
@@ -251,6 +260,7 @@ int run_alu_probe(cudaStream_t st, int which, int iters, double* tpc, double* mh
   if (which == 0) alu_probe_kernel<0><<<blocks, threads, 0, st>>>(sink, cyc, ns, iters, 7);
   if (which == 1) alu_probe_kernel<1><<<blocks, threads, 0, st>>>(sink, cyc, ns, iters, 7);
   if (which == 2) alu_probe_kernel<2><<<blocks, threads, 0, st>>>(sink, cyc, ns, iters, 7);
+  if (which == 3) alu_probe_kernel<3><<<blocks, threads, 0, st>>>(sink, cyc, ns, iters, 7);
   PACO_CUDA_TRY(cudaGetLastError());
   long long hc[kNumSMs * 2], hn[kNumSMs * 2];
   PACO_CUDA_TRY(cudaMemcpyAsync(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost, st));

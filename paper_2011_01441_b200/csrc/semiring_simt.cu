@@ -35,6 +35,9 @@ namespace paco {
 
 // 8192^3 (min,+) with 1/2/3/4/5/8 waves of 296: 37.5/35.2/34.6/34.3/35.1/35.6 ms
 constexpr int kDefaultWaves = 4;
+#ifndef PACO_SIMT_WIDE_TILE
+#define PACO_SIMT_WIDE_TILE 128
+#endif
 #ifndef PACO_SIMT_MBAR
 #define PACO_SIMT_MBAR 1
 #endif
@@ -55,8 +58,11 @@ long long* g_trace_buffer = nullptr;
 template <class Op>
 struct SimtCfg {
   static constexpr bool kWide = sizeof(typename Op::Acc) == 8;
-  static constexpr int BM = kWide ? 64 : 128;
-  static constexpr int BN = kWide ? 64 : 128 * PACO_SIMT_NSPAN;
+  // 64-bit accumulators: 128x128 tiles too (8x8 per thread = 128 registers of
+  // accumulators, one CTA per SM) -- 64x64 tiles left DFMA at 38 % of its issue
+  // rate (smem-bound: 2 loaded values per term pair)
+  static constexpr int BM = kWide ? PACO_SIMT_WIDE_TILE : 128;
+  static constexpr int BN = kWide ? PACO_SIMT_WIDE_TILE : 128 * PACO_SIMT_NSPAN;
   static constexpr int BK = kWide ? 16 : 32;
   static constexpr int GM = BM / 64;  // 4-row groups per thread along m
   static constexpr int GN = BN / 64;
@@ -64,7 +70,7 @@ struct SimtCfg {
   static constexpr int TN = 4 * GN;
   static constexpr int THREADS = 256;
   static constexpr int STAGES = kWide ? 4 : (PACO_SIMT_NSPAN > 1 ? 4 : 3);
-  static constexpr int MIN_BLOCKS = (!kWide && PACO_SIMT_NSPAN > 1) ? 1 : 2;
+  static constexpr int MIN_BLOCKS = (!kWide && PACO_SIMT_NSPAN > 1) || (kWide && BM > 64) ? 1 : 2;
   static constexpr int VA = 16 / sizeof(typename Op::TA);  // elements per 16 B chunk
   static constexpr int VB = 16 / sizeof(typename Op::TB);
   static constexpr int KQ = VA;          // k quantum of piece boundaries
