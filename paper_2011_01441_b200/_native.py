@@ -159,16 +159,23 @@ def cta_grid(sr: int, n: int, m: int, k: int) -> tuple[int, int]:
     return s.value, ctas.value
 
 
+GRID_BAND = 8  # cta_plan.cuh kGridBand
+
+
 def grid_pieces(sr: int, n: int, m: int, k: int) -> list[tuple[int, ...]]:
-    """The default tile-grid plan as (ti0, tj0, tl0, tn, tm, tk) rows, CTA order."""
+    """The default tile-grid plan as (ti0, tj0, tl0, tn, tm, tk) rows, CTA order
+    (C tiles in row-block bands of GRID_BAND, column by column inside a band)."""
     bm, bn, kq, _ = tile_shape(sr)
     s, ctas = cta_grid(sr, n, m, k)
-    tm_, ku = -(-m // bn), -(-k // kq)
+    tn_, tm_, ku = -(-n // bm), -(-m // bn), -(-k // kq)
     out = []
     for idx in range(ctas):
         tile, part = divmod(idx, s)
+        r0 = (tile // (GRID_BAND * tm_)) * GRID_BAND
+        rows = min(GRID_BAND, tn_ - r0)
+        v = tile - r0 * tm_
         l0 = part * ku // s
-        out.append((tile // tm_, tile % tm_, l0, 1, 1, (part + 1) * ku // s - l0))
+        out.append((r0 + v % rows, v // rows, l0, 1, 1, (part + 1) * ku // s - l0))
     return out
 
 

@@ -96,13 +96,20 @@ __host__ __device__ inline bool plan_piece(int64_t n, int64_t m, int64_t k, int 
 }
 
 // Tile-grid plan: piece idx = (C tile idx / s, k part idx % s); the k units
-// split as evenly as possible.
+// split as evenly as possible.  C tiles are numbered in row-block bands of
+// kGridBand (inside a band column by column), so the tiles in flight share a
+// few A row blocks and B column blocks in L2.
+constexpr int64_t kGridBand = 8;
+
 __host__ __device__ inline void plan_grid_piece(int64_t n, int64_t m, int64_t k, int bm, int bn, int kq,
                                                 int s, int idx, UnitBox& out) {
   const UnitBox r = plan_root(n, m, k, bm, bn, kq);
   const int64_t tile = idx / s, part = idx % s;
-  out.o[0] = tile / r.e[1];
-  out.o[1] = tile % r.e[1];
+  const int64_t band = tile / (kGridBand * r.e[1]), r0 = band * kGridBand;
+  const int64_t rows = r.e[0] - r0 < kGridBand ? r.e[0] - r0 : kGridBand;
+  const int64_t v = tile - r0 * r.e[1];
+  out.o[0] = r0 + v % rows;
+  out.o[1] = v / rows;
   out.e[0] = out.e[1] = 1;
   out.o[2] = part * r.e[2] / s;
   out.e[2] = (part + 1) * r.e[2] / s - out.o[2];
