@@ -271,12 +271,13 @@ class FusedDistributedMM:
         self.views = [View.raw(p, self.n, self.m, self.itemsize, device) for p in self.ptrs]
         owners, self.launches = fused_launches(plan, self.rank)
         self.owned = [rect for rect, w in owners if w == self.rank]
-        # remote folds: "stage" = compute into a local temporary, one bulk copy
-        # into a staging slot in the owner's memory (IPC), the owner folds it
-        # after a barrier; "atomic" = the epilogue folds straight into the
-        # owner's C over NVLink (element atomics, or TMA bulk reductions with
-        # PACO_REMOTE_BULK=1).
-        self.fold_style = fold_style or os.environ.get("PACO_FOLD_STYLE", "stage")
+        # remote folds: "atomic" (default) = the kernel's epilogue folds each
+        # finished tile straight into the owner's C over NVLink (element atomics,
+        # or TMA bulk reductions with PACO_REMOTE_BULK=1) -- compute and transfer
+        # overlap tile by tile, ~1/p of C spread over the whole kernel; "stage" =
+        # compute into a local temporary, one bulk copy into a staging slot in the
+        # owner's memory (IPC), the owner folds it after a barrier.
+        self.fold_style = fold_style or os.environ.get("PACO_FOLD_STYLE", "atomic")
         if self.fold_style not in ("stage", "atomic"):
             raise ValueError(f"fold_style must be 'stage' or 'atomic', got {self.fold_style!r}")
         self.remote_bulk = self._probe_remote_bulk() if self.fold_style == "atomic" else False

@@ -354,7 +354,9 @@ def fold_destinations(plan: Plan) -> dict[int, tuple[int, int, int]]:
 
 
 _TC_KERNELS = (nat.SR_BF16_F32, nat.SR_F32_TC)
-_STAGE_ALL = os.environ.get("PACO_MM_STAGE_ALL") == "1"  # test hook: every worker takes the remote path
+# test hook: every worker takes the remote-GPU path, "fused" (epilogue folds over
+# NVLink) or "stage" (local block, one copy, staged atomic fold)
+_REMOTE_ALL = os.environ.get("PACO_MM_REMOTE_ALL", "")
 
 
 def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str = "serial_sim",
@@ -460,11 +462,18 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
                     batched.append((task.id, (av.ptr, av.ld, bv.ptr, bv.ld, out.ptr, out.ld, cb.n, cb.m, cb.k,
                                               flags)))
                     return
-                if dv != home or _STAGE_ALL:
-                    # a worker on another GPU computes its block locally (plain epilogue),
-                    # ships it over NVLink in one copy into a staging buffer on the home
-                    # GPU, and the block is folded into its destination there with
-                    # per-element atomics (a k-cut partner may fold into the same block)
+                remote = dv != home or bool(_REMOTE_ALL)
+                staged = remote and (kid in _TC_KERNELS or _REMOTE_ALL == "stage")
+                if remote and not staged:
+                    # fused over NVLink: the kernel on the worker's GPU folds each finished
+                    # tile into C on the home GPU with the semiring's (+) as per-element
+                    # atomics (PACO_MM_REMOTE) -- the transfer overlaps the math tile by
+                    # tile, no second pass (a k-cut partner may fold into the same block)
+                    launch_mm(kid, st, av, bv, out, flags=nat.MM_ATOMIC | nat.MM_REMOTE, device=dv)
+                elif staged:
+                    # the tcgen05 kernels never address peer memory: the block is computed
+                    # locally, shipped in one copy into a staging buffer on the home GPU
+                    # and folded into its destination there with per-element atomics
                     with torch.cuda.device(dv):
                         loc = torch.empty((cb.n, cb.m), dtype=tdt, device=dv)
                         loc.record_stream(st)

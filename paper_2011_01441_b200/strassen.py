@@ -404,7 +404,7 @@ def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stre
     _combine(ws, C, dt, stream)
 
 
-_STAGE_ALL = __import__("os").environ.get("PACO_MM_STAGE_ALL") == "1"  # test hook (see mm.py)
+_STAGE_ALL = bool(__import__("os").environ.get("PACO_MM_REMOTE_ALL"))  # test hook (see mm.py)
 
 
 def _dtype_of_view(v: View) -> torch.dtype:

@@ -1,6 +1,6 @@
 """Helper of tests/test_gpu_mm.py::test_remote_worker_staging (run with
-PACO_MM_STAGE_ALL=1): every plan worker takes mm_execute's remote-GPU path
-(local block, one copy, staged atomic fold) on the single test GPU."""
+PACO_MM_REMOTE_ALL=fused|stage): every plan worker takes mm_execute's remote-GPU
+path on the single test GPU."""
 import os
 import sys
 

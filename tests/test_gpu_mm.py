@@ -472,14 +472,16 @@ def test_plan_as_one_batched_launch(fused):
     assert np.array_equal(C, Ai.astype(np.int64) @ Bi.astype(np.int64))
 
 
-def test_remote_worker_staging():
-    """mm_execute's path for workers on another GPU (local block -> one copy ->
-    staged atomic fold / direct copy), forced on for every worker of the single
-    test GPU (PACO_MM_STAGE_ALL=1, a fresh process: the hook is read at import)."""
+@pytest.mark.parametrize("style", ["fused", "stage"])
+def test_remote_worker_paths(style):
+    """mm_execute's paths for workers on another GPU -- fused (the epilogue folds
+    into the home C with atomics) and staged (local block -> one copy -> atomic
+    fold) -- forced on for every worker of the single test GPU
+    (PACO_MM_REMOTE_ALL, a fresh process: the hook is read at import)."""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, os.path.join(here, "stage_all_check.py")], capture_output=True, text=True,
-                       env=dict(os.environ, PACO_MM_STAGE_ALL="1"), timeout=600)
+                       env=dict(os.environ, PACO_MM_REMOTE_ALL=style), timeout=600)
     assert r.returncode == 0 and "stage-all ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
