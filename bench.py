@@ -4,11 +4,11 @@
 
 One step = one full C (+)= A (x) B over the 8192^3 iteration cuboid, inputs
 resident in HBM: the GPU-level PACO plan (mm_one_piece_partition over N ranks,
-matmul.py:250-300) gives each rank one cuboid; inside each rank the CTA-level
-plan (MM-1-Piece over the tile grid, 148 SMs x 2 CTAs) drives one persistent
-sm_100a launch; k-cut folds (N >= 5) are fused into the kernels (upper-k ranks
-fold straight into the owner's C over CUDA IPC / NVLink; --fold nccl uses NCCL
-MIN reductions instead).  The timed region
+matmul.py:250-300) gives each rank one cuboid; inside each rank one sm_100a
+launch covers it with the tile-grid CTA plan (one CTA per 128x128 C tile, k split
+by the cost model); k-cut folds (N >= 5) are fused into the kernels (upper-k
+ranks fold straight into the owner's C over CUDA IPC / NVLink; --fold nccl uses
+NCCL MIN reductions instead).  The timed region
 is bracketed by barrier + synchronize, timed with CUDA events and max'ed over
 ranks.  A, B (256 MiB each) exceed the 126 MB L2, so no flush is needed.
 

@@ -1,4 +1,5 @@
-// CTA-level PACO plan shared by host and device.
+// CTA-level plans shared by host and device: the PACO cuboid plan
+// (plan_piece, PACO_MM_PACO_PLAN) and the default tile grid (plan_grid_piece).
 //
 // The recursion is mm_one_piece_partition's (matmul.py:250-300): the worker
 // list [lo, hi) splits floor(cnt/2) : ceil(cnt/2); the cut axis is the longest

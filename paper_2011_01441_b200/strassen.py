@@ -4,7 +4,7 @@ Follows SPEC.md:474-552 and the identities of PAPER.md:1839-1852:
 
 * ``strassen_seq(A, B, n, base=64)`` -- C = A x B with Strassen's 7-way
   recursion down to ``base`` (B_str), then classic semiring MM leaves
-  (``mm_seq`` -> the sm_100a kernels with the CTA-level PACO plan).  S_r/T_r
+  (``mm_seq`` -> the sm_100a kernels; fp32 leaves as batched 3xTF32).  S_r/T_r
   formation and the C-block combination are ``paco_lincomb`` launches.
   Non-power-of-two n is zero-padded.
 * ``strassen_paco_partition(n, p, base)`` -- pruned BFS of the arity-7 tree
