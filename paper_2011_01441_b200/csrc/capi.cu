@@ -61,10 +61,12 @@ int check_sr(int sr) {
   return PACO_OK;
 }
 
+// Always cudaSetDevice: besides selecting the device it makes the primary
+// context current on this thread, which the driver-API calls we make
+// (cuTensorMapEncodeTiled) need -- a fresh worker thread whose device is
+// already 0 otherwise has no current context (CUDA_ERROR_INVALID_CONTEXT).
 int use_device(int device) {
-  int cur = -1;
-  PACO_CUDA_TRY(cudaGetDevice(&cur));
-  if (cur != device) PACO_CUDA_TRY(cudaSetDevice(device));
+  PACO_CUDA_TRY(cudaSetDevice(device));
   return PACO_OK;
 }
 

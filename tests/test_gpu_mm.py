@@ -485,3 +485,31 @@ def test_remote_worker_paths(style):
     r = subprocess.run([sys.executable, os.path.join(here, "stage_all_check.py")], capture_output=True, text=True,
                        env=dict(os.environ, PACO_MM_REMOTE_ALL=style), timeout=600)
     assert r.returncode == 0 and "stage-all ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_tensor_core_call_from_fresh_thread():
+    """The first CUDA call of a new host thread may be a tcgen05 paco_mm (its
+    tensor maps use the driver API, which needs the primary context current on
+    that thread -- use_device() makes it so)."""
+    import threading
+    a = torch.randn(300, 200, device="cuda").to(torch.bfloat16)
+    b = torch.randn(200, 260, device="cuda").to(torch.bfloat16)
+    c = torch.zeros(300, 260, device="cuda")
+    torch.cuda.synchronize()
+    errs = []
+
+    def work():
+        try:
+            nat.check(nat.load().paco_mm(0, None, nat.SR_BF16_F32, a.data_ptr(), a.stride(0), b.data_ptr(),
+                                         b.stride(0), c.data_ptr(), c.stride(0), 300, 260, 200, None, 0,
+                                         nat.MM_OVERWRITE))
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    t = threading.Thread(target=work)
+    t.start()
+    t.join()
+    torch.cuda.synchronize()
+    assert not errs, errs
+    ref = a.double() @ b.double()
+    assert float((c.double() - ref).norm() / ref.norm()) < 1e-5
