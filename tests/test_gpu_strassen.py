@@ -139,3 +139,18 @@ def test_tf32_split_fused_sum_and_presplit_mm(transpose):
     for q, C in enumerate(Cs):
         got = C.double() - (1.0 if q == 1 else 0.0)
         assert float((got - ref).norm() / ref.norm()) < 1e-5, q
+
+
+@pytest.mark.parametrize("n,base", [(1000, 128), (777, 200), (33, 8)])
+def test_f32_non_power_of_two(n, base):
+    """fp32 Strassen on a zero-padded non-power-of-two n (3xTF32 leaves, fused
+    leaf-level splits where the sizes allow), seq and a split-leftover plan."""
+    rng = np.random.default_rng(n)
+    A = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    B = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    C = S.strassen_seq(A, B, n, base=base)
+    assert C.shape == (n, n)
+    assert np.linalg.norm(C - ref) <= 1e-4 * np.linalg.norm(ref)
+    C2 = S.strassen_execute(S.strassen_paco_partition(n, 6, base=base, split_leftover=True), A, B, "parallel")
+    assert np.linalg.norm(C2 - ref) <= 1e-4 * np.linalg.norm(ref)
