@@ -434,3 +434,207 @@ class FusedDistributedMM:
             lib.paco_device_free(self.device, self.stage_ptr)
         lib.paco_device_free(self.device, self.own_ptr)
         self.ptrs, self.stage_ptrs, self.stage_ptr = [], [None] * self.world, None
+
+
+# ------------------------------------------------------------------ Strassen
+
+class CudaStrassenOps:
+    """Device arithmetic for ``DistributedStrassen`` (sm_100a kernels)."""
+
+    def __init__(self, dtype: torch.dtype, stream: torch.cuda.Stream | None = None):
+        from . import strassen as S
+
+        self.S = S
+        self.dtype = dtype
+        self.kid, self.dt = S._RING[dtype]
+        self.stream = stream
+
+    def _st(self, t: torch.Tensor):
+        return self.stream or torch.cuda.current_stream(t.device)
+
+    def zeros(self, shape, like: torch.Tensor) -> torch.Tensor:
+        return torch.zeros(shape, dtype=like.dtype, device=like.device)
+
+    def lincomb(self, out: torch.Tensor, terms, accumulate: bool) -> None:
+        from .device import View
+
+        self.S._lincomb(self.dt, self._st(out), View.of(out), [(c, View.of(t)) for c, t in terms], accumulate)
+
+    def strassen(self, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, base: int) -> None:
+        from .device import View
+
+        self.S._strassen_dev(View.of(a), View.of(b), View.of(out), base, self.dtype, self._st(out))
+
+    def mm(self, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:
+        from .device import View
+        from .mm import launch_mm
+
+        launch_mm(self.kid, self._st(out), View.of(a), View.of(b), View.of(out), overwrite=True)
+
+
+def strassen_placements(path: tuple[int, ...], size: int) -> list[tuple[int, int, int]]:
+    """Where the product of tree node ``path`` lands in C: (sign, row, col) of
+    each signed copy, the block being ``size >> len(path)`` square.
+
+    Composes the C-block formulas top-down: at each level
+    M_r is added with coefficient c into every quadrant whose formula holds r
+    (M1 -> C00, C11; M2 -> C10, -C11; ...), inside the block its parent landed in.
+    """
+    from .strassen import C_TERMS
+
+    out = [(1, 0, 0)]
+    h = size
+    for r in path:
+        h //= 2
+        nxt = []
+        for s, i, j in out:
+            for q, terms in C_TERMS.items():
+                for c, rr in terms:
+                    if rr == r:
+                        nxt.append((s * c, i + int(q[0]) * h, j + int(q[1]) * h))
+        out = nxt
+    return out
+
+
+class DistributedStrassen:
+    """One process per GPU for a Strassen plan.
+
+    A and B are replicated, so every rank forms the S/T operands of its own
+    tree nodes locally (the path's S_r / T_r formulas applied level by level,
+    shared prefixes formed once) and multiplies them (``strassen_seq`` of the
+    node, 3xTF32 leaves for fp32).  Each product is added, with the signs of
+    the C-block formulas composed along its path (``strassen_placements``),
+    into a rank-local partial C; the pieces of split leftover leaves
+    (``split_leftover``) are added the same way at their cuboid's final place
+    inside the leaf product, so a k-cut pair's fold is part of the sum.  C is
+    then ONE signed-sum reduce-scatter of the partials (NCCL): rank r holds
+    rows [r*R, (r+1)*R) of C; ``gather`` assembles the whole C on one rank.
+    The plan's FORM / COMBINE / REDUCE tasks need no execution of their own
+    here: forming is per rank, combining and folding are the reduce-scatter.
+    """
+
+    def __init__(self, plan: Plan, ops, *, group=None):
+        from .strassen import LeafPiece, StrassenNode
+
+        meta = plan.meta
+        if meta.get("algo") != "strassen":
+            raise PlanError("not a Strassen plan")
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if plan.p != self.world:
+            raise PlanError(f"plan built for p={plan.p}, world size is {self.world}")
+        plan.validate()
+        self.plan, self.ops, self.group = plan, ops, group
+        self.n, self.size, self.base = meta["n"], meta["n_padded"], meta["base"]
+        self.rows = -(-self.size // self.world)   # C rows per rank after the reduce-scatter
+        self.nodes: list = []    # (path, StrassenNode)
+        self.pieces: list = []   # (path, LeafPiece, (row, col) of the piece inside the leaf product)
+        from .mm import fold_destinations
+        dests = {}
+        for t in plan.tasks:
+            if t.kind != COMPUTE or t.worker != self.rank:
+                continue
+            if isinstance(t.region, LeafPiece):
+                leaf = t.region.node
+                mp = meta["split_leaves"][str(leaf)]
+                if str(leaf) not in dests:
+                    dests[str(leaf)] = fold_destinations(mp)
+                cb = t.region.cuboid
+                _, fi, fj = dests[str(leaf)].get(cb.out, (0, 0, 0))
+                self.pieces.append((leaf.path, t.region, (fi + cb.out_i0, fj + cb.out_j0)))
+            elif isinstance(t.region, StrassenNode):
+                self.nodes.append((t.region.path, t.region))
+
+    def _operands(self, A: torch.Tensor, B: torch.Tensor, path: tuple[int, ...], cache: dict):
+        """S and T of tree node ``path``: the S_r / T_r formulas applied level by level."""
+        from .strassen import S_TERMS, T_TERMS
+
+        if path in cache:
+            return cache[path]
+        if not path:
+            return A, B
+        pa, pb = self._operands(A, B, path[:-1], cache)
+        r = path[-1]
+        h = pa.shape[0] // 2
+
+        def quad(x, q):
+            return x[int(q[0]) * h:(int(q[0]) + 1) * h, int(q[1]) * h:(int(q[1]) + 1) * h]
+
+        res = []
+        for src, terms in ((pa, S_TERMS[r]), (pb, T_TERMS[r])):
+            if len(terms) == 1 and terms[0][0] == 1:
+                res.append(quad(src, terms[0][1]))
+                continue
+            out = self.ops.zeros((h, h), src)
+            self.ops.lincomb(out, [(c, quad(src, q)) for c, q in terms], False)
+            res.append(out)
+        cache[path] = tuple(res)
+        return cache[path]
+
+    def partial(self, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+        """This rank's signed partial C (rows padded to world * rows)."""
+        N = self.size
+        if tuple(A.shape) != (N, N) or tuple(B.shape) != (N, N):
+            raise ValueError(f"operands must be padded to {N}x{N}, got A{tuple(A.shape)} B{tuple(B.shape)}")
+        Cp = self.ops.zeros((self.rows * self.world, N), A)
+        cache: dict = {}
+        for path, nd in self.nodes:
+            s, t = self._operands(A, B, path, cache)
+            h = nd.size
+            M = self.ops.zeros((h, h), A)
+            self.ops.strassen(s, t, M, self.base)
+            for sign, i, j in strassen_placements(path, N):
+                self.ops.lincomb(Cp[i:i + h, j:j + h], [(sign, M)], True)
+        for path, piece, (ri, rj) in self.pieces:
+            s, t = self._operands(A, B, path, cache)
+            cb = piece.cuboid
+            P = self.ops.zeros((cb.n, cb.m), A)
+            self.ops.mm(s[cb.i0:cb.i0 + cb.n, cb.l0:cb.l0 + cb.k], t[cb.l0:cb.l0 + cb.k, cb.j0:cb.j0 + cb.m], P)
+            for sign, i, j in strassen_placements(path, N):
+                self.ops.lincomb(Cp[i + ri:i + ri + cb.n, j + rj:j + rj + cb.m], [(sign, P)], True)
+        return Cp
+
+    def run(self, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+        """Rows [rank*rows, (rank+1)*rows) of C = A x B (padded size; rows past
+        the padded size are zero)."""
+        Cp = self.partial(A, B)
+        slab = self.ops.zeros((self.rows, self.size), A)
+        _reduce_scatter_sum(slab, Cp, self.group)
+        return slab
+
+    def gather(self, slab: torch.Tensor, dst: int = 0) -> torch.Tensor | None:
+        """The whole n x n C on ``dst`` (None elsewhere)."""
+        full = self.ops.zeros((self.rows * self.world, self.size), slab)
+        _all_gather(full, slab, self.group)
+        return full[:self.n, :self.n] if self.rank == dst else None
+
+
+def _gloo(group) -> bool:
+    return dist.get_backend(group) == "gloo"
+
+
+def _reduce_scatter_sum(out: torch.Tensor, inp: torch.Tensor, group) -> None:
+    """out = rank's row slab of the SUM of every rank's ``inp`` (NCCL
+    reduce-scatter; gloo, which has none, does all-reduce + slice on host copies)."""
+    if dist.get_world_size(group) == 1:
+        out.copy_(inp)
+        return
+    if not _gloo(group):
+        dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=group)
+        return
+    h = inp.cpu()
+    dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+    r, rows = dist.get_rank(group), out.shape[0]
+    out.copy_(h[r * rows:(r + 1) * rows])
+
+
+def _all_gather(out: torch.Tensor, inp: torch.Tensor, group) -> None:
+    if dist.get_world_size(group) == 1:
+        out.copy_(inp)
+        return
+    if not _gloo(group):
+        dist.all_gather_into_tensor(out, inp, group=group)
+        return
+    parts = [torch.empty_like(inp, device="cpu") for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, inp.cpu(), group=group)
+    out.copy_(torch.cat(parts))

@@ -426,11 +426,14 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
             if d != home:
                 torch.cuda.current_stream(d).wait_event(staged)
 
-        streams = [torch.cuda.Stream(device=dev_of[w]) for w in range(plan.p)]
-        for s in streams:
-            s.wait_event(staged)
-        fold_stream = torch.cuda.Stream(device=home)   # staged remote blocks fold here
-        fold_stream.wait_event(staged)
+        if batch:  # one launch on the staging stream: no worker streams to fork and join
+            streams, fold_stream = [stage] * plan.p, stage
+        else:
+            streams = [torch.cuda.Stream(device=dev_of[w]) for w in range(plan.p)]
+            for s in streams:
+                s.wait_event(staged)
+            fold_stream = torch.cuda.Stream(device=home)   # staged remote blocks fold here
+            fold_stream.wait_event(staged)
         tdt = torch_dtype(semiring.dtype)
         events: list[torch.cuda.Event | None] = [None] * len(plan.tasks)
         reduces = meta["reduces"]
@@ -499,18 +502,20 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
                     return
                 launch_fold(semiring.kernel_id, st, buffer(tgt).sub(oi, oj, rn, rm),
                             temps[bid], reset=True)
-            ev = torch.cuda.Event()
-            ev.record(st)
-            events[task.id] = ev
+            if not batch:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                events[task.id] = ev
 
         report = execute_plan(plan, runner, mode)
         if batch:  # the whole plan on one device: one launch, then the folds in plan order
             nat.mm_batch(home, stage.cuda_stream, kid, [p for _, p in sorted(batched)])
             for _, dst, src in sorted(deferred, key=lambda x: x[0]):
                 launch_fold(semiring.kernel_id, stage, dst, src, reset=True)
-        for s in streams:
-            stage.wait_stream(s)
-        stage.wait_stream(fold_stream)
+        if not batch:
+            for s in streams:
+                stage.wait_stream(s)
+            stage.wait_stream(fold_stream)
         t_end = torch.cuda.Event(enable_timing=True)
         t_end.record(stage)
         out.finish()

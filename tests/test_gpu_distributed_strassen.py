@@ -1,0 +1,78 @@
+"""DistributedStrassen on the GPU: ranks as processes sharing the test box's one
+GPU (no kernel waits on another rank), gloo for the reduce-scatter of the
+signed partial C.  fp32 (3xTF32 leaves, 1e-4 relative Frobenius, the cfg5
+tolerance) and the exact int64 ring, plain / split-leftover / const-pieces plans.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, cases, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2011_01441_b200 import strassen as S
+    from paper_2011_01441_b200.distributed import CudaStrassenOps, DistributedStrassen
+    try:
+        for n, base, variant, ring, seed in cases:
+            rng = np.random.default_rng(seed)
+            if ring == "f32":
+                A = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+                B = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+                dt = torch.float32
+            else:
+                A = rng.integers(-1000, 1000, (n, n)).astype(np.int64)
+                B = rng.integers(-1000, 1000, (n, n)).astype(np.int64)
+                dt = torch.int64
+            if variant == "const":
+                plan = S.strassen_const_pieces_partition(n, world, S.SuperRoundCfg(1), base=base)
+            else:
+                plan = S.strassen_paco_partition(n, world, base=base, split_leftover=variant == "split")
+            size = plan.meta["n_padded"]
+            a = torch.zeros((size, size), dtype=dt, device="cuda")
+            b = torch.zeros((size, size), dtype=dt, device="cuda")
+            a[:n, :n] = torch.from_numpy(A)
+            b[:n, :n] = torch.from_numpy(B)
+            ds = DistributedStrassen(plan, CudaStrassenOps(dt))
+            C = ds.gather(ds.run(a, b))
+            if rank == 0:
+                C = C.cpu().numpy()
+                if ring == "f32":
+                    ref = A.astype(np.float64) @ B.astype(np.float64)
+                    ok = float(np.linalg.norm(C - ref) / np.linalg.norm(ref)) <= 1e-4
+                else:
+                    ok = bool(np.array_equal(C, A @ B))
+                q.put(((n, base, variant, ring), ok, len(ds.pieces)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_strassen_gpu(world):
+    cases = [(512, 64, "split", "f32", 1), (1000, 128, "paco", "f32", 2), (256, 32, "split", "i64", 3),
+             (384, 32, "const", "i64", 4)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    res = [q.get(timeout=5) for _ in cases]
+    assert all(r[1] for r in res), res
