@@ -37,6 +37,15 @@
 
 namespace paco {
 
+#ifndef PACO_RES_AST
+#define PACO_RES_AST 5
+#define PACO_RES_EB 1
+#define PACO_RES_EC 16
+#endif
+#ifndef PACO_EPI_RING
+#define PACO_EPI_RING 1
+#endif
+
 namespace tc {
 
 #define PACO_TC_ARGS(...) __VA_ARGS__
@@ -59,7 +68,12 @@ struct KindBF16T {
 };
 // streaming default: 4 stages of 48 KB + 8 warps x 2 x 2 KB staging (16-column
 // boxes) -- 8192^3 bf16 1000 -> 936 us vs 3 stages / 32-column boxes
-using KindBF16 = KindBF16T<4, 2, 8, 16>;
+#ifndef PACO_BF16_ST
+#define PACO_BF16_ST 4
+#define PACO_BF16_EB 2
+#define PACO_BF16_EC 16
+#endif
+using KindBF16 = KindBF16T<PACO_BF16_ST, PACO_BF16_EB, 8, PACO_BF16_EC>;
 // fp32 inputs as 3xTF32 (hi/lo operand tiles), N=128 tiles, 32-deep k blocks.
 // BK_ = 32: 128-byte K-major rows (SWIZZLE_128B); BK_ = 16: 64-byte rows
 // (SWIZZLE_64B) -- half the bytes per stage, so twice the stages in the ring.
@@ -508,6 +522,8 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
     const int c_lo = (ew / 4) * PER;
     unsigned char* stage0 = smem + L::SMEM_EPI + ew * K::EPI_BUFS * L::EPI_BUF;
     int tile = 0;
+    uint32_t box = 0;  // boxes staged by this warp (PACO_EPI_RING buffer index)
+    (void)box;
     for (int64_t i = 0;; ++i, ++tile) {
       const int qs = int(i % QD);
       mbar_wait(&qfull[qs], uint32_t(i / QD) & 1);
@@ -546,8 +562,42 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
         }
         const int col0 = nb * BN + 32 * c;
         if (col0 >= args.m) continue;  // warp-uniform: nothing left to store
-        // 64 columns in SUBS boxes of EPI_COLS; buffer h % EPI_BUFS
+        // 64 columns in SUBS boxes of EPI_COLS
         constexpr int EC = K::EPI_COLS, SUBS = 64 / EC, EB = K::EPI_BUFS;
+#if PACO_EPI_RING
+        // ring of EB staging buffers per warp, one bulk group per box: before
+        // box b reuses buffer b % EB, wait until at most EB-1 younger groups are
+        // still reading shared memory (box b-EB has been read), so EB-1 stores
+        // stay in flight while the next box is staged
+#pragma unroll
+        for (int h = 0; h < SUBS; ++h) {
+          if (col0 + EC * h >= args.m) break;
+          unsigned char* buf = stage0 + (box % EB) * L::EPI_BUF;
+          ++box;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(EB - 1) : "memory");
+          __syncwarp();
+          if (!(args.ablate & 4)) {
+#pragma unroll
+            for (int j = 0; j < EC / 4; ++j) {
+              const uint4 w = make_uint4(v[EC * h + 4 * j], v[EC * h + 4 * j + 1], v[EC * h + 4 * j + 2],
+                                         v[EC * h + 4 * j + 3]);
+              const int sw = EC == 32 ? (j ^ (lane & 7)) : (j ^ ((lane >> 1) & 3));
+              *reinterpret_cast<uint4*>(buf + lane * (EC * 4) + sw * 16) = w;
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          }
+          __syncwarp();
+          if (lane == 0) {
+            if (row0 < args.n && !(args.ablate & 1)) {
+              if (args.overwrite)
+                tma_store_2d(&P.c, buf, P.c_col0 + col0 + EC * h, row0);
+              else
+                tma_reduce_add_2d(&P.c, buf, P.c_col0 + col0 + EC * h, row0);
+            }
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          }
+        }
+#else
         // groups of EB boxes: wait for the buffers, stage EB boxes, ONE proxy
         // fence, EB TMA stores (or reduce-adds), one bulk group
 #pragma unroll
@@ -588,6 +638,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
             asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
           }
         }
+#endif
       }
       if (ew == 0 && lane == 0 && i < 15) tc_stamp(args, i, 5);
     }
@@ -1109,7 +1160,7 @@ int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t ld
   // DESIGN.md section 6); PACO_TC_RESV=-1 forces the streaming kind.
   static const int resv = getenv("PACO_TC_RESV") ? atoi(getenv("PACO_TC_RESV")) : 7;
 #define PACO_TC_GO(KIND) return launch_tc<KIND>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags)
-  if (k <= 256 && resv >= 0) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<5, 1, 8, 16>));
+  if (k <= 256 && resv >= 0) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<PACO_RES_AST, PACO_RES_EB, 8, PACO_RES_EC>));
 #undef PACO_TC_GO
   return launch_tc<tc::KindBF16>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
 }
