@@ -30,7 +30,9 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <atomic>
 #include <vector>
 
 #include "common.cuh"
@@ -253,7 +255,8 @@ struct TcArgs {
   int32_t kblocks;
   int32_t ablate;    // diagnostics: 1 = no C stores, 2 = no MMAs, 4 = no smem staging, 8 = no A loads
   long long* trace;  // diagnostics (paco_debug_trace): per CTA x 16 tiles x 6 globaltimer stamps
-  int32_t* sched;    // per-group tile counters (zeroed before the launch)
+  int32_t* sched;    // per-group tile counters + a CTA-done counter at [groups]
+                     // (zero at launch; the last CTA to finish zeroes them again)
   int32_t groups;    // CTA c serves group c % groups: column blocks g, g + groups, ...
 };
 
@@ -308,6 +311,18 @@ __device__ __forceinline__ int32_t claim_tile(const TcArgs& a, bool first) {
   const int32_t in_group = int32_t((gridDim.x - g + a.groups - 1) / a.groups);
   const int32_t t = first ? int32_t(blockIdx.x / a.groups) : in_group + atomicAdd(&a.sched[g], 1);
   return tile_of(a, g, t);
+}
+// Split form for the producer: issue the claim now (atomic result in flight),
+// turn it into a tile id only when it is needed (the next publish), so the
+// ~1 us round trip of 148 contending atomics never delays the current tile's
+// TMA loads.
+__device__ __forceinline__ int32_t claim_issue(const TcArgs& a) {
+  return atomicAdd(&a.sched[blockIdx.x % uint32_t(a.groups)], 1);
+}
+__device__ __forceinline__ int32_t claim_resolve(const TcArgs& a, int32_t raw) {
+  const int g = int(blockIdx.x % uint32_t(a.groups));
+  const int32_t in_group = int32_t((gridDim.x - g + a.groups - 1) / a.groups);
+  return tile_of(a, g, in_group + raw);
 }
 
 // One problem: operand maps (hi/lo for 3xTF32), the output map, and the column
@@ -376,6 +391,13 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the set-up above (barriers, TMEM, tensor-map
+  // prefetch) overlaps the previous kernel on the stream; every global access
+  // (operand loads, tile claims, C stores) comes after its grid has completed.
+  // The next launch may start as soon as SMs free up (one CTA per SM: only
+  // SMs whose CTA has exited take one of its CTAs).
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (threadIdx.x == 0) tc_stamp(args, 15, 1);
 
   if (warp == 0) {
@@ -384,16 +406,17 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
       {
         uint32_t it = 0, bloads = 0;
         int loaded_nb = -1;
-        int32_t next = claim_tile(args, true);
+        const int32_t first_id = claim_tile(args, true);
+        int32_t raw = 0;
         for (int64_t i = 0;; ++i) {
-          const int32_t id = next;
+          const int32_t id = i == 0 ? first_id : claim_resolve(args, raw);
           if (i == 0) tc_stamp(args, 15, 3);
           const int qs = int(i % QD);
           mbar_wait(&qempty[qs], (uint32_t(i / QD) & 1) ^ 1);
           qid[qs] = id;
           mbar_arrive(&qfull[qs]);
           if (id < 0) break;
-          next = claim_tile(args, false);  // one tile ahead; only the next publish (release) waits for it
+          raw = claim_issue(args);  // one tile ahead; resolved (waited for) at the next publish
           const int tpp = args.tiles_rb * args.tiles_nb, lid = id % tpp;
           const int nb = lid / args.tiles_rb, rb = lid % args.tiles_rb;
           const TcProb& P = maps.p[id / tpp];
@@ -650,7 +673,17 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   tc_fence_after();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(L::TMEM_COLS));
-  if (threadIdx.x == 0) tc_stamp(args, 15, 2);
+  if (threadIdx.x == 0) {
+    tc_stamp(args, 15, 2);
+    // every claim of this CTA has returned; the last CTA out re-zeroes the
+    // counters for the next launch on this stream (no memset per launch)
+    __threadfence();
+    if (atomicAdd(&args.sched[args.groups], 1) == int32_t(gridDim.x) - 1) {
+      for (int g = 0; g < args.groups; ++g) args.sched[g] = 0;
+      args.sched[args.groups] = 0;
+      __threadfence();
+    }
+  }
 }
 
 }  // namespace tc
@@ -712,6 +745,35 @@ struct Scratch {
     for (void* p : bufs) cudaFreeAsync(p, st);
   }
 };
+
+// Tile-scheduler counters of the tcgen05 launches on one (device, stream):
+// allocated zeroed once; each kernel leaves them zeroed when it finishes, so
+// consecutive launches on a stream need no memset, and launches on different
+// streams (the parallel executors) never share counters.
+// PDL on the tcgen05 launches (PACO_TC_PDL=0 turns it off)
+static const bool kPdl = !getenv("PACO_TC_PDL") || atoi(getenv("PACO_TC_PDL")) != 0;
+
+int stream_counters(int device, cudaStream_t st, int32_t** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, int32_t*> slots;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(device, st);
+  auto it = slots.find(key);
+  if (it == slots.end()) {
+    cudaStreamCaptureStatus cap;
+    PACO_CUDA_TRY(cudaStreamIsCapturing(st, &cap));
+    if (cap != cudaStreamCaptureStatusNone) {  // no synchronous allocation inside a capture
+      *out = nullptr;
+      return PACO_OK;
+    }
+    void* p = nullptr;
+    PACO_CUDA_TRY(cudaMalloc(&p, sizeof(int32_t) * (kNumSMs + 1)));
+    PACO_CUDA_TRY(cudaMemset(p, 0, sizeof(int32_t) * (kNumSMs + 1)));
+    it = slots.emplace(key, static_cast<int32_t*>(p)).first;
+  }
+  *out = it->second;
+  return PACO_OK;
+}
 
 int scratch(int device, Scratch& sc, size_t bytes, cudaStream_t st, void** out) {
   static std::mutex mu;
@@ -1069,15 +1131,35 @@ int run_tc(int device, Scratch& sc, cudaStream_t stream, const tc::TcMaps& maps,
     while (g > 1 && grid % g) --g;
     args.groups = g;
   }
-  {
+  if ((rc = stream_counters(device, stream, &args.sched))) return rc;
+  if (!args.sched) {  // first launch on a capturing stream: stream-ordered counters
     void* counters;
-    if ((rc = scratch(device, sc, sizeof(int32_t) * args.groups, stream, &counters))) return rc;
-    PACO_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(int32_t) * args.groups, stream));
+    if ((rc = scratch(device, sc, sizeof(int32_t) * (kNumSMs + 1), stream, &counters))) return rc;
+    PACO_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(int32_t) * (kNumSMs + 1), stream));
     args.sched = static_cast<int32_t*>(counters);
   }
   auto kern = tc::tc_gemm_kernel<K>;
-  PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
-  kern<<<grid, L::THREADS, L::SMEM_ALLOC, stream>>>(maps, args);
+  {
+    static std::atomic<uint64_t> attr_set{0};  // devices whose attribute is set
+    const uint64_t bit = uint64_t(1) << (device & 63);
+    if (!(attr_set.load() & bit)) {
+      PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
+      attr_set.fetch_or(bit);
+    }
+  }
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(L::THREADS);
+    cfg.dynamicSmemBytes = L::SMEM_ALLOC;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = kPdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PACO_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps, args));
+  }
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;
 }

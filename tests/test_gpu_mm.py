@@ -513,3 +513,42 @@ def test_tensor_core_call_from_fresh_thread():
     assert not errs, errs
     ref = a.double() @ b.double()
     assert float((c.double() - ref).norm() / ref.norm()) < 1e-5
+
+
+@pytest.mark.parametrize("warm", [False, True])
+def test_tensor_core_launches_in_cuda_graph(warm):
+    """tcgen05 launches captured into a CUDA graph (first use of the stream
+    inside the capture, or after eager launches on it) replay correctly, and
+    back-to-back launches on one stream reuse the self-resetting tile counters
+    (different shapes / group counts in a row)."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    shapes = [(1000, 256, 1024), (777, 96, 300), (4096, 512, 2048)]   # (n, k, m): resident and streaming kinds
+    ops = []
+    for n, k, m in shapes:
+        a = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+        b = torch.randn(k, m, device="cuda", generator=g).to(torch.bfloat16)
+        ops.append((a, b, torch.zeros(n, m, device="cuda"), a.double() @ b.double()))
+    st = torch.cuda.Stream()
+
+    def run():
+        for a, b, c, _ in ops:
+            launch_mm(nat.SR_BF16_F32, st, View.of(a), View.of(b), View.of(c), overwrite=True)
+
+    with torch.cuda.stream(st):
+        if warm:
+            for _ in range(3):
+                run()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=st):
+            run()
+        for _ in range(3):
+            for _, _, c, _ in ops:
+                c.zero_()
+            graph.replay()
+            st.synchronize()
+            for _, _, c, ref in ops:
+                assert float((c.double() - ref).norm() / ref.norm()) < 1e-5
+        run()   # eager again on the same stream after the replays
+        st.synchronize()
+    for _, _, c, ref in ops:
+        assert float((c.double() - ref).norm() / ref.norm()) < 1e-5
