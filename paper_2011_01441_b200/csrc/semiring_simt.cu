@@ -290,11 +290,20 @@ __device__ __forceinline__ void epilogue(const MMArgs& a,
   using TC = typename Op::TC;
   TC* Cp = static_cast<TC*>(a.C);
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const bool rmw = !atomic && !a.overwrite;
 #pragma unroll
   for (int i = 0; i < C::TM; ++i) {
     const int64_t gr = row0 + (i / 4) * 64 + ty * 4 + (i % 4);
     if (gr >= a.n) continue;
     TC* crow = Cp + gr * a.ldc;
+    // read-modify-write: issue the row's TN loads before any store, so they
+    // are in flight together (one memory round trip per row, not per element)
+    TC old[C::TN];
+#pragma unroll
+    for (int j = 0; j < C::TN; ++j) {
+      const int64_t gc = col0 + (j / 4) * 64 + tx * 4 + (j % 4);
+      old[j] = (rmw && gc < a.m) ? crow[gc] : TC(0);
+    }
 #pragma unroll
     for (int j = 0; j < C::TN; ++j) {
       const int64_t gc = col0 + (j / 4) * 64 + tx * 4 + (j % 4);
@@ -305,7 +314,7 @@ __device__ __forceinline__ void epilogue(const MMArgs& a,
       else if (a.overwrite)
         crow[gc] = v;
       else
-        crow[gc] = Op::combine(crow[gc], v);
+        crow[gc] = Op::combine(old[j], v);
     }
   }
 }
@@ -374,6 +383,82 @@ __device__ __forceinline__ void epilogue_bulk(const MMArgs& a,
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
     __syncthreads();  // smem free again (next round / the next cp.async stage)
+  }
+}
+
+// Bulk epilogue for 8-byte C elements (64-bit tiles, 128 x 128, 1 KB rows):
+// RPR rows per round are staged in shared memory and each row is folded into
+// C by one cp.reduce.async.bulk (or stored by cp.async.bulk when overwriting)
+// -- coalesced, order-free, no per-element atomics or load round trips.
+// kWhole: the CTA's last tile, when every pipeline stage is free -- the whole
+// stage area holds 64 (32-bit inputs) or 128 (64-bit inputs) rows, 2 or 1
+// rounds; otherwise 16 rows per round in the just-consumed stage (8 in its B
+// part, 8 in its A part).
+template <class Op, bool kWhole>
+__device__ __forceinline__ void epilogue_bulk_wide(const MMArgs& a,
+                                                   typename Op::Acc (&acc)[SimtCfg<Op>::TM][SimtCfg<Op>::TN],
+                                                   int64_t row0, int64_t col0, void* bufA, void* bufB,
+                                                   uint32_t bytes) {
+  using C = SimtCfg<Op>;
+  using TC = typename Op::TC;
+  static_assert(C::BM == 128 && C::BN == 128 && sizeof(TC) == 8, "wide bulk epilogue layout");
+  static_assert(C::B_STAGE * sizeof(typename Op::TB) >= 8 * C::BN * sizeof(TC) &&
+                C::A_STAGE * sizeof(typename Op::TA) >= 8 * C::BN * sizeof(TC), "staging room");
+  constexpr int WHOLE_ROWS = int(C::SMEM / (C::BN * sizeof(TC)));
+  constexpr int RPR = !kWhole ? 16 : (WHOLE_ROWS >= 128 ? 128 : 64);
+  static_assert(!kWhole || WHOLE_ROWS >= 64, "whole-stage staging room");
+  constexpr int ROUNDS = C::BM / RPR;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  TC* Cp = static_cast<TC*>(a.C);
+  auto row_buf = [&](int lr) -> TC* {
+    if constexpr (kWhole) return static_cast<TC*>(bufA) + lr * C::BN;
+    return lr < 8 ? static_cast<TC*>(bufB) + lr * C::BN : static_cast<TC*>(bufA) + (lr - 8) * C::BN;
+  };
+  __syncthreads();  // every warp is done reading the stage buffers
+#pragma unroll
+  for (int h = 0; h < ROUNDS; ++h) {
+#pragma unroll
+    for (int g = 0; g < C::GM; ++g) {
+      const int lr0 = 64 * g + ty * 4 - RPR * h;  // this thread's first row, local to the round
+      if (lr0 >= 0 && lr0 < RPR) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          TC* dst = row_buf(lr0 + r);
+#pragma unroll
+          for (int gn = 0; gn < C::GN; ++gn) {
+            TC v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = Op::finish(acc[4 * g + r][4 * gn + e]);
+            uint4 bits[2];
+            memcpy(bits, v, 32);  // bit copy (TC may be double)
+            reinterpret_cast<uint4*>(dst + gn * 64 + tx * 4)[0] = bits[0];
+            reinterpret_cast<uint4*>(dst + gn * 64 + tx * 4)[1] = bits[1];
+          }
+        }
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll 1
+      for (int q = 0; q < RPR / 8; ++q) {
+        const int lr = warp * (RPR / 8) + q;
+        const int64_t gr = row0 + RPR * h + lr;
+        if (gr < a.n) {
+          const void* src = row_buf(lr);
+          TC* gdst = Cp + gr * a.ldc + col0;
+          if (a.overwrite)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+                         "r"(smem_u32(src)), "r"(bytes) : "memory");
+          else
+            Op::bulk_combine(gdst, smem_u32(src), bytes);
+        }
+      }
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+    __syncthreads();  // smem free again
   }
 }
 
@@ -452,11 +537,17 @@ __device__ __forceinline__ void simt_mm_body(const MMArgs& args, const Piece pc)
       if (cw.kt == KT - 1) {
         const int64_t row0 = int64_t(pc.ti0 + cw.ti) * C::BM, col0 = int64_t(pc.tj0 + cw.tj) * C::BN;
         bool done = false;
-        if constexpr (!C::kWide) {
+        {
           const int64_t cols = (args.m - col0 < C::BN) ? args.m - col0 : C::BN;
           const uint32_t bytes = uint32_t(cols * sizeof(typename Op::TC));
           if (args.bulk_ok && (bytes % 16) == 0) {  // stages the tile in stage s (CTA-wide syncs)
-            epilogue_bulk<Op>(args, acc, row0, col0, As + s * C::A_STAGE, Bs + s * C::B_STAGE, bytes);
+            if constexpr (!C::kWide)
+              epilogue_bulk<Op>(args, acc, row0, col0, As + s * C::A_STAGE, Bs + s * C::B_STAGE, bytes);
+            else if (it == total - 1)  // last tile: no stage is in use any more
+              epilogue_bulk_wide<Op, true>(args, acc, row0, col0, smem_raw, nullptr, bytes);
+            else
+              epilogue_bulk_wide<Op, false>(args, acc, row0, col0, As + s * C::A_STAGE, Bs + s * C::B_STAGE,
+                                            bytes);
             done = true;
           }
         }
@@ -513,11 +604,17 @@ __device__ __forceinline__ void simt_mm_body(const MMArgs& args, const Piece pc)
     if (cw.kt == KT - 1) {
       const int64_t row0 = int64_t(pc.ti0 + cw.ti) * C::BM, col0 = int64_t(pc.tj0 + cw.tj) * C::BN;
       bool done = false;
-      if constexpr (!C::kWide) {
+      {
         const int64_t cols = (args.m - col0 < C::BN) ? args.m - col0 : C::BN;
         const uint32_t bytes = uint32_t(cols * sizeof(typename Op::TC));
         if (args.bulk_ok && (bytes % 16) == 0) {
-          epilogue_bulk<Op>(args, acc, row0, col0, As + s_cur * C::A_STAGE, Bs + s_cur * C::B_STAGE, bytes);
+          if constexpr (!C::kWide)
+            epilogue_bulk<Op>(args, acc, row0, col0, As + s_cur * C::A_STAGE, Bs + s_cur * C::B_STAGE, bytes);
+          else if (it == total - 1)
+            epilogue_bulk_wide<Op, true>(args, acc, row0, col0, smem_raw, nullptr, bytes);
+          else
+            epilogue_bulk_wide<Op, false>(args, acc, row0, col0, As + s_cur * C::A_STAGE,
+                                          Bs + s_cur * C::B_STAGE, bytes);
           done = true;
         }
       }

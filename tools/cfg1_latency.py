@@ -60,7 +60,31 @@ def main():
             e1.synchronize()
             out[f"graph_ms_{name}"] = e0.elapsed_time(e1) / 100
     ks, ctas = nat.cta_grid(nat.SR_INT_I32_I64, 384, 320, 256)
-    out["cta_grid"] = {"ksplit": ks, "ctas": ctas}
+    out["cta_grid"] = {"ksplit": ks, "ctas": ctas, "tile_shape": nat.tile_shape(nat.SR_INT_I32_I64)}
+    bm, bn, kq, _ = nat.tile_shape(nat.SR_INT_I32_I64)
+    ku = -(-256 // kq)
+    tiles = [(i, j) for i in range(-(-384 // bm)) for j in range(-(-320 // bn))]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for s in (1, 2, 4, 8, 16, 32):
+            if s > ku:
+                break
+            pieces = [(i, j, p * ku // s, 1, 1, (p + 1) * ku // s - p * ku // s) for i, j in tiles for p in range(s)]
+            fn = lambda: launch_mm(nat.SR_INT_I32_I64, st, av, bv, cv, pieces=pieces)
+            fn()
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=st):
+                for _ in range(50):
+                    fn()
+            graph.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            graph.replay()
+            e1.record(st)
+            e1.synchronize()
+            out[f"graph_ms_ksplit{s}"] = e0.elapsed_time(e1) / 50
     plan = M.mm_paco_partition(384, 320, 256, 3)
     for _ in range(3):
         M.mm_execute(plan, a, b, c, M.SEMIRING_INT)
