@@ -12,8 +12,9 @@ NCCL MIN reductions instead).  The timed region
 is bracketed by barrier + synchronize, timed with CUDA events and max'ed over
 ranks.  A, B (256 MiB each) exceed the 126 MB L2, so no flush is needed.
 
-``e2e`` runs the same metric through the public API (``matmul.mm_seq``) from
-pinned HOST buffers: H2D of A, B and C and D2H of C inside the timed region.
+``e2e`` runs the same metric through the public API (``matmul.mm_seq``; at N>1
+``FusedDistributedMM.run_host``) from pinned HOST buffers: H2D of the operands
+(and C at N=1) and D2H of C inside the timed region.
 
 ``--impl reference`` times the reference's CPU algorithm (the NumPy port in
 oracle/, process-sharded over every host core) on a bounded row sample of the
@@ -299,6 +300,30 @@ def main():
         e2e = {"value": OPS_PER_STEP / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s",
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": 3 * N * N * 4,
                "d2h_bytes_per_step": N * N * 4, "api": "paper_2011_01441_b200.matmul.mm_seq (pinned host numpy-equivalent tensors)"}
+    elif args.fold == "fused":
+        # every rank uploads the A/B blocks its cuboid reads (k-chunked, overlapped with
+        # the folds into the owners' C) and reads its owned C rectangles back
+        C_h = torch.empty((N, N), dtype=torch.int32).pin_memory()
+        ex.run_host(A_h, B_h, C_h)  # warm
+        t_e2e, nbytes = [], (0, 0)
+        for _ in range(args.e2e_steps):
+            barrier()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(st)
+            nbytes = ex.run_host(A_h, B_h, C_h)
+            f1.record(st)
+            f1.synchronize()
+            t = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e.append(float(t.item()))
+        tot = torch.tensor(list(nbytes), device=dev, dtype=torch.float64)
+        dist.all_reduce(tot)
+        e2e_ms = statistics.median(t_e2e)
+        e2e = {"value": OPS_PER_STEP / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item()),
+               "bytes": "summed over ranks; time = max over ranks",
+               "api": "paper_2011_01441_b200.distributed.FusedDistributedMM.run_host (pinned host tensors)"}
 
     if rank == 0:
         peak_max = 2 * tpc * 148 * 1965.0 / 1e6  # Top/s at the 1965 MHz max SM clock

@@ -415,6 +415,82 @@ class FusedDistributedMM:
                 launch_fold(self.semiring.kernel_id, st, mine.sub(ci, cj, cn, cm), src, False)
             torch.cuda.synchronize(self.device)
 
+    def run_host(self, A_h: torch.Tensor, B_h: torch.Tensor, C_h: torch.Tensor) -> tuple[int, int]:
+        """End to end from pinned host operands: C_h's owned rectangles <- C.
+
+        Each rank uploads only the blocks of A and B its launches read, in k
+        chunks of growing width on a copy stream (``mm._kphased_edges``), and
+        folds each chunk into the owners' C as soon as it lands -- the atomic
+        epilogue makes a k-chunked launch the same product, since C starts at
+        the semiring zero.  After the barrier that makes every remote fold
+        visible, the rank's owned rectangles of C are read back into ``C_h``
+        (every rank holds the full-size host C, as every rank holds A_h, B_h
+        in the reference's shared-memory setting).  Returns (H2D, D2H) bytes.
+        """
+        from .device import View
+        from .mm import _copy2d, _kphased_edges, launch_fill, launch_fold, launch_mm
+
+        dev, es = self.device, self.itemsize
+        st = torch.cuda.current_stream(dev)
+        if getattr(self, "_host_bufs", None) is None or self._host_bufs[0].shape != A_h.shape \
+                or self._host_bufs[1].shape != B_h.shape:
+            self._host_bufs = (torch.empty(tuple(A_h.shape), dtype=A_h.dtype, device=dev),
+                               torch.empty(tuple(B_h.shape), dtype=B_h.dtype, device=dev),
+                               torch.cuda.Stream(device=dev))
+        a_d, b_d, h2d = self._host_bufs
+        av, bv = View.of(a_d), View.of(b_d)
+        mine = self.views[self.rank]
+        launch_fill(self.semiring.kernel_id, st, mine)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=self.group)          # every owner's C is initialised
+        h2d.wait_stream(st)
+        sent_a, sent_b, h2d_bytes = set(), set(), 0
+        for j, ((ai, al, an, ak), (bl, bj, bk, bm), owner, (ci, cj, cn, cm)) in enumerate(self.launches):
+            staged = owner != self.rank and self.fold_style == "stage"
+            if staged or ak < 256:
+                spans = [(0, ak)]
+            else:
+                edges, front = _kphased_edges(ak)
+                spans = list(zip(edges[:-1], edges[1:])) + [(front, ak)]
+            for (l0, l1) in spans:
+                ka = (ai, an, al + l0, al + l1)
+                if ka not in sent_a:
+                    sent_a.add(ka)
+                    _copy2d(h2d, a_d, ai, al + l0, A_h, ai, al + l0, an, l1 - l0)
+                    h2d_bytes += an * (l1 - l0) * es
+                kb = (bj, bm, bl + l0, bl + l1)
+                if kb not in sent_b:
+                    sent_b.add(kb)
+                    _copy2d(h2d, b_d, bl + l0, bj, B_h, bl + l0, bj, l1 - l0, bm)
+                    h2d_bytes += bm * (l1 - l0) * es
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                st.wait_event(ev)
+                a, b = av.sub(ai, al + l0, an, l1 - l0), bv.sub(bl + l0, bj, l1 - l0, bm)
+                if staged:
+                    t = self.temps[j]
+                    launch_mm(self.kid, st, a, b, View.of(t), overwrite=True, device=dev)
+                    slot = self.stage_ptrs[owner] + self.outgoing[j] * es
+                    self.nat.check(self.nat.load().paco_copy2d(dev, st.cuda_stream, slot, cm * es, t.data_ptr(),
+                                                               t.stride(0) * es, cm * es, cn))
+                    continue
+                remote = owner != self.rank and not self.remote_bulk
+                flags = self.nat.MM_ATOMIC | (self.nat.MM_REMOTE if remote else 0)
+                launch_mm(self.kid, st, a, b, self.views[owner].sub(ci, cj, cn, cm), flags=flags, device=dev)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=self.group)          # every remote fold / staged block has landed
+        for (ci, cj, cn, cm), off in self.incoming:
+            src = View.raw(self.stage_ptr + off * es, cn, cm, es, dev, ld=cm)
+            launch_fold(self.semiring.kernel_id, st, mine.sub(ci, cj, cn, cm), src, False)
+        d2h_bytes = 0
+        for (i0, j0, n, m) in self.owned:
+            self.nat.check(self.nat.load().paco_copy2d(
+                dev, st.cuda_stream, C_h.data_ptr() + (i0 * C_h.stride(0) + j0) * es, C_h.stride(0) * es,
+                self.own_ptr + (i0 * self.m + j0) * es, self.m * es, m * es, n))
+            d2h_bytes += n * m * es
+        torch.cuda.synchronize(dev)
+        return h2d_bytes, d2h_bytes
+
     def gather(self, out: torch.Tensor, dst: int = 0) -> None:
         """Copy this rank's C into ``out`` and reduce the owners' pieces onto ``dst``."""
         from .mm import _copy2d_raw

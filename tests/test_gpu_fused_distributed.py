@@ -94,3 +94,59 @@ def test_fused_ipc_distributed_matches_oracle(world, remote_bulk, style):
     assert any(r[2] > 0 for r in res)
     # the probe needs a C of >= 128 x 128: only the 200 x 150 case can use bulk folds
     assert [r[3] for r in res] == [False, remote_bulk == "1", False], res
+
+
+def _host_worker(rank, world, port, cases, q, style):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PACO_FOLD_STYLE=style)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2011_01441_b200 import _native as nat
+    from paper_2011_01441_b200 import matmul as M
+    from paper_2011_01441_b200.distributed import FusedDistributedMM
+    try:
+        for idx, (variant, n, m, k) in enumerate(cases):
+            A, B, _ = _inputs(n, m, k, 100 + idx)
+            plan = (M.mm_one_piece_partition(n, m, k, world) if variant == "one_piece"
+                    else M.mm_paco_partition(n, m, k, world, base=48))
+            ex = FusedDistributedMM(plan, M.SEMIRING_MINPLUS_SAT, nat.SR_MINPLUS_SAT32, 0)
+            A_h = torch.from_numpy(A).pin_memory()
+            B_h = torch.from_numpy(B).pin_memory()
+            C_h = torch.full((n, m), -1, dtype=torch.int32).pin_memory()
+            h2d, d2h = ex.run_host(A_h, B_h, C_h)
+            host = C_h.numpy()
+            pieces = [(r, host[r[0]:r[0] + r[2], r[1]:r[1] + r[3]].copy()) for r in ex.owned]
+            allp = [None] * world
+            dist.all_gather_object(allp, (pieces, h2d, d2h))
+            dist.barrier()
+            ex.close()
+            if rank == 0:
+                from oracle import cref
+                C = np.full((n, m), -1, np.int32)
+                for plist, _, _ in allp:
+                    for (i0, j0, rn, rm), blk in plist:
+                        C[i0:i0 + rn, j0:j0 + rm] = blk
+                want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, np.full((n, m), INF, np.int32))
+                d2h_total = sum(x[2] for x in allp)
+                q.put((idx, bool(np.array_equal(C, want)), d2h_total == n * m * 4,
+                       sum(x[1] for x in allp) >= (n * k + k * m) * 4))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,style", [(2, "atomic"), (3, "atomic"), (5, "atomic"), (3, "stage")])
+def test_fused_run_host_matches_oracle(world, style):
+    """End-to-end path from pinned host operands (bench.py's N>1 e2e): each rank
+    uploads the blocks its cuboid reads in k chunks, folds them into the owners' C,
+    and reads its owned rectangles back; the assembled host C equals the oracle."""
+    cases = [("one_piece", 200, 150, 1500), ("one_piece", 300, 260, 2100), ("paco", 130, 90, 700)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_host_worker, args=(r, world, port, cases, q, style)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    res = sorted(q.get(timeout=5) for _ in cases)
+    assert all(r[1] and r[2] and r[3] for r in res), res
