@@ -380,13 +380,22 @@ class FusedDistributedMM:
         dist.all_gather_object(flags, ok, group=self.group)
         return all(flags)
 
+    def _fill_owned(self, st) -> None:
+        """Semiring zero into the owned rectangles only (every fold, local or
+        remote, lands inside them; the rest of the buffer is never read)."""
+        from .mm import launch_fill
+
+        mine = self.views[self.rank]
+        for (i0, j0, n, m) in self.owned:
+            launch_fill(self.semiring.kernel_id, st, mine.sub(i0, j0, n, m))
+
     def run(self, A: torch.Tensor, B: torch.Tensor, C_init: torch.Tensor | None = None) -> None:
         from .device import View
         from .mm import launch_fill, launch_fold, launch_mm
 
         st = torch.cuda.current_stream(self.device)
         mine = self.views[self.rank]
-        launch_fill(self.semiring.kernel_id, st, mine)
+        self._fill_owned(st)
         if C_init is not None:
             ci = View.of(C_init)
             for (i0, j0, n, m) in self.owned:
@@ -440,7 +449,7 @@ class FusedDistributedMM:
         a_d, b_d, h2d = self._host_bufs
         av, bv = View.of(a_d), View.of(b_d)
         mine = self.views[self.rank]
-        launch_fill(self.semiring.kernel_id, st, mine)
+        self._fill_owned(st)
         torch.cuda.synchronize(dev)
         dist.barrier(group=self.group)          # every owner's C is initialised
         h2d.wait_stream(st)
@@ -492,10 +501,18 @@ class FusedDistributedMM:
         return h2d_bytes, d2h_bytes
 
     def gather(self, out: torch.Tensor, dst: int = 0) -> None:
-        """Copy this rank's C into ``out`` and reduce the owners' pieces onto ``dst``."""
-        from .mm import _copy2d_raw
+        """Copy this rank's owned C rectangles into ``out`` (semiring zero
+        elsewhere) and reduce the owners' pieces onto ``dst``."""
+        from .device import View
+        from .mm import launch_fill
 
-        _copy2d_raw(self.device, out, self.own_ptr, self.m * self.itemsize)
+        st = torch.cuda.current_stream(self.device)
+        launch_fill(self.semiring.kernel_id, st, View.of(out))
+        es = self.itemsize
+        for (i0, j0, n, m) in self.owned:
+            self.nat.check(self.nat.load().paco_copy2d(
+                self.device, st.cuda_stream, out.data_ptr() + (i0 * out.stride(0) + j0) * es, out.stride(0) * es,
+                self.own_ptr + (i0 * self.m + j0) * es, self.m * es, m * es, n))
         dist.reduce(out, dst=dst, op=self.op, group=self.group)
 
     def close(self) -> None:
