@@ -219,21 +219,22 @@ def main():
         plan_desc = (f"1 GPU, CTA-level tile grid: {ctas} CTAs of one 128x128 C tile, k split {ks} way(s) "
                      "(cost-model choice over the PACO cuboid plan, DESIGN.md section 5)")
     elif args.fold == "fused":
-        plan = M.mm_one_piece_partition(N, N, N, world)
+        plan = M.mm_one_piece_partition(N, N, N, world, quantum=nat.tile_shape(kid)[:3])
         ex = FusedDistributedMM(plan, sr, kid, dev)
         nred = sum(1 for t in plan.tasks if t.kind == "reduce")
 
         def step():
             ex.run(A, B)
-        launches_per_step = 1 + len(ex.launches) + len(ex.incoming)
+        launches_per_step = len(ex.owned) + len(ex.launches) + len(ex.incoming)
         how = ("staged: local temporary -> one NVLink copy into the owner's staging slot -> owner fold"
                if ex.fold_style == "stage" else
                f"{'TMA bulk' if ex.remote_bulk else 'element'} atomics into the owner's C over NVLink")
-        plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}); its {nred} k-cut folds "
+        plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}, cuts on 128-row/column tile "
+                     f"multiples); its {nred} k-cut folds "
                      f"need no REDUCE temporaries or NCCL call: local ones are fused into the kernels' epilogues, "
                      f"remote ones {how} (CUDA IPC); tile-grid CTA plan inside each rank")
     else:
-        plan = M.mm_one_piece_partition(N, N, N, world)
+        plan = M.mm_one_piece_partition(N, N, N, world, quantum=nat.tile_shape(kid)[:3])
         ex = DistributedMM(plan, sr, CudaOps(sr, kid, st))
         C = torch.empty((N, N), dtype=torch.int32, device=dev)
         nred = sum(1 for t in plan.tasks if t.kind == "reduce" and rank in t.workers())

@@ -131,6 +131,13 @@ int paco_plan_one_piece(int64_t n, int64_t m, int64_t k, int p, int64_t* out);
  * SM-waves of pieces, each charged a fixed per-visit cost.  Host only. */
 int paco_cta_grid(int semiring, int64_t n, int64_t m, int64_t k, int* ksplit, int64_t* ctas);
 
+/* Tail split of that tile grid (used when ksplit == 1): the tiles of the partial
+ * last SM-wave -- from tile `*head` on -- are each split into `*tail` k parts
+ * (CTA idx >= head: tile head + (idx - head) / tail, k part (idx - head) % tail),
+ * minimising ceil(rem * t / 148) * (k / t + 64) against one wave of whole tiles.
+ * *tail = 0: no tail split.  PACO_CTA_TAIL=0 disables it, > 1 forces it.  Host only. */
+int paco_cta_grid_tail(int semiring, int64_t n, int64_t m, int64_t k, int* tail, int64_t* head);
+
 /* The CTA-level plan paco_mm builds with PACO_MM_PACO_PLAN: MM-1-Piece over the
  * (bm, bn, bk) unit grid of `semiring` for p workers, with nearest-unit cuts
  * and a fall-back to the finest axis when a cut would miss the p-ratio by

@@ -53,6 +53,7 @@ SIGNATURES = {
     "paco_plan_one_piece": (_int, [_i64, _i64, _i64, _int, ctypes.POINTER(_i64)]),
     "paco_plan_cta": (_int, [_int, _i64, _i64, _i64, _int, ctypes.POINTER(ctypes.c_int32)]),
     "paco_cta_grid": (_int, [_int, _i64, _i64, _i64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_i64)]),
+    "paco_cta_grid_tail": (_int, [_int, _i64, _i64, _i64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_i64)]),
     "paco_fold": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _i64, _i64, _int]),
     "paco_fill": (_int, [_int, _vp, _int, _vp, _i64, _i64, _i64]),
     "paco_mm_naive": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64]),
@@ -164,13 +165,21 @@ GRID_BAND = 8  # cta_plan.cuh kGridBand
 
 def grid_pieces(sr: int, n: int, m: int, k: int) -> list[tuple[int, ...]]:
     """The default tile-grid plan as (ti0, tj0, tl0, tn, tm, tk) rows, CTA order
-    (C tiles in row-block bands of GRID_BAND, column by column inside a band)."""
+    (C tiles in row-block bands of GRID_BAND, column by column inside a band;
+    the partial last SM-wave's tiles split ``paco_cta_grid_tail`` ways in k)."""
     bm, bn, kq, _ = tile_shape(sr)
     s, ctas = cta_grid(sr, n, m, k)
+    tail, head = ctypes.c_int(), _i64()
+    check(load().paco_cta_grid_tail(sr, n, m, k, ctypes.byref(tail), ctypes.byref(head)))
+    tail, head = tail.value, head.value
     tn_, tm_, ku = -(-n // bm), -(-m // bn), -(-k // kq)
     out = []
     for idx in range(ctas):
-        tile, part = divmod(idx, s)
+        if tail > 1 and idx >= head:
+            tile, part = head + (idx - head) // tail, (idx - head) % tail
+            s = tail
+        else:
+            tile, part = divmod(idx, s)
         r0 = (tile // (GRID_BAND * tm_)) * GRID_BAND
         rows = min(GRID_BAND, tn_ - r0)
         v = tile - r0 * tm_

@@ -22,6 +22,8 @@ struct PieceTable {
   int32_t count;
   int32_t ksplit;  // 1 if any piece covers a strict sub-range of k
   int32_t grid_s;  // count == 0: 0 = PACO plan derived per CTA; s > 0 = tile grid, k split s ways
+  int32_t grid_tail;  // tile grid: > 1 = the tiles from grid_head on are split grid_tail ways in k
+  int32_t grid_head;
   Piece p[kMaxPieces];
 };
 

@@ -100,20 +100,34 @@ __host__ __device__ inline bool plan_piece(int64_t n, int64_t m, int64_t k, int 
 // split as evenly as possible.  C tiles are numbered in row-block bands of
 // kGridBand (inside a band column by column), so the tiles in flight share a
 // few A row blocks and B column blocks in L2.
+//
+// Tail split (tail > 1, s == 1): the first `head` tiles are whole pieces and
+// the remaining tiles -- the partial last SM-wave -- are each split into
+// `tail` k parts, so the last wave's work spreads over every SM instead of
+// leaving (148 - remainder) SMs idle for a whole tile.
 constexpr int64_t kGridBand = 8;
 
 __host__ __device__ inline void plan_grid_piece(int64_t n, int64_t m, int64_t k, int bm, int bn, int kq,
-                                                int s, int idx, UnitBox& out) {
+                                                int s, int idx, UnitBox& out, int tail = 0, int64_t head = 0) {
   const UnitBox r = plan_root(n, m, k, bm, bn, kq);
-  const int64_t tile = idx / s, part = idx % s;
+  int64_t tile, part, parts;
+  if (tail > 1 && idx >= head) {
+    tile = head + (idx - head) / tail;
+    part = (idx - head) % tail;
+    parts = tail;
+  } else {
+    tile = idx / s;
+    part = idx % s;
+    parts = s;
+  }
   const int64_t band = tile / (kGridBand * r.e[1]), r0 = band * kGridBand;
   const int64_t rows = r.e[0] - r0 < kGridBand ? r.e[0] - r0 : kGridBand;
   const int64_t v = tile - r0 * r.e[1];
   out.o[0] = r0 + v % rows;
   out.o[1] = v / rows;
   out.e[0] = out.e[1] = 1;
-  out.o[2] = part * r.e[2] / s;
-  out.e[2] = (part + 1) * r.e[2] / s - out.o[2];
+  out.o[2] = part * r.e[2] / parts;
+  out.e[2] = (part + 1) * r.e[2] / parts - out.o[2];
 }
 
 }  // namespace paco

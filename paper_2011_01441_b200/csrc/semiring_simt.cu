@@ -4,7 +4,8 @@
 // (matmul.py:342-397, block kernels 45-50) with one launch:
 //   * grid = the CTA-level plan.  Default: the tile grid -- one CTA per 128x128
 //     C tile and k range, the k extent split s ways by a cost model (whole
-//     SM-waves x per-visit cost, grid_ksplit); measured faster than the
+//     SM-waves x per-visit cost, grid_plan; the partial last wave's tiles
+//     split in k on their own); measured faster than the
 //     balanced PACO cuboid plan (MM-1-Piece over tile units,
 //     plan_pieces_balanced), which stays available (PACO_MM_PACO_PLAN) and
 //     for explicit piece tables;
@@ -127,6 +128,8 @@ struct MMArgs {
 struct BatchTable {
   int32_t count;
   int32_t grid_s[PACO_MAX_BATCH];
+  int32_t grid_tail[PACO_MAX_BATCH];  // tail split (plan_grid_piece)
+  int32_t grid_head[PACO_MAX_BATCH];
   int64_t first[PACO_MAX_BATCH + 1];  // CTA prefix sums
   MMArgs args[PACO_MAX_BATCH];
 };
@@ -657,7 +660,8 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
   } else {  // derive this CTA's piece of the default plan (same code as paco_plan_cta)
     UnitBox b;
     if (table.grid_s > 0)
-      plan_grid_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, table.grid_s, int(blockIdx.x), b);
+      plan_grid_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, table.grid_s, int(blockIdx.x), b,
+                      table.grid_tail, table.grid_head);
     else
       plan_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, int(gridDim.x), int(blockIdx.x), b, args.kw);
     pc = Piece{int32_t(b.o[0]), int32_t(b.o[1]), int32_t(b.o[2]), int32_t(b.e[0]), int32_t(b.e[1]),
@@ -677,7 +681,8 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
   while (q + 1 < bt.count && int64_t(blockIdx.x) >= bt.first[q + 1]) ++q;
   const MMArgs& args = bt.args[q];
   UnitBox b;
-  plan_grid_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, bt.grid_s[q], int(blockIdx.x - bt.first[q]), b);
+  plan_grid_piece(args.n, args.m, args.k, C::BM, C::BN, C::KQ, bt.grid_s[q], int(blockIdx.x - bt.first[q]), b,
+                  bt.grid_tail[q], bt.grid_head[q]);
   const Piece pc{int32_t(b.o[0]), int32_t(b.o[1]), int32_t(b.o[2]), int32_t(b.e[0]), int32_t(b.e[1]),
                  int32_t(b.e[2])};
   simt_mm_body<Op, kVec>(args, pc);
@@ -771,14 +776,24 @@ int default_pieces(int ctas_per_sm) {
 // (ring fill, epilogue, fold) worth kVisitK k elements of MACs.  Measured on B200:
 // lone CTAs run an SM at nearly full ALU rate, so only SM-level waves count.
 // PACO_CTA_KSPLIT overrides s.
-int grid_ksplit(const int64_t units[3], int kq, int64_t* ctas) {
-  static int env = -1;
+struct GridPlan {
+  int s;         // k split of every tile
+  int tail;      // > 1: tiles from `head` on are split `tail` ways instead
+  int64_t head;  // whole-tile pieces before the tail
+  int64_t ctas;
+};
+
+GridPlan grid_plan(const int64_t units[3], int kq) {
+  static int env = -1, env_tail = -2;
   if (env < 0) {
     const char* e = getenv("PACO_CTA_KSPLIT");
     env = e ? atoi(e) : 0;
+    const char* t = getenv("PACO_CTA_TAIL");  // 0/1: no tail split; > 1: forced
+    env_tail = t ? atoi(t) : -1;
   }
   const int64_t tiles = units[0] * units[1];
   const int64_t smax = units[2] < kMaxKSplit ? units[2] : kMaxKSplit;
+  const double kk = double(units[2] * kq);
   int64_t best = 1;
   if (env > 0) {
     best = env < smax ? env : smax;
@@ -786,15 +801,38 @@ int grid_ksplit(const int64_t units[3], int kq, int64_t* ctas) {
     double best_cost = 1e300;
     for (int64_t s = 1; s <= smax; ++s) {
       const double waves = double((tiles * s + kNumSMs - 1) / kNumSMs);
-      const double cost = waves * (double(units[2] * kq) / double(s) + kVisitK);
+      const double cost = waves * (kk / double(s) + kVisitK);
       if (cost < best_cost * (1.0 - 1e-9)) {
         best_cost = cost;
         best = s;
       }
     }
   }
-  *ctas = tiles * best;
-  return int(best);
+  GridPlan g{int(best), 0, tiles * best, tiles * best};
+  // Tail split of the partial last SM-wave (whole tiles only): the rem tiles
+  // left after the full waves cost one wave of full-k visits; split into t k
+  // parts they cost ceil(rem * t / 148) waves of k/t visits.
+  const int64_t rem = tiles % kNumSMs;
+  if (best != 1 || rem == 0 || tiles < kNumSMs || env_tail == 0 || env_tail == 1) return g;
+  int64_t tail = 1;
+  double tail_cost = kk + kVisitK;
+  if (env_tail > 1) {
+    tail = env_tail < smax ? env_tail : smax;
+  } else {
+    for (int64_t t = 2; t <= smax; ++t) {
+      const double c = double((rem * t + kNumSMs - 1) / kNumSMs) * (kk / double(t) + kVisitK);
+      if (c < tail_cost * (1.0 - 1e-9)) {
+        tail_cost = c;
+        tail = t;
+      }
+    }
+  }
+  if (tail > 1) {
+    g.tail = int(tail);
+    g.head = tiles - rem;
+    g.ctas = g.head + rem * tail;
+  }
+  return g;
 }
 
 int fill_table(PieceTable& t, int* grid, int64_t n, int64_t m, int64_t k, int bm, int bn, int kq,
@@ -802,6 +840,8 @@ int fill_table(PieceTable& t, int* grid, int64_t n, int64_t m, int64_t k, int bm
   const int64_t units[3] = {(n + bm - 1) / bm, (m + bn - 1) / bn, (k + kq - 1) / kq};
   t.ksplit = 0;
   t.grid_s = 0;
+  t.grid_tail = 0;
+  t.grid_head = 0;
   if (pieces && n_pieces > 0) {
     if (n_pieces > kMaxPieces) {
       set_error("n_pieces=%d exceeds PACO_MAX_PIECES=%d", n_pieces, kMaxPieces);
@@ -824,11 +864,13 @@ int fill_table(PieceTable& t, int* grid, int64_t n, int64_t m, int64_t k, int bm
     return PACO_OK;
   }
   if (!(flags & PACO_MM_PACO_PLAN)) {
-    int64_t ctas = 0;
+    const GridPlan g = grid_plan(units, kq);
     t.count = 0;
-    t.grid_s = grid_ksplit(units, kq, &ctas);
-    t.ksplit = t.grid_s > 1;
-    *grid = int(ctas);
+    t.grid_s = g.s;
+    t.grid_tail = g.tail;
+    t.grid_head = int32_t(g.head);
+    t.ksplit = g.s > 1 || g.tail > 1;
+    *grid = int(g.ctas);
     return PACO_OK;
   }
   // default: the largest feasible p <= default_p, cached per shape
@@ -988,13 +1030,14 @@ int launch_simt_batch(int device, cudaStream_t stream, int count, const paco_mm_
     }
     const int64_t units[3] = {(P.n + Cfg::BM - 1) / Cfg::BM, (P.m + Cfg::BN - 1) / Cfg::BN,
                               (P.k + Cfg::KQ - 1) / Cfg::KQ};
-    int64_t ctas = 0;
-    const int s = grid_ksplit(units, Cfg::KQ, &ctas);
+    const GridPlan g = grid_plan(units, Cfg::KQ);
+    const int s = g.s;
+    const int64_t ctas = g.ctas;
     MMArgs a{pa, pb, P.C, plda, pldb, P.ldc, P.n, P.m, P.k, Cfg::KQ, (P.flags & PACO_MM_OVERWRITE) ? 1 : 0,
              g_trace_buffer,
              (reinterpret_cast<uintptr_t>(P.C) % 16 == 0 && (P.ldc * sizeof(typename Op::TC)) % 16 == 0) ? 1 : 0,
              (P.flags & PACO_MM_ATOMIC) ? 1 : 0, plan_kw()};
-    if (a.overwrite && s > 1) {  // k-split pieces fold into C: it must hold the semiring zero first
+    if (a.overwrite && (s > 1 || g.tail > 1)) {  // k-split pieces fold into C: it must hold the semiring zero first
       const int rc = paco_fill(device, stream, Op::kId, P.C, P.ldc, P.n, P.m);
       if (rc) return rc;
       a.overwrite = 0;
@@ -1002,6 +1045,8 @@ int launch_simt_batch(int device, cudaStream_t stream, int count, const paco_mm_
     vec = vec && aligned16(pa, plda, sizeof(typename Op::TA)) && aligned16(pb, pldb, sizeof(typename Op::TB));
     bt.args[c] = a;
     bt.grid_s[c] = s;
+    bt.grid_tail[c] = g.tail;
+    bt.grid_head[c] = int32_t(g.head);
     bt.first[c] = total;
     total += ctas;
     ++c;
@@ -1093,7 +1138,25 @@ extern "C" int paco_cta_grid(int semiring, int64_t n, int64_t m, int64_t k, int*
     return PACO_ERR_ARG;
   }
   const int64_t units[3] = {(n + bm - 1) / bm, (m + bn - 1) / bn, (k + kq - 1) / kq};
-  *ksplit = grid_ksplit(units, kq, ctas);
+  const GridPlan g = grid_plan(units, kq);
+  *ksplit = g.s;
+  *ctas = g.ctas;
+  return PACO_OK;
+}
+
+extern "C" int paco_cta_grid_tail(int semiring, int64_t n, int64_t m, int64_t k, int* tail, int64_t* head) {
+  using namespace paco;
+  int bm, bn, kq, cps;
+  int rc = paco_mm_tile_shape(semiring, &bm, &bn, &kq, &cps);
+  if (rc) return rc;
+  if (n < 1 || m < 1 || k < 1 || !tail || !head) {
+    set_error("paco_cta_grid_tail: need extents >= 1 and output pointers");
+    return PACO_ERR_ARG;
+  }
+  const int64_t units[3] = {(n + bm - 1) / bm, (m + bn - 1) / bn, (k + kq - 1) / kq};
+  const GridPlan g = grid_plan(units, kq);
+  *tail = g.tail;
+  *head = g.head;
   return PACO_OK;
 }
 

@@ -211,13 +211,41 @@ def _ratio_split(length: int, a: int, b: int) -> int:
     return max(1, length * a // (a + b))
 
 
-def mm_one_piece_partition(n: int, m: int, k: int, p: int) -> Plan:
+def _quantized_split(length: int, a: int, b: int, q: int) -> int:
+    """Cut ``length`` a:b on a multiple of ``q`` (keyword extension).
+
+    A worker's kernel pays for whole tiles, so its cost is ceil(len / q); of the
+    two multiples of q around the exact ratio point the one with the smaller
+    max(cost_lo / a, cost_hi / b) wins (ties: the exact-ratio rounding).  Falls
+    back to the reference split when the axis is shorter than two quanta.
+    """
+    exact = _ratio_split(length, a, b)
+    if q <= 1 or length < 2 * q:
+        return exact
+    best = None
+    for left in (max(q, exact // q * q), min(length - 1, -(-exact // q) * q)):
+        if left <= 0 or left >= length:
+            continue
+        cost = max(-(-left // q) / a, -(-(length - left) // q) / b)
+        key = (cost, abs(left - length * a / (a + b)))
+        if best is None or key < best[0]:
+            best = (key, left)
+    return exact if best is None else best[1]
+
+
+def mm_one_piece_partition(n: int, m: int, k: int, p: int, *, quantum: tuple[int, int, int] | None = None) -> Plan:
     """MM-1-Piece: exactly one cuboid per worker (matmul.py:250-300).
 
     The cut axis is whatever an evenly-halved *virtual* cuboid would cut; the
     real length is split floor(p/2):ceil(p/2), so prime p stays balanced.
+
+    ``quantum=(qn, qm, qk)`` (keyword extension, not in the reference): cuts
+    land on multiples of the kernel's tile / k quantum (``_quantized_split``),
+    so no GPU-level cuboid ends in a partial C tile row or column -- the GPU
+    level of the two-level plan then balances whole tiles, not elements.
     """
     _check_extents(n, m, k)
+    quanta = dict(zip(AXES, quantum)) if quantum else None
     temps = _Temps()
     root = _Node(Cuboid(0, 0, 0, n, m, k))
     tasks: list[Task] = []
@@ -237,7 +265,9 @@ def mm_one_piece_partition(n: int, m: int, k: int, p: int) -> Plan:
         if length < 2:
             raise PlanError(
                 f"extents too small to give every worker a nonempty piece (axis {axis})")
-        lo, hi = _cut(node, axis, _ratio_split(length, len(left_procs), len(right_procs)), temps)
+        a, b = len(left_procs), len(right_procs)
+        left = _quantized_split(length, a, b, quanta[axis]) if quanta else _ratio_split(length, a, b)
+        lo, hi = _cut(node, axis, left, temps)
         half = tuple(v / 2 if a == axis else v for a, v in zip(AXES, virt))
         walk(lo, left_procs, half)
         walk(hi, right_procs, half)

@@ -271,6 +271,9 @@ class FusedDistributedMM:
         self.views = [View.raw(p, self.n, self.m, self.itemsize, device) for p in self.ptrs]
         owners, self.launches = fused_launches(plan, self.rank)
         self.owned = [rect for rect, w in owners if w == self.rank]
+        # no rank writes into another's C (p <= 4 on a cube: no k cut): the
+        # ranks are independent and a step needs no barrier at all
+        self.exchange = any(o != r for r in range(self.world) for _, _, o, _ in fused_launches(plan, r)[1])
         # remote folds: "atomic" (default) = the kernel's epilogue folds each
         # finished tile straight into the owner's C over NVLink (element atomics,
         # or TMA bulk reductions with PACO_REMOTE_BULK=1) -- compute and transfer
@@ -400,8 +403,9 @@ class FusedDistributedMM:
             ci = View.of(C_init)
             for (i0, j0, n, m) in self.owned:
                 launch_fold(self.semiring.kernel_id, st, mine.sub(i0, j0, n, m), ci.sub(i0, j0, n, m), False)
-        torch.cuda.synchronize(self.device)
-        dist.barrier(group=self.group)          # every owner's C is initialised
+        if self.exchange:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)      # every owner's C is initialised
         av, bv = View.of(A), View.of(B)
         es = self.itemsize
         for j, ((ai, al, an, ak), (bl, bj, bk, bm), owner, (ci, cj, cn, cm)) in enumerate(self.launches):
@@ -416,6 +420,8 @@ class FusedDistributedMM:
             remote = owner != self.rank and not self.remote_bulk
             flags = self.nat.MM_ATOMIC | (self.nat.MM_REMOTE if remote else 0)
             launch_mm(self.kid, st, a, b, self.views[owner].sub(ci, cj, cn, cm), flags=flags, device=self.device)
+        if not self.exchange:
+            return
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self.group)          # every remote fold / staged block has landed
         if self.incoming:
@@ -450,8 +456,9 @@ class FusedDistributedMM:
         av, bv = View.of(a_d), View.of(b_d)
         mine = self.views[self.rank]
         self._fill_owned(st)
-        torch.cuda.synchronize(dev)
-        dist.barrier(group=self.group)          # every owner's C is initialised
+        if self.exchange:
+            torch.cuda.synchronize(dev)
+            dist.barrier(group=self.group)      # every owner's C is initialised
         h2d.wait_stream(st)
         sent_a, sent_b, h2d_bytes = set(), set(), 0
         for j, ((ai, al, an, ak), (bl, bj, bk, bm), owner, (ci, cj, cn, cm)) in enumerate(self.launches):
@@ -486,8 +493,9 @@ class FusedDistributedMM:
                 remote = owner != self.rank and not self.remote_bulk
                 flags = self.nat.MM_ATOMIC | (self.nat.MM_REMOTE if remote else 0)
                 launch_mm(self.kid, st, a, b, self.views[owner].sub(ci, cj, cn, cm), flags=flags, device=dev)
-        torch.cuda.synchronize(dev)
-        dist.barrier(group=self.group)          # every remote fold / staged block has landed
+        if self.exchange:
+            torch.cuda.synchronize(dev)
+            dist.barrier(group=self.group)      # every remote fold / staged block has landed
         for (ci, cj, cn, cm), off in self.incoming:
             src = View.raw(self.stage_ptr + off * es, cn, cm, es, dev, ld=cm)
             launch_fold(self.semiring.kernel_id, st, mine.sub(ci, cj, cn, cm), src, False)

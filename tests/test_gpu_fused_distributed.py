@@ -79,7 +79,9 @@ def test_fused_ipc_distributed_matches_oracle(world, remote_bulk, style):
     """Remote folds staged (default: local temporary, one bulk copy into the
     owner's staging slot, owner folds), as element atomics into the owner's C,
     or, with PACO_REMOTE_BULK=1, as TMA bulk reductions into its IPC mapping."""
-    cases = [("one_piece", 96, 80, 700), ("one_piece", 200, 150, 260), ("paco", 130, 90, 333)]
+    # the last case cuts only n (no rank writes into another's C: no barriers)
+    cases = [("one_piece", 96, 80, 700), ("one_piece", 200, 150, 260), ("paco", 130, 90, 333),
+             ("one_piece", 600, 90, 100)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -93,7 +95,7 @@ def test_fused_ipc_distributed_matches_oracle(world, remote_bulk, style):
     assert all(r[1] for r in res), res
     assert any(r[2] > 0 for r in res)
     # the probe needs a C of >= 128 x 128: only the 200 x 150 case can use bulk folds
-    assert [r[3] for r in res] == [False, remote_bulk == "1", False], res
+    assert [r[3] for r in res] == [False, remote_bulk == "1", False, False], res
 
 
 def _host_worker(rank, world, port, cases, q, style):
@@ -138,7 +140,8 @@ def test_fused_run_host_matches_oracle(world, style):
     """End-to-end path from pinned host operands (bench.py's N>1 e2e): each rank
     uploads the blocks its cuboid reads in k chunks, folds them into the owners' C,
     and reads its owned rectangles back; the assembled host C equals the oracle."""
-    cases = [("one_piece", 200, 150, 1500), ("one_piece", 300, 260, 2100), ("paco", 130, 90, 700)]
+    cases = [("one_piece", 200, 150, 1500), ("one_piece", 300, 260, 2100), ("paco", 130, 90, 700),
+             ("one_piece", 1200, 90, 300)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()

@@ -269,7 +269,8 @@ def test_device_derived_cta_plan_matches_host_plan(paco_plan):
     (tile grid: paco_cta_grid; PACO_MM_PACO_PLAN: paco_plan_cta)."""
     lib = nat.load()
     rng = np.random.default_rng(31)
-    for (n, m, k) in [(1000, 700, 900), (300, 4000, 129), (2048, 2048, 2048), (200, 150, 3000)]:
+    # (3963, 1007, 1024): 248 ragged tiles, the last 100 split 4 ways in k (tail split)
+    for (n, m, k) in [(1000, 700, 900), (300, 4000, 129), (2048, 2048, 2048), (200, 150, 3000), (3963, 1007, 1024)]:
         A = torch.from_numpy(tropical(rng, (n, k), 0, 2**20)).cuda()
         B = torch.from_numpy(tropical(rng, (k, m), 0, 2**20)).cuda()
         C = torch.full((n, m), INF, dtype=torch.int32, device="cuda")

@@ -248,3 +248,31 @@ def test_cta_grid_plan_tiles_iteration_space_once():
                 assert dk >= 1
                 cover[a:a + dn, b:b + dm, c:c + dk] += 1
             assert (cover == 1).all()
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 6, 7, 8, 13])
+def test_quantized_one_piece_plan(p):
+    """quantum= (keyword extension): cuts on tile multiples, the cuboid still tiled
+    exactly once, and the max per-worker whole-tile cost never worse than the
+    reference cut's (the GPU level of bench.py --gpus N)."""
+    rng = np.random.default_rng(p)
+    shapes = [(8192, 8192, 8192), (16384, 16384, 16384), (65536, 1024, 256), (3000, 5000, 700)]
+    shapes += [tuple(int(x) for x in rng.integers(300, 9000, 3)) for _ in range(6)]
+    q = (128, 128, 4)
+    for (n, m, k) in shapes:
+        ref = M.mm_one_piece_partition(n, m, k, p)
+        pl = M.mm_one_piece_partition(n, m, k, p, quantum=q)
+        pl.validate()
+        regs = [t.region for t in pl.tasks if t.kind == COMPUTE]
+        assert len(regs) == p
+        vol = sum(r.n * r.m * r.k for r in regs)
+        assert vol == n * m * k
+        for r in regs:
+            for ax, (o, full) in enumerate(((r.i0, n), (r.j0, m), (r.l0, k))):
+                # every cut lands on a quantum unless the axis is shorter than two quanta
+                assert o % q[ax] == 0 or full < 2 * q[ax], (n, m, k, p, r)
+
+        def worst(plan):
+            return max(-(-t.region.n // 128) * -(-t.region.m // 128) * t.region.k
+                       for t in plan.tasks if t.kind == COMPUTE)
+        assert worst(pl) <= worst(ref) * 1.02, (n, m, k, p, worst(pl), worst(ref))

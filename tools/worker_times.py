@@ -39,7 +39,8 @@ def timed(fn, reps=2):
 out = {"n": n, "semiring": which + "_sat32", "plans": []}
 t1 = None
 for p in ps:
-    plan = M.mm_one_piece_partition(n, n, n, p)
+    # QUANTUM=1: GPU-level cuts on tile multiples (the plan bench.py --gpus N runs)
+    plan = M.mm_one_piece_partition(n, n, n, p, quantum=nat.tile_shape(kid)[:3] if os.environ.get("QUANTUM") == "1" else None)
     dest = fold_destinations(plan)
     per_worker = []
     for w in range(p):
