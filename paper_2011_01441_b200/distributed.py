@@ -443,7 +443,7 @@ class FusedDistributedMM:
         in the reference's shared-memory setting).  Returns (H2D, D2H) bytes.
         """
         from .device import View
-        from .mm import _copy2d, _kphased_edges, launch_fill, launch_fold, launch_mm
+        from .mm import _PIPE_MIN_ROWS, _copy2d, _kphased_edges, launch_fill, launch_fold, launch_mm
 
         dev, es = self.device, self.itemsize
         st = torch.cuda.current_stream(dev)
@@ -451,8 +451,16 @@ class FusedDistributedMM:
                 or self._host_bufs[1].shape != B_h.shape:
             self._host_bufs = (torch.empty(tuple(A_h.shape), dtype=A_h.dtype, device=dev),
                                torch.empty(tuple(B_h.shape), dtype=B_h.dtype, device=dev),
-                               torch.cuda.Stream(device=dev))
-        a_d, b_d, h2d = self._host_bufs
+                               torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
+        a_d, b_d, h2d, d2h = self._host_bufs
+        # no exchange and disjoint launch rectangles: every C row block is final as
+        # soon as this rank's last k chunk for it ran -- return it while the next
+        # block computes (the row-blocked last phase of mm._kphased_host_mm)
+        rects = [x[3] for x in self.launches]
+        streamed = not self.exchange and all(_rect_intersect(r, q) is None
+                                             for i, r in enumerate(rects) for q in rects[i + 1:])
+        returned = []
+        d2h.wait_stream(st)
         av, bv = View.of(a_d), View.of(b_d)
         mine = self.views[self.rank]
         self._fill_owned(st)
@@ -492,6 +500,21 @@ class FusedDistributedMM:
                     continue
                 remote = owner != self.rank and not self.remote_bulk
                 flags = self.nat.MM_ATOMIC | (self.nat.MM_REMOTE if remote else 0)
+                if streamed and len(spans) > 1 and (l0, l1) == spans[-1] and an >= 2 * _PIPE_MIN_ROWS:
+                    R = max(1, min(16, an // _PIPE_MIN_ROWS))
+                    redges = [((an * i // R) // 128) * 128 for i in range(R)] + [an]
+                    for r0, r1 in zip(redges[:-1], redges[1:]):
+                        launch_mm(self.kid, st, av.sub(ai + r0, al + l0, r1 - r0, l1 - l0), b,
+                                  self.views[owner].sub(ci + r0, cj, r1 - r0, cm), flags=flags, device=dev)
+                        done = torch.cuda.Event()
+                        done.record(st)
+                        d2h.wait_event(done)
+                        self.nat.check(self.nat.load().paco_copy2d(
+                            dev, d2h.cuda_stream, C_h.data_ptr() + ((ci + r0) * C_h.stride(0) + cj) * es,
+                            C_h.stride(0) * es, self.own_ptr + ((ci + r0) * self.m + cj) * es, self.m * es,
+                            cm * es, r1 - r0))
+                    returned.append((ci, cj, cn, cm))
+                    continue
                 launch_mm(self.kid, st, a, b, self.views[owner].sub(ci, cj, cn, cm), flags=flags, device=dev)
         if self.exchange:
             torch.cuda.synchronize(dev)
@@ -499,12 +522,17 @@ class FusedDistributedMM:
         for (ci, cj, cn, cm), off in self.incoming:
             src = View.raw(self.stage_ptr + off * es, cn, cm, es, dev, ld=cm)
             launch_fold(self.semiring.kernel_id, st, mine.sub(ci, cj, cn, cm), src, False)
-        d2h_bytes = 0
+        d2h_bytes = sum(r[2] * r[3] * es for r in returned)
         for (i0, j0, n, m) in self.owned:
-            self.nat.check(self.nat.load().paco_copy2d(
-                dev, st.cuda_stream, C_h.data_ptr() + (i0 * C_h.stride(0) + j0) * es, C_h.stride(0) * es,
-                self.own_ptr + (i0 * self.m + j0) * es, self.m * es, m * es, n))
-            d2h_bytes += n * m * es
+            for x in returned:  # rows already streamed back
+                if _rect_intersect(x, (i0, j0, n, m)) == (i0, j0, n, m):
+                    break
+            else:
+                self.nat.check(self.nat.load().paco_copy2d(
+                    dev, st.cuda_stream, C_h.data_ptr() + (i0 * C_h.stride(0) + j0) * es, C_h.stride(0) * es,
+                    self.own_ptr + (i0 * self.m + j0) * es, self.m * es, m * es, n))
+                d2h_bytes += n * m * es
+        st.wait_stream(d2h)
         torch.cuda.synchronize(dev)
         return h2d_bytes, d2h_bytes
 

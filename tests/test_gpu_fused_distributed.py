@@ -140,8 +140,10 @@ def test_fused_run_host_matches_oracle(world, style):
     """End-to-end path from pinned host operands (bench.py's N>1 e2e): each rank
     uploads the blocks its cuboid reads in k chunks, folds them into the owners' C,
     and reads its owned rectangles back; the assembled host C equals the oracle."""
+    # the last two cut only n: no exchange; (2600, 130, 600) at p = 2 also streams C
+    # back in row blocks behind the last k chunk
     cases = [("one_piece", 200, 150, 1500), ("one_piece", 300, 260, 2100), ("paco", 130, 90, 700),
-             ("one_piece", 1200, 90, 300)]
+             ("one_piece", 1200, 90, 300), ("one_piece", 2600, 130, 600)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
