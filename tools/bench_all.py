@@ -128,7 +128,7 @@ def main():
         res["cfg4"] = {"ms": med, "top_s": ops / med / 1e9, "frac_alu_peak": ops / med / 1e9 / alu_peak}
         del a, b, c
 
-    if 5 in only:  # cfg5: Strassen fp32 n=16384, 2 levels, FFMA leaves
+    if 5 in only:  # cfg5: Strassen fp32 n=16384, 2 levels, 3xTF32 tcgen05 leaves
         n = 16384
         a = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
         b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
@@ -137,6 +137,14 @@ def main():
         res["cfg5"] = {"ms": med, "tflop_s_algorithmic": alg / med / 1e9,
                        "tflop_s_classic_equivalent": 2 * n ** 3 / med / 1e9,
                        "frac_ffma_peak": alg / med / 1e9 / ffma_peak, "alg_flop": alg}
+        # the leaves run 3xTF32 on the tensor pipe: whole-step tensor work vs the
+        # TF32 dense peak (half the measured bf16 cuBLAS rate of MEASURED_PEAKS.json)
+        tf32_peak = PEAKS.get("bf16_tflops", 2250.0) / 2
+        mma = 3 * 49 * 2 * 4096 ** 3
+        res["cfg5"].update({"tf32x3_mma_flop": mma, "tensor_tflop_s": mma / med / 1e9,
+                            "tf32_peak_tflop_s": tf32_peak, "frac_tf32_tensor_peak": mma / med / 1e9 / tf32_peak,
+                            "tf32_peak_source": "MEASURED_PEAKS.json bf16_tflops / 2" if "bf16_tflops" in PEAKS
+                            else "nominal 2250 / 2"})
         del a, b
     print(json.dumps(res, indent=1))
     if args.out:
