@@ -6,6 +6,8 @@
 //   finish(acc)       accumulator -> stored C value (tropical: saturate at +-INF)
 //   combine(c, x)     the semiring (+) used to fold into existing C (vadd)
 //   atomic_combine    the same fold as one global atomic (k-split pieces)
+//   atomic_combine_sys  ... at system scope (C in a peer GPU's memory: the owner's
+//                     own folds and this GPU's must be atomic w.r.t. each other)
 //   bulk_combine      the same fold for a contiguous smem row, done by the TMA
 //                     unit in L2 (cp.reduce.async.bulk)
 //   zero()            the semiring zero the reference fills temps with
@@ -42,6 +44,7 @@ struct OpMinPlusSat32 {
   }
   __device__ __forceinline__ static TC combine(TC c, TC x) { return min(c, x); }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicMin(p, x); }
+  __device__ __forceinline__ static void atomic_combine_sys(TC* p, TC x) { atomicMin_system(p, x); }
   PACO_BULK_RED(bulk_combine, "min.s32")
   __host__ __device__ static TC zero() { return PACO_TROPICAL_INF; }
 };
@@ -58,6 +61,7 @@ struct OpMaxPlusSat32 {
   __device__ __forceinline__ static TC finish(Acc acc) { return max(acc, -PACO_TROPICAL_INF); }
   __device__ __forceinline__ static TC combine(TC c, TC x) { return max(c, x); }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicMax(p, x); }
+  __device__ __forceinline__ static void atomic_combine_sys(TC* p, TC x) { atomicMax_system(p, x); }
   PACO_BULK_RED(bulk_combine, "max.s32")
   __host__ __device__ static TC zero() { return -PACO_TROPICAL_INF; }
 };
@@ -73,6 +77,7 @@ struct OpF32 {
   __device__ __forceinline__ static TC finish(Acc acc) { return acc; }
   __device__ __forceinline__ static TC combine(TC c, TC x) { return c + x; }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicAdd(p, x); }
+  __device__ __forceinline__ static void atomic_combine_sys(TC* p, TC x) { atomicAdd_system(p, x); }
   PACO_BULK_RED(bulk_combine, "add.f32")
   __host__ __device__ static TC zero() { return 0.f; }
 };
@@ -88,6 +93,7 @@ struct OpF64 {
   __device__ __forceinline__ static TC finish(Acc acc) { return acc; }
   __device__ __forceinline__ static TC combine(TC c, TC x) { return c + x; }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicAdd(p, x); }
+  __device__ __forceinline__ static void atomic_combine_sys(TC* p, TC x) { atomicAdd_system(p, x); }
   PACO_BULK_RED(bulk_combine, "add.f64")
   __host__ __device__ static TC zero() { return 0.0; }
 };
@@ -109,6 +115,9 @@ struct OpIntI64 {
   }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) {
     atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(x));
+  }
+  __device__ __forceinline__ static void atomic_combine_sys(TC* p, TC x) {
+    atomicAdd_system(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(x));
   }
   PACO_BULK_RED(bulk_combine, "add.u64")
   __host__ __device__ static TC zero() { return 0; }
@@ -132,6 +141,9 @@ struct OpIntI32I64 {
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) {
     atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(x));
   }
+  __device__ __forceinline__ static void atomic_combine_sys(TC* p, TC x) {
+    atomicAdd_system(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(x));
+  }
   PACO_BULK_RED(bulk_combine, "add.u64")
   __host__ __device__ static TC zero() { return 0; }
 };
@@ -154,6 +166,9 @@ struct OpMinPlusI64 {
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) {
     atomicMin(reinterpret_cast<long long*>(p), static_cast<long long>(x));
   }
+  __device__ __forceinline__ static void atomic_combine_sys(TC* p, TC x) {
+    atomicMin_system(reinterpret_cast<long long*>(p), static_cast<long long>(x));
+  }
   PACO_BULK_RED(bulk_combine, "min.s64")
   __host__ __device__ static TC zero() { return static_cast<TC>(1) << 62; }
 };
@@ -173,6 +188,7 @@ struct OpBF16F32 {
   __device__ __forceinline__ static TC finish(Acc acc) { return acc; }
   __device__ __forceinline__ static TC combine(TC c, TC x) { return c + x; }
   __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicAdd(p, x); }
+  __device__ __forceinline__ static void atomic_combine_sys(TC* p, TC x) { atomicAdd_system(p, x); }
   PACO_BULK_RED(bulk_combine, "add.f32")
   __host__ __device__ static TC zero() { return 0.f; }
 };

@@ -123,6 +123,7 @@ struct MMArgs {
   int32_t bulk_ok;   // C is 16 B aligned with ldc*sizeof(TC) % 16 == 0: TMA bulk epilogue
   int32_t all_atomic;  // every piece folds atomically (other kernels fold into the same C)
   double kw;           // virtual k weight of the CTA plan (cta_plan.cuh)
+  int32_t sys_atomic;  // C is peer memory (PACO_MM_REMOTE): element folds at system scope
 };
 
 struct BatchTable {
@@ -312,7 +313,9 @@ __device__ __forceinline__ void epilogue(const MMArgs& a,
       const int64_t gc = col0 + (j / 4) * 64 + tx * 4 + (j % 4);
       if (gc >= a.m) continue;
       const TC v = Op::finish(acc[i][j]);
-      if (atomic)
+      if (atomic && a.sys_atomic)
+        Op::atomic_combine_sys(crow + gc, v);
+      else if (atomic)
         Op::atomic_combine(crow + gc, v);
       else if (a.overwrite)
         crow[gc] = v;
@@ -974,6 +977,7 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
               (reinterpret_cast<uintptr_t>(C) % 16 == 0 && (ldc * sizeof(typename Op::TC)) % 16 == 0 &&
                !(flags & PACO_MM_REMOTE)) ? 1 : 0,
               (flags & (PACO_MM_ATOMIC | PACO_MM_REMOTE)) ? 1 : 0, plan_kw()};
+  args.sys_atomic = (flags & PACO_MM_REMOTE) ? 1 : 0;
   if (args.overwrite && (flags & (PACO_MM_ATOMIC | PACO_MM_REMOTE))) {
     set_error("PACO_MM_OVERWRITE cannot be combined with atomic / remote folding");
     return PACO_ERR_ARG;
