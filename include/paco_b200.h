@@ -183,6 +183,17 @@ int paco_mm_tf32x3(int device, void* stream, int count, const void* const* a_hi,
                    int64_t lda, const void* const* bt_hi, const void* const* bt_lo, int64_t ldb, void* const* C,
                    int64_t ldc, int64_t n, int64_t m, int64_t k, int flags);
 
+/* As paco_mm_tf32x3, but product q is folded into each of its ndst[q] (1..4)
+ * destinations dst[4q + d] with sign sign[4q + d] (+1: C += AB, -1: C -= AB) by
+ * the epilogue's TMA reduce-adds -- the Strassen C-block combination
+ * (C00 = M1 + M4 - M5 + M7, ...) composed over the levels
+ * above the leaves, with no M buffers and no combination pass.  Destinations
+ * share ldc; they must hold their initial values (e.g. zero). */
+int paco_mm_tf32x3_multi(int device, void* stream, int count, const void* const* a_hi, const void* const* a_lo,
+                         int64_t lda, const void* const* bt_hi, const void* const* bt_lo, int64_t ldb,
+                         const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc, int64_t n,
+                         int64_t m, int64_t k);
+
 /* Asynchronous 2-D copy (host<->device or device<->device; pitches and width in
  * BYTES): the staging primitive of the overlapped host pipeline. */
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,

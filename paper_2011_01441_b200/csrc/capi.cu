@@ -36,6 +36,10 @@ int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, int count, const 
                               const void* const* al, int64_t lda, const void* const* bth, const void* const* btl,
                               int64_t ldb, void* const* C, int64_t ldc, int64_t n, int64_t m, int64_t k,
                               int flags);
+int launch_mm_tf32x3_multi(int device, cudaStream_t stream, int count, const void* const* ah,
+                           const void* const* al, int64_t lda, const void* const* bth, const void* const* btl,
+                           int64_t ldb, const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc,
+                           int64_t n, int64_t m, int64_t k, int flags);
 int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,
                       const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* lo,
                       int64_t ldo);
@@ -236,6 +240,31 @@ int paco_mm_tf32x3(int device, void* stream, int count, const void* const* a_hi,
     return PACO_OK;
   }
   return launch_mm_tf32x3_presplit(device, st, count, a_hi, a_lo, lda, bt_hi, bt_lo, ldb, C, ldc, n, m, k, flags);
+}
+
+int paco_mm_tf32x3_multi(int device, void* stream, int count, const void* const* a_hi, const void* const* a_lo,
+                         int64_t lda, const void* const* bt_hi, const void* const* bt_lo, int64_t ldb,
+                         const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc, int64_t n,
+                         int64_t m, int64_t k) {
+  if (count < 1 || count > 8 || !a_hi || !a_lo || !bt_hi || !bt_lo || !ndst || !dst || !sign) {
+    set_error("paco_mm_tf32x3_multi: need 1 <= count <= 8, pointer arrays and destination lists");
+    return PACO_ERR_ARG;
+  }
+  if (n <= 0 || m <= 0 || k <= 0) return PACO_OK;  // (+)= of an empty product: nothing to fold
+  for (int q = 0; q < count; ++q) {
+    if (ndst[q] < 1 || ndst[q] > 4) {
+      set_error("paco_mm_tf32x3_multi: problem %d has %d destinations (1..4)", q, ndst[q]);
+      return PACO_ERR_ARG;
+    }
+    for (int d = 0; d < ndst[q]; ++d) PACO_TRY(check_view("C", dst[4 * q + d], ldc, n, m));
+    PACO_TRY(check_view("A_hi", a_hi[q], lda, n, k));
+    PACO_TRY(check_view("A_lo", a_lo[q], lda, n, k));
+    PACO_TRY(check_view("Bt_hi", bt_hi[q], ldb, m, k));
+    PACO_TRY(check_view("Bt_lo", bt_lo[q], ldb, m, k));
+  }
+  PACO_TRY(use_device(device));
+  return launch_mm_tf32x3_multi(device, static_cast<cudaStream_t>(stream), count, a_hi, a_lo, lda, bt_hi, bt_lo,
+                                ldb, ndst, dst, sign, ldc, n, m, k, 0);
 }
 
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,

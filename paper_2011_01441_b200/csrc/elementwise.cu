@@ -7,6 +7,8 @@
 // multiple of the 148 SMs.
 #include <cstdio>
 
+#include <cstring>
+
 #include "common.cuh"
 #include "semiring_ops.cuh"
 
@@ -132,7 +134,17 @@ int launch_fill(int sr, cudaStream_t st, void* dst, int64_t ld, int64_t n, int64
   if (n <= 0 || m <= 0) return PACO_OK;
   return dispatch_op(sr, [&](auto op) -> int {
     using Op = decltype(op);
-    fill_kernel<Op><<<ew_grid(n * m, 256), 256, 0, st>>>(static_cast<typename Op::TC*>(dst), ld, n, m);
+    using TC = typename Op::TC;
+    const TC z = Op::zero();
+    unsigned char bytes[sizeof(TC)];
+    memcpy(bytes, &z, sizeof(TC));
+    bool all_zero = true;
+    for (size_t i = 0; i < sizeof(TC); ++i) all_zero = all_zero && bytes[i] == 0;
+    if (all_zero) {  // (+,x) zero: a 2-D memset runs at the copy engine's write rate
+      PACO_CUDA_TRY(cudaMemset2DAsync(dst, size_t(ld) * sizeof(TC), 0, size_t(m) * sizeof(TC), size_t(n), st));
+      return PACO_OK;
+    }
+    fill_kernel<Op><<<ew_grid(n * m, 256), 256, 0, st>>>(static_cast<TC*>(dst), ld, n, m);
     PACO_CUDA_TRY(cudaGetLastError());
     return PACO_OK;
   });

@@ -329,7 +329,10 @@ __device__ __forceinline__ int32_t claim_resolve(const TcArgs& a, int32_t raw) {
 // offset of each view inside its 16-byte aligned map base.
 struct TcProb {
   CUtensorMap a[2], b[2], c;
-  int32_t a_col0[2], b_col0[2], c_col0;
+  CUtensorMap cx[3];  // further destinations of the same product (reduce-add only)
+  int32_t a_col0[2], b_col0[2], c_col0, cx_col0[3];
+  int32_t ndst;  // 1 + number of cx maps in use
+  uint32_t neg;  // bit d: destination d receives -AB
 };
 constexpr int kMaxBatch = 8;
 struct TcMaps {
@@ -595,29 +598,35 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
 #pragma unroll
         for (int h = 0; h < SUBS; ++h) {
           if (col0 + EC * h >= args.m) break;
-          unsigned char* buf = stage0 + (box % EB) * L::EPI_BUF;
-          ++box;
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(EB - 1) : "memory");
-          __syncwarp();
-          if (!(args.ablate & 4)) {
+#pragma unroll 1
+          for (int d = 0; d < P.ndst; ++d) {  // every destination of the product (Strassen C terms)
+            const uint32_t sgn = ((P.neg >> d) & 1u) << 31;  // -AB: flip the fp32 sign bits
+            unsigned char* buf = stage0 + (box % EB) * L::EPI_BUF;
+            ++box;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(EB - 1) : "memory");
+            __syncwarp();
+            if (!(args.ablate & 4)) {
 #pragma unroll
-            for (int j = 0; j < EC / 4; ++j) {
-              const uint4 w = make_uint4(v[EC * h + 4 * j], v[EC * h + 4 * j + 1], v[EC * h + 4 * j + 2],
-                                         v[EC * h + 4 * j + 3]);
-              const int sw = EC == 32 ? (j ^ (lane & 7)) : (j ^ ((lane >> 1) & 3));
-              *reinterpret_cast<uint4*>(buf + lane * (EC * 4) + sw * 16) = w;
+              for (int j = 0; j < EC / 4; ++j) {
+                const uint4 w = make_uint4(v[EC * h + 4 * j] ^ sgn, v[EC * h + 4 * j + 1] ^ sgn,
+                                           v[EC * h + 4 * j + 2] ^ sgn, v[EC * h + 4 * j + 3] ^ sgn);
+                const int sw = EC == 32 ? (j ^ (lane & 7)) : (j ^ ((lane >> 1) & 3));
+                *reinterpret_cast<uint4*>(buf + lane * (EC * 4) + sw * 16) = w;
+              }
+              asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             }
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          }
-          __syncwarp();
-          if (lane == 0) {
-            if (row0 < args.n && !(args.ablate & 1)) {
-              if (args.overwrite)
-                tma_store_2d(&P.c, buf, P.c_col0 + col0 + EC * h, row0);
-              else
-                tma_reduce_add_2d(&P.c, buf, P.c_col0 + col0 + EC * h, row0);
+            __syncwarp();
+            if (lane == 0) {
+              if (row0 < args.n && !(args.ablate & 1)) {
+                const CUtensorMap* cm = d == 0 ? &P.c : &P.cx[d - 1];
+                const int cc0 = d == 0 ? P.c_col0 : P.cx_col0[d - 1];
+                if (args.overwrite)
+                  tma_store_2d(cm, buf, cc0 + col0 + EC * h, row0);
+                else
+                  tma_reduce_add_2d(cm, buf, cc0 + col0 + EC * h, row0);
+              }
+              asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
             }
-            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
           }
         }
 #else
@@ -1069,9 +1078,14 @@ int build_operands(int device, Scratch& sc, cudaStream_t stream, const void* A, 
 }
 
 template <class K>
-int build_output(tc::TcProb& P, void* C, int64_t ldc, int64_t n, int64_t m) {
-  return make_map(&P.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, n, m, ldc, K::EPI_COLS, 32, &P.c_col0,
-                  K::EPI_COLS == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+int build_output(tc::TcProb& P, void* C, int64_t ldc, int64_t n, int64_t m, CUtensorMap* map = nullptr,
+                 int32_t* col0 = nullptr) {
+  if (!map) {
+    P.ndst = 1;
+    P.neg = 0;
+  }
+  return make_map(map ? map : &P.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, C, n, m, ldc, K::EPI_COLS, 32,
+                  col0 ? col0 : &P.c_col0, K::EPI_COLS == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 template <class K>
@@ -1196,19 +1210,32 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
 
 // A batch of same-shape 3xTF32 problems from pre-split operands, one launch
 // (one tile queue): Strassen's seven leaf products of a node.
+// Optional destination lists (ndst/dst/sign, problem q's at [4q, 4q + ndst[q])):
+// each product is folded (+)= or (-)= into every one of its destinations by the
+// epilogue's TMA reduce-adds -- Strassen's C-block combination without the
+// M buffers or the combination pass.
 template <class K>
 int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* pre, int64_t lda, int64_t ldb,
-                    int64_t ldc, int64_t n, int64_t m, int64_t k, int flags) {
+                    int64_t ldc, int64_t n, int64_t m, int64_t k, int flags, const int32_t* ndst = nullptr,
+                    void* const* dst = nullptr, const int32_t* sign = nullptr) {
   int rc;
   if (count < 1 || count > tc::kMaxBatch) {
     set_error("paco_mm_tf32x3: count=%d (1..%d)", count, tc::kMaxBatch);
     return PACO_ERR_ARG;
   }
   for (int q = 0; q < count; ++q) {
-    if ((rc = check_tc_call<K>(pre[q].c, ldc, n, m, k, nullptr, 0, flags))) return rc;
-    if (!c_ok(pre[q].c, ldc, m)) {
-      set_error("paco_mm_tf32x3: C needs a 16-byte aligned start, row pitch and row length");
-      return PACO_ERR_UNSUPPORTED;
+    const int nd = ndst ? ndst[q] : 1;
+    if (nd < 1 || nd > 4) {
+      set_error("paco_mm_tf32x3_multi: problem %d has %d destinations (1..4)", q, nd);
+      return PACO_ERR_ARG;
+    }
+    for (int d = 0; d < nd; ++d) {
+      void* c = ndst ? dst[4 * q + d] : pre[q].c;
+      if ((rc = check_tc_call<K>(c, ldc, n, m, k, nullptr, 0, flags))) return rc;
+      if (!c_ok(c, ldc, m)) {
+        set_error("paco_mm_tf32x3: C needs a 16-byte aligned start, row pitch and row length");
+        return PACO_ERR_UNSUPPORTED;
+      }
     }
   }
   Scratch sc;
@@ -1218,7 +1245,16 @@ int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* 
   for (int q = 0; q < count; ++q) {
     if ((rc = build_operands<K>(device, sc, stream, nullptr, 0, nullptr, 0, n, m, k, &pre[q], lda, ldb, maps.p[q])))
       return rc;
-    if ((rc = build_output<K>(maps.p[q], pre[q].c, ldc, n, m))) return rc;
+    tc::TcProb& P = maps.p[q];
+    if ((rc = build_output<K>(P, ndst ? dst[4 * q] : pre[q].c, ldc, n, m))) return rc;
+    if (ndst) {
+      P.ndst = ndst[q];
+      for (int d = 0; d < ndst[q]; ++d) {
+        if (sign[4 * q + d] < 0) P.neg |= 1u << d;
+        if (d > 0 && (rc = build_output<K>(P, dst[4 * q + d], ldc, n, m, &P.cx[d - 1], &P.cx_col0[d - 1])))
+          return rc;
+      }
+    }
   }
   return run_tc<K>(device, sc, stream, maps, count, n, m, k, flags);
 }
@@ -1268,6 +1304,22 @@ int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, int count, const 
   if (tf32_wide(n, m, count))
     return launch_tc_batch<tc::KindTF32x3W>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags);
   return launch_tc_batch<tc::KindTF32x3>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags);
+}
+
+int launch_mm_tf32x3_multi(int device, cudaStream_t stream, int count, const void* const* ah,
+                           const void* const* al, int64_t lda, const void* const* bth, const void* const* btl,
+                           int64_t ldb, const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc,
+                           int64_t n, int64_t m, int64_t k, int flags) {
+  Presplit pre[tc::kMaxBatch];
+  if (count < 1 || count > tc::kMaxBatch || !ndst || !dst || !sign) {
+    set_error("paco_mm_tf32x3_multi: count=%d (1..%d) and destination arrays required", count, tc::kMaxBatch);
+    return PACO_ERR_ARG;
+  }
+  for (int q = 0; q < count; ++q) pre[q] = Presplit{ah[q], al[q], bth[q], btl[q], dst[4 * q]};
+  if (tf32_wide(n, m, count))
+    return launch_tc_batch<tc::KindTF32x3W>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags, ndst, dst,
+                                            sign);
+  return launch_tc_batch<tc::KindTF32x3>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags, ndst, dst, sign);
 }
 
 int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,

@@ -32,7 +32,7 @@ import torch
 from . import _native as nat
 from .device import View, pick_device, stage_in
 from .engine import execute_plan
-from .mm import launch_fold, launch_mm
+from .mm import launch_fill, launch_fold, launch_mm
 from .plan import COMPUTE, MERGE, REDUCE, Plan, PlanError, Task, pruned_bfs_assign
 
 DEFAULT_STRASSEN_BASE = 64
@@ -46,6 +46,9 @@ T_TERMS = {1: ((1, "00"), (1, "11")), 2: ((1, "00"),), 3: ((1, "01"), (-1, "11")
            7: ((1, "10"), (1, "11"))}
 C_TERMS = {"00": ((1, 1), (1, 4), (-1, 5), (1, 7)), "01": ((1, 3), (1, 5)),
            "10": ((1, 2), (1, 4)), "11": ((1, 1), (1, 3), (-1, 2), (1, 6))}
+
+# where M_r lands in C (the inverse of C_TERMS): r -> ((coef, quadrant), ...)
+M_DESTS = {r: tuple((c, q) for q, terms in C_TERMS.items() for c, rr in terms if rr == r) for r in range(1, 8)}
 
 _RING = {  # torch dtype -> (leaf kernel id, lincomb dtype id)
     torch.float32: (nat.SR_F32_TC, nat.DT_F32),   # 3xTF32 tensor-core leaves
@@ -322,7 +325,8 @@ class _Workspace:
     not copies.  ``leaf_split`` nodes (3xTF32 children) keep no S/T at all:
     their operands are formed straight into split tf32 pairs."""
 
-    def __init__(self, size: int, dtype: torch.dtype, device: int, A: View, B: View, leaf_split: bool = False):
+    def __init__(self, size: int, dtype: torch.dtype, device: int, A: View, B: View, leaf_split: bool = False,
+                 with_m: bool = True):
         h = size // 2
 
         def buf():
@@ -332,7 +336,7 @@ class _Workspace:
                   for r in range(1, 8)]
         self.T = [None if leaf_split else (_quad(B, q) if (q := _single(T_TERMS[r])) else buf())
                   for r in range(1, 8)]
-        self.M = [buf() for _ in range(7)]
+        self.M = [buf() for _ in range(7)] if with_m else None
 
 
 def _form(ws: _Workspace, A: View, B: View, dt: int, stream) -> None:
@@ -387,6 +391,81 @@ def _leaf_level_tf32(A: View, B: View, C: View, stream) -> None:
     _combine(ws, C, nat.DT_F32, stream)
 
 
+def _leaf_level(n: int, base: int) -> bool:
+    """A node of size n whose seven children are 3xTF32 leaves."""
+    h = n // 2
+    return n % 2 == 0 and (h <= base or h % 2) and h % 4 == 0
+
+
+def _leaf_level_multi(A: View, B: View, dests, stream) -> None:
+    """Leaf-level node whose product lands in ``dests`` [(View, sign)]: each
+    child M_r = S_r T_r is folded by the GEMM epilogue straight into every C
+    block it contributes to -- M_DESTS[r] inside each destination, signs
+    multiplied (<= 4 blocks) -- so no M buffer is written and no combination
+    pass reads one (paco_mm_tf32x3_multi, TMA reduce-adds)."""
+    h = A.rows // 2
+    dev = A.device
+    ops = [[torch.empty((h, h), dtype=torch.float32, device=dev) for _ in range(4)] for _ in range(7)]
+    for r in range(1, 8):
+        ah, al, bh, bl = ops[r - 1]
+        _split(stream, S_TERMS[r], A, ah, al, transpose=False)
+        _split(stream, T_TERMS[r], B, bh, bl, transpose=True)
+    ndst = (ctypes.c_int32 * 7)()
+    dst = (ctypes.c_void_p * 28)()
+    sign = (ctypes.c_int32 * 28)()
+    ld = None
+    for r in range(1, 8):
+        targets = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
+        if len(targets) > 4:
+            raise ValueError("a leaf product folds into at most 4 C blocks")
+        ndst[r - 1] = len(targets)
+        for d, (v, sg) in enumerate(targets):
+            dst[4 * (r - 1) + d] = v.ptr
+            sign[4 * (r - 1) + d] = sg
+            if ld is None:
+                ld = v.ld
+            elif v.ld != ld:
+                raise ValueError("destinations must share one row pitch")
+
+    def arr(vals):
+        return (ctypes.c_void_p * 7)(*vals)
+
+    nat.check(nat.load().paco_mm_tf32x3_multi(
+        dev, stream.cuda_stream, 7, arr([o[0].data_ptr() for o in ops]), arr([o[1].data_ptr() for o in ops]), h,
+        arr([o[2].data_ptr() for o in ops]), arr([o[3].data_ptr() for o in ops]), h, ndst, dst, sign, ld, h, h, h))
+    for o in ops:
+        for t in o:
+            t.record_stream(stream)
+
+
+def _strassen_tc_fused(A: View, B: View, dests, base: int, stream) -> None:
+    """dests (+/-)= A x B for the fp32 (3xTF32) ring, depth-first, with the
+    C-block combinations folded into the leaf GEMMs' epilogues: a node hands
+    each child the C blocks its M_r lands in (M_DESTS) instead of an M buffer,
+    as long as the leaves then fold into <= 4 blocks; deeper trees materialise
+    an M_r (zero-filled) at the level where that bound would break."""
+    n = A.rows
+    if _leaf_level(n, base) and len(dests) <= 2:
+        _leaf_level_multi(A, B, dests, stream)
+        return
+    h = n // 2
+    ws = _Workspace(n, torch.float32, A.device, A, B, with_m=False)
+    _form(ws, A, B, nat.DT_F32, stream)
+    for r in range(1, 8):
+        child = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
+        fits = len(child) <= (2 if _leaf_level(h, base) else 1)
+        if h > base and h % 2 == 0 and fits:
+            _strassen_tc_fused(ws.S[r - 1], ws.T[r - 1], child, base, stream)
+            continue
+        M = View.of(torch.empty((h, h), dtype=torch.float32, device=A.device))
+        _strassen_dev(ws.S[r - 1], ws.T[r - 1], M, base, torch.float32, stream)
+        for D, sd in child:
+            _lincomb(nat.DT_F32, stream, D, [(sd, M)], accumulate=True)
+
+
+_FUSED_COMBINE = __import__("os").environ.get("PACO_STRASSEN_FUSED", "1") != "0"
+
+
 def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stream) -> None:
     """C = A x B (square, power-of-two size) on one device, depth-first."""
     kid, dt = _RING[dtype]
@@ -394,6 +473,10 @@ def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stre
         launch_mm(kid, stream, A, B, C, overwrite=True)
         return
     h = C.rows // 2
+    if kid == nat.SR_F32_TC and _FUSED_COMBINE and (C.ld * 4) % 16 == 0 and C.ptr % 16 == 0:
+        launch_fill(nat.SR_F32, stream, C)
+        _strassen_tc_fused(A, B, [(C, 1)], base, stream)
+        return
     if kid == nat.SR_F32_TC and (h <= base or h % 2) and h % 4 == 0:
         _leaf_level_tf32(A, B, C, stream)
         return
