@@ -154,3 +154,48 @@ def test_f32_non_power_of_two(n, base):
     assert np.linalg.norm(C - ref) <= 1e-4 * np.linalg.norm(ref)
     C2 = S.strassen_execute(S.strassen_paco_partition(n, 6, base=base, split_leftover=True), A, B, "parallel")
     assert np.linalg.norm(C2 - ref) <= 1e-4 * np.linalg.norm(ref)
+
+
+def test_tf32x3_multi_signed_destinations():
+    """paco_mm_tf32x3_multi: product q folded with sign into each of its 1..4
+    destinations (the fused Strassen C combination); destinations shared by two
+    products receive both contributions; ragged n x m x k."""
+    import ctypes
+    from paper_2011_01441_b200 import _native as nat
+    lib = nat.load()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    n, m, k = 260, 200, 300
+    kp = (k + 3) // 4 * 4
+    prods, ops = [], []
+    for _ in range(2):
+        S = torch.rand(n, k, device="cuda", generator=g) * 2 - 1
+        T = torch.rand(k, m, device="cuda", generator=g) * 2 - 1
+        ah = torch.empty(n, kp, device="cuda"); al = torch.empty_like(ah)
+        bh = torch.empty(m, kp, device="cuda"); bl = torch.empty_like(bh)
+        one = (ctypes.c_int32 * 1)(1)
+        nat.check(lib.paco_tf32_split(0, None, 1, (ctypes.c_void_p * 1)(S.data_ptr()),
+                                      (ctypes.c_int64 * 1)(S.stride(0)), one, n, k, 0, ah.data_ptr(), al.data_ptr(), kp))
+        nat.check(lib.paco_tf32_split(0, None, 1, (ctypes.c_void_p * 1)(T.data_ptr()),
+                                      (ctypes.c_int64 * 1)(T.stride(0)), one, k, m, 1, bh.data_ptr(), bl.data_ptr(), kp))
+        prods.append(S.double() @ T.double())
+        ops.append((ah, al, bh, bl))
+    mp = (m + 3) // 4 * 4
+    D = [torch.zeros(n, mp, device="cuda") for _ in range(4)]
+    D[3].fill_(2.0)
+    # product 0 -> D0 (+), D1 (-), D2 (+), D3 (-); product 1 -> D1 (+), D3 (+)
+    plan = [[(0, 1), (1, -1), (2, 1), (3, -1)], [(1, 1), (3, 1)]]
+    ndst = (ctypes.c_int32 * 2)(*[len(p) for p in plan])
+    dst = (ctypes.c_void_p * 8)()
+    sign = (ctypes.c_int32 * 8)()
+    for q, p in enumerate(plan):
+        for d, (i, sg) in enumerate(p):
+            dst[4 * q + d] = D[i].data_ptr()
+            sign[4 * q + d] = sg
+    arr = lambda j: (ctypes.c_void_p * 2)(*[o[j].data_ptr() for o in ops])
+    nat.check(lib.paco_mm_tf32x3_multi(0, None, 2, arr(0), arr(1), kp, arr(2), arr(3), kp, ndst, dst, sign, mp,
+                                       n, m, k))
+    torch.cuda.synchronize()
+    want = [prods[0], -prods[0] + prods[1], prods[0], 2.0 - prods[0] + prods[1]]
+    for i in range(4):
+        got = D[i][:, :m].double()
+        assert float((got - want[i]).norm() / want[i].norm()) < 1e-5, i
