@@ -858,12 +858,33 @@ __global__ void __launch_bounds__(256) split_tf32_t_kernel(const SplitIn in, flo
   __shared__ float th[64][65], tl[64][65];
   const int64_t r0 = int64_t(blockIdx.y) * 64, c0 = int64_t(blockIdx.x) * 64;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  // interior tile: all 4 rows x nin 16-byte loads in flight before any arithmetic
+  float4 xin[4][4];
+  const bool interior = kVec && r0 + 64 <= rows && c0 + 64 <= cols;
+  if (interior) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < in.nin)
+          xin[p][q] = __ldcs(reinterpret_cast<const float4*>(in.p[q] + (r0 + ty + 16 * p) * in.ld[q] + c0 + 4 * tx));
+  }
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     const int r = ty + 16 * p;
     const int64_t i = r0 + r, j = c0 + 4 * tx;
     float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (i < rows) {
+    if (interior) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < in.nin) {
+          const float sg = in.coef[q] > 0 ? 1.f : -1.f;
+          v[0] += sg * xin[p][q].x;
+          v[1] += sg * xin[p][q].y;
+          v[2] += sg * xin[p][q].z;
+          v[3] += sg * xin[p][q].w;
+        }
+    } else if (i < rows) {
       if (kVec && j + 3 < cols) {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -917,7 +938,45 @@ __global__ void split_tf32_n_kernel(const SplitIn in, float* __restrict__ hi, fl
                                     int64_t ldo, int64_t rows, int64_t cols) {
   const int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
   if (j >= cols) return;
-  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+  int64_t i0 = blockIdx.y;
+  if (kVec) {
+    // U rows per pass, every row's loads issued before any arithmetic or store:
+    // U x nin 16-byte loads in flight per thread (one row at a time left the
+    // kernel at ~4.6 TB/s)
+    constexpr int U = 4;
+    const int64_t gy = gridDim.y;
+    for (; i0 + (U - 1) * gy < rows; i0 += U * gy) {
+      float4 x[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < in.nin) x[u][q] = __ldcs(reinterpret_cast<const float4*>(in.p[q] + (i0 + u * gy) * in.ld[q] + j));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < in.nin) {
+            const float sg = in.coef[q] > 0 ? 1.f : -1.f;
+            v[0] += sg * x[u][q].x;
+            v[1] += sg * x[u][q].y;
+            v[2] += sg * x[u][q].z;
+            v[3] += sg * x[u][q].w;
+          }
+        float h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          h[e] = round_tf32(v[e]);
+          l[e] = round_tf32(v[e] - h[e]);
+        }
+        const int64_t i = i0 + u * gy;
+        __stcs(reinterpret_cast<float4*>(hi + i * ldo + j), make_float4(h[0], h[1], h[2], h[3]));
+        __stcs(reinterpret_cast<float4*>(lo + i * ldo + j), make_float4(l[0], l[1], l[2], l[3]));
+      }
+    }
+  }
+  for (int64_t i = i0; i < rows; i += gridDim.y) {
     float v[4];
     if (kVec) {
 #pragma unroll
