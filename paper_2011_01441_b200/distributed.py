@@ -600,6 +600,16 @@ class CudaStrassenOps:
 
         launch_mm(self.kid, self._st(out), View.of(a), View.of(b), View.of(out), overwrite=True)
 
+    def strassen_into(self, a: torch.Tensor, b: torch.Tensor, dests, base: int) -> bool:
+        """dests = [(sign, C block)] (+/-)= a x b with the combinations folded into
+        the 3xTF32 leaf epilogues (fp32 only); False: not applicable here."""
+        from .device import View
+
+        if self.dtype != torch.float32:
+            return False
+        return self.S.strassen_into(View.of(a), View.of(b), [(View.of(d), sg) for sg, d in dests], base,
+                                    self._st(a))
+
 
 def strassen_placements(path: tuple[int, ...], size: int) -> list[tuple[int, int, int]]:
     """Where the product of tree node ``path`` lands in C: (sign, row, col) of
@@ -710,9 +720,13 @@ class DistributedStrassen:
         for path, nd in self.nodes:
             s, t = self._operands(A, B, path, cache)
             h = nd.size
+            places = strassen_placements(path, N)
+            into = getattr(self.ops, "strassen_into", None)
+            if into is not None and into(s, t, [(sign, Cp[i:i + h, j:j + h]) for sign, i, j in places], self.base):
+                continue  # the leaf epilogues folded every signed copy into Cp
             M = self.ops.zeros((h, h), A)
             self.ops.strassen(s, t, M, self.base)
-            for sign, i, j in strassen_placements(path, N):
+            for sign, i, j in places:
                 self.ops.lincomb(Cp[i:i + h, j:j + h], [(sign, M)], True)
         for path, piece, (ri, rj) in self.pieces:
             s, t = self._operands(A, B, path, cache)

@@ -463,6 +463,53 @@ def _strassen_tc_fused(A: View, B: View, dests, base: int, stream) -> None:
             _lincomb(nat.DT_F32, stream, D, [(sd, M)], accumulate=True)
 
 
+def _leaf_multi(A: View, B: View, dests, stream) -> None:
+    """One 3xTF32 leaf product folded (+/-) into <= 4 blocks (count-1 batch)."""
+    n, k = A.rows, A.cols
+    m = B.cols
+    dev = A.device
+    kp = (k + 3) // 4 * 4
+    ah = torch.empty((n, kp), dtype=torch.float32, device=dev)
+    al = torch.empty_like(ah)
+    bh = torch.empty((m, kp), dtype=torch.float32, device=dev)
+    bl = torch.empty_like(bh)
+    lib = nat.load()
+    one = (ctypes.c_int32 * 1)(1)
+    for src, rows, cols, tr, hi, lo in ((A, n, k, 0, ah, al), (B, k, m, 1, bh, bl)):
+        nat.check(lib.paco_tf32_split(dev, stream.cuda_stream, 1, (ctypes.c_void_p * 1)(src.ptr),
+                                      (ctypes.c_int64 * 1)(src.ld), one, rows, cols, tr, hi.data_ptr(),
+                                      lo.data_ptr(), kp))
+    ndst = (ctypes.c_int32 * 1)(len(dests))
+    dst = (ctypes.c_void_p * 4)(*[d.ptr for d, _ in dests])
+    sign = (ctypes.c_int32 * 4)(*[sg for _, sg in dests])
+    one_p = lambda t: (ctypes.c_void_p * 1)(t.data_ptr())  # noqa: E731
+    nat.check(lib.paco_mm_tf32x3_multi(dev, stream.cuda_stream, 1, one_p(ah), one_p(al), kp, one_p(bh), one_p(bl),
+                                       kp, ndst, dst, sign, dests[0][0].ld, n, m, k))
+    for t in (ah, al, bh, bl):
+        t.record_stream(stream)
+
+
+def strassen_into(A: View, B: View, dests, base: int, stream) -> bool:
+    """dests (+/-)= A x B for fp32 operands with every C-block combination folded
+    into the leaf epilogues (the executor of ``distributed.DistributedStrassen``
+    hands a node its signed C placements).  Returns False when the fused path
+    does not apply (alignment, more than 4 leaf destinations), so the caller
+    takes the M-buffer path."""
+    n = A.rows
+    ok = _FUSED_COMBINE and all(d.ptr % 16 == 0 and d.ld % 4 == 0 for d, _ in dests) and n % 4 == 0
+    if not ok:
+        return False
+    if n <= base or n % 2:
+        if len(dests) > 4:
+            return False
+        _leaf_multi(A, B, dests, stream)
+        return True
+    if _leaf_level(n, base) and len(dests) > 2:
+        return False
+    _strassen_tc_fused(A, B, dests, base, stream)
+    return True
+
+
 _FUSED_COMBINE = __import__("os").environ.get("PACO_STRASSEN_FUSED", "1") != "0"
 
 
