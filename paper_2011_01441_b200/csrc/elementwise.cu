@@ -87,7 +87,39 @@ __global__ void lincomb_kernel(T* out, int64_t ldo, int64_t n, int64_t m, const 
   constexpr int V = kVec ? Vec16<T>::N : 1;
   const int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * V;
   if (j >= m) return;
-  for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
+  int64_t i0 = blockIdx.y;
+  if (kVec) {
+    // U rows per pass with every 16-byte load issued before any arithmetic or
+    // store (U x (nin + accumulate) loads in flight per thread)
+    constexpr int U = 4;
+    const int64_t gy = gridDim.y;
+    for (; i0 + (U - 1) * gy < n; i0 += U * gy) {
+      Vec16<T> x[U][NIN], acc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * gy;
+        if (accumulate)
+          acc[u] = *reinterpret_cast<const Vec16<T>*>(out + i * ldo + j);
+        else
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc[u].v[e] = T(0);
+#pragma unroll
+        for (int q = 0; q < NIN; ++q)
+          if (q < nin) x[u][q] = *reinterpret_cast<const Vec16<T>*>(a.in[q] + i * a.ld[q] + j);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int q = 0; q < NIN; ++q)
+          if (q < nin)
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+              acc[u].v[e] = a.coef[q] > 0 ? acc[u].v[e] + x[u][q].v[e] : acc[u].v[e] - x[u][q].v[e];
+        *reinterpret_cast<Vec16<T>*>(out + (i0 + u * gy) * ldo + j) = acc[u];
+      }
+    }
+  }
+  for (int64_t i = i0; i < n; i += gridDim.y) {
     if (kVec) {
       Vec16<T> acc;
       if (accumulate)
