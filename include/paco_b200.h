@@ -64,7 +64,9 @@ extern "C" {
 #define PACO_SR_F32 6             /* (+,x)  f32 -> f32 (FFMA)                                          */
 #define PACO_SR_BF16_F32 7        /* (+,x)  bf16,bf16 -> f32 (tcgen05 tensor cores)                    */
 #define PACO_SR_F32_TC 8          /* (+,x)  f32 -> f32 as 3xTF32 on tcgen05 (hi/lo split, ~fp32 accuracy) */
-#define PACO_SR_COUNT 9
+#define PACO_SR_MINPLUS_U32 9     /* (min,+) u32 lanes, no clamp, zero 2^32-1: SEMIRING_MINPLUS on operands
+                                     in [0, 2^31) (range-checked narrowing, paco_narrow_i64)            */
+#define PACO_SR_COUNT 10
 
 #define PACO_TROPICAL_INF (1 << 30)
 
@@ -193,6 +195,21 @@ int paco_mm_tf32x3_multi(int device, void* stream, int count, const void* const*
                          int64_t lda, const void* const* bt_hi, const void* const* bt_lo, int64_t ldb,
                          const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc, int64_t n,
                          int64_t m, int64_t k);
+
+/* Range-checked narrowing of an int64 view to 32-bit words -- the fast path
+ * for the reference's own int64 semirings (SEMIRING_MINPLUS, SEMIRING_INT,
+ * matmul.py:45-55) when their operands fit 32 bits: dst = (uint32)src for
+ * lo <= src <= hi.  A value below lo, or above hi without `saturate`, sets
+ * *flag (device int32, caller-zeroed) to 1 and the caller must take the int64
+ * kernel instead; with `saturate` values above hi are stored as hi. */
+int paco_narrow_i64(int device, void* stream, const int64_t* src, int64_t ld_src, void* dst32, int64_t ld_dst,
+                    int64_t rows, int64_t cols, int64_t lo, int64_t hi, int saturate, int32_t* flag);
+
+/* Widen a PACO_SR_MINPLUS_U32 result into the int64 C it was narrowed from:
+ * c = (r == 2^32 - 1) ? c : r  (r == 2^32 - 1 only where no term reached C's
+ * saturated image, i.e. C's original int64 value stands). */
+int paco_widen_u32_i64(int device, void* stream, const void* r32, int64_t ld_r, int64_t* c, int64_t ld_c,
+                       int64_t rows, int64_t cols);
 
 /* Asynchronous 2-D copy (host<->device or device<->device; pitches and width in
  * BYTES): the staging primitive of the overlapped host pipeline. */

@@ -26,7 +26,8 @@ SR_MAXPLUS_SAT32 = 5
 SR_F32 = 6
 SR_BF16_F32 = 7
 SR_F32_TC = 8
-SR_COUNT = 9
+SR_MINPLUS_U32 = 9
+SR_COUNT = 10
 
 DT_F32, DT_F64, DT_I64 = 0, 1, 2
 
@@ -69,6 +70,8 @@ SIGNATURES = {
     "paco_mm_tf32x3_multi": (_int, [_int, _vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64,
                                     ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, ctypes.POINTER(ctypes.c_int32),
                                     ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
+    "paco_narrow_i64": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _int, _vp]),
+    "paco_widen_u32_i64": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_copy2d": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_device_alloc": (_int, [_int, ctypes.c_size_t, ctypes.POINTER(_vp)]),
     "paco_device_free": (_int, [_int, _vp]),

@@ -6,6 +6,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace paco {
@@ -50,6 +52,10 @@ int launch_naive(int sr, cudaStream_t st, const void* A, int64_t lda, const void
                  void* C, int64_t ldc, int64_t n, int64_t m, int64_t k);
 int launch_lincomb(int dtype, cudaStream_t st, void* out, int64_t ldo, int64_t n, int64_t m, int nin,
                    const void* const* ins, const int64_t* lds, const int32_t* coefs, int acc);
+int launch_narrow_i64(cudaStream_t st, const int64_t* src, int64_t lds, void* dst, int64_t ldd, int64_t n,
+                      int64_t m, int64_t lo, int64_t hi, int saturate, int32_t* flag);
+int launch_widen_u32_i64(cudaStream_t st, const void* r, int64_t ldr, int64_t* c, int64_t ldc, int64_t n,
+                         int64_t m);
 int run_alu_probe(cudaStream_t st, int which, int iters, double* tpc, double* mhz);
 struct Box;
 }  // namespace paco
@@ -65,14 +71,51 @@ int check_sr(int sr) {
   return PACO_OK;
 }
 
-// Always cudaSetDevice: besides selecting the device it makes the primary
-// context current on this thread, which the driver-API calls we make
-// (cuTensorMapEncodeTiled) need -- a fresh worker thread whose device is
-// already 0 otherwise has no current context (CUDA_ERROR_INVALID_CONTEXT).
-int use_device(int device) {
-  PACO_CUDA_TRY(cudaSetDevice(device));
-  return PACO_OK;
-}
+// Every entry point selects `device` with cudaSetDevice -- besides selecting
+// the device that makes its primary context current on this thread, which the
+// driver-API calls we make (cuTensorMapEncodeTiled) need; a fresh worker thread
+// whose device is already 0 otherwise has no current context -- and restores
+// the caller's context on return, so a C or Python caller's later CUDA work
+// without an explicit device still lands where it did before the call.  A
+// thread that had no current context gets the previous runtime device back
+// only if that device's primary context already exists (never creates one).
+class DeviceGuard {
+ public:
+  int use(int device) {
+    static auto get_cur = reinterpret_cast<CUresult (*)(CUcontext*)>(driver_fn("cuCtxGetCurrent"));
+    if (get_cur) get_cur(&prev_ctx_);
+    cudaGetDevice(&prev_dev_);
+    PACO_CUDA_TRY(cudaSetDevice(device));
+    dev_ = device;
+    return PACO_OK;
+  }
+  ~DeviceGuard() {
+    if (dev_ < 0) return;
+    static auto set_cur = reinterpret_cast<CUresult (*)(CUcontext)>(driver_fn("cuCtxSetCurrent"));
+    static auto state = reinterpret_cast<CUresult (*)(CUdevice, unsigned*, int*)>(
+        driver_fn("cuDevicePrimaryCtxGetState"));
+    if (prev_ctx_ && set_cur) {
+      set_cur(prev_ctx_);
+    } else if (prev_dev_ >= 0 && prev_dev_ != dev_ && state) {
+      unsigned flags = 0;
+      int active = 0;
+      if (state(CUdevice(prev_dev_), &flags, &active) == CUDA_SUCCESS && active) cudaSetDevice(prev_dev_);
+    }
+  }
+
+ private:
+  static void* driver_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return p;
+  }
+  CUcontext prev_ctx_ = nullptr;
+  int prev_dev_ = -1;
+  int dev_ = -1;
+};
 
 int check_view(const char* what, const void* p, int64_t ld, int64_t rows, int64_t cols) {
   if (rows < 0 || cols < 0) {
@@ -112,7 +155,8 @@ int paco_mm(int device, void* stream, int semiring, const void* A, int64_t lda, 
   PACO_TRY(check_view("B", B, ldb, k, m));
   PACO_TRY(check_view("C", C, ldc, n, m));
   if (n == 0 || m == 0) return PACO_OK;
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (k == 0) {
     // empty reduction: C (+)= zero leaves C as is, or C = zero when overwriting
@@ -144,14 +188,16 @@ int paco_fold(int device, void* stream, int semiring, void* dst, int64_t ld_dst,
   }
   PACO_TRY(check_view("dst", dst, ld_dst, n, m));
   PACO_TRY(check_view("src", src, ld_src, n, m));
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   return launch_fold(semiring, static_cast<cudaStream_t>(stream), dst, ld_dst, src, ld_src, n, m, flags);
 }
 
 int paco_fill(int device, void* stream, int semiring, void* dst, int64_t ld, int64_t n, int64_t m) {
   PACO_TRY(check_sr(semiring));
   PACO_TRY(check_view("dst", dst, ld, n, m));
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   return launch_fill(semiring, static_cast<cudaStream_t>(stream), dst, ld, n, m);
 }
 
@@ -161,7 +207,8 @@ int paco_mm_naive(int device, void* stream, int semiring, const void* A, int64_t
   PACO_TRY(check_view("A", A, lda, n, k));
   PACO_TRY(check_view("B", B, ldb, k, m));
   PACO_TRY(check_view("C", C, ldc, n, m));
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   return launch_naive(semiring, static_cast<cudaStream_t>(stream), A, lda, B, ldb, C, ldc, n, m, k);
 }
 
@@ -170,7 +217,8 @@ int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out,
                  int accumulate) {
   PACO_TRY(check_view("out", out, ld_out, n, m));
   for (int q = 0; q < nin; ++q) PACO_TRY(check_view("in", ins[q], lds[q], n, m));
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   return launch_lincomb(dtype, static_cast<cudaStream_t>(stream), out, ld_out, n, m, nin, ins, lds,
                         coefs, accumulate);
 }
@@ -197,7 +245,8 @@ int paco_mm_batch(int device, void* stream, int semiring, int count, const paco_
       PACO_TRY(check_view("B", P.B, P.ldb, P.k, P.m));
     }
   }
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   return launch_mm_simt_batch(semiring, device, static_cast<cudaStream_t>(stream), count, problems);
 }
 
@@ -210,7 +259,8 @@ int paco_tf32_split(int device, void* stream, int nin, const void* const* ins, c
     return PACO_ERR_ARG;
   }
   for (int q = 0; q < nin; ++q) PACO_TRY(check_view("in", ins[q], lds[q], rows, cols));
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   return launch_tf32_split(static_cast<cudaStream_t>(stream), nin, ins, lds, coefs, rows, cols, transpose, hi,
                            lo, ldo);
 }
@@ -232,7 +282,8 @@ int paco_mm_tf32x3(int device, void* stream, int count, const void* const* a_hi,
       PACO_TRY(check_view("Bt_lo", bt_lo[q], ldb, m, k));
     }
   }
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (k <= 0) {
     if (flags & PACO_MM_OVERWRITE)
@@ -262,9 +313,37 @@ int paco_mm_tf32x3_multi(int device, void* stream, int count, const void* const*
     PACO_TRY(check_view("Bt_hi", bt_hi[q], ldb, m, k));
     PACO_TRY(check_view("Bt_lo", bt_lo[q], ldb, m, k));
   }
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   return launch_mm_tf32x3_multi(device, static_cast<cudaStream_t>(stream), count, a_hi, a_lo, lda, bt_hi, bt_lo,
                                 ldb, ndst, dst, sign, ldc, n, m, k, 0);
+}
+
+int paco_narrow_i64(int device, void* stream, const int64_t* src, int64_t ld_src, void* dst32, int64_t ld_dst,
+                    int64_t rows, int64_t cols, int64_t lo, int64_t hi, int saturate, int32_t* flag) {
+  PACO_TRY(check_view("src", src, ld_src, rows, cols));
+  PACO_TRY(check_view("dst", dst32, ld_dst, rows, cols));
+  if (rows > 0 && cols > 0 && !flag) {
+    set_error("paco_narrow_i64: null flag");
+    return PACO_ERR_ARG;
+  }
+  if (lo > hi || lo < INT32_MIN || hi > int64_t(UINT32_MAX)) {
+    set_error("paco_narrow_i64: range [%lld, %lld] is not a 32-bit range", (long long)lo, (long long)hi);
+    return PACO_ERR_ARG;
+  }
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_narrow_i64(static_cast<cudaStream_t>(stream), src, ld_src, dst32, ld_dst, rows, cols, lo, hi,
+                           saturate, flag);
+}
+
+int paco_widen_u32_i64(int device, void* stream, const void* r32, int64_t ld_r, int64_t* c, int64_t ld_c,
+                       int64_t rows, int64_t cols) {
+  PACO_TRY(check_view("r", r32, ld_r, rows, cols));
+  PACO_TRY(check_view("c", c, ld_c, rows, cols));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_widen_u32_i64(static_cast<cudaStream_t>(stream), r32, ld_r, c, ld_c, rows, cols);
 }
 
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,
@@ -274,7 +353,8 @@ int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void*
     set_error("paco_copy2d: bad pointers or pitches");
     return PACO_ERR_ARG;
   }
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   PACO_CUDA_TRY(cudaMemcpy2DAsync(dst, size_t(dpitch), src, size_t(spitch), size_t(width), size_t(rows),
                                   cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
   return PACO_OK;
@@ -285,20 +365,23 @@ int paco_device_alloc(int device, size_t bytes, void** ptr) {
     set_error("paco_device_alloc: null output");
     return PACO_ERR_ARG;
   }
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   PACO_CUDA_TRY(cudaMalloc(ptr, bytes));
   return PACO_OK;
 }
 
 int paco_device_free(int device, void* ptr) {
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   PACO_CUDA_TRY(cudaFree(ptr));
   return PACO_OK;
 }
 
 int paco_ipc_handle(int device, void* ptr, void* handle64) {
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   cudaIpcMemHandle_t h;
   PACO_CUDA_TRY(cudaIpcGetMemHandle(&h, ptr));
   memcpy(handle64, &h, sizeof(h));
@@ -306,7 +389,8 @@ int paco_ipc_handle(int device, void* ptr, void* handle64) {
 }
 
 int paco_ipc_open(int device, const void* handle64, void** ptr) {
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   cudaIpcMemHandle_t h;
   memcpy(&h, handle64, sizeof(h));
   PACO_CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
@@ -314,7 +398,8 @@ int paco_ipc_open(int device, const void* handle64, void** ptr) {
 }
 
 int paco_ipc_close(int device, void* ptr) {
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   PACO_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
   return PACO_OK;
 }
@@ -327,7 +412,8 @@ int paco_enable_peer(int device, int peer) {
     set_error("device %d cannot access peer %d", device, peer);
     return PACO_ERR_UNSUPPORTED;
   }
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
   if (e == cudaErrorPeerAccessAlreadyEnabled) {
     cudaGetLastError();
@@ -342,7 +428,8 @@ int paco_alu_probe(int device, void* stream, int which, int iters, double* tpc, 
     set_error("paco_alu_probe: bad arguments");
     return PACO_ERR_ARG;
   }
-  PACO_TRY(use_device(device));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
   return run_alu_probe(static_cast<cudaStream_t>(stream), which, iters, tpc, mhz);
 }
 

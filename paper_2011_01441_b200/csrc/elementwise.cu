@@ -241,6 +241,66 @@ int launch_lincomb(int dtype, cudaStream_t st, void* out, int64_t ldo, int64_t n
   }
 }
 
+// Range-checked int64 -> 32-bit narrowing (paco_narrow_i64): two elements per
+// thread per row pass, rows over blockIdx.y; out-of-range values raise the
+// block's vote and one thread stores the flag.
+__global__ void narrow_i64_kernel(const int64_t* __restrict__ src, int64_t lds, uint32_t* __restrict__ dst,
+                                  int64_t ldd, int64_t n, int64_t m, int64_t lo, int64_t hi, int saturate,
+                                  int32_t* flag) {
+  int bad = 0;
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
+    for (int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 2; j < m;
+         j += int64_t(gridDim.x) * blockDim.x * 2) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (j + e >= m) break;
+        int64_t v = __ldcs(src + i * lds + j + e);
+        if (v < lo) bad = 1;
+        if (v > hi) {
+          if (saturate)
+            v = hi;
+          else
+            bad = 1;
+        }
+        dst[i * ldd + j + e] = static_cast<uint32_t>(v);
+      }
+    }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+__global__ void widen_u32_i64_kernel(const uint32_t* __restrict__ r, int64_t ldr, int64_t* __restrict__ c,
+                                     int64_t ldc, int64_t n, int64_t m) {
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < m; j += int64_t(gridDim.x) * blockDim.x) {
+      const uint32_t v = __ldcs(r + i * ldr + j);
+      if (v != 0xFFFFFFFFu) c[i * ldc + j] = int64_t(v);
+    }
+}
+
+namespace {
+dim3 rows_grid(int64_t n, int64_t m, int per_block) {
+  const int64_t xb = (m + per_block - 1) / per_block, yb = n < 65535 ? n : 65535, ycap = 2368 / xb + 1;
+  return dim3(unsigned(xb), unsigned(yb < ycap ? yb : ycap));
+}
+}  // namespace
+
+int launch_narrow_i64(cudaStream_t st, const int64_t* src, int64_t lds, void* dst, int64_t ldd, int64_t n,
+                      int64_t m, int64_t lo, int64_t hi, int saturate, int32_t* flag) {
+  if (n <= 0 || m <= 0) return PACO_OK;
+  narrow_i64_kernel<<<rows_grid(n, m, 512), 256, 0, st>>>(src, lds, static_cast<uint32_t*>(dst), ldd, n, m, lo,
+                                                           hi, saturate, flag);
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
+int launch_widen_u32_i64(cudaStream_t st, const void* r, int64_t ldr, int64_t* c, int64_t ldc, int64_t n,
+                         int64_t m) {
+  if (n <= 0 || m <= 0) return PACO_OK;
+  widen_u32_i64_kernel<<<rows_grid(n, m, 256), 256, 0, st>>>(static_cast<const uint32_t*>(r), ldr, c, ldc, n, m);
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
 // ---------------------------------------------------------------------------
 // ALU issue-rate probe (the roofline denominator for the non-tensor kernels).
 // 32 independent accumulators per thread, 8 warps x 2 CTAs per SM; per-SM

@@ -49,6 +49,27 @@ struct OpMinPlusSat32 {
   __host__ __device__ static TC zero() { return PACO_TROPICAL_INF; }
 };
 
+// The reference (min,+) semiring (int64, zero 2^62, matmul.py:29,49-50,55) on
+// operands that fit [0, 2^31): on that domain a + b <= 2^32 - 2 never wraps in
+// u32, so min(acc, a + b) on u32 lanes is the reference's int64 arithmetic
+// exactly, with no clamp -- one VIADDMNMX.U32 per term.  C's narrowed image
+// saturates at 2^32 - 1 (paco_narrow_i64); paco_widen_u32_i64 restores it.
+struct OpMinPlusU32 {
+  using TA = uint32_t;
+  using TB = uint32_t;
+  using TC = uint32_t;
+  using Acc = uint32_t;
+  static constexpr int kId = PACO_SR_MINPLUS_U32;
+  __device__ __forceinline__ static Acc identity() { return 0xFFFFFFFFu; }
+  __device__ __forceinline__ static Acc mac(Acc acc, TA a, TB b) { return min(acc, a + b); }
+  __device__ __forceinline__ static TC finish(Acc acc) { return acc; }
+  __device__ __forceinline__ static TC combine(TC c, TC x) { return min(c, x); }
+  __device__ __forceinline__ static void atomic_combine(TC* p, TC x) { atomicMin(p, x); }
+  __device__ __forceinline__ static void atomic_combine_sys(TC* p, TC x) { atomicMin_system(p, x); }
+  PACO_BULK_RED(bulk_combine, "min.u32")
+  __host__ __device__ static TC zero() { return 0xFFFFFFFFu; }
+};
+
 // (max,+) on signed 32-bit lanes, -INF = -2^30: sums stay in [-2^31, 2^31).
 struct OpMaxPlusSat32 {
   using TA = int32_t;
@@ -203,6 +224,7 @@ int dispatch_op(int sr, F&& f) {
     case PACO_SR_MINPLUS_I64: return f(OpMinPlusI64{});
     case PACO_SR_MINPLUS_SAT32: return f(OpMinPlusSat32{});
     case PACO_SR_MAXPLUS_SAT32: return f(OpMaxPlusSat32{});
+    case PACO_SR_MINPLUS_U32: return f(OpMinPlusU32{});
     case PACO_SR_F32:
     case PACO_SR_F32_TC: return f(OpF32{});
     case PACO_SR_BF16_F32: return f(OpBF16F32{});

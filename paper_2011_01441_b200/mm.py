@@ -28,7 +28,7 @@ from .cuboid import DEFAULT_BASE, Cuboid, temp_shape
 from .device import Output, View, is_host, pick_device, stage_in, torch_dtype
 from .engine import execute_plan
 from .plan import COMPUTE, REDUCE, CostReport, Plan, PlanError
-from .semiring import SEMIRING_INT, Semiring
+from .semiring import SEMIRING_INT, SEMIRING_MINPLUS, SEMIRING_MINPLUS_U32, Semiring
 
 
 def _dtype_of(x):
@@ -49,6 +49,73 @@ def kernel_for(semiring: Semiring, A, B) -> tuple[int, object]:
     if semiring.narrow_kernel_id is not None and _is_i32(A) and _is_i32(B):
         return semiring.narrow_kernel_id, semiring.narrow_in_dtype
     return semiring.kernel_id, semiring.in_dtype
+
+
+# --- the reference's own int64 semirings on 32-bit kernels ----------------------
+# SEMIRING_INT and SEMIRING_MINPLUS keep int64 storage (matmul.py:45-55), but a
+# 64-bit add+min or multiply-add is 4-6 ALU instructions per term.  When every
+# operand fits 32 bits the product is computed on 32-bit lanes with the same
+# result bit for bit: (+,x) on int32 x int32 -> int64 (IMAD.WIDE, wrapping
+# int64 accumulation, as NumPy's), (min,+) on u32 lanes for operands in
+# [0, 2^31) (a + b <= 2^32 - 2: no wrap, so no clamp either).  The range check
+# runs on the device while narrowing; any value outside (the INF = 2^62
+# sentinel, negatives, wrap-around cases) keeps the int64 kernel.
+NARROW_MIN_TERMS = 1 << 22   # below this the 64-bit kernel is cheaper than a narrowing pass + flag read
+_NARROW_RANGE = {"int": (-(2**31), 2**31 - 1), "minplus": (0, 2**31 - 1)}
+
+
+def _is_i64(x) -> bool:
+    dt = _dtype_of(x)
+    return dt == np.int64 or dt == torch.int64
+
+
+def _narrowable(semiring: Semiring, A, B, C, n: int, m: int, k: int) -> bool:
+    return (semiring in (SEMIRING_INT, SEMIRING_MINPLUS) and _is_i64(A) and _is_i64(B) and _is_i64(C)
+            and float(n) * m * k >= NARROW_MIN_TERMS)
+
+
+def _narrow_dev(x: torch.Tensor, lo: int, hi: int, saturate: bool, flag: torch.Tensor, st) -> torch.Tensor:
+    """int32 image of a device int64 matrix (paco_narrow_i64); range misses set ``flag``."""
+    out = torch.empty(tuple(x.shape), dtype=torch.int32, device=x.device)
+    xv, ov = View.of(x), View.of(out)
+    nat.check(nat.load().paco_narrow_i64(xv.device, st.cuda_stream, xv.ptr, xv.ld, ov.ptr, ov.ld, xv.rows, xv.cols,
+                                         lo, hi, int(saturate), flag.data_ptr()))
+    return out
+
+
+class _Narrowed:
+    """Device operands of a narrowed product and how to put C back (int64)."""
+
+    def __init__(self, semiring: Semiring, A, B, C, dev: int, st, overwrite: bool):
+        lo, hi = _NARROW_RANGE[semiring.name]
+        self.a64 = stage_in(A, np.int64, dev)
+        self.b64 = stage_in(B, np.int64, dev)
+        self.out = Output(C, np.int64, dev, load=not overwrite)
+        if overwrite:
+            launch_fill(semiring.kernel_id, st, View.of(self.out.dev))
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.a32 = _narrow_dev(self.a64, lo, hi, False, flag, st)
+        self.b32 = _narrow_dev(self.b64, lo, hi, False, flag, st)
+        self.minplus = semiring is SEMIRING_MINPLUS
+        self.c32 = None
+        if self.minplus:  # C's u32 image: values >= 2^32 - 1 saturate (restored by the widen)
+            self.c32 = _narrow_dev(self.out.dev, 0, 2**32 - 1, True, flag, st)
+        self.ok = int(flag.item()) == 0   # one 4-byte read: the range verdict
+
+    @property
+    def semiring(self) -> Semiring:
+        return SEMIRING_MINPLUS_U32 if self.minplus else SEMIRING_INT
+
+    @property
+    def c(self) -> torch.Tensor:
+        return self.c32 if self.minplus else self.out.dev
+
+    def finish(self, st) -> None:
+        if self.minplus:
+            r, c = View.of(self.c32), View.of(self.out.dev)
+            nat.check(nat.load().paco_widen_u32_i64(c.device, st.cuda_stream, r.ptr, r.ld, c.ptr, c.ld, c.rows,
+                                                    c.cols))
+        self.out.finish()
 
 
 def launch_mm(kid: int, stream: torch.cuda.Stream, a: View, b: View, c: View, *,
@@ -87,7 +154,7 @@ def _shape_check(A, B, C) -> tuple[int, int, int]:
 
 def mm_seq(A, B, C, semiring: Semiring = SEMIRING_INT, base: int = DEFAULT_BASE, sim=None,
            ids: tuple[int, int, int] = (100, 101, 0), *, stream: torch.cuda.Stream | None = None,
-           pieces=None, overwrite: bool = False) -> None:
+           pieces=None, overwrite: bool = False, _narrow: bool = True) -> None:
     """C <- C (+) A (x) B on one B200 (matmul.py:342-366).
 
     ``base`` is accepted for signature compatibility: the leaf size of the
@@ -102,6 +169,16 @@ def mm_seq(A, B, C, semiring: Semiring = SEMIRING_INT, base: int = DEFAULT_BASE,
     dev = pick_device(A, B, C)
     with torch.cuda.device(dev):
         st = stream if stream is not None else torch.cuda.current_stream(dev)
+        if _narrow and _narrowable(semiring, A, B, C, n, m, k):
+            with torch.cuda.stream(st):
+                nw = _Narrowed(semiring, A, B, C, dev, st, overwrite)
+                if nw.ok:
+                    mm_seq(nw.a32, nw.b32, nw.c, nw.semiring, stream=st, pieces=pieces)
+                else:  # some operand needs 64 bits: the int64 kernel on the staged operands
+                    mm_seq(nw.a64, nw.b64, nw.out.dev, semiring, stream=st, pieces=pieces, _narrow=False)
+                    nw.minplus = False
+                nw.finish(st)
+            return
         if pieces is None and _pinned_host(A, in_dt) and _pinned_host(B, in_dt) \
                 and _pinned_host(C, semiring.dtype) and n >= 2 * _PIPE_MIN_ROWS:
             mode = _PIPE_MODE or ("k" if k >= 4 * _PIPE_MIN_K else "grid")
@@ -361,7 +438,7 @@ _REMOTE_ALL = os.environ.get("PACO_MM_REMOTE_ALL", "")
 
 def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str = "serial_sim",
                sims: dict | None = None, *, devices: list[int] | None = None,
-               fused_folds: bool | None = None, batch: bool | None = None) -> CostReport:
+               fused_folds: bool | None = None, batch: bool | None = None, _narrow: bool = True) -> CostReport:
     """Run an MM plan on B200s (matmul.py:417-462).
 
     Worker ``w`` runs on ``devices[w % len(devices)]`` with its own stream
@@ -385,6 +462,20 @@ def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str
     if (meta.get("n"), meta.get("m"), meta.get("k")) not in ((n, m, k), (None, None, None)):
         raise PlanError(f"plan built for {meta.get('n')}x{meta.get('m')}x{meta.get('k')}, "
                         f"operands are {n}x{m}x{k}")
+    if _narrow and _narrowable(semiring, A, B, C, n, m, k):
+        dev = devices[0] if devices else pick_device(A, B, C)
+        with torch.cuda.device(dev):
+            st = torch.cuda.current_stream(dev)
+            nw = _Narrowed(semiring, A, B, C, dev, st, False)
+            if nw.ok:
+                report = mm_execute(plan, nw.a32, nw.b32, nw.c, nw.semiring, mode, devices=devices,
+                                    fused_folds=fused_folds, batch=batch)
+            else:
+                report = mm_execute(plan, nw.a64, nw.b64, nw.out.dev, semiring, mode, devices=devices,
+                                    fused_folds=fused_folds, batch=batch, _narrow=False)
+                nw.minplus = False
+            nw.finish(st)
+        return report
     kid, in_dt = kernel_for(semiring, A, B)
     if devices is None:
         devices = [pick_device(A, B, C)]

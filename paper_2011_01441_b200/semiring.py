@@ -77,6 +77,10 @@ SEMIRING_F32 = Semiring("f32", np.float32, np.float32(0.0), nat.SR_F32_TC)
 SEMIRING_F32_SIMT = Semiring("f32_simt", np.float32, np.float32(0.0), nat.SR_F32)
 SEMIRING_BF16 = Semiring("bf16", np.float32, np.float32(0.0), nat.SR_BF16_F32, in_dtype="bfloat16")
 
+# internal: SEMIRING_MINPLUS's image on u32 lanes (operands range-checked into
+# [0, 2^31), no clamp; mm.py narrows to it and widens the result back)
+SEMIRING_MINPLUS_U32 = Semiring("minplus_u32", np.uint32, np.uint32(0xFFFFFFFF), nat.SR_MINPLUS_U32)
+
 # reference registry (matmul.py:57) plus the B200 additions
 SEMIRINGS = {s.name: s for s in (SEMIRING_INT, SEMIRING_F64, SEMIRING_MINPLUS)}
 ALL_SEMIRINGS = dict(SEMIRINGS, **{s.name: s for s in (
