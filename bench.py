@@ -1,24 +1,32 @@
-"""Headline benchmark: (min,+) saturating tropical MM, n=m=k=8192 (BASELINE cfg2).
+"""Benchmark of the B200 PACO semiring-MM hot path (BASELINE.json's metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--cfg 2|3|4|5] [--configs 1,2,3,4,5|none]
 
-One step = one full C (+)= A (x) B over the 8192^3 iteration cuboid, inputs
-resident in HBM: the GPU-level PACO plan (mm_one_piece_partition over N ranks,
+Headline (``value``): cfg2, (min,+) saturating tropical MM n=m=k=8192
+(BASELINE.json configs[1], the config the metric is quoted on).  One step =
+one full C (+)= A (x) B over the 8192^3 iteration cuboid, inputs resident in
+HBM: the GPU-level PACO plan (mm_one_piece_partition over N ranks,
 matmul.py:250-300) gives each rank one cuboid; inside each rank one sm_100a
-launch covers it with the tile-grid CTA plan (one CTA per 128x128 C tile, k split
-by the cost model); k-cut folds (N >= 5) are fused into the kernels (upper-k
-ranks fold straight into the owner's C over CUDA IPC / NVLink; --fold nccl uses
-NCCL MIN reductions instead).  The timed region
-is bracketed by barrier + synchronize, timed with CUDA events and max'ed over
-ranks.  A, B (256 MiB each) exceed the 126 MB L2, so no flush is needed.
+launch covers it with the tile-grid CTA plan; k-cut folds (N >= 5) are fused
+into the kernels (upper-k ranks fold straight into the owner's C over CUDA
+IPC / NVLink; --fold nccl uses NCCL MIN reductions instead).  The timed
+region is bracketed by barrier + synchronize, timed with CUDA events and
+max'ed over ranks.  A, B (256 MiB each) exceed the 126 MB L2: no flush needed.
 
-``e2e`` runs the same metric through the public API (``matmul.mm_seq``; at N>1
-``FusedDistributedMM.run_host``) from pinned HOST buffers: H2D of the operands
-(and C at N=1) and D2H of C inside the timed region.
+``configs`` (N=1): every BASELINE config measured in the same run -- cfg1..cfg5
+with ms, throughput, algorithmic ops/bytes, roofline fraction against a live
+or driver-measured peak, launches and a clocks sample of its own timed region.
+
+``e2e``: the same metric through the reference-facing API
+``matmul.mm_seq(A, B, C, SEMIRING_MINPLUS_SAT)`` with pageable NumPy arrays
+(the reference's own calling convention): host staging, H2D of A, B, C and the
+D2H of C are inside the host-wall-clock timed region.  At N>1
+``FusedDistributedMM.run_host`` from pinned host tensors.
 
 ``--impl reference`` times the reference's CPU algorithm (the NumPy port in
 oracle/, process-sharded over every host core) on a bounded row sample of the
-same config.
+same config, plus one sample of the reference's threaded parallel mode.
 """
 
 from __future__ import annotations
@@ -37,10 +45,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "semiring MM Gop/s at 1/2/4/8 B200, % of roofline, vs CPU ref on host cores"
-N = 8192
 INF = 2**30
-OPS_PER_STEP = 2.0 * N * N * N
-ALG_BYTES = 3 * N * N * 4  # A, B read once, C written once (int32)
+SM_COUNT = 148
+
+WORKLOADS = {
+    1: "cfg1: (+,x) int32 [-8,8] 384x256 . 256x320 -> int64, mm_paco_partition p=3 (BASELINE.json configs[0])",
+    2: "cfg2: (min,+) saturating tropical MM n=m=k=8192, int32 [0,2^20) + 10% INF=2^30 (BASELINE.json configs[1])",
+    3: "cfg3: (+,x) bf16 N(0,1) 65536x256 . 256x1024 -> fp32, tcgen05 (BASELINE.json configs[2])",
+    4: "cfg4: (max,+) MM n=m=k=16384, int32 [-2^20,2^20) (BASELINE.json configs[3])",
+    5: "cfg5: Strassen (+,x) fp32 U(-1,1) n=16384, 2 levels (49 leaves of 4096^3), 3xTF32 tcgen05 leaves "
+       "(BASELINE.json configs[4])",
+}
 
 
 def env_int(name, default):
@@ -50,15 +65,29 @@ def env_int(name, default):
         return default
 
 
+def load_peaks():
+    """MEASURED_PEAKS.json (driver-written), else the profiling guide's stated fallback."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        p = json.load(open(path))
+        return {"hbm_gbs": float(p["hbm_gbs"]), "bf16_tflops": float(p["bf16_tflops"]),
+                "bf16_tflops_sustained": float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                "source": "of measured (MEASURED_PEAKS.json)"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "of fallback (B200_PROFILING.md: 6.65 TB/s, 1.59 PFLOP/s)"}
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during a timed region."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.1):
         self.index = index
+        self.period = period
         self.rows = []
         self._stop = threading.Event()
         self._th = threading.Thread(target=self._loop, daemon=True)
@@ -73,7 +102,7 @@ class ClockSampler:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         self._th.start()
@@ -85,7 +114,7 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -94,24 +123,9 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_inputs(device):
-    """cfg2 inputs: default_rng(1002), A then B, uniform [0, 2^20) with 10% INF."""
-    import numpy as np
-    import torch
-
-    rng = np.random.default_rng(1002)
-    A = rng.integers(0, 2**20, (N, N), dtype=np.int32)
-    A[rng.random(A.shape) < 0.10] = INF
-    B = rng.integers(0, 2**20, (N, N), dtype=np.int32)
-    B[rng.random(B.shape) < 0.10] = INF
-    A_h = torch.from_numpy(A).pin_memory()
-    B_h = torch.from_numpy(B).pin_memory()
-    return A_h, B_h
-
-
-def ncu_traffic():
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "r1_minplus_ncu.json")
+def ncu_traffic(name):
+    """DRAM bytes per launch of a kernel from a committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", name)
     try:
         k = json.load(open(path))["kernels"][0]
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -121,12 +135,12 @@ def ncu_traffic():
         return None, None
 
 
-def alu_peak(device):
-    """VIADDMNMX.U32 issue rate measured live (terms/clk/SM) -> Top/s at a given clock."""
+def alu_probe(device, which):
+    """Issue rate of one term (0: VIADDMNMX.U32 min-plus, 1: VIADDMNMX.S32 max-plus), terms/clk/SM."""
     from paper_2011_01441_b200 import _native as nat
 
     tpc, mhz = ctypes.c_double(), ctypes.c_double()
-    nat.check(nat.load().paco_alu_probe(device, None, 0, 20000, ctypes.byref(tpc), ctypes.byref(mhz)))
+    nat.check(nat.load().paco_alu_probe(device, None, which, 20000, ctypes.byref(tpc), ctypes.byref(mhz)))
     return tpc.value, mhz.value
 
 
@@ -140,26 +154,283 @@ def cpu_baseline(rows_per_proc=48, repeat=1):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
+def workload_config(cfg):
+    """The ``config`` object: identical in both arms for the same workload."""
+    return {"workload": WORKLOADS[cfg],
+            "inputs": f"numpy default_rng({1000 + cfg}) draws, A then B (SURVEY.md 8d)"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference CPU algorithm on the host cores."""
+    """--impl reference: the reference's CPU algorithm on the host cores.
+
+    Each step is a bounded sample of cfg2 (full k and m, a slab of rows) run
+    by the reference algorithm's NumPy port process-sharded over every host
+    core; ``value`` is that sample's op count over its wall time.  Before the
+    steps, one sample of the reference's shipped threaded mode
+    (mm_execute(..., mode="parallel"), GIL-bound) is timed and reported."""
     if rank != 0:
         return
+    from oracle import cpu_baseline as cb
+
+    threaded = cb.measure_threaded(2, args.ref_threaded_rows)
     last = cpu_baseline(rows_per_proc=args.ref_rows, repeat=args.warmup + args.steps)
     vals = (last.get("values") or [last["value"]])[args.warmup:] or [last["value"]]
     value = statistics.median(vals)
+    rows = args.ref_rows * last["cores"]
+    sample_ops = 2.0 * rows * 8192 * 8192
+    ms = sample_ops / (value * 1e9) * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gop/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": OPS_PER_STEP / (value * 1e9) * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic (seeded, BASELINE cfg2 distribution)",
-        "config": {"workload": "cfg2: (min,+) saturating MM n=m=k=8192, int32 [0,2^20) + 10% INF=2^30",
-                   "sample_per_step": last["sample"]},
+        "data": "synthetic (seeded numpy default_rng(1002), BASELINE cfg2 distribution)",
+        "config": workload_config(2),
+        "step": f"one bounded sample per step: {rows} of the 8192 rows of A at full k and m "
+                f"({sample_ops:.3e} ops, {ms / 1e3:.2f} s)",
         "cpu_baseline": {"value": value, "unit": "Gop/s", "cores": last["cores"], "kind": last["kind"],
-                         "sample": last["sample"]},
+                         "sample": last["sample"], "cpu_model": cb.cpu_model(),
+                         "threaded_parallel_mode": threaded},
         "e2e": {"value": value, "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
+
+# ----------------------------------------------------------------------------- our arm: configs
+
+def _events_time(fn, steps, warmup, st, per_step_calls=1):
+    """CUDA-event time (ms) of `steps` calls of fn on stream st after `warmup` calls."""
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        fn()
+    e1.record(st)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def measure_config(cfg, dev, args, peaks, probes):
+    """One BASELINE config on this GPU: dict for the line's ``configs``."""
+    import numpy as np
+    import torch
+
+    from paper_2011_01441_b200 import _native as nat
+    from paper_2011_01441_b200 import matmul as M
+    from paper_2011_01441_b200 import strassen as S
+    from paper_2011_01441_b200.device import View
+    from paper_2011_01441_b200.mm import launch_mm
+
+    st = torch.cuda.current_stream(dev)
+    rng = np.random.default_rng(1000 + cfg)
+    out = {"workload": WORKLOADS[cfg]}
+    if cfg == 1:
+        A = rng.integers(-8, 9, (384, 256), dtype=np.int32)
+        B = rng.integers(-8, 9, (256, 320), dtype=np.int32)
+        a, b = torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev)
+        c = torch.zeros(384, 320, dtype=torch.int64, device=dev)
+        plan = M.mm_paco_partition(384, 320, 256, 3)
+        steps, warmup = max(100, args.steps * 5), max(3, args.warmup)
+        with ClockSampler(dev, 0.02) as clk:
+            ms = _events_time(lambda: M.mm_execute(plan, a, b, c, M.SEMIRING_INT), steps, warmup, st)
+        ops = 2.0 * 384 * 320 * 256
+        out.update(ms=ms, value=ops / ms / 1e6, unit="Gop/s", ops_per_step=ops, steps=steps, warmup=warmup,
+                   algorithmic_bytes=1703936, gpu_launches_per_step=1,
+                   step="mm_execute(mm_paco_partition(384,320,256,3), device int32 A/B, int64 C, SEMIRING_INT): "
+                        "17 COMPUTE cuboids as one paco_mm_batch launch, 4 REDUCEs fused into its epilogues; "
+                        "includes the host-side plan walk",
+                   roofline={"bound": "latency", "note": "correctness config (0.06 Gop per step): no roofline "
+                                                          "claim (SURVEY.md 8d)"},
+                   clocks=clk.summary())
+        return out
+    if cfg in (2, 4):
+        n = 8192 if cfg == 2 else 16384
+        if cfg == 2:
+            A = rng.integers(0, 2**20, (n, n), dtype=np.int32)
+            A[rng.random(A.shape) < 0.10] = INF
+            B = rng.integers(0, 2**20, (n, n), dtype=np.int32)
+            B[rng.random(B.shape) < 0.10] = INF
+        else:
+            A = rng.integers(-2**20, 2**20, (n, n), dtype=np.int32)
+            B = rng.integers(-2**20, 2**20, (n, n), dtype=np.int32)
+        a, b = torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev)
+        del A, B
+        kid = nat.SR_MINPLUS_SAT32 if cfg == 2 else nat.SR_MAXPLUS_SAT32
+        c = torch.full((n, n), INF if cfg == 2 else -INF, dtype=torch.int32, device=dev)
+        av, bv, cv = View.of(a), View.of(b), View.of(c)
+        steps = args.steps if cfg == 2 else max(3, min(args.steps, 6))
+        warmup = max(3, args.warmup) if cfg == 2 else 3
+        with ClockSampler(dev) as clk:
+            ms = _events_time(lambda: launch_mm(kid, st, av, bv, cv), steps, warmup, st)
+        ops = 2.0 * n ** 3
+        tpc, probe_mhz = probes[0 if cfg == 2 else 1]
+        peak = 2 * tpc * SM_COUNT * 1965.0 / 1e6
+        achieved = ops / ms / 1e9
+        clocks = clk.summary()
+        traffic, src = ncu_traffic("r1_minplus_ncu.json") if cfg == 2 else (None, None)
+        ks, ctas = nat.cta_grid(kid, n, n, n)
+        out.update(ms=ms, value=ops / ms / 1e6, unit="Gop/s", ops_per_step=ops, steps=steps, warmup=warmup,
+                   algorithmic_bytes=3 * n * n * 4, gpu_launches_per_step=1,
+                   step=f"one paco_mm launch (simt_mm_kernel, {ctas} CTAs: 128x128 C tiles, k split {ks} way(s) "
+                        "+ tail split), device-resident operands",
+                   l2=f"inputs 2 x {n * n * 4 >> 20} MiB > 126 MB L2 (no flush)",
+                   roofline={"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Top/s",
+                             "frac": achieved / peak,
+                             "peak_source": (f"live VIADDMNMX.{'U32' if cfg == 2 else 'S32'} probe: {tpc:.2f} "
+                                             f"terms/clk/SM x 2 op x 148 SM x 1965 MHz max clock (probe ran at "
+                                             f"{probe_mhz:.0f} MHz)"),
+                             "peak_at_run_clock": (2 * tpc * SM_COUNT * clocks["sm_mhz"] / 1e6
+                                                   if clocks.get("sm_mhz") else None),
+                             "traffic": traffic, "traffic_source": src, "algorithmic_bytes": 3 * n * n * 4},
+                   clocks=clocks)
+        out["_tensors"] = (a, b, c)
+        return out
+    if cfg == 3:
+        n, k, m = 65536, 256, 1024
+        A = rng.standard_normal((n, k), dtype=np.float32)
+        B = rng.standard_normal((k, m), dtype=np.float32)
+        a = torch.from_numpy(A).to(dev).to(torch.bfloat16)
+        b = torch.from_numpy(B).to(dev).to(torch.bfloat16)
+        c = torch.empty(n, m, dtype=torch.float32, device=dev)
+        av, bv, cv = View.of(a), View.of(b), View.of(c)
+        steps, warmup = max(200, args.steps * 10), max(10, args.warmup)
+        with ClockSampler(dev, 0.02) as clk:
+            ms = _events_time(lambda: launch_mm(nat.SR_BF16_F32, st, av, bv, cv, overwrite=True), steps, warmup, st)
+        # the same launches one at a time after a 512 MiB L2 flush each (cold L2, event pair per launch)
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        cold = []
+        for i in range(20):
+            flush.fill_(i & 0xFF)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            launch_mm(nat.SR_BF16_F32, st, av, bv, cv, overwrite=True)
+            e1.record(st)
+            e1.synchronize()
+            cold.append(e0.elapsed_time(e1))
+        del flush
+        byts = 2 * n * k + 2 * k * m + 4 * n * m
+        flop = 2.0 * n * m * k
+        achieved = byts / ms / 1e6
+        traffic, src = ncu_traffic("r1_bf16_ncu.json")
+        out.update(ms=ms, value=flop / ms / 1e6, unit="Gop/s", ops_per_step=flop, steps=steps, warmup=warmup,
+                   algorithmic_bytes=byts, gpu_launches_per_step=1,
+                   ms_l2_flushed=statistics.median(cold),
+                   step="one paco_mm launch (tc_gemm_kernel<KindBF16Res>: persistent tcgen05, resident B), "
+                        "C overwritten (fp32, not read)",
+                   l2="back-to-back launches; working set 302 MB > 126 MB L2 (the 268 MB fp32 C write "
+                      "evicts A); ms_l2_flushed: each launch alone after a 512 MiB flush",
+                   roofline={"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                             "frac": achieved / peaks["hbm_gbs"],
+                             "frac_l2_flushed": byts / statistics.median(cold) / 1e6 / peaks["hbm_gbs"],
+                             "peak_source": f"hbm_gbs {peaks['source']}",
+                             "traffic": traffic, "traffic_source": src, "algorithmic_bytes": byts},
+                   clocks=clk.summary())
+        return out
+    if cfg == 5:
+        n = 16384
+        A = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+        B = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+        a, b = torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev)
+        del A, B
+        steps, warmup = max(3, min(args.steps, 10)), 3
+        fn = lambda: S.strassen_seq(a, b, n, base=n // 4)  # noqa: E731
+        with ClockSampler(dev) as clk:
+            ms = _events_time(fn, steps, warmup, st)
+        # live per-kernel timing of the same step (event pair around every launch; a separate pass)
+        with nat.kernel_timing() as kt:
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            fam = {name: kt.read(f) for name, f in (("tc_gemm", nat.KT_TC_GEMM), ("tf32_split", nat.KT_TF32_SPLIT),
+                                                    ("lincomb", nat.KT_LINCOMB),
+                                                    ("elementwise", nat.KT_ELEMENTWISE))}
+        per_step = {k_: {"ms": v[0] / 3, "launches": v[1] // 3} for k_, v in fam.items()}
+        alg = 49 * 2 * 4096 ** 3 + 18 * 8192 ** 2 + 7 * 18 * 4096 ** 2
+        mma = 3 * 49 * 2 * 4096 ** 3
+        tf32_peak = peaks["bf16_tflops"] / 2
+        leaf_ms = per_step["tc_gemm"]["ms"]
+        leaf_launch_ms = leaf_ms / max(1, per_step["tc_gemm"]["launches"])
+        leaf_flop = mma / max(1, per_step["tc_gemm"]["launches"])   # one launch = 7 products of 4096^3
+        achieved = leaf_flop / leaf_launch_ms / 1e9
+        traffic, src = ncu_traffic("r1_tf32x3_ncu.json")
+        out.update(ms=ms, value=alg / ms / 1e6, unit="Gop/s", ops_per_step=alg, steps=steps, warmup=warmup,
+                   classic_equivalent_gop_s=2.0 * n ** 3 / ms / 1e6,
+                   gpu_launches_per_step=sum(v["launches"] for v in per_step.values()),
+                   kernels_per_step=per_step,
+                   step="strassen_seq(A, B, 16384, base=4096): 2 Strassen levels, 49 leaf products on tcgen05 as "
+                        "3xTF32 (7 batched launches), C combination fused into the leaf epilogues",
+                   l2="A, B 1 GiB each > 126 MB L2 (no flush)",
+                   roofline={"bound": "tensor", "kernel": "tc_gemm_kernel<KindTF32x3> (Strassen leaves)",
+                             "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
+                             "achieved_note": "3 x 7 x 2 x 4096^3 MMA flop per launch / its average CUDA-event "
+                                              "duration inside the step",
+                             "step_frac": mma / ms / 1e9 / tf32_peak,
+                             "step_note": "whole step: 3 x 49 x 2 x 4096^3 tf32 MMA flop / step time",
+                             "peak_source": f"TF32 dense = bf16_tflops / 2 {peaks['source']}",
+                             "traffic": traffic, "traffic_source": src},
+                   clocks=clk.summary())
+        return out
+    raise ValueError(cfg)
+
+
+def e2e_numpy_cfg2(dev, steps):
+    """cfg2 end to end through matmul.mm_seq with pageable NumPy A, B, C (host wall clock)."""
+    import numpy as np
+    import torch
+
+    from paper_2011_01441_b200 import matmul as M
+
+    rng = np.random.default_rng(1002)
+    n = 8192
+    A = rng.integers(0, 2**20, (n, n), dtype=np.int32)
+    A[rng.random(A.shape) < 0.10] = INF
+    B = rng.integers(0, 2**20, (n, n), dtype=np.int32)
+    B[rng.random(B.shape) < 0.10] = INF
+    C = np.full((n, n), INF, np.int32)
+    M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)  # warm (pinned staging buffers, streams)
+    times = []
+    for _ in range(steps):
+        C.fill(INF)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)
+        times.append((time.perf_counter() - t0) * 1e3)
+    ms = statistics.median(times)
+    return {"value": 2.0 * n ** 3 / (ms * 1e-3) / 1e9, "unit": "Gop/s", "ms_per_step": ms,
+            "ms_all": times, "h2d_bytes_per_step": 3 * n * n * 4, "d2h_bytes_per_step": n * n * 4,
+            "api": "paper_2011_01441_b200.matmul.mm_seq(A, B, C, SEMIRING_MINPLUS_SAT) with pageable NumPy int32 "
+                   "arrays (staged through pinned buffers by host threads, k-phased H2D/compute/D2H pipeline); "
+                   "host wall clock"}
+
+
+def e2e_pinned_cfg2(dev, st, A_h, B_h, steps):
+    import torch
+
+    from paper_2011_01441_b200 import matmul as M
+
+    n = 8192
+    C_h = torch.full((n, n), INF, dtype=torch.int32).pin_memory()
+    M.mm_seq(A_h, B_h, C_h, M.SEMIRING_MINPLUS_SAT)  # warm
+    torch.cuda.synchronize(dev)
+    t = []
+    for _ in range(steps):
+        C_h.fill_(INF)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        M.mm_seq(A_h, B_h, C_h, M.SEMIRING_MINPLUS_SAT)
+        t.append((time.perf_counter() - t0) * 1e3)
+    ms = statistics.median(t)
+    return {"value": 2.0 * n ** 3 / (ms * 1e-3) / 1e9, "unit": "Gop/s", "ms_per_step": ms,
+            "api": "matmul.mm_seq with pinned torch host tensors; host wall clock"}
+
+
+# ----------------------------------------------------------------------------- our arm: main
 
 def main():
     ap = argparse.ArgumentParser()
@@ -167,12 +438,18 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cfg", type=int, default=2, choices=[2, 4],
+                    help="headline config at N>1 (cfg2 min-plus or cfg4 max-plus, GPU-level PACO plan)")
+    ap.add_argument("--configs", default="1,2,3,4,5",
+                    help="N=1: BASELINE configs measured into the line's `configs` ('none' to skip)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--ref-rows", type=int, default=48, help="rows of A per host process (reference arm)")
+    ap.add_argument("--ref-rows", type=int, default=24, help="rows of A per host process (reference arm)")
+    ap.add_argument("--ref-threaded-rows", type=int, default=32, help="rows of A for the threaded-mode sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fold", default="fused", choices=["fused", "nccl"],
                     help="N>1: k-cut folds fused into the kernels over IPC, or NCCL reductions")
     args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -180,6 +457,7 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -201,155 +479,153 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    A_h, B_h = make_inputs(dev)
-    A = A_h.to(dev)
-    B = B_h.to(dev)
-    sr = M.SEMIRING_MINPLUS_SAT
-    kid = nat.SR_MINPLUS_SAT32
+    peaks = load_peaks()
+    probes = {0: alu_probe(dev, 0), 1: alu_probe(dev, 1)}
+    cfg = 2 if world == 1 else args.cfg
+    n = 8192 if cfg == 2 else 16384
+    ops_per_step = 2.0 * n ** 3
+    sr = M.SEMIRING_MINPLUS_SAT if cfg == 2 else M.SEMIRING_MAXPLUS
+    kid = nat.SR_MINPLUS_SAT32 if cfg == 2 else nat.SR_MAXPLUS_SAT32
+    zero = INF if cfg == 2 else -INF
     st = torch.cuda.current_stream(dev)
+    configs = {}
+    wanted = [] if args.configs == "none" or world > 1 else [int(x) for x in args.configs.split(",") if x]
 
     if world == 1:
-        C = torch.full((N, N), INF, dtype=torch.int32, device=dev)
-        a, b, c = View.of(A), View.of(B), View.of(C)
-
-        def step():
-            launch_mm(kid, st, a, b, c)
-        launches_per_step = 1
-        ks, ctas = nat.cta_grid(kid, N, N, N)
+        # the headline IS configs.cfg2: measured once, with the contract's K/W and barrier-free timing
+        res2 = measure_config(2, dev, args, peaks, probes)
+        a, b, c = res2.pop("_tensors")
+        ms = res2["ms"]
+        ks, ctas = nat.cta_grid(kid, n, n, n)
         plan_desc = (f"1 GPU, CTA-level tile grid: {ctas} CTAs of one 128x128 C tile, k split {ks} way(s) "
                      "(cost-model choice over the PACO cuboid plan, DESIGN.md section 5)")
-    elif args.fold == "fused":
-        plan = M.mm_one_piece_partition(N, N, N, world, quantum=nat.tile_shape(kid)[:3])
-        ex = FusedDistributedMM(plan, sr, kid, dev)
-        nred = sum(1 for t in plan.tasks if t.kind == "reduce")
-
-        def step():
-            ex.run(A, B)
-        launches_per_step = len(ex.owned) + len(ex.launches) + len(ex.incoming)
-        how = ("staged: local temporary -> one NVLink copy into the owner's staging slot -> owner fold"
-               if ex.fold_style == "stage" else
-               f"{'TMA bulk' if ex.remote_bulk else 'element'} atomics into the owner's C over NVLink")
-        plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}, cuts on 128-row/column tile "
-                     f"multiples); its {nred} k-cut folds "
-                     f"need no REDUCE temporaries or NCCL call: local ones are fused into the kernels' epilogues, "
-                     f"remote ones {how} (CUDA IPC); tile-grid CTA plan inside each rank")
+        launches_per_step = 1
+        clocks = res2["clocks"]
+        roofline = res2["roofline"]
+        A_h, B_h = a.cpu().pin_memory(), b.cpu().pin_memory()
+        del a, b, c
+        torch.cuda.empty_cache()
     else:
-        plan = M.mm_one_piece_partition(N, N, N, world, quantum=nat.tile_shape(kid)[:3])
-        ex = DistributedMM(plan, sr, CudaOps(sr, kid, st))
-        C = torch.empty((N, N), dtype=torch.int32, device=dev)
-        nred = sum(1 for t in plan.tasks if t.kind == "reduce" and rank in t.workers())
+        rng = np.random.default_rng(1000 + cfg)
+        if cfg == 2:
+            A = rng.integers(0, 2**20, (n, n), dtype=np.int32)
+            A[rng.random(A.shape) < 0.10] = INF
+            B = rng.integers(0, 2**20, (n, n), dtype=np.int32)
+            B[rng.random(B.shape) < 0.10] = INF
+        else:
+            A = rng.integers(-2**20, 2**20, (n, n), dtype=np.int32)
+            B = rng.integers(-2**20, 2**20, (n, n), dtype=np.int32)
+        A_h, B_h = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+        A, B = A_h.to(dev), B_h.to(dev)
+        plan = M.mm_one_piece_partition(n, n, n, world, quantum=nat.tile_shape(kid)[:3])
+        nred = sum(1 for t in plan.tasks if t.kind == "reduce")
+        if args.fold == "fused":
+            ex = FusedDistributedMM(plan, sr, kid, dev)
 
-        def step():
-            ex.run(A, B, C)
-        launches_per_step = 2 + len(ex.temp_ids) + 3 * nred + len(ex.mine)
-        plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}) "
-                     f"({sum(1 for t in plan.tasks if t.kind == 'reduce')} k-cut NCCL MIN folds), "
-                     "tile-grid CTA plan inside each rank")
+            def step():
+                ex.run(A, B)
+            launches_per_step = len(ex.owned) + len(ex.launches) + len(ex.incoming)
+            how = ("staged: local temporary -> one NVLink copy into the owner's staging slot -> owner fold"
+                   if ex.fold_style == "stage" else
+                   f"{'TMA bulk' if ex.remote_bulk else 'element'} atomics into the owner's C over NVLink")
+            plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}, cuts on 128-row/column tile "
+                         f"multiples); its {nred} k-cut folds need no REDUCE temporaries or NCCL call: local ones "
+                         f"are fused into the kernels' epilogues, remote ones {how} (CUDA IPC); tile-grid CTA plan "
+                         "inside each rank")
+        else:
+            ex = DistributedMM(plan, sr, CudaOps(sr, kid, st))
+            C = torch.empty((n, n), dtype=torch.int32, device=dev)
+            mine = sum(1 for t in plan.tasks if t.kind == "reduce" and rank in t.workers())
 
-    def barrier():
-        if world > 1:
+            def step():
+                ex.run(A, B, C)
+            launches_per_step = 2 + len(ex.temp_ids) + 3 * mine + len(ex.mine)
+            plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}) ({nred} k-cut NCCL "
+                         f"{'MIN' if cfg == 2 else 'MAX'} folds), tile-grid CTA plan inside each rank")
+
+        def barrier():
             dist.barrier()
-        torch.cuda.synchronize(dev)
+            torch.cuda.synchronize(dev)
 
-    # live roofline denominator: VIADDMNMX.U32 issue rate on this GPU
-    tpc, probe_mhz = alu_peak(dev)
-
-    for _ in range(args.warmup):
-        step()
-    barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
-        barrier()
-        e0.record(st)
-        for _ in range(args.steps):
+        for _ in range(args.warmup):
             step()
-        e1.record(st)
         barrier()
-    ms_total = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with ClockSampler(dev) as clk:
+            barrier()
+            e0.record(st)
+            for _ in range(args.steps):
+                step()
+            e1.record(st)
+            barrier()
+        t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
-    ms = ms_total / args.steps
-    value = OPS_PER_STEP / (ms * 1e-3) / 1e9  # whole-job Gop/s
+        ms = float(t.item()) / args.steps
+        clocks = clk.summary()
+        tpc, probe_mhz = probes[0 if cfg == 2 else 1]
+        peak = 2 * tpc * SM_COUNT * 1965.0 / 1e6
+        per_gpu = ops_per_step / world / (ms * 1e-3) / 1e12
+        roofline = {"bound": "alu", "achieved": per_gpu, "peak": peak, "unit": "Top/s", "frac": per_gpu / peak,
+                    "per": "GPU (whole-job Top/s / N)",
+                    "peak_source": f"live VIADDMNMX probe: {tpc:.2f} terms/clk/SM x 2 x 148 x 1965 MHz"}
 
-    # kernel-only timing of the dominant kernel on the same stream (1 GPU shape / this rank's cuboid)
-    kern_ms = None
-    if world == 1:
-        kern_ms = ms  # the step is exactly one paco_mm launch
-    clocks = clk.summary()
+    value = ops_per_step / (ms * 1e-3) / 1e9  # whole-job Gop/s
 
-    # e2e: public API from pinned host buffers (H2D A, B, C; D2H C) -- rank 0's GPU, whole problem
+    # e2e through the public API from host memory
     e2e = None
     if world == 1:
-        C_h = torch.full((N, N), INF, dtype=torch.int32).pin_memory()
-        M.mm_seq(A_h, B_h, C_h, sr)  # warm
-        torch.cuda.synchronize(dev)
-        t_e2e = []
-        for _ in range(args.e2e_steps):
-            C_h.fill_(INF)
-            f0 = torch.cuda.Event(enable_timing=True)
-            f1 = torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize(dev)
-            f0.record(st)
-            M.mm_seq(A_h, B_h, C_h, sr)
-            f1.record(st)
-            f1.synchronize()
-            t_e2e.append(f0.elapsed_time(f1))
-        e2e_ms = statistics.median(t_e2e)
-        e2e = {"value": OPS_PER_STEP / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s",
-               "ms_per_step": e2e_ms, "h2d_bytes_per_step": 3 * N * N * 4,
-               "d2h_bytes_per_step": N * N * 4, "api": "paper_2011_01441_b200.matmul.mm_seq (pinned host numpy-equivalent tensors)"}
+        e2e = e2e_numpy_cfg2(dev, args.e2e_steps)
+        e2e["pinned_torch"] = e2e_pinned_cfg2(dev, st, A_h, B_h, args.e2e_steps)
     elif args.fold == "fused":
-        # every rank uploads the A/B blocks its cuboid reads (k-chunked, overlapped with
-        # the folds into the owners' C) and reads its owned C rectangles back
-        C_h = torch.empty((N, N), dtype=torch.int32).pin_memory()
+        C_h = torch.empty((n, n), dtype=torch.int32).pin_memory()
         ex.run_host(A_h, B_h, C_h)  # warm
         t_e2e, nbytes = [], (0, 0)
         for _ in range(args.e2e_steps):
-            barrier()
-            f0 = torch.cuda.Event(enable_timing=True)
-            f1 = torch.cuda.Event(enable_timing=True)
-            f0.record(st)
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
             nbytes = ex.run_host(A_h, B_h, C_h)
-            f1.record(st)
-            f1.synchronize()
-            t = torch.tensor([f0.elapsed_time(f1)], device=dev, dtype=torch.float64)
+            torch.cuda.synchronize(dev)
+            t = torch.tensor([(time.perf_counter() - t0) * 1e3], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_e2e.append(float(t.item()))
         tot = torch.tensor(list(nbytes), device=dev, dtype=torch.float64)
         dist.all_reduce(tot)
         e2e_ms = statistics.median(t_e2e)
-        e2e = {"value": OPS_PER_STEP / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s", "ms_per_step": e2e_ms,
+        e2e = {"value": ops_per_step / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item()),
-               "bytes": "summed over ranks; time = max over ranks",
+               "bytes": "summed over ranks; time = max over ranks (host wall clock)",
                "api": "paper_2011_01441_b200.distributed.FusedDistributedMM.run_host (pinned host tensors)"}
 
+    if world == 1:
+        configs["cfg2"] = res2
+        for c_ in wanted:
+            if c_ == 2:
+                continue
+            torch.cuda.empty_cache()
+            r = measure_config(c_, dev, args, peaks, probes)
+            r.pop("_tensors", None)
+            configs[f"cfg{c_}"] = r
+        configs = {k_: configs[k_] for k_ in sorted(configs)}
+
     if rank == 0:
-        peak_max = 2 * tpc * 148 * 1965.0 / 1e6  # Top/s at the 1965 MHz max SM clock
-        traffic, traffic_src = ncu_traffic()
-        achieved = OPS_PER_STEP / (kern_ms * 1e-3) / 1e12 if kern_ms else value / world / 1e3
         line = {
             "metric": METRIC, "value": value, "unit": "Gop/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic (seeded numpy default_rng(1002), BASELINE cfg2 distribution)",
-            "config": {"workload": "cfg2: (min,+) saturating tropical MM n=m=k=8192, int32 [0,2^20) "
-                                   "+ 10% INF=2^30 (BASELINE.json configs[1])",
-                       "plan": plan_desc, "l2": "inputs 2 x 256 MiB > 126 MB L2 (no flush)",
-                       "ops_per_step": OPS_PER_STEP},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_max, "unit": "Top/s",
-                         "frac": achieved / peak_max,
-                         "peak_source": (f"live VIADDMNMX.U32 probe: {tpc:.2f} terms/clk/SM x 2 op x 148 SM "
-                                         f"x 1965 MHz max clock (probe ran at {probe_mhz:.0f} MHz)"),
-                         "peak_at_run_clock": (2 * tpc * 148 * clocks["sm_mhz"] / 1e6) if clocks.get("sm_mhz") else None,
-                         "traffic": traffic, "traffic_source": traffic_src,
-                         "algorithmic_bytes": ALG_BYTES},
+            "vs_baseline": None, "dtype": "u32" if cfg == 2 else "s32",
+            "data": f"synthetic (seeded numpy default_rng({1000 + cfg}), BASELINE cfg{cfg} distribution)",
+            "config": workload_config(cfg),
+            "plan": plan_desc,
+            "l2": f"inputs 2 x {n * n * 4 >> 20} MiB > 126 MB L2 (no flush)",
+            "ops_per_step": ops_per_step,
+            "roofline": roofline,
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
         }
+        if configs:
+            line["configs"] = configs
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
         print(json.dumps(line), flush=True)

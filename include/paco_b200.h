@@ -78,6 +78,8 @@ extern "C" {
 #define PACO_MM_REMOTE 4    /* C is peer memory (NVLink): fold with element atomics, not TMA */
 #define PACO_MM_PACO_PLAN 8 /* pieces == NULL: CTAs take the balanced PACO plan (paco_plan_cta over
                                148 x ctas_per_sm x 4 workers) instead of the tile grid (paco_cta_grid) */
+#define PACO_MM_SYS 16      /* with PACO_MM_ATOMIC: element folds at system scope (another GPU folds into
+                               the same C over NVLink); TMA bulk folds stay allowed (SIMT kernels only) */
 
 /* dtype ids for paco_lincomb */
 #define PACO_DT_F32 0
@@ -216,6 +218,14 @@ int paco_widen_u32_i64(int device, void* stream, const void* r32, int64_t ld_r, 
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,
                 int64_t width, int64_t rows);
 
+/* Parallel host memcpy (pitches and width in BYTES) between pageable and pinned
+ * host memory, `threads` participants (a persistent pool + the caller): the
+ * staging step that feeds paco_copy2d from the reference's pageable NumPy
+ * operands (matmul.py:342-366).  Synchronous; call without holding locks the
+ * pool could need.  */
+int paco_host_copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t rows,
+                     int threads);
+
 /* Device memory for buffers shared across processes (CUDA IPC) -- the only
  * allocation the library makes on a caller's behalf. */
 int paco_device_alloc(int device, size_t bytes, void** ptr);
@@ -233,6 +243,20 @@ int paco_enable_peer(int device, int peer);
  * measured terms per clock per SM and the SM clock (MHz) seen during the run. */
 int paco_alu_probe(int device, void* stream, int which, int iters, double* terms_per_clk_sm,
                    double* sm_mhz);
+
+/* Live kernel timing.  paco_kernel_timing(1) clears the record and starts
+ * bracketing every launch of the library with a CUDA event pair on its
+ * stream (0 stops); paco_kernel_timing_read synchronises the recorded events
+ * of one kernel family and returns their summed duration and launch count.
+ * Families: */
+#define PACO_KT_SIMT_MM 0     /* simt_mm_kernel / simt_mm_batch_kernel (tropical, integer, fp32, fp64) */
+#define PACO_KT_TC_GEMM 1     /* tc_gemm_kernel (tcgen05: bf16, 3xTF32) */
+#define PACO_KT_TF32_SPLIT 2  /* split_tf32_{n,t}_kernel (Strassen leaf operands) */
+#define PACO_KT_LINCOMB 3     /* lincomb_kernel (Strassen S/T/C sums) */
+#define PACO_KT_ELEMENTWISE 4 /* fold / fill / narrow / widen */
+#define PACO_KT_COUNT 5
+int paco_kernel_timing(int enable);
+int paco_kernel_timing_read(int family, double* ms_total, int64_t* launches);
 
 /* Diagnostics: while `device_buffer` (>= 10 x grid int64) is set, each
  * SIMT paco_mm CTA writes (smid, start ns, end ns, stage count, its piece

@@ -98,6 +98,49 @@ def measure(cfg: int, rows_per_proc: int, procs: int | None = None, repeat: int 
     }
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def measure_threaded(cfg: int, rows: int, threads: int | None = None) -> dict:
+    """The reference's shipped parallel mode on a row slab: mm_execute(
+    mm_one_piece_partition(rows, m, k, P), ..., mode="parallel") with P worker
+    threads (core.py:299-326; the one-piece plan is the product planner's,
+    byte-identical to the reference's by tests/test_plans.py), (min,+) int64."""
+    from paper_2011_01441_b200.cuboid import mm_one_piece_partition
+
+    threads = threads or len(os.sched_getaffinity(0))
+    A, B, kind = cfg_inputs(cfg, rows)
+    n, k = A.shape
+    m = B.shape[1]
+    plan = mm_one_piece_partition(n, m, k, threads)
+    if kind == "minplus":
+        A64, B64 = A.astype(np.int64), B.astype(np.int64)
+        C = np.full((n, m), PN.MINPLUS_INF, np.int64)
+        sem = "minplus"
+    elif kind == "maxplus":
+        A64, B64 = -A.astype(np.int64), -B.astype(np.int64)
+        C = np.full((n, m), PN.MINPLUS_INF, np.int64)
+        sem = "minplus"
+    else:
+        A64, B64, C, sem = A.astype(np.int64), B.astype(np.int64), np.zeros((n, m), np.int64), "int"
+    t0 = time.perf_counter()
+    PN.mm_execute_parallel(plan, A64, B64, C, sem)
+    wall = time.perf_counter() - t0
+    ops = 2.0 * n * m * k
+    return {"value": ops / wall / 1e9, "unit": "Gop/s", "cores": threads, "wall_s": wall,
+            "sample": (f"cfg{cfg}: {n} rows of A (full k={k}, m={m}), mm_execute(mm_one_piece_partition"
+                       f"({n}, {m}, {k}, {threads}), mode='parallel'): {threads} worker threads, 32^3 NumPy leaves "
+                       "(oracle/paco_numpy.py mm_execute_parallel; GIL-bound like the reference's own)")}
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", type=int, default=2)

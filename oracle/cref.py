@@ -35,6 +35,10 @@ def lib():
             subprocess.run([sys.executable, "-c",
                             "import __graft_entry__ as g; g.build_oracle()"], cwd=root, check=True)
         _lib = ctypes.CDLL(_LIB_PATH)
+        _lib.oracle_mm_rows_simple.restype = ctypes.c_int
+        _lib.oracle_mm_rows_simple.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                               ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                               ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
         _lib.oracle_mm_rows.restype = ctypes.c_int
         _lib.oracle_mm_rows.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
@@ -42,7 +46,9 @@ def lib():
     return _lib
 
 
-def mm(sr: int, A: np.ndarray, B: np.ndarray, C: np.ndarray, threads: int | None = None) -> np.ndarray:
+def mm(sr: int, A: np.ndarray, B: np.ndarray, C: np.ndarray, threads: int | None = None,
+       simple: bool = False) -> np.ndarray:
+    """C (+)= A (x) B in place; ``simple`` forces the plain loop (no cache blocking)."""
     n, k = A.shape
     k2, m = B.shape
     assert k == k2 and C.shape == (n, m), (A.shape, B.shape, C.shape)
@@ -51,7 +57,8 @@ def mm(sr: int, A: np.ndarray, B: np.ndarray, C: np.ndarray, threads: int | None
     assert C.dtype == _OUT[sr] and C.flags["C_CONTIGUOUS"], (C.dtype, C.flags)
     if threads is not None:
         os.environ["OMP_NUM_THREADS"] = str(threads)
-    rc = lib().oracle_mm_rows(sr, A.ctypes.data, A.strides[0] // A.itemsize, B.ctypes.data,
+    fn = lib().oracle_mm_rows_simple if simple else lib().oracle_mm_rows
+    rc = fn(sr, A.ctypes.data, A.strides[0] // A.itemsize, B.ctypes.data,
                               B.strides[0] // B.itemsize, C.ctypes.data, C.strides[0] // C.itemsize,
                               n, m, k, 0, n)
     assert rc == 0, f"oracle rc={rc}"

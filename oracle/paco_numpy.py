@@ -9,6 +9,10 @@ CPU baseline in bench.py, and a second oracle for tests):
 * ``mm_execute_serial``               -- matmul.py:417-462 in serial order:
   temps filled with zero, COMPUTE -> mm_seq into C or a temp view, REDUCE ->
   copyto(t, vadd(t, temp)) then temp.fill(zero)
+* ``mm_execute_parallel``             -- the same runner from one host thread
+  per worker, each task after its dependencies (core.py:299-326: a REDUCE
+  runs on its first worker's thread), i.e. the reference's shipped
+  ``mode="parallel"``
 * ``strassen``                        -- the spec'd (absent) strassen_seq,
   SPEC.md:490-498 + PAPER.md:1839-1852, float64 or int64 ring, fixed levels
 
@@ -90,6 +94,57 @@ def mm_execute_serial(plan, A, B, C, semiring: str = "int") -> None:
             view = target[oi:oi + n, oj:oj + m]
             np.copyto(view, vadd(view, temps[bid]))
             temps[bid].fill(zero)
+
+
+def _runner(plan, A, B, C, semiring):
+    dtype, zero, block, vadd = SEMIRINGS[semiring]
+    reduces = plan.meta["reduces"]
+    shapes = {spec[0]: (spec[4], spec[5]) for spec in reduces.values()}
+    temps = {bid: np.full(shapes[bid], zero, dtype=dtype) for bid in plan.meta["temp_sizes"]}
+    base = plan.meta.get("base") or 32
+
+    def run(t):
+        if t.kind == "compute":
+            c = t.region
+            out = C if c.out == 0 else temps[c.out]
+            mm_seq(A[c.i0:c.i0 + c.n, c.l0:c.l0 + c.k], B[c.l0:c.l0 + c.k, c.j0:c.j0 + c.m],
+                   out[c.out_i0:c.out_i0 + c.n, c.out_j0:c.out_j0 + c.m], semiring, base)
+        elif t.kind == "reduce":
+            bid, tgt, oi, oj, n, m = reduces[t.id]
+            target = C if tgt == 0 else temps[tgt]
+            view = target[oi:oi + n, oj:oj + m]
+            np.copyto(view, vadd(view, temps[bid]))
+            temps[bid].fill(zero)
+    return run
+
+
+def mm_execute_parallel(plan, A, B, C, semiring: str = "int") -> None:
+    """core.py:299-326 restated: worker threads, dependency events, first error re-raised."""
+    import threading
+
+    run = _runner(plan, A, B, C, semiring)
+    done = [threading.Event() for _ in plan.tasks]
+    mine = [[t for t in plan.tasks if t.workers()[0] == w] for w in range(plan.p)]
+    errors = []
+
+    def loop(w):
+        for t in mine[w]:
+            for d in t.deps:
+                done[d].wait()
+            if not errors:
+                try:
+                    run(t)
+                except BaseException as exc:  # noqa: BLE001 -- re-raised after the join
+                    errors.append(exc)
+            done[t.id].set()
+
+    ths = [threading.Thread(target=loop, args=(w,)) for w in range(plan.p)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    if errors:
+        raise errors[0]
 
 
 def minplus_sat(A32, B32, C32):

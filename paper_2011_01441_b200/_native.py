@@ -31,10 +31,14 @@ SR_COUNT = 10
 
 DT_F32, DT_F64, DT_I64 = 0, 1, 2
 
+# kernel families of paco_kernel_timing_read
+KT_SIMT_MM, KT_TC_GEMM, KT_TF32_SPLIT, KT_LINCOMB, KT_ELEMENTWISE = 0, 1, 2, 3, 4
+
 MM_OVERWRITE = 1
 MM_ATOMIC = 2
 MM_REMOTE = 4
 MM_PACO_PLAN = 8
+MM_SYS = 16
 FOLD_RESET = 1
 FOLD_ATOMIC = 2
 TROPICAL_INF = 1 << 30
@@ -72,6 +76,7 @@ SIGNATURES = {
                                     ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
     "paco_narrow_i64": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _int, _vp]),
     "paco_widen_u32_i64": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
+    "paco_host_copy2d": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _int]),
     "paco_copy2d": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_device_alloc": (_int, [_int, ctypes.c_size_t, ctypes.POINTER(_vp)]),
     "paco_device_free": (_int, [_int, _vp]),
@@ -82,6 +87,8 @@ SIGNATURES = {
     "paco_alu_probe": (_int, [_int, _vp, _int, _int, ctypes.POINTER(ctypes.c_double),
                               ctypes.POINTER(ctypes.c_double)]),
     "paco_debug_trace": (_int, [_vp]),
+    "paco_kernel_timing": (_int, [_int]),
+    "paco_kernel_timing_read": (_int, [_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]),
     "paco_last_error": (ctypes.c_char_p, []),
     "paco_abi_version": (_int, []),
 }
@@ -209,3 +216,23 @@ def pieces_array(pieces):
         raise PlanError(f"{len(pieces)} CTA pieces exceed PACO_MAX_PIECES={MAX_PIECES}")
     flat = [int(v) for pc in pieces for v in pc]
     return (ctypes.c_int32 * len(flat))(*flat), len(pieces)
+
+
+class kernel_timing:
+    """Context manager: live CUDA-event timing of the library's own launches.
+
+    ``with kernel_timing() as kt: ...`` then ``kt.read(KT_TC_GEMM)`` ->
+    (summed ms, launches) of that kernel family inside the block."""
+
+    def __enter__(self):
+        check(load().paco_kernel_timing(1))
+        return self
+
+    def __exit__(self, *exc):
+        check(load().paco_kernel_timing(0))
+
+    @staticmethod
+    def read(family: int) -> tuple[float, int]:
+        ms, cnt = ctypes.c_double(), _i64()
+        check(load().paco_kernel_timing_read(family, ctypes.byref(ms), ctypes.byref(cnt)))
+        return ms.value, cnt.value

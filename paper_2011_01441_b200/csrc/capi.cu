@@ -2,8 +2,10 @@
 // Validates arguments, selects the device, maps semirings to kernels and
 // reports errors through return codes + a thread-local message.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include <cuda.h>
@@ -13,6 +15,46 @@
 namespace paco {
 
 static thread_local char g_err[512] = "";
+
+std::atomic<int> g_ktime_on{0};
+
+namespace {
+struct KRec {
+  cudaEvent_t a = nullptr, b = nullptr;
+  int fam = 0;
+  int dev = 0;
+};
+std::mutex g_kt_mu;
+std::vector<KRec> g_kt_recs;
+thread_local std::vector<size_t> t_kt_open;  // records opened by this thread, innermost last
+}  // namespace
+
+void ktime_record(int family, cudaStream_t st, bool start) {
+  if (start) {
+    KRec r;
+    r.fam = family;
+    cudaGetDevice(&r.dev);
+    if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
+    cudaEventRecord(r.a, st);
+    std::lock_guard<std::mutex> lock(g_kt_mu);
+    g_kt_recs.push_back(r);
+    t_kt_open.push_back(g_kt_recs.size() - 1);
+  } else {
+    if (t_kt_open.empty()) return;
+    std::lock_guard<std::mutex> lock(g_kt_mu);
+    const size_t idx = t_kt_open.back();
+    t_kt_open.pop_back();
+    if (idx < g_kt_recs.size()) cudaEventRecord(g_kt_recs[idx].b, st);
+  }
+}
+
+const char* dev_knob(const char* name) {
+  static const bool on = [] {
+    const char* e = getenv("PACO_DEV_KNOBS");
+    return e && e[0] == '1';
+  }();
+  return on ? getenv(name) : nullptr;
+}
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -344,6 +386,42 @@ int paco_widen_u32_i64(int device, void* stream, const void* r32, int64_t ld_r, 
   DeviceGuard dg;
   PACO_TRY(dg.use(device));
   return launch_widen_u32_i64(static_cast<cudaStream_t>(stream), r32, ld_r, c, ld_c, rows, cols);
+}
+
+int paco_kernel_timing(int enable) {
+  std::lock_guard<std::mutex> lock(g_kt_mu);
+  if (enable) {
+    for (KRec& r : g_kt_recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    g_kt_recs.clear();
+  }
+  g_ktime_on.store(enable ? 1 : 0);
+  return PACO_OK;
+}
+
+int paco_kernel_timing_read(int family, double* ms_total, int64_t* launches) {
+  if (!ms_total || !launches || family < 0 || family >= PACO_KT_COUNT) {
+    set_error("paco_kernel_timing_read: family %d (0..%d) and output pointers", family, PACO_KT_COUNT - 1);
+    return PACO_ERR_ARG;
+  }
+  std::lock_guard<std::mutex> lock(g_kt_mu);
+  double tot = 0;
+  int64_t cnt = 0;
+  for (KRec& r : g_kt_recs) {
+    if (r.fam != family) continue;
+    DeviceGuard dg;
+    PACO_TRY(dg.use(r.dev));
+    PACO_CUDA_TRY(cudaEventSynchronize(r.b));
+    float ms = 0;
+    PACO_CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
+    tot += ms;
+    ++cnt;
+  }
+  *ms_total = tot;
+  *launches = cnt;
+  return PACO_OK;
 }
 
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,

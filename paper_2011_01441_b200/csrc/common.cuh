@@ -1,5 +1,6 @@
 // Shared definitions for the sm_100a PACO semiring-MM library.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -32,6 +33,29 @@ extern long long* g_trace_buffer;
 
 // thread-local error text behind paco_last_error()
 void set_error(const char* fmt, ...);
+
+// Developer tuning knobs (CTA-plan overrides, kernel ablations, ...): read from
+// the environment ONLY when PACO_DEV_KNOBS=1, so an ordinary user environment
+// can never select an unmeasured configuration.  nullptr when unset or gated.
+const char* dev_knob(const char* name);
+
+// Live per-kernel timing (paco_kernel_timing): while on, every launch site
+// brackets its kernel with a CUDA event pair on the launching stream, so a
+// caller can measure the dominant kernel's average duration inside a real
+// multi-kernel step (bench.py's roofline).  Off: one relaxed atomic load.
+extern std::atomic<int> g_ktime_on;
+void ktime_record(int family, cudaStream_t st, bool start);
+struct KernelSpan {
+  int fam;
+  cudaStream_t st;
+  bool on;
+  KernelSpan(int f, cudaStream_t s) : fam(f), st(s), on(g_ktime_on.load(std::memory_order_relaxed) != 0) {
+    if (on) ktime_record(fam, st, true);
+  }
+  ~KernelSpan() {
+    if (on) ktime_record(fam, st, false);
+  }
+};
 
 #define PACO_CUDA_TRY(expr)                                                     \
   do {                                                                          \

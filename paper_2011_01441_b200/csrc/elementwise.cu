@@ -156,6 +156,7 @@ int launch_fold(int sr, cudaStream_t st, void* dst, int64_t ldd, void* src, int6
     using TC = typename Op::TC;
     const int64_t xb = (m + 255) / 256, yb0 = n < 65535 ? n : 65535, ycap = 2368 / xb + 1;
     const dim3 grid(unsigned(xb), unsigned(yb0 < ycap ? yb0 : ycap));
+    KernelSpan ks(PACO_KT_ELEMENTWISE, st);
     fold_kernel<Op><<<grid, 256, 0, st>>>(static_cast<TC*>(dst), ldd, static_cast<TC*>(src), lds, n, m, flags);
     PACO_CUDA_TRY(cudaGetLastError());
     return PACO_OK;
@@ -176,6 +177,7 @@ int launch_fill(int sr, cudaStream_t st, void* dst, int64_t ld, int64_t n, int64
       PACO_CUDA_TRY(cudaMemset2DAsync(dst, size_t(ld) * sizeof(TC), 0, size_t(m) * sizeof(TC), size_t(n), st));
       return PACO_OK;
     }
+    KernelSpan ks(PACO_KT_ELEMENTWISE, st);
     fill_kernel<Op><<<ew_grid(n * m, 256), 256, 0, st>>>(static_cast<TC*>(dst), ld, n, m);
     PACO_CUDA_TRY(cudaGetLastError());
     return PACO_OK;
@@ -218,6 +220,7 @@ int lincomb_t(cudaStream_t st, void* out, int64_t ldo, int64_t n, int64_t m, int
   const int64_t yb = n < 65535 ? n : 65535;
   const int64_t ycap = 2368 / xb + 1;
   dim3 grid(unsigned(xb), unsigned(yb < ycap ? yb : ycap));
+  KernelSpan ks(PACO_KT_LINCOMB, st);
   if (vec)
     lincomb_kernel<T, 4, true><<<grid, 128, 0, st>>>(static_cast<T*>(out), ldo, n, m, a, nin, acc);
   else
@@ -287,6 +290,7 @@ dim3 rows_grid(int64_t n, int64_t m, int per_block) {
 int launch_narrow_i64(cudaStream_t st, const int64_t* src, int64_t lds, void* dst, int64_t ldd, int64_t n,
                       int64_t m, int64_t lo, int64_t hi, int saturate, int32_t* flag) {
   if (n <= 0 || m <= 0) return PACO_OK;
+  KernelSpan ks(PACO_KT_ELEMENTWISE, st);
   narrow_i64_kernel<<<rows_grid(n, m, 512), 256, 0, st>>>(src, lds, static_cast<uint32_t*>(dst), ldd, n, m, lo,
                                                            hi, saturate, flag);
   PACO_CUDA_TRY(cudaGetLastError());
@@ -296,6 +300,7 @@ int launch_narrow_i64(cudaStream_t st, const int64_t* src, int64_t lds, void* ds
 int launch_widen_u32_i64(cudaStream_t st, const void* r, int64_t ldr, int64_t* c, int64_t ldc, int64_t n,
                          int64_t m) {
   if (n <= 0 || m <= 0) return PACO_OK;
+  KernelSpan ks(PACO_KT_ELEMENTWISE, st);
   widen_u32_i64_kernel<<<rows_grid(n, m, 256), 256, 0, st>>>(static_cast<const uint32_t*>(r), ldr, c, ldc, n, m);
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;

@@ -740,7 +740,7 @@ bool plan_pieces(int64_t n, int64_t m, int64_t k, int p, std::vector<Box>& out) 
 double plan_kw() {
   static double kw = -1.0;
   if (kw < 0.0) {
-    const char* e = getenv("PACO_CTA_KW");
+    const char* e = dev_knob("PACO_CTA_KW");
     kw = e ? atof(e) : kDefaultKw;
   }
   return kw;
@@ -766,7 +766,7 @@ bool plan_pieces_balanced(int64_t n, int64_t m, int64_t k, int bm, int bn, int k
 int default_pieces(int ctas_per_sm) {
   static int env = -1;
   if (env < 0) {
-    const char* e = getenv("PACO_CTA_PIECES");
+    const char* e = dev_knob("PACO_CTA_PIECES");
     env = e ? atoi(e) : 0;
   }
   return env > 0 ? env : kNumSMs * ctas_per_sm * kDefaultWaves;
@@ -789,9 +789,9 @@ struct GridPlan {
 GridPlan grid_plan(const int64_t units[3], int kq) {
   static int env = -1, env_tail = -2;
   if (env < 0) {
-    const char* e = getenv("PACO_CTA_KSPLIT");
+    const char* e = dev_knob("PACO_CTA_KSPLIT");
     env = e ? atoi(e) : 0;
-    const char* t = getenv("PACO_CTA_TAIL");  // 0/1: no tail split; > 1: forced
+    const char* t = dev_knob("PACO_CTA_TAIL");  // 0/1: no tail split; > 1: forced
     env_tail = t ? atoi(t) : -1;
   }
   const int64_t tiles = units[0] * units[1];
@@ -977,7 +977,7 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
               (reinterpret_cast<uintptr_t>(C) % 16 == 0 && (ldc * sizeof(typename Op::TC)) % 16 == 0 &&
                !(flags & PACO_MM_REMOTE)) ? 1 : 0,
               (flags & (PACO_MM_ATOMIC | PACO_MM_REMOTE)) ? 1 : 0, plan_kw()};
-  args.sys_atomic = (flags & PACO_MM_REMOTE) ? 1 : 0;
+  args.sys_atomic = (flags & (PACO_MM_REMOTE | PACO_MM_SYS)) ? 1 : 0;
   if (args.overwrite && (flags & (PACO_MM_ATOMIC | PACO_MM_REMOTE))) {
     set_error("PACO_MM_OVERWRITE cannot be combined with atomic / remote folding");
     return PACO_ERR_ARG;
@@ -992,7 +992,10 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
                    ((lda * sizeof(typename Op::TA)) % 16 == 0) && ((ldb * sizeof(typename Op::TB)) % 16 == 0);
   auto kern = vec ? simt_mm_kernel<Op, true> : simt_mm_kernel<Op, false>;
   PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, stream>>>(args, table);
+  {
+    KernelSpan ks(PACO_KT_SIMT_MM, stream);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, stream>>>(args, table);
+  }
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;
 }
@@ -1041,6 +1044,7 @@ int launch_simt_batch(int device, cudaStream_t stream, int count, const paco_mm_
              g_trace_buffer,
              (reinterpret_cast<uintptr_t>(P.C) % 16 == 0 && (P.ldc * sizeof(typename Op::TC)) % 16 == 0) ? 1 : 0,
              (P.flags & PACO_MM_ATOMIC) ? 1 : 0, plan_kw()};
+    a.sys_atomic = (P.flags & PACO_MM_SYS) ? 1 : 0;
     if (a.overwrite && (s > 1 || g.tail > 1)) {  // k-split pieces fold into C: it must hold the semiring zero first
       const int rc = paco_fill(device, stream, Op::kId, P.C, P.ldc, P.n, P.m);
       if (rc) return rc;
@@ -1064,7 +1068,10 @@ int launch_simt_batch(int device, cudaStream_t stream, int count, const paco_mm_
   }
   auto kern = vec ? simt_mm_batch_kernel<Op, true> : simt_mm_batch_kernel<Op, false>;
   PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
-  kern<<<unsigned(total), Cfg::THREADS, Cfg::SMEM, stream>>>(bt);
+  {
+    KernelSpan ks(PACO_KT_SIMT_MM, stream);
+    kern<<<unsigned(total), Cfg::THREADS, Cfg::SMEM, stream>>>(bt);
+  }
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;
 }

@@ -760,7 +760,7 @@ struct Scratch {
 // consecutive launches on a stream need no memset, and launches on different
 // streams (the parallel executors) never share counters.
 // PDL on the tcgen05 launches (PACO_TC_PDL=0 turns it off)
-static const bool kPdl = !getenv("PACO_TC_PDL") || atoi(getenv("PACO_TC_PDL")) != 0;
+static const bool kPdl = !dev_knob("PACO_TC_PDL") || atoi(dev_knob("PACO_TC_PDL")) != 0;
 
 int stream_counters(int device, cudaStream_t st, int32_t** out) {
   static std::mutex mu;
@@ -1037,6 +1037,7 @@ int repack(int device, Scratch& sc, const void** p, int64_t* ld, int64_t rows, i
 int launch_split(const tc::SplitIn& in, int64_t rows, int64_t cols, bool transpose, float* h, float* l,
                  int64_t ldo, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return PACO_OK;
+  KernelSpan ks(PACO_KT_TF32_SPLIT, st);
   bool vec = (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(h) % 16 == 0) &&
              (reinterpret_cast<uintptr_t>(l) % 16 == 0);
   for (int q = 0; q < in.nin; ++q)
@@ -1158,7 +1159,7 @@ int check_tc_call(void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const i
     set_error("tcgen05 path: extents must fit int32");
     return PACO_ERR_ARG;
   }
-  if ((flags & PACO_MM_REMOTE) || ((flags & PACO_MM_ATOMIC) && !c_ok(C, ldc, m))) {
+  if ((flags & (PACO_MM_REMOTE | PACO_MM_SYS)) || ((flags & PACO_MM_ATOMIC) && !c_ok(C, ldc, m))) {
     // the TMA reduce-add epilogue is atomic, but only on local C with a TMA-able pitch
     set_error("tcgen05 path: atomic folding needs a local C with a 16-byte aligned start, pitch and row length");
     return PACO_ERR_UNSUPPORTED;
@@ -1185,7 +1186,7 @@ int run_tc(int device, Scratch& sc, cudaStream_t stream, const tc::TcMaps& maps,
   args.tiles_nb = int32_t((m + K::BN - 1) / K::BN);
   args.kblocks = int32_t((k + K::BK - 1) / K::BK);
   {
-    static const int ablate = getenv("PACO_TC_ABLATE") ? atoi(getenv("PACO_TC_ABLATE")) : 0;
+    static const int ablate = dev_knob("PACO_TC_ABLATE") ? atoi(dev_knob("PACO_TC_ABLATE")) : 0;
     args.ablate = ablate;
     args.trace = g_trace_buffer;
   }
@@ -1231,6 +1232,7 @@ int run_tc(int device, Scratch& sc, cudaStream_t stream, const tc::TcMaps& maps,
     attr[0].val.programmaticStreamSerializationAllowed = kPdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    KernelSpan ks(PACO_KT_TC_GEMM, stream);
     PACO_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps, args));
   }
   PACO_CUDA_TRY(cudaGetLastError());
@@ -1282,6 +1284,12 @@ int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* 
     set_error("paco_mm_tf32x3: count=%d (1..%d)", count, tc::kMaxBatch);
     return PACO_ERR_ARG;
   }
+#if !PACO_EPI_RING
+  if (ndst) {  // only the staging-ring epilogue walks the destination list and applies the signs
+    set_error("paco_mm_tf32x3_multi: this build's epilogue (PACO_EPI_RING=0) has no multi-destination fold");
+    return PACO_ERR_UNSUPPORTED;
+  }
+#endif
   for (int q = 0; q < count; ++q) {
     const int nd = ndst ? ndst[q] : 1;
     if (nd < 1 || nd > 4) {
@@ -1323,7 +1331,7 @@ int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* 
 // pays when the batch has enough tiles for the 148 SMs (4096^3 alone: 512
 // tiles = 3.5 per SM).  PACO_TF32_V=0/1 forces 128/256.
 bool tf32_wide(int64_t n, int64_t m, int count) {
-  static const int v = getenv("PACO_TF32_V") ? atoi(getenv("PACO_TF32_V")) : -1;
+  static const int v = dev_knob("PACO_TF32_V") ? atoi(dev_knob("PACO_TF32_V")) : -1;
   if (v >= 0) return v != 0;
   return ((n + 127) / 128) * ((m + 255) / 256) * count >= 6 * kNumSMs;
 }
@@ -1335,7 +1343,7 @@ int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t ld
   // 16-column boxes -- measured best of 10 layouts (ring depth 2-8, staging
   // buffers 1-4 per warp, 16/32-column boxes, N = 128 tiles: 58 vs 59.5-84 us;
   // DESIGN.md section 6); PACO_TC_RESV=-1 forces the streaming kind.
-  static const int resv = getenv("PACO_TC_RESV") ? atoi(getenv("PACO_TC_RESV")) : 7;
+  static const int resv = dev_knob("PACO_TC_RESV") ? atoi(dev_knob("PACO_TC_RESV")) : 7;
 #define PACO_TC_GO(KIND) return launch_tc<KIND>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags)
   if (k <= 256 && resv >= 0) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<PACO_RES_AST, PACO_RES_EB, 8, PACO_RES_EC>));
 #undef PACO_TC_GO

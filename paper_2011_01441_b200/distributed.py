@@ -225,13 +225,13 @@ class FusedDistributedMM:
     owners (element atomics, ``PACO_MM_REMOTE``), locally with the TMA bulk
     reduction -- so the plan's REDUCE tasks vanish: no temporaries, no fold
     pass, no NCCL call on the data path.  Remote folds use the TMA bulk
-    reduction too when ``PACO_REMOTE_BULK=1`` and a start-up probe shows it
+    reduction too when ``remote_bulk=True`` and a start-up probe shows it
     lands correctly in peer memory (``remote_bulk``).  Construct on every rank (it exchanges IPC
     handles with ``all_gather_object``).
     """
 
     def __init__(self, plan: Plan, semiring, kernel_id: int, device: int, *, group=None,
-                 fold_style: str | None = None):
+                 fold_style: str = "atomic", remote_bulk: bool = False):
         import ctypes
         import os
 
@@ -276,14 +276,29 @@ class FusedDistributedMM:
         self.exchange = any(o != r for r in range(self.world) for _, _, o, _ in fused_launches(plan, r)[1])
         # remote folds: "atomic" (default) = the kernel's epilogue folds each
         # finished tile straight into the owner's C over NVLink (element atomics,
-        # or TMA bulk reductions with PACO_REMOTE_BULK=1) -- compute and transfer
+        # or TMA bulk reductions with remote_bulk=True) -- compute and transfer
         # overlap tile by tile, ~1/p of C spread over the whole kernel; "stage" =
         # compute into a local temporary, one bulk copy into a staging slot in the
         # owner's memory (IPC), the owner folds it after a barrier.
-        self.fold_style = fold_style or os.environ.get("PACO_FOLD_STYLE", "atomic")
+        self.fold_style = fold_style
         if self.fold_style not in ("stage", "atomic"):
             raise ValueError(f"fold_style must be 'stage' or 'atomic', got {self.fold_style!r}")
-        self.remote_bulk = self._probe_remote_bulk() if self.fold_style == "atomic" else False
+        from .mm import _TC_KERNELS
+        if kernel_id in _TC_KERNELS:
+            # the tcgen05 epilogue folds only into local C (TMA reduce-add): a
+            # remote owner's share goes through a staged block
+            self.fold_style = "stage"
+        self.remote_bulk = self._probe_remote_bulk() if self.fold_style == "atomic" and remote_bulk else False
+        # C rectangles of mine that another rank folds into over NVLink: the
+        # owner's own folds there must be atomic w.r.t. the peer's at system
+        # scope too, so those launches use system-scope element atomics
+        # (MM_REMOTE semantics on local memory) -- or, when remote folds are TMA
+        # bulk reductions, the same bulk path with system-scope element edges
+        incoming_rects = [rect for r in range(self.world) if r != self.rank
+                          for _, _, o, rect in fused_launches(plan, r)[1] if o == self.rank]
+        self.shared = [owner == self.rank and self.fold_style == "atomic"
+                       and any(_rect_intersect(rect, ir) for ir in incoming_rects)
+                       for _, _, owner, rect in self.launches]
         self._setup_staging()
 
     def _setup_staging(self) -> None:
@@ -345,12 +360,9 @@ class FusedDistributedMM:
         from .device import View
         from .mm import launch_fill, launch_mm
 
-        import os
-        # Off unless asked for: a TMA bulk reduction that the fabric rejected
-        # would leave a sticky CUDA error, and element atomics over NVLink are
-        # always legal for peer-mapped memory.
-        if os.environ.get("PACO_REMOTE_BULK", "0") != "1":
-            return False
+        # Off unless asked for (remote_bulk=True): a TMA bulk reduction that the
+        # fabric rejected would leave a sticky CUDA error, and element atomics
+        # over NVLink are always legal for peer-mapped memory.
         if self.world == 1 or self.n < 128 or self.m < 128:
             return False
         dev = self.device
@@ -382,6 +394,13 @@ class FusedDistributedMM:
         flags = [None] * self.world
         dist.all_gather_object(flags, ok, group=self.group)
         return all(flags)
+
+    def _flags(self, j: int, owner: int) -> int:
+        """Fold flags of launch j: remote or shared-with-a-peer folds at system scope."""
+        nat = self.nat
+        if owner != self.rank or self.shared[j]:
+            return nat.MM_ATOMIC | (nat.MM_SYS if self.remote_bulk else nat.MM_REMOTE)
+        return nat.MM_ATOMIC
 
     def _fill_owned(self, st) -> None:
         """Semiring zero into the owned rectangles only (every fold, local or
@@ -417,9 +436,8 @@ class FusedDistributedMM:
                 self.nat.check(self.nat.load().paco_copy2d(self.device, st.cuda_stream, slot, cm * es, t.data_ptr(),
                                                            t.stride(0) * es, cm * es, cn))
                 continue
-            remote = owner != self.rank and not self.remote_bulk
-            flags = self.nat.MM_ATOMIC | (self.nat.MM_REMOTE if remote else 0)
-            launch_mm(self.kid, st, a, b, self.views[owner].sub(ci, cj, cn, cm), flags=flags, device=self.device)
+            launch_mm(self.kid, st, a, b, self.views[owner].sub(ci, cj, cn, cm), flags=self._flags(j, owner),
+                      device=self.device)
         if not self.exchange:
             return
         torch.cuda.synchronize(self.device)
@@ -498,8 +516,7 @@ class FusedDistributedMM:
                     self.nat.check(self.nat.load().paco_copy2d(dev, st.cuda_stream, slot, cm * es, t.data_ptr(),
                                                                t.stride(0) * es, cm * es, cn))
                     continue
-                remote = owner != self.rank and not self.remote_bulk
-                flags = self.nat.MM_ATOMIC | (self.nat.MM_REMOTE if remote else 0)
+                flags = self._flags(j, owner)
                 if streamed and len(spans) > 1 and (l0, l1) == spans[-1] and an >= 2 * _PIPE_MIN_ROWS:
                     R = max(1, min(16, an // _PIPE_MIN_ROWS))
                     redges = [((an * i // R) // 128) * 128 for i in range(R)] + [an]

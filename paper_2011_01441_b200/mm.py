@@ -179,13 +179,15 @@ def mm_seq(A, B, C, semiring: Semiring = SEMIRING_INT, base: int = DEFAULT_BASE,
                     nw.minplus = False
                 nw.finish(st)
             return
-        if pieces is None and _pinned_host(A, in_dt) and _pinned_host(B, in_dt) \
-                and _pinned_host(C, semiring.dtype) and n >= 2 * _PIPE_MIN_ROWS:
-            mode = _PIPE_MODE or ("k" if k >= 4 * _PIPE_MIN_K else "grid")
-            if mode == "k":
+        pinned = _pinned_host(A, in_dt) and _pinned_host(B, in_dt) and _pinned_host(C, semiring.dtype)
+        if pieces is None and n >= 2 * _PIPE_MIN_ROWS and (pinned or (
+                _numpy_host(A, in_dt) and _numpy_host(B, in_dt) and _numpy_host(C, semiring.dtype))):
+            if k >= 4 * _PIPE_MIN_K:
                 _kphased_host_mm(A, B, C, kid, dev, st, overwrite)
-            else:
+            elif pinned:
                 _pipelined_host_mm(A, B, C, kid, semiring, dev, st, overwrite)
+            else:
+                _kphased_host_mm(A, B, C, kid, dev, st, overwrite, front_share=0.0)
             return
         with torch.cuda.stream(st):
             a = View.of(stage_in(A, in_dt, dev))
@@ -196,17 +198,52 @@ def mm_seq(A, B, C, semiring: Semiring = SEMIRING_INT, base: int = DEFAULT_BASE,
 
 
 _PIPE_MIN_ROWS = 512
-_PIPE_GRID = tuple(int(x) for x in os.environ.get("PACO_PIPE_GRID", "4,2").split(","))  # measured best of 4x4/8x1/4x2/2x4/8x2 for 8192^3
-_PIPE_MODE = os.environ.get("PACO_PIPE_MODE", "")          # "k" | "grid" | "" (auto)
+_PIPE_GRID = (4, 2)  # 2-D block grid for short k: measured best of 4x4/8x1/4x2/2x4/8x2 for 8192^3
 _PIPE_MIN_K = 512
 # k-phased schedule: first k chunk, growth factor, chunk cap, share of k in the
-# row-blocked last phase, and its number of row blocks
-_KP = tuple(float(x) for x in os.environ.get("PACO_PIPE_KP", "128,2,2048,0.25,16").split(","))
+# row-blocked last phase, and its number of row blocks (tools/kp_sweep.py:
+# within 0.3 % of the best of eight shapes on 8192^3)
+_KP = (128, 2, 2048, 0.25, 16)
+# staged (pageable NumPy) operands: every chunk costs a host copy before its
+# DMA, so the chunks grow more slowly (growth <= compute rate / staging rate
+# keeps the GPU fed) and each chunk's staging is cut into ~8 MiB row parts whose
+# DMAs start while the next part is being copied
+_KP_STAGED = (128, 1.5, 2048, 0.25, 16)
+_STAGE_PART_BYTES = 8 << 20
 
 
 def _pinned_host(x, dtype) -> bool:
     return (isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.is_contiguous()
             and x.dtype == torch_dtype(dtype))
+
+
+def _numpy_host(x, dtype) -> bool:
+    """A pageable NumPy matrix the pipeline can stage (unit column stride, exact dtype)."""
+    return (isinstance(x, np.ndarray) and x.ndim == 2 and x.dtype == np.dtype(dtype) and x.dtype != object
+            and (x.shape[1] <= 1 or x.strides[1] == x.itemsize) and x.dtype.itemsize in (4, 8))
+
+
+# Participants of the native staging memcpy (paco_host_copy2d).  Measured on the
+# 16-core GPU host (tools/e2e_numpy_timeline.py, cfg2 NumPy e2e): 4/6/8/12/16
+# threads -> 53.7/42.5/36.6/33.9/34.1 ms per call
+_HOST_THREADS = max(1, min(12, (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 16) * 3 // 4))
+
+
+def _host_copy(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[...] = src for equal-shape 2-D row-major views (unit column stride),
+    by the library's native parallel memcpy (paco_host_copy2d, GIL released)."""
+    assert dst.shape == src.shape and dst.itemsize == src.itemsize, (dst.shape, src.shape)
+    if dst.size == 0:
+        return
+    rows, cols = dst.shape
+    nat.check(nat.load().paco_host_copy2d(dst.ctypes.data, dst.strides[0] if rows > 1 else cols * dst.itemsize,
+                                          src.ctypes.data, src.strides[0] if rows > 1 else cols * src.itemsize,
+                                          cols * dst.itemsize, rows, _HOST_THREADS))
+
+
+def _pinned_like(shape, dtype) -> torch.Tensor:
+    """Pinned staging buffer (PyTorch's caching host allocator keeps it for the next call)."""
+    return torch.empty(tuple(shape), dtype=torch_dtype(dtype), pin_memory=True)
 
 
 def _copy2d(stream, dst: torch.Tensor, dr0: int, dc0: int, src: torch.Tensor, sr0: int, sc0: int,
@@ -283,10 +320,10 @@ def _pipelined_host_mm(A, B, C, kid: int, semiring: Semiring, dev: int, st, over
     d2h.synchronize()
 
 
-def _kphased_edges(k: int) -> tuple[list[int], int]:
+def _kphased_edges(k: int, kp: tuple = _KP) -> tuple[list[int], int]:
     """k-chunk edges of the front phase (geometric growth from a small first
     chunk, capped) and the start of the row-blocked last phase."""
-    first, growth, cap, share, _ = _KP
+    first, growth, cap, share, _ = kp
     align = 128
     last = min(k - align, max(align, -(-int(k * share) // align) * align))
     front = k - last
@@ -301,58 +338,91 @@ def _kphased_edges(k: int) -> tuple[list[int], int]:
     return edges, front
 
 
-def _kphased_host_mm(A, B, C, kid: int, dev: int, st, overwrite: bool) -> None:
-    """Host (pinned) operands with a long k: overlap H2D, compute and D2H by
-    cutting k first, rows last.
+def _kphased_host_mm(A, B, C, kid: int, dev: int, st, overwrite: bool, front_share: float | None = None) -> None:
+    """Host operands with a long k: overlap H2D, compute and D2H by cutting k
+    first, rows last.
 
-    Front phase: k chunks [l0, l1) of geometrically growing width; the H2D
-    stream uploads A[:, l0:l1] and B[l0:l1, :] and the compute stream runs the
+    Front phase: k chunks [l0, l1) of geometrically growing width; A[:, l0:l1]
+    and B[l0:l1, :] go up on the H2D stream and the compute stream runs the
     whole C (+)= A[:, l0:l1] (x) B[l0:l1, :] as soon as they land (the first
     chunk overwrites; C's upload queues behind every chunk's, hidden by the
-    front phase's compute, and is folded in with one (+) pass).  Last phase: the final k chunk row block by
-    row block, each block's rows of C returned by the D2H stream while the next
-    block computes.  So only the small first chunk's upload and the last row
-    block's download are exposed, versus a whole A row block + B column block
-    + C block for the 2-D grid (``_pipelined_host_mm``).  The semiring's (+)
-    is associative and commutative, so the result is the one-shot product
-    (integer/tropical bit-identical; float within its summation tolerance).
+    front phase's compute, and is folded in with one (+) pass).  Last phase:
+    the final k chunk row block by row block, each block's rows of C returned
+    by the D2H stream while the next block computes.  So only the small first
+    chunk's upload and the last row block's download are exposed.  The
+    semiring's (+) is associative and commutative, so the result is the
+    one-shot product (integer/tropical bit-identical; float within its
+    summation tolerance).
+
+    Pinned torch operands are DMA'd straight from host memory.  Pageable NumPy
+    operands (the reference's own calling convention, matmul.py:342-366) are
+    first copied chunk by chunk into pinned staging by the host thread pool --
+    each chunk's upload is enqueued as soon as it is staged, so the staging of
+    chunk i + 1 overlaps the DMA and compute of chunk i -- and C's row blocks
+    are copied out of pinned staging while later blocks still compute.
+    ``front_share`` (default the schedule's 0.75) = 0 skips the k chunks (short k).
     """
     n, k = tuple(A.shape)
     m = B.shape[1]
-    edges, front = _kphased_edges(k)
+    staged = isinstance(A, np.ndarray)
+    if front_share is not None and front_share <= 0:
+        edges, front = [0], 0
+    else:
+        edges, front = _kphased_edges(k, _KP_STAGED if staged else _KP)
     R = max(1, min(int(_KP[4]), n // _PIPE_MIN_ROWS))
     redges = [((n * i // R) // 128) * 128 for i in range(R)] + [n]
     h2d = torch.cuda.Stream(device=dev)
     d2h = torch.cuda.Stream(device=dev)
     h2d.wait_stream(st)
-    a_d = torch.empty((n, k), dtype=A.dtype, device=dev)
-    b_d = torch.empty((k, m), dtype=B.dtype, device=dev)
-    c_d = torch.empty((n, m), dtype=C.dtype, device=dev)
-    c_in = None if overwrite else torch.empty((n, m), dtype=C.dtype, device=dev)
+    a_d = torch.empty((n, k), dtype=torch_dtype(A.dtype), device=dev)
+    b_d = torch.empty((k, m), dtype=torch_dtype(B.dtype), device=dev)
+    c_d = torch.empty((n, m), dtype=torch_dtype(C.dtype), device=dev)
+    c_in = None if overwrite or front == 0 else torch.empty((n, m), dtype=torch_dtype(C.dtype), device=dev)
     for t in (a_d, b_d, c_d, c_in):
         if t is not None:
             t.record_stream(h2d)
             t.record_stream(d2h)
-    av, bv, cv = View.of(a_d), View.of(b_d), View.of(c_d)
-    spans = list(zip(edges[:-1], edges[1:])) + [(front, k)]
-    landed, c_landed = [], None
-    for idx, (l0, l1) in enumerate(spans):
-        _copy2d(h2d, a_d, 0, l0, A, 0, l0, n, l1 - l0)
-        _copy2d(h2d, b_d, l0, 0, B, l0, 0, l1 - l0, m)
+    if staged:  # whole-operand pinned staging, filled chunk by chunk
+        a_s, b_s = _pinned_like(A.shape, A.dtype), _pinned_like(B.shape, B.dtype)
+        c_s = _pinned_like(C.shape, C.dtype)
+        a_sn, b_sn, c_sn = a_s.numpy(), b_s.numpy(), c_s.numpy()
+        A_src, B_src, C_src = a_s, b_s, c_s
+    else:
+        A_src, B_src, C_src = A, B, C
+
+    def upload(dst, r0, c0, rows, cols, src_t, src_np=None, host=None):
+        if staged:  # row parts: part i's DMA runs while part i + 1 is staged
+            parts = max(1, min(rows, rows * cols * host.itemsize // _STAGE_PART_BYTES))
+            cuts = [r0 + rows * i // parts for i in range(parts + 1)]
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                _host_copy(src_np[a:b, c0:c0 + cols], host[a:b, c0:c0 + cols])
+                _copy2d(h2d, dst, a, c0, src_t, a, c0, b - a, cols)
+        else:
+            _copy2d(h2d, dst, r0, c0, src_t, r0, c0, rows, cols)
         ev = torch.cuda.Event()
         ev.record(h2d)
-        landed.append(ev)
-        if c_in is not None and idx == len(spans) - 1:
-            _copy2d(h2d, c_in, 0, 0, C, 0, 0, n, m)
-            c_landed = torch.cuda.Event()
-            c_landed.record(h2d)
-    for idx, (l0, l1) in enumerate(spans[:-1]):
-        st.wait_event(landed[idx])
-        launch_mm(kid, st, av.sub(0, l0, n, l1 - l0), bv.sub(l0, 0, l1 - l0, m), cv, overwrite=idx == 0)
-    if c_landed is not None:
-        st.wait_event(c_landed)
+        return ev
+
+    av, bv, cv = View.of(a_d), View.of(b_d), View.of(c_d)
+    spans = list(zip(edges[:-1], edges[1:])) + [(front, k)]
+    for idx, (l0, l1) in enumerate(spans):
+        upload(a_d, 0, l0, n, l1 - l0, A_src, a_sn if staged else None, A)
+        ev = upload(b_d, l0, 0, l1 - l0, m, B_src, b_sn if staged else None, B)
+        if idx < len(spans) - 1:
+            st.wait_event(ev)
+            launch_mm(kid, st, av.sub(0, l0, n, l1 - l0), bv.sub(l0, 0, l1 - l0, m), cv, overwrite=idx == 0)
+    last_ev = ev
+    if front == 0:
+        # no front phase: C is loaded first and the row blocks accumulate into it
+        if not overwrite:
+            st.wait_event(upload(c_d, 0, 0, n, m, C_src, c_sn if staged else None, C))
+        else:
+            launch_fill(kid, st, cv)
+    elif c_in is not None:
+        st.wait_event(upload(c_in, 0, 0, n, m, C_src, c_sn if staged else None, C))
         launch_fold(kid, st, cv, View.of(c_in), reset=False)
-    st.wait_event(landed[-1])
+    st.wait_event(last_ev)
+    outs = []
     for i in range(R):
         r0, r1 = redges[i], redges[i + 1]
         if r1 <= r0:
@@ -362,7 +432,14 @@ def _kphased_host_mm(A, B, C, kid: int, dev: int, st, overwrite: bool) -> None:
         done = torch.cuda.Event()
         done.record(st)
         d2h.wait_event(done)
-        _copy2d(d2h, C, r0, 0, c_d, r0, 0, r1 - r0, m)
+        _copy2d(d2h, C_src, r0, 0, c_d, r0, 0, r1 - r0, m)
+        if staged:
+            back = torch.cuda.Event()
+            back.record(d2h)
+            outs.append((back, r0, r1))
+    for back, r0, r1 in outs:  # copy each landed row block out while later ones compute
+        back.synchronize()
+        _host_copy(C[r0:r1], c_sn[r0:r1])
     st.wait_stream(d2h)
     d2h.synchronize()
 
@@ -431,9 +508,10 @@ def fold_destinations(plan: Plan) -> dict[int, tuple[int, int, int]]:
 
 
 _TC_KERNELS = (nat.SR_BF16_F32, nat.SR_F32_TC)
-# test hook: every worker takes the remote-GPU path, "fused" (epilogue folds over
-# NVLink) or "stage" (local block, one copy, staged atomic fold)
-_REMOTE_ALL = os.environ.get("PACO_MM_REMOTE_ALL", "")
+# test hook (set by tests/stage_all_check.py, never from the environment): every
+# worker takes the remote-GPU path, "fused" (epilogue folds over NVLink) or
+# "stage" (local block, one copy, staged atomic fold)
+_REMOTE_ALL = ""
 
 
 def mm_execute(plan: Plan, A, B, C, semiring: Semiring = SEMIRING_INT, mode: str = "serial_sim",

@@ -496,7 +496,7 @@ def strassen_into(A: View, B: View, dests, base: int, stream) -> bool:
     does not apply (alignment, more than 4 leaf destinations), so the caller
     takes the M-buffer path."""
     n = A.rows
-    ok = _FUSED_COMBINE and all(d.ptr % 16 == 0 and d.ld % 4 == 0 for d, _ in dests) and n % 4 == 0
+    ok = FUSED_COMBINE and all(d.ptr % 16 == 0 and d.ld % 4 == 0 for d, _ in dests) and n % 4 == 0
     if not ok:
         return False
     if n <= base or n % 2:
@@ -510,7 +510,9 @@ def strassen_into(A: View, B: View, dests, base: int, stream) -> bool:
     return True
 
 
-_FUSED_COMBINE = __import__("os").environ.get("PACO_STRASSEN_FUSED", "1") != "0"
+# fp32 Strassen: fold the C-block combination into the leaf epilogues (True, the
+# measured default) or materialise M buffers + lincomb (False; kept for A/B runs)
+FUSED_COMBINE = True
 
 
 def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stream) -> None:
@@ -520,7 +522,7 @@ def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stre
         launch_mm(kid, stream, A, B, C, overwrite=True)
         return
     h = C.rows // 2
-    if kid == nat.SR_F32_TC and _FUSED_COMBINE and (C.ld * 4) % 16 == 0 and C.ptr % 16 == 0:
+    if kid == nat.SR_F32_TC and FUSED_COMBINE and (C.ld * 4) % 16 == 0 and C.ptr % 16 == 0:
         launch_fill(nat.SR_F32, stream, C)
         _strassen_tc_fused(A, B, [(C, 1)], base, stream)
         return
@@ -534,7 +536,7 @@ def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stre
     _combine(ws, C, dt, stream)
 
 
-_STAGE_ALL = bool(__import__("os").environ.get("PACO_MM_REMOTE_ALL"))  # test hook (see mm.py)
+_STAGE_ALL = False  # test hook (set by tests/stage_all_check.py; see mm._REMOTE_ALL)
 
 
 def _dtype_of_view(v: View) -> torch.dtype:

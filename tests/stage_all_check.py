@@ -1,6 +1,6 @@
-"""Helper of tests/test_gpu_mm.py::test_remote_worker_staging (run with
-PACO_MM_REMOTE_ALL=fused|stage): every plan worker takes mm_execute's remote-GPU
-path on the single test GPU."""
+"""Helper of tests/test_gpu_mm.py::test_remote_worker_paths (argv[1] = fused |
+stage): every plan worker takes mm_execute's remote-GPU path on the single
+test GPU (the product's test hooks mm._REMOTE_ALL / strassen._STAGE_ALL)."""
 import os
 import sys
 
@@ -9,6 +9,11 @@ import numpy as np
 
 from oracle import cref
 from paper_2011_01441_b200 import matmul as M
+from paper_2011_01441_b200 import mm as _mm
+from paper_2011_01441_b200 import strassen as _st
+
+_mm._REMOTE_ALL = sys.argv[1]
+_st._STAGE_ALL = True
 
 rng = np.random.default_rng(71)
 n, m, k = 301, 257, 603

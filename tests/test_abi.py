@@ -45,3 +45,29 @@ def test_argument_errors_without_device():
         nat.check(rc)
     with pytest.raises(nat.PlanError):
         nat.plan_one_piece(1, 1, 1, 2)
+
+
+@pytest.mark.parametrize("shape,cols", [((1, 1), (0, 1)), ((7, 5), (1, 4)), ((3000, 700), (13, 555)),
+                                        ((8192, 2048), (128, 1152))])
+def test_host_copy2d_parallel_staging(shape, cols):
+    """paco_host_copy2d (the pageable -> pinned staging memcpy of the NumPy e2e
+    path) copies strided 2-D views exactly, from 1 to 16 participants, repeatedly
+    (the persistent pool is reused across calls)."""
+    import numpy as np
+
+    from paper_2011_01441_b200 import mm as MM
+    rng = np.random.default_rng(shape[0])
+    src = rng.integers(-2**31, 2**31 - 1, shape, dtype=np.int64).astype(np.int32)
+    c0, c1 = cols
+    for threads in (1, 3, 8, 16):
+        dst = np.zeros(shape, np.int32)
+        old = MM._HOST_THREADS
+        MM._HOST_THREADS = threads
+        try:
+            for _ in range(3):
+                MM._host_copy(dst[:, c0:c1], src[:, c0:c1])
+        finally:
+            MM._HOST_THREADS = old
+        want = np.zeros(shape, np.int32)
+        want[:, c0:c1] = src[:, c0:c1]
+        assert np.array_equal(dst, want), threads

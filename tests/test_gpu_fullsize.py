@@ -1,10 +1,11 @@
 """BASELINE configs at FULL size on the GPU, checked against the CPU oracle.
 
-The CPU oracle cannot redo 5.5e11-4.4e12 terms per test, so each check is
-(1) a bit-exact oracle comparison on a seeded random sample of whole C rows
-(full k and m), and (2) size-independent properties the domain offers:
-every PACO plan of the same product -- GPU-level one-piece / multi-piece with
-k-cut folds, and the CTA-level plan -- must produce the bit-identical C
+cfg2 (8192^3 min-plus) and cfg4 (16384^3 max-plus) are compared with the
+pinned CPU oracle on EVERY element of C (np.array_equal on the whole matrix;
+the oracle's cache-blocked tropical path does the 5.5e11 / 4.4e12 terms in
+seconds / about half a minute on the host cores).  On top, size-independent
+properties the domain offers: every PACO plan of the same product --
+GPU-level one-piece with k-cut folds -- must give the bit-identical C
 (min/max are associative, commutative and idempotent), and C is a fixed point
 of C (+)= A (x) B.  Seeds/distributions follow SURVEY.md 8(d).
 """
@@ -38,10 +39,9 @@ def cfg4_inputs():
     return A, B
 
 
-def sample_rows_match(sr, A, B, C, zero, nrows, seed):
-    rows = np.sort(np.random.default_rng(seed).choice(A.shape[0], nrows, replace=False))
-    want = cref.mm_rows(sr, A, B, np.full((nrows, B.shape[1]), zero, np.int32), rows)
-    return np.array_equal(C[rows], want)
+def oracle_c(sr, A, B, zero):
+    """The whole oracle C = zero (+) A (x) B on the host cores."""
+    return cref.mm(sr, A, B, np.full((A.shape[0], B.shape[1]), zero, np.int32))
 
 
 def test_cfg2_minplus_8192_full():
@@ -50,7 +50,7 @@ def test_cfg2_minplus_8192_full():
     c = torch.full((8192, 8192), INF, dtype=torch.int32, device="cuda")
     M.mm_seq(a, b, c, M.SEMIRING_MINPLUS_SAT)
     C = c.cpu().numpy()
-    assert sample_rows_match(cref.SR_MINPLUS_SAT32, A, B, C, INF, 2048, 2)
+    assert np.array_equal(C, oracle_c(cref.SR_MINPLUS_SAT32, A, B, INF))
     # GPU-level PACO plans with k-cut MIN folds (p=5: 1 fold, p=7: 3 folds) agree bit for bit
     for p in (3, 5, 7):
         c2 = torch.full((8192, 8192), INF, dtype=torch.int32, device="cuda")
@@ -69,7 +69,7 @@ def test_cfg4_maxplus_16384_full_all_p():
     c = torch.full((16384, 16384), -INF, dtype=torch.int32, device="cuda")
     M.mm_seq(a, b, c, M.SEMIRING_MAXPLUS)
     C = c.cpu().numpy()
-    assert sample_rows_match(cref.SR_MAXPLUS_SAT32, A, B, C, -INF, 256, 4)
+    assert np.array_equal(C, oracle_c(cref.SR_MAXPLUS_SAT32, A, B, -INF))
     for p in (1, 2, 3, 4, 5, 7, 8):
         c2 = torch.full((16384, 16384), -INF, dtype=torch.int32, device="cuda")
         M.mm_execute(M.mm_one_piece_partition(16384, 16384, 16384, p), a, b, c2, M.SEMIRING_MAXPLUS,

@@ -36,20 +36,30 @@ def _inputs(n, m, k, seed):
     return A, B, C
 
 
-def _worker(rank, world, port, cases, q, remote_bulk="0", style="atomic"):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PACO_REMOTE_BULK=remote_bulk,
-                      PACO_FOLD_STYLE=style)
+def _maxplus_inputs(n, m, k, seed):
+    """cfg4's distribution at a reduced size; C starts at -INF."""
+    rng = np.random.default_rng(seed)
+    A = rng.integers(-2**20, 2**20, (n, k), dtype=np.int32)
+    B = rng.integers(-2**20, 2**20, (k, m), dtype=np.int32)
+    return A, B, np.full((n, m), -INF, np.int32)
+
+
+def _worker(rank, world, port, cases, q, remote_bulk="0", style="atomic", semiring="minplus"):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     from paper_2011_01441_b200 import _native as nat
     from paper_2011_01441_b200 import matmul as M
     from paper_2011_01441_b200.distributed import FusedDistributedMM
     try:
+        maxp = semiring == "maxplus"
+        sr, kid = ((M.SEMIRING_MAXPLUS, nat.SR_MAXPLUS_SAT32) if maxp else
+                   (M.SEMIRING_MINPLUS_SAT, nat.SR_MINPLUS_SAT32))
         for idx, (variant, n, m, k) in enumerate(cases):
-            A, B, C0 = _inputs(n, m, k, idx)
+            A, B, C0 = (_maxplus_inputs if maxp else _inputs)(n, m, k, idx)
             plan = (M.mm_one_piece_partition(n, m, k, world) if variant == "one_piece"
                     else M.mm_paco_partition(n, m, k, world, base=48))
-            ex = FusedDistributedMM(plan, M.SEMIRING_MINPLUS_SAT, nat.SR_MINPLUS_SAT32, 0)
+            ex = FusedDistributedMM(plan, sr, kid, 0, fold_style=style, remote_bulk=remote_bulk == "1")
             ex.run(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), torch.from_numpy(C0).cuda())
             mine = torch.empty((n, m), dtype=torch.int32, device="cuda")
             from paper_2011_01441_b200.mm import _copy2d_raw
@@ -66,7 +76,7 @@ def _worker(rank, world, port, cases, q, remote_bulk="0", style="atomic"):
                 for plist in allp:
                     for (i0, j0, rn, rm), blk in plist:
                         C[i0:i0 + rn, j0:j0 + rm] = blk
-                want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, C0.copy())
+                want = cref.mm(cref.SR_MAXPLUS_SAT32 if maxp else cref.SR_MINPLUS_SAT32, A, B, C0.copy())
                 nred = sum(1 for t in plan.tasks if t.kind == "reduce")
                 q.put((idx, bool(np.array_equal(C, want)), nred, ex.remote_bulk))
     finally:
@@ -78,7 +88,7 @@ def _worker(rank, world, port, cases, q, remote_bulk="0", style="atomic"):
 def test_fused_ipc_distributed_matches_oracle(world, remote_bulk, style):
     """Remote folds staged (default: local temporary, one bulk copy into the
     owner's staging slot, owner folds), as element atomics into the owner's C,
-    or, with PACO_REMOTE_BULK=1, as TMA bulk reductions into its IPC mapping."""
+    or, with remote_bulk=True, as TMA bulk reductions into its IPC mapping."""
     # the last case cuts only n (no rank writes into another's C: no barriers)
     cases = [("one_piece", 96, 80, 700), ("one_piece", 200, 150, 260), ("paco", 130, 90, 333),
              ("one_piece", 600, 90, 100)]
@@ -98,8 +108,30 @@ def test_fused_ipc_distributed_matches_oracle(world, remote_bulk, style):
     assert [r[3] for r in res] == [False, remote_bulk == "1", False, False], res
 
 
+@pytest.mark.parametrize("world", [5, 7])
+def test_fused_ipc_cfg4_maxplus_prime_p(world):
+    """cfg4's (max,+) at the prime GPU counts of the north star, one process per
+    worker: MM-1-Piece gives p = 5 one k-cut pair and p = 7 three, whose MAX
+    folds run fused in the kernels' epilogues over IPC; the owners' C equals
+    the oracle bit for bit (reduced size 1536^3 and a ragged 1000 x 1100 x 1300)."""
+    cases = [("one_piece", 1536, 1536, 1536), ("one_piece", 1000, 1100, 1300)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q, "0", "atomic", "maxplus"))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    res = sorted(q.get(timeout=5) for _ in cases)
+    assert all(r[1] for r in res), res
+    assert res[0][2] == (1 if world == 5 else 3) and all(r[2] >= 1 for r in res), res
+
+
 def _host_worker(rank, world, port, cases, q, style):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PACO_FOLD_STYLE=style)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     from paper_2011_01441_b200 import _native as nat
@@ -110,7 +142,7 @@ def _host_worker(rank, world, port, cases, q, style):
             A, B, _ = _inputs(n, m, k, 100 + idx)
             plan = (M.mm_one_piece_partition(n, m, k, world) if variant == "one_piece"
                     else M.mm_paco_partition(n, m, k, world, base=48))
-            ex = FusedDistributedMM(plan, M.SEMIRING_MINPLUS_SAT, nat.SR_MINPLUS_SAT32, 0)
+            ex = FusedDistributedMM(plan, M.SEMIRING_MINPLUS_SAT, nat.SR_MINPLUS_SAT32, 0, fold_style=style)
             A_h = torch.from_numpy(A).pin_memory()
             B_h = torch.from_numpy(B).pin_memory()
             C_h = torch.full((n, m), -1, dtype=torch.int32).pin_memory()

@@ -308,10 +308,34 @@ def test_pinned_host_pipeline_matches_oracle():
     assert np.array_equal(C2.numpy(), want2)
 
 
+def test_numpy_host_pipeline_short_k_matches_oracle(monkeypatch):
+    """Pageable NumPy operands with a short k: staged row-blocked pipeline."""
+    from paper_2011_01441_b200 import mm as MMmod
+    calls = []
+    real = MMmod._kphased_host_mm
+    monkeypatch.setattr(MMmod, "_kphased_host_mm", lambda *a, **kw: calls.append(kw) or real(*a, **kw))
+    rng = np.random.default_rng(42)
+    n, m, k = 1500, 700, 333
+    A = tropical(rng, (n, k), 0, 2**20, 0.1)
+    B = tropical(rng, (k, m), 0, 2**20, 0.1)
+    C0 = tropical(rng, (n, m), 0, 2**21, 0.3)
+    for overwrite in (False, True):
+        C = C0.copy() if not overwrite else np.full((n, m), 12345, np.int32)
+        M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT, overwrite=overwrite)
+        want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, C0.copy() if not overwrite else np.full((n, m), INF, np.int32))
+        assert np.array_equal(C, want), overwrite
+    assert len(calls) == 2 and all(c.get("front_share") == 0.0 for c in calls)
+
+
 @pytest.mark.parametrize("sr", ["minplus", "maxplus", "int", "f32", "bf16"])
 @pytest.mark.parametrize("overwrite", [False, True])
-def test_pinned_k_phased_pipeline(sr, overwrite):
-    """Long-k pinned operands take the k-first / rows-last pipeline; same C as the oracle."""
+@pytest.mark.parametrize("host", ["pinned", "numpy"])
+def test_host_k_phased_pipeline(sr, overwrite, host, monkeypatch):
+    """Long-k host operands -- pinned torch tensors, or pageable NumPy arrays staged
+    through pinned buffers by host threads -- take the k-first / rows-last
+    pipeline; same C as the oracle."""
+    if host == "numpy" and sr == "bf16":
+        pytest.skip("NumPy has no bfloat16")
     from paper_2011_01441_b200 import mm as MMmod
     rng = np.random.default_rng(43)
     n, m, k = 1100, 650, 2600
@@ -339,20 +363,31 @@ def test_pinned_k_phased_pipeline(sr, overwrite):
         sem, zero = (M.SEMIRING_F32 if sr == "f32" else M.SEMIRING_BF16), 0.0
     if overwrite:
         C0 = np.full((n, m), zero, C0.dtype)
-    Ah, Bh = torch.from_numpy(A), torch.from_numpy(B)
-    if sr == "bf16":
-        Ah, Bh = Ah.to(torch.bfloat16), Bh.to(torch.bfloat16)
-    Ah, Bh = Ah.pin_memory(), Bh.pin_memory()
-    C = torch.full(C0.shape, 7, dtype=torch.from_numpy(C0).dtype).pin_memory() if overwrite \
-        else torch.from_numpy(C0.copy()).pin_memory()
+    calls = []
+    real = MMmod._kphased_host_mm
+    monkeypatch.setattr(MMmod, "_kphased_host_mm", lambda *a, **kw: calls.append(1) or real(*a, **kw))
+    if sr == "int":
+        monkeypatch.setattr(MMmod, "NARROW_MIN_TERMS", 1 << 62)  # the int64 kernel's own pipeline
+    if host == "numpy":
+        Ah, Bh = A.copy(), B.copy()
+        C = np.full(C0.shape, 7, C0.dtype) if overwrite else C0.copy()
+    else:
+        Ah, Bh = torch.from_numpy(A), torch.from_numpy(B)
+        if sr == "bf16":
+            Ah, Bh = Ah.to(torch.bfloat16), Bh.to(torch.bfloat16)
+        Ah, Bh = Ah.pin_memory(), Bh.pin_memory()
+        C = torch.full(C0.shape, 7, dtype=torch.from_numpy(C0).dtype).pin_memory() if overwrite \
+            else torch.from_numpy(C0.copy()).pin_memory()
     M.mm_seq(Ah, Bh, C, sem, overwrite=overwrite)
+    got = C if host == "numpy" else C.numpy()
+    assert calls, "host pipeline not taken"
     if sr in ("f32", "bf16"):
         want = C0.astype(np.float64) + A.astype(np.float64) @ B.astype(np.float64)
-        err = np.linalg.norm(C.numpy() - want) / np.linalg.norm(want)
+        err = np.linalg.norm(got - want) / np.linalg.norm(want)
         assert err <= (1e-5 if sr == "f32" else 1e-5), err   # exact-bf16 inputs, f32 accumulation
     else:
         want = cref.mm(cid, A, B, C0.copy())
-        assert np.array_equal(C.numpy(), want)
+        assert np.array_equal(got, want)
 
 
 @pytest.mark.parametrize("fused", [True, False])
@@ -478,13 +513,13 @@ def test_remote_worker_paths(style):
     """mm_execute's paths for workers on another GPU -- fused (the epilogue folds
     into the home C with atomics) and staged (local block -> one copy -> atomic
     fold) -- forced on for every worker of the single test GPU
-    (PACO_MM_REMOTE_ALL, a fresh process: the hook is read at import)."""
+    (mm._REMOTE_ALL, in a fresh process)."""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
-    r = subprocess.run([sys.executable, os.path.join(here, "stage_all_check.py")], capture_output=True, text=True,
-                       env=dict(os.environ, PACO_MM_REMOTE_ALL=style), timeout=600)
+    r = subprocess.run([sys.executable, os.path.join(here, "stage_all_check.py"), style], capture_output=True,
+                       text=True, timeout=600)
     assert r.returncode == 0 and "stage-all ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 

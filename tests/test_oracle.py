@@ -38,11 +38,36 @@ def test_c_oracle_pins(golden_cases):
     np.testing.assert_allclose(cref.mm(cref.SR_F64, g["f64_A"], g["f64_B"], C), g["f64_C"], rtol=1e-12)
 
 
+@pytest.mark.parametrize("shape", [(1, 1, 1), (5, 17, 3), (6, 16, 256), (7, 33, 257), (100, 517, 300),
+                                   (97, 1025, 600)])
+def test_c_oracle_blocked_tropical_equals_plain_loop(shape, golden_cases):
+    """The cache-blocked 32-bit tropical path (used for the whole-C full-size checks)
+    gives the plain loop's bits on ragged shapes, with and without INF entries."""
+    n, m, k = shape
+    rng = np.random.default_rng(n * 7 + m)
+    for sr, lo, hi, zero in ((cref.SR_MINPLUS_SAT32, 0, 2**20, INF), (cref.SR_MAXPLUS_SAT32, -2**20, 2**20, -INF)):
+        A = rng.integers(lo, hi, (n, k), dtype=np.int32)
+        B = rng.integers(lo, hi, (k, m), dtype=np.int32)
+        if sr == cref.SR_MINPLUS_SAT32:
+            A[rng.random(A.shape) < 0.1] = INF
+            B[rng.random(B.shape) < 0.1] = INF
+        C0 = rng.integers(lo, hi, (n, m), dtype=np.int32)
+        C0[rng.random(C0.shape) < 0.3] = zero
+        assert np.array_equal(cref.mm(sr, A, B, C0.copy()), cref.mm(sr, A, B, C0.copy(), simple=True)), (sr, shape)
+    for tag in ("minplus_sat", "minplus_inf"):  # and the blocked path alone reproduces the goldens
+        A, B = golden_cases[f"{tag}_A"], golden_cases[f"{tag}_B"]
+        C = np.full((A.shape[0], B.shape[1]), INF, np.int32)
+        assert np.array_equal(cref.mm(cref.SR_MINPLUS_SAT32, A, B, C, simple=True), golden_cases[f"{tag}_C"])
+
+
 def test_numpy_port_pins(golden_cases):
     g = golden_cases
     plan = M.mm_paco_partition(384, 320, 256, 3)
     C = np.zeros((384, 320), np.int64)
     PN.mm_execute_serial(plan, g["cfg1_A"].astype(np.int64), g["cfg1_B"].astype(np.int64), C, "int")
+    assert np.array_equal(C, g["cfg1_C"])
+    C = np.zeros((384, 320), np.int64)  # the threaded (mode="parallel") restatement: same C
+    PN.mm_execute_parallel(plan, g["cfg1_A"].astype(np.int64), g["cfg1_B"].astype(np.int64), C, "int")
     assert np.array_equal(C, g["cfg1_C"])
     A, B = g["minplus_sat_A"], g["minplus_sat_B"]
     assert np.array_equal(PN.minplus_sat(A, B, np.full((A.shape[0], B.shape[1]), INF, np.int32)),
