@@ -438,8 +438,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cfg", type=int, default=2, choices=[2, 4],
-                    help="headline config at N>1 (cfg2 min-plus or cfg4 max-plus, GPU-level PACO plan)")
+    ap.add_argument("--cfg", type=int, default=2, choices=[2, 3, 4, 5],
+                    help="headline config at N>1 (GPU-level PACO plan of that BASELINE config)")
     ap.add_argument("--configs", default="1,2,3,4,5",
                     help="N=1: BASELINE configs measured into the line's `configs` ('none' to skip)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -462,10 +462,6 @@ def main():
     import torch.distributed as dist
 
     from paper_2011_01441_b200 import _native as nat
-    from paper_2011_01441_b200 import matmul as M
-    from paper_2011_01441_b200.device import View
-    from paper_2011_01441_b200.distributed import CudaOps, DistributedMM, FusedDistributedMM
-    from paper_2011_01441_b200.mm import launch_mm
 
     dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
@@ -482,11 +478,6 @@ def main():
     peaks = load_peaks()
     probes = {0: alu_probe(dev, 0), 1: alu_probe(dev, 1)}
     cfg = 2 if world == 1 else args.cfg
-    n = 8192 if cfg == 2 else 16384
-    ops_per_step = 2.0 * n ** 3
-    sr = M.SEMIRING_MINPLUS_SAT if cfg == 2 else M.SEMIRING_MAXPLUS
-    kid = nat.SR_MINPLUS_SAT32 if cfg == 2 else nat.SR_MAXPLUS_SAT32
-    zero = INF if cfg == 2 else -INF
     st = torch.cuda.current_stream(dev)
     configs = {}
     wanted = [] if args.configs == "none" or world > 1 else [int(x) for x in args.configs.split(",") if x]
@@ -496,7 +487,9 @@ def main():
         res2 = measure_config(2, dev, args, peaks, probes)
         a, b, c = res2.pop("_tensors")
         ms = res2["ms"]
-        ks, ctas = nat.cta_grid(kid, n, n, n)
+        n = 8192
+        ops_per_step = 2.0 * n ** 3
+        ks, ctas = nat.cta_grid(nat.SR_MINPLUS_SAT32, n, n, n)
         plan_desc = (f"1 GPU, CTA-level tile grid: {ctas} CTAs of one 128x128 C tile, k split {ks} way(s) "
                      "(cost-model choice over the PACO cuboid plan, DESIGN.md section 5)")
         launches_per_step = 1
@@ -505,50 +498,18 @@ def main():
         A_h, B_h = a.cpu().pin_memory(), b.cpu().pin_memory()
         del a, b, c
         torch.cuda.empty_cache()
+        dtype, l2 = "u32", f"inputs 2 x {n * n * 4 >> 20} MiB > 126 MB L2 (no flush)"
     else:
-        rng = np.random.default_rng(1000 + cfg)
-        if cfg == 2:
-            A = rng.integers(0, 2**20, (n, n), dtype=np.int32)
-            A[rng.random(A.shape) < 0.10] = INF
-            B = rng.integers(0, 2**20, (n, n), dtype=np.int32)
-            B[rng.random(B.shape) < 0.10] = INF
-        else:
-            A = rng.integers(-2**20, 2**20, (n, n), dtype=np.int32)
-            B = rng.integers(-2**20, 2**20, (n, n), dtype=np.int32)
-        A_h, B_h = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
-        A, B = A_h.to(dev), B_h.to(dev)
-        plan = M.mm_one_piece_partition(n, n, n, world, quantum=nat.tile_shape(kid)[:3])
-        nred = sum(1 for t in plan.tasks if t.kind == "reduce")
-        if args.fold == "fused":
-            ex = FusedDistributedMM(plan, sr, kid, dev)
-
-            def step():
-                ex.run(A, B)
-            launches_per_step = len(ex.owned) + len(ex.launches) + len(ex.incoming)
-            how = ("staged: local temporary -> one NVLink copy into the owner's staging slot -> owner fold"
-                   if ex.fold_style == "stage" else
-                   f"{'TMA bulk' if ex.remote_bulk else 'element'} atomics into the owner's C over NVLink")
-            plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}, cuts on 128-row/column tile "
-                         f"multiples); its {nred} k-cut folds need no REDUCE temporaries or NCCL call: local ones "
-                         f"are fused into the kernels' epilogues, remote ones {how} (CUDA IPC); tile-grid CTA plan "
-                         "inside each rank")
-        else:
-            ex = DistributedMM(plan, sr, CudaOps(sr, kid, st))
-            C = torch.empty((n, n), dtype=torch.int32, device=dev)
-            mine = sum(1 for t in plan.tasks if t.kind == "reduce" and rank in t.workers())
-
-            def step():
-                ex.run(A, B, C)
-            launches_per_step = 2 + len(ex.temp_ids) + 3 * mine + len(ex.mine)
-            plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}) ({nred} k-cut NCCL "
-                         f"{'MIN' if cfg == 2 else 'MAX'} folds), tile-grid CTA plan inside each rank")
+        mg = MultiGPU(cfg, world, rank, dev, args, peaks, probes)
+        ops_per_step, plan_desc, launches_per_step, dtype, l2 = (mg.ops_per_step, mg.plan_desc,
+                                                                 mg.launches_per_step, mg.dtype, mg.l2)
 
         def barrier():
             dist.barrier()
             torch.cuda.synchronize(dev)
 
         for _ in range(args.warmup):
-            step()
+            mg.step()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -556,47 +517,23 @@ def main():
             barrier()
             e0.record(st)
             for _ in range(args.steps):
-                step()
+                mg.step()
             e1.record(st)
             barrier()
         t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item()) / args.steps
         clocks = clk.summary()
-        tpc, probe_mhz = probes[0 if cfg == 2 else 1]
-        peak = 2 * tpc * SM_COUNT * 1965.0 / 1e6
-        per_gpu = ops_per_step / world / (ms * 1e-3) / 1e12
-        roofline = {"bound": "alu", "achieved": per_gpu, "peak": peak, "unit": "Top/s", "frac": per_gpu / peak,
-                    "per": "GPU (whole-job Top/s / N)",
-                    "peak_source": f"live VIADDMNMX probe: {tpc:.2f} terms/clk/SM x 2 x 148 x 1965 MHz"}
+        roofline = mg.roofline(ms)
 
     value = ops_per_step / (ms * 1e-3) / 1e9  # whole-job Gop/s
 
     # e2e through the public API from host memory
-    e2e = None
     if world == 1:
         e2e = e2e_numpy_cfg2(dev, args.e2e_steps)
         e2e["pinned_torch"] = e2e_pinned_cfg2(dev, st, A_h, B_h, args.e2e_steps)
-    elif args.fold == "fused":
-        C_h = torch.empty((n, n), dtype=torch.int32).pin_memory()
-        ex.run_host(A_h, B_h, C_h)  # warm
-        t_e2e, nbytes = [], (0, 0)
-        for _ in range(args.e2e_steps):
-            dist.barrier()
-            torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
-            nbytes = ex.run_host(A_h, B_h, C_h)
-            torch.cuda.synchronize(dev)
-            t = torch.tensor([(time.perf_counter() - t0) * 1e3], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e.append(float(t.item()))
-        tot = torch.tensor(list(nbytes), device=dev, dtype=torch.float64)
-        dist.all_reduce(tot)
-        e2e_ms = statistics.median(t_e2e)
-        e2e = {"value": ops_per_step / (e2e_ms * 1e-3) / 1e9, "unit": "Gop/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item()),
-               "bytes": "summed over ranks; time = max over ranks (host wall clock)",
-               "api": "paper_2011_01441_b200.distributed.FusedDistributedMM.run_host (pinned host tensors)"}
+    else:
+        e2e = mg.e2e(args.e2e_steps)
 
     if world == 1:
         configs["cfg2"] = res2
@@ -613,11 +550,11 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "Gop/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u32" if cfg == 2 else "s32",
+            "vs_baseline": None, "dtype": dtype,
             "data": f"synthetic (seeded numpy default_rng({1000 + cfg}), BASELINE cfg{cfg} distribution)",
             "config": workload_config(cfg),
             "plan": plan_desc,
-            "l2": f"inputs 2 x {n * n * 4 >> 20} MiB > 126 MB L2 (no flush)",
+            "l2": l2,
             "ops_per_step": ops_per_step,
             "roofline": roofline,
             "clocks": clocks,
@@ -632,6 +569,178 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+class MultiGPU:
+    """One rank's share of a BASELINE config at N > 1 GPUs (one process per GPU).
+
+    cfg2 / cfg4: GPU-level MM-1-Piece (k-cut folds fused into the kernels over
+    IPC, or NCCL reductions with --fold nccl).  cfg3: MM-1-Piece's n-only cuts
+    of the skinny shape, B replicated, every rank's block a sole-writer tcgen05
+    launch (no exchange).  cfg5: DistributedStrassen (PACO-balanced nodes and
+    split leftover leaves, one NCCL reduce-scatter of the signed partials)."""
+
+    def __init__(self, cfg, world, rank, dev, args, peaks, probes):
+        import numpy as np
+        import torch
+
+        from paper_2011_01441_b200 import _native as nat
+        from paper_2011_01441_b200 import matmul as M
+        from paper_2011_01441_b200 import strassen as S
+        from paper_2011_01441_b200.distributed import (CudaOps, CudaStrassenOps, DistributedMM,
+                                                       DistributedStrassen, FusedDistributedMM)
+
+        self.cfg, self.world, self.rank, self.dev, self.peaks = cfg, world, rank, dev, peaks
+        self.torch, self.nat = torch, nat
+        rng = np.random.default_rng(1000 + cfg)
+        st = torch.cuda.current_stream(dev)
+        self.l2 = "operands > 126 MB L2 (no flush)"
+        if cfg in (2, 4):
+            n = 8192 if cfg == 2 else 16384
+            if cfg == 2:
+                A = rng.integers(0, 2**20, (n, n), dtype=np.int32)
+                A[rng.random(A.shape) < 0.10] = INF
+                B = rng.integers(0, 2**20, (n, n), dtype=np.int32)
+                B[rng.random(B.shape) < 0.10] = INF
+            else:
+                A = rng.integers(-2**20, 2**20, (n, n), dtype=np.int32)
+                B = rng.integers(-2**20, 2**20, (n, n), dtype=np.int32)
+            sr = M.SEMIRING_MINPLUS_SAT if cfg == 2 else M.SEMIRING_MAXPLUS
+            kid = nat.SR_MINPLUS_SAT32 if cfg == 2 else nat.SR_MAXPLUS_SAT32
+            self.A_h, self.B_h = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+            self.A, self.B = self.A_h.to(dev), self.B_h.to(dev)
+            self.ops_per_step = 2.0 * n ** 3
+            self.dtype = "u32" if cfg == 2 else "s32"
+            self.l2 = f"inputs 2 x {n * n * 4 >> 20} MiB > 126 MB L2 (no flush)"
+            self.tpc = probes[0 if cfg == 2 else 1][0]
+            plan = M.mm_one_piece_partition(n, n, n, world, quantum=nat.tile_shape(kid)[:3])
+            nred = sum(1 for t in plan.tasks if t.kind == "reduce")
+            if args.fold == "fused":
+                self.ex = FusedDistributedMM(plan, sr, kid, dev)
+                self.step = lambda: self.ex.run(self.A, self.B)
+                self.launches_per_step = len(self.ex.fill_rects) + len(self.ex.launches) + len(self.ex.incoming)
+                how = ("staged: local temporary -> one NVLink copy into the owner's staging slot -> owner fold"
+                       if self.ex.fold_style == "stage" else
+                       f"{'TMA bulk' if self.ex.remote_bulk else 'element'} system-scope atomics into the owner's "
+                       "C over NVLink")
+                sync = "NCCL 1-element all-reduce (stream-ordered, no host sync)" if self.ex._nccl else \
+                    "host barrier (gloo)"
+                self.plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}, cuts on 128-row/column "
+                                  f"tile multiples); its {nred} k-cut folds need no REDUCE temporaries or NCCL "
+                                  f"reduction: local ones are fused into the kernels' epilogues, remote ones {how} "
+                                  f"(CUDA IPC); fold handshake: {sync if self.ex.exchange else 'none (no k cut)'}; "
+                                  "tile-grid CTA plan inside each rank")
+            else:
+                self.ex = DistributedMM(plan, sr, CudaOps(sr, kid, st))
+                self.C = torch.empty((n, n), dtype=torch.int32, device=dev)
+                mine = sum(1 for t in plan.tasks if t.kind == "reduce" and rank in t.workers())
+                self.step = lambda: self.ex.run(self.A, self.B, self.C)
+                self.launches_per_step = 2 + len(self.ex.temp_ids) + 3 * mine + len(self.ex.mine)
+                self.plan_desc = (f"{world} GPUs, GPU-level mm_one_piece_partition(p={world}) ({nred} k-cut NCCL "
+                                  f"{'MIN' if cfg == 2 else 'MAX'} folds), tile-grid CTA plan inside each rank")
+        elif cfg == 3:
+            n, k, m = 65536, 256, 1024
+            A = rng.standard_normal((n, k), dtype=np.float32)
+            B = rng.standard_normal((k, m), dtype=np.float32)
+            self.A_h = torch.from_numpy(A).to(torch.bfloat16).pin_memory()
+            self.B_h = torch.from_numpy(B).to(torch.bfloat16).pin_memory()
+            self.A, self.B = self.A_h.to(dev), self.B_h.to(dev)
+            plan = M.mm_one_piece_partition(n, m, k, world, quantum=nat.tile_shape(nat.SR_BF16_F32)[:3])
+            self.ex = FusedDistributedMM(plan, M.SEMIRING_BF16, nat.SR_BF16_F32, dev)
+            self.step = lambda: self.ex.run(self.A, self.B)
+            self.launches_per_step = len(self.ex.fill_rects) + len(self.ex.launches)
+            self.ops_per_step = 2.0 * n * m * k
+            self.dtype = "bf16"
+            rows = sum(r[2] for r in self.ex.owned)
+            self.bytes_rank = 2 * rows * k + 2 * k * m + 4 * rows * m
+            self.plan_desc = (f"{world} GPUs, mm_one_piece_partition(65536, 1024, 256, p={world}): n-only cuts, B "
+                              f"replicated, each rank's {rows}-row block one sole-writer tcgen05 launch (C stored "
+                              "once, no fill, no exchange)")
+        elif cfg == 5:
+            n = 16384
+            A = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+            B = rng.uniform(-1, 1, (n, n)).astype(np.float32)
+            self.A_h, self.B_h = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+            self.A, self.B = self.A_h.to(dev), self.B_h.to(dev)
+            plan = S.strassen_paco_partition(n, world, base=n // 4, split_leftover=True)
+            self.ex = DistributedStrassen(plan, CudaStrassenOps(torch.float32))
+            self.step = lambda: self.ex.run(self.A, self.B)
+            self.launches_per_step = None
+            self.ops_per_step = 49 * 2 * 4096 ** 3 + 18 * 8192 ** 2 + 7 * 18 * 4096 ** 2
+            self.dtype = "f32 (3xTF32)"
+            self.plan_desc = (f"{world} GPUs, strassen_paco_partition(16384, p={world}, base=4096, split_leftover): "
+                              f"{len(self.ex.nodes)} node(s) + {len(self.ex.pieces)} leaf piece(s) on this rank; "
+                              "signed partial C folded by the leaf epilogues, then one NCCL reduce-scatter")
+            with nat.kernel_timing() as kt:
+                self.step()
+                torch.cuda.synchronize(dev)
+                self.launches_per_step = sum(kt.read(f)[1] for f in range(5))
+        else:
+            raise SystemExit(f"--cfg {cfg}: no multi-GPU bench for this config")
+
+    def roofline(self, ms):
+        per_gpu = self.ops_per_step / self.world / (ms * 1e-3)
+        if self.cfg in (2, 4):
+            peak = 2 * self.tpc * SM_COUNT * 1965.0 / 1e6
+            return {"bound": "alu", "achieved": per_gpu / 1e12, "peak": peak, "unit": "Top/s",
+                    "frac": per_gpu / 1e12 / peak, "per": "GPU (whole-job Top/s / N)",
+                    "peak_source": f"live VIADDMNMX probe: {self.tpc:.2f} terms/clk/SM x 2 x 148 x 1965 MHz"}
+        if self.cfg == 3:
+            gbs = self.bytes_rank / (ms * 1e-3) / 1e9
+            return {"bound": "hbm", "achieved": gbs, "peak": self.peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": gbs / self.peaks["hbm_gbs"], "per": "GPU (rank 0's algorithmic bytes / step time)",
+                    "peak_source": f"hbm_gbs {self.peaks['source']}"}
+        mma = 3 * 49 * 2 * 4096 ** 3 / self.world
+        tf = mma / (ms * 1e-3) / 1e12
+        peak = self.peaks["bf16_tflops"] / 2
+        return {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                "per": "GPU (3xTF32 MMA flop / N / step time, reduce-scatter included)",
+                "peak_source": f"TF32 dense = bf16_tflops / 2 {self.peaks['source']}"}
+
+    def e2e(self, steps):
+        """The same step from pinned host operands, host wall clock, max over ranks."""
+        import torch
+        import torch.distributed as dist
+
+        torch_ = self.torch
+        dev = self.dev
+        if self.cfg in (2, 3, 4) and hasattr(self.ex, "run_host"):
+            C_h = torch_.empty((self.ex.n, self.ex.m), dtype=self.ex.tdtype).pin_memory()
+            fn = lambda: self.ex.run_host(self.A_h, self.B_h, C_h)  # noqa: E731
+            api = "paper_2011_01441_b200.distributed.FusedDistributedMM.run_host (pinned host tensors)"
+        elif self.cfg == 5:
+            rows = self.ex.rows
+            C_h = torch_.empty((rows, self.ex.size), dtype=torch_.float32).pin_memory()
+
+            def fn():
+                self.A.copy_(self.A_h, non_blocking=True)
+                self.B.copy_(self.B_h, non_blocking=True)
+                slab = self.ex.run(self.A, self.B)
+                C_h.copy_(slab, non_blocking=True)
+                torch_.cuda.synchronize(dev)
+                n = self.A_h.shape[0]
+                return (2 * n * n * 4, rows * self.ex.size * 4)
+            api = ("paper_2011_01441_b200.distributed.DistributedStrassen.run with pinned A/B uploaded and the rank's "
+                   "C row slab downloaded every step")
+        else:
+            return None
+        fn()  # warm
+        t_e2e, nbytes = [], (0, 0)
+        for _ in range(steps):
+            dist.barrier()
+            torch_.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            nbytes = fn()
+            torch_.cuda.synchronize(dev)
+            t = torch_.tensor([(time.perf_counter() - t0) * 1e3], device=dev, dtype=torch_.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e.append(float(t.item()))
+        tot = torch_.tensor(list(nbytes), device=dev, dtype=torch_.float64)
+        dist.all_reduce(tot)
+        ms = statistics.median(t_e2e)
+        return {"value": self.ops_per_step / (ms * 1e-3) / 1e9, "unit": "Gop/s", "ms_per_step": ms,
+                "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item()),
+                "bytes": "summed over ranks; time = max over ranks (host wall clock)", "api": api}
 
 
 if __name__ == "__main__":

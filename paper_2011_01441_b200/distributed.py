@@ -209,6 +209,18 @@ def fused_launches(plan: Plan, rank: int):
     return owners, launches
 
 
+def sole_launches(plan: Plan, rank: int) -> list[bool]:
+    """Per launch of ``rank`` (``fused_launches`` order): does it alone write its
+    C rectangle -- local owner, the whole k extent, and no other launch of any
+    rank folding into an intersecting rectangle of the same owner?"""
+    k_all = plan.meta["k"]
+    mine = fused_launches(plan, rank)[1]
+    every = [(r, jj, o, rr) for r in range(plan.p) for jj, (_, _, o, rr) in enumerate(fused_launches(plan, r)[1])]
+    return [owner == rank and a[3] == k_all and not any(
+        (r, jj) != (rank, j) and o == owner and _rect_intersect(rect, rr) for r, jj, o, rr in every)
+        for j, (a, _, owner, rect) in enumerate(mine)]
+
+
 def _rect_intersect(a, b):
     i0, j0 = max(a[0], b[0]), max(a[1], b[1])
     i1, j1 = min(a[0] + a[2], b[0] + b[2]), min(a[1] + a[3], b[1] + b[3])
@@ -299,6 +311,15 @@ class FusedDistributedMM:
         self.shared = [owner == self.rank and self.fold_style == "atomic"
                        and any(_rect_intersect(rect, ir) for ir in incoming_rects)
                        for _, _, owner, rect in self.launches]
+        # sole writers: a local launch over the whole k whose C rectangle no other
+        # launch (of any rank) touches computes its block with a plain store
+        # (PACO_MM_OVERWRITE) -- no zero fill, no atomics, C written once (the
+        # n-only cuts of cfg3's skinny shape make every launch one)
+        self.sole = sole_launches(plan, self.rank)
+        sole_rects = {tuple(rect) for s_, (_, _, _, rect) in zip(self.sole, self.launches) if s_}
+        self.fill_rects = [r for r in self.owned if tuple(r) not in sole_rects]
+        self._nccl = dist.get_backend(group) == "nccl"
+        self._tok = torch.zeros(1, dtype=torch.int32, device=device) if self._nccl else None
         self._setup_staging()
 
     def _setup_staging(self) -> None:
@@ -402,14 +423,28 @@ class FusedDistributedMM:
             return nat.MM_ATOMIC | (nat.MM_SYS if self.remote_bulk else nat.MM_REMOTE)
         return nat.MM_ATOMIC
 
-    def _fill_owned(self, st) -> None:
+    def _fill_owned(self, st, every: bool = False) -> None:
         """Semiring zero into the owned rectangles only (every fold, local or
-        remote, lands inside them; the rest of the buffer is never read)."""
+        remote, lands inside them; the rest of the buffer is never read) --
+        except those a sole-writer launch overwrites, unless ``every``."""
         from .mm import launch_fill
 
         mine = self.views[self.rank]
-        for (i0, j0, n, m) in self.owned:
+        for (i0, j0, n, m) in (self.owned if every else self.fill_rects):
             launch_fill(self.semiring.kernel_id, st, mine.sub(i0, j0, n, m))
+
+    def _device_barrier(self) -> None:
+        """Every rank's work enqueued so far is done before any rank's next work.
+
+        NCCL: a one-element all-reduce, stream-ordered -- the host never
+        blocks, the GPUs wait for each other (the collective completes only
+        when every rank's stream reached it).  gloo (CPU tests, ranks sharing
+        one GPU): synchronize + host barrier."""
+        if self._nccl:
+            dist.all_reduce(self._tok, group=self.group)
+        else:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)
 
     def run(self, A: torch.Tensor, B: torch.Tensor, C_init: torch.Tensor | None = None) -> None:
         from .device import View
@@ -421,10 +456,11 @@ class FusedDistributedMM:
         if C_init is not None:
             ci = View.of(C_init)
             for (i0, j0, n, m) in self.owned:
+                if (i0, j0, n, m) not in self.fill_rects:   # a sole writer would overwrite it: fill first
+                    launch_fill(self.semiring.kernel_id, st, mine.sub(i0, j0, n, m))
                 launch_fold(self.semiring.kernel_id, st, mine.sub(i0, j0, n, m), ci.sub(i0, j0, n, m), False)
         if self.exchange:
-            torch.cuda.synchronize(self.device)
-            dist.barrier(group=self.group)      # every owner's C is initialised
+            self._device_barrier()              # every owner's C is initialised
         av, bv = View.of(A), View.of(B)
         es = self.itemsize
         for j, ((ai, al, an, ak), (bl, bj, bk, bm), owner, (ci, cj, cn, cm)) in enumerate(self.launches):
@@ -436,17 +472,19 @@ class FusedDistributedMM:
                 self.nat.check(self.nat.load().paco_copy2d(self.device, st.cuda_stream, slot, cm * es, t.data_ptr(),
                                                            t.stride(0) * es, cm * es, cn))
                 continue
+            if self.sole[j] and C_init is None:
+                launch_mm(self.kid, st, a, b, mine.sub(ci, cj, cn, cm), overwrite=True, device=self.device)
+                continue
             launch_mm(self.kid, st, a, b, self.views[owner].sub(ci, cj, cn, cm), flags=self._flags(j, owner),
                       device=self.device)
         if not self.exchange:
             return
-        torch.cuda.synchronize(self.device)
-        dist.barrier(group=self.group)          # every remote fold / staged block has landed
-        if self.incoming:
-            for (ci, cj, cn, cm), off in self.incoming:
-                src = View.raw(self.stage_ptr + off * es, cn, cm, es, self.device, ld=cm)
-                launch_fold(self.semiring.kernel_id, st, mine.sub(ci, cj, cn, cm), src, False)
-            torch.cuda.synchronize(self.device)
+        self._device_barrier()                  # every remote fold / staged block has landed
+        for (ci, cj, cn, cm), off in self.incoming:
+            src = View.raw(self.stage_ptr + off * es, cn, cm, es, self.device, ld=cm)
+            launch_fold(self.semiring.kernel_id, st, mine.sub(ci, cj, cn, cm), src, False)
+        # (a sender refills this rank's staging slots only after the next step's
+        # first barrier, which this rank's stream reaches after these folds)
 
     def run_host(self, A_h: torch.Tensor, B_h: torch.Tensor, C_h: torch.Tensor) -> tuple[int, int]:
         """End to end from pinned host operands: C_h's owned rectangles <- C.
@@ -481,10 +519,9 @@ class FusedDistributedMM:
         d2h.wait_stream(st)
         av, bv = View.of(a_d), View.of(b_d)
         mine = self.views[self.rank]
-        self._fill_owned(st)
+        self._fill_owned(st, every=True)        # k-chunked launches fold into C: all of it starts at zero
         if self.exchange:
-            torch.cuda.synchronize(dev)
-            dist.barrier(group=self.group)      # every owner's C is initialised
+            self._device_barrier()              # every owner's C is initialised
         h2d.wait_stream(st)
         sent_a, sent_b, h2d_bytes = set(), set(), 0
         for j, ((ai, al, an, ak), (bl, bj, bk, bm), owner, (ci, cj, cn, cm)) in enumerate(self.launches):
@@ -534,8 +571,7 @@ class FusedDistributedMM:
                     continue
                 launch_mm(self.kid, st, a, b, self.views[owner].sub(ci, cj, cn, cm), flags=flags, device=dev)
         if self.exchange:
-            torch.cuda.synchronize(dev)
-            dist.barrier(group=self.group)      # every remote fold / staged block has landed
+            self._device_barrier()              # every remote fold / staged block has landed
         for (ci, cj, cn, cm), off in self.incoming:
             src = View.raw(self.stage_ptr + off * es, cn, cm, es, dev, ld=cm)
             launch_fold(self.semiring.kernel_id, st, mine.sub(ci, cj, cn, cm), src, False)

@@ -146,3 +146,32 @@ def test_fused_launches_cover_iteration_space_once(p):
                     assert any(o[0][0] <= ci and o[0][1] <= cj and ci + cn <= o[0][0] + o[0][2]
                                and cj + cm <= o[0][1] + o[0][3] for o in owner_rects)
             assert (cover == 1).all()
+
+
+@pytest.mark.parametrize("shape,p", [((65536, 1024, 256), 2), ((65536, 1024, 256), 8), ((8192, 8192, 8192), 4),
+                                     ((8192, 8192, 8192), 5), ((8192, 8192, 8192), 7), ((384, 320, 256), 3)])
+def test_sole_writer_launches(shape, p):
+    """FusedDistributedMM's store-only launches (PACO_MM_OVERWRITE: no zero fill,
+    no atomics): exactly the local full-k launches whose C rectangle no other
+    launch touches.  cfg3's n-only cuts make every launch one; a k-cut pair's
+    two launches never are; sole rectangles tile what they cover once."""
+    from paper_2011_01441_b200.distributed import _rect_intersect, fused_launches, sole_launches
+    n, m, k = shape
+    plan = M.mm_one_piece_partition(n, m, k, p) if shape != (384, 320, 256) else M.mm_paco_partition(n, m, k, p)
+    nred = sum(1 for t in plan.tasks if t.kind == "reduce")
+    covered = 0
+    all_l = [(r, j, L) for r in range(p) for j, L in enumerate(fused_launches(plan, r)[1])]
+    for r in range(p):
+        launches = fused_launches(plan, r)[1]
+        sole = sole_launches(plan, r)
+        assert len(sole) == len(launches)
+        for j, ((ai, al, an, ak), _, owner, rect) in enumerate(launches):
+            others = [L for rr, jj, L in all_l if (rr, jj) != (r, j) and L[2] == owner and _rect_intersect(rect, L[3])]
+            assert sole[j] == (owner == r and ak == k and not others)
+            if sole[j]:
+                covered += rect[2] * rect[3]
+    if nred == 0:
+        assert all(all(sole_launches(plan, r)) for r in range(p))
+        assert covered == n * m
+    else:
+        assert covered < n * m
