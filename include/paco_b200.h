@@ -213,6 +213,27 @@ int paco_narrow_i64(int device, void* stream, const int64_t* src, int64_t ld_src
 int paco_widen_u32_i64(int device, void* stream, const void* r32, int64_t ld_r, int64_t* c, int64_t ld_c,
                        int64_t rows, int64_t cols);
 
+/* Strassen's leaf level with the operand formation fused into the 3xTF32
+ * kernel: problem q (< count <= 8) multiplies
+ * A_q = sum_{t < nta[q]} a_sign[2q+t] * a_terms[2q+t]   (n x k, pitch lda)
+ * by B_q, passed transposed as
+ * B_q^T = sum_{t < ntb[q]} b_sign[2q+t] * bt_terms[2q+t] (m x k, pitch ldb),
+ * with nta, ntb in 1..2 and signs +1/-1 -- i.e. the leaf's S_r of A and T_r^T
+ * of B^T as quadrant views -- and folds the product into its ndst[q] (1..4)
+ * destinations with sign[4q+d] (as paco_mm_tf32x3_multi).  The sums and the
+ * tf32 hi/lo split happen in shared memory inside the GEMM: no split launches,
+ * no hi/lo round trip through HBM.  Views: 16-byte aligned starts and pitches. */
+int paco_mm_tf32x3_fused(int device, void* stream, int count, const int32_t* nta, const void* const* a_terms,
+                         const int32_t* a_sign, int64_t lda, const int32_t* ntb, const void* const* bt_terms,
+                         const int32_t* b_sign, int64_t ldb, const int32_t* ndst, void* const* dst,
+                         const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k);
+
+/* dst (cols x rows, pitch ld_dst) = src^T (rows x cols, pitch ld_src); 4- or
+ * 8-byte elements.  Strassen transposes B once so every T_r^T operand of the
+ * fused leaves is a K-major view. */
+int paco_transpose(int device, void* stream, int elsize, void* dst, int64_t ld_dst, const void* src, int64_t ld_src,
+                   int64_t rows, int64_t cols);
+
 /* Asynchronous 2-D copy (host<->device or device<->device; pitches and width in
  * BYTES): the staging primitive of the overlapped host pipeline. */
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,

@@ -77,6 +77,12 @@ SIGNATURES = {
     "paco_narrow_i64": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _int, _vp]),
     "paco_widen_u32_i64": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_host_copy2d": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _int]),
+    "paco_mm_tf32x3_fused": (_int, [_int, _vp, _int, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_vp),
+                                    ctypes.POINTER(ctypes.c_int32), _i64, ctypes.POINTER(ctypes.c_int32),
+                                    ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), _i64,
+                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32),
+                                    _i64, _i64, _i64, _i64]),
+    "paco_transpose": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_copy2d": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_device_alloc": (_int, [_int, ctypes.c_size_t, ctypes.POINTER(_vp)]),
     "paco_device_free": (_int, [_int, _vp]),

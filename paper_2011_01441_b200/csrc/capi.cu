@@ -84,6 +84,10 @@ int launch_mm_tf32x3_multi(int device, cudaStream_t stream, int count, const voi
                            const void* const* al, int64_t lda, const void* const* bth, const void* const* btl,
                            int64_t ldb, const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc,
                            int64_t n, int64_t m, int64_t k, int flags);
+int launch_mm_tf32x3_fused(int device, cudaStream_t stream, int count, const int32_t* nta, const void* const* a_terms,
+                           const int32_t* a_sign, int64_t lda, const int32_t* ntb, const void* const* bt_terms,
+                           const int32_t* b_sign, int64_t ldb, const int32_t* ndst, void* const* dst,
+                           const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k);
 int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,
                       const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* lo,
                       int64_t ldo);
@@ -98,6 +102,8 @@ int launch_narrow_i64(cudaStream_t st, const int64_t* src, int64_t lds, void* ds
                       int64_t m, int64_t lo, int64_t hi, int saturate, int32_t* flag);
 int launch_widen_u32_i64(cudaStream_t st, const void* r, int64_t ldr, int64_t* c, int64_t ldc, int64_t n,
                          int64_t m);
+int launch_transpose(cudaStream_t st, int elsize, void* dst, int64_t ldd, const void* src, int64_t lds, int64_t rows,
+                     int64_t cols);
 int run_alu_probe(cudaStream_t st, int which, int iters, double* tpc, double* mhz);
 struct Box;
 }  // namespace paco
@@ -422,6 +428,35 @@ int paco_kernel_timing_read(int family, double* ms_total, int64_t* launches) {
   *ms_total = tot;
   *launches = cnt;
   return PACO_OK;
+}
+
+int paco_mm_tf32x3_fused(int device, void* stream, int count, const int32_t* nta, const void* const* a_terms,
+                         const int32_t* a_sign, int64_t lda, const int32_t* ntb, const void* const* bt_terms,
+                         const int32_t* b_sign, int64_t ldb, const int32_t* ndst, void* const* dst,
+                         const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k) {
+  if (count >= 1 && nta && ntb && a_terms && bt_terms && ndst && dst)
+    for (int q = 0; q < count && q < 8; ++q) {
+      for (int t = 0; t < nta[q] && t < 2; ++t) PACO_TRY(check_view("A term", a_terms[2 * q + t], lda, n, k));
+      for (int t = 0; t < ntb[q] && t < 2; ++t) PACO_TRY(check_view("B^T term", bt_terms[2 * q + t], ldb, m, k));
+      for (int d = 0; d < ndst[q] && d < 4; ++d) PACO_TRY(check_view("C", dst[4 * q + d], ldc, n, m));
+    }
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_mm_tf32x3_fused(device, static_cast<cudaStream_t>(stream), count, nta, a_terms, a_sign, lda, ntb,
+                                bt_terms, b_sign, ldb, ndst, dst, sign, ldc, n, m, k);
+}
+
+int paco_transpose(int device, void* stream, int elsize, void* dst, int64_t ld_dst, const void* src, int64_t ld_src,
+                   int64_t rows, int64_t cols) {
+  PACO_TRY(check_view("src", src, ld_src, rows, cols));
+  PACO_TRY(check_view("dst", dst, ld_dst, cols, rows));
+  if (elsize != 4 && elsize != 8) {
+    set_error("paco_transpose: element size %d (4 or 8)", elsize);
+    return PACO_ERR_ARG;
+  }
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_transpose(static_cast<cudaStream_t>(stream), elsize, dst, ld_dst, src, ld_src, rows, cols);
 }
 
 int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void* src, int64_t spitch,

@@ -280,6 +280,55 @@ __global__ void widen_u32_i64_kernel(const uint32_t* __restrict__ r, int64_t ldr
     }
 }
 
+// dst (cols x rows) = src^T through a padded 32 x 32 smem tile: reads and
+// writes both coalesced along rows (blockDim 32 x 8, each thread 4 rows).
+template <class T>
+__global__ void __launch_bounds__(256) transpose_kernel(T* __restrict__ dst, int64_t ldd, const T* __restrict__ src,
+                                                        int64_t lds, int64_t rows, int64_t cols) {
+  __shared__ T tile[32][33];
+  const int64_t c0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int64_t r = r0 + ty + k, c = c0 + tx;
+    if (r < rows && c < cols) tile[ty + k][tx] = __ldcs(src + r * lds + c);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int64_t orow = c0 + ty + k, ocol = r0 + tx;  // output row = input column
+    if (orow < cols && ocol < rows) __stcs(dst + orow * ldd + ocol, tile[tx][ty + k]);
+  }
+}
+
+int launch_transpose(cudaStream_t st, int elsize, void* dst, int64_t ldd, const void* src, int64_t lds, int64_t rows,
+                     int64_t cols) {
+  if (rows <= 0 || cols <= 0) return PACO_OK;
+  if ((cols + 31) / 32 > INT32_MAX || (rows + 31) / 32 > 65535 * 32) {
+    set_error("paco_transpose: %lld x %lld exceeds the grid", (long long)rows, (long long)cols);
+    return PACO_ERR_ARG;
+  }
+  KernelSpan ks(PACO_KT_ELEMENTWISE, st);
+  const dim3 block(32, 8);
+  const int64_t gy = (rows + 31) / 32;
+  // grid.y is capped at 65535: walk the row tiles in chunks
+  for (int64_t y0 = 0; y0 < gy; y0 += 65535) {
+    const int64_t ny = gy - y0 < 65535 ? gy - y0 : 65535;
+    const dim3 grid(unsigned((cols + 31) / 32), unsigned(ny));
+    const int64_t r_off = y0 * 32;
+    if (elsize == 4)
+      transpose_kernel<uint32_t><<<grid, block, 0, st>>>(static_cast<uint32_t*>(dst) + r_off, ldd,
+                                                         static_cast<const uint32_t*>(src) + r_off * lds, lds,
+                                                         rows - r_off, cols);
+    else
+      transpose_kernel<unsigned long long><<<grid, block, 0, st>>>(
+          static_cast<unsigned long long*>(dst) + r_off, ldd, static_cast<const unsigned long long*>(src) + r_off * lds,
+          lds, rows - r_off, cols);
+  }
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
 namespace {
 dim3 rows_grid(int64_t n, int64_t m, int per_block) {
   const int64_t xb = (m + per_block - 1) / per_block, yb = n < 65535 ? n : 65535, ycap = 2368 / xb + 1;

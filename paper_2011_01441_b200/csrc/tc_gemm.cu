@@ -62,7 +62,8 @@ struct KindBF16T {
   static constexpr int BN = 256, BK = 64, UMMA_K = 16, STAGES = ST, ELEM = 2, NOPS = 1, PASSES = 1;
   static constexpr int RING_BYTES = ST * 48 * 1024, EPI_WARPS = EW, EPI_BUFS = EB, KB_MAX = 0, EPI_COLS = EC;
   static constexpr int SWZ = 128;  // operand swizzle (bytes per K-major row)
-  static constexpr bool B_KMAJOR = false, B_RES = false;
+  static constexpr bool B_KMAJOR = false, B_RES = false, FUSED = false;
+  static constexpr int CONV_WARPS = 0, RAW_STAGES = 0, NT = 0, RAW_BYTES = 0;
   // F32 accumulate, BF16 A/B (format 1), A K-major, B MN-major (bit 16)
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -84,7 +85,8 @@ struct KindTF32x3T {
   static constexpr int BN = BN_, BK = BK_, UMMA_K = 8, STAGES = ST, ELEM = 4, NOPS = 2, PASSES = 3;
   static constexpr int RING_BYTES = ST * 2 * (128 + BN_) * BK * 4, EPI_WARPS = 4, EPI_BUFS = 2, KB_MAX = 0,
                        EPI_COLS = 32, SWZ = BK_ * 4;
-  static constexpr bool B_KMAJOR = true, B_RES = false;  // B^T tiles (the split writes B transposed)
+  static constexpr bool B_KMAJOR = true, B_RES = false, FUSED = false;  // B^T tiles (the split writes B transposed)
+  static constexpr int CONV_WARPS = 0, RAW_STAGES = 0, NT = 0, RAW_BYTES = 0;
   // F32 accumulate, TF32 A/B (format 2), both K-major
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -98,6 +100,34 @@ using KindTF32x3W = KindTF32x3T<256, 4, 16>;
 // (MN-major B -- bit 16 of the descriptor -- is what the bf16 kind uses; with
 // kind::tf32 it returned all-zero products here, hence the transposed split.)
 
+// 3xTF32 with the operand formation fused into the kernel (Strassen leaves):
+// each operand is a signed sum of NT_ <= 2 raw fp32 K-major views (S_r of A,
+// T_r^T of B^T).  The producer TMA-loads the raw term
+// tiles straight into the hi / lo slots of an operand stage; CW converter
+// warps then form x = (+/-)t0 (+/-) t1 and split it IN PLACE into
+// hi = tf32_rn(x), lo = tf32_rn(x - hi) -- raw and operand tiles share one
+// 64B-swizzled box layout, so every 16-byte chunk is read and rewritten by one
+// thread at one position.  So the ring keeps the split path's bytes in flight
+// (ST stages of 48 KB) while the separate split launches and their HBM round
+// trip of hi/lo pairs disappear.
+template <int ST, int NT_, int CW = 4>
+struct KindTF32x3FT {
+  static constexpr int BN = 256, BK = 16, UMMA_K = 8, STAGES = ST, ELEM = 4, NOPS = 2, PASSES = 3;
+  static constexpr int EPI_WARPS = 4, EPI_BUFS = 2, KB_MAX = 0, EPI_COLS = 16, SWZ = 64;
+  static constexpr bool B_KMAJOR = true, B_RES = false, FUSED = true;
+  static constexpr int CONV_WARPS = CW, RAW_STAGES = 0, NT = NT_, RAW_BYTES = 0;
+  static_assert(NT_ >= 1 && NT_ <= NOPS, "raw terms live in the hi / lo slots");
+  static constexpr int RING_BYTES = ST * 2 * (128 + BN) * BK * 4;
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
+                                    (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+  static constexpr CUtensorMapDataType DT = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+};
+#ifndef PACO_TF32F_ST
+#define PACO_TF32F_ST 4
+#define PACO_TF32F_CW 8
+#endif
+using KindTF32x3F = KindTF32x3FT<PACO_TF32F_ST, 2, PACO_TF32F_CW>;
+
 // bf16 with K <= KB_MAX * BK: the CTA's whole B column block (K x 256, 128 KB)
 // stays resident in shared memory across its consecutive tiles of that block,
 // so per tile only A (64 KB) is loaded -- the streaming kind re-reads B's
@@ -109,7 +139,8 @@ struct KindBF16Res {
   static constexpr int BN = BN_, BK = 64, UMMA_K = 16, STAGES = AST, ELEM = 2, NOPS = 1, PASSES = 1;
   static constexpr int KB_MAX = 4, EPI_WARPS = EW, EPI_BUFS = EB, EPI_COLS = EC, SWZ = 128;
   static constexpr int RING_BYTES = KB_MAX * BN * BK * 2 + AST * 128 * BK * 2;
-  static constexpr bool B_KMAJOR = false, B_RES = true;
+  static constexpr bool B_KMAJOR = false, B_RES = true, FUSED = false;
+  static constexpr int CONV_WARPS = 0, RAW_STAGES = 0, NT = 0, RAW_BYTES = 0;
   // F32 accumulate, BF16 A/B, A K-major, B MN-major, N = BN
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -126,8 +157,8 @@ struct Layout {
   static constexpr int SMEM_EPI = K::RING_BYTES;
   static constexpr int EPI_BUF = 32 * K::EPI_COLS * 4;        // one C store box: 32 rows x EPI_COLS fp32
   static constexpr int SMEM_BAR = SMEM_EPI + K::EPI_WARPS * K::EPI_BUFS * EPI_BUF;
-  static constexpr int THREADS = 64 + 32 * K::EPI_WARPS;
-  static_assert(B_REGION + K::STAGES * STAGE_BYTES <= K::RING_BYTES, "stage ring");
+  static constexpr int THREADS = 64 + 32 * (K::EPI_WARPS + K::CONV_WARPS);
+  static_assert(B_REGION + K::STAGES * STAGE_BYTES + K::RAW_BYTES <= K::RING_BYTES, "stage ring");
   static constexpr int SMEM_ALLOC = SMEM_BAR + 512 + 1024;    // + runtime 1024-B alignment slack
   static constexpr uint32_t TMEM_COLS = 2 * K::BN;            // double-buffered accumulator
   static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
@@ -220,6 +251,30 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const 
   asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+// Round to the nearest tf32 (10 mantissa bits; the result's low 13 bits are 0).
+__device__ __forceinline__ float round_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// The same rounding on the integer ALU (cvt.rna.tf32 issues on the narrow XU
+// pipe): add half an ulp of tf32 to the magnitude bits and clear the 13 low
+// bits -- round half away from zero, as .rna; carries roll into the exponent
+// exactly like a rounding up (finite inputs).
+__device__ __forceinline__ uint32_t round_tf32_bits(uint32_t b) { return (b + 0x1000u) & 0xFFFFE000u; }
+
+// 16-byte shared-memory accesses by 32-bit shared address (the generic
+// LD.E / ST.E the compiler emits for computed smem pointers cost a translation)
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
 
@@ -333,6 +388,8 @@ struct TcProb {
   int32_t a_col0[2], b_col0[2], c_col0, cx_col0[3];
   int32_t ndst;  // 1 + number of cx maps in use
   uint32_t neg;  // bit d: destination d receives -AB
+  int32_t nta, ntb;      // fused kinds: raw terms of A (maps a[0..nta)) and of B^T (b[0..ntb))
+  uint32_t sga, sgb;     // bit t: term t enters with coefficient -1
 };
 constexpr int kMaxBatch = 8;
 struct TcMaps {
@@ -354,8 +411,9 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   uint64_t* bempty = bfull + 4;   // MMAs reading the resident B completed (B_RES)
   constexpr int QD = 4;           // tile queue depth
   uint64_t* qfull = bempty + 1;   // tile id published by the producer
-  uint64_t* qempty = qfull + QD;  // ... and read by the MMA warp + every epilogue warp
-  int32_t* qid = reinterpret_cast<int32_t*>(qempty + QD);
+  uint64_t* qempty = qfull + QD;  // ... and read by the MMA warp + every epilogue (+ converter) warp
+  uint64_t* rfull = qempty + QD;  // fused kinds: raw term tiles landed in a stage (TMA)
+  int32_t* qid = reinterpret_cast<int32_t*>(rfull + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qid + QD);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -363,9 +421,11 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], K::FUSED ? K::CONV_WARPS : 1);  // fused: one arrival per converter warp
       mbar_init(&empty[s], 1);
     }
+    if (K::FUSED)
+      for (int s = 0; s < STAGES; ++s) mbar_init(&rfull[s], 1);  // raw terms landed in stage s
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], K::EPI_WARPS);
@@ -374,7 +434,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
     mbar_init(bempty, 1);
     for (int j = 0; j < QD; ++j) {
       mbar_init(&qfull[j], 1);
-      mbar_init(&qempty[j], 1 + K::EPI_WARPS);
+      mbar_init(&qempty[j], 1 + K::EPI_WARPS + K::CONV_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     for (int q = 0; q < args.count; ++q) {
@@ -437,6 +497,23 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
               ++bloads;
               if (i == 0) tc_stamp(args, 15, 4);
             }
+          }
+          if constexpr (K::FUSED) {
+            // raw fp32 term tiles into the stage's hi / lo slots; the converter
+            // warps form and split them in place (rfull -> full)
+            const uint32_t bytes = uint32_t(P.nta * L::A_BYTES + P.ntb * L::B_BYTES);
+            for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
+              const int s = it % STAGES;
+              mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+              if (kb == 0 && i < 15) tc_stamp(args, i, 0);
+              mbar_expect_tx_relaxed(&rfull[s], bytes);
+#pragma unroll
+              for (int t = 0; t < K::NT; ++t) {
+                if (t < P.nta) tma_load_2d(smem + L::a_off(s, t), &P.a[t], &rfull[s], P.a_col0[t] + kb * BK, rb * BM);
+                if (t < P.ntb) tma_load_2d(smem + L::b_off(s, t), &P.b[t], &rfull[s], P.b_col0[t] + kb * BK, nb * BN);
+              }
+            }
+            continue;
           }
           for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
             const int s = it % STAGES;
@@ -535,6 +612,79 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
         new_b = false;
       }
     }
+  } else if (warp >= 2 + K::EPI_WARPS) {
+   if constexpr (K::FUSED) {
+    // ---------------- converter warps (fused kinds) ----------------
+    // x = (+/-)t0 (+/-)t1, hi = tf32_rn(x), lo = tf32_rn(x - hi), in place over
+    // the stage's hi (t0) / lo (t1) slots, 16-byte chunk by chunk.
+    const int ct = (warp - 2 - K::EPI_WARPS) * 32 + lane;  // 0 .. 32 * CONV_WARPS - 1
+    constexpr int NTH = 32 * K::CONV_WARPS;
+    constexpr int A_CH = L::A_BYTES / 16, B_CH = L::B_BYTES / 16;
+    constexpr int PER = (A_CH + B_CH) / NTH;  // chunks per thread per stage
+    static_assert((A_CH + B_CH) % NTH == 0 && A_CH % NTH == 0, "whole chunks per converter thread");
+    uint32_t it = 0;
+    for (int64_t i = 0;; ++i) {
+      const int qs = int(i % QD);
+      mbar_wait(&qfull[qs], uint32_t(i / QD) & 1);
+      const int32_t id = qid[qs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty[qs]);
+      if (id < 0) break;
+      const int tpp = args.tiles_rb * args.tiles_nb;
+      const TcProb& P = maps.p[id / tpp];
+      const int nta = P.nta, ntb = P.ntb;
+      const uint32_t sga = P.sga, sgb = P.sgb;
+      for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&rfull[s], (it / STAGES) & 1);
+        const uint32_t sbase = smem_u32(smem);
+        uint4 x0[PER], x1[PER];
+        // every load of the stage first (PER x 2 LDS.128 in flight), then the math and stores
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int c = ct + u * NTH;
+          constexpr int UA = A_CH / NTH;  // the first UA chunk rounds cover A (A_CH % NTH == 0)
+          const bool isa = u < UA;
+          const uint32_t off = sbase + (isa ? L::a_off(s, 0) + c * 16 : L::b_off(s, 0) + (c - A_CH) * 16);
+          const uint32_t off1 = sbase + (isa ? L::a_off(s, 1) + c * 16 : L::b_off(s, 1) + (c - A_CH) * 16);
+          x0[u] = lds128(off);
+          if ((isa ? nta : ntb) > 1) x1[u] = lds128(off1);
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int c = ct + u * NTH;
+          const bool isa = u < A_CH / NTH;
+          const int nt = isa ? nta : ntb;
+          const uint32_t sg = isa ? sga : sgb;
+          float x[4] = {__uint_as_float(x0[u].x), __uint_as_float(x0[u].y), __uint_as_float(x0[u].z),
+                        __uint_as_float(x0[u].w)};
+          if (sg & 1u)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = -x[e];
+          if (nt > 1) {
+            const float y[4] = {__uint_as_float(x1[u].x), __uint_as_float(x1[u].y), __uint_as_float(x1[u].z),
+                                __uint_as_float(x1[u].w)};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = (sg & 2u) ? x[e] - y[e] : x[e] + y[e];
+          }
+          uint32_t h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            h[e] = round_tf32_bits(__float_as_uint(x[e]));
+            l[e] = round_tf32_bits(__float_as_uint(x[e] - __uint_as_float(h[e])));
+          }
+          const uint32_t off = sbase + (isa ? L::a_off(s, 0) + c * 16 : L::b_off(s, 0) + (c - A_CH) * 16);
+          const uint32_t off1 = sbase + (isa ? L::a_off(s, 1) + c * 16 : L::b_off(s, 1) + (c - A_CH) * 16);
+          sts128(off, make_uint4(h[0], h[1], h[2], h[3]));
+          sts128(off1, make_uint4(l[0], l[1], l[2], l[3]));
+        }
+        // generic-proxy smem writes -> visible to the tensor core's async-proxy reads
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+      }
+    }
+   }
   } else {
     // ---------------- epilogue warps ----------------
     // Each warp drains its TMEM lane quadrant for PER 32-column chunks of the
@@ -611,7 +761,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
                 const uint4 w = make_uint4(v[EC * h + 4 * j] ^ sgn, v[EC * h + 4 * j + 1] ^ sgn,
                                            v[EC * h + 4 * j + 2] ^ sgn, v[EC * h + 4 * j + 3] ^ sgn);
                 const int sw = EC == 32 ? (j ^ (lane & 7)) : (j ^ ((lane >> 1) & 3));
-                *reinterpret_cast<uint4*>(buf + lane * (EC * 4) + sw * 16) = w;
+                sts128(smem_u32(buf) + lane * (EC * 4) + sw * 16, w);
               }
               asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             }
@@ -821,12 +971,6 @@ bool c_ok(const void* p, int64_t ld, int64_t m) { return pitch_ok(p, ld, 4) && (
 namespace tc {
 // x -> (hi, lo) = (tf32_rn(x), tf32_rn(x - hi)).  Packed outputs with a 16-byte row pitch `ldo`; kT writes them transposed
 // (cols x rows) through a 32x32 smem tile so both sides stay coalesced.
-// Round to the nearest tf32 (10 mantissa bits; the result's low 13 bits are 0).
-__device__ __forceinline__ float round_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
 
 // Up to four signed input views summed (Strassen S/T formation, PAPER.md:
 // 1839-1852) and split; nin = 1, coef = +1 is the plain split.
@@ -1387,6 +1531,81 @@ int launch_mm_tf32x3_multi(int device, cudaStream_t stream, int count, const voi
     return launch_tc_batch<tc::KindTF32x3W>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags, ndst, dst,
                                             sign);
   return launch_tc_batch<tc::KindTF32x3>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags, ndst, dst, sign);
+}
+
+// Strassen leaf products with the S_r / T_r formation fused into the kernel
+// (KindTF32x3F): problem q multiplies A_q = sum_t a_sign * a_terms[2q + t]
+// (n x k, K contiguous, pitch lda; t < nta[q] <= 2) by B_q, given as
+// B_q^T = sum_t b_sign * bt_terms[2q + t] (m x k, pitch ldb; t < ntb[q] <= 2),
+// and folds the product (+/-) into its ndst[q] destinations (as _multi).
+int launch_mm_tf32x3_fused(int device, cudaStream_t stream, int count, const int32_t* nta, const void* const* a_terms,
+                           const int32_t* a_sign, int64_t lda, const int32_t* ntb, const void* const* bt_terms,
+                           const int32_t* b_sign, int64_t ldb, const int32_t* ndst, void* const* dst,
+                           const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k) {
+  using K = tc::KindTF32x3F;
+  int rc;
+  if (count < 1 || count > tc::kMaxBatch || !nta || !a_terms || !a_sign || !ntb || !bt_terms || !b_sign || !ndst ||
+      !dst || !sign) {
+    set_error("paco_mm_tf32x3_fused: count=%d (1..%d) and every term / destination array required", count,
+              tc::kMaxBatch);
+    return PACO_ERR_ARG;
+  }
+  if (n <= 0 || m <= 0 || k <= 0) return PACO_OK;
+  if (n > INT32_MAX || m > INT32_MAX || k > INT32_MAX) {
+    set_error("tcgen05 path: extents must fit int32");
+    return PACO_ERR_ARG;
+  }
+  for (int q = 0; q < count; ++q) {
+    if (nta[q] < 1 || nta[q] > K::NT || ntb[q] < 1 || ntb[q] > K::NT) {
+      set_error("paco_mm_tf32x3_fused: problem %d has %d / %d operand terms (1..%d)", q, nta[q], ntb[q], K::NT);
+      return PACO_ERR_ARG;
+    }
+    for (int t = 0; t < nta[q]; ++t)
+      if (!a_terms[2 * q + t] || !pitch_ok(a_terms[2 * q + t], lda, 4)) {
+        set_error("paco_mm_tf32x3_fused: A term %d of problem %d needs a 16-byte aligned start and pitch", t, q);
+        return PACO_ERR_UNSUPPORTED;
+      }
+    for (int t = 0; t < ntb[q]; ++t)
+      if (!bt_terms[2 * q + t] || !pitch_ok(bt_terms[2 * q + t], ldb, 4)) {
+        set_error("paco_mm_tf32x3_fused: B^T term %d of problem %d needs a 16-byte aligned start and pitch", t, q);
+        return PACO_ERR_UNSUPPORTED;
+      }
+    if (ndst[q] < 1 || ndst[q] > 4) {
+      set_error("paco_mm_tf32x3_fused: problem %d has %d destinations (1..4)", q, ndst[q]);
+      return PACO_ERR_ARG;
+    }
+    for (int d = 0; d < ndst[q]; ++d)
+      if (!c_ok(dst[4 * q + d], ldc, m)) {
+        set_error("paco_mm_tf32x3_fused: C needs a 16-byte aligned start, row pitch and row length");
+        return PACO_ERR_UNSUPPORTED;
+      }
+  }
+  Scratch sc;
+  static tc::TcMaps maps;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  constexpr CUtensorMapSwizzle SW = CU_TENSOR_MAP_SWIZZLE_64B;
+  for (int q = 0; q < count; ++q) {
+    tc::TcProb& P = maps.p[q];
+    for (int t = 0; t < K::NT; ++t) {  // unused term slots repeat term 0 (never loaded)
+      const int ta = t < nta[q] ? t : 0, tb = t < ntb[q] ? t : 0;
+      if ((rc = make_map(&P.a[t], K::DT, 4, a_terms[2 * q + ta], n, k, lda, K::BK, tc::BM, &P.a_col0[t], SW)))
+        return rc;
+      if ((rc = make_map(&P.b[t], K::DT, 4, bt_terms[2 * q + tb], m, k, ldb, K::BK, K::BN, &P.b_col0[t], SW)))
+        return rc;
+    }
+    P.nta = nta[q];
+    P.ntb = ntb[q];
+    P.sga = (a_sign[2 * q] < 0 ? 1u : 0u) | (nta[q] > 1 && a_sign[2 * q + 1] < 0 ? 2u : 0u);
+    P.sgb = (b_sign[2 * q] < 0 ? 1u : 0u) | (ntb[q] > 1 && b_sign[2 * q + 1] < 0 ? 2u : 0u);
+    if ((rc = build_output<K>(P, dst[4 * q], ldc, n, m))) return rc;
+    P.ndst = ndst[q];
+    for (int d = 0; d < ndst[q]; ++d) {
+      if (sign[4 * q + d] < 0) P.neg |= 1u << d;
+      if (d > 0 && (rc = build_output<K>(P, dst[4 * q + d], ldc, n, m, &P.cx[d - 1], &P.cx_col0[d - 1]))) return rc;
+    }
+  }
+  return run_tc<K>(device, sc, stream, maps, count, n, m, k, 0);
 }
 
 int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,

@@ -463,6 +463,98 @@ def _strassen_tc_fused(A: View, B: View, dests, base: int, stream) -> None:
             _lincomb(nat.DT_F32, stream, D, [(sd, M)], accumulate=True)
 
 
+def _tquad(q: str) -> str:
+    """Quadrant (r, c) of B is quadrant (c, r) of B^T."""
+    return q[1] + q[0]
+
+
+def _transpose(src: View, stream) -> View:
+    """A fresh row-major src^T (paco_transpose)."""
+    out = View.of(torch.empty((src.cols, src.rows), dtype=torch.float32, device=src.device))
+    nat.check(nat.load().paco_transpose(src.device, stream.cuda_stream, 4, out.ptr, out.ld, src.ptr, src.ld, src.rows,
+                                        src.cols))
+    return out
+
+
+def _leaf_level_fused(A: View, Bt: View, dests, stream) -> None:
+    """Leaf-level node, B given transposed: its seven products M_r = S_r T_r as
+    ONE paco_mm_tf32x3_fused launch.  S_r's terms are A's quadrants, T_r^T's
+    are B^T's (transposed quadrant names); the kernel forms each operand tile
+    and splits it into tf32 hi/lo in shared memory, and the epilogue folds M_r
+    (+/-) into every C block it lands in -- no split launches, no hi/lo or M
+    buffers in HBM."""
+    h = A.rows // 2
+    nta, ntb = (ctypes.c_int32 * 7)(), (ctypes.c_int32 * 7)()
+    at, bt = (ctypes.c_void_p * 14)(), (ctypes.c_void_p * 14)()
+    asg, bsg = (ctypes.c_int32 * 14)(), (ctypes.c_int32 * 14)()
+    ndst, dst, sign = (ctypes.c_int32 * 7)(), (ctypes.c_void_p * 28)(), (ctypes.c_int32 * 28)()
+    ld = None
+    for r in range(1, 8):
+        q = r - 1
+        nta[q], ntb[q] = len(S_TERMS[r]), len(T_TERMS[r])
+        for t, (c, qq) in enumerate(S_TERMS[r]):
+            at[2 * q + t], asg[2 * q + t] = _quad(A, qq).ptr, c
+        for t, (c, qq) in enumerate(T_TERMS[r]):
+            bt[2 * q + t], bsg[2 * q + t] = _quad(Bt, _tquad(qq)).ptr, c
+        targets = [(_quad(D, qq), sd * c) for D, sd in dests for c, qq in M_DESTS[r]]
+        if len(targets) > 4:
+            raise ValueError("a leaf product folds into at most 4 C blocks")
+        ndst[q] = len(targets)
+        for d, (v, sg) in enumerate(targets):
+            dst[4 * q + d], sign[4 * q + d] = v.ptr, sg
+            if ld is None:
+                ld = v.ld
+            elif v.ld != ld:
+                raise ValueError("destinations must share one row pitch")
+    nat.check(nat.load().paco_mm_tf32x3_fused(A.device, stream.cuda_stream, 7, nta, at, asg, A.ld, ntb, bt, bsg, Bt.ld,
+                                              ndst, dst, sign, ld, h, h, h))
+
+
+def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream) -> None:
+    """dests (+/-)= A x B for the fp32 (3xTF32) ring with B given as B^T (the
+    fused-producer path): S_r from A's quadrants and T_r^T from B^T's, formed
+    by lincomb above the leaf level only; at the leaf level the formation runs
+    inside the GEMM (``_leaf_level_fused``).  C combinations fold into the leaf
+    epilogues as in ``_strassen_tc_fused``."""
+    n = A.rows
+    if _leaf_level(n, base) and len(dests) <= 2:
+        _leaf_level_fused(A, Bt, dests, stream)
+        return
+    h = n // 2
+    dev = A.device
+
+    def formed(src: View, terms, transpose: bool) -> View:
+        names = [(_tquad(q) if transpose else q) for _, q in terms]
+        if len(terms) == 1 and terms[0][0] == 1:
+            return _quad(src, names[0])
+        out = View.of(torch.empty((h, h), dtype=torch.float32, device=dev))
+        _lincomb(nat.DT_F32, stream, out, [(c, _quad(src, nm)) for (c, _), nm in zip(terms, names)])
+        return out
+
+    for r in range(1, 8):
+        S = formed(A, S_TERMS[r], False)
+        Tt = formed(Bt, T_TERMS[r], True)
+        child = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
+        fits = len(child) <= (2 if _leaf_level(h, base) else 1)
+        if h > base and h % 2 == 0 and fits:
+            _strassen_tc_fused_t(S, Tt, child, base, stream)
+            continue
+        M = View.of(torch.empty((h, h), dtype=torch.float32, device=dev))
+        _strassen_dev(S, _transpose(Tt, stream), M, base, torch.float32, stream)
+        for D, sd in child:
+            _lincomb(nat.DT_F32, stream, D, [(sd, M)], accumulate=True)
+
+
+def _fused_producer_ok(n: int, base: int) -> bool:
+    """The fused-formation leaves apply: a square power-of-two-halving chain down
+    to a leaf level whose blocks keep 16-byte aligned quadrant views."""
+    while n > base and n % 2 == 0:
+        if _leaf_level(n, base):
+            return (n // 2) % 4 == 0
+        n //= 2
+    return False
+
+
 def _leaf_multi(A: View, B: View, dests, stream) -> None:
     """One 3xTF32 leaf product folded (+/-) into <= 4 blocks (count-1 batch)."""
     n, k = A.rows, A.cols
@@ -513,6 +605,13 @@ def strassen_into(A: View, B: View, dests, base: int, stream) -> bool:
 # fp32 Strassen: fold the C-block combination into the leaf epilogues (True, the
 # measured default) or materialise M buffers + lincomb (False; kept for A/B runs)
 FUSED_COMBINE = True
+# Form the leaf operands inside the 3xTF32 GEMM from B^T quadrants
+# (paco_mm_tf32x3_fused) instead of split launches.  Off: measured slower on
+# cfg5 (44 vs 34 ms) -- the in-smem formation adds ~89 KB
+# of shared-memory traffic per 16-deep k block to the MMAs' 72 KB and the
+# TMA's 48 KB, and the kernel is shared-memory-bandwidth bound (ncu: LSU
+# wavefronts 76 % of peak, tensor pipe 51 % active).
+FUSED_PRODUCER = False
 
 
 def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stream) -> None:
@@ -524,7 +623,10 @@ def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stre
     h = C.rows // 2
     if kid == nat.SR_F32_TC and FUSED_COMBINE and (C.ld * 4) % 16 == 0 and C.ptr % 16 == 0:
         launch_fill(nat.SR_F32, stream, C)
-        _strassen_tc_fused(A, B, [(C, 1)], base, stream)
+        if FUSED_PRODUCER and _fused_producer_ok(C.rows, base) and A.ptr % 16 == 0 and (A.ld * 4) % 16 == 0:
+            _strassen_tc_fused_t(A, _transpose(B, stream), [(C, 1)], base, stream)
+        else:
+            _strassen_tc_fused(A, B, [(C, 1)], base, stream)
         return
     if kid == nat.SR_F32_TC and (h <= base or h % 2) and h % 4 == 0:
         _leaf_level_tf32(A, B, C, stream)

@@ -1,0 +1,24 @@
+"""One cfg5 leaf-level launch of the fused-formation 3xTF32 kernel (for ncu)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_2011_01441_b200 import strassen as S
+from paper_2011_01441_b200.device import View
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192   # a level-1 node: 7 leaf products of n/2
+S.FUSED_PRODUCER = sys.argv[2] != "split" if len(sys.argv) > 2 else True
+g = torch.Generator(device="cuda").manual_seed(1)
+a = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+c = torch.zeros(n, n, device="cuda")
+st = torch.cuda.current_stream()
+for _ in range(2):
+    if S.FUSED_PRODUCER:
+        S._leaf_level_fused(View.of(a), View.of(b.t().contiguous()), [(View.of(c), 1)], st)
+    else:
+        S._leaf_level_multi(View.of(a), View.of(b), [(View.of(c), 1)], st)
+torch.cuda.synchronize()
+print("ok")
