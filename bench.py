@@ -289,6 +289,14 @@ def measure_config(cfg, dev, args, peaks, probes):
                                                    if clocks.get("sm_mhz") else None),
                              "traffic": traffic, "traffic_source": src, "algorithmic_bytes": 3 * n * n * 4},
                    clocks=clocks)
+        if cfg == 2:
+            # the north star's second PACO level as the CTA plan (MM-1-Piece over 148 x 2 x 4 workers)
+            # beside the default tile grid, same launches, same inputs
+            paco_ms = _events_time(lambda: launch_mm(kid, st, av, bv, cv, flags=nat.MM_PACO_PLAN), 3, 1, st)
+            out["cta_plan_compare"] = {
+                "tile_grid_ms": ms, "paco_cuboid_plan_ms": paco_ms,
+                "paco_cuboid_plan": "PACO_MM_PACO_PLAN: paco_plan_cta's MM-1-Piece over the (128, 128, 4) unit grid "
+                                    "for p = 1184 workers (DESIGN.md section 5)"}
         out["_tensors"] = (a, b, c)
         return out
     if cfg == 3:

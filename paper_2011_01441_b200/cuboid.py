@@ -14,7 +14,8 @@ once both sides finished.  Reference behaviour followed (file:line in
 * ``mm_one_piece_partition``  -- 246-300
 * ``mm_hetero_partition``     -- 303-339
 
-The same geometry is reused one level down (``tiling.py``) to spread one
+The same geometry is reused one level down (``csrc/cta_plan.cuh``, the
+PACO CTA plan ``paco_plan_cta`` / ``PACO_MM_PACO_PLAN``) to spread one
 device's cuboid over its 148 SMs.
 """
 
