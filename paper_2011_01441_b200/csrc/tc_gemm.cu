@@ -845,6 +845,288 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   }
 }
 
+// ---------------------------------------------------------------------------
+// 3xTF32 on a CTA PAIR (tcgen05 cta_group::2) -- the Strassen leaf GEMM.
+//
+// The single-CTA kernel moves, per 16-deep k block of a 128 x 256 tile, 48 KB
+// of TMA writes and 72 KB of MMA operand reads (three passes) through one
+// SM's shared memory -- ~940 clocks at 128 B/clk against ~1000 clocks of
+// tf32 MMA work, so the tensor pipe stalls on shared memory.  A CTA pair
+// issues M = 256 x N = 256 MMAs: each CTA holds its 128 rows of A and HALF of
+// B^T (128 rows), so per CTA the stage is 32 KB of TMA writes and 48 KB of
+// operand reads for the same 128 x 256 of output.  The leader CTA (rank 0)
+// issues every MMA; both CTAs' TMA loads complete on the leader's stage
+// barrier; the leader's commits arrive on both CTAs' barriers (multicast);
+// each CTA drains its own TMEM half (its 128 rows) and the peer's epilogue
+// releases the accumulator with a remote arrive on the leader's barrier.
+// Tiles (256 x 256 of C) are dealt to pairs statically in row-band order.
+// ---------------------------------------------------------------------------
+template <int ST>
+struct PairLayout {
+  static constexpr int BK = 16, BN = 256, BNH = 128, EC = 16, EW = 4, EB = 2;
+  static constexpr int A_BYTES = BM * BK * 4;          // 8 KB: 128 rows x 16 fp32
+  static constexpr int B_BYTES = BNH * BK * 4;         // 8 KB: this CTA's half of B^T
+  static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
+  static constexpr int SMEM_EPI = ST * STAGE_BYTES;
+  static constexpr int EPI_BUF = 32 * EC * 4;
+  static constexpr int SMEM_BAR = SMEM_EPI + EW * EB * EPI_BUF;
+  static constexpr int THREADS = 64 + 32 * EW;
+  static constexpr int SMEM_ALLOC = SMEM_BAR + 512 + 1024;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
+  // F32 accumulate, TF32 A/B (both K-major), N = 256, M = 256 (cta_group::2)
+  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(BN >> 3) << 17) |
+                                    (uint32_t(256 >> 4) << 24);
+  __device__ static int a_off(int s, int o) { return s * STAGE_BYTES + o * A_BYTES; }
+  __device__ static int b_off(int s, int o) { return s * STAGE_BYTES + 2 * A_BYTES + o * B_BYTES; }
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// arrive on an mbarrier given by its shared::cluster address (own or the peer's)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+// TMA load into this CTA's smem completing on a barrier in either CTA of the pair
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit: arrive on the barrier at this offset in BOTH CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+
+// tile t (of all problems) -> (problem, 256-row block, 256-column block), row-band walk
+__device__ __forceinline__ void pair_tile(const TcArgs& a, int32_t t, int& q, int& rb, int& nb) {
+  const int32_t tpp = a.tiles_rb * a.tiles_nb;
+  q = t / tpp;
+  const int32_t u = t % tpp;
+  const int32_t band = u / (kRowBand * a.tiles_nb), r0 = band * kRowBand;
+  const int32_t rows = a.tiles_rb - r0 < kRowBand ? a.tiles_rb - r0 : kRowBand;
+  const int32_t v = u - r0 * a.tiles_nb;
+  nb = v / rows;
+  rb = r0 + v % rows;
+}
+
+template <int ST>
+__global__ void __launch_bounds__(PairLayout<ST>::THREADS, 1)
+    tc_pair_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
+  using L = PairLayout<ST>;
+  constexpr int BK = L::BK, BN = L::BN;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::SMEM_BAR);
+  uint64_t* empty = full + 16;
+  uint64_t* tfull = empty + 16;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  int32_t pair, npairs;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(pair));
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(npairs));
+  const int32_t total = args.tiles_rb * args.tiles_nb * args.count;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * L::EW);  // both CTAs' epilogue warps release the (pair) accumulator
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int q = 0; q < args.count; ++q) {
+      for (int o = 0; o < 2; ++o) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.p[q].a[o])) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.p[q].b[o])) : "memory");
+      }
+    }
+  }
+  if (warp == 1) {
+    // one warp in EACH CTA of the pair (tools/microbench/pair_probe.cu)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's barriers are initialised before any remote complete_tx / arrive
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs: own A rows, own half of B^T) ----------------
+      const uint32_t full_leader0 = mapa_rank(smem_u32(&full[0]), 0);
+      uint32_t it = 0;
+      for (int32_t t = pair; t < total; t += npairs) {
+        int q, rb, nb;
+        pair_tile(args, t, q, rb, nb);
+        const TcProb& P = maps.p[q];
+        const int arow = rb * 256 + int(rank) * BM, brow = nb * BN + int(rank) * L::BNH;
+        for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
+          const uint32_t fb = full_leader0 + uint32_t(s) * 8u;
+          if (leader) mbar_expect_tx_relaxed(&full[s], 2 * L::STAGE_BYTES);
+#pragma unroll
+          for (int o = 0; o < 2; ++o) {
+            tma_load_2d_pair(smem + L::a_off(s, o), &P.a[o], fb, P.a_col0[o] + kb * BK, arow);
+            tma_load_2d_pair(smem + L::b_off(s, o), &P.b[o], fb, P.b_col0[o] + kb * BK, brow);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ---------------- MMA issuer (leader CTA only) ----------------
+      uint32_t it = 0;
+      int tile = 0;
+      for (int32_t t = pair; t < total; t += npairs, ++tile) {
+        const int a = tile & 1;
+        const uint32_t use = uint32_t(tile >> 1);
+        mbar_wait(&tempty[a], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(a * BN);
+        for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&full[s], (it / ST) & 1);
+          tc_fence_after();
+          const uint64_t ad[2] = {smem_desc_sw64(smem_u32(smem + L::a_off(s, 0))),
+                                  smem_desc_sw64(smem_u32(smem + L::a_off(s, 1)))};
+          const uint64_t bd[2] = {smem_desc_sw64(smem_u32(smem + L::b_off(s, 0))),
+                                  smem_desc_sw64(smem_u32(smem + L::b_off(s, 1)))};
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+#pragma unroll
+            for (int ps = 0; ps < 3; ++ps) {  // hi*hi, hi*lo, lo*hi
+              const int ao = ps == 2 ? 1 : 0, bo = ps == 1 ? 1 : 0;
+              umma_pair(d_tmem, ad[ao] + uint64_t(2 * kk), bd[bo] + uint64_t(2 * kk), L::IDESC, (kb | kk | ps) != 0);
+            }
+          umma_commit_pair(&empty[s]);  // both CTAs' stage s is free once these MMAs complete
+        }
+        umma_commit_pair(&tfull[a]);    // both CTAs' accumulator halves are ready
+      }
+    }
+  } else {
+    // ---------------- epilogue warps (both CTAs: own 128 rows of the pair tile) ----------------
+    const int q4 = warp % 4;  // TMEM lane quadrant
+    const int ew = warp - 2;
+    unsigned char* stage0 = smem + L::SMEM_EPI + ew * L::EB * L::EPI_BUF;
+    const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty[0]), 0);
+    int tile = 0;
+    uint32_t box = 0;
+    for (int32_t t = pair; t < total; t += npairs, ++tile) {
+      int pq, rb, nb;
+      pair_tile(args, t, pq, rb, nb);
+      const TcProb& P = maps.p[pq];
+      const int a = tile & 1;
+      const uint32_t use = uint32_t(tile >> 1);
+      mbar_wait(&tfull[a], use & 1);
+      tc_fence_after();
+      const int row0 = rb * 256 + int(rank) * BM + 32 * q4;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; c += 2) {
+        uint32_t v[64];
+        const uint32_t taddr = tmem_base + (uint32_t(32 * q4) << 16) + uint32_t(a * BN + 32 * c);
+#define PACO_R8(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), "=r"(v[i + 5]), \
+                   "=r"(v[i + 6]), "=r"(v[i + 7])
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, "
+            "%34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, "
+            "%54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];\n"
+            : PACO_R8(0), PACO_R8(8), PACO_R8(16), PACO_R8(24), PACO_R8(32), PACO_R8(40), PACO_R8(48), PACO_R8(56)
+            : "r"(taddr));
+#undef PACO_R8
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (c + 2 == BN / 32) {
+          tc_fence_before();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader0 + uint32_t(a) * 8u);
+        }
+        const int col0 = nb * BN + 32 * c;
+        if (col0 >= args.m) continue;
+        constexpr int EC = L::EC, SUBS = 64 / EC, EB = L::EB;
+#pragma unroll
+        for (int h = 0; h < SUBS; ++h) {
+          if (col0 + EC * h >= args.m) break;
+#pragma unroll 1
+          for (int d = 0; d < P.ndst; ++d) {
+            const uint32_t sgn = ((P.neg >> d) & 1u) << 31;
+            unsigned char* buf = stage0 + (box % EB) * L::EPI_BUF;
+            ++box;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(EB - 1) : "memory");
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < EC / 4; ++j) {
+              const uint4 w = make_uint4(v[EC * h + 4 * j] ^ sgn, v[EC * h + 4 * j + 1] ^ sgn,
+                                         v[EC * h + 4 * j + 2] ^ sgn, v[EC * h + 4 * j + 3] ^ sgn);
+              const int sw = j ^ ((lane >> 1) & 3);  // 64B swizzle of the [32][16 fp32] box
+              sts128(smem_u32(buf) + lane * (EC * 4) + sw * 16, w);
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              if (row0 < args.n) {
+                const CUtensorMap* cm = d == 0 ? &P.c : &P.cx[d - 1];
+                const int cc0 = d == 0 ? P.c_col0 : P.cx_col0[d - 1];
+                if (args.overwrite)
+                  tma_store_2d(cm, buf, cc0 + col0 + EC * h, row0);
+                else
+                  tma_reduce_add_2d(cm, buf, cc0 + col0 + EC * h, row0);
+              }
+              asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            }
+          }
+        }
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // no MMA of the pair writes TMEM and no remote arrive is pending any more
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(L::TMEM_COLS));
+  }
+}
+
 }  // namespace tc
 
 namespace {
@@ -1470,6 +1752,92 @@ int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* 
   return run_tc<K>(device, sc, stream, maps, count, n, m, k, flags);
 }
 
+#ifndef PACO_PAIR_ST
+#define PACO_PAIR_ST 6
+#endif
+// 3xTF32 batch on CTA pairs (tc_pair_kernel): same contract as launch_tc_batch
+// for pre-split operands, optional destination lists.
+int launch_tc_pair(int device, cudaStream_t stream, int count, const Presplit* pre, int64_t lda, int64_t ldb,
+                   int64_t ldc, int64_t n, int64_t m, int64_t k, int flags, const int32_t* ndst, void* const* dst,
+                   const int32_t* sign) {
+  using L = tc::PairLayout<PACO_PAIR_ST>;
+  int rc;
+  constexpr CUtensorMapSwizzle SW = CU_TENSOR_MAP_SWIZZLE_64B;
+  static tc::TcMaps maps;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int q = 0; q < count; ++q) {
+    const Presplit& p = pre[q];
+    if (!pitch_ok(p.ah, lda, 4) || !pitch_ok(p.al, lda, 4) || !pitch_ok(p.bh, ldb, 4) || !pitch_ok(p.bl, ldb, 4)) {
+      set_error("paco_mm_tf32x3: operand row pitches must be multiples of 16 bytes");
+      return PACO_ERR_UNSUPPORTED;
+    }
+    tc::TcProb& P = maps.p[q];
+    if ((rc = make_map(&P.a[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.ah, n, k, lda, L::BK, tc::BM, &P.a_col0[0], SW)) ||
+        (rc = make_map(&P.a[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.al, n, k, lda, L::BK, tc::BM, &P.a_col0[1], SW)) ||
+        (rc = make_map(&P.b[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.bh, m, k, ldb, L::BK, L::BNH, &P.b_col0[0], SW)) ||
+        (rc = make_map(&P.b[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.bl, m, k, ldb, L::BK, L::BNH, &P.b_col0[1], SW)))
+      return rc;
+    const int nd = ndst ? ndst[q] : 1;
+    P.ndst = nd;
+    P.neg = 0;
+    for (int d = 0; d < nd; ++d) {
+      void* c = ndst ? dst[4 * q + d] : p.c;
+      if (ndst && sign[4 * q + d] < 0) P.neg |= 1u << d;
+      if ((rc = make_map(d == 0 ? &P.c : &P.cx[d - 1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c, n, m, ldc, L::EC, 32,
+                         d == 0 ? &P.c_col0 : &P.cx_col0[d - 1], SW)))
+        return rc;
+    }
+  }
+  tc::TcArgs args{};
+  args.n = n;
+  args.m = m;
+  args.k = k;
+  args.count = count;
+  args.overwrite = (flags & PACO_MM_OVERWRITE) ? 1 : 0;
+  args.tiles_rb = int32_t((n + 255) / 256);
+  args.tiles_nb = int32_t((m + L::BN - 1) / L::BN);
+  args.kblocks = int32_t((k + L::BK - 1) / L::BK);
+  args.groups = 1;
+  const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb * count;
+  const int pairs = int(tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
+  auto kern = tc::tc_pair_kernel<PACO_PAIR_ST>;
+  {
+    static std::atomic<uint64_t> attr_set{0};
+    const uint64_t bit = uint64_t(1) << (device & 63);
+    if (!(attr_set.load() & bit)) {
+      PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
+      attr_set.fetch_or(bit);
+    }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(2 * pairs));
+  cfg.blockDim = dim3(L::THREADS);
+  cfg.dynamicSmemBytes = L::SMEM_ALLOC;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = kPdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  KernelSpan ks(PACO_KT_TC_GEMM, stream);
+  PACO_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps, args));
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
+// CTA pairs for the 3xTF32 batches with enough 256 x 256 tiles to keep the 74
+// pairs busy (Strassen's leaf levels); PACO_TF32_PAIR=0 forces single CTAs.
+bool tf32_pair(int64_t n, int64_t m, int count) {
+  static const int v = dev_knob("PACO_TF32_PAIR") ? atoi(dev_knob("PACO_TF32_PAIR")) : -1;
+  if (v >= 0) return v != 0;
+  return ((n + 255) / 256) * ((m + 255) / 256) * count >= 3 * (kNumSMs / 2);
+}
+
 // 3xTF32 tile width: N = 256 halves the B-operand traffic per output (the
 // kernel is L2-bandwidth bound at N = 128: 48 flop per loaded byte) but only
 // pays when the batch has enough tiles for the 148 SMs (4096^3 alone: 512
@@ -1512,6 +1880,17 @@ int launch_mm_tf32x3_presplit(int device, cudaStream_t stream, int count, const 
     return PACO_ERR_ARG;
   }
   for (int q = 0; q < count; ++q) pre[q] = Presplit{ah[q], al[q], bth[q], btl[q], C[q]};
+  if (tf32_pair(n, m, count)) {
+    for (int q = 0; q < count; ++q) {
+      int rc = check_tc_call<tc::KindTF32x3W>(C[q], ldc, n, m, k, nullptr, 0, flags);
+      if (rc) return rc;
+      if (!c_ok(C[q], ldc, m)) {
+        set_error("paco_mm_tf32x3: C needs a 16-byte aligned start, row pitch and row length");
+        return PACO_ERR_UNSUPPORTED;
+      }
+    }
+    return launch_tc_pair(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags, nullptr, nullptr, nullptr);
+  }
   if (tf32_wide(n, m, count))
     return launch_tc_batch<tc::KindTF32x3W>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags);
   return launch_tc_batch<tc::KindTF32x3>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags);
@@ -1527,6 +1906,20 @@ int launch_mm_tf32x3_multi(int device, cudaStream_t stream, int count, const voi
     return PACO_ERR_ARG;
   }
   for (int q = 0; q < count; ++q) pre[q] = Presplit{ah[q], al[q], bth[q], btl[q], dst[4 * q]};
+  if (tf32_pair(n, m, count)) {
+    for (int q = 0; q < count; ++q) {
+      if (ndst[q] < 1 || ndst[q] > 4) {
+        set_error("paco_mm_tf32x3_multi: problem %d has %d destinations (1..4)", q, ndst[q]);
+        return PACO_ERR_ARG;
+      }
+      for (int d = 0; d < ndst[q]; ++d)
+        if (!c_ok(dst[4 * q + d], ldc, m)) {
+          set_error("paco_mm_tf32x3: C needs a 16-byte aligned start, row pitch and row length");
+          return PACO_ERR_UNSUPPORTED;
+        }
+    }
+    return launch_tc_pair(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags, ndst, dst, sign);
+  }
   if (tf32_wide(n, m, count))
     return launch_tc_batch<tc::KindTF32x3W>(device, stream, count, pre, lda, ldb, ldc, n, m, k, flags, ndst, dst,
                                             sign);

@@ -146,3 +146,43 @@ def test_fused_rounding_bit_identical_to_split_path():
                                        (ctypes.c_int32 * 4)(1, 1, 1, 1), m, n, m, k))
     torch.cuda.synchronize()
     assert torch.equal(c_fused, c_split)
+
+
+@pytest.mark.parametrize("shape", [(2048, 2048, 256, 4), (2000, 1800, 333, 8)])
+def test_cta_pair_kernel_multi_destination(shape):
+    """Batches big enough for the CTA-pair 3xTF32 kernel (tcgen05 cta_group::2:
+    M = 256 per pair, each CTA holding half of B^T), ragged extents, two signed
+    destinations per product; vs the float64 products."""
+    n, m, k, cnt = shape
+    lib = nat.load()
+    st = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(n + cnt)
+    kp = (k + 3) // 4 * 4
+    a = [(torch.rand(n, kp, device="cuda", generator=g) * 2 - 1) for _ in range(cnt)]
+    b = [(torch.rand(m, kp, device="cuda", generator=g) * 2 - 1) for _ in range(cnt)]
+    for x in a + b:
+        x[:, k:] = 0
+    hl = []
+    for x in a + b:
+        h, lo = torch.empty_like(x), torch.empty_like(x)
+        nat.check(lib.paco_tf32_split(0, st, 1, (ctypes.c_void_p * 1)(x.data_ptr()), (ctypes.c_int64 * 1)(kp),
+                                      (ctypes.c_int32 * 1)(1), x.shape[0], k, 0, h.data_ptr(), lo.data_ptr(), kp))
+        hl.append((h, lo))
+    arr = lambda xs: (ctypes.c_void_p * cnt)(*[x.data_ptr() for x in xs])  # noqa: E731
+    C = [torch.zeros(n, m, device="cuda") for _ in range(2)]
+    ndst = (ctypes.c_int32 * cnt)(*[2] * cnt)
+    dst = (ctypes.c_void_p * (4 * cnt))()
+    sign = (ctypes.c_int32 * (4 * cnt))()
+    ref = [torch.zeros(n, m, dtype=torch.float64, device="cuda") for _ in range(2)]
+    for q in range(cnt):
+        dst[4 * q], dst[4 * q + 1] = C[q % 2].data_ptr(), C[(q + 1) % 2].data_ptr()
+        sign[4 * q], sign[4 * q + 1] = 1, (-1 if q % 2 else 1)
+        p = a[q][:, :k].double() @ b[q][:, :k].double().t()
+        ref[q % 2] += p
+        ref[(q + 1) % 2] += -p if q % 2 else p
+    nat.check(lib.paco_mm_tf32x3_multi(0, st, cnt, arr([x[0] for x in hl[:cnt]]), arr([x[1] for x in hl[:cnt]]), kp,
+                                       arr([x[0] for x in hl[cnt:]]), arr([x[1] for x in hl[cnt:]]), kp, ndst, dst,
+                                       sign, m, n, m, k))
+    torch.cuda.synchronize()
+    for i in range(2):
+        assert float((C[i].double() - ref[i]).norm() / ref[i].norm()) < 1e-5, i
