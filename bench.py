@@ -374,7 +374,8 @@ def measure_config(cfg, dev, args, peaks, probes):
                    step="strassen_seq(A, B, 16384, base=4096): 2 Strassen levels, 49 leaf products on tcgen05 as "
                         "3xTF32 (7 batched launches), C combination fused into the leaf epilogues",
                    l2="A, B 1 GiB each > 126 MB L2 (no flush)",
-                   roofline={"bound": "tensor", "kernel": "tc_gemm_kernel<KindTF32x3> (Strassen leaves)",
+                   roofline={"bound": "tensor", "kernel": "tc_pair_kernel (3xTF32 Strassen leaves on CTA pairs, "
+                                                           "tcgen05 cta_group::2)",
                              "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
                              "achieved_note": "3 x 7 x 2 x 4096^3 MMA flop per launch / its average CUDA-event "
                                               "duration inside the step",
