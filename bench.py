@@ -451,7 +451,7 @@ def main():
                     help="headline config at N>1 (GPU-level PACO plan of that BASELINE config)")
     ap.add_argument("--configs", default="1,2,3,4,5",
                     help="N=1: BASELINE configs measured into the line's `configs` ('none' to skip)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--ref-rows", type=int, default=24, help="rows of A per host process (reference arm)")
     ap.add_argument("--ref-threaded-rows", type=int, default=32, help="rows of A for the threaded-mode sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
