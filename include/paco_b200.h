@@ -228,6 +228,17 @@ int paco_mm_tf32x3_fused(int device, void* stream, int count, const int32_t* nta
                          const int32_t* b_sign, int64_t ldb, const int32_t* ndst, void* const* dst,
                          const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k);
 
+/* The leaf level on CTA pairs with only the A side formed in the kernel: A_q =
+ * sum_{t < nta[q] <= 2} a_sign * a_terms[2q+t] (n x k, pitch lda) is TMA'd raw and
+ * split into tf32 hi/lo in shared memory; B_q^T comes pre-split (bt_hi / bt_lo,
+ * m x k, pitch ldb, from paco_tf32_split); destinations as _multi.  The A-side
+ * split launches disappear while each SM's shared-memory traffic stays under
+ * its bandwidth (the pair halves the B bytes per SM). */
+int paco_mm_tf32x3_fused_a(int device, void* stream, int count, const int32_t* nta, const void* const* a_terms,
+                           const int32_t* a_sign, int64_t lda, const void* const* bt_hi, const void* const* bt_lo,
+                           int64_t ldb, const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc,
+                           int64_t n, int64_t m, int64_t k);
+
 /* dst (cols x rows, pitch ld_dst) = src^T (rows x cols, pitch ld_src); 4- or
  * 8-byte elements.  Strassen transposes B once so every T_r^T operand of the
  * fused leaves is a K-major view. */

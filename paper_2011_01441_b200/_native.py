@@ -82,6 +82,10 @@ SIGNATURES = {
                                     ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), _i64,
                                     ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32),
                                     _i64, _i64, _i64, _i64]),
+    "paco_mm_tf32x3_fused_a": (_int, [_int, _vp, _int, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_vp),
+                                      ctypes.POINTER(ctypes.c_int32), _i64, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                      _i64, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_vp),
+                                      ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
     "paco_transpose": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_copy2d": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_device_alloc": (_int, [_int, ctypes.c_size_t, ctypes.POINTER(_vp)]),

@@ -88,6 +88,10 @@ int launch_mm_tf32x3_fused(int device, cudaStream_t stream, int count, const int
                            const int32_t* a_sign, int64_t lda, const int32_t* ntb, const void* const* bt_terms,
                            const int32_t* b_sign, int64_t ldb, const int32_t* ndst, void* const* dst,
                            const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k);
+int launch_mm_tf32x3_fused_a(int device, cudaStream_t stream, int count, const int32_t* nta,
+                             const void* const* a_terms, const int32_t* a_sign, int64_t lda, const void* const* bt_hi,
+                             const void* const* bt_lo, int64_t ldb, const int32_t* ndst, void* const* dst,
+                             const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k);
 int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,
                       const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* lo,
                       int64_t ldo);
@@ -444,6 +448,23 @@ int paco_mm_tf32x3_fused(int device, void* stream, int count, const int32_t* nta
   PACO_TRY(dg.use(device));
   return launch_mm_tf32x3_fused(device, static_cast<cudaStream_t>(stream), count, nta, a_terms, a_sign, lda, ntb,
                                 bt_terms, b_sign, ldb, ndst, dst, sign, ldc, n, m, k);
+}
+
+int paco_mm_tf32x3_fused_a(int device, void* stream, int count, const int32_t* nta, const void* const* a_terms,
+                           const int32_t* a_sign, int64_t lda, const void* const* bt_hi, const void* const* bt_lo,
+                           int64_t ldb, const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc,
+                           int64_t n, int64_t m, int64_t k) {
+  if (count >= 1 && nta && a_terms && bt_hi && bt_lo && ndst && dst)
+    for (int q = 0; q < count && q < 8; ++q) {
+      for (int t = 0; t < nta[q] && t < 2; ++t) PACO_TRY(check_view("A term", a_terms[2 * q + t], lda, n, k));
+      PACO_TRY(check_view("Bt_hi", bt_hi[q], ldb, m, k));
+      PACO_TRY(check_view("Bt_lo", bt_lo[q], ldb, m, k));
+      for (int d = 0; d < ndst[q] && d < 4; ++d) PACO_TRY(check_view("C", dst[4 * q + d], ldc, n, m));
+    }
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_mm_tf32x3_fused_a(device, static_cast<cudaStream_t>(stream), count, nta, a_terms, a_sign, lda, bt_hi,
+                                  bt_lo, ldb, ndst, dst, sign, ldc, n, m, k);
 }
 
 int paco_transpose(int device, void* stream, int elsize, void* dst, int64_t ld_dst, const void* src, int64_t ld_src,

@@ -861,16 +861,20 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
 // releases the accumulator with a remote arrive on the leader's barrier.
 // Tiles (256 x 256 of C) are dealt to pairs statically in row-band order.
 // ---------------------------------------------------------------------------
-template <int ST>
+template <int ST, bool FA = false>
 struct PairLayout {
   static constexpr int BK = 16, BN = 256, BNH = 128, EC = 16, EW = 4, EB = 2;
+  // FA: A is formed in the kernel (Strassen's S_r from <= 2 signed raw views,
+  // TMA'd into the stage's hi / lo slots and split there in place by CW
+  // converter warps); B^T arrives pre-split
+  static constexpr int CW = FA ? 4 : 0;
   static constexpr int A_BYTES = BM * BK * 4;          // 8 KB: 128 rows x 16 fp32
   static constexpr int B_BYTES = BNH * BK * 4;         // 8 KB: this CTA's half of B^T
   static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
   static constexpr int SMEM_EPI = ST * STAGE_BYTES;
   static constexpr int EPI_BUF = 32 * EC * 4;
   static constexpr int SMEM_BAR = SMEM_EPI + EW * EB * EPI_BUF;
-  static constexpr int THREADS = 64 + 32 * EW;
+  static constexpr int THREADS = 64 + 32 * (EW + CW);
   static constexpr int SMEM_ALLOC = SMEM_BAR + 512 + 1024;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
@@ -936,10 +940,10 @@ __device__ __forceinline__ void pair_tile(const TcArgs& a, int32_t t, int& q, in
   rb = r0 + v % rows;
 }
 
-template <int ST>
-__global__ void __launch_bounds__(PairLayout<ST>::THREADS, 1)
+template <int ST, bool FA>
+__global__ void __launch_bounds__(PairLayout<ST, FA>::THREADS, 1)
     tc_pair_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
-  using L = PairLayout<ST>;
+  using L = PairLayout<ST, FA>;
   constexpr int BK = L::BK, BN = L::BN;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -947,7 +951,9 @@ __global__ void __launch_bounds__(PairLayout<ST>::THREADS, 1)
   uint64_t* empty = full + 16;
   uint64_t* tfull = empty + 16;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;  // FA: this CTA's raw A terms landed in stage s
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 16);
+  unsigned char* sig = reinterpret_cast<unsigned char*>(rfull + 18);  // FA: 2 x 16 B signal landing slots
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
@@ -959,8 +965,9 @@ __global__ void __launch_bounds__(PairLayout<ST>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 1);  // the leader's expect_tx; TMA and (FA) converter signals complete it
       mbar_init(&empty[s], 1);
+      mbar_init(&rfull[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -1002,11 +1009,24 @@ __global__ void __launch_bounds__(PairLayout<ST>::THREADS, 1)
           const int s = it % ST;
           mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
           const uint32_t fb = full_leader0 + uint32_t(s) * 8u;
-          if (leader) mbar_expect_tx_relaxed(&full[s], 2 * L::STAGE_BYTES);
+          if constexpr (FA) {
+            // raw A terms -> own stage (own barrier, the converters split them);
+            // pre-split B^T halves -> the leader's stage barrier
+            // B^T halves of both CTAs + both CTAs' 16-byte "A converted" signals
+            if (leader) mbar_expect_tx_relaxed(&full[s], 2 * 2 * L::B_BYTES + 2 * 16);
+            mbar_expect_tx_relaxed(&rfull[s], uint32_t(P.nta * L::A_BYTES));
 #pragma unroll
-          for (int o = 0; o < 2; ++o) {
-            tma_load_2d_pair(smem + L::a_off(s, o), &P.a[o], fb, P.a_col0[o] + kb * BK, arow);
-            tma_load_2d_pair(smem + L::b_off(s, o), &P.b[o], fb, P.b_col0[o] + kb * BK, brow);
+            for (int o = 0; o < 2; ++o) {
+              if (o < P.nta) tma_load_2d(smem + L::a_off(s, o), &P.a[o], &rfull[s], P.a_col0[o] + kb * BK, arow);
+              tma_load_2d_pair(smem + L::b_off(s, o), &P.b[o], fb, P.b_col0[o] + kb * BK, brow);
+            }
+          } else {
+            if (leader) mbar_expect_tx_relaxed(&full[s], 2 * L::STAGE_BYTES);
+#pragma unroll
+            for (int o = 0; o < 2; ++o) {
+              tma_load_2d_pair(smem + L::a_off(s, o), &P.a[o], fb, P.a_col0[o] + kb * BK, arow);
+              tma_load_2d_pair(smem + L::b_off(s, o), &P.b[o], fb, P.b_col0[o] + kb * BK, brow);
+            }
           }
         }
       }
@@ -1040,6 +1060,70 @@ __global__ void __launch_bounds__(PairLayout<ST>::THREADS, 1)
           umma_commit_pair(&empty[s]);  // both CTAs' stage s is free once these MMAs complete
         }
         umma_commit_pair(&tfull[a]);    // both CTAs' accumulator halves are ready
+      }
+    }
+  } else if (warp >= 2 + L::EW) {
+    if constexpr (FA) {
+      // ---------------- converter warps (FA, both CTAs): S_r tile formed and split in place ----------------
+      const int ct = (warp - 2 - L::EW) * 32 + lane;
+      constexpr int NTH = 32 * (L::CW > 0 ? L::CW : 1), A_CH = L::A_BYTES / 16, PER = A_CH / NTH;
+      static_assert(A_CH % NTH == 0, "whole A chunks per converter thread");
+      const uint32_t full_leader0 = mapa_rank(smem_u32(&full[0]), 0);
+      const uint32_t sig_leader = mapa_rank(smem_u32(sig), 0);
+      const uint32_t sbase = smem_u32(smem);
+      uint32_t it = 0;
+      for (int32_t t = pair; t < total; t += npairs) {
+        int q, rb, nb;
+        pair_tile(args, t, q, rb, nb);
+        const int nta = maps.p[q].nta;
+        const uint32_t sga = maps.p[q].sga;
+        for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&rfull[s], (it / ST) & 1);
+          uint4 x0[PER], x1[PER];
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const uint32_t off = sbase + L::a_off(s, 0) + (ct + u * NTH) * 16;
+            x0[u] = lds128(off);
+            if (nta > 1) x1[u] = lds128(off + L::A_BYTES);
+          }
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            float x[4] = {__uint_as_float(x0[u].x), __uint_as_float(x0[u].y), __uint_as_float(x0[u].z),
+                          __uint_as_float(x0[u].w)};
+            if (sga & 1u)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) x[e] = -x[e];
+            if (nta > 1) {
+              const float y[4] = {__uint_as_float(x1[u].x), __uint_as_float(x1[u].y), __uint_as_float(x1[u].z),
+                                  __uint_as_float(x1[u].w)};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) x[e] = (sga & 2u) ? x[e] - y[e] : x[e] + y[e];
+            }
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              h[e] = round_tf32_bits(__float_as_uint(x[e]));
+              l[e] = round_tf32_bits(__float_as_uint(x[e] - __uint_as_float(h[e])));
+            }
+            const uint32_t off = sbase + L::a_off(s, 0) + (ct + u * NTH) * 16;
+            sts128(off, make_uint4(h[0], h[1], h[2], h[3]));
+            sts128(off + L::A_BYTES, make_uint4(l[0], l[1], l[2], l[3]));
+          }
+          // generic-proxy writes -> the tensor core's async-proxy reads (of both CTAs' A halves).
+          // The handoff to the leader is itself an async-proxy op -- a 16-byte bulk copy into
+          // the leader's signal slot completing on its stage barrier -- so it needs no
+          // cluster-scope release fence (a release.cluster arrive per stage stalled the
+          // converters on ERRBAR for ~1 us each)
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          asm volatile("bar.sync 1, %0;\n" ::"n"(32 * (L::CW > 0 ? L::CW : 1)) : "memory");
+          if (ct == 0)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];\n" ::"r"(
+                    sig_leader + rank * 16u),
+                "r"(smem_u32(sig)), "r"(full_leader0 + uint32_t(s) * 8u)
+                : "memory");
+        }
       }
     }
   } else {
@@ -1757,10 +1841,14 @@ int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* 
 #endif
 // 3xTF32 batch on CTA pairs (tc_pair_kernel): same contract as launch_tc_batch
 // for pre-split operands, optional destination lists.
+// fa_terms (FA): problem q's A is the signed sum of fa_nt[q] raw views fa_terms[2q + t]
+// (pre[q].ah/al unused); B^T always pre-split.
 int launch_tc_pair(int device, cudaStream_t stream, int count, const Presplit* pre, int64_t lda, int64_t ldb,
                    int64_t ldc, int64_t n, int64_t m, int64_t k, int flags, const int32_t* ndst, void* const* dst,
-                   const int32_t* sign) {
+                   const int32_t* sign, const int32_t* fa_nt = nullptr, const void* const* fa_terms = nullptr,
+                   const int32_t* fa_sign = nullptr) {
   using L = tc::PairLayout<PACO_PAIR_ST>;
+  const bool fa = fa_nt != nullptr;
   int rc;
   constexpr CUtensorMapSwizzle SW = CU_TENSOR_MAP_SWIZZLE_64B;
   static tc::TcMaps maps;
@@ -1768,13 +1856,17 @@ int launch_tc_pair(int device, cudaStream_t stream, int count, const Presplit* p
   std::lock_guard<std::mutex> lock(mu);
   for (int q = 0; q < count; ++q) {
     const Presplit& p = pre[q];
-    if (!pitch_ok(p.ah, lda, 4) || !pitch_ok(p.al, lda, 4) || !pitch_ok(p.bh, ldb, 4) || !pitch_ok(p.bl, ldb, 4)) {
+    const void* a0 = fa ? fa_terms[2 * q] : p.ah;
+    const void* a1 = fa ? (fa_nt[q] > 1 ? fa_terms[2 * q + 1] : fa_terms[2 * q]) : p.al;
+    if (!pitch_ok(a0, lda, 4) || !pitch_ok(a1, lda, 4) || !pitch_ok(p.bh, ldb, 4) || !pitch_ok(p.bl, ldb, 4)) {
       set_error("paco_mm_tf32x3: operand row pitches must be multiples of 16 bytes");
       return PACO_ERR_UNSUPPORTED;
     }
     tc::TcProb& P = maps.p[q];
-    if ((rc = make_map(&P.a[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.ah, n, k, lda, L::BK, tc::BM, &P.a_col0[0], SW)) ||
-        (rc = make_map(&P.a[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.al, n, k, lda, L::BK, tc::BM, &P.a_col0[1], SW)) ||
+    P.nta = fa ? fa_nt[q] : 2;
+    P.sga = fa ? ((fa_sign[2 * q] < 0 ? 1u : 0u) | (fa_nt[q] > 1 && fa_sign[2 * q + 1] < 0 ? 2u : 0u)) : 0u;
+    if ((rc = make_map(&P.a[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a0, n, k, lda, L::BK, tc::BM, &P.a_col0[0], SW)) ||
+        (rc = make_map(&P.a[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a1, n, k, lda, L::BK, tc::BM, &P.a_col0[1], SW)) ||
         (rc = make_map(&P.b[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.bh, m, k, ldb, L::BK, L::BNH, &P.b_col0[0], SW)) ||
         (rc = make_map(&P.b[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.bl, m, k, ldb, L::BK, L::BNH, &P.b_col0[1], SW)))
       return rc;
@@ -1801,10 +1893,10 @@ int launch_tc_pair(int device, cudaStream_t stream, int count, const Presplit* p
   args.groups = 1;
   const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb * count;
   const int pairs = int(tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
-  auto kern = tc::tc_pair_kernel<PACO_PAIR_ST>;
+  auto kern = fa ? tc::tc_pair_kernel<PACO_PAIR_ST, true> : tc::tc_pair_kernel<PACO_PAIR_ST, false>;
   {
     static std::atomic<uint64_t> attr_set{0};
-    const uint64_t bit = uint64_t(1) << (device & 63);
+    const uint64_t bit = uint64_t(1) << ((device & 31) * 2 + (fa ? 1 : 0));
     if (!(attr_set.load() & bit)) {
       PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
       attr_set.fetch_or(bit);
@@ -1812,7 +1904,7 @@ int launch_tc_pair(int device, cudaStream_t stream, int count, const Presplit* p
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(2 * pairs));
-  cfg.blockDim = dim3(L::THREADS);
+  cfg.blockDim = dim3(fa ? tc::PairLayout<PACO_PAIR_ST, true>::THREADS : L::THREADS);
   cfg.dynamicSmemBytes = L::SMEM_ALLOC;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -1999,6 +2091,43 @@ int launch_mm_tf32x3_fused(int device, cudaStream_t stream, int count, const int
     }
   }
   return run_tc<K>(device, sc, stream, maps, count, n, m, k, 0);
+}
+
+// Strassen leaf batch on CTA pairs with S_r formed in the kernel (tc_pair_kernel<.., true>):
+// A_q = sum_t a_sign * a_terms[2q + t] (t < nta[q] <= 2, pitch lda), B_q^T pre-split (bt_hi / bt_lo).
+int launch_mm_tf32x3_fused_a(int device, cudaStream_t stream, int count, const int32_t* nta,
+                             const void* const* a_terms, const int32_t* a_sign, int64_t lda, const void* const* bt_hi,
+                             const void* const* bt_lo, int64_t ldb, const int32_t* ndst, void* const* dst,
+                             const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k) {
+  if (count < 1 || count > tc::kMaxBatch || !nta || !a_terms || !a_sign || !bt_hi || !bt_lo || !ndst || !dst ||
+      !sign) {
+    set_error("paco_mm_tf32x3_fused_a: count=%d (1..%d) and every term / destination array required", count,
+              tc::kMaxBatch);
+    return PACO_ERR_ARG;
+  }
+  if (n <= 0 || m <= 0 || k <= 0) return PACO_OK;
+  if (n > INT32_MAX || m > INT32_MAX || k > INT32_MAX) {
+    set_error("tcgen05 path: extents must fit int32");
+    return PACO_ERR_ARG;
+  }
+  Presplit pre[tc::kMaxBatch];
+  for (int q = 0; q < count; ++q) {
+    if (nta[q] < 1 || nta[q] > 2) {
+      set_error("paco_mm_tf32x3_fused_a: problem %d has %d A terms (1..2)", q, nta[q]);
+      return PACO_ERR_ARG;
+    }
+    if (ndst[q] < 1 || ndst[q] > 4) {
+      set_error("paco_mm_tf32x3_fused_a: problem %d has %d destinations (1..4)", q, ndst[q]);
+      return PACO_ERR_ARG;
+    }
+    for (int d = 0; d < ndst[q]; ++d)
+      if (!c_ok(dst[4 * q + d], ldc, m)) {
+        set_error("paco_mm_tf32x3_fused_a: C needs a 16-byte aligned start, row pitch and row length");
+        return PACO_ERR_UNSUPPORTED;
+      }
+    pre[q] = Presplit{nullptr, nullptr, bt_hi[q], bt_lo[q], dst[4 * q]};
+  }
+  return launch_tc_pair(device, stream, count, pre, lda, ldb, ldc, n, m, k, 0, ndst, dst, sign, nta, a_terms, a_sign);
 }
 
 int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,

@@ -405,10 +405,15 @@ def _leaf_level_multi(A: View, B: View, dests, stream) -> None:
     pass reads one (paco_mm_tf32x3_multi, TMA reduce-adds)."""
     h = A.rows // 2
     dev = A.device
-    ops = [[torch.empty((h, h), dtype=torch.float32, device=dev) for _ in range(4)] for _ in range(7)]
+    fuse_a = FUSED_A and _pair_batch(h, h, 7) and A.ptr % 16 == 0 and (A.ld * 4) % 16 == 0
+    ops = [[torch.empty((h, h), dtype=torch.float32, device=dev) for _ in range(2 if fuse_a else 4)]
+           for _ in range(7)]
     for r in range(1, 8):
-        ah, al, bh, bl = ops[r - 1]
-        _split(stream, S_TERMS[r], A, ah, al, transpose=False)
+        if fuse_a:
+            bh, bl = ops[r - 1]
+        else:
+            ah, al, bh, bl = ops[r - 1]
+            _split(stream, S_TERMS[r], A, ah, al, transpose=False)
         _split(stream, T_TERMS[r], B, bh, bl, transpose=True)
     ndst = (ctypes.c_int32 * 7)()
     dst = (ctypes.c_void_p * 28)()
@@ -430,9 +435,21 @@ def _leaf_level_multi(A: View, B: View, dests, stream) -> None:
     def arr(vals):
         return (ctypes.c_void_p * 7)(*vals)
 
-    nat.check(nat.load().paco_mm_tf32x3_multi(
-        dev, stream.cuda_stream, 7, arr([o[0].data_ptr() for o in ops]), arr([o[1].data_ptr() for o in ops]), h,
-        arr([o[2].data_ptr() for o in ops]), arr([o[3].data_ptr() for o in ops]), h, ndst, dst, sign, ld, h, h, h))
+    if fuse_a:
+        # S_r formed inside the pair kernel from A's quadrants (no A-side split launches)
+        nta = (ctypes.c_int32 * 7)()
+        at, asg = (ctypes.c_void_p * 14)(), (ctypes.c_int32 * 14)()
+        for r in range(1, 8):
+            nta[r - 1] = len(S_TERMS[r])
+            for t, (c, q) in enumerate(S_TERMS[r]):
+                at[2 * (r - 1) + t], asg[2 * (r - 1) + t] = _quad(A, q).ptr, c
+        nat.check(nat.load().paco_mm_tf32x3_fused_a(
+            dev, stream.cuda_stream, 7, nta, at, asg, A.ld, arr([o[0].data_ptr() for o in ops]),
+            arr([o[1].data_ptr() for o in ops]), h, ndst, dst, sign, ld, h, h, h))
+    else:
+        nat.check(nat.load().paco_mm_tf32x3_multi(
+            dev, stream.cuda_stream, 7, arr([o[0].data_ptr() for o in ops]), arr([o[1].data_ptr() for o in ops]), h,
+            arr([o[2].data_ptr() for o in ops]), arr([o[3].data_ptr() for o in ops]), h, ndst, dst, sign, ld, h, h, h))
     for o in ops:
         for t in o:
             t.record_stream(stream)
@@ -612,6 +629,16 @@ FUSED_COMBINE = True
 # TMA's 48 KB, and the kernel is shared-memory-bandwidth bound (ncu: LSU
 # wavefronts 76 % of peak, tensor pipe 51 % active).
 FUSED_PRODUCER = False
+# On CTA pairs (big leaf batches) form only S_r inside the kernel (paco_mm_tf32x3_fused_a):
+# the A side's split launches go away, B^T stays pre-split.  Off: measured a wash on
+# cfg5 (32.1-33.1 vs 32.0-32.9 ms; the leaf launches slow by ~8 %, the same as the
+# 1.9 ms of A-side splits they save -- DESIGN.md section 5)
+FUSED_A = False
+
+
+def _pair_batch(n: int, m: int, count: int) -> bool:
+    """The library runs this 3xTF32 batch on CTA pairs (tc_gemm.cu tf32_pair)."""
+    return ((n + 255) // 256) * ((m + 255) // 256) * count >= 3 * 74
 
 
 def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stream) -> None:

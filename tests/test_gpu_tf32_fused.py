@@ -186,3 +186,22 @@ def test_cta_pair_kernel_multi_destination(shape):
     torch.cuda.synchronize()
     for i in range(2):
         assert float((C[i].double() - ref[i]).norm() / ref[i].norm()) < 1e-5, i
+
+
+def test_strassen_pair_leaves_fused_a(monkeypatch):
+    """8192 / base 2048: leaf batches of 7 x 64 pair tiles (>= 222) run on CTA pairs,
+    S_r formed inside the kernel (FUSED_A) or split beforehand; both vs f64, and the
+    two paths agree to fp32 rounding (same sums, same rounding, same MMAs)."""
+    n, base = 8192, 2048
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+    b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+    rows = torch.arange(0, n, 97, device="cuda")
+    ref = a[rows].double() @ b.double()
+    out = {}
+    for fuse_a in (True, False):
+        monkeypatch.setattr(S, "FUSED_A", fuse_a)
+        c = S.strassen_seq(a, b, n, base=base)
+        assert float((c[rows].double() - ref).norm() / ref.norm()) < 1e-4, fuse_a
+        out[fuse_a] = c
+    assert float((out[True] - out[False]).norm() / out[False].norm()) < 1e-6
