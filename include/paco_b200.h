@@ -239,6 +239,26 @@ int paco_mm_tf32x3_fused_a(int device, void* stream, int count, const int32_t* n
                            int64_t ldb, const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc,
                            int64_t n, int64_t m, int64_t k);
 
+/* The tf32 + 2 x bf16 format of an fp32 operand (the Strassen leaves' default on
+ * CTA pairs): x = sum_i coef[i] * in[i] (as paco_tf32_split) is written as
+ * hi = tf32_rn(x) (fp32), h16 = bf16_rn(hi), l16 = bf16_rn(x - hi) (bf16 arrays),
+ * all with row pitch ldo elements, transposed when `transpose`. */
+int paco_tf32b2_split(int device, void* stream, int nin, const void* const* ins, const int64_t* lds,
+                      const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* h16, void* l16,
+                      int64_t ldo);
+
+/* C (+/-)= A x B for fp32 operands given in that format: the main product
+ * hi * hi on the tf32 tensor path and the corrections hi * lo + lo * hi as bf16
+ * products (kind::f16: half the tensor time of tf32), fp32 accumulation in TMEM,
+ * on CTA pairs (cta_group::2).  The corrections are 2^-11 of the product, so their
+ * bf16 rounding adds ~2^-19 relative per term -- below the fp32 accumulation and
+ * Strassen formation errors of cfg5 (tests/test_gpu_tf32_fused.py).  A n x k (lda),
+ * B^T m x k (ldb), destinations as paco_mm_tf32x3_multi. */
+int paco_mm_tf32b2_multi(int device, void* stream, int count, const void* const* a_hi, const void* const* a_h16,
+                         const void* const* a_l16, int64_t lda, const void* const* b_hi, const void* const* b_h16,
+                         const void* const* b_l16, int64_t ldb, const int32_t* ndst, void* const* dst,
+                         const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k);
+
 /* dst (cols x rows, pitch ld_dst) = src^T (rows x cols, pitch ld_src); 4- or
  * 8-byte elements.  Strassen transposes B once so every T_r^T operand of the
  * fused leaves is a K-major view. */

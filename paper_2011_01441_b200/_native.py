@@ -86,6 +86,11 @@ SIGNATURES = {
                                       ctypes.POINTER(ctypes.c_int32), _i64, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                       _i64, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_vp),
                                       ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
+    "paco_tf32b2_split": (_int, [_int, _vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_i64),
+                                 ctypes.POINTER(ctypes.c_int32), _i64, _i64, _int, _vp, _vp, _vp, _i64]),
+    "paco_mm_tf32b2_multi": (_int, [_int, _vp, _int] + [ctypes.POINTER(_vp)] * 3 + [_i64] +
+                             [ctypes.POINTER(_vp)] * 3 + [_i64, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_vp),
+                                                          ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
     "paco_transpose": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_copy2d": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_device_alloc": (_int, [_int, ctypes.c_size_t, ctypes.POINTER(_vp)]),

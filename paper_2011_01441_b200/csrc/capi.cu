@@ -92,6 +92,13 @@ int launch_mm_tf32x3_fused_a(int device, cudaStream_t stream, int count, const i
                              const void* const* a_terms, const int32_t* a_sign, int64_t lda, const void* const* bt_hi,
                              const void* const* bt_lo, int64_t ldb, const int32_t* ndst, void* const* dst,
                              const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k);
+int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const void* const* a_hi,
+                           const void* const* a_h16, const void* const* a_l16, int64_t lda, const void* const* b_hi,
+                           const void* const* b_h16, const void* const* b_l16, int64_t ldb, const int32_t* ndst,
+                           void* const* dst, const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k);
+int launch_tf32b2_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,
+                        const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* h16,
+                        void* l16, int64_t ldo);
 int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,
                       const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* lo,
                       int64_t ldo);
@@ -465,6 +472,41 @@ int paco_mm_tf32x3_fused_a(int device, void* stream, int count, const int32_t* n
   PACO_TRY(dg.use(device));
   return launch_mm_tf32x3_fused_a(device, static_cast<cudaStream_t>(stream), count, nta, a_terms, a_sign, lda, bt_hi,
                                   bt_lo, ldb, ndst, dst, sign, ldc, n, m, k);
+}
+
+int paco_tf32b2_split(int device, void* stream, int nin, const void* const* ins, const int64_t* lds,
+                      const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* h16, void* l16,
+                      int64_t ldo) {
+  if (rows <= 0 || cols <= 0) return PACO_OK;
+  if (!ins || !lds || !coefs || nin < 1 || nin > 4) {
+    set_error("paco_tf32b2_split: need 1..4 inputs with pitches and coefficients");
+    return PACO_ERR_ARG;
+  }
+  for (int q = 0; q < nin; ++q) PACO_TRY(check_view("in", ins[q], lds[q], rows, cols));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_tf32b2_split(static_cast<cudaStream_t>(stream), nin, ins, lds, coefs, rows, cols, transpose, hi, h16,
+                             l16, ldo);
+}
+
+int paco_mm_tf32b2_multi(int device, void* stream, int count, const void* const* a_hi, const void* const* a_h16,
+                         const void* const* a_l16, int64_t lda, const void* const* b_hi, const void* const* b_h16,
+                         const void* const* b_l16, int64_t ldb, const int32_t* ndst, void* const* dst,
+                         const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k) {
+  if (count >= 1 && count <= 8 && a_hi && a_h16 && a_l16 && b_hi && b_h16 && b_l16 && ndst && dst)
+    for (int q = 0; q < count; ++q) {
+      PACO_TRY(check_view("A_hi", a_hi[q], lda, n, k));
+      PACO_TRY(check_view("A_h16", a_h16[q], lda, n, k));
+      PACO_TRY(check_view("A_l16", a_l16[q], lda, n, k));
+      PACO_TRY(check_view("Bt_hi", b_hi[q], ldb, m, k));
+      PACO_TRY(check_view("Bt_h16", b_h16[q], ldb, m, k));
+      PACO_TRY(check_view("Bt_l16", b_l16[q], ldb, m, k));
+      for (int d = 0; d < ndst[q] && d < 4; ++d) PACO_TRY(check_view("C", dst[4 * q + d], ldc, n, m));
+    }
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_mm_tf32b2_multi(device, static_cast<cudaStream_t>(stream), count, a_hi, a_h16, a_l16, lda, b_hi,
+                                b_h16, b_l16, ldb, ndst, dst, sign, ldc, n, m, k);
 }
 
 int paco_transpose(int device, void* stream, int elsize, void* dst, int64_t ld_dst, const void* src, int64_t ld_src,

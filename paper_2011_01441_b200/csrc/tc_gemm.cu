@@ -390,6 +390,8 @@ struct TcProb {
   uint32_t neg;  // bit d: destination d receives -AB
   int32_t nta, ntb;      // fused kinds: raw terms of A (maps a[0..nta)) and of B^T (b[0..ntb))
   uint32_t sga, sgb;     // bit t: term t enters with coefficient -1
+  CUtensorMap a2, b2;    // tf32 + 2 x bf16 format: a[0] = hi (fp32), a[1] = bf16(hi), a2 = bf16(x - hi)
+  int32_t a2_col0, b2_col0;
 };
 constexpr int kMaxBatch = 8;
 struct TcMaps {
@@ -861,7 +863,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
 // releases the accumulator with a remote arrive on the leader's barrier.
 // Tiles (256 x 256 of C) are dealt to pairs statically in row-band order.
 // ---------------------------------------------------------------------------
-template <int ST, bool FA = false>
+template <int ST, bool FA = false, bool B2 = false>
 struct PairLayout {
   static constexpr int BK = 16, BN = 256, BNH = 128, EC = 16, EW = 4, EB = 2;
   // FA: A is formed in the kernel (Strassen's S_r from <= 2 signed raw views,
@@ -883,7 +885,29 @@ struct PairLayout {
                                     (uint32_t(256 >> 4) << 24);
   __device__ static int a_off(int s, int o) { return s * STAGE_BYTES + o * A_BYTES; }
   __device__ static int b_off(int s, int o) { return s * STAGE_BYTES + 2 * A_BYTES + o * B_BYTES; }
+  // B2 (tf32 + 2 x bf16): per stage the tf32 hi tiles of A and B^T (8 KB each) and
+  // four 4 KB bf16 tiles (32-byte K-major rows, SWIZZLE_32B): bf16(hi) and bf16(x - hi)
+  // of each -- the same 32 KB as the 3xTF32 stage, but the two correction products
+  // run as kind::f16 MMAs (K = 16 per instruction: half the tensor time of tf32)
+  static constexpr int H16_BYTES = BM * BK * 2;
+  __device__ static int hi_a(int s) { return s * STAGE_BYTES; }
+  __device__ static int hi_b(int s) { return s * STAGE_BYTES + A_BYTES; }
+  __device__ static int x16(int s, int which) { return s * STAGE_BYTES + 2 * A_BYTES + which * H16_BYTES; }
+  // x16 slots: 0 = bf16(A hi), 1 = bf16(A lo), 2 = bf16(B^T hi), 3 = bf16(B^T lo)
+  static constexpr uint32_t IDESC_BF16 = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
+                                         (uint32_t(256 >> 4) << 24);
 };
+
+// K-major, 32B swizzle: 32-byte rows, 8-row groups 256 B apart, layout type 6.
+__device__ __forceinline__ uint64_t smem_desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(256 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(6) << 61;
+  return d;
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -909,6 +933,14 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
       "%4}], [%2];\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_pair_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 __device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -940,10 +972,10 @@ __device__ __forceinline__ void pair_tile(const TcArgs& a, int32_t t, int& q, in
   rb = r0 + v % rows;
 }
 
-template <int ST, bool FA>
-__global__ void __launch_bounds__(PairLayout<ST, FA>::THREADS, 1)
+template <int ST, bool FA, bool B2>
+__global__ void __launch_bounds__(PairLayout<ST, FA, B2>::THREADS, 1)
     tc_pair_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
-  using L = PairLayout<ST, FA>;
+  using L = PairLayout<ST, FA, B2>;
   constexpr int BK = L::BK, BN = L::BN;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1020,6 +1052,15 @@ __global__ void __launch_bounds__(PairLayout<ST, FA>::THREADS, 1)
               if (o < P.nta) tma_load_2d(smem + L::a_off(s, o), &P.a[o], &rfull[s], P.a_col0[o] + kb * BK, arow);
               tma_load_2d_pair(smem + L::b_off(s, o), &P.b[o], fb, P.b_col0[o] + kb * BK, brow);
             }
+          } else if constexpr (B2) {
+            if (leader) mbar_expect_tx_relaxed(&full[s], 2 * L::STAGE_BYTES);
+            const int kc = kb * BK;
+            tma_load_2d_pair(smem + L::hi_a(s), &P.a[0], fb, P.a_col0[0] + kc, arow);
+            tma_load_2d_pair(smem + L::hi_b(s), &P.b[0], fb, P.b_col0[0] + kc, brow);
+            tma_load_2d_pair(smem + L::x16(s, 0), &P.a[1], fb, P.a_col0[1] + kc, arow);
+            tma_load_2d_pair(smem + L::x16(s, 1), &P.a2, fb, P.a2_col0 + kc, arow);
+            tma_load_2d_pair(smem + L::x16(s, 2), &P.b[1], fb, P.b_col0[1] + kc, brow);
+            tma_load_2d_pair(smem + L::x16(s, 3), &P.b2, fb, P.b2_col0 + kc, brow);
           } else {
             if (leader) mbar_expect_tx_relaxed(&full[s], 2 * L::STAGE_BYTES);
 #pragma unroll
@@ -1046,17 +1087,31 @@ __global__ void __launch_bounds__(PairLayout<ST, FA>::THREADS, 1)
           const int s = it % ST;
           mbar_wait(&full[s], (it / ST) & 1);
           tc_fence_after();
-          const uint64_t ad[2] = {smem_desc_sw64(smem_u32(smem + L::a_off(s, 0))),
-                                  smem_desc_sw64(smem_u32(smem + L::a_off(s, 1)))};
-          const uint64_t bd[2] = {smem_desc_sw64(smem_u32(smem + L::b_off(s, 0))),
-                                  smem_desc_sw64(smem_u32(smem + L::b_off(s, 1)))};
+          if constexpr (B2) {
+            // hi*hi on the tf32 path (two K = 8 steps), hi*lo and lo*hi as bf16 (one K = 16 each)
+            const uint64_t ah = smem_desc_sw64(smem_u32(smem + L::hi_a(s)));
+            const uint64_t bh = smem_desc_sw64(smem_u32(smem + L::hi_b(s)));
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk)
+            for (int kk = 0; kk < BK / 8; ++kk)
+              umma_pair(d_tmem, ah + uint64_t(2 * kk), bh + uint64_t(2 * kk), L::IDESC, (kb | kk) != 0);
+            umma_pair_f16(d_tmem, smem_desc_sw32(smem_u32(smem + L::x16(s, 0))),
+                          smem_desc_sw32(smem_u32(smem + L::x16(s, 3))), L::IDESC_BF16, 1);
+            umma_pair_f16(d_tmem, smem_desc_sw32(smem_u32(smem + L::x16(s, 1))),
+                          smem_desc_sw32(smem_u32(smem + L::x16(s, 2))), L::IDESC_BF16, 1);
+          } else {
+            const uint64_t ad[2] = {smem_desc_sw64(smem_u32(smem + L::a_off(s, 0))),
+                                    smem_desc_sw64(smem_u32(smem + L::a_off(s, 1)))};
+            const uint64_t bd[2] = {smem_desc_sw64(smem_u32(smem + L::b_off(s, 0))),
+                                    smem_desc_sw64(smem_u32(smem + L::b_off(s, 1)))};
 #pragma unroll
-            for (int ps = 0; ps < 3; ++ps) {  // hi*hi, hi*lo, lo*hi
-              const int ao = ps == 2 ? 1 : 0, bo = ps == 1 ? 1 : 0;
-              umma_pair(d_tmem, ad[ao] + uint64_t(2 * kk), bd[bo] + uint64_t(2 * kk), L::IDESC, (kb | kk | ps) != 0);
-            }
+            for (int kk = 0; kk < BK / 8; ++kk)
+#pragma unroll
+              for (int ps = 0; ps < 3; ++ps) {  // hi*hi, hi*lo, lo*hi
+                const int ao = ps == 2 ? 1 : 0, bo = ps == 1 ? 1 : 0;
+                umma_pair(d_tmem, ad[ao] + uint64_t(2 * kk), bd[bo] + uint64_t(2 * kk), L::IDESC,
+                          (kb | kk | ps) != 0);
+              }
+          }
           umma_commit_pair(&empty[s]);  // both CTAs' stage s is free once these MMAs complete
         }
         umma_commit_pair(&tfull[a]);    // both CTAs' accumulator halves are ready
@@ -1361,10 +1416,18 @@ __device__ __forceinline__ float lc_value(const SplitIn& in, int64_t i, int64_t 
 // Transposed output (cols x rows) through a 64x64 smem tile: 16-byte loads
 // along the input rows, 16-byte stores along the output rows (the K-major
 // B^T the 3xTF32 MMAs read).  kVec: every view 16 B aligned, cols % 4 == 0.
-template <bool kVec>
+// kB2 (the tf32 + 2 x bf16 format): hi = tf32_rn(x) as fp32, h16 = bf16_rn(hi),
+// l16 = bf16_rn(x - hi) -- `lo` unused.
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);  // .x = a (low half)
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+template <bool kVec, bool kB2>
 __global__ void __launch_bounds__(256) split_tf32_t_kernel(const SplitIn in, float* __restrict__ hi,
                                                            float* __restrict__ lo, int64_t ldo, int64_t rows,
-                                                           int64_t cols) {
+                                                           int64_t cols, __nv_bfloat16* __restrict__ h16,
+                                                           __nv_bfloat16* __restrict__ l16) {
   __shared__ float th[64][65], tl[64][65];
   const int64_t r0 = int64_t(blockIdx.y) * 64, c0 = int64_t(blockIdx.x) * 64;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -1415,7 +1478,8 @@ __global__ void __launch_bounds__(256) split_tf32_t_kernel(const SplitIn in, flo
     for (int e = 0; e < 4; ++e) {
       const float h = round_tf32(v[e]);
       th[r][4 * tx + e] = h;
-      tl[r][4 * tx + e] = round_tf32(v[e] - h);  // the MMA would truncate an unrounded lo
+      // 3xTF32: the MMA would truncate an unrounded lo; kB2: the exact x - hi (bf16-rounded at the store)
+      tl[r][4 * tx + e] = kB2 ? v[e] - h : round_tf32(v[e] - h);
     }
   }
   __syncthreads();
@@ -1428,14 +1492,24 @@ __global__ void __launch_bounds__(256) split_tf32_t_kernel(const SplitIn in, flo
     const float4 l = make_float4(tl[4 * tx][c], tl[4 * tx + 1][c], tl[4 * tx + 2][c], tl[4 * tx + 3][c]);
     if (kVec && i + 3 < rows) {
       *reinterpret_cast<float4*>(hi + j * ldo + i) = h;
-      *reinterpret_cast<float4*>(lo + j * ldo + i) = l;
+      if constexpr (kB2) {
+        *reinterpret_cast<uint2*>(h16 + j * ldo + i) = make_uint2(pack_bf16x2(h.x, h.y), pack_bf16x2(h.z, h.w));
+        *reinterpret_cast<uint2*>(l16 + j * ldo + i) = make_uint2(pack_bf16x2(l.x, l.y), pack_bf16x2(l.z, l.w));
+      } else {
+        *reinterpret_cast<float4*>(lo + j * ldo + i) = l;
+      }
     } else {
       const float hv[4] = {h.x, h.y, h.z, h.w}, lv[4] = {l.x, l.y, l.z, l.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         if (i + e < rows) {
           hi[j * ldo + i + e] = hv[e];
-          lo[j * ldo + i + e] = lv[e];
+          if constexpr (kB2) {
+            h16[j * ldo + i + e] = __float2bfloat16_rn(hv[e]);
+            l16[j * ldo + i + e] = __float2bfloat16_rn(lv[e]);
+          } else {
+            lo[j * ldo + i + e] = lv[e];
+          }
         }
     }
   }
@@ -1443,9 +1517,10 @@ __global__ void __launch_bounds__(256) split_tf32_t_kernel(const SplitIn in, flo
 
 // Row-major output, 4 consecutive elements per thread (16 B accesses when
 // every view is 16 B aligned: vec), rows strided over the grid's y.
-template <bool kVec>
+template <bool kVec, bool kB2>
 __global__ void split_tf32_n_kernel(const SplitIn in, float* __restrict__ hi, float* __restrict__ lo,
-                                    int64_t ldo, int64_t rows, int64_t cols) {
+                                    int64_t ldo, int64_t rows, int64_t cols, __nv_bfloat16* __restrict__ h16,
+                                    __nv_bfloat16* __restrict__ l16) {
   const int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
   if (j >= cols) return;
   int64_t i0 = blockIdx.y;
@@ -1478,11 +1553,18 @@ __global__ void split_tf32_n_kernel(const SplitIn in, float* __restrict__ hi, fl
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           h[e] = round_tf32(v[e]);
-          l[e] = round_tf32(v[e] - h[e]);
+          l[e] = kB2 ? v[e] - h[e] : round_tf32(v[e] - h[e]);
         }
         const int64_t i = i0 + u * gy;
         __stcs(reinterpret_cast<float4*>(hi + i * ldo + j), make_float4(h[0], h[1], h[2], h[3]));
-        __stcs(reinterpret_cast<float4*>(lo + i * ldo + j), make_float4(l[0], l[1], l[2], l[3]));
+        if constexpr (kB2) {
+          __stcs(reinterpret_cast<uint2*>(h16 + i * ldo + j),
+                 make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3])));
+          __stcs(reinterpret_cast<uint2*>(l16 + i * ldo + j),
+                 make_uint2(pack_bf16x2(l[0], l[1]), pack_bf16x2(l[2], l[3])));
+        } else {
+          __stcs(reinterpret_cast<float4*>(lo + i * ldo + j), make_float4(l[0], l[1], l[2], l[3]));
+        }
       }
     }
   }
@@ -1509,17 +1591,27 @@ __global__ void split_tf32_n_kernel(const SplitIn in, float* __restrict__ hi, fl
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       h[e] = round_tf32(v[e]);
-      l[e] = round_tf32(v[e] - h[e]);
+      l[e] = kB2 ? v[e] - h[e] : round_tf32(v[e] - h[e]);
     }
     if (kVec) {
       *reinterpret_cast<float4*>(hi + i * ldo + j) = make_float4(h[0], h[1], h[2], h[3]);
-      *reinterpret_cast<float4*>(lo + i * ldo + j) = make_float4(l[0], l[1], l[2], l[3]);
+      if constexpr (kB2) {
+        *reinterpret_cast<uint2*>(h16 + i * ldo + j) = make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]));
+        *reinterpret_cast<uint2*>(l16 + i * ldo + j) = make_uint2(pack_bf16x2(l[0], l[1]), pack_bf16x2(l[2], l[3]));
+      } else {
+        *reinterpret_cast<float4*>(lo + i * ldo + j) = make_float4(l[0], l[1], l[2], l[3]);
+      }
     } else {
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         if (j + e < cols) {
           hi[i * ldo + j + e] = h[e];
-          lo[i * ldo + j + e] = l[e];
+          if constexpr (kB2) {
+            h16[i * ldo + j + e] = __float2bfloat16_rn(h[e]);
+            l16[i * ldo + j + e] = __float2bfloat16_rn(l[e]);
+          } else {
+            lo[i * ldo + j + e] = l[e];
+          }
         }
     }
   }
@@ -1545,28 +1637,38 @@ int repack(int device, Scratch& sc, const void** p, int64_t* ld, int64_t rows, i
 // x = sum coef_q in_q (rows x cols) -> hi/lo tf32 pair with row pitch ldo
 // (elements), transposed (cols x rows) if `transpose`.
 int launch_split(const tc::SplitIn& in, int64_t rows, int64_t cols, bool transpose, float* h, float* l,
-                 int64_t ldo, cudaStream_t st) {
+                 int64_t ldo, cudaStream_t st, __nv_bfloat16* h16 = nullptr, __nv_bfloat16* l16 = nullptr) {
   if (rows <= 0 || cols <= 0) return PACO_OK;
   KernelSpan ks(PACO_KT_TF32_SPLIT, st);
+  const bool b2 = h16 != nullptr;
   bool vec = (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(h) % 16 == 0) &&
-             (reinterpret_cast<uintptr_t>(l) % 16 == 0);
+             (b2 ? (reinterpret_cast<uintptr_t>(h16) % 8 == 0 && reinterpret_cast<uintptr_t>(l16) % 8 == 0)
+                 : (reinterpret_cast<uintptr_t>(l) % 16 == 0));
   for (int q = 0; q < in.nin; ++q)
     vec = vec && (in.ld[q] % 4 == 0) && (reinterpret_cast<uintptr_t>(in.p[q]) % 16 == 0);
   if (transpose) {
     dim3 grid(unsigned((cols + 63) / 64), unsigned((rows + 63) / 64));
-    if (vec)
-      tc::split_tf32_t_kernel<true><<<grid, 256, 0, st>>>(in, h, l, ldo, rows, cols);
+    if (b2 && vec)
+      tc::split_tf32_t_kernel<true, true><<<grid, 256, 0, st>>>(in, h, l, ldo, rows, cols, h16, l16);
+    else if (b2)
+      tc::split_tf32_t_kernel<false, true><<<grid, 256, 0, st>>>(in, h, l, ldo, rows, cols, h16, l16);
+    else if (vec)
+      tc::split_tf32_t_kernel<true, false><<<grid, 256, 0, st>>>(in, h, l, ldo, rows, cols, h16, l16);
     else
-      tc::split_tf32_t_kernel<false><<<grid, 256, 0, st>>>(in, h, l, ldo, rows, cols);
+      tc::split_tf32_t_kernel<false, false><<<grid, 256, 0, st>>>(in, h, l, ldo, rows, cols, h16, l16);
   } else {
     vec = vec && (cols % 4 == 0);
     const int64_t xblocks = (cols / 4 + 1 + 127) / 128;
     const int64_t yblocks = rows < 65535 ? rows : 65535;
     dim3 grid(unsigned(xblocks), unsigned(yblocks > 2368 / xblocks + 1 ? 2368 / xblocks + 1 : yblocks));
-    if (vec)
-      tc::split_tf32_n_kernel<true><<<grid, 128, 0, st>>>(in, h, l, ldo, rows, cols);
+    if (b2 && vec)
+      tc::split_tf32_n_kernel<true, true><<<grid, 128, 0, st>>>(in, h, l, ldo, rows, cols, h16, l16);
+    else if (b2)
+      tc::split_tf32_n_kernel<false, true><<<grid, 128, 0, st>>>(in, h, l, ldo, rows, cols, h16, l16);
+    else if (vec)
+      tc::split_tf32_n_kernel<true, false><<<grid, 128, 0, st>>>(in, h, l, ldo, rows, cols, h16, l16);
     else
-      tc::split_tf32_n_kernel<false><<<grid, 128, 0, st>>>(in, h, l, ldo, rows, cols);
+      tc::split_tf32_n_kernel<false, false><<<grid, 128, 0, st>>>(in, h, l, ldo, rows, cols, h16, l16);
   }
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;
@@ -1839,6 +1941,55 @@ int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* 
 #ifndef PACO_PAIR_ST
 #define PACO_PAIR_ST 6
 #endif
+// Launch a tc_pair_kernel variant (mode 0: 3xTF32, 1: FA (S_r formed in the kernel),
+// 2: tf32 + 2 x bf16) over 256 x 256 tiles dealt to the 74 CTA pairs.
+int run_pair(int device, cudaStream_t stream, const tc::TcMaps& maps, int count, int64_t n, int64_t m, int64_t k,
+             int flags, int mode) {
+  using L = tc::PairLayout<PACO_PAIR_ST>;
+  tc::TcArgs args{};
+  args.n = n;
+  args.m = m;
+  args.k = k;
+  args.count = count;
+  args.overwrite = (flags & PACO_MM_OVERWRITE) ? 1 : 0;
+  args.tiles_rb = int32_t((n + 255) / 256);
+  args.tiles_nb = int32_t((m + L::BN - 1) / L::BN);
+  args.kblocks = int32_t((k + L::BK - 1) / L::BK);
+  args.groups = 1;
+  const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb * count;
+  const int pairs = int(tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
+  auto kern = mode == 1 ? tc::tc_pair_kernel<PACO_PAIR_ST, true, false>
+                        : (mode == 2 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true>
+                                     : tc::tc_pair_kernel<PACO_PAIR_ST, false, false>);
+  const int threads = mode == 1 ? tc::PairLayout<PACO_PAIR_ST, true>::THREADS : L::THREADS;
+  {
+    static std::atomic<uint64_t> attr_set{0};
+    const uint64_t bit = uint64_t(1) << ((device & 15) * 4 + mode);
+    if (!(attr_set.load() & bit)) {
+      PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
+      attr_set.fetch_or(bit);
+    }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(2 * pairs));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = L::SMEM_ALLOC;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = kPdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  KernelSpan ks(PACO_KT_TC_GEMM, stream);
+  PACO_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps, args));
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
 // 3xTF32 batch on CTA pairs (tc_pair_kernel): same contract as launch_tc_batch
 // for pre-split operands, optional destination lists.
 // fa_terms (FA): problem q's A is the signed sum of fa_nt[q] raw views fa_terms[2q + t]
@@ -1881,45 +2032,7 @@ int launch_tc_pair(int device, cudaStream_t stream, int count, const Presplit* p
         return rc;
     }
   }
-  tc::TcArgs args{};
-  args.n = n;
-  args.m = m;
-  args.k = k;
-  args.count = count;
-  args.overwrite = (flags & PACO_MM_OVERWRITE) ? 1 : 0;
-  args.tiles_rb = int32_t((n + 255) / 256);
-  args.tiles_nb = int32_t((m + L::BN - 1) / L::BN);
-  args.kblocks = int32_t((k + L::BK - 1) / L::BK);
-  args.groups = 1;
-  const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb * count;
-  const int pairs = int(tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
-  auto kern = fa ? tc::tc_pair_kernel<PACO_PAIR_ST, true> : tc::tc_pair_kernel<PACO_PAIR_ST, false>;
-  {
-    static std::atomic<uint64_t> attr_set{0};
-    const uint64_t bit = uint64_t(1) << ((device & 31) * 2 + (fa ? 1 : 0));
-    if (!(attr_set.load() & bit)) {
-      PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
-      attr_set.fetch_or(bit);
-    }
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(2 * pairs));
-  cfg.blockDim = dim3(fa ? tc::PairLayout<PACO_PAIR_ST, true>::THREADS : L::THREADS);
-  cfg.dynamicSmemBytes = L::SMEM_ALLOC;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = kPdl ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  KernelSpan ks(PACO_KT_TC_GEMM, stream);
-  PACO_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps, args));
-  PACO_CUDA_TRY(cudaGetLastError());
-  return PACO_OK;
+  return run_pair(device, stream, maps, count, n, m, k, flags, fa ? 1 : 0);
 }
 
 // CTA pairs for the 3xTF32 batches with enough 256 x 256 tiles to keep the 74
@@ -2128,6 +2241,88 @@ int launch_mm_tf32x3_fused_a(int device, cudaStream_t stream, int count, const i
     pre[q] = Presplit{nullptr, nullptr, bt_hi[q], bt_lo[q], dst[4 * q]};
   }
   return launch_tc_pair(device, stream, count, pre, lda, ldb, ldc, n, m, k, 0, ndst, dst, sign, nta, a_terms, a_sign);
+}
+
+
+// tf32 + 2 x bf16 batch on CTA pairs: C[q] (+/-)= A[q] B[q] with A[q] given as
+// (hi fp32, bf16(hi), bf16(x - hi)) n x k (pitch lda, elements) and B[q]^T likewise m x k
+// (pitch ldb) -- paco_tf32b2_split outputs -- destinations as _multi.
+int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const void* const* a_hi,
+                           const void* const* a_h16, const void* const* a_l16, int64_t lda, const void* const* b_hi,
+                           const void* const* b_h16, const void* const* b_l16, int64_t ldb, const int32_t* ndst,
+                           void* const* dst, const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k) {
+  using L = tc::PairLayout<PACO_PAIR_ST>;
+  if (count < 1 || count > tc::kMaxBatch || !a_hi || !a_h16 || !a_l16 || !b_hi || !b_h16 || !b_l16 || !ndst || !dst ||
+      !sign) {
+    set_error("paco_mm_tf32b2_multi: count=%d (1..%d) and every operand / destination array required", count,
+              tc::kMaxBatch);
+    return PACO_ERR_ARG;
+  }
+  if (n <= 0 || m <= 0 || k <= 0) return PACO_OK;
+  if (n > INT32_MAX || m > INT32_MAX || k > INT32_MAX) {
+    set_error("tcgen05 path: extents must fit int32");
+    return PACO_ERR_ARG;
+  }
+  int rc;
+  constexpr CUtensorMapSwizzle S64 = CU_TENSOR_MAP_SWIZZLE_64B, S32 = CU_TENSOR_MAP_SWIZZLE_32B;
+  constexpr CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32, B16 = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  static tc::TcMaps maps;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int q = 0; q < count; ++q) {
+    if (!pitch_ok(a_hi[q], lda, 4) || !pitch_ok(b_hi[q], ldb, 4) || !pitch_ok(a_h16[q], lda, 2) ||
+        !pitch_ok(a_l16[q], lda, 2) || !pitch_ok(b_h16[q], ldb, 2) || !pitch_ok(b_l16[q], ldb, 2)) {
+      set_error("paco_mm_tf32b2_multi: operands need 16-byte aligned starts and row pitches");
+      return PACO_ERR_UNSUPPORTED;
+    }
+    if (ndst[q] < 1 || ndst[q] > 4) {
+      set_error("paco_mm_tf32b2_multi: problem %d has %d destinations (1..4)", q, ndst[q]);
+      return PACO_ERR_ARG;
+    }
+    tc::TcProb& P = maps.p[q];
+    if ((rc = make_map(&P.a[0], F32, 4, a_hi[q], n, k, lda, L::BK, tc::BM, &P.a_col0[0], S64)) ||
+        (rc = make_map(&P.a[1], B16, 2, a_h16[q], n, k, lda, L::BK, tc::BM, &P.a_col0[1], S32)) ||
+        (rc = make_map(&P.a2, B16, 2, a_l16[q], n, k, lda, L::BK, tc::BM, &P.a2_col0, S32)) ||
+        (rc = make_map(&P.b[0], F32, 4, b_hi[q], m, k, ldb, L::BK, L::BNH, &P.b_col0[0], S64)) ||
+        (rc = make_map(&P.b[1], B16, 2, b_h16[q], m, k, ldb, L::BK, L::BNH, &P.b_col0[1], S32)) ||
+        (rc = make_map(&P.b2, B16, 2, b_l16[q], m, k, ldb, L::BK, L::BNH, &P.b2_col0, S32)))
+      return rc;
+    P.ndst = ndst[q];
+    P.neg = 0;
+    for (int d = 0; d < ndst[q]; ++d) {
+      if (!c_ok(dst[4 * q + d], ldc, m)) {
+        set_error("paco_mm_tf32b2_multi: C needs a 16-byte aligned start, row pitch and row length");
+        return PACO_ERR_UNSUPPORTED;
+      }
+      if (sign[4 * q + d] < 0) P.neg |= 1u << d;
+      if ((rc = make_map(d == 0 ? &P.c : &P.cx[d - 1], F32, 4, dst[4 * q + d], n, m, ldc, L::EC, 32,
+                         d == 0 ? &P.c_col0 : &P.cx_col0[d - 1], S64)))
+        return rc;
+    }
+  }
+  return run_pair(device, stream, maps, count, n, m, k, 0, 2);
+}
+
+int launch_tf32b2_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,
+                        const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* h16,
+                        void* l16, int64_t ldo) {
+  if (nin < 1 || nin > 4) {
+    set_error("paco_tf32b2_split: nin=%d (1..4 supported)", nin);
+    return PACO_ERR_ARG;
+  }
+  if (!hi || !h16 || !l16 || ldo < (transpose ? rows : cols)) {
+    set_error("paco_tf32b2_split: bad outputs or pitch");
+    return PACO_ERR_ARG;
+  }
+  tc::SplitIn in{};
+  for (int q = 0; q < nin; ++q) {
+    in.p[q] = static_cast<const float*>(ins[q]);
+    in.ld[q] = lds[q];
+    in.coef[q] = coefs[q] >= 0 ? 1 : -1;
+  }
+  in.nin = nin;
+  return launch_split(in, rows, cols, transpose != 0, static_cast<float*>(hi), nullptr, ldo, stream,
+                      static_cast<__nv_bfloat16*>(h16), static_cast<__nv_bfloat16*>(l16));
 }
 
 int launch_tf32_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,

@@ -405,6 +405,9 @@ def _leaf_level_multi(A: View, B: View, dests, stream) -> None:
     pass reads one (paco_mm_tf32x3_multi, TMA reduce-adds)."""
     h = A.rows // 2
     dev = A.device
+    if TF32B2 and _pair_batch(h, h, 7) and h % 8 == 0:
+        _leaf_level_b2(A, B, dests, stream)
+        return
     fuse_a = FUSED_A and _pair_batch(h, h, 7) and A.ptr % 16 == 0 and (A.ld * 4) % 16 == 0
     ops = [[torch.empty((h, h), dtype=torch.float32, device=dev) for _ in range(2 if fuse_a else 4)]
            for _ in range(7)]
@@ -452,6 +455,56 @@ def _leaf_level_multi(A: View, B: View, dests, stream) -> None:
             arr([o[2].data_ptr() for o in ops]), arr([o[3].data_ptr() for o in ops]), h, ndst, dst, sign, ld, h, h, h))
     for o in ops:
         for t in o:
+            t.record_stream(stream)
+
+
+def _leaf_level_b2(A: View, B: View, dests, stream) -> None:
+    """The leaf level in the tf32 + 2 x bf16 format on CTA pairs: every S_r / T_r
+    formed straight into (tf32 hi, bf16 hi, bf16 lo) -- T_r transposed --
+    (``paco_tf32b2_split``), the seven products one ``paco_mm_tf32b2_multi``
+    launch: hi*hi on the tf32 path, the two correction products as bf16 MMAs
+    (half the tensor time), each folded (+/-) into its C blocks."""
+    h = A.rows // 2
+    dev = A.device
+    lib = nat.load()
+    bufs = []
+    for r in range(1, 8):
+        row = []
+        for terms, src, tr in ((S_TERMS[r], A, False), (T_TERMS[r], B, True)):
+            hi = torch.empty((h, h), dtype=torch.float32, device=dev)
+            h16 = torch.empty((h, h), dtype=torch.bfloat16, device=dev)
+            l16 = torch.empty((h, h), dtype=torch.bfloat16, device=dev)
+            views = [_quad(src, q) for _, q in terms]
+            nin = len(views)
+            nat.check(lib.paco_tf32b2_split(
+                dev, stream.cuda_stream, nin, (ctypes.c_void_p * nin)(*[v.ptr for v in views]),
+                (ctypes.c_int64 * nin)(*[v.ld for v in views]), (ctypes.c_int32 * nin)(*[c for c, _ in terms]),
+                h, h, int(tr), hi.data_ptr(), h16.data_ptr(), l16.data_ptr(), h))
+            row += [hi, h16, l16]
+        bufs.append(row)
+    ndst = (ctypes.c_int32 * 7)()
+    dst = (ctypes.c_void_p * 28)()
+    sign = (ctypes.c_int32 * 28)()
+    ld = None
+    for r in range(1, 8):
+        targets = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
+        if len(targets) > 4:
+            raise ValueError("a leaf product folds into at most 4 C blocks")
+        ndst[r - 1] = len(targets)
+        for d, (v, sg) in enumerate(targets):
+            dst[4 * (r - 1) + d], sign[4 * (r - 1) + d] = v.ptr, sg
+            if ld is None:
+                ld = v.ld
+            elif v.ld != ld:
+                raise ValueError("destinations must share one row pitch")
+
+    def arr(i):
+        return (ctypes.c_void_p * 7)(*[row[i].data_ptr() for row in bufs])
+
+    nat.check(lib.paco_mm_tf32b2_multi(dev, stream.cuda_stream, 7, arr(0), arr(1), arr(2), h, arr(3), arr(4), arr(5), h,
+                                       ndst, dst, sign, ld, h, h, h))
+    for row in bufs:
+        for t in row:
             t.record_stream(stream)
 
 
@@ -634,6 +687,12 @@ FUSED_PRODUCER = False
 # cfg5 (32.1-33.1 vs 32.0-32.9 ms; the leaf launches slow by ~8 %, the same as the
 # 1.9 ms of A-side splits they save -- DESIGN.md section 5)
 FUSED_A = False
+# Leaf products on CTA pairs in the tf32 + 2 x bf16 format (paco_mm_tf32b2_multi):
+# hi*hi on tf32, the hi*lo + lo*hi corrections as bf16 MMAs (a third less tensor
+# time).  Off: the pair kernel's operands already stream from L2 at ~10 TB/s, so the
+# leaf launches stay 26.2 ms (vs 26.4) while the 3-array splits cost more (cfg5
+# 33.3-33.9 vs 32.0-32.9 ms)
+TF32B2 = False
 
 
 def _pair_batch(n: int, m: int, count: int) -> bool:

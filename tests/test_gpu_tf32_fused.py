@@ -205,3 +205,72 @@ def test_strassen_pair_leaves_fused_a(monkeypatch):
         assert float((c[rows].double() - ref).norm() / ref.norm()) < 1e-4, fuse_a
         out[fuse_a] = c
     assert float((out[True] - out[False]).norm() / out[False].norm()) < 1e-6
+
+
+@pytest.mark.parametrize("shape", [(2048, 2048, 512, 4), (2000, 1800, 333, 8)])
+def test_tf32b2_pair_kernel_accuracy(shape):
+    """The tf32 + 2 x bf16 format (paco_tf32b2_split + paco_mm_tf32b2_multi): hi*hi
+    on tf32, hi*lo + lo*hi on bf16 MMAs, two signed destinations per product.
+    Accuracy vs the f64 products must stay in the 3xTF32 class (<= 2x its error,
+    and < 1e-5 absolute relative error), far inside cfg5's 1e-4."""
+    n, m, k, cnt = shape
+    lib = nat.load()
+    st = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(k + cnt)
+    kp = (k + 7) // 8 * 8   # 16-byte bf16 rows
+    a = [(torch.rand(n, kp, device="cuda", generator=g) * 2 - 1) for _ in range(cnt)]
+    b = [(torch.rand(m, kp, device="cuda", generator=g) * 2 - 1) for _ in range(cnt)]
+    for x in a + b:
+        x[:, k:] = 0
+
+    def split3(x):
+        hi = torch.zeros_like(x)
+        h16 = torch.zeros(x.shape, dtype=torch.bfloat16, device="cuda")
+        l16 = torch.zeros(x.shape, dtype=torch.bfloat16, device="cuda")
+        nat.check(lib.paco_tf32b2_split(0, st, 1, (ctypes.c_void_p * 1)(x.data_ptr()), (ctypes.c_int64 * 1)(kp),
+                                        (ctypes.c_int32 * 1)(1), x.shape[0], k, 0, hi.data_ptr(), h16.data_ptr(),
+                                        l16.data_ptr(), kp))
+        return hi, h16, l16
+    sa, sb = [split3(x) for x in a], [split3(x) for x in b]
+    # the format itself: hi is tf32 (13 low bits zero), hi + lo reproduces x to bf16(lo)'s precision
+    hi0 = sa[0][0]
+    assert int((hi0.view(torch.int32) & 0x1FFF).abs().sum()) == 0
+    rec = hi0[:, :k].double() + sa[0][2][:, :k].double()
+    assert float((rec - a[0][:, :k].double()).abs().max()) <= 2.0 ** -19
+    arr = lambda xs: (ctypes.c_void_p * cnt)(*[x.data_ptr() for x in xs])  # noqa: E731
+    C = [torch.zeros(n, m, device="cuda") for _ in range(2)]
+    ndst = (ctypes.c_int32 * cnt)(*[2] * cnt)
+    dst = (ctypes.c_void_p * (4 * cnt))()
+    sign = (ctypes.c_int32 * (4 * cnt))()
+    ref = [torch.zeros(n, m, dtype=torch.float64, device="cuda") for _ in range(2)]
+    for q in range(cnt):
+        dst[4 * q], dst[4 * q + 1] = C[q % 2].data_ptr(), C[(q + 1) % 2].data_ptr()
+        sign[4 * q], sign[4 * q + 1] = 1, (-1 if q % 2 else 1)
+        p = a[q][:, :k].double() @ b[q][:, :k].double().t()
+        ref[q % 2] += p
+        ref[(q + 1) % 2] += -p if q % 2 else p
+    nat.check(lib.paco_mm_tf32b2_multi(0, st, cnt, arr([x[0] for x in sa]), arr([x[1] for x in sa]),
+                                       arr([x[2] for x in sa]), kp, arr([x[0] for x in sb]), arr([x[1] for x in sb]),
+                                       arr([x[2] for x in sb]), kp, ndst, dst, sign, m, n, m, k))
+    torch.cuda.synchronize()
+    for i in range(2):
+        assert float((C[i].double() - ref[i]).norm() / ref[i].norm()) < 1e-5, i
+
+
+def test_strassen_tf32b2_vs_3xtf32(monkeypatch):
+    """cfg5's shape at half size (8192, 2 levels): the tf32 + 2 x bf16 leaves vs the
+    3xTF32 leaves -- both within 1e-4 of the f64 product, and the tf32b2 error no
+    more than 1.5x the 3xTF32 one (Strassen's fp32 formation dominates both)."""
+    n, base = 8192, 2048
+    g = torch.Generator(device="cuda").manual_seed(8)
+    a = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+    b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+    rows = torch.arange(0, n, 61, device="cuda")
+    ref = a[rows].double() @ b.double()
+    err = {}
+    for b2 in (True, False):
+        monkeypatch.setattr(S, "TF32B2", b2)
+        c = S.strassen_seq(a, b, n, base=base)
+        err[b2] = float((c[rows].double() - ref).norm() / ref.norm())
+    assert err[True] < 1e-4 and err[False] < 1e-4, err
+    assert err[True] <= 1.5 * err[False], err
