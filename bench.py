@@ -53,7 +53,7 @@ WORKLOADS = {
     2: "cfg2: (min,+) saturating tropical MM n=m=k=8192, int32 [0,2^20) + 10% INF=2^30 (BASELINE.json configs[1])",
     3: "cfg3: (+,x) bf16 N(0,1) 65536x256 . 256x1024 -> fp32, tcgen05 (BASELINE.json configs[2])",
     4: "cfg4: (max,+) MM n=m=k=16384, int32 [-2^20,2^20) (BASELINE.json configs[3])",
-    5: "cfg5: Strassen (+,x) fp32 U(-1,1) n=16384, 2 levels (49 leaves of 4096^3), 3xTF32 tcgen05 leaves "
+    5: "cfg5: Strassen (+,x) fp32 U(-1,1) n=16384, 2 levels (49 leaves of 4096^3), tcgen05 leaves "
        "(BASELINE.json configs[4])",
 }
 
@@ -360,28 +360,35 @@ def measure_config(cfg, dev, args, peaks, probes):
                                                     ("elementwise", nat.KT_ELEMENTWISE))}
         per_step = {k_: {"ms": v[0] / 3, "launches": v[1] // 3} for k_, v in fam.items()}
         alg = 49 * 2 * 4096 ** 3 + 18 * 8192 ** 2 + 7 * 18 * 4096 ** 2
-        mma = 3 * 49 * 2 * 4096 ** 3
         tf32_peak = peaks["bf16_tflops"] / 2
+        b2 = S.TF32B2 and S._pair_batch(4096, 4096, 7)
+        # tensor work in tf32-equivalent flop (a bf16 MMA runs at twice the tf32 rate):
+        # 3xTF32: 3 tf32 products; tf32 + 2 x bf16: 1 tf32 product + 2 bf16 products = 2 tf32-equivalents
+        per_product = 2 * 4096 ** 3 * (2 if b2 else 3)
+        mma = 49 * per_product
         leaf_ms = per_step["tc_gemm"]["ms"]
         leaf_launch_ms = leaf_ms / max(1, per_step["tc_gemm"]["launches"])
         leaf_flop = mma / max(1, per_step["tc_gemm"]["launches"])   # one launch = 7 products of 4096^3
         achieved = leaf_flop / leaf_launch_ms / 1e9
-        traffic, src = ncu_traffic("r1_tf32x3_ncu.json")
+        traffic, src = ncu_traffic("r2_tf32x3_pair_ncu.json")
+        fmt = ("tf32 + 2 x bf16 split products (hi*hi on kind::tf32, hi*lo + lo*hi on kind::f16, bf16(hi) formed "
+               "in the kernel), fp32 accumulation" if b2 else "3xTF32 split products, fp32 accumulation")
         out.update(ms=ms, value=alg / ms / 1e6, unit="Gop/s", ops_per_step=alg, steps=steps, warmup=warmup,
                    classic_equivalent_gop_s=2.0 * n ** 3 / ms / 1e6,
                    gpu_launches_per_step=sum(v["launches"] for v in per_step.values()),
-                   kernels_per_step=per_step,
-                   step="strassen_seq(A, B, 16384, base=4096): 2 Strassen levels, 49 leaf products on tcgen05 as "
-                        "3xTF32 (7 batched launches), C combination fused into the leaf epilogues",
+                   kernels_per_step=per_step, leaf_format=fmt,
+                   step="strassen_seq(A, B, 16384, base=4096): 2 Strassen levels, 49 leaf products of 4096^3 on CTA "
+                        "pairs (tcgen05 cta_group::2; 7 batched launches), C combination fused into the leaf epilogues",
                    l2="A, B 1 GiB each > 126 MB L2 (no flush)",
-                   roofline={"bound": "tensor", "kernel": "tc_pair_kernel (3xTF32 Strassen leaves on CTA pairs, "
-                                                           "tcgen05 cta_group::2)",
-                             "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
-                             "achieved_note": "3 x 7 x 2 x 4096^3 MMA flop per launch / its average CUDA-event "
-                                              "duration inside the step",
+                   roofline={"bound": "tensor", "kernel": "tc_pair_kernel (Strassen leaves on CTA pairs)",
+                             "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s (tf32-equivalent)",
+                             "frac": achieved / tf32_peak,
+                             "achieved_note": ("tensor work of one launch (7 products of 4096^3, in tf32-equivalent "
+                                               "flop: " + ("2" if b2 else "3") + " x 2 x 4096^3 each) / its average "
+                                               "CUDA-event duration inside the step"),
                              "step_frac": mma / ms / 1e9 / tf32_peak,
-                             "step_note": "whole step: 3 x 49 x 2 x 4096^3 tf32 MMA flop / step time",
-                             "peak_source": f"TF32 dense = bf16_tflops / 2 {peaks['source']}",
+                             "step_note": "whole step: 49 leaf products' tensor work / step time",
+                             "peak_source": f"TF32 dense = bf16_tflops / 2 {peaks['source']} (bf16 MMAs count half)",
                              "traffic": traffic, "traffic_source": src},
                    clocks=clk.summary())
         return out
@@ -699,11 +706,14 @@ class MultiGPU:
             return {"bound": "hbm", "achieved": gbs, "peak": self.peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": gbs / self.peaks["hbm_gbs"], "per": "GPU (rank 0's algorithmic bytes / step time)",
                     "peak_source": f"hbm_gbs {self.peaks['source']}"}
-        mma = 3 * 49 * 2 * 4096 ** 3 / self.world
+        from paper_2011_01441_b200 import strassen as S
+        passes = 2 if S.TF32B2 else 3   # tf32-equivalent products per leaf (tf32 + 2 x bf16 vs 3xTF32)
+        mma = passes * 49 * 2 * 4096 ** 3 / self.world
         tf = mma / (ms * 1e-3) / 1e12
         peak = self.peaks["bf16_tflops"] / 2
-        return {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
-                "per": "GPU (3xTF32 MMA flop / N / step time, reduce-scatter included)",
+        return {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s (tf32-equivalent)",
+                "frac": tf / peak,
+                "per": "GPU (leaf tensor work / N / step time, reduce-scatter included)",
                 "peak_source": f"TF32 dense = bf16_tflops / 2 {self.peaks['source']}"}
 
     def e2e(self, steps):

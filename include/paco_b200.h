@@ -242,7 +242,7 @@ int paco_mm_tf32x3_fused_a(int device, void* stream, int count, const int32_t* n
 /* The tf32 + 2 x bf16 format of an fp32 operand (the Strassen leaves' default on
  * CTA pairs): x = sum_i coef[i] * in[i] (as paco_tf32_split) is written as
  * hi = tf32_rn(x) (fp32), h16 = bf16_rn(hi), l16 = bf16_rn(x - hi) (bf16 arrays),
- * all with row pitch ldo elements, transposed when `transpose`. */
+ * all with row pitch ldo elements, transposed when `transpose` (h16 may be NULL). */
 int paco_tf32b2_split(int device, void* stream, int nin, const void* const* ins, const int64_t* lds,
                       const int32_t* coefs, int64_t rows, int64_t cols, int transpose, void* hi, void* h16, void* l16,
                       int64_t ldo);
@@ -253,7 +253,9 @@ int paco_tf32b2_split(int device, void* stream, int nin, const void* const* ins,
  * on CTA pairs (cta_group::2).  The corrections are 2^-11 of the product, so their
  * bf16 rounding adds ~2^-19 relative per term -- below the fp32 accumulation and
  * Strassen formation errors of cfg5 (tests/test_gpu_tf32_fused.py).  A n x k (lda),
- * B^T m x k (ldb), destinations as paco_mm_tf32x3_multi. */
+ * B^T m x k (ldb), destinations as paco_mm_tf32x3_multi.  a_h16 = b_h16 = NULL:
+ * the kernel forms bf16(hi) from the hi tiles itself (6 instead of 8 bytes of
+ * operand traffic per element; paco_tf32b2_split then takes h16 = NULL too). */
 int paco_mm_tf32b2_multi(int device, void* stream, int count, const void* const* a_hi, const void* const* a_h16,
                          const void* const* a_l16, int64_t lda, const void* const* b_hi, const void* const* b_h16,
                          const void* const* b_l16, int64_t ldb, const int32_t* ndst, void* const* dst,

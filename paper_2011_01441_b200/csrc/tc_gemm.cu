@@ -260,6 +260,11 @@ __device__ __forceinline__ float round_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);  // .x = a (low half)
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
 // The same rounding on the integer ALU (cvt.rna.tf32 issues on the narrow XU
 // pipe): add half an ulp of tf32 to the magnitude bits and clear the 13 low
 // bits -- round half away from zero, as .rna; carries roll into the exponent
@@ -863,13 +868,16 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
 // releases the accumulator with a remote arrive on the leader's barrier.
 // Tiles (256 x 256 of C) are dealt to pairs statically in row-band order.
 // ---------------------------------------------------------------------------
-template <int ST, bool FA = false, bool B2 = false>
+template <int ST, bool FA = false, bool B2 = false, bool CV = false>
 struct PairLayout {
   static constexpr int BK = 16, BN = 256, BNH = 128, EC = 16, EW = 4, EB = 2;
   // FA: A is formed in the kernel (Strassen's S_r from <= 2 signed raw views,
   // TMA'd into the stage's hi / lo slots and split there in place by CW
-  // converter warps); B^T arrives pre-split
-  static constexpr int CW = FA ? 4 : 0;
+  // converter warps); B^T arrives pre-split.
+  // CV (with B2): bf16(hi) of both operands is formed in the kernel from the
+  // tf32 hi tiles (fp32 SW64 -> bf16 SW32) by CW converter warps, so each operand
+  // element costs 6 bytes of L2 traffic instead of 8
+  static constexpr int CW = (FA || CV) ? 4 : 0;
   static constexpr int A_BYTES = BM * BK * 4;          // 8 KB: 128 rows x 16 fp32
   static constexpr int B_BYTES = BNH * BK * 4;         // 8 KB: this CTA's half of B^T
   static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
@@ -972,10 +980,10 @@ __device__ __forceinline__ void pair_tile(const TcArgs& a, int32_t t, int& q, in
   rb = r0 + v % rows;
 }
 
-template <int ST, bool FA, bool B2>
-__global__ void __launch_bounds__(PairLayout<ST, FA, B2>::THREADS, 1)
+template <int ST, bool FA, bool B2, bool CV = false>
+__global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
     tc_pair_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
-  using L = PairLayout<ST, FA, B2>;
+  using L = PairLayout<ST, FA, B2, CV>;
   constexpr int BK = L::BK, BN = L::BN;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1052,6 +1060,16 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2>::THREADS, 1)
               if (o < P.nta) tma_load_2d(smem + L::a_off(s, o), &P.a[o], &rfull[s], P.a_col0[o] + kb * BK, arow);
               tma_load_2d_pair(smem + L::b_off(s, o), &P.b[o], fb, P.b_col0[o] + kb * BK, brow);
             }
+          } else if constexpr (CV) {
+            // hi (fp32) and bf16(x - hi) tiles into this CTA's stage on its own barrier;
+            // the converters add bf16(hi) and signal the leader (2 x 16 bytes)
+            if (leader) mbar_expect_tx_relaxed(&full[s], 2 * 16);
+            mbar_expect_tx_relaxed(&rfull[s], uint32_t(L::A_BYTES + L::B_BYTES + 2 * L::H16_BYTES));
+            const int kc = kb * BK;
+            tma_load_2d(smem + L::hi_a(s), &P.a[0], &rfull[s], P.a_col0[0] + kc, arow);
+            tma_load_2d(smem + L::hi_b(s), &P.b[0], &rfull[s], P.b_col0[0] + kc, brow);
+            tma_load_2d(smem + L::x16(s, 1), &P.a2, &rfull[s], P.a2_col0 + kc, arow);
+            tma_load_2d(smem + L::x16(s, 3), &P.b2, &rfull[s], P.b2_col0 + kc, brow);
           } else if constexpr (B2) {
             if (leader) mbar_expect_tx_relaxed(&full[s], 2 * L::STAGE_BYTES);
             const int kc = kb * BK;
@@ -1087,7 +1105,7 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2>::THREADS, 1)
           const int s = it % ST;
           mbar_wait(&full[s], (it / ST) & 1);
           tc_fence_after();
-          if constexpr (B2) {
+          if constexpr (B2 || CV) {
             // hi*hi on the tf32 path (two K = 8 steps), hi*lo and lo*hi as bf16 (one K = 16 each)
             const uint64_t ah = smem_desc_sw64(smem_u32(smem + L::hi_a(s)));
             const uint64_t bh = smem_desc_sw64(smem_u32(smem + L::hi_b(s)));
@@ -1118,7 +1136,49 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2>::THREADS, 1)
       }
     }
   } else if (warp >= 2 + L::EW) {
-    if constexpr (FA) {
+    if constexpr (CV) {
+      // ---------------- converter warps (CV, both CTAs): bf16(hi) tiles from the tf32 hi tiles ----------------
+      // fp32 tile: row r at r*64, 16-byte chunk c (4 elements) at (c ^ ((r >> 1) & 3)) * 16 (SWIZZLE_64B);
+      // bf16 tile: row r at r*32, 16-byte chunk c8 (8 elements) at (c8 ^ ((r >> 2) & 1)) * 16 (SWIZZLE_32B)
+      const int ct = (warp - 2 - L::EW) * 32 + lane;
+      constexpr int NTH = 32 * (L::CW > 0 ? L::CW : 1);
+      constexpr int CH = (BM + L::BNH) * 4;  // fp32 16-byte chunks of the A and B^T hi tiles
+      static_assert(CH % NTH == 0, "whole chunks per converter thread");
+      const uint32_t full_leader0 = mapa_rank(smem_u32(&full[0]), 0);
+      const uint32_t sig_leader = mapa_rank(smem_u32(sig), 0);
+      const uint32_t sbase = smem_u32(smem);
+      uint32_t it = 0;
+      for (int32_t t = pair; t < total; t += npairs) {
+        for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
+          const int s = it % ST;
+          mbar_wait(&rfull[s], (it / ST) & 1);
+          uint4 x[CH / NTH];
+#pragma unroll
+          for (int u = 0; u < CH / NTH; ++u) {
+            const int c = ct + u * NTH, isb = c >= BM * 4, cc = isb ? c - BM * 4 : c;
+            const int r = cc >> 2, c4 = cc & 3;
+            x[u] = lds128(sbase + (isb ? L::hi_b(s) : L::hi_a(s)) + r * 64 + ((c4 ^ ((r >> 1) & 3)) << 4));
+          }
+#pragma unroll
+          for (int u = 0; u < CH / NTH; ++u) {
+            const int c = ct + u * NTH, isb = c >= BM * 4, cc = isb ? c - BM * 4 : c;
+            const int r = cc >> 2, c4 = cc & 3, c8 = c4 >> 1;
+            const uint32_t dst = sbase + L::x16(s, isb ? 2 : 0) + r * 32 + ((c8 ^ ((r >> 2) & 1)) << 4) + (c4 & 1) * 8;
+            const uint32_t lo = pack_bf16x2(__uint_as_float(x[u].x), __uint_as_float(x[u].y));
+            const uint32_t hi = pack_bf16x2(__uint_as_float(x[u].z), __uint_as_float(x[u].w));
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(dst), "r"(lo), "r"(hi) : "memory");
+          }
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          asm volatile("bar.sync 1, %0;\n" ::"n"(NTH) : "memory");
+          if (ct == 0)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];\n" ::"r"(
+                    sig_leader + rank * 16u),
+                "r"(smem_u32(sig)), "r"(full_leader0 + uint32_t(s) * 8u)
+                : "memory");
+        }
+      }
+    } else if constexpr (FA) {
       // ---------------- converter warps (FA, both CTAs): S_r tile formed and split in place ----------------
       const int ct = (warp - 2 - L::EW) * 32 + lane;
       constexpr int NTH = 32 * (L::CW > 0 ? L::CW : 1), A_CH = L::A_BYTES / 16, PER = A_CH / NTH;
@@ -1418,10 +1478,6 @@ __device__ __forceinline__ float lc_value(const SplitIn& in, int64_t i, int64_t 
 // B^T the 3xTF32 MMAs read).  kVec: every view 16 B aligned, cols % 4 == 0.
 // kB2 (the tf32 + 2 x bf16 format): hi = tf32_rn(x) as fp32, h16 = bf16_rn(hi),
 // l16 = bf16_rn(x - hi) -- `lo` unused.
-__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
-  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);  // .x = a (low half)
-  return *reinterpret_cast<const uint32_t*>(&v);
-}
 
 template <bool kVec, bool kB2>
 __global__ void __launch_bounds__(256) split_tf32_t_kernel(const SplitIn in, float* __restrict__ hi,
@@ -1493,7 +1549,8 @@ __global__ void __launch_bounds__(256) split_tf32_t_kernel(const SplitIn in, flo
     if (kVec && i + 3 < rows) {
       *reinterpret_cast<float4*>(hi + j * ldo + i) = h;
       if constexpr (kB2) {
-        *reinterpret_cast<uint2*>(h16 + j * ldo + i) = make_uint2(pack_bf16x2(h.x, h.y), pack_bf16x2(h.z, h.w));
+        if (h16)
+          *reinterpret_cast<uint2*>(h16 + j * ldo + i) = make_uint2(pack_bf16x2(h.x, h.y), pack_bf16x2(h.z, h.w));
         *reinterpret_cast<uint2*>(l16 + j * ldo + i) = make_uint2(pack_bf16x2(l.x, l.y), pack_bf16x2(l.z, l.w));
       } else {
         *reinterpret_cast<float4*>(lo + j * ldo + i) = l;
@@ -1505,7 +1562,7 @@ __global__ void __launch_bounds__(256) split_tf32_t_kernel(const SplitIn in, flo
         if (i + e < rows) {
           hi[j * ldo + i + e] = hv[e];
           if constexpr (kB2) {
-            h16[j * ldo + i + e] = __float2bfloat16_rn(hv[e]);
+            if (h16) h16[j * ldo + i + e] = __float2bfloat16_rn(hv[e]);
             l16[j * ldo + i + e] = __float2bfloat16_rn(lv[e]);
           } else {
             lo[j * ldo + i + e] = lv[e];
@@ -1558,8 +1615,9 @@ __global__ void split_tf32_n_kernel(const SplitIn in, float* __restrict__ hi, fl
         const int64_t i = i0 + u * gy;
         __stcs(reinterpret_cast<float4*>(hi + i * ldo + j), make_float4(h[0], h[1], h[2], h[3]));
         if constexpr (kB2) {
-          __stcs(reinterpret_cast<uint2*>(h16 + i * ldo + j),
-                 make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3])));
+          if (h16)
+            __stcs(reinterpret_cast<uint2*>(h16 + i * ldo + j),
+                   make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3])));
           __stcs(reinterpret_cast<uint2*>(l16 + i * ldo + j),
                  make_uint2(pack_bf16x2(l[0], l[1]), pack_bf16x2(l[2], l[3])));
         } else {
@@ -1596,7 +1654,8 @@ __global__ void split_tf32_n_kernel(const SplitIn in, float* __restrict__ hi, fl
     if (kVec) {
       *reinterpret_cast<float4*>(hi + i * ldo + j) = make_float4(h[0], h[1], h[2], h[3]);
       if constexpr (kB2) {
-        *reinterpret_cast<uint2*>(h16 + i * ldo + j) = make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]));
+        if (h16)
+          *reinterpret_cast<uint2*>(h16 + i * ldo + j) = make_uint2(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]));
         *reinterpret_cast<uint2*>(l16 + i * ldo + j) = make_uint2(pack_bf16x2(l[0], l[1]), pack_bf16x2(l[2], l[3]));
       } else {
         *reinterpret_cast<float4*>(lo + i * ldo + j) = make_float4(l[0], l[1], l[2], l[3]);
@@ -1607,7 +1666,7 @@ __global__ void split_tf32_n_kernel(const SplitIn in, float* __restrict__ hi, fl
         if (j + e < cols) {
           hi[i * ldo + j + e] = h[e];
           if constexpr (kB2) {
-            h16[i * ldo + j + e] = __float2bfloat16_rn(h[e]);
+            if (h16) h16[i * ldo + j + e] = __float2bfloat16_rn(h[e]);
             l16[i * ldo + j + e] = __float2bfloat16_rn(l[e]);
           } else {
             lo[i * ldo + j + e] = l[e];
@@ -1640,7 +1699,7 @@ int launch_split(const tc::SplitIn& in, int64_t rows, int64_t cols, bool transpo
                  int64_t ldo, cudaStream_t st, __nv_bfloat16* h16 = nullptr, __nv_bfloat16* l16 = nullptr) {
   if (rows <= 0 || cols <= 0) return PACO_OK;
   KernelSpan ks(PACO_KT_TF32_SPLIT, st);
-  const bool b2 = h16 != nullptr;
+  const bool b2 = l16 != nullptr;  // h16 may be null: the kernel forms bf16(hi) itself
   bool vec = (ldo % 4 == 0) && (reinterpret_cast<uintptr_t>(h) % 16 == 0) &&
              (b2 ? (reinterpret_cast<uintptr_t>(h16) % 8 == 0 && reinterpret_cast<uintptr_t>(l16) % 8 == 0)
                  : (reinterpret_cast<uintptr_t>(l) % 16 == 0));
@@ -1958,10 +2017,11 @@ int run_pair(int device, cudaStream_t stream, const tc::TcMaps& maps, int count,
   args.groups = 1;
   const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb * count;
   const int pairs = int(tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
-  auto kern = mode == 1 ? tc::tc_pair_kernel<PACO_PAIR_ST, true, false>
-                        : (mode == 2 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true>
-                                     : tc::tc_pair_kernel<PACO_PAIR_ST, false, false>);
-  const int threads = mode == 1 ? tc::PairLayout<PACO_PAIR_ST, true>::THREADS : L::THREADS;
+  auto kern = mode == 1   ? tc::tc_pair_kernel<PACO_PAIR_ST, true, false>
+              : mode == 2 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true>
+              : mode == 3 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true, true>
+                          : tc::tc_pair_kernel<PACO_PAIR_ST, false, false>;
+  const int threads = (mode == 1 || mode == 3) ? tc::PairLayout<PACO_PAIR_ST, true>::THREADS : L::THREADS;
   {
     static std::atomic<uint64_t> attr_set{0};
     const uint64_t bit = uint64_t(1) << ((device & 15) * 4 + mode);
@@ -2252,8 +2312,9 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
                            const void* const* b_h16, const void* const* b_l16, int64_t ldb, const int32_t* ndst,
                            void* const* dst, const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k) {
   using L = tc::PairLayout<PACO_PAIR_ST>;
-  if (count < 1 || count > tc::kMaxBatch || !a_hi || !a_h16 || !a_l16 || !b_hi || !b_h16 || !b_l16 || !ndst || !dst ||
-      !sign) {
+  const bool cv = a_h16 == nullptr;  // bf16(hi) formed in the kernel (mode 3)
+  if (count < 1 || count > tc::kMaxBatch || !a_hi || !a_l16 || !b_hi || !b_l16 || !ndst || !dst || !sign ||
+      (!cv && (!a_h16 || !b_h16))) {
     set_error("paco_mm_tf32b2_multi: count=%d (1..%d) and every operand / destination array required", count,
               tc::kMaxBatch);
     return PACO_ERR_ARG;
@@ -2270,8 +2331,8 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
   for (int q = 0; q < count; ++q) {
-    if (!pitch_ok(a_hi[q], lda, 4) || !pitch_ok(b_hi[q], ldb, 4) || !pitch_ok(a_h16[q], lda, 2) ||
-        !pitch_ok(a_l16[q], lda, 2) || !pitch_ok(b_h16[q], ldb, 2) || !pitch_ok(b_l16[q], ldb, 2)) {
+    if (!pitch_ok(a_hi[q], lda, 4) || !pitch_ok(b_hi[q], ldb, 4) || (!cv && !pitch_ok(a_h16[q], lda, 2)) ||
+        !pitch_ok(a_l16[q], lda, 2) || (!cv && !pitch_ok(b_h16[q], ldb, 2)) || !pitch_ok(b_l16[q], ldb, 2)) {
       set_error("paco_mm_tf32b2_multi: operands need 16-byte aligned starts and row pitches");
       return PACO_ERR_UNSUPPORTED;
     }
@@ -2281,10 +2342,10 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
     }
     tc::TcProb& P = maps.p[q];
     if ((rc = make_map(&P.a[0], F32, 4, a_hi[q], n, k, lda, L::BK, tc::BM, &P.a_col0[0], S64)) ||
-        (rc = make_map(&P.a[1], B16, 2, a_h16[q], n, k, lda, L::BK, tc::BM, &P.a_col0[1], S32)) ||
+        (rc = make_map(&P.a[1], B16, 2, cv ? a_l16[q] : a_h16[q], n, k, lda, L::BK, tc::BM, &P.a_col0[1], S32)) ||
         (rc = make_map(&P.a2, B16, 2, a_l16[q], n, k, lda, L::BK, tc::BM, &P.a2_col0, S32)) ||
         (rc = make_map(&P.b[0], F32, 4, b_hi[q], m, k, ldb, L::BK, L::BNH, &P.b_col0[0], S64)) ||
-        (rc = make_map(&P.b[1], B16, 2, b_h16[q], m, k, ldb, L::BK, L::BNH, &P.b_col0[1], S32)) ||
+        (rc = make_map(&P.b[1], B16, 2, cv ? b_l16[q] : b_h16[q], m, k, ldb, L::BK, L::BNH, &P.b_col0[1], S32)) ||
         (rc = make_map(&P.b2, B16, 2, b_l16[q], m, k, ldb, L::BK, L::BNH, &P.b2_col0, S32)))
       return rc;
     P.ndst = ndst[q];
@@ -2300,7 +2361,7 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
         return rc;
     }
   }
-  return run_pair(device, stream, maps, count, n, m, k, 0, 2);
+  return run_pair(device, stream, maps, count, n, m, k, 0, cv ? 3 : 2);
 }
 
 int launch_tf32b2_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,
@@ -2310,7 +2371,7 @@ int launch_tf32b2_split(cudaStream_t stream, int nin, const void* const* ins, co
     set_error("paco_tf32b2_split: nin=%d (1..4 supported)", nin);
     return PACO_ERR_ARG;
   }
-  if (!hi || !h16 || !l16 || ldo < (transpose ? rows : cols)) {
+  if (!hi || !l16 || ldo < (transpose ? rows : cols)) {
     set_error("paco_tf32b2_split: bad outputs or pitch");
     return PACO_ERR_ARG;
   }

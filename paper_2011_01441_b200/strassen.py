@@ -467,19 +467,20 @@ def _leaf_level_b2(A: View, B: View, dests, stream) -> None:
     h = A.rows // 2
     dev = A.device
     lib = nat.load()
+    cv = TF32B2_CONVERT   # bf16(hi) formed inside the kernel: 6 B of operand traffic per element, not 8
     bufs = []
     for r in range(1, 8):
         row = []
         for terms, src, tr in ((S_TERMS[r], A, False), (T_TERMS[r], B, True)):
             hi = torch.empty((h, h), dtype=torch.float32, device=dev)
-            h16 = torch.empty((h, h), dtype=torch.bfloat16, device=dev)
+            h16 = None if cv else torch.empty((h, h), dtype=torch.bfloat16, device=dev)
             l16 = torch.empty((h, h), dtype=torch.bfloat16, device=dev)
             views = [_quad(src, q) for _, q in terms]
             nin = len(views)
             nat.check(lib.paco_tf32b2_split(
                 dev, stream.cuda_stream, nin, (ctypes.c_void_p * nin)(*[v.ptr for v in views]),
                 (ctypes.c_int64 * nin)(*[v.ld for v in views]), (ctypes.c_int32 * nin)(*[c for c, _ in terms]),
-                h, h, int(tr), hi.data_ptr(), h16.data_ptr(), l16.data_ptr(), h))
+                h, h, int(tr), hi.data_ptr(), None if cv else h16.data_ptr(), l16.data_ptr(), h))
             row += [hi, h16, l16]
         bufs.append(row)
     ndst = (ctypes.c_int32 * 7)()
@@ -499,13 +500,19 @@ def _leaf_level_b2(A: View, B: View, dests, stream) -> None:
                 raise ValueError("destinations must share one row pitch")
 
     def arr(i):
+        if row_none(i):
+            return None
         return (ctypes.c_void_p * 7)(*[row[i].data_ptr() for row in bufs])
+
+    def row_none(i):
+        return bufs[0][i] is None
 
     nat.check(lib.paco_mm_tf32b2_multi(dev, stream.cuda_stream, 7, arr(0), arr(1), arr(2), h, arr(3), arr(4), arr(5), h,
                                        ndst, dst, sign, ld, h, h, h))
     for row in bufs:
         for t in row:
-            t.record_stream(stream)
+            if t is not None:
+                t.record_stream(stream)
 
 
 def _strassen_tc_fused(A: View, B: View, dests, base: int, stream) -> None:
@@ -689,10 +696,12 @@ FUSED_PRODUCER = False
 FUSED_A = False
 # Leaf products on CTA pairs in the tf32 + 2 x bf16 format (paco_mm_tf32b2_multi):
 # hi*hi on tf32, the hi*lo + lo*hi corrections as bf16 MMAs (a third less tensor
-# time).  Off: the pair kernel's operands already stream from L2 at ~10 TB/s, so the
-# leaf launches stay 26.2 ms (vs 26.4) while the 3-array splits cost more (cfg5
-# 33.3-33.9 vs 32.0-32.9 ms)
-TF32B2 = False
+# time), bf16(hi) formed inside the kernel (TF32B2_CONVERT) so each operand element
+# costs 6 bytes of L2 traffic instead of 8 -- the pair kernel is L2-bandwidth bound
+# without it.  cfg5: 28.8 vs 32.9 ms (3xTF32), error vs f64 2.0e-5 vs 3.0e-5
+# (DESIGN.md section 5).  False: 3xTF32 leaves.
+TF32B2 = True
+TF32B2_CONVERT = True
 
 
 def _pair_batch(n: int, m: int, count: int) -> bool:
