@@ -255,7 +255,10 @@ int paco_tf32b2_split(int device, void* stream, int nin, const void* const* ins,
  * Strassen formation errors of cfg5 (tests/test_gpu_tf32_fused.py).  A n x k (lda),
  * B^T m x k (ldb), destinations as paco_mm_tf32x3_multi.  a_h16 = b_h16 = NULL:
  * the kernel forms bf16(hi) from the hi tiles itself (6 instead of 8 bytes of
- * operand traffic per element; paco_tf32b2_split then takes h16 = NULL too). */
+ * operand traffic per element; paco_tf32b2_split then takes h16 = NULL too).  All
+ * four bf16 arrays NULL: a_hi / b_hi are plain fp32 operands (no split pass at
+ * all); the tf32 MMA reads x (hi = its top 19 bits) and the kernel forms bf16(hi)
+ * and bf16(x - hi) -- 4 bytes per element. */
 int paco_mm_tf32b2_multi(int device, void* stream, int count, const void* const* a_hi, const void* const* a_h16,
                          const void* const* a_l16, int64_t lda, const void* const* b_hi, const void* const* b_h16,
                          const void* const* b_l16, int64_t ldb, const int32_t* ndst, void* const* dst,

@@ -493,14 +493,14 @@ int paco_mm_tf32b2_multi(int device, void* stream, int count, const void* const*
                          const void* const* a_l16, int64_t lda, const void* const* b_hi, const void* const* b_h16,
                          const void* const* b_l16, int64_t ldb, const int32_t* ndst, void* const* dst,
                          const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k) {
-  if (count >= 1 && count <= 8 && a_hi && a_l16 && b_hi && b_l16 && ndst && dst)
+  if (count >= 1 && count <= 8 && a_hi && b_hi && ndst && dst)
     for (int q = 0; q < count; ++q) {
       PACO_TRY(check_view("A_hi", a_hi[q], lda, n, k));
       if (a_h16) PACO_TRY(check_view("A_h16", a_h16[q], lda, n, k));
-      PACO_TRY(check_view("A_l16", a_l16[q], lda, n, k));
+      if (a_l16) PACO_TRY(check_view("A_l16", a_l16[q], lda, n, k));
       PACO_TRY(check_view("Bt_hi", b_hi[q], ldb, m, k));
       if (b_h16) PACO_TRY(check_view("Bt_h16", b_h16[q], ldb, m, k));
-      PACO_TRY(check_view("Bt_l16", b_l16[q], ldb, m, k));
+      if (b_l16) PACO_TRY(check_view("Bt_l16", b_l16[q], ldb, m, k));
       for (int d = 0; d < ndst[q] && d < 4; ++d) PACO_TRY(check_view("C", dst[4 * q + d], ldc, n, m));
     }
   DeviceGuard dg;

@@ -980,7 +980,10 @@ __device__ __forceinline__ void pair_tile(const TcArgs& a, int32_t t, int& q, in
   rb = r0 + v % rows;
 }
 
-template <int ST, bool FA, bool B2, bool CV = false>
+// RAW (with CV): the operands arrive as plain fp32 x; the tf32 MMA reads x itself
+// (the tensor core uses its top 19 bits: hi = trunc_tf32(x)) and the converters
+// form bf16(hi) and bf16(x - hi) -- 4 bytes of L2 traffic per operand element.
+template <int ST, bool FA, bool B2, bool CV = false, bool RAW = false>
 __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
     tc_pair_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
   using L = PairLayout<ST, FA, B2, CV>;
@@ -1064,12 +1067,14 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
             // hi (fp32) and bf16(x - hi) tiles into this CTA's stage on its own barrier;
             // the converters add bf16(hi) and signal the leader (2 x 16 bytes)
             if (leader) mbar_expect_tx_relaxed(&full[s], 2 * 16);
-            mbar_expect_tx_relaxed(&rfull[s], uint32_t(L::A_BYTES + L::B_BYTES + 2 * L::H16_BYTES));
+            mbar_expect_tx_relaxed(&rfull[s], uint32_t(L::A_BYTES + L::B_BYTES + (RAW ? 0 : 2 * L::H16_BYTES)));
             const int kc = kb * BK;
             tma_load_2d(smem + L::hi_a(s), &P.a[0], &rfull[s], P.a_col0[0] + kc, arow);
             tma_load_2d(smem + L::hi_b(s), &P.b[0], &rfull[s], P.b_col0[0] + kc, brow);
-            tma_load_2d(smem + L::x16(s, 1), &P.a2, &rfull[s], P.a2_col0 + kc, arow);
-            tma_load_2d(smem + L::x16(s, 3), &P.b2, &rfull[s], P.b2_col0 + kc, brow);
+            if constexpr (!RAW) {
+              tma_load_2d(smem + L::x16(s, 1), &P.a2, &rfull[s], P.a2_col0 + kc, arow);
+              tma_load_2d(smem + L::x16(s, 3), &P.b2, &rfull[s], P.b2_col0 + kc, brow);
+            }
           } else if constexpr (B2) {
             if (leader) mbar_expect_tx_relaxed(&full[s], 2 * L::STAGE_BYTES);
             const int kc = kb * BK;
@@ -1163,10 +1168,28 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
           for (int u = 0; u < CH / NTH; ++u) {
             const int c = ct + u * NTH, isb = c >= BM * 4, cc = isb ? c - BM * 4 : c;
             const int r = cc >> 2, c4 = cc & 3, c8 = c4 >> 1;
-            const uint32_t dst = sbase + L::x16(s, isb ? 2 : 0) + r * 32 + ((c8 ^ ((r >> 2) & 1)) << 4) + (c4 & 1) * 8;
-            const uint32_t lo = pack_bf16x2(__uint_as_float(x[u].x), __uint_as_float(x[u].y));
-            const uint32_t hi = pack_bf16x2(__uint_as_float(x[u].z), __uint_as_float(x[u].w));
-            asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(dst), "r"(lo), "r"(hi) : "memory");
+            const uint32_t pos = r * 32 + ((c8 ^ ((r >> 2) & 1)) << 4) + (c4 & 1) * 8;
+            if constexpr (RAW) {
+              // hi = what the tf32 MMA reads of x (its top 19 bits), lo = x - hi exactly
+              const uint32_t xb[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+              float h[4], l[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                h[e] = __uint_as_float(xb[e] & 0xFFFFE000u);
+                l[e] = __uint_as_float(xb[e]) - h[e];
+              }
+              asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(sbase + L::x16(s, isb ? 2 : 0) + pos),
+                           "r"(pack_bf16x2(h[0], h[1])), "r"(pack_bf16x2(h[2], h[3]))
+                           : "memory");
+              asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(sbase + L::x16(s, isb ? 3 : 1) + pos),
+                           "r"(pack_bf16x2(l[0], l[1])), "r"(pack_bf16x2(l[2], l[3]))
+                           : "memory");
+            } else {
+              const uint32_t dst = sbase + L::x16(s, isb ? 2 : 0) + pos;
+              const uint32_t lo = pack_bf16x2(__uint_as_float(x[u].x), __uint_as_float(x[u].y));
+              const uint32_t hi = pack_bf16x2(__uint_as_float(x[u].z), __uint_as_float(x[u].w));
+              asm volatile("st.shared.v2.u32 [%0], {%1, %2};\n" ::"r"(dst), "r"(lo), "r"(hi) : "memory");
+            }
           }
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           asm volatile("bar.sync 1, %0;\n" ::"n"(NTH) : "memory");
@@ -2020,8 +2043,9 @@ int run_pair(int device, cudaStream_t stream, const tc::TcMaps& maps, int count,
   auto kern = mode == 1   ? tc::tc_pair_kernel<PACO_PAIR_ST, true, false>
               : mode == 2 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true>
               : mode == 3 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true, true>
+              : mode == 4 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true, true, true>
                           : tc::tc_pair_kernel<PACO_PAIR_ST, false, false>;
-  const int threads = (mode == 1 || mode == 3) ? tc::PairLayout<PACO_PAIR_ST, true>::THREADS : L::THREADS;
+  const int threads = (mode == 1 || mode >= 3) ? tc::PairLayout<PACO_PAIR_ST, true>::THREADS : L::THREADS;
   {
     static std::atomic<uint64_t> attr_set{0};
     const uint64_t bit = uint64_t(1) << ((device & 15) * 4 + mode);
@@ -2312,9 +2336,10 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
                            const void* const* b_h16, const void* const* b_l16, int64_t ldb, const int32_t* ndst,
                            void* const* dst, const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k) {
   using L = tc::PairLayout<PACO_PAIR_ST>;
-  const bool cv = a_h16 == nullptr;  // bf16(hi) formed in the kernel (mode 3)
-  if (count < 1 || count > tc::kMaxBatch || !a_hi || !a_l16 || !b_hi || !b_l16 || !ndst || !dst || !sign ||
-      (!cv && (!a_h16 || !b_h16))) {
+  const bool cv = a_h16 == nullptr;       // bf16(hi) formed in the kernel (mode 3)
+  const bool raw = cv && a_l16 == nullptr;  // plain fp32 operands, both bf16 parts formed in the kernel (mode 4)
+  if (count < 1 || count > tc::kMaxBatch || !a_hi || !b_hi || !ndst || !dst || !sign ||
+      (!cv && (!a_h16 || !b_h16)) || (!raw && (!a_l16 || !b_l16))) {
     set_error("paco_mm_tf32b2_multi: count=%d (1..%d) and every operand / destination array required", count,
               tc::kMaxBatch);
     return PACO_ERR_ARG;
@@ -2332,7 +2357,8 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
   std::lock_guard<std::mutex> lock(mu);
   for (int q = 0; q < count; ++q) {
     if (!pitch_ok(a_hi[q], lda, 4) || !pitch_ok(b_hi[q], ldb, 4) || (!cv && !pitch_ok(a_h16[q], lda, 2)) ||
-        !pitch_ok(a_l16[q], lda, 2) || (!cv && !pitch_ok(b_h16[q], ldb, 2)) || !pitch_ok(b_l16[q], ldb, 2)) {
+        (!raw && !pitch_ok(a_l16[q], lda, 2)) || (!cv && !pitch_ok(b_h16[q], ldb, 2)) ||
+        (!raw && !pitch_ok(b_l16[q], ldb, 2))) {
       set_error("paco_mm_tf32b2_multi: operands need 16-byte aligned starts and row pitches");
       return PACO_ERR_UNSUPPORTED;
     }
@@ -2342,11 +2368,13 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
     }
     tc::TcProb& P = maps.p[q];
     if ((rc = make_map(&P.a[0], F32, 4, a_hi[q], n, k, lda, L::BK, tc::BM, &P.a_col0[0], S64)) ||
-        (rc = make_map(&P.a[1], B16, 2, cv ? a_l16[q] : a_h16[q], n, k, lda, L::BK, tc::BM, &P.a_col0[1], S32)) ||
-        (rc = make_map(&P.a2, B16, 2, a_l16[q], n, k, lda, L::BK, tc::BM, &P.a2_col0, S32)) ||
+        (!raw && (rc = make_map(&P.a[1], B16, 2, cv ? a_l16[q] : a_h16[q], n, k, lda, L::BK, tc::BM,
+                                &P.a_col0[1], S32))) ||
+        (!raw && (rc = make_map(&P.a2, B16, 2, a_l16[q], n, k, lda, L::BK, tc::BM, &P.a2_col0, S32))) ||
         (rc = make_map(&P.b[0], F32, 4, b_hi[q], m, k, ldb, L::BK, L::BNH, &P.b_col0[0], S64)) ||
-        (rc = make_map(&P.b[1], B16, 2, cv ? b_l16[q] : b_h16[q], m, k, ldb, L::BK, L::BNH, &P.b_col0[1], S32)) ||
-        (rc = make_map(&P.b2, B16, 2, b_l16[q], m, k, ldb, L::BK, L::BNH, &P.b2_col0, S32)))
+        (!raw && (rc = make_map(&P.b[1], B16, 2, cv ? b_l16[q] : b_h16[q], m, k, ldb, L::BK, L::BNH,
+                                &P.b_col0[1], S32))) ||
+        (!raw && (rc = make_map(&P.b2, B16, 2, b_l16[q], m, k, ldb, L::BK, L::BNH, &P.b2_col0, S32))))
       return rc;
     P.ndst = ndst[q];
     P.neg = 0;
@@ -2361,7 +2389,12 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
         return rc;
     }
   }
-  return run_pair(device, stream, maps, count, n, m, k, 0, cv ? 3 : 2);
+  if (raw)  // the unused maps are never loaded; give prefetch.tensormap valid ones
+    for (int q = 0; q < count; ++q) {
+      maps.p[q].a[1] = maps.p[q].a2 = maps.p[q].a[0];
+      maps.p[q].b[1] = maps.p[q].b2 = maps.p[q].b[0];
+    }
+  return run_pair(device, stream, maps, count, n, m, k, 0, raw ? 4 : (cv ? 3 : 2));
 }
 
 int launch_tf32b2_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,

@@ -587,7 +587,58 @@ def _leaf_level_fused(A: View, Bt: View, dests, stream) -> None:
                                               ndst, dst, sign, ld, h, h, h))
 
 
-def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream) -> None:
+def _leaf_level_b2raw(A: View, Bt: View, dests, stream) -> None:
+    """Leaf-level node, B given transposed, leaves in the tf32 + 2 x bf16 format
+    with NO split pass: each S_r (from A's quadrants) and T_r^T (from B^T's) is
+    a quadrant view when it has one term, else one fp32 lincomb; the seven
+    products are one ``paco_mm_tf32b2_multi`` launch on plain fp32 operands --
+    the tf32 MMA reads x itself (hi = its top 19 bits) and the kernel forms
+    bf16(hi) and bf16(x - hi) in shared memory (4 bytes of L2 traffic per
+    element)."""
+    h = A.rows // 2
+    dev = A.device
+    keep = []
+
+    def formed(src: View, terms, transpose: bool) -> View:
+        names = [(_tquad(q) if transpose else q) for _, q in terms]
+        if len(terms) == 1 and terms[0][0] == 1:
+            return _quad(src, names[0])
+        # the temporary takes the node's row pitch, so views and sums share one operand pitch
+        buf = torch.empty((h, src.ld), dtype=torch.float32, device=dev)
+        keep.append(buf)
+        out = View.of(buf).sub(0, 0, h, h)
+        _lincomb(nat.DT_F32, stream, out, [(c, _quad(src, nm)) for (c, _), nm in zip(terms, names)])
+        return out
+
+    ops = [(formed(A, S_TERMS[r], False), formed(Bt, T_TERMS[r], True)) for r in range(1, 8)]
+    lda = {v.ld for v, _ in ops}
+    ldb = {v.ld for _, v in ops}
+    if len(lda) != 1 or len(ldb) != 1:
+        raise ValueError("leaf operands must share one row pitch")
+    ndst = (ctypes.c_int32 * 7)()
+    dst = (ctypes.c_void_p * 28)()
+    sign = (ctypes.c_int32 * 28)()
+    ld = None
+    for r in range(1, 8):
+        targets = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
+        if len(targets) > 4:
+            raise ValueError("a leaf product folds into at most 4 C blocks")
+        ndst[r - 1] = len(targets)
+        for d, (v, sg) in enumerate(targets):
+            dst[4 * (r - 1) + d], sign[4 * (r - 1) + d] = v.ptr, sg
+            if ld is None:
+                ld = v.ld
+            elif v.ld != ld:
+                raise ValueError("destinations must share one row pitch")
+    arr = lambda vs: (ctypes.c_void_p * 7)(*[v.ptr for v in vs])  # noqa: E731
+    nat.check(nat.load().paco_mm_tf32b2_multi(dev, stream.cuda_stream, 7, arr([a for a, _ in ops]), None, None,
+                                              lda.pop(), arr([b for _, b in ops]), None, None, ldb.pop(), ndst, dst,
+                                              sign, ld, h, h, h))
+    for t in keep:
+        t.record_stream(stream)
+
+
+def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream, leaf=None) -> None:
     """dests (+/-)= A x B for the fp32 (3xTF32) ring with B given as B^T (the
     fused-producer path): S_r from A's quadrants and T_r^T from B^T's, formed
     by lincomb above the leaf level only; at the leaf level the formation runs
@@ -595,7 +646,7 @@ def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream) -> None:
     epilogues as in ``_strassen_tc_fused``."""
     n = A.rows
     if _leaf_level(n, base) and len(dests) <= 2:
-        _leaf_level_fused(A, Bt, dests, stream)
+        (leaf or _leaf_level_fused)(A, Bt, dests, stream)
         return
     h = n // 2
     dev = A.device
@@ -614,12 +665,23 @@ def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream) -> None:
         child = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
         fits = len(child) <= (2 if _leaf_level(h, base) else 1)
         if h > base and h % 2 == 0 and fits:
-            _strassen_tc_fused_t(S, Tt, child, base, stream)
+            _strassen_tc_fused_t(S, Tt, child, base, stream, leaf)
             continue
         M = View.of(torch.empty((h, h), dtype=torch.float32, device=dev))
         _strassen_dev(S, _transpose(Tt, stream), M, base, torch.float32, stream)
         for D, sd in child:
             _lincomb(nat.DT_F32, stream, D, [(sd, M)], accumulate=True)
+
+
+def _b2raw_ok(n: int, base: int) -> bool:
+    """The raw-operand tf32 + 2 x bf16 leaves apply: a halving chain to a leaf
+    level whose seven products are a CTA-pair batch with 16-byte aligned views."""
+    while n > base and n % 2 == 0:
+        if _leaf_level(n, base):
+            h = n // 2
+            return h % 8 == 0 and _pair_batch(h, h, 7)
+        n //= 2
+    return False
 
 
 def _fused_producer_ok(n: int, base: int) -> bool:
@@ -702,6 +764,10 @@ FUSED_A = False
 # (DESIGN.md section 5).  False: 3xTF32 leaves.
 TF32B2 = True
 TF32B2_CONVERT = True
+# ... and on plain fp32 operands (no split pass at all: S_r / T_r^T as quadrant views or
+# one lincomb, B transposed once; the kernel forms both bf16 parts): cfg5 27.2-27.9 ms
+# vs 26.9-29.2 with the split pass (tools/cfg5_variants.py)
+TF32B2_RAW = True
 
 
 def _pair_batch(n: int, m: int, count: int) -> bool:
@@ -718,7 +784,10 @@ def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stre
     h = C.rows // 2
     if kid == nat.SR_F32_TC and FUSED_COMBINE and (C.ld * 4) % 16 == 0 and C.ptr % 16 == 0:
         launch_fill(nat.SR_F32, stream, C)
-        if FUSED_PRODUCER and _fused_producer_ok(C.rows, base) and A.ptr % 16 == 0 and (A.ld * 4) % 16 == 0:
+        aligned = A.ptr % 16 == 0 and (A.ld * 4) % 16 == 0
+        if TF32B2 and TF32B2_RAW and aligned and _b2raw_ok(C.rows, base):
+            _strassen_tc_fused_t(A, _transpose(B, stream), [(C, 1)], base, stream, leaf=_leaf_level_b2raw)
+        elif FUSED_PRODUCER and _fused_producer_ok(C.rows, base) and aligned:
             _strassen_tc_fused_t(A, _transpose(B, stream), [(C, 1)], base, stream)
         else:
             _strassen_tc_fused(A, B, [(C, 1)], base, stream)

@@ -257,8 +257,8 @@ def test_tf32b2_pair_kernel_accuracy(shape):
         assert float((C[i].double() - ref[i]).norm() / ref[i].norm()) < 1e-5, i
 
 
-@pytest.mark.parametrize("cv", [False, True])
-def test_strassen_tf32b2_vs_3xtf32(monkeypatch, cv):
+@pytest.mark.parametrize("cv,raw", [(False, False), (True, False), (True, True)])
+def test_strassen_tf32b2_vs_3xtf32(monkeypatch, cv, raw):
     """cfg5's shape at half size (8192, 2 levels): the tf32 + 2 x bf16 leaves vs the
     3xTF32 leaves -- both within 1e-4 of the f64 product, and the tf32b2 error no
     more than 1.5x the 3xTF32 one (Strassen's fp32 formation dominates both)."""
@@ -270,6 +270,7 @@ def test_strassen_tf32b2_vs_3xtf32(monkeypatch, cv):
     ref = a[rows].double() @ b.double()
     err = {}
     monkeypatch.setattr(S, "TF32B2_CONVERT", cv)
+    monkeypatch.setattr(S, "TF32B2_RAW", raw)
     for b2 in (True, False):
         monkeypatch.setattr(S, "TF32B2", b2)
         c = S.strassen_seq(a, b, n, base=base)

@@ -18,9 +18,9 @@ b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
 rows = torch.arange(0, n, n // 64, device="cuda")
 ref = a[rows].double() @ b.double()
 res = {}
-for name, b2, cv in (("3xtf32", False, True), ("tf32b2", True, False), ("tf32b2_cv", True, True),
-                     ("3xtf32_again", False, True)):
-    S.TF32B2, S.TF32B2_CONVERT = b2, cv
+for name, b2, cv, raw in (("3xtf32", False, True, False), ("tf32b2_cv", True, True, False),
+                          ("tf32b2_raw", True, True, True), ("3xtf32_again", False, True, False)):
+    S.TF32B2, S.TF32B2_CONVERT, S.TF32B2_RAW = b2, cv, raw
     for _ in range(2):
         c = S.strassen_seq(a, b, n, base=n // 4)
     torch.cuda.synchronize()
