@@ -169,6 +169,13 @@ int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out,
                  int64_t m, int nin, const void* const* ins, const int64_t* lds,
                  const int32_t* coefs, int accumulate);
 
+/* nout (<= 8) fp32 sums of the same nin (<= 4) n x m inputs in one pass:
+ * outs[o] = sum_i coefs[o * nin + i] * ins[i] (coefs in {-1, 0, +1}) -- Strassen's
+ * formation of a node (S1, S2, S5, S6, S7 from A's four quadrants) reads every
+ * input once.  16-byte aligned views, m % 4 == 0. */
+int paco_lincomb_multi(int device, void* stream, int64_t n, int64_t m, int nin, const void* const* ins,
+                       const int64_t* lds, int nout, void* const* outs, const int64_t* ldo, const int32_t* coefs);
+
 /* Strassen leaf operands for the 3xTF32 tensor-core MM, with the S/T sum
  * fused in (replaces a lincomb + split pair): x = sum_i
  * coef[i] * in[i] over rows x cols fp32 views (nin 1..4, coef +1/-1) is

@@ -65,6 +65,8 @@ SIGNATURES = {
     "paco_lincomb": (_int, [_int, _vp, _int, _vp, _i64, _i64, _i64, _int,
                             ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                             ctypes.POINTER(ctypes.c_int32), _int]),
+    "paco_lincomb_multi": (_int, [_int, _vp, _i64, _i64, _int, ctypes.POINTER(_vp), ctypes.POINTER(_i64), _int,
+                                  ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int32)]),
     "paco_mm_batch": (_int, [_int, _vp, _int, _int, ctypes.c_void_p]),
     "paco_tf32_split": (_int, [_int, _vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                                ctypes.POINTER(ctypes.c_int32), _i64, _i64, _int, _vp, _vp, _i64]),

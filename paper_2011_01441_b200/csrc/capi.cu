@@ -115,6 +115,8 @@ int launch_widen_u32_i64(cudaStream_t st, const void* r, int64_t ldr, int64_t* c
                          int64_t m);
 int launch_transpose(cudaStream_t st, int elsize, void* dst, int64_t ldd, const void* src, int64_t lds, int64_t rows,
                      int64_t cols);
+int launch_lincomb_multi(cudaStream_t st, int64_t n, int64_t m, int nin, const void* const* ins, const int64_t* lds,
+                         int nout, void* const* outs, const int64_t* ldo, const int32_t* coefs);
 int run_alu_probe(cudaStream_t st, int which, int iters, double* tpc, double* mhz);
 struct Box;
 }  // namespace paco
@@ -280,6 +282,19 @@ int paco_lincomb(int device, void* stream, int dtype, void* out, int64_t ld_out,
   PACO_TRY(dg.use(device));
   return launch_lincomb(dtype, static_cast<cudaStream_t>(stream), out, ld_out, n, m, nin, ins, lds,
                         coefs, accumulate);
+}
+
+int paco_lincomb_multi(int device, void* stream, int64_t n, int64_t m, int nin, const void* const* ins,
+                       const int64_t* lds, int nout, void* const* outs, const int64_t* ldo, const int32_t* coefs) {
+  if (!ins || !lds || (nout > 0 && (!outs || !ldo || !coefs))) {
+    set_error("paco_lincomb_multi: null arrays");
+    return PACO_ERR_ARG;
+  }
+  for (int q = 0; q < nin && q < 4; ++q) PACO_TRY(check_view("in", ins[q], lds[q], n, m));
+  for (int o = 0; o < nout && o < 8; ++o) PACO_TRY(check_view("out", outs[o], ldo[o], n, m));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_lincomb_multi(static_cast<cudaStream_t>(stream), n, m, nin, ins, lds, nout, outs, ldo, coefs);
 }
 
 int paco_mm_batch(int device, void* stream, int semiring, int count, const paco_mm_problem* problems) {

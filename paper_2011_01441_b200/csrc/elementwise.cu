@@ -229,6 +229,81 @@ int lincomb_t(cudaStream_t st, void* out, int64_t ldo, int64_t n, int64_t m, int
   return PACO_OK;
 }
 
+// Several signed sums of the same inputs in one pass (Strassen's formation of a
+// node: S1, S2, S5, S6, S7 from A's four quadrants): every input element is
+// read once and every output written once -- 4 reads + 5 writes per element
+// instead of 10 + 5 for five separate two-term lincombs.  coef[o * NIN + i] in
+// {-1, 0, +1}; fp32, 16-byte vectors (all views 16-byte aligned, m % 4 == 0).
+constexpr int kMultiIn = 4, kMultiOut = 8;
+struct MultiArgs {
+  const float* in[kMultiIn];
+  int64_t ldi[kMultiIn];
+  float* out[kMultiOut];
+  int64_t ldo[kMultiOut];
+  int8_t coef[kMultiOut * kMultiIn];
+  int32_t nin, nout;
+};
+
+__global__ void __launch_bounds__(128) lincomb_multi_kernel(const MultiArgs a, int64_t n, int64_t m) {
+  const int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (j >= m) return;
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
+    float4 x[kMultiIn];
+#pragma unroll
+    for (int q = 0; q < kMultiIn; ++q)
+      if (q < a.nin) x[q] = __ldcs(reinterpret_cast<const float4*>(a.in[q] + i * a.ldi[q] + j));
+#pragma unroll
+    for (int o = 0; o < kMultiOut; ++o) {
+      if (o >= a.nout) break;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < kMultiIn; ++q) {
+        if (q >= a.nin) break;
+        const int c = a.coef[o * kMultiIn + q];
+        if (c > 0) {
+          v.x += x[q].x; v.y += x[q].y; v.z += x[q].z; v.w += x[q].w;
+        } else if (c < 0) {
+          v.x -= x[q].x; v.y -= x[q].y; v.z -= x[q].z; v.w -= x[q].w;
+        }
+      }
+      __stcs(reinterpret_cast<float4*>(a.out[o] + i * a.ldo[o] + j), v);
+    }
+  }
+}
+
+int launch_lincomb_multi(cudaStream_t st, int64_t n, int64_t m, int nin, const void* const* ins, const int64_t* lds,
+                         int nout, void* const* outs, const int64_t* ldo, const int32_t* coefs) {
+  if (n <= 0 || m <= 0 || nout == 0) return PACO_OK;
+  if (nin < 1 || nin > kMultiIn || nout < 0 || nout > kMultiOut) {
+    set_error("paco_lincomb_multi: %d inputs (1..%d), %d outputs (0..%d)", nin, kMultiIn, nout, kMultiOut);
+    return PACO_ERR_ARG;
+  }
+  MultiArgs a{};
+  a.nin = nin;
+  a.nout = nout;
+  bool ok = m % 4 == 0;
+  for (int q = 0; q < nin; ++q) {
+    a.in[q] = static_cast<const float*>(ins[q]);
+    a.ldi[q] = lds[q];
+    ok = ok && lds[q] % 4 == 0 && reinterpret_cast<uintptr_t>(ins[q]) % 16 == 0;
+  }
+  for (int o = 0; o < nout; ++o) {
+    a.out[o] = static_cast<float*>(outs[o]);
+    a.ldo[o] = ldo[o];
+    ok = ok && ldo[o] % 4 == 0 && reinterpret_cast<uintptr_t>(outs[o]) % 16 == 0;
+    for (int q = 0; q < nin; ++q) a.coef[o * kMultiIn + q] = int8_t(coefs[o * nin + q] > 0 ? 1 : (coefs[o * nin + q] < 0 ? -1 : 0));
+  }
+  if (!ok) {
+    set_error("paco_lincomb_multi: views need 16-byte aligned starts, pitches and a column count % 4 == 0");
+    return PACO_ERR_UNSUPPORTED;
+  }
+  KernelSpan ks(PACO_KT_LINCOMB, st);
+  const int64_t xb = (m / 4 + 127) / 128, yb = n < 65535 ? n : 65535, ycap = 2368 / xb + 1;
+  lincomb_multi_kernel<<<dim3(unsigned(xb), unsigned(yb < ycap ? yb : ycap)), 128, 0, st>>>(a, n, m);
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
 int launch_lincomb(int dtype, cudaStream_t st, void* out, int64_t ldo, int64_t n, int64_t m, int nin,
                    const void* const* ins, const int64_t* lds, const int32_t* coefs, int acc) {
   if (nin < 0 || nin > 4) {

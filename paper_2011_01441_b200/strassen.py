@@ -587,6 +587,37 @@ def _leaf_level_fused(A: View, Bt: View, dests, stream) -> None:
                                               ndst, dst, sign, ld, h, h, h))
 
 
+def _form_all(src: View, table, transpose: bool, stream, keep: list, pitch: int | None = None) -> list:
+    """The seven S_r (table = S_TERMS, from A) or T_r^T (T_TERMS, from B^T with
+    transposed quadrant names) of a node: one-term formulas as quadrant views,
+    every multi-term one written by ONE ``paco_lincomb_multi`` pass over the four
+    quadrants (each read once).  New buffers get row pitch ``pitch`` (default h)."""
+    h = src.rows // 2
+    names = ("00", "01", "10", "11")
+    quads = [_quad(src, _tquad(q) if transpose else q) for q in names]
+    out, multi = [None] * 7, []
+    for r in range(1, 8):
+        terms = table[r]
+        if len(terms) == 1 and terms[0][0] == 1:
+            out[r - 1] = quads[names.index(terms[0][1])]
+            continue
+        buf = torch.empty((h, pitch or h), dtype=torch.float32, device=src.device)
+        keep.append(buf)
+        out[r - 1] = View.of(buf).sub(0, 0, h, h)
+        row = [0] * 4
+        for c, q in terms:
+            row[names.index(q)] = c
+        multi.append((out[r - 1], row))
+    if multi:
+        nat.check(nat.load().paco_lincomb_multi(
+            src.device, stream.cuda_stream, h, h, 4, (ctypes.c_void_p * 4)(*[v.ptr for v in quads]),
+            (ctypes.c_int64 * 4)(*[v.ld for v in quads]), len(multi),
+            (ctypes.c_void_p * len(multi))(*[v.ptr for v, _ in multi]),
+            (ctypes.c_int64 * len(multi))(*[v.ld for v, _ in multi]),
+            (ctypes.c_int32 * (4 * len(multi)))(*[c for _, row in multi for c in row])))
+    return out
+
+
 def _leaf_level_b2raw(A: View, Bt: View, dests, stream) -> None:
     """Leaf-level node, B given transposed, leaves in the tf32 + 2 x bf16 format
     with NO split pass: each S_r (from A's quadrants) and T_r^T (from B^T's) is
@@ -598,19 +629,10 @@ def _leaf_level_b2raw(A: View, Bt: View, dests, stream) -> None:
     h = A.rows // 2
     dev = A.device
     keep = []
-
-    def formed(src: View, terms, transpose: bool) -> View:
-        names = [(_tquad(q) if transpose else q) for _, q in terms]
-        if len(terms) == 1 and terms[0][0] == 1:
-            return _quad(src, names[0])
-        # the temporary takes the node's row pitch, so views and sums share one operand pitch
-        buf = torch.empty((h, src.ld), dtype=torch.float32, device=dev)
-        keep.append(buf)
-        out = View.of(buf).sub(0, 0, h, h)
-        _lincomb(nat.DT_F32, stream, out, [(c, _quad(src, nm)) for (c, _), nm in zip(terms, names)])
-        return out
-
-    ops = [(formed(A, S_TERMS[r], False), formed(Bt, T_TERMS[r], True)) for r in range(1, 8)]
+    # sums take the node's row pitch, so views and sums share one operand pitch
+    S_ = _form_all(A, S_TERMS, False, stream, keep, pitch=A.ld)
+    T_ = _form_all(Bt, T_TERMS, True, stream, keep, pitch=Bt.ld)
+    ops = list(zip(S_, T_))
     lda = {v.ld for v, _ in ops}
     ldb = {v.ld for _, v in ops}
     if len(lda) != 1 or len(ldb) != 1:
@@ -650,18 +672,11 @@ def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream, leaf=None)
         return
     h = n // 2
     dev = A.device
-
-    def formed(src: View, terms, transpose: bool) -> View:
-        names = [(_tquad(q) if transpose else q) for _, q in terms]
-        if len(terms) == 1 and terms[0][0] == 1:
-            return _quad(src, names[0])
-        out = View.of(torch.empty((h, h), dtype=torch.float32, device=dev))
-        _lincomb(nat.DT_F32, stream, out, [(c, _quad(src, nm)) for (c, _), nm in zip(terms, names)])
-        return out
-
+    keep = []
+    S_all = _form_all(A, S_TERMS, False, stream, keep)
+    T_all = _form_all(Bt, T_TERMS, True, stream, keep)
     for r in range(1, 8):
-        S = formed(A, S_TERMS[r], False)
-        Tt = formed(Bt, T_TERMS[r], True)
+        S, Tt = S_all[r - 1], T_all[r - 1]
         child = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
         fits = len(child) <= (2 if _leaf_level(h, base) else 1)
         if h > base and h % 2 == 0 and fits:
@@ -765,8 +780,8 @@ FUSED_A = False
 TF32B2 = True
 TF32B2_CONVERT = True
 # ... and on plain fp32 operands (no split pass at all: S_r / T_r^T as quadrant views or
-# one lincomb, B transposed once; the kernel forms both bf16 parts): cfg5 27.2-27.9 ms
-# vs 26.9-29.2 with the split pass (tools/cfg5_variants.py)
+# one lincomb_multi pass per node side, B transposed once; the kernel forms both bf16
+# parts): cfg5 23.8-25.4 ms vs 27.5-28.2 with the split pass (tools/cfg5_variants.py)
 TF32B2_RAW = True
 
 

@@ -277,3 +277,26 @@ def test_strassen_tf32b2_vs_3xtf32(monkeypatch, cv, raw):
         err[b2] = float((c[rows].double() - ref).norm() / ref.norm())
     assert err[True] < 1e-4 and err[False] < 1e-4, err
     assert err[True] <= 1.5 * err[False], err
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (257, 1028), (4096, 4096)])
+def test_lincomb_multi(shape):
+    """paco_lincomb_multi: several signed sums of the same inputs in one pass
+    (Strassen's S1, S2, S5, S6, S7 from four quadrants), exact vs torch."""
+    n, m = shape
+    lib = nat.load()
+    g = torch.Generator(device="cuda").manual_seed(n)
+    big = torch.randn(2 * n, 2 * m + 8, device="cuda", generator=g)   # quadrant views with a padded pitch
+    q = [big[:n, :m], big[:n, m:2 * m], big[n:, :m], big[n:, m:2 * m]]
+    rows = [[1, 0, 0, 1], [0, 0, 1, 1], [1, 1, 0, 0], [-1, 0, 1, 0], [0, 1, 0, -1]]
+    outs = [torch.full((n, m + 4), float("nan"), device="cuda")[:, :m] for _ in rows]
+    nat.check(lib.paco_lincomb_multi(0, torch.cuda.current_stream().cuda_stream, n, m, 4,
+                                     (ctypes.c_void_p * 4)(*[x.data_ptr() for x in q]),
+                                     (ctypes.c_int64 * 4)(*[x.stride(0) for x in q]), len(rows),
+                                     (ctypes.c_void_p * len(rows))(*[o.data_ptr() for o in outs]),
+                                     (ctypes.c_int64 * len(rows))(*[o.stride(0) for o in outs]),
+                                     (ctypes.c_int32 * 20)(*[c for r in rows for c in r])))
+    torch.cuda.synchronize()
+    for o, r in zip(outs, rows):
+        want = sum(c * x for c, x in zip(r, q) if c)
+        assert torch.equal(o, want)
