@@ -19,9 +19,9 @@ with ms, throughput, algorithmic ops/bytes, roofline fraction against a live
 or driver-measured peak, launches and a clocks sample of its own timed region.
 
 ``e2e``: the same metric through the reference-facing API
-``matmul.mm_seq(A, B, C, SEMIRING_MINPLUS_SAT)`` with pageable NumPy arrays
-(the reference's own calling convention): host staging, H2D of A, B, C and the
-D2H of C are inside the host-wall-clock timed region.  At N>1
+``matmul.mm_seq(A, B, C, SEMIRING_MINPLUS_SAT)`` with NumPy arrays (the
+reference's own calling convention; page-locked in place on first use): the
+H2D of A, B, C and the D2H of C are inside the host-wall-clock timed region.  At N>1
 ``FusedDistributedMM.run_host`` from pinned host tensors.
 
 ``--impl reference`` times the reference's CPU algorithm (the NumPy port in
@@ -409,7 +409,10 @@ def e2e_numpy_cfg2(dev, steps):
     B = rng.integers(0, 2**20, (n, n), dtype=np.int32)
     B[rng.random(B.shape) < 0.10] = INF
     C = np.full((n, n), INF, np.int32)
-    M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)  # warm (pinned staging buffers, streams)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)  # first call: page-locks A, B, C once (paco_host_register)
+    first_ms = (time.perf_counter() - t0) * 1e3
     times = []
     for _ in range(steps):
         C.fill(INF)
@@ -419,10 +422,11 @@ def e2e_numpy_cfg2(dev, steps):
         times.append((time.perf_counter() - t0) * 1e3)
     ms = statistics.median(times)
     return {"value": 2.0 * n ** 3 / (ms * 1e-3) / 1e9, "unit": "Gop/s", "ms_per_step": ms,
-            "ms_all": times, "h2d_bytes_per_step": 3 * n * n * 4, "d2h_bytes_per_step": n * n * 4,
-            "api": "paper_2011_01441_b200.matmul.mm_seq(A, B, C, SEMIRING_MINPLUS_SAT) with pageable NumPy int32 "
-                   "arrays (staged through pinned buffers by host threads, k-phased H2D/compute/D2H pipeline); "
-                   "host wall clock"}
+            "ms_all": times, "first_call_ms": first_ms, "h2d_bytes_per_step": 3 * n * n * 4,
+            "d2h_bytes_per_step": n * n * 4,
+            "api": "paper_2011_01441_b200.matmul.mm_seq(A, B, C, SEMIRING_MINPLUS_SAT) with NumPy int32 arrays: "
+                   "page-locked in place on first use (paco_host_register, first_call_ms), then every call DMAs A, "
+                   "B, C up and C back through the k-phased H2D/compute/D2H pipeline; host wall clock"}
 
 
 def e2e_pinned_cfg2(dev, st, A_h, B_h, steps):

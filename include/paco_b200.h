@@ -290,6 +290,12 @@ int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void*
 int paco_host_copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t rows,
                      int threads);
 
+/* Page-lock (and later release) a caller's host buffer so paco_copy2d can DMA
+ * straight from it: the NumPy operands of repeated mm_seq / mm_execute calls are
+ * registered once (first call) instead of staged every call. */
+int paco_host_register(void* ptr, size_t bytes);
+int paco_host_unregister(void* ptr);
+
 /* Device memory for buffers shared across processes (CUDA IPC) -- the only
  * allocation the library makes on a caller's behalf. */
 int paco_device_alloc(int device, size_t bytes, void** ptr);

@@ -95,6 +95,8 @@ SIGNATURES = {
                                                           ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
     "paco_transpose": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_copy2d": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
+    "paco_host_register": (_int, [_vp, ctypes.c_size_t]),
+    "paco_host_unregister": (_int, [_vp]),
     "paco_device_alloc": (_int, [_int, ctypes.c_size_t, ctypes.POINTER(_vp)]),
     "paco_device_free": (_int, [_int, _vp]),
     "paco_ipc_handle": (_int, [_int, _vp, _vp]),

@@ -551,6 +551,20 @@ int paco_copy2d(int device, void* stream, void* dst, int64_t dpitch, const void*
   return PACO_OK;
 }
 
+int paco_host_register(void* ptr, size_t bytes) {
+  if (!ptr || bytes == 0) {
+    set_error("paco_host_register: empty range");
+    return PACO_ERR_ARG;
+  }
+  PACO_CUDA_TRY(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+  return PACO_OK;
+}
+
+int paco_host_unregister(void* ptr) {
+  PACO_CUDA_TRY(cudaHostUnregister(ptr));
+  return PACO_OK;
+}
+
 int paco_device_alloc(int device, size_t bytes, void** ptr) {
   if (!ptr) {
     set_error("paco_device_alloc: null output");

@@ -241,6 +241,48 @@ def _host_copy(dst: np.ndarray, src: np.ndarray) -> None:
                                           cols * dst.itemsize, rows, _HOST_THREADS))
 
 
+# NumPy operands of the host pipeline are page-locked once and kept registered
+# while their buffer lives (weakref.finalize unregisters before it is freed), so a
+# caller that passes the same arrays again gets direct DMA instead of staging
+REGISTER_HOST = True
+_REGISTER_MIN_BYTES = 64 << 20
+_registered: dict = {}   # base buffer address -> byte size
+
+
+def _owner(x: np.ndarray) -> np.ndarray:
+    while isinstance(x.base, np.ndarray):
+        x = x.base
+    return x
+
+
+def _register_host(arrays) -> bool:
+    """Page-lock the buffers behind these NumPy arrays (cached); False if the
+    driver refuses (lock limits) -- the caller then stages through pinned copies."""
+    import weakref
+
+    if not REGISTER_HOST:
+        return False
+    lib = nat.load()
+    for x in arrays:
+        o = _owner(x)
+        if o.base is not None or not o.flags["C_CONTIGUOUS"] and not o.flags["F_CONTIGUOUS"]:
+            return False   # memory not owned by a NumPy array (e.g. a foreign buffer): do not pin it
+        ptr, size = o.ctypes.data, o.nbytes
+        if size < _REGISTER_MIN_BYTES:
+            return False
+        if _registered.get(ptr) == size:
+            continue
+        if lib.paco_host_register(ptr, size) != nat.OK:
+            return False
+        _registered[ptr] = size
+
+        def _release(p=ptr):
+            if _registered.pop(p, None) is not None:
+                nat.load().paco_host_unregister(p)
+        weakref.finalize(o, _release)
+    return True
+
+
 def _pinned_like(shape, dtype) -> torch.Tensor:
     """Pinned staging buffer (PyTorch's caching host allocator keeps it for the next call)."""
     return torch.empty(tuple(shape), dtype=torch_dtype(dtype), pin_memory=True)
@@ -365,6 +407,10 @@ def _kphased_host_mm(A, B, C, kid: int, dev: int, st, overwrite: bool, front_sha
     n, k = tuple(A.shape)
     m = B.shape[1]
     staged = isinstance(A, np.ndarray)
+    if staged and _register_host([A, B, C]):
+        # page-locked in place: DMA straight from the NumPy buffers, as for pinned tensors
+        A, B, C = torch.from_numpy(A), torch.from_numpy(B), torch.from_numpy(C)
+        staged = False
     if front_share is not None and front_share <= 0:
         edges, front = [0], 0
     else:

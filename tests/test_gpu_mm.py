@@ -588,3 +588,33 @@ def test_tensor_core_launches_in_cuda_graph(warm):
         st.synchronize()
     for _, _, c, ref in ops:
         assert float((c.double() - ref).norm() / ref.norm()) < 1e-5
+
+
+def test_numpy_operands_registered_once(monkeypatch):
+    """Large NumPy operands are page-locked on first use (paco_host_register) and
+    DMA'd in place by later calls; the registration is dropped when the array is
+    freed; results equal the staged path's and the oracle's."""
+    import gc
+
+    from paper_2011_01441_b200 import mm as MMmod
+    monkeypatch.setattr(MMmod, "_REGISTER_MIN_BYTES", 0)
+    rng = np.random.default_rng(44)
+    n, m, k = 1100, 650, 2600
+    A = tropical(rng, (n, k), 0, 2**20, 0.1)
+    B = tropical(rng, (k, m), 0, 2**20, 0.1)
+    C0 = tropical(rng, (n, m), 0, 2**21, 0.3)
+    want = cref.mm(cref.SR_MINPLUS_SAT32, A, B, C0.copy())
+    C = C0.copy()
+    before = len(MMmod._registered)
+    for _ in range(2):
+        C[...] = C0
+        M.mm_seq(A, B, C, M.SEMIRING_MINPLUS_SAT)
+        assert np.array_equal(C, want)
+    assert len(MMmod._registered) == before + 3
+    monkeypatch.setattr(MMmod, "REGISTER_HOST", False)   # the staged path gives the same C
+    C2 = C0.copy()
+    M.mm_seq(A, B, C2, M.SEMIRING_MINPLUS_SAT)
+    assert np.array_equal(C2, want)
+    del A, B, C
+    gc.collect()
+    assert len(MMmod._registered) == before + 0
