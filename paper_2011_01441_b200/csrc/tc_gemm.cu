@@ -868,6 +868,9 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
 // releases the accumulator with a remote arrive on the leader's barrier.
 // Tiles (256 x 256 of C) are dealt to pairs statically in row-band order.
 // ---------------------------------------------------------------------------
+#ifndef PACO_PAIR_CG
+#define PACO_PAIR_CG 2
+#endif
 template <int ST, bool FA = false, bool B2 = false, bool CV = false>
 struct PairLayout {
   static constexpr int BK = 16, BN = 256, BNH = 128, EC = 16, EW = 4, EB = 2;
@@ -877,7 +880,10 @@ struct PairLayout {
   // CV (with B2): bf16(hi) of both operands is formed in the kernel from the
   // tf32 hi tiles (fp32 SW64 -> bf16 SW32) by CW converter warps, so each operand
   // element costs 6 bytes of L2 traffic instead of 8
-  static constexpr int CW = (FA || CV) ? 4 : 0;
+  // CV: CG groups of 4 converter warps take alternate stages, so one group's
+  // per-stage latency (loads, fence, named barrier, signal) overlaps the next's
+  static constexpr int CG = CV ? PACO_PAIR_CG : 1;
+  static constexpr int CW = FA ? 4 : CV ? 4 * CG : 0;
   static constexpr int A_BYTES = BM * BK * 4;          // 8 KB: 128 rows x 16 fp32
   static constexpr int B_BYTES = BNH * BK * 4;         // 8 KB: this CTA's half of B^T
   static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
@@ -996,7 +1002,7 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* rfull = tempty + 2;  // FA: this CTA's raw A terms landed in stage s
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 16);
-  unsigned char* sig = reinterpret_cast<unsigned char*>(rfull + 18);  // FA: 2 x 16 B signal landing slots
+  unsigned char* sig = reinterpret_cast<unsigned char*>(rfull + 18);  // converter signal landing slots: 16 B per (group, rank)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
@@ -1145,8 +1151,9 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
       // ---------------- converter warps (CV, both CTAs): bf16(hi) tiles from the tf32 hi tiles ----------------
       // fp32 tile: row r at r*64, 16-byte chunk c (4 elements) at (c ^ ((r >> 1) & 3)) * 16 (SWIZZLE_64B);
       // bf16 tile: row r at r*32, 16-byte chunk c8 (8 elements) at (c8 ^ ((r >> 2) & 1)) * 16 (SWIZZLE_32B)
-      const int ct = (warp - 2 - L::EW) * 32 + lane;
-      constexpr int NTH = 32 * (L::CW > 0 ? L::CW : 1);
+      const int grp = (warp - 2 - L::EW) / 4;
+      const int ct = ((warp - 2 - L::EW) & 3) * 32 + lane;
+      constexpr int NTH = 128;
       constexpr int CH = (BM + L::BNH) * 4;  // fp32 16-byte chunks of the A and B^T hi tiles
       static_assert(CH % NTH == 0, "whole chunks per converter thread");
       const uint32_t full_leader0 = mapa_rank(smem_u32(&full[0]), 0);
@@ -1155,6 +1162,7 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
       uint32_t it = 0;
       for (int32_t t = pair; t < total; t += npairs) {
         for (int kb = 0; kb < args.kblocks; ++kb, ++it) {
+          if (int(it % L::CG) != grp) continue;
           const int s = it % ST;
           mbar_wait(&rfull[s], (it / ST) & 1);
           uint4 x[CH / NTH];
@@ -1192,11 +1200,11 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
             }
           }
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          asm volatile("bar.sync 1, %0;\n" ::"n"(NTH) : "memory");
+          asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(NTH) : "memory");
           if (ct == 0)
             asm volatile(
                 "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];\n" ::"r"(
-                    sig_leader + rank * 16u),
+                    sig_leader + uint32_t(grp * 2 + int(rank)) * 16u),
                 "r"(smem_u32(sig)), "r"(full_leader0 + uint32_t(s) * 8u)
                 : "memory");
         }
@@ -2045,7 +2053,9 @@ int run_pair(int device, cudaStream_t stream, const tc::TcMaps& maps, int count,
               : mode == 3 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true, true>
               : mode == 4 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true, true, true>
                           : tc::tc_pair_kernel<PACO_PAIR_ST, false, false>;
-  const int threads = (mode == 1 || mode >= 3) ? tc::PairLayout<PACO_PAIR_ST, true>::THREADS : L::THREADS;
+  const int threads = mode == 1   ? tc::PairLayout<PACO_PAIR_ST, true>::THREADS
+                      : mode >= 3 ? tc::PairLayout<PACO_PAIR_ST, false, true, true>::THREADS
+                                  : L::THREADS;
   {
     static std::atomic<uint64_t> attr_set{0};
     const uint64_t bit = uint64_t(1) << ((device & 15) * 4 + mode);
