@@ -655,7 +655,7 @@ class CudaStrassenOps:
 
     def strassen_into(self, a: torch.Tensor, b: torch.Tensor, dests, base: int) -> bool:
         """dests = [(sign, C block)] (+/-)= a x b with the combinations folded into
-        the 3xTF32 leaf epilogues (fp32 only); False: not applicable here."""
+        the leaf epilogues (fp32 only); False: not applicable here."""
         from .device import View
 
         if self.dtype != torch.float32:
@@ -694,7 +694,8 @@ class DistributedStrassen:
     A and B are replicated, so every rank forms the S/T operands of its own
     tree nodes locally (the path's S_r / T_r formulas applied level by level,
     shared prefixes formed once) and multiplies them (``strassen_seq`` of the
-    node, 3xTF32 leaves for fp32).  Each product is added, with the signs of
+    node; for fp32 the single-GPU leaves: tf32 + 2 x bf16 products on raw
+    operands when the node's leaf batch fills the CTA pairs, else 3xTF32).  Each product is added, with the signs of
     the C-block formulas composed along its path (``strassen_placements``),
     into a rank-local partial C; the pieces of split leftover leaves
     (``split_leftover``) are added the same way at their cuboid's final place

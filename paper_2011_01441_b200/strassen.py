@@ -750,6 +750,10 @@ def strassen_into(A: View, B: View, dests, base: int, stream) -> bool:
             return False
         _leaf_multi(A, B, dests, stream)
         return True
+    if TF32B2 and TF32B2_RAW and A.ptr % 16 == 0 and A.ld % 4 == 0 and _b2raw_ok(n, base):
+        # the default single-GPU leaves: plain fp32 operands, B transposed once
+        _strassen_tc_fused_t(A, _transpose(B, stream), dests, base, stream, leaf=_leaf_level_b2raw)
+        return True
     if _leaf_level(n, base) and len(dests) > 2:
         return False
     _strassen_tc_fused(A, B, dests, base, stream)

@@ -76,3 +76,53 @@ def test_distributed_strassen_gpu(world):
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     res = [q.get(timeout=5) for _ in cases]
     assert all(r[1] for r in res), res
+
+
+def _raw_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2011_01441_b200 import strassen as S
+    from paper_2011_01441_b200.distributed import CudaStrassenOps, DistributedStrassen
+    calls = []
+    leaf = S._leaf_level_b2raw
+
+    def counted(*a, **k):
+        calls.append(1)
+        return leaf(*a, **k)
+
+    S._leaf_level_b2raw = counted
+    try:
+        n, base = 8192, 2048
+        g = torch.Generator(device="cuda").manual_seed(7)
+        a = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+        b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+        plan = S.strassen_paco_partition(n, world, base=base)
+        ds = DistributedStrassen(plan, CudaStrassenOps(torch.float32))
+        C = ds.gather(ds.run(a, b))
+        n_calls = [None] * world
+        dist.all_gather_object(n_calls, len(calls))
+        if rank == 0:
+            rows = torch.arange(0, n, 97, device="cuda")
+            ref = a[rows].double() @ b.double()
+            err = float((C[rows].double() - ref).norm() / ref.norm())
+            q.put((err, n_calls))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_strassen_raw_leaves():
+    """Rank nodes big enough for the CTA-pair batch take the same raw-operand
+    tf32 + 2 x bf16 leaves as the single-GPU path (strassen.strassen_into)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_raw_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    err, n_calls = q.get(timeout=5)
+    assert err <= 1e-4, err
+    assert all(c >= 1 for c in n_calls), n_calls
