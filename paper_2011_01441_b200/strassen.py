@@ -550,6 +550,7 @@ def _transpose(src: View, stream) -> View:
     out = View.of(torch.empty((src.cols, src.rows), dtype=torch.float32, device=src.device))
     nat.check(nat.load().paco_transpose(src.device, stream.cuda_stream, 4, out.ptr, out.ld, src.ptr, src.ld, src.rows,
                                         src.cols))
+    out.tensor.record_stream(stream)
     return out
 
 
@@ -710,10 +711,22 @@ def _fused_producer_ok(n: int, base: int) -> bool:
 
 
 def _leaf_multi(A: View, B: View, dests, stream) -> None:
-    """One 3xTF32 leaf product folded (+/-) into <= 4 blocks (count-1 batch)."""
+    """One leaf product folded (+/-) into <= 4 blocks (count-1 batch): on CTA
+    pairs in the raw-operand tf32 + 2 x bf16 format when it fills them (B
+    transposed once), else 3xTF32 from split operands."""
     n, k = A.rows, A.cols
     m = B.cols
     dev = A.device
+    if (TF32B2 and TF32B2_RAW and _pair_batch(n, m, 1) and A.ptr % 16 == 0 and A.ld % 4 == 0 and k % 4 == 0
+            and all(d.ld == dests[0][0].ld for d, _ in dests)):
+        Bt = _transpose(B, stream)
+        one_v = lambda v: (ctypes.c_void_p * 1)(v.ptr)  # noqa: E731
+        ndst = (ctypes.c_int32 * 1)(len(dests))
+        dst = (ctypes.c_void_p * 4)(*[d.ptr for d, _ in dests])
+        sign = (ctypes.c_int32 * 4)(*[sg for _, sg in dests])
+        nat.check(nat.load().paco_mm_tf32b2_multi(dev, stream.cuda_stream, 1, one_v(A), None, None, A.ld, one_v(Bt),
+                                                  None, None, Bt.ld, ndst, dst, sign, dests[0][0].ld, n, m, k))
+        return
     kp = (k + 3) // 4 * 4
     ah = torch.empty((n, kp), dtype=torch.float32, device=dev)
     al = torch.empty_like(ah)

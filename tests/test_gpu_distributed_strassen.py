@@ -126,3 +126,24 @@ def test_distributed_strassen_raw_leaves():
     err, n_calls = q.get(timeout=5)
     assert err <= 1e-4, err
     assert all(c >= 1 for c in n_calls), n_calls
+
+
+def test_strassen_into_leaf_raw_pair():
+    """A rank's leaf-sized node (n <= base) with signed placements: one CTA-pair
+    product on raw fp32 operands folded +/- into two C blocks."""
+    from paper_2011_01441_b200 import strassen as S
+    from paper_2011_01441_b200.device import View
+    n = 4096
+    g = torch.Generator(device="cuda").manual_seed(11)
+    a = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+    b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+    C = torch.rand(n, 2 * n, device="cuda", generator=g)
+    C0 = C.clone()
+    st = torch.cuda.current_stream()
+    assert S.strassen_into(View.of(a), View.of(b), [(View.of(C[:, :n]), 1), (View.of(C[:, n:]), -1)], n, st)
+    rows = torch.arange(0, n, 61, device="cuda")
+    ref = a[rows].double() @ b.double()
+    for half, sg in ((0, 1), (1, -1)):
+        got = C[rows, half * n:(half + 1) * n].double() - C0[rows, half * n:(half + 1) * n].double()
+        err = float((got - sg * ref).norm() / ref.norm())
+        assert err <= 1e-4, (half, err)
