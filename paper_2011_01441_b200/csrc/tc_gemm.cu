@@ -37,6 +37,9 @@
 
 #include "common.cuh"
 
+#ifndef PACO_EXIT_WAIT_READ
+#define PACO_EXIT_WAIT_READ 1
+#endif
 namespace paco {
 
 #ifndef PACO_RES_AST
@@ -398,7 +401,10 @@ struct TcProb {
   CUtensorMap a2, b2;    // tf32 + 2 x bf16 format: a[0] = hi (fp32), a[1] = bf16(hi), a2 = bf16(x - hi)
   int32_t a2_col0, b2_col0;
 };
-constexpr int kMaxBatch = 8;
+#ifndef PACO_TC_MAXBATCH
+#define PACO_TC_MAXBATCH 8
+#endif
+constexpr int kMaxBatch = PACO_TC_MAXBATCH;
 struct TcMaps {
   TcProb p[kMaxBatch];
 };
@@ -831,7 +837,14 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
       }
       if (ew == 0 && lane == 0 && i < 15) tc_stamp(args, i, 5);
     }
+#if PACO_EXIT_WAIT_READ
+    // exit once the last boxes have been READ out of shared memory: the global
+    // writes still complete before the grid does (a dependent launch's
+    // griddepcontrol.wait sees them), and the next CTA can take this SM meanwhile
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+#else
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+#endif
   }
 
   tc_fence_before();
@@ -1345,7 +1358,14 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
         }
       }
     }
+#if PACO_EXIT_WAIT_READ
+    // exit once the last boxes have been READ out of shared memory: the global
+    // writes still complete before the grid does (a dependent launch's
+    // griddepcontrol.wait sees them), and the next CTA can take this SM meanwhile
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+#else
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+#endif
   }
 
   tc_fence_before();
