@@ -936,7 +936,9 @@ int repack16(SimtScratch& sc, cudaStream_t st, const void** p, int64_t* ld, int6
     int dev = 0;
     PACO_CUDA_TRY(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(mu);
-    if (!ready[dev & 63]) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    PACO_CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+    if (!ready[dev & 63] && cs == cudaStreamCaptureStatusNone) {  // no pool changes inside a capture
       cudaMemPool_t pool;
       PACO_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
       uint64_t keep = UINT64_MAX;

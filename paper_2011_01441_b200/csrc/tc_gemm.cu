@@ -1471,7 +1471,11 @@ int scratch(int device, Scratch& sc, size_t bytes, cudaStream_t st, void** out) 
   static bool pool_ready[64] = {};
   {
     std::lock_guard<std::mutex> lock(mu);
-    if (!pool_ready[device & 63]) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    PACO_CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+    // pool attributes may not change while a stream captures (a CUDA graph's
+    // first launch through the library): set them at the next uncaptured call
+    if (!pool_ready[device & 63] && cs == cudaStreamCaptureStatusNone) {
       cudaMemPool_t pool;
       PACO_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
       uint64_t keep = UINT64_MAX;
