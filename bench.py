@@ -303,7 +303,7 @@ def measure_config(cfg, dev, args, peaks, probes):
         peak = 2 * tpc * SM_COUNT * 1965.0 / 1e6
         achieved = ops / ms / 1e9
         clocks = clk.summary()
-        traffic, src = ncu_traffic("r1_minplus_ncu.json") if cfg == 2 else (None, None)
+        traffic, src = ncu_traffic("r2_minplus_ncu.json" if cfg == 2 else "r2_maxplus_ncu.json")
         ks, ctas = nat.cta_grid(kid, n, n, n)
         out.update(ms=ms, value=ops / ms / 1e6, unit="Gop/s", ops_per_step=ops, steps=steps, warmup=warmup,
                    algorithmic_bytes=3 * n * n * 4, gpu_launches_per_step=1,
@@ -360,7 +360,7 @@ def measure_config(cfg, dev, args, peaks, probes):
         byts = 2 * n * k + 2 * k * m + 4 * n * m
         flop = 2.0 * n * m * k
         achieved = byts / ms / 1e6
-        traffic, src = ncu_traffic("r1_bf16_ncu.json")
+        traffic, src = ncu_traffic("r2_bf16_ncu.json")
         out.update(ms=ms, value=flop / ms / 1e6, unit="Gop/s", ops_per_step=flop, steps=steps, warmup=warmup,
                    algorithmic_bytes=byts, gpu_launches_per_step=1,
                    ms_direct=ms_direct, ms_l2_flushed=statistics.median(cold),
@@ -407,7 +407,7 @@ def measure_config(cfg, dev, args, peaks, probes):
         leaf_launch_ms = leaf_ms / max(1, per_step["tc_gemm"]["launches"])
         leaf_flop = mma / max(1, per_step["tc_gemm"]["launches"])   # one launch = 7 products of 4096^3
         achieved = leaf_flop / leaf_launch_ms / 1e9
-        traffic, src = ncu_traffic("r2_tf32x3_pair_ncu.json")
+        traffic, src = ncu_traffic("r2_tf32b2_raw_ncu.json")
         fmt = ("tf32 + 2 x bf16 split products (hi*hi on kind::tf32, hi*lo + lo*hi on kind::f16, bf16(hi) formed "
                "in the kernel), fp32 accumulation" if b2 else "3xTF32 split products, fp32 accumulation")
         out.update(ms=ms, value=alg / ms / 1e6, unit="Gop/s", ops_per_step=alg, steps=steps, warmup=warmup,
