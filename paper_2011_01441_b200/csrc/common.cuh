@@ -2,6 +2,7 @@
 #pragma once
 #include <atomic>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/paco_b200.h"
@@ -38,6 +39,10 @@ void set_error(const char* fmt, ...);
 // the environment ONLY when PACO_DEV_KNOBS=1, so an ordinary user environment
 // can never select an unmeasured configuration.  nullptr when unset or gated.
 const char* dev_knob(const char* name);
+// 2-D row-major tensor map of 4- or 8-byte elements (no swizzle, zero OOB fill)
+// over a 16-byte aligned base with a 16-byte row pitch (tc_gemm.cu)
+int encode_map_2d(CUtensorMap* map, int elsize, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                  uint32_t box_cols, uint32_t box_rows);
 
 // Live per-kernel timing (paco_kernel_timing): while on, every launch site
 // brackets its kernel with a CUDA event pair on the launching stream, so a

@@ -87,6 +87,12 @@ struct SimtCfg {
   static constexpr int B_PASSES = BK / B_RPP;
   static constexpr size_t SMEM =
       size_t(STAGES) * (A_STAGE * sizeof(typename Op::TA) + B_STAGE * sizeof(typename Op::TB));
+  // TMA stage loads (32-bit operands): A as one [BM rows][LDA_S k] box -- the box's
+  // inner extent IS the padded smem row, so the bank-conflict-free layout comes for
+  // free (the 4 extra k per row are read and ignored) -- and B as one [BK][BN] box
+  static constexpr bool kTmaOk = !kWide && sizeof(typename Op::TA) == 4 && sizeof(typename Op::TB) == 4 &&
+                                 LDA_S * 4 % 16 == 0 && BN <= 256;
+  static constexpr uint32_t TMA_BYTES = uint32_t(BM * LDA_S * 4 + BK * BN * 4);
   static_assert(A_RPP * A_CPR == THREADS && A_PASSES * A_RPP == BM, "A load mapping");
   static_assert(B_RPP * B_CPR == THREADS && B_PASSES * B_RPP == BK, "B load mapping");
 };
@@ -468,6 +474,29 @@ __device__ __forceinline__ void epilogue_bulk_wide(const MMArgs& a,
   }
 }
 
+// Operand tensor maps of a TMA-loaded launch (simt_mm_kernel<Op, true, true>).
+struct SimtMaps {
+  CUtensorMap a, b;
+};
+
+__device__ __forceinline__ void tma_load_2d_cta(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_cta(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// CTA-scope acq_rel counter bump (the slot-release vote of the TMA ring)
+__device__ __forceinline__ uint32_t smem_add_acq_rel(uint32_t* p) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;\n" : "=r"(old) : "r"(smem_u32(p)) : "memory");
+  return old;
+}
+
 // (ti, tj, kt) walk of one piece: k fastest, then C tile columns, then rows.
 struct TileWalk {
   int ti, tj, kt;
@@ -483,8 +512,8 @@ struct TileWalk {
 };
 
 // One CTA's piece of one problem: the whole pipeline (ring, MACs, epilogue).
-template <class Op, bool kVec>
-__device__ __forceinline__ void simt_mm_body(const MMArgs& args, const Piece pc) {
+template <class Op, bool kVec, bool kTma = false>
+__device__ __forceinline__ void simt_mm_body(const MMArgs& args, const Piece pc, const SimtMaps* maps = nullptr) {
   using C = SimtCfg<Op>;
   using TA = typename Op::TA;
   using TB = typename Op::TB;
@@ -508,7 +537,64 @@ __device__ __forceinline__ void simt_mm_body(const MMArgs& args, const Piece pc)
     for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::identity();
   TileWalk cw{0, 0, 0};
 
-  if constexpr (kMbarPipe) {
+  if constexpr (kTma) {
+    // TMA ring: stage j of the piece's (tile, k tile) walk lands in slot j % STAGES
+    // by two tensor copies completing on full[slot].  No thread issues per-element
+    // copies or waits for a free slot: each warp votes on freed[slot] after reading
+    // it (and after an epilogue staged in it), and the warp casting the slot's
+    // last vote refills it with stage j + STAGES -- so a slow warp delays only the
+    // refill of the slot it still reads, never another warp's arithmetic.
+    static_assert(C::kTmaOk, "TMA stage layout");
+    constexpr int NWARPS = C::THREADS / 32;
+    static_assert((NWARPS & (NWARPS - 1)) == 0, "vote modulus");
+    __shared__ uint64_t full[C::STAGES];
+    __shared__ uint32_t freed[C::STAGES];
+    const int lane = threadIdx.x % 32;
+    auto issue = [&](int j, int slot) {
+      const int kt = j % KT, t = j / KT;
+      const int tj = t % pc.tm, ti = t / pc.tm;
+      const int row0 = (pc.ti0 + ti) * C::BM, col0 = (pc.tj0 + tj) * C::BN;
+      const int k0 = int(kb) + kt * C::BK;
+      mbar_arrive_expect_tx_cta(&full[slot], C::TMA_BYTES);
+      tma_load_2d_cta(As + slot * C::A_STAGE, &maps->a, &full[slot], k0, row0);
+      tma_load_2d_cta(Bs + slot * C::B_STAGE, &maps->b, &full[slot], col0, k0);
+    };
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < C::STAGES; ++s) {
+        mbar_init_cta(&full[s], 1);
+        freed[s] = 0;
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      for (int s = 0; s < C::STAGES && s < total; ++s) issue(s, s);
+    }
+    __syncthreads();
+    for (int it = 0; it < total; ++it) {
+      const int s = it % C::STAGES;
+      mbar_wait_cta(&full[s], uint32_t(it / C::STAGES) & 1);
+      const int64_t k0 = kb + int64_t(cw.kt) * C::BK;
+      const int kvalid = (kend - k0 < C::BK) ? int(kend - k0) : C::BK;
+      compute_stage<Op>(acc, As + s * C::A_STAGE, Bs + s * C::B_STAGE, kvalid);
+      if (cw.kt == KT - 1) {
+        const int64_t row0 = int64_t(pc.ti0 + cw.ti) * C::BM, col0 = int64_t(pc.tj0 + cw.tj) * C::BN;
+        const int64_t cols = (args.m - col0 < C::BN) ? args.m - col0 : C::BN;
+        const uint32_t bytes = uint32_t(cols * sizeof(typename Op::TC));
+        if (args.bulk_ok && (bytes % 16) == 0)  // stages the tile in slot s (CTA-wide syncs)
+          epilogue_bulk<Op>(args, acc, row0, col0, As + s * C::A_STAGE, Bs + s * C::B_STAGE, bytes);
+        else
+          epilogue<Op>(args, acc, row0, col0, atomic);
+#pragma unroll
+        for (int i = 0; i < C::TM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::TN; ++j) acc[i][j] = Op::identity();
+      }
+      cw.next(pc.tm, KT);
+      if (it + C::STAGES < total) {
+        __syncwarp();
+        if (lane == 0 && (smem_add_acq_rel(&freed[s]) & (NWARPS - 1)) == NWARPS - 1) issue(it + C::STAGES, s);
+      }
+    }
+  } else if constexpr (kMbarPipe) {
     // Split arrive/wait ring: full[s] completes when every thread's cp.async
     // into stage s has landed (cp.async.mbarrier.arrive.noinc); empty[s]
     // when every thread has finished reading it.  A stage is refilled one
@@ -653,9 +739,10 @@ __device__ __forceinline__ void simt_mm_body(const MMArgs& args, const Piece pc)
   }
 }
 
-template <class Op, bool kVec>
+template <class Op, bool kVec, bool kTma = false>
 __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
-    simt_mm_kernel(const MMArgs args, const __grid_constant__ PieceTable table) {
+    simt_mm_kernel(const MMArgs args, const __grid_constant__ PieceTable table,
+                   const __grid_constant__ SimtMaps maps) {
   using C = SimtCfg<Op>;
   Piece pc;
   if (table.count > 0) {
@@ -670,7 +757,7 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
     pc = Piece{int32_t(b.o[0]), int32_t(b.o[1]), int32_t(b.o[2]), int32_t(b.e[0]), int32_t(b.e[1]),
                int32_t(b.e[2])};
   }
-  simt_mm_body<Op, kVec>(args, pc);
+  simt_mm_body<Op, kVec, kTma>(args, pc, &maps);
 }
 
 // A batch of independent problems (e.g. every COMPUTE cuboid of a GPU-level
@@ -992,11 +1079,26 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
   }
   const bool vec = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
                    ((lda * sizeof(typename Op::TA)) % 16 == 0) && ((ldb * sizeof(typename Op::TB)) % 16 == 0);
-  auto kern = vec ? simt_mm_kernel<Op, true> : simt_mm_kernel<Op, false>;
+  static SimtMaps maps;
+  bool tma = false;
+  if constexpr (Cfg::kTmaOk) {
+    // TMA stage loads for aligned operands whose coordinates fit the tensor-map
+    // int32 range (PACO_SIMT_TMA=0: per-thread cp.async ring)
+    static const bool on = !dev_knob("PACO_SIMT_TMA") || atoi(dev_knob("PACO_SIMT_TMA")) != 0;
+    tma = on && vec && n < INT32_MAX && m < INT32_MAX && k < INT32_MAX - 64;
+    if (tma) {
+      rc = encode_map_2d(&maps.a, 4, A, n, k, lda, Cfg::LDA_S, Cfg::BM);
+      if (!rc) rc = encode_map_2d(&maps.b, 4, B, k, m, ldb, Cfg::BN, Cfg::BK);
+      if (rc) return rc;
+    }
+  }
+  auto kern = tma   ? simt_mm_kernel<Op, true, Cfg::kTmaOk>
+              : vec ? simt_mm_kernel<Op, true>
+                    : simt_mm_kernel<Op, false>;
   PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
   {
     KernelSpan ks(PACO_KT_SIMT_MM, stream);
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM, stream>>>(args, table);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, stream>>>(args, table, maps);
   }
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;

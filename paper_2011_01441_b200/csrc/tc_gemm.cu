@@ -1425,6 +1425,20 @@ int make_map(CUtensorMap* map, CUtensorMapDataType dt, int elsize, const void* p
   return PACO_OK;
 }
 
+}  // namespace
+
+int encode_map_2d(CUtensorMap* map, int elsize, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                  uint32_t box_cols, uint32_t box_rows) {
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0) {
+    set_error("internal: tensor map base must be 16-byte aligned");
+    return PACO_ERR_UNSUPPORTED;
+  }
+  int32_t off = 0;
+  return make_map(map, elsize == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, elsize, ptr,
+                  rows, cols, ld, box_cols, box_rows, &off, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+namespace {
 // Scratch for split / repacked operands: stream-ordered allocations from the
 // device's default memory pool (kept cached: release threshold = max), freed
 // on the launch stream after the kernel.  Concurrent launches on different
