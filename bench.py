@@ -303,7 +303,7 @@ def measure_config(cfg, dev, args, peaks, probes):
         peak = 2 * tpc * SM_COUNT * 1965.0 / 1e6
         achieved = ops / ms / 1e9
         clocks = clk.summary()
-        traffic, src = ncu_traffic("r2_minplus_ncu.json" if cfg == 2 else "r2_maxplus_ncu.json")
+        traffic, src = ncu_traffic("r2_minplus_tma_ncu.json" if cfg == 2 else "r2_maxplus_tma_ncu.json")
         ks, ctas = nat.cta_grid(kid, n, n, n)
         out.update(ms=ms, value=ops / ms / 1e6, unit="Gop/s", ops_per_step=ops, steps=steps, warmup=warmup,
                    algorithmic_bytes=3 * n * n * 4, gpu_launches_per_step=1,
