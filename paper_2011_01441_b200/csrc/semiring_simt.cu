@@ -51,6 +51,9 @@ constexpr double kVisitK = 64.0;  // per-visit cost in k elements (re-fitted wit
 // non-null every CTA of the next launches records smid and start/end times.
 long long* g_trace_buffer = nullptr;
 
+#ifndef PACO_SIMT_BK
+#define PACO_SIMT_BK 32  // 32-bit ops: k depth of a ring stage (16: six stages of the same total size)
+#endif
 #ifndef PACO_SIMT_NSPAN
 #define PACO_SIMT_NSPAN 1  // 32-bit ops: C tile width in units of 128 columns (2 = 128x256 tiles,
                            // 1 CTA/SM: measured 34.7 vs 34.4 ms on 8192^3 min-plus -- kept at 1)
@@ -64,13 +67,13 @@ struct SimtCfg {
   // rate (smem-bound: 2 loaded values per term pair)
   static constexpr int BM = kWide ? PACO_SIMT_WIDE_TILE : 128;
   static constexpr int BN = kWide ? PACO_SIMT_WIDE_TILE : 128 * PACO_SIMT_NSPAN;
-  static constexpr int BK = kWide ? 16 : 32;
+  static constexpr int BK = kWide ? 16 : PACO_SIMT_BK;
   static constexpr int GM = BM / 64;  // 4-row groups per thread along m
   static constexpr int GN = BN / 64;
   static constexpr int TM = 4 * GM;
   static constexpr int TN = 4 * GN;
   static constexpr int THREADS = 256;
-  static constexpr int STAGES = kWide ? 4 : (PACO_SIMT_NSPAN > 1 ? 4 : 3);
+  static constexpr int STAGES = kWide ? 4 : (PACO_SIMT_NSPAN > 1 ? 4 : (PACO_SIMT_BK == 16 ? 6 : 3));
   static constexpr int MIN_BLOCKS = (!kWide && PACO_SIMT_NSPAN > 1) || (kWide && BM > 64) ? 1 : 2;
   static constexpr int VA = 16 / sizeof(typename Op::TA);  // elements per 16 B chunk
   static constexpr int VB = 16 / sizeof(typename Op::TB);
@@ -344,15 +347,17 @@ __device__ __forceinline__ void epilogue_bulk(const MMArgs& a,
   using C = SimtCfg<Op>;
   using TC = typename Op::TC;
   static_assert(C::BM == 128 && sizeof(TC) == 4, "bulk epilogue layout");
-  // rows per round: the B stage buffer holds BK = 32 rows of the C tile; the
-  // padded A buffer adds 32 more when the tile is 128 wide
-  constexpr int RPR = (C::A_STAGE >= 32 * C::BN) ? 64 : 32;
+  // rows per round: the B stage buffer holds BK rows of the C tile, the padded
+  // A buffer A_STAGE / BN more
+  constexpr int ROOM = C::BK + C::A_STAGE / C::BN;
+  static_assert(ROOM >= 32, "bulk epilogue staging room");
+  constexpr int RPR = ROOM >= 64 ? 64 : 32;
   constexpr int ROUNDS = C::BM / RPR;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   TC* Cp = static_cast<TC*>(a.C);
   auto row_buf = [&](int lr) -> TC* {
-    return lr < 32 ? static_cast<TC*>(bufB) + lr * C::BN : static_cast<TC*>(bufA) + (lr - 32) * C::BN;
+    return lr < C::BK ? static_cast<TC*>(bufB) + lr * C::BN : static_cast<TC*>(bufA) + (lr - C::BK) * C::BN;
   };
   __syncthreads();  // every warp is done reading the stage buffer
 #pragma unroll
