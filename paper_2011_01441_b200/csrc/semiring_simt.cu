@@ -765,6 +765,180 @@ __global__ void __launch_bounds__(SimtCfg<Op>::THREADS, SimtCfg<Op>::MIN_BLOCKS)
   simt_mm_body<Op, kVec, kTma>(args, pc, &maps);
 }
 
+// ---------------------------------------------------------------------------
+// f64 (+,x) -- the reference's SEMIRING_F64 -- on the FP64 tensor pipe: warp-level
+// DMMA (mma.sync m8n8k4 f64).  The SIMT DFMA kernel is shared-memory bound (one
+// LDS.128 per 8 DFMAs per thread: 0.65 of the DFMA rate); a DMMA reuses each
+// loaded A element across 8 columns and each B element across 8 rows inside the
+// tensor unit, so operand traffic falls 4x and the FP64 pipe sets the pace
+// (tools/microbench/dmma_probe.cu: 37.2 TFLOP/s DMMA vs 33.7 DFMA).
+// Same CTA plan (128 x 128 tiles, pieces, k splits) and C semantics as the SIMT
+// kernel; TMA stage ring with the last-vote refill; fragments stored straight
+// from registers (atomic adds for k-split pieces).
+// ---------------------------------------------------------------------------
+#ifndef PACO_DMMA_WN
+#define PACO_DMMA_WN 4  // warps along n (x 4 along m): 4 -> 32 x 32 warp tiles, 16 warps (2 -> 32 x 64, 8 warps: 31.4 vs 33.8 TFLOP/s at 4096^3)
+#endif
+struct DmmaCfg {
+  static constexpr int WM = 4, WN = PACO_DMMA_WN, NW = WM * WN;
+  static constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 32 * NW;
+  static constexpr int MI = BM / WM / 8, NJ = BN / WN / 8;  // 8 x 8 fragments per warp along m, n
+  // padded rows: A k-rows of 20 doubles (160 B), B n-rows of 136 doubles (1088 B) --
+  // both fragment loads then take the minimum two wavefronts.  The TMA boxes are
+  // [BM][20] and [BK][136]: a box's inner extent is the padded row.
+  static constexpr int LDA_S = BK + 4, LDB_S = BN + 8;
+  static constexpr int A_STAGE = BM * LDA_S, B_STAGE = BK * LDB_S;  // doubles
+  static constexpr uint32_t TMA_BYTES = uint32_t((A_STAGE + B_STAGE) * 8);
+  static constexpr size_t SMEM = size_t(STAGES) * TMA_BYTES;
+  static_assert(BM == SimtCfg<OpF64>::BM && BN == SimtCfg<OpF64>::BN, "same CTA plan as the SIMT f64 kernel");
+};
+
+__device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
+    dmma_f64_kernel(const MMArgs args, const __grid_constant__ PieceTable table, const __grid_constant__ SimtMaps maps) {
+  using D = DmmaCfg;
+  using S = SimtCfg<OpF64>;
+  Piece pc;
+  if (table.count > 0) {
+    pc = table.p[blockIdx.x];
+  } else {
+    UnitBox b;
+    if (table.grid_s > 0)
+      plan_grid_piece(args.n, args.m, args.k, S::BM, S::BN, S::KQ, table.grid_s, int(blockIdx.x), b,
+                      table.grid_tail, table.grid_head);
+    else
+      plan_piece(args.n, args.m, args.k, S::BM, S::BN, S::KQ, int(gridDim.x), int(blockIdx.x), b, args.kw);
+    pc = Piece{int32_t(b.o[0]), int32_t(b.o[1]), int32_t(b.o[2]), int32_t(b.e[0]), int32_t(b.e[1]),
+               int32_t(b.e[2])};
+  }
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* As = reinterpret_cast<double*>(smem_raw);
+  double* Bs = As + D::STAGES * D::A_STAGE;
+  __shared__ uint64_t full[D::STAGES];
+  __shared__ uint32_t freed[D::STAGES];
+
+  const int64_t kb = int64_t(pc.tl0) * args.kq;
+  const int64_t kend = min(args.k, kb + int64_t(pc.tk) * args.kq);
+  const bool atomic = args.all_atomic || !(kb == 0 && kend == args.k);
+  const int KT = int((kend - kb + D::BK - 1) / D::BK);
+  const int total = pc.tn * pc.tm * KT;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int wm = warp % D::WM, wn = warp / D::WM;  // warp tile: rows 8 MI wm .., columns 8 NJ wn ..
+  const int lr = lane / 4, lc = lane % 4;  // fragment row / column group
+
+  auto issue = [&](int j, int slot) {
+    const int kt = j % KT, t = j / KT;
+    const int tj = t % pc.tm, ti = t / pc.tm;
+    const int k0 = int(kb) + kt * D::BK;
+    mbar_arrive_expect_tx_cta(&full[slot], D::TMA_BYTES);
+    tma_load_2d_cta(As + slot * D::A_STAGE, &maps.a, &full[slot], k0, (pc.ti0 + ti) * D::BM);
+    tma_load_2d_cta(Bs + slot * D::B_STAGE, &maps.b, &full[slot], (pc.tj0 + tj) * D::BN, k0);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < D::STAGES; ++s) {
+      mbar_init_cta(&full[s], 1);
+      freed[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    for (int s = 0; s < D::STAGES && s < total; ++s) issue(s, s);
+  }
+  __syncthreads();
+
+  double acc[D::MI][D::NJ][2];
+#pragma unroll
+  for (int i = 0; i < D::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < D::NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  TileWalk cw{0, 0, 0};
+  for (int it = 0; it < total; ++it) {
+    const int s = it % D::STAGES;
+    mbar_wait_cta(&full[s], uint32_t(it / D::STAGES) & 1);
+    const double* a_s = As + s * D::A_STAGE + (wm * 8 * D::MI + lr) * D::LDA_S + lc;
+    const double* b_s = Bs + s * D::B_STAGE + lc * D::LDB_S + wn * 8 * D::NJ + lr;
+    const int64_t k0 = kb + int64_t(cw.kt) * D::BK;
+    const int kvalid = (kend - k0 < D::BK) ? int(kend - k0) : D::BK;
+    if (kvalid == D::BK) {
+#pragma unroll
+      for (int ks = 0; ks < D::BK / 4; ++ks) {
+        double a[D::MI], b[D::NJ];
+#pragma unroll
+        for (int i = 0; i < D::MI; ++i) a[i] = a_s[i * 8 * D::LDA_S + ks * 4];
+#pragma unroll
+        for (int j = 0; j < D::NJ; ++j) b[j] = b_s[ks * 4 * D::LDB_S + j * 8];
+#pragma unroll
+        for (int i = 0; i < D::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < D::NJ; ++j) dmma_m8n8k4(acc[i][j], a[i], b[j]);
+      }
+    } else {  // the piece's (or the matrix's) last, partial k block: k >= kvalid contributes 0
+      for (int ks = 0; ks * 4 < kvalid; ++ks) {
+        const bool ok = ks * 4 + lc < kvalid;
+        double a[D::MI], b[D::NJ];
+#pragma unroll
+        for (int i = 0; i < D::MI; ++i) a[i] = ok ? a_s[i * 8 * D::LDA_S + ks * 4] : 0.0;
+#pragma unroll
+        for (int j = 0; j < D::NJ; ++j) b[j] = ok ? b_s[ks * 4 * D::LDB_S + j * 8] : 0.0;
+#pragma unroll
+        for (int i = 0; i < D::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < D::NJ; ++j) dmma_m8n8k4(acc[i][j], a[i], b[j]);
+      }
+    }
+    if (cw.kt == KT - 1) {
+      // fragment (i, j): rows row0 + 32 wm + 8 i + lr, columns col0 + 64 wn + 8 j + 2 lc + {0, 1}
+      const int64_t row0 = int64_t(pc.ti0 + cw.ti) * D::BM + wm * 8 * D::MI + lr;
+      const int64_t col0 = int64_t(pc.tj0 + cw.tj) * D::BN + wn * 8 * D::NJ + 2 * lc;
+      double* Cp = static_cast<double*>(args.C);
+      const bool pair_ok = (args.ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(Cp) % 16 == 0);
+#pragma unroll
+      for (int i = 0; i < D::MI; ++i) {
+        const int64_t r = row0 + 8 * i;
+        if (r >= args.n) continue;
+        double* crow = Cp + r * args.ldc;
+#pragma unroll
+        for (int j = 0; j < D::NJ; ++j) {
+          const int64_t c = col0 + 8 * j;
+          if (c >= args.m) continue;
+          const bool two = c + 1 < args.m;
+          if (atomic) {
+            if (args.sys_atomic) {
+              OpF64::atomic_combine_sys(crow + c, acc[i][j][0]);
+              if (two) OpF64::atomic_combine_sys(crow + c + 1, acc[i][j][1]);
+            } else {
+              OpF64::atomic_combine(crow + c, acc[i][j][0]);
+              if (two) OpF64::atomic_combine(crow + c + 1, acc[i][j][1]);
+            }
+          } else if (two && pair_ok) {
+            double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+            if (!args.overwrite) {
+              const double2 o = *reinterpret_cast<const double2*>(crow + c);
+              v.x += o.x;
+              v.y += o.y;
+            }
+            *reinterpret_cast<double2*>(crow + c) = v;
+          } else {
+            crow[c] = args.overwrite ? acc[i][j][0] : crow[c] + acc[i][j][0];
+            if (two) crow[c + 1] = args.overwrite ? acc[i][j][1] : crow[c + 1] + acc[i][j][1];
+          }
+          acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+      }
+    }
+    cw.next(pc.tm, KT);
+    if (it + D::STAGES < total) {
+      __syncwarp();
+      if (lane == 0 && (smem_add_acq_rel(&freed[s]) & uint32_t(D::NW - 1)) == uint32_t(D::NW - 1))
+        issue(it + D::STAGES, s);
+    }
+  }
+}
+
 // A batch of independent problems (e.g. every COMPUTE cuboid of a GPU-level
 // PACO plan on one device) as ONE launch: CTA ranges [first[q], first[q+1])
 // take problem q's tile-grid pieces (k split grid_s[q] ways).
@@ -1095,6 +1269,23 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
       rc = encode_map_2d(&maps.a, 4, A, n, k, lda, Cfg::LDA_S, Cfg::BM);
       if (!rc) rc = encode_map_2d(&maps.b, 4, B, k, m, ldb, Cfg::BN, Cfg::BK);
       if (rc) return rc;
+    }
+  }
+  if constexpr (Op::kId == PACO_SR_F64) {
+    // the FP64 tensor pipe (PACO_SIMT_DMMA=0: the DFMA kernel)
+    static const bool dmma = !dev_knob("PACO_SIMT_DMMA") || atoi(dev_knob("PACO_SIMT_DMMA")) != 0;
+    if (dmma && vec && n < INT32_MAX && m < INT32_MAX && k < INT32_MAX - 64) {
+      rc = encode_map_2d(&maps.a, 8, A, n, k, lda, DmmaCfg::LDA_S, DmmaCfg::BM);
+      if (!rc) rc = encode_map_2d(&maps.b, 8, B, k, m, ldb, DmmaCfg::LDB_S, DmmaCfg::BK);
+      if (rc) return rc;
+      PACO_CUDA_TRY(cudaFuncSetAttribute(dmma_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(DmmaCfg::SMEM)));
+      {
+        KernelSpan ks(PACO_KT_SIMT_MM, stream);
+        dmma_f64_kernel<<<grid, DmmaCfg::THREADS, DmmaCfg::SMEM, stream>>>(args, table, maps);
+      }
+      PACO_CUDA_TRY(cudaGetLastError());
+      return PACO_OK;
     }
   }
   auto kern = tma   ? simt_mm_kernel<Op, true, Cfg::kTmaOk>
