@@ -1300,9 +1300,39 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
   return PACO_OK;
 }
 
+// f64 batch problems of at least this many terms run alone on the DMMA kernel
+constexpr double kDmmaAloneTerms = double(1 << 27);
+
 template <class Op>
 int launch_simt_batch(int device, cudaStream_t stream, int count, const paco_mm_problem* pr) {
   using Cfg = SimtCfg<Op>;
+  if constexpr (Op::kId == PACO_SR_F64) {
+    // f64 problems big enough to fill the GPU on their own go to the FP64 tensor
+    // pipe one launch each (each gets its own all-SM tile-grid plan, so running
+    // them back to back loses nothing); the rest stay in one DFMA batch launch
+    static const bool dmma = !dev_knob("PACO_SIMT_DMMA") || atoi(dev_knob("PACO_SIMT_DMMA")) != 0;
+    if (dmma) {
+      paco_mm_problem rest[PACO_MAX_BATCH];
+      int nrest = 0;
+      for (int q = 0; q < count; ++q) {
+        const paco_mm_problem& P = pr[q];
+        const bool big = double(P.n) * double(P.m) * double(P.k) >= kDmmaAloneTerms && !(P.flags & PACO_MM_REMOTE) &&
+                         !((P.flags & PACO_MM_OVERWRITE) && (P.flags & PACO_MM_ATOMIC));
+        if (big) {
+          const int rc = launch_simt<Op>(device, stream, P.A, P.lda, P.B, P.ldb, P.C, P.ldc, P.n, P.m, P.k, nullptr,
+                                         0, P.flags);
+          if (rc) return rc;
+        } else {
+          rest[nrest++] = P;
+        }
+      }
+      if (nrest < count) {
+        if (nrest == 0) return PACO_OK;
+        pr = rest;
+        count = nrest;
+      }
+    }
+  }
   SimtScratch sc;
   static BatchTable bt;  // ~7.5 KB; copied into the launch's parameter buffer
   static std::mutex mu;

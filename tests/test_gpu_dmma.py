@@ -52,3 +52,21 @@ def test_dmma_views():
     assert _run(600, 500, 800, a=big_a[2:602, 4:804].contiguous()[:, :], b=big_b[:800, 6:506]) < 1e-12
     # ... and views off 16-byte alignment (odd row pitch: repacked or the element path)
     assert _run(600, 500, 800, a=big_a[1:601, 1:801], b=big_b[1:801, 1:501]) < 1e-12
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+def test_dmma_mm_execute_plans(p):
+    """The reference's executor on SEMIRING_F64: big COMPUTE cuboids leave the
+    batched DFMA launch for one DMMA launch each; k-cut folds stay exact to 1e-12."""
+    from paper_2011_01441_b200 import matmul as M
+    g = torch.Generator(device="cuda").manual_seed(10 + p)
+    n, m, k = 1536, 1280, 2048
+    a = torch.randn(n, k, device="cuda", dtype=torch.float64, generator=g)
+    b = torch.randn(k, m, device="cuda", dtype=torch.float64, generator=g)
+    c = torch.randn(n, m, device="cuda", dtype=torch.float64, generator=g)
+    want = c + a @ b
+    for fused in (True, False):
+        got = c.clone()
+        M.mm_execute(M.mm_one_piece_partition(n, m, k, p), a, b, got, M.SEMIRING_F64, fused_folds=fused)
+        torch.cuda.synchronize()
+        assert float((got - want).norm() / want.norm()) < 1e-12, (p, fused)
