@@ -1301,7 +1301,7 @@ int launch_simt(int device, cudaStream_t stream, const void* A, int64_t lda, con
 }
 
 // f64 batch problems of at least this many terms run alone on the DMMA kernel
-constexpr double kDmmaAloneTerms = double(1 << 27);
+constexpr double kDmmaAloneTerms = double(1 << 30);  // ~60 us of DMMA work: a whole-GPU plan of its own
 
 template <class Op>
 int launch_simt_batch(int device, cudaStream_t stream, int count, const paco_mm_problem* pr) {
