@@ -220,6 +220,24 @@ int paco_narrow_i64(int device, void* stream, const int64_t* src, int64_t ld_src
 int paco_widen_u32_i64(int device, void* stream, const void* r32, int64_t ld_r, int64_t* c, int64_t ld_c,
                        int64_t rows, int64_t cols);
 
+/* Narrowing of a SEMIRING_MINPLUS operand (int64, zero INF = 2^62,
+ * matmul.py:29,55) for the u32 kernel with the INF sentinel kept exact:
+ * x in [0, 2^30 - 2] -> x + 1, x == 2^62 -> 2^31; any other value sets *flag.
+ * On the kernel's wrapping u32 adds a term is then a + b + 2 < 2^31 (both
+ * finite), 2^31 + f + 1 (one INF: the reference's 2^62 + f) or 0 (both INF:
+ * the reference's int64 wrap of 2^63 to -2^63), an order-preserving code that
+ * paco_widen_minplus_i64 decodes.  Replaces the reference's int64 inner loop
+ * (matmul.py:49-50) when the operands hold INF. */
+int paco_narrow_minplus_inf(int device, void* stream, const int64_t* src, int64_t ld_src, void* dst32,
+                            int64_t ld_dst, int64_t rows, int64_t cols, int32_t* flag);
+
+/* c = min(c, decode(r)) in int64 for a PACO_SR_MINPLUS_U32 product r computed
+ * from the semiring zero (r == 2^32 - 1: no term): with inf_encoded the
+ * paco_narrow_minplus_inf code (0 -> -2^63, r < 2^31 -> r - 2, else
+ * 2^62 + r - 2^31 - 1), else r itself. */
+int paco_widen_minplus_i64(int device, void* stream, const void* r32, int64_t ld_r, int64_t* c, int64_t ld_c,
+                           int64_t rows, int64_t cols, int inf_encoded);
+
 /* Strassen's leaf level with the operand formation fused into the 3xTF32
  * kernel: problem q (< count <= 8) multiplies
  * A_q = sum_{t < nta[q]} a_sign[2q+t] * a_terms[2q+t]   (n x k, pitch lda)

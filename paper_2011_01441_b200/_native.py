@@ -78,6 +78,8 @@ SIGNATURES = {
                                     ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
     "paco_narrow_i64": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _int, _vp]),
     "paco_widen_u32_i64": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
+    "paco_narrow_minplus_inf": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _vp]),
+    "paco_widen_minplus_i64": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _int]),
     "paco_host_copy2d": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _int]),
     "paco_mm_tf32x3_fused": (_int, [_int, _vp, _int, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_vp),
                                     ctypes.POINTER(ctypes.c_int32), _i64, ctypes.POINTER(ctypes.c_int32),

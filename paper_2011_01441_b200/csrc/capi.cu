@@ -111,6 +111,10 @@ int launch_lincomb(int dtype, cudaStream_t st, void* out, int64_t ldo, int64_t n
                    const void* const* ins, const int64_t* lds, const int32_t* coefs, int acc);
 int launch_narrow_i64(cudaStream_t st, const int64_t* src, int64_t lds, void* dst, int64_t ldd, int64_t n,
                       int64_t m, int64_t lo, int64_t hi, int saturate, int32_t* flag);
+int launch_narrow_minplus_inf(cudaStream_t st, const int64_t* src, int64_t lds, void* dst, int64_t ldd, int64_t n,
+                              int64_t m, int32_t* flag);
+int launch_widen_minplus(cudaStream_t st, const void* r, int64_t ldr, int64_t* c, int64_t ldc, int64_t n, int64_t m,
+                         int inf_encoded);
 int launch_widen_u32_i64(cudaStream_t st, const void* r, int64_t ldr, int64_t* c, int64_t ldc, int64_t n,
                          int64_t m);
 int launch_transpose(cudaStream_t st, int elsize, void* dst, int64_t ldd, const void* src, int64_t lds, int64_t rows,
@@ -418,6 +422,28 @@ int paco_widen_u32_i64(int device, void* stream, const void* r32, int64_t ld_r, 
   DeviceGuard dg;
   PACO_TRY(dg.use(device));
   return launch_widen_u32_i64(static_cast<cudaStream_t>(stream), r32, ld_r, c, ld_c, rows, cols);
+}
+
+int paco_narrow_minplus_inf(int device, void* stream, const int64_t* src, int64_t ld_src, void* dst32,
+                            int64_t ld_dst, int64_t rows, int64_t cols, int32_t* flag) {
+  PACO_TRY(check_view("src", src, ld_src, rows, cols));
+  PACO_TRY(check_view("dst", dst32, ld_dst, rows, cols));
+  if (rows > 0 && cols > 0 && !flag) {
+    set_error("paco_narrow_minplus_inf: null flag");
+    return PACO_ERR_ARG;
+  }
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_narrow_minplus_inf(static_cast<cudaStream_t>(stream), src, ld_src, dst32, ld_dst, rows, cols, flag);
+}
+
+int paco_widen_minplus_i64(int device, void* stream, const void* r32, int64_t ld_r, int64_t* c, int64_t ld_c,
+                           int64_t rows, int64_t cols, int inf_encoded) {
+  PACO_TRY(check_view("r", r32, ld_r, rows, cols));
+  PACO_TRY(check_view("c", c, ld_c, rows, cols));
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_widen_minplus(static_cast<cudaStream_t>(stream), r32, ld_r, c, ld_c, rows, cols, inf_encoded);
 }
 
 int paco_kernel_timing(int enable) {

@@ -355,6 +355,52 @@ __global__ void widen_u32_i64_kernel(const uint32_t* __restrict__ r, int64_t ldr
     }
 }
 
+// SEMIRING_MINPLUS operand -> u32 code keeping INF = 2^62 exact (paco_narrow_minplus_inf)
+__global__ void narrow_minplus_inf_kernel(const int64_t* __restrict__ src, int64_t lds, uint32_t* __restrict__ dst,
+                                          int64_t ldd, int64_t n, int64_t m, int32_t* flag) {
+  constexpr int64_t kInf = int64_t(1) << 62, kMaxFinite = (int64_t(1) << 30) - 2;
+  int bad = 0;
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
+    for (int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 2; j < m;
+         j += int64_t(gridDim.x) * blockDim.x * 2) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (j + e >= m) break;
+        const int64_t v = __ldcs(src + i * lds + j + e);
+        uint32_t code = 0;
+        if (v == kInf)
+          code = 0x80000000u;
+        else if (v >= 0 && v <= kMaxFinite)
+          code = uint32_t(v) + 1u;
+        else
+          bad = 1;
+        dst[i * ldd + j + e] = code;
+      }
+    }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+// c = min(c, decode(r)) in int64 (paco_widen_minplus_i64)
+__global__ void widen_minplus_kernel(const uint32_t* __restrict__ r, int64_t ldr, int64_t* __restrict__ c,
+                                     int64_t ldc, int64_t n, int64_t m, int inf_encoded) {
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y)
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < m; j += int64_t(gridDim.x) * blockDim.x) {
+      const uint32_t v = __ldcs(r + i * ldr + j);
+      if (v == 0xFFFFFFFFu) continue;  // no term reached this element
+      int64_t x;
+      if (!inf_encoded)
+        x = int64_t(v);
+      else if (v == 0u)
+        x = INT64_MIN;  // INF + INF: the reference's int64 sum 2^63 wraps
+      else if (v < 0x80000000u)
+        x = int64_t(v) - 2;
+      else
+        x = (int64_t(1) << 62) + int64_t(v - 0x80000001u);
+      int64_t* p = c + i * ldc + j;
+      if (x < *p) *p = x;
+    }
+}
+
 // dst (cols x rows) = src^T through a padded 32 x 32 smem tile: reads and
 // writes both coalesced along rows (blockDim 32 x 8, each thread 4 rows).
 template <class T>
@@ -417,6 +463,26 @@ int launch_narrow_i64(cudaStream_t st, const int64_t* src, int64_t lds, void* ds
   KernelSpan ks(PACO_KT_ELEMENTWISE, st);
   narrow_i64_kernel<<<rows_grid(n, m, 512), 256, 0, st>>>(src, lds, static_cast<uint32_t*>(dst), ldd, n, m, lo,
                                                            hi, saturate, flag);
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
+int launch_narrow_minplus_inf(cudaStream_t st, const int64_t* src, int64_t lds, void* dst, int64_t ldd, int64_t n,
+                              int64_t m, int32_t* flag) {
+  if (n <= 0 || m <= 0) return PACO_OK;
+  KernelSpan ks(PACO_KT_ELEMENTWISE, st);
+  narrow_minplus_inf_kernel<<<rows_grid(n, m, 512), 256, 0, st>>>(src, lds, static_cast<uint32_t*>(dst), ldd, n, m,
+                                                                   flag);
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
+int launch_widen_minplus(cudaStream_t st, const void* r, int64_t ldr, int64_t* c, int64_t ldc, int64_t n, int64_t m,
+                         int inf_encoded) {
+  if (n <= 0 || m <= 0) return PACO_OK;
+  KernelSpan ks(PACO_KT_ELEMENTWISE, st);
+  widen_minplus_kernel<<<rows_grid(n, m, 256), 256, 0, st>>>(static_cast<const uint32_t*>(r), ldr, c, ldc, n, m,
+                                                              inf_encoded);
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;
 }

@@ -56,10 +56,14 @@ def kernel_for(semiring: Semiring, A, B) -> tuple[int, object]:
 # 64-bit add+min or multiply-add is 4-6 ALU instructions per term.  When every
 # operand fits 32 bits the product is computed on 32-bit lanes with the same
 # result bit for bit: (+,x) on int32 x int32 -> int64 (IMAD.WIDE, wrapping
-# int64 accumulation, as NumPy's), (min,+) on u32 lanes for operands in
-# [0, 2^31) (a + b <= 2^32 - 2: no wrap, so no clamp either).  The range check
-# runs on the device while narrowing; any value outside (the INF = 2^62
-# sentinel, negatives, wrap-around cases) keeps the int64 kernel.
+# int64 accumulation, as NumPy's); (min,+) on u32 lanes, either with the INF
+# sentinel kept exact (paco_narrow_minplus_inf: finite operands in [0, 2^30 - 2]
+# and INF = 2^62, whose sums -- including the reference's INF + INF wrap to
+# -2^63 -- map to an order-preserving u32 code) or, failing that, for operands
+# in [0, 2^31) (a + b <= 2^32 - 2: no wrap).  The product is formed from the
+# semiring zero and min-ed into the int64 C by paco_widen_minplus_i64.  The
+# range checks run on the device while narrowing; any other value (negatives,
+# big finite values next to INF) keeps the int64 kernel.
 NARROW_MIN_TERMS = 1 << 22   # below this the 64-bit kernel is cheaper than a narrowing pass + flag read
 _NARROW_RANGE = {"int": (-(2**31), 2**31 - 1), "minplus": (0, 2**31 - 1)}
 
@@ -83,24 +87,47 @@ def _narrow_dev(x: torch.Tensor, lo: int, hi: int, saturate: bool, flag: torch.T
     return out
 
 
+def _narrow_inf(x: torch.Tensor, flag: torch.Tensor, st) -> torch.Tensor:
+    """u32 code of a SEMIRING_MINPLUS operand with INF kept (paco_narrow_minplus_inf)."""
+    out = torch.empty(tuple(x.shape), dtype=torch.int32, device=x.device)
+    xv, ov = View.of(x), View.of(out)
+    nat.check(nat.load().paco_narrow_minplus_inf(xv.device, st.cuda_stream, xv.ptr, xv.ld, ov.ptr, ov.ld, xv.rows,
+                                                 xv.cols, flag.data_ptr()))
+    return out
+
+
 class _Narrowed:
     """Device operands of a narrowed product and how to put C back (int64)."""
 
     def __init__(self, semiring: Semiring, A, B, C, dev: int, st, overwrite: bool):
-        lo, hi = _NARROW_RANGE[semiring.name]
         self.a64 = stage_in(A, np.int64, dev)
         self.b64 = stage_in(B, np.int64, dev)
         self.out = Output(C, np.int64, dev, load=not overwrite)
         if overwrite:
             launch_fill(semiring.kernel_id, st, View.of(self.out.dev))
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.a32 = _narrow_dev(self.a64, lo, hi, False, flag, st)
-        self.b32 = _narrow_dev(self.b64, lo, hi, False, flag, st)
         self.minplus = semiring is SEMIRING_MINPLUS
-        self.c32 = None
-        if self.minplus:  # C's u32 image: values >= 2^32 - 1 saturate (restored by the widen)
-            self.c32 = _narrow_dev(self.out.dev, 0, 2**32 - 1, True, flag, st)
-        self.ok = int(flag.item()) == 0   # one 4-byte read: the range verdict
+        self.inf = False
+        self.r = None
+        if self.minplus:
+            # INF-keeping code first (distance matrices hold the 2^62 sentinel);
+            # plain [0, 2^31) operands without INF as the second try
+            self.a32 = _narrow_inf(self.a64, flag, st)
+            self.b32 = _narrow_inf(self.b64, flag, st)
+            self.inf = int(flag.item()) == 0
+            if not self.inf:
+                flag.zero_()
+                lo, hi = _NARROW_RANGE["minplus"]
+                self.a32 = _narrow_dev(self.a64, lo, hi, False, flag, st)
+                self.b32 = _narrow_dev(self.b64, lo, hi, False, flag, st)
+            # the product from the u32 zero, min-ed into the int64 C by finish()
+            self.r = torch.empty(tuple(self.out.dev.shape), dtype=torch.int32, device=dev)
+            launch_fill(nat.SR_MINPLUS_U32, st, View.of(self.r))
+        else:
+            lo, hi = _NARROW_RANGE["int"]
+            self.a32 = _narrow_dev(self.a64, lo, hi, False, flag, st)
+            self.b32 = _narrow_dev(self.b64, lo, hi, False, flag, st)
+        self.ok = self.inf or int(flag.item()) == 0   # one 4-byte read: the range verdict
 
     @property
     def semiring(self) -> Semiring:
@@ -108,13 +135,13 @@ class _Narrowed:
 
     @property
     def c(self) -> torch.Tensor:
-        return self.c32 if self.minplus else self.out.dev
+        return self.r if self.minplus else self.out.dev
 
     def finish(self, st) -> None:
         if self.minplus:
-            r, c = View.of(self.c32), View.of(self.out.dev)
-            nat.check(nat.load().paco_widen_u32_i64(c.device, st.cuda_stream, r.ptr, r.ld, c.ptr, c.ld, c.rows,
-                                                    c.cols))
+            r, c = View.of(self.r), View.of(self.out.dev)
+            nat.check(nat.load().paco_widen_minplus_i64(c.device, st.cuda_stream, r.ptr, r.ld, c.ptr, c.ld, c.rows,
+                                                        c.cols, int(self.inf)))
         self.out.finish()
 
 

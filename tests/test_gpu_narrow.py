@@ -157,3 +157,85 @@ def test_int64_ring_narrowed_wraps_like_numpy(always_narrow, monkeypatch, golden
     M.mm_seq(g["int_wrap_A"], g["int_wrap_B"], C, M.SEMIRING_INT)
     assert np.array_equal(C, g["int_wrap_C"])
     assert 1 not in seen
+
+
+def _inf_operands(rng, n, m, k, p_inf=0.2, hi=2**30 - 2):
+    A = rng.integers(0, hi + 1, (n, k), dtype=np.int64)
+    B = rng.integers(0, hi + 1, (k, m), dtype=np.int64)
+    A[rng.random(A.shape) < p_inf] = ZERO
+    B[rng.random(B.shape) < p_inf] = ZERO
+    return A, B
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (37, 45, 29), (200, 130, 257), (513, 260, 300)])
+def test_minplus_i64_inf_kept_on_u32(always_narrow, monkeypatch, shape):
+    """INF = 2^62 sentinels stay on the u32 kernel: one-INF terms give the
+    reference's 2^62 + f, an all-INF row against an all-INF column its int64
+    wrap INF + INF = -2^63 -- bit for bit."""
+    n, m, k = shape
+    rng = np.random.default_rng(21 + n)
+    A, B = _inf_operands(rng, n, m, k)
+    A[0, 0] = 2**30 - 2  # extreme finite sums
+    B[0, 0] = 2**30 - 2
+    if n > 2 and m > 2:
+        A[1, :] = ZERO          # row 1: every term has an INF on the A side ...
+        B[:, 2] = ZERO          # ... and column 2 every term on the B side: C[1, 2] = INF + INF wrap
+        A[2, :] = ZERO          # row 2 against a finite column: C[2, 0] = 2^62 + min_l B[l, 0]
+        B[:, 0] = rng.integers(0, 2**30 - 1, k)
+    C0 = np.full((n, m), ZERO, np.int64)
+    mask = rng.random((n, m)) < 0.2
+    C0[mask] = rng.integers(-(2**40), 2**63 - 1, int(mask.sum()))  # any int64 C, negatives included
+    want = _want_minplus(A, B, C0)
+    seen = _spy(monkeypatch)
+    C = C0.copy()
+    M.mm_seq(A, B, C, M.SEMIRING_MINPLUS)
+    assert np.array_equal(C, want)
+    assert seen and all(s == 9 for s in seen)  # PACO_SR_MINPLUS_U32
+    if n > 2 and m > 2:
+        assert C[1, 2] == np.iinfo(np.int64).min
+        assert C[2, 0] == min(C0[2, 0], ZERO + int(B[:, 0].min()))
+
+
+@pytest.mark.parametrize("p", [3, 5, 7])
+def test_minplus_i64_inf_plans(always_narrow, monkeypatch, p):
+    n, m, k = 300, 260, 515
+    rng = np.random.default_rng(300 + p)
+    A, B = _inf_operands(rng, n, m, k, p_inf=0.5)
+    C0 = np.full((n, m), ZERO, np.int64)
+    want = _want_minplus(A, B, C0)
+    seen = _spy(monkeypatch)
+    for fused in (True, False):
+        C = C0.copy()
+        M.mm_execute(M.mm_one_piece_partition(n, m, k, p), A, B, C, M.SEMIRING_MINPLUS, fused_folds=fused)
+        assert np.array_equal(C, want), (p, fused)
+    assert seen and all(s == 9 for s in seen)
+
+
+def test_minplus_i64_inf_ranges(always_narrow, monkeypatch):
+    rng = np.random.default_rng(77)
+    n, m, k = 90, 70, 110
+    # finite values up to 2^31 - 1 without INF: the plain u32 code (second narrowing try)
+    A = rng.integers(2**30, 2**31, (n, k), dtype=np.int64)
+    B = rng.integers(0, 2**31, (k, m), dtype=np.int64)
+    C0 = np.full((n, m), ZERO, np.int64)
+    want = _want_minplus(A, B, C0)
+    seen = _spy(monkeypatch)
+    C = C0.copy()
+    M.mm_seq(A, B, C, M.SEMIRING_MINPLUS)
+    assert np.array_equal(C, want) and seen and all(s == 9 for s in seen)
+    # INF next to a finite value >= 2^30 - 1: no u32 code holds both -> int64 kernel, same answer
+    A2, B2 = _inf_operands(rng, n, m, k)
+    A2[3, 3] = 2**30 - 1
+    want2 = _want_minplus(A2, B2, C0)
+    seen.clear()
+    C2 = C0.copy()
+    M.mm_seq(A2, B2, C2, M.SEMIRING_MINPLUS)
+    assert np.array_equal(C2, want2) and 9 not in seen
+    # a device-side run with overwrite: garbage C, INF operands
+    a, b = torch.from_numpy(A2 * 0 + B2[:1, :1].item()).cuda(), torch.from_numpy(B2).cuda()
+    A3, B3 = _inf_operands(rng, n, m, k)
+    want3 = _want_minplus(A3, B3, C0)
+    c = torch.empty((n, m), dtype=torch.int64, device="cuda")
+    M.mm_seq(torch.from_numpy(A3).cuda(), torch.from_numpy(B3).cuda(), c, M.SEMIRING_MINPLUS, overwrite=True)
+    assert np.array_equal(c.cpu().numpy(), want3)
+    del a, b
