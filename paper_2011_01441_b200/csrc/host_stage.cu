@@ -31,9 +31,12 @@ class StagePool {
   }
 
   // Copy with `threads` participants (the caller is one of them).  A worker
-  // takes the job and the part counter under the same lock run() resets them
-  // with, and run() returns only when every part is done and no worker is
-  // still inside: a late worker can never pair an old job with a new counter.
+  // joins a job only while it is open, under the lock run() opens and closes
+  // it with; run() closes the job once every part is done and no worker is
+  // inside.  So a worker that wakes late -- after its job finished -- finds it
+  // closed and takes nothing: it can never pair an old job's pointers with the
+  // part counter of the next job (which would mark a part done that nobody
+  // copied, and write into the old job's buffers).
   void run(const CopyJob& job, int threads) {
     std::lock_guard<std::mutex> serial(call_mu_);  // one job at a time
     ensure_workers(threads - 1);
@@ -44,11 +47,13 @@ class StagePool {
       done_.store(0);
       ++gen_;
       active_ = threads - 1;
+      open_ = true;
     }
     cv_.notify_all();
     work(job);
     std::unique_lock<std::mutex> lock(mu_);
     done_cv_.wait(lock, [&] { return done_.load() == job.parts && inside_ == 0; });
+    open_ = false;
   }
 
  private:
@@ -66,8 +71,9 @@ class StagePool {
       CopyJob j;
       {
         std::unique_lock<std::mutex> lock(mu_);
-        cv_.wait(lock, [&] { return gen_ != seen && id < active_; });
+        cv_.wait(lock, [&] { return gen_ != seen; });
         seen = gen_;
+        if (!open_ || id >= active_) continue;  // finished already, or not a participant
         j = job_;
         ++inside_;
       }
@@ -105,6 +111,7 @@ class StagePool {
   uint64_t gen_ = 0;
   int active_ = 0;
   int inside_ = 0;
+  bool open_ = false;
 };
 
 }  // namespace

@@ -71,3 +71,26 @@ def test_host_copy2d_parallel_staging(shape, cols):
         want = np.zeros(shape, np.int32)
         want[:, c0:c1] = src[:, c0:c1]
         assert np.array_equal(dst, want), threads
+
+
+def test_host_copy2d_back_to_back_jobs():
+    """Many short jobs back to back, each into a fresh destination: a pool
+    worker that wakes after its job finished must not take part in the next
+    one with the old job's pointers (which would leave a part of the new
+    destination uncopied)."""
+    import numpy as np
+
+    from paper_2011_01441_b200 import mm as MM
+    rng = np.random.default_rng(7)
+    srcs = [rng.integers(0, 2**31 - 1, (256 + 64 * (i % 5), 1024 + 256 * (i % 3)), dtype=np.int64).astype(np.int32)
+            for i in range(8)]
+    old = MM._HOST_THREADS
+    MM._HOST_THREADS = 12
+    try:
+        for it in range(400):
+            src = srcs[it % len(srcs)]
+            dst = np.zeros_like(src)
+            MM._host_copy(dst, src)
+            assert np.array_equal(dst, src), it
+    finally:
+        MM._HOST_THREADS = old
