@@ -37,6 +37,9 @@
 
 #include "common.cuh"
 
+#ifndef PACO_TC_EARLY_ABLATE
+#define PACO_TC_EARLY_ABLATE 0
+#endif
 #ifndef PACO_EXIT_WAIT_READ
 #define PACO_EXIT_WAIT_READ 1
 #endif
@@ -321,6 +324,8 @@ struct TcArgs {
   int32_t* sched;    // per-group tile counters + a CTA-done counter at [groups]
                      // (zero at launch; the last CTA to finish zeroes them again)
   int32_t groups;    // CTA c serves group c % groups: column blocks g, g + groups, ...
+  int32_t early;     // operands are not written by the previous launch on the stream (run_tc): the
+                     // producer loads its first tile and the MMAs run before griddepcontrol.wait
 };
 
 // slot 15 of each CTA: (entry, after setup, exit)
@@ -473,7 +478,11 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   // The next launch may start as soon as SMs free up (one CTA per SM: only
   // SMs whose CTA has exited take one of its CTAs).
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  // early (resident-B kinds): the producer's first-tile loads and the MMA warp
+  // (TMEM and shared memory only) run ahead of the wait; tile claims and every
+  // C store still come after the previous grid has completed
+  const bool early = K::B_RES && args.early;
+  if (!(early && warp <= 1)) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (threadIdx.x == 0) tc_stamp(args, 15, 1);
 
   if (warp == 0) {
@@ -491,8 +500,12 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
           mbar_wait(&qempty[qs], (uint32_t(i / QD) & 1) ^ 1);
           qid[qs] = id;
           mbar_arrive(&qfull[qs]);
-          if (id < 0) break;
-          raw = claim_issue(args);  // one tile ahead; resolved (waited for) at the next publish
+          if (id < 0) {
+            if (early && i == 0) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+            break;
+          }
+          const bool late_claim = early && i == 0;  // the first claim waits for the previous grid
+          if (!late_claim) raw = claim_issue(args);  // one tile ahead; resolved (waited for) at the next publish
           const int tpp = args.tiles_rb * args.tiles_nb, lid = id % tpp;
           const int nb = lid / args.tiles_rb, rb = lid % args.tiles_rb;
           const TcProb& P = maps.p[id / tpp];
@@ -557,6 +570,10 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
                               P.b_col0[o] + nb * BN + L::BOX_N * j, kb * BK);
               }
             }
+          }
+          if (late_claim) {
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
+            raw = claim_issue(args);
           }
         }
       }
@@ -1439,6 +1456,57 @@ int encode_map_2d(CUtensorMap* map, int elsize, const void* ptr, int64_t rows, i
 }
 
 namespace {
+// ---------------------------------------------------------------------------
+// Early operand loads under programmatic dependent launch.  The tcgen05 kernels
+// signal launch_dependents at entry, so the next launch on the stream may start
+// while they (and, transitively, their own predecessors) still run; its
+// griddepcontrol.wait then orders everything after it.  A resident-B launch may
+// TMA-load its first tile before that wait only if no operand byte can be
+// written by a launch still in flight: kernels without the early signal (every
+// other kernel of this library, and the caller's) finish before a dependent
+// starts, so only this library's tcgen05 launches matter, and their outputs
+// are recorded per stream here (the last kPdlKeep ranges: a superset of any
+// chain that can still be resident).  Assumes no third-party kernel that
+// itself signals launch_dependents early writes the operands right before.
+// ---------------------------------------------------------------------------
+struct MemRange {
+  uintptr_t lo, hi;
+};
+MemRange view_range(const void* p, int64_t ld, int64_t rows, int64_t cols, int es) {
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(p);
+  if (rows <= 0 || cols <= 0) return {lo, lo};
+  return {lo, lo + uintptr_t(((rows - 1) * ld + cols) * int64_t(es))};
+}
+std::mutex g_pdl_mu;  // held from the check to the launch: record order = stream order
+std::map<std::pair<int, cudaStream_t>, std::vector<MemRange>> g_pdl_out;
+constexpr size_t kPdlKeep = 1024;
+// true: none of `reads` overlaps a recorded output; then `writes` are recorded
+bool pdl_track(int device, cudaStream_t st, const MemRange* reads, int nr, const MemRange* writes, int nw) {
+  std::vector<MemRange>& q = g_pdl_out[{device, st}];
+  bool ok = nr > 0;
+  for (int i = 0; i < nr && ok; ++i)
+    for (const MemRange& w : q)
+      if (reads[i].lo < w.hi && w.lo < reads[i].hi) {
+        ok = false;
+        break;
+      }
+  for (int i = 0; i < nw; ++i) q.push_back(writes[i]);
+  if (q.size() > kPdlKeep) q.erase(q.begin(), q.begin() + (q.size() - kPdlKeep));
+  return ok;
+}
+// record a batch's destinations: dst[4 q + d] for d < ndst[q], or single[q]
+void pdl_record(int device, cudaStream_t st, int count, const int32_t* ndst, void* const* dst,
+                const void* const* single, int64_t ldc, int64_t n, int64_t m) {
+  std::vector<MemRange> w;
+  for (int q = 0; q < count; ++q) {
+    if (ndst)
+      for (int d = 0; d < ndst[q]; ++d) w.push_back(view_range(dst[4 * q + d], ldc, n, m, 4));
+    else if (single)
+      w.push_back(view_range(single[q], ldc, n, m, 4));
+  }
+  pdl_track(device, st, nullptr, 0, w.data(), int(w.size()));
+}
+
 // Scratch for split / repacked operands: stream-ordered allocations from the
 // device's default memory pool (kept cached: release threshold = max), freed
 // on the launch stream after the kernel.  Concurrent launches on different
@@ -1913,7 +1981,7 @@ int check_tc_call(void* C, int64_t ldc, int64_t n, int64_t m, int64_t k, const i
 
 template <class K>
 int run_tc(int device, Scratch& sc, cudaStream_t stream, const tc::TcMaps& maps, int count, int64_t n, int64_t m,
-           int64_t k, int flags) {
+           int64_t k, int flags, bool early = false) {
   using L = tc::Layout<K>;
   int rc;
   tc::TcArgs args;
@@ -1945,6 +2013,8 @@ int run_tc(int device, Scratch& sc, cudaStream_t stream, const tc::TcMaps& maps,
     while (g > 1 && grid % g) --g;
     args.groups = g;
   }
+  static const bool early_on = !dev_knob("PACO_TC_EARLY") || atoi(dev_knob("PACO_TC_EARLY")) != 0;
+  args.early = (early && early_on) || PACO_TC_EARLY_ABLATE ? 1 : 0;
   if ((rc = stream_counters(device, stream, &args.sched))) return rc;
   if (!args.sched) {  // first launch on a capturing stream: stream-ordered counters
     void* counters;
@@ -2003,7 +2073,15 @@ int launch_tc(int device, cudaStream_t stream, const void* A, int64_t lda, const
     ldc = ld2;
   }
   if ((rc = build_output<K>(maps.p[0], C, ldc, n, m))) return rc;
-  if ((rc = run_tc<K>(device, sc, stream, maps, 1, n, m, k, flags))) return rc;
+  bool early;
+  {
+    std::lock_guard<std::mutex> pl(g_pdl_mu);
+    const MemRange rd[2] = {view_range(A, lda, n, k, K::ELEM),
+                            K::B_KMAJOR ? view_range(B, ldb, m, k, K::ELEM) : view_range(B, ldb, k, m, K::ELEM)};
+    const MemRange wr[2] = {view_range(C, ldc, n, m, 4), view_range(c_user ? c_user : C, ldc_user, n, m, 4)};
+    early = pdl_track(device, stream, rd, 2, wr, 2);
+    if ((rc = run_tc<K>(device, sc, stream, maps, 1, n, m, k, flags, early))) return rc;
+  }
   if (c_user)
     PACO_CUDA_TRY(cudaMemcpy2DAsync(c_user, ldc_user * 4, C, ldc * 4, m * 4, n, cudaMemcpyDeviceToDevice, stream));
   return PACO_OK;
@@ -2062,6 +2140,12 @@ int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* 
           return rc;
       }
     }
+  }
+  std::lock_guard<std::mutex> pl(g_pdl_mu);
+  {
+    const void* cs[tc::kMaxBatch];
+    for (int q = 0; q < count; ++q) cs[q] = pre[q].c;
+    pdl_record(device, stream, count, ndst, dst, cs, ldc, n, m);
   }
   return run_tc<K>(device, sc, stream, maps, count, n, m, k, flags);
 }
@@ -2163,6 +2247,12 @@ int launch_tc_pair(int device, cudaStream_t stream, int count, const Presplit* p
                          d == 0 ? &P.c_col0 : &P.cx_col0[d - 1], SW)))
         return rc;
     }
+  }
+  std::lock_guard<std::mutex> pl(g_pdl_mu);
+  {
+    const void* cs[tc::kMaxBatch];
+    for (int q = 0; q < count; ++q) cs[q] = pre[q].c;
+    pdl_record(device, stream, count, ndst, dst, cs, ldc, n, m);
   }
   return run_pair(device, stream, maps, count, n, m, k, flags, fa ? 1 : 0);
 }
@@ -2335,6 +2425,8 @@ int launch_mm_tf32x3_fused(int device, cudaStream_t stream, int count, const int
       if (d > 0 && (rc = build_output<K>(P, dst[4 * q + d], ldc, n, m, &P.cx[d - 1], &P.cx_col0[d - 1]))) return rc;
     }
   }
+  std::lock_guard<std::mutex> pl(g_pdl_mu);
+  pdl_record(device, stream, count, ndst, dst, nullptr, ldc, n, m);
   return run_tc<K>(device, sc, stream, maps, count, n, m, k, 0);
 }
 
@@ -2442,6 +2534,8 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
       maps.p[q].a[1] = maps.p[q].a2 = maps.p[q].a[0];
       maps.p[q].b[1] = maps.p[q].b2 = maps.p[q].b[0];
     }
+  std::lock_guard<std::mutex> pl(g_pdl_mu);
+  pdl_record(device, stream, count, ndst, dst, nullptr, ldc, n, m);
   return run_pair(device, stream, maps, count, n, m, k, 0, raw ? 4 : (cv ? 3 : 2));
 }
 
