@@ -289,6 +289,24 @@ int paco_mm_tf32b2_multi(int device, void* stream, int count, const void* const*
                          const void* const* b_l16, int64_t ldb, const int32_t* ndst, void* const* dst,
                          const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k);
 
+/* Strassen leaf operands in the bf16x3 format: like paco_lincomb_multi, but
+ * output o is written as two bf16 planes his[o] = bf16_rn(x), los[o] =
+ * bf16_rn(x - his[o]) (pitch ldo[o] elements, shared by both planes); a
+ * one-term row is a split copy.  16-byte aligned views, m % 8 == 0. */
+int paco_lincomb_split(int device, void* stream, int64_t n, int64_t m, int nin, const void* const* ins,
+                       const int64_t* lds, int nout, void* const* his, void* const* los, const int64_t* ldo,
+                       const int32_t* coefs);
+
+/* bf16x3 batch on tcgen05 CTA pairs -- cfg5's Strassen leaf products: C[q] (+/-)=
+ * A[q] B[q] with A[q] = a_hi[q] + a_lo[q] (bf16 planes, n x k, pitch lda) and
+ * B[q]^T = b_hi[q] + b_lo[q] (m x k, pitch ldb), computed as hi*hi + hi*lo +
+ * lo*hi on kind::f16 with fp32 accumulation; destinations and signs as
+ * paco_mm_tf32x3_multi (up to 4 per problem, count <= 8). */
+int paco_mm_bf16x3_multi(int device, void* stream, int count, const void* const* a_hi, const void* const* a_lo,
+                         int64_t lda, const void* const* b_hi, const void* const* b_lo, int64_t ldb,
+                         const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc, int64_t n,
+                         int64_t m, int64_t k);
+
 /* dst (cols x rows, pitch ld_dst) = src^T (rows x cols, pitch ld_src); 4- or
  * 8-byte elements.  Strassen transposes B once so every T_r^T operand of the
  * fused leaves is a K-major view. */

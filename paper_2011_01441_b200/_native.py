@@ -95,6 +95,12 @@ SIGNATURES = {
     "paco_mm_tf32b2_multi": (_int, [_int, _vp, _int] + [ctypes.POINTER(_vp)] * 3 + [_i64] +
                              [ctypes.POINTER(_vp)] * 3 + [_i64, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_vp),
                                                           ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
+    "paco_lincomb_split": (_int, [_int, _vp, _i64, _i64, _int, ctypes.POINTER(_vp), ctypes.POINTER(_i64), _int,
+                                  ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64),
+                                  ctypes.POINTER(ctypes.c_int32)]),
+    "paco_mm_bf16x3_multi": (_int, [_int, _vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64,
+                                    ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, ctypes.POINTER(ctypes.c_int32),
+                                    ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
     "paco_transpose": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_copy2d": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_host_register": (_int, [_vp, ctypes.c_size_t]),

@@ -121,6 +121,12 @@ int launch_transpose(cudaStream_t st, int elsize, void* dst, int64_t ldd, const 
                      int64_t cols);
 int launch_lincomb_multi(cudaStream_t st, int64_t n, int64_t m, int nin, const void* const* ins, const int64_t* lds,
                          int nout, void* const* outs, const int64_t* ldo, const int32_t* coefs);
+int launch_lincomb_split(cudaStream_t st, int64_t n, int64_t m, int nin, const void* const* ins, const int64_t* lds,
+                         int nout, void* const* his, void* const* los, const int64_t* ldo, const int32_t* coefs);
+int launch_mm_bf16x3_multi(int device, cudaStream_t stream, int count, const void* const* a_hi,
+                           const void* const* a_lo, int64_t lda, const void* const* b_hi, const void* const* b_lo,
+                           int64_t ldb, const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc,
+                           int64_t n, int64_t m, int64_t k);
 int run_alu_probe(cudaStream_t st, int which, int iters, double* tpc, double* mhz);
 struct Box;
 }  // namespace paco
@@ -299,6 +305,41 @@ int paco_lincomb_multi(int device, void* stream, int64_t n, int64_t m, int nin, 
   DeviceGuard dg;
   PACO_TRY(dg.use(device));
   return launch_lincomb_multi(static_cast<cudaStream_t>(stream), n, m, nin, ins, lds, nout, outs, ldo, coefs);
+}
+
+int paco_lincomb_split(int device, void* stream, int64_t n, int64_t m, int nin, const void* const* ins,
+                       const int64_t* lds, int nout, void* const* his, void* const* los, const int64_t* ldo,
+                       const int32_t* coefs) {
+  if (!ins || !lds || (nout > 0 && (!his || !los || !ldo || !coefs))) {
+    set_error("paco_lincomb_split: null arrays");
+    return PACO_ERR_ARG;
+  }
+  for (int q = 0; q < nin && q < 4; ++q) PACO_TRY(check_view("in", ins[q], lds[q], n, m));
+  for (int o = 0; o < nout && o < 8; ++o) {
+    PACO_TRY(check_view("hi", his[o], ldo[o], n, m));
+    PACO_TRY(check_view("lo", los[o], ldo[o], n, m));
+  }
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_lincomb_split(static_cast<cudaStream_t>(stream), n, m, nin, ins, lds, nout, his, los, ldo, coefs);
+}
+
+int paco_mm_bf16x3_multi(int device, void* stream, int count, const void* const* a_hi, const void* const* a_lo,
+                         int64_t lda, const void* const* b_hi, const void* const* b_lo, int64_t ldb,
+                         const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc, int64_t n,
+                         int64_t m, int64_t k) {
+  if (count >= 1 && count <= 8 && a_hi && a_lo && b_hi && b_lo && ndst && dst)
+    for (int q = 0; q < count; ++q) {
+      PACO_TRY(check_view("A_hi", a_hi[q], lda, n, k));
+      PACO_TRY(check_view("A_lo", a_lo[q], lda, n, k));
+      PACO_TRY(check_view("Bt_hi", b_hi[q], ldb, m, k));
+      PACO_TRY(check_view("Bt_lo", b_lo[q], ldb, m, k));
+      for (int d = 0; d < ndst[q] && d < 4; ++d) PACO_TRY(check_view("C", dst[4 * q + d], ldc, n, m));
+    }
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_mm_bf16x3_multi(device, static_cast<cudaStream_t>(stream), count, a_hi, a_lo, lda, b_hi, b_lo, ldb,
+                                ndst, dst, sign, ldc, n, m, k);
 }
 
 int paco_mm_batch(int device, void* stream, int semiring, int count, const paco_mm_problem* problems) {

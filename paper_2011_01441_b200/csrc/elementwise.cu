@@ -9,6 +9,8 @@
 
 #include <cstring>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "semiring_ops.cuh"
 
@@ -300,6 +302,98 @@ int launch_lincomb_multi(cudaStream_t st, int64_t n, int64_t m, int nin, const v
   KernelSpan ks(PACO_KT_LINCOMB, st);
   const int64_t xb = (m / 4 + 127) / 128, yb = n < 65535 ? n : 65535, ycap = 2368 / xb + 1;
   lincomb_multi_kernel<<<dim3(unsigned(xb), unsigned(yb < ycap ? yb : ycap)), 128, 0, st>>>(a, n, m);
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
+// Strassen leaf operands in the bf16x3 format (paco_lincomb_split): the same
+// signed sums as lincomb_multi, each written as two bf16 planes hi = bf16_rn(x),
+// lo = bf16_rn(x - hi) (x = hi + lo to 2^-17 relative); a one-term row is a
+// split copy.  Eight columns per thread: 2 x 16-byte loads per input, one
+// 16-byte store per plane; 4 bytes written per output element, as an fp32 sum.
+struct SplitArgs {
+  const float* in[kMultiIn];
+  int64_t ldi[kMultiIn];
+  __nv_bfloat16* hi[kMultiOut];
+  __nv_bfloat16* lo[kMultiOut];
+  int64_t ldo[kMultiOut];
+  int8_t coef[kMultiOut * kMultiIn];
+  int32_t nin, nout;
+};
+
+__device__ __forceinline__ uint32_t bf16x2_bits(__nv_bfloat16 a, __nv_bfloat16 b) {
+  return uint32_t(__bfloat16_as_ushort(a)) | (uint32_t(__bfloat16_as_ushort(b)) << 16);
+}
+
+__global__ void __launch_bounds__(128) lincomb_split_kernel(const SplitArgs a, int64_t n, int64_t m) {
+  const int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+  if (j >= m) return;
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
+    float x[kMultiIn][8];
+#pragma unroll
+    for (int q = 0; q < kMultiIn; ++q)
+      if (q < a.nin) {
+        const float4* p = reinterpret_cast<const float4*>(a.in[q] + i * a.ldi[q] + j);
+        const float4 u = __ldcs(p), w = __ldcs(p + 1);
+        x[q][0] = u.x; x[q][1] = u.y; x[q][2] = u.z; x[q][3] = u.w;
+        x[q][4] = w.x; x[q][5] = w.y; x[q][6] = w.z; x[q][7] = w.w;
+      }
+#pragma unroll
+    for (int o = 0; o < kMultiOut; ++o) {
+      if (o >= a.nout) break;
+      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int q = 0; q < kMultiIn; ++q) {
+        if (q >= a.nin) break;
+        const int c = a.coef[o * kMultiIn + q];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = c > 0 ? v[e] + x[q][e] : (c < 0 ? v[e] - x[q][e] : v[e]);
+      }
+      uint32_t h[4], l[4];
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) {
+        const __nv_bfloat16 h0 = __float2bfloat16_rn(v[e]), h1 = __float2bfloat16_rn(v[e + 1]);
+        h[e / 2] = bf16x2_bits(h0, h1);
+        l[e / 2] = bf16x2_bits(__float2bfloat16_rn(v[e] - __bfloat162float(h0)),
+                               __float2bfloat16_rn(v[e + 1] - __bfloat162float(h1)));
+      }
+      __stcs(reinterpret_cast<uint4*>(a.hi[o] + i * a.ldo[o] + j), make_uint4(h[0], h[1], h[2], h[3]));
+      __stcs(reinterpret_cast<uint4*>(a.lo[o] + i * a.ldo[o] + j), make_uint4(l[0], l[1], l[2], l[3]));
+    }
+  }
+}
+
+int launch_lincomb_split(cudaStream_t st, int64_t n, int64_t m, int nin, const void* const* ins, const int64_t* lds,
+                         int nout, void* const* his, void* const* los, const int64_t* ldo, const int32_t* coefs) {
+  if (n <= 0 || m <= 0 || nout == 0) return PACO_OK;
+  if (nin < 1 || nin > kMultiIn || nout < 0 || nout > kMultiOut) {
+    set_error("paco_lincomb_split: %d inputs (1..%d), %d outputs (0..%d)", nin, kMultiIn, nout, kMultiOut);
+    return PACO_ERR_ARG;
+  }
+  SplitArgs a{};
+  a.nin = nin;
+  a.nout = nout;
+  bool ok = m % 8 == 0;
+  for (int q = 0; q < nin; ++q) {
+    a.in[q] = static_cast<const float*>(ins[q]);
+    a.ldi[q] = lds[q];
+    ok = ok && lds[q] % 4 == 0 && reinterpret_cast<uintptr_t>(ins[q]) % 16 == 0;
+  }
+  for (int o = 0; o < nout; ++o) {
+    a.hi[o] = static_cast<__nv_bfloat16*>(his[o]);
+    a.lo[o] = static_cast<__nv_bfloat16*>(los[o]);
+    a.ldo[o] = ldo[o];
+    ok = ok && ldo[o] % 8 == 0 && reinterpret_cast<uintptr_t>(his[o]) % 16 == 0 &&
+         reinterpret_cast<uintptr_t>(los[o]) % 16 == 0;
+    for (int q = 0; q < nin; ++q) a.coef[o * kMultiIn + q] = int8_t(coefs[o * nin + q] > 0 ? 1 : (coefs[o * nin + q] < 0 ? -1 : 0));
+  }
+  if (!ok) {
+    set_error("paco_lincomb_split: views need 16-byte aligned starts and pitches and a column count %% 8 == 0");
+    return PACO_ERR_UNSUPPORTED;
+  }
+  KernelSpan ks(PACO_KT_LINCOMB, st);
+  const int64_t xb = (m / 8 + 127) / 128, yb = n < 65535 ? n : 65535, ycap = 2368 / xb + 1;
+  lincomb_split_kernel<<<dim3(unsigned(xb), unsigned(yb < ycap ? yb : ycap)), 128, 0, st>>>(a, n, m);
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;
 }

@@ -1019,11 +1019,19 @@ __device__ __forceinline__ void pair_tile(const TcArgs& a, int32_t t, int& q, in
 // RAW (with CV): the operands arrive as plain fp32 x; the tf32 MMA reads x itself
 // (the tensor core uses its top 19 bits: hi = trunc_tf32(x)) and the converters
 // form bf16(hi) and bf16(x - hi) -- 4 bytes of L2 traffic per operand element.
-template <int ST, bool FA, bool B2, bool CV = false, bool RAW = false>
+//
+// B3 (bf16x3): the operands arrive pre-split as bf16 planes hi = bf16(x), lo =
+// bf16(x - hi) (paco_lincomb_split); a stage holds 32 k of A hi / lo and of this
+// CTA's half of B^T hi / lo (four 8 KB SW64 tiles, the 3xTF32 stage geometry) and
+// the leader issues hi*hi, hi*lo, lo*hi as kind::f16 MMAs: no converter warps, and
+// per CTA a stage is 32 KB of TMA writes + 48 KB of operand reads against 768
+// clocks of MMA -- the tensor pipe, not shared memory, bounds it.
+template <int ST, bool FA, bool B2, bool CV = false, bool RAW = false, bool B3 = false>
 __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
     tc_pair_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
   using L = PairLayout<ST, FA, B2, CV>;
   constexpr int BK = L::BK, BN = L::BN;
+  constexpr int KSTEP = B3 ? 2 * BK : BK;  // k per stage
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::SMEM_BAR);
@@ -1124,8 +1132,8 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
             if (leader) mbar_expect_tx_relaxed(&full[s], 2 * L::STAGE_BYTES);
 #pragma unroll
             for (int o = 0; o < 2; ++o) {
-              tma_load_2d_pair(smem + L::a_off(s, o), &P.a[o], fb, P.a_col0[o] + kb * BK, arow);
-              tma_load_2d_pair(smem + L::b_off(s, o), &P.b[o], fb, P.b_col0[o] + kb * BK, brow);
+              tma_load_2d_pair(smem + L::a_off(s, o), &P.a[o], fb, P.a_col0[o] + kb * KSTEP, arow);
+              tma_load_2d_pair(smem + L::b_off(s, o), &P.b[o], fb, P.b_col0[o] + kb * KSTEP, brow);
             }
           }
         }
@@ -1162,13 +1170,18 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
                                     smem_desc_sw64(smem_u32(smem + L::a_off(s, 1)))};
             const uint64_t bd[2] = {smem_desc_sw64(smem_u32(smem + L::b_off(s, 0))),
                                     smem_desc_sw64(smem_u32(smem + L::b_off(s, 1)))};
+            // 32 bytes of a 64-byte K-major row per step: 8 fp32 (tf32 K = 8) or 16 bf16 (f16 K = 16)
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk)
 #pragma unroll
               for (int ps = 0; ps < 3; ++ps) {  // hi*hi, hi*lo, lo*hi
                 const int ao = ps == 2 ? 1 : 0, bo = ps == 1 ? 1 : 0;
-                umma_pair(d_tmem, ad[ao] + uint64_t(2 * kk), bd[bo] + uint64_t(2 * kk), L::IDESC,
-                          (kb | kk | ps) != 0);
+                if constexpr (B3)
+                  umma_pair_f16(d_tmem, ad[ao] + uint64_t(2 * kk), bd[bo] + uint64_t(2 * kk), L::IDESC_BF16,
+                                (kb | kk | ps) != 0);
+                else
+                  umma_pair(d_tmem, ad[ao] + uint64_t(2 * kk), bd[bo] + uint64_t(2 * kk), L::IDESC,
+                            (kb | kk | ps) != 0);
               }
           }
           umma_commit_pair(&empty[s]);  // both CTAs' stage s is free once these MMAs complete
@@ -2154,7 +2167,8 @@ int launch_tc_batch(int device, cudaStream_t stream, int count, const Presplit* 
 #define PACO_PAIR_ST 6
 #endif
 // Launch a tc_pair_kernel variant (mode 0: 3xTF32, 1: FA (S_r formed in the kernel),
-// 2: tf32 + 2 x bf16) over 256 x 256 tiles dealt to the 74 CTA pairs.
+// 2: tf32 + 2 x bf16, 3/4: ... with bf16 parts formed in the kernel, 5: bf16x3 on
+// pre-split bf16 planes) over 256 x 256 tiles dealt to the 74 CTA pairs.
 int run_pair(int device, cudaStream_t stream, const tc::TcMaps& maps, int count, int64_t n, int64_t m, int64_t k,
              int flags, int mode) {
   using L = tc::PairLayout<PACO_PAIR_ST>;
@@ -2166,21 +2180,23 @@ int run_pair(int device, cudaStream_t stream, const tc::TcMaps& maps, int count,
   args.overwrite = (flags & PACO_MM_OVERWRITE) ? 1 : 0;
   args.tiles_rb = int32_t((n + 255) / 256);
   args.tiles_nb = int32_t((m + L::BN - 1) / L::BN);
-  args.kblocks = int32_t((k + L::BK - 1) / L::BK);
+  const int kstep = mode == 5 ? 2 * L::BK : L::BK;
+  args.kblocks = int32_t((k + kstep - 1) / kstep);
   args.groups = 1;
   const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb * count;
   const int pairs = int(tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
-  auto kern = mode == 1   ? tc::tc_pair_kernel<PACO_PAIR_ST, true, false>
+  auto kern = mode == 5   ? tc::tc_pair_kernel<PACO_PAIR_ST, false, false, false, false, true>
+              : mode == 1 ? tc::tc_pair_kernel<PACO_PAIR_ST, true, false>
               : mode == 2 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true>
               : mode == 3 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true, true>
               : mode == 4 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true, true, true>
                           : tc::tc_pair_kernel<PACO_PAIR_ST, false, false>;
   const int threads = mode == 1   ? tc::PairLayout<PACO_PAIR_ST, true>::THREADS
-                      : mode >= 3 ? tc::PairLayout<PACO_PAIR_ST, false, true, true>::THREADS
+                      : mode == 3 || mode == 4 ? tc::PairLayout<PACO_PAIR_ST, false, true, true>::THREADS
                                   : L::THREADS;
   {
     static std::atomic<uint64_t> attr_set{0};
-    const uint64_t bit = uint64_t(1) << ((device & 15) * 4 + mode);
+    const uint64_t bit = uint64_t(1) << ((device & 7) * 8 + mode);
     if (!(attr_set.load() & bit)) {
       PACO_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM_ALLOC));
       attr_set.fetch_or(bit);
@@ -2537,6 +2553,67 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
   std::lock_guard<std::mutex> pl(g_pdl_mu);
   pdl_record(device, stream, count, ndst, dst, nullptr, ldc, n, m);
   return run_pair(device, stream, maps, count, n, m, k, 0, raw ? 4 : (cv ? 3 : 2));
+}
+
+// bf16x3 batch on CTA pairs: C[q] (+/-)= A[q] B[q] with A[q] = a_hi + a_lo (bf16
+// planes, n x k, pitch lda elements) and B[q]^T = b_hi + b_lo (m x k, pitch ldb);
+// hi*hi + hi*lo + lo*hi accumulate in fp32 TMEM; destinations as _multi.
+int launch_mm_bf16x3_multi(int device, cudaStream_t stream, int count, const void* const* a_hi,
+                           const void* const* a_lo, int64_t lda, const void* const* b_hi, const void* const* b_lo,
+                           int64_t ldb, const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc,
+                           int64_t n, int64_t m, int64_t k) {
+  using L = tc::PairLayout<PACO_PAIR_ST>;
+  constexpr int KSTEP = 2 * L::BK;  // 32 bf16 = one 64-byte swizzled row
+  if (count < 1 || count > tc::kMaxBatch || !a_hi || !a_lo || !b_hi || !b_lo || !ndst || !dst || !sign) {
+    set_error("paco_mm_bf16x3_multi: count=%d (1..%d) and every operand / destination array required", count,
+              tc::kMaxBatch);
+    return PACO_ERR_ARG;
+  }
+  if (n <= 0 || m <= 0 || k <= 0) return PACO_OK;
+  if (n > INT32_MAX || m > INT32_MAX || k > INT32_MAX) {
+    set_error("tcgen05 path: extents must fit int32");
+    return PACO_ERR_ARG;
+  }
+  int rc;
+  constexpr CUtensorMapSwizzle S64 = CU_TENSOR_MAP_SWIZZLE_64B;
+  constexpr CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32, B16 = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  static tc::TcMaps maps;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int q = 0; q < count; ++q) {
+    if (!pitch_ok(a_hi[q], lda, 2) || !pitch_ok(a_lo[q], lda, 2) || !pitch_ok(b_hi[q], ldb, 2) ||
+        !pitch_ok(b_lo[q], ldb, 2)) {
+      set_error("paco_mm_bf16x3_multi: operands need 16-byte aligned starts and row pitches");
+      return PACO_ERR_UNSUPPORTED;
+    }
+    if (ndst[q] < 1 || ndst[q] > 4) {
+      set_error("paco_mm_bf16x3_multi: problem %d has %d destinations (1..4)", q, ndst[q]);
+      return PACO_ERR_ARG;
+    }
+    tc::TcProb& P = maps.p[q];
+    if ((rc = make_map(&P.a[0], B16, 2, a_hi[q], n, k, lda, KSTEP, tc::BM, &P.a_col0[0], S64)) ||
+        (rc = make_map(&P.a[1], B16, 2, a_lo[q], n, k, lda, KSTEP, tc::BM, &P.a_col0[1], S64)) ||
+        (rc = make_map(&P.b[0], B16, 2, b_hi[q], m, k, ldb, KSTEP, L::BNH, &P.b_col0[0], S64)) ||
+        (rc = make_map(&P.b[1], B16, 2, b_lo[q], m, k, ldb, KSTEP, L::BNH, &P.b_col0[1], S64)))
+      return rc;
+    P.a2 = P.a[0];  // never loaded; valid maps for prefetch.tensormap
+    P.b2 = P.b[0];
+    P.ndst = ndst[q];
+    P.neg = 0;
+    for (int d = 0; d < ndst[q]; ++d) {
+      if (!c_ok(dst[4 * q + d], ldc, m)) {
+        set_error("paco_mm_bf16x3_multi: C needs a 16-byte aligned start, row pitch and row length");
+        return PACO_ERR_UNSUPPORTED;
+      }
+      if (sign[4 * q + d] < 0) P.neg |= 1u << d;
+      if ((rc = make_map(d == 0 ? &P.c : &P.cx[d - 1], F32, 4, dst[4 * q + d], n, m, ldc, L::EC, 32,
+                         d == 0 ? &P.c_col0 : &P.cx_col0[d - 1], S64)))
+        return rc;
+    }
+  }
+  std::lock_guard<std::mutex> pl(g_pdl_mu);
+  pdl_record(device, stream, count, ndst, dst, nullptr, ldc, n, m);
+  return run_pair(device, stream, maps, count, n, m, k, 0, 5);
 }
 
 int launch_tf32b2_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,

@@ -661,6 +661,77 @@ def _leaf_level_b2raw(A: View, Bt: View, dests, stream) -> None:
         t.record_stream(stream)
 
 
+def _split_all(src: View, table, transpose: bool, stream, keep: list) -> list:
+    """The seven S_r (table = S_TERMS, from A) or T_r^T (T_TERMS, from B^T) of a
+    leaf-level node as bf16x3 (hi, lo) plane pairs, all written by ONE
+    ``paco_lincomb_split`` pass over the four quadrants (one-term formulas are
+    split copies).  Returns [(hi, lo)] views of pitch h."""
+    h = src.rows // 2
+    names = ("00", "01", "10", "11")
+    quads = [_quad(src, _tquad(q) if transpose else q) for q in names]
+    planes = torch.empty((2, 7, h, h), dtype=torch.bfloat16, device=src.device)
+    keep.append(planes)
+    coefs = []
+    for r in range(1, 8):
+        row = [0] * 4
+        for c, q in table[r]:
+            row[names.index(q)] = c
+        coefs += row
+    his = [planes[0, r].data_ptr() for r in range(7)]
+    los = [planes[1, r].data_ptr() for r in range(7)]
+    nat.check(nat.load().paco_lincomb_split(
+        src.device, stream.cuda_stream, h, h, 4, (ctypes.c_void_p * 4)(*[v.ptr for v in quads]),
+        (ctypes.c_int64 * 4)(*[v.ld for v in quads]), 7, (ctypes.c_void_p * 7)(*his), (ctypes.c_void_p * 7)(*los),
+        (ctypes.c_int64 * 7)(*([h] * 7)), (ctypes.c_int32 * 28)(*coefs)))
+    return list(zip(his, los))
+
+
+def _leaf_level_b3(A: View, Bt: View, dests, stream) -> None:
+    """Leaf-level node, B given transposed, leaves in the bf16x3 format: the seven
+    S_r and T_r^T are written as bf16 (hi, lo) planes by one
+    ``paco_lincomb_split`` pass per side, and the seven products are one
+    ``paco_mm_bf16x3_multi`` launch (hi*hi + hi*lo + lo*hi on kind::f16, fp32
+    accumulation) whose epilogues reduce-add each product with its signs into
+    its C blocks (M_DESTS)."""
+    h = A.rows // 2
+    dev = A.device
+    keep = []
+    S_ = _split_all(A, S_TERMS, False, stream, keep)
+    T_ = _split_all(Bt, T_TERMS, True, stream, keep)
+    ndst = (ctypes.c_int32 * 7)()
+    dst = (ctypes.c_void_p * 28)()
+    sign = (ctypes.c_int32 * 28)()
+    ld = None
+    for r in range(1, 8):
+        targets = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
+        if len(targets) > 4:
+            raise ValueError("a leaf product folds into at most 4 C blocks")
+        ndst[r - 1] = len(targets)
+        for d, (v, sg) in enumerate(targets):
+            dst[4 * (r - 1) + d], sign[4 * (r - 1) + d] = v.ptr, sg
+            if ld is None:
+                ld = v.ld
+            elif v.ld != ld:
+                raise ValueError("destinations must share one row pitch")
+    arr = lambda vs: (ctypes.c_void_p * 7)(*vs)  # noqa: E731
+    nat.check(nat.load().paco_mm_bf16x3_multi(dev, stream.cuda_stream, 7, arr([a for a, _ in S_]),
+                                              arr([a for _, a in S_]), h, arr([b for b, _ in T_]),
+                                              arr([b for _, b in T_]), h, ndst, dst, sign, ld, h, h, h))
+    for t in keep:
+        t.record_stream(stream)
+
+
+def _default_leaf(n: int, base: int):
+    """The leaf-level routine of the single-GPU fp32 Strassen path (B transposed
+    once): bf16x3 (LEAF_BF16X3, leaf blocks a multiple of 8) or the raw-operand
+    tf32 + 2 x bf16 format."""
+    while n > base and n % 2 == 0:
+        if _leaf_level(n, base):
+            return _leaf_level_b3 if LEAF_BF16X3 and (n // 2) % 8 == 0 else _leaf_level_b2raw
+        n //= 2
+    return _leaf_level_b2raw
+
+
 def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream, leaf=None) -> None:
     """dests (+/-)= A x B for the fp32 (3xTF32) ring with B given as B^T (the
     fused-producer path): S_r from A's quadrants and T_r^T from B^T's, formed
@@ -765,7 +836,7 @@ def strassen_into(A: View, B: View, dests, base: int, stream) -> bool:
         return True
     if TF32B2 and TF32B2_RAW and A.ptr % 16 == 0 and A.ld % 4 == 0 and _b2raw_ok(n, base):
         # the default single-GPU leaves: plain fp32 operands, B transposed once
-        _strassen_tc_fused_t(A, _transpose(B, stream), dests, base, stream, leaf=_leaf_level_b2raw)
+        _strassen_tc_fused_t(A, _transpose(B, stream), dests, base, stream, leaf=_default_leaf(n, base))
         return True
     if _leaf_level(n, base) and len(dests) > 2:
         return False
@@ -800,6 +871,12 @@ TF32B2_CONVERT = True
 # one lincomb_multi pass per node side, B transposed once; the kernel forms both bf16
 # parts): cfg5 23.8-25.4 ms vs 27.5-28.2 with the split pass (tools/cfg5_variants.py)
 TF32B2_RAW = True
+# ... or (the default where leaf blocks are a multiple of 8) in the bf16x3 format:
+# S_r / T_r^T written as bf16 hi / lo planes by one paco_lincomb_split pass per node
+# side, products hi*hi + hi*lo + lo*hi all on kind::f16 (paco_mm_bf16x3_multi): per CTA
+# a 32-deep stage is 32 KB of TMA writes + 48 KB of MMA reads against 768 MMA clocks,
+# so the leaves are tensor-bound instead of shared-memory bound
+LEAF_BF16X3 = True
 
 
 def _pair_batch(n: int, m: int, count: int) -> bool:
@@ -818,7 +895,7 @@ def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stre
         launch_fill(nat.SR_F32, stream, C)
         aligned = A.ptr % 16 == 0 and (A.ld * 4) % 16 == 0
         if TF32B2 and TF32B2_RAW and aligned and _b2raw_ok(C.rows, base):
-            _strassen_tc_fused_t(A, _transpose(B, stream), [(C, 1)], base, stream, leaf=_leaf_level_b2raw)
+            _strassen_tc_fused_t(A, _transpose(B, stream), [(C, 1)], base, stream, leaf=_default_leaf(C.rows, base))
         elif FUSED_PRODUCER and _fused_producer_ok(C.rows, base) and aligned:
             _strassen_tc_fused_t(A, _transpose(B, stream), [(C, 1)], base, stream)
         else:

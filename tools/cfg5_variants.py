@@ -1,6 +1,6 @@
-"""cfg5 (Strassen fp32 n=16384, 2 levels) per leaf format: 3xTF32 on CTA pairs,
-tf32 + 2 x bf16 (pre-split bf16(hi)), tf32 + 2 x bf16 with bf16(hi) formed in the
-kernel -- step time, per-kernel-family time, error on sampled rows vs f64."""
+"""cfg5 (Strassen fp32 n=16384, 2 levels) per leaf format: bf16x3 on pre-split
+planes (default) vs tf32 + 2 x bf16 on raw fp32 operands -- step time,
+per-kernel-family time, error on sampled rows vs f64."""
 import json
 import os
 import sys
@@ -18,9 +18,9 @@ b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
 rows = torch.arange(0, n, n // 64, device="cuda")
 ref = a[rows].double() @ b.double()
 res = {}
-for name, b2, cv, raw in (("3xtf32", False, True, False), ("tf32b2_cv", True, True, False),
-                          ("tf32b2_raw", True, True, True), ("3xtf32_again", False, True, False)):
-    S.TF32B2, S.TF32B2_CONVERT, S.TF32B2_RAW = b2, cv, raw
+for name, b2, cv, raw, b3 in (("bf16x3", True, True, True, True), ("tf32b2_raw", True, True, True, False),
+                              ("bf16x3_again", True, True, True, True)):
+    S.TF32B2, S.TF32B2_CONVERT, S.TF32B2_RAW, S.LEAF_BF16X3 = b2, cv, raw, b3
     for _ in range(2):
         c = S.strassen_seq(a, b, n, base=n // 4)
     torch.cuda.synchronize()
