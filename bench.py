@@ -397,39 +397,57 @@ def measure_config(cfg, dev, args, peaks, probes):
                                                     ("elementwise", nat.KT_ELEMENTWISE))}
         per_step = {k_: {"ms": v[0] / 3, "launches": v[1] // 3} for k_, v in fam.items()}
         alg = 49 * 2 * 4096 ** 3 + 18 * 8192 ** 2 + 7 * 18 * 4096 ** 2
-        tf32_peak = peaks["bf16_tflops"] / 2
-        b2 = S.TF32B2 and S._pair_batch(4096, 4096, 7)
-        # tensor work in tf32-equivalent flop (a bf16 MMA runs at twice the tf32 rate):
-        # 3xTF32: 3 tf32 products; tf32 + 2 x bf16: 1 tf32 product + 2 bf16 products = 2 tf32-equivalents
-        per_product = 2 * 4096 ** 3 * (2 if b2 else 3)
-        mma = 49 * per_product
+        lw = leaf_work(S, peaks)
+        mma = 49 * lw["per_product"]
         leaf_ms = per_step["tc_gemm"]["ms"]
         leaf_launch_ms = leaf_ms / max(1, per_step["tc_gemm"]["launches"])
         leaf_flop = mma / max(1, per_step["tc_gemm"]["launches"])   # one launch = 7 products of 4096^3
         achieved = leaf_flop / leaf_launch_ms / 1e9
-        traffic, src = ncu_traffic("r2_tf32b2_raw_ncu.json")
-        fmt = ("tf32 + 2 x bf16 split products (hi*hi on kind::tf32, hi*lo + lo*hi on kind::f16, bf16(hi) formed "
-               "in the kernel), fp32 accumulation" if b2 else "3xTF32 split products, fp32 accumulation")
+        traffic, src = ncu_traffic(lw["ncu"])
         out.update(ms=ms, value=alg / ms / 1e6, unit="Gop/s", ops_per_step=alg, steps=steps, warmup=warmup,
                    classic_equivalent_gop_s=2.0 * n ** 3 / ms / 1e6,
                    gpu_launches_per_step=sum(v["launches"] for v in per_step.values()),
-                   kernels_per_step=per_step, leaf_format=fmt,
+                   kernels_per_step=per_step, leaf_format=lw["format"],
                    step="strassen_seq(A, B, 16384, base=4096): 2 Strassen levels, 49 leaf products of 4096^3 on CTA "
                         "pairs (tcgen05 cta_group::2; 7 batched launches), C combination fused into the leaf epilogues",
                    l2="A, B 1 GiB each > 126 MB L2 (no flush)",
                    roofline={"bound": "tensor", "kernel": "tc_pair_kernel (Strassen leaves on CTA pairs)",
-                             "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s (tf32-equivalent)",
-                             "frac": achieved / tf32_peak,
-                             "achieved_note": ("tensor work of one launch (7 products of 4096^3, in tf32-equivalent "
-                                               "flop: " + ("2" if b2 else "3") + " x 2 x 4096^3 each) / its average "
-                                               "CUDA-event duration inside the step"),
-                             "step_frac": mma / ms / 1e9 / tf32_peak,
+                             "achieved": achieved, "peak": lw["peak"], "unit": lw["unit"],
+                             "frac": achieved / lw["peak"], "frac_burst": achieved / lw["peak_burst"],
+                             "achieved_note": ("tensor work of one launch (7 products of 4096^3: " + lw["note"] +
+                                               ") / its average CUDA-event duration inside the step"),
+                             "step_frac": mma / ms / 1e9 / lw["peak"],
                              "step_note": "whole step: 49 leaf products' tensor work / step time",
-                             "peak_source": f"TF32 dense = bf16_tflops / 2 {peaks['source']} (bf16 MMAs count half)",
+                             "peak_source": lw["peak_source"],
                              "traffic": traffic, "traffic_source": src},
                    clocks=clk.summary())
         return out
     raise ValueError(cfg)
+
+
+def leaf_work(S, peaks):
+    """Tensor work of one cfg5 leaf product (4096^3) in the leaf format the library
+    runs, and the peak it is held to.  The leaf launches run inside a ~20 ms step
+    repeated back to back, so the denominator is the SUSTAINED bf16 figure of
+    MEASURED_PEAKS.json (B200_PROFILING: burst for a kernel timed alone, sustained
+    for one inside a long step); frac_burst is reported beside it."""
+    p3 = 2 * 4096 ** 3
+    if S.LEAF_BF16X3:
+        return {"per_product": 3 * p3, "unit": "TFLOP/s (bf16)", "peak": peaks["bf16_tflops_sustained"],
+                "peak_burst": peaks["bf16_tflops"], "ncu": "r2_bf16x3_ncu.json",
+                "note": "3 bf16 products (hi*hi, hi*lo, lo*hi) x 2 x 4096^3 each",
+                "format": ("bf16x3: operands as bf16 hi/lo planes (one paco_lincomb_split pass per node side), "
+                           "hi*hi + hi*lo + lo*hi on kind::f16, fp32 accumulation"),
+                "peak_source": (f"bf16_tflops_sustained {peaks['source']} (kernel inside a long step; "
+                                f"burst {peaks['bf16_tflops']:.1f} gives frac_burst)")}
+    b2 = S.TF32B2
+    return {"per_product": (2 if b2 else 3) * p3, "unit": "TFLOP/s (tf32-equivalent)",
+            "peak": peaks["bf16_tflops_sustained"] / 2, "peak_burst": peaks["bf16_tflops"] / 2,
+            "ncu": "r2_tf32b2_raw_ncu.json",
+            "note": ("2" if b2 else "3") + " tf32-equivalent products x 2 x 4096^3 each (a bf16 MMA counts half)",
+            "format": ("tf32 + 2 x bf16 split products, fp32 accumulation" if b2
+                       else "3xTF32 split products, fp32 accumulation"),
+            "peak_source": f"TF32 dense = bf16_tflops_sustained / 2 {peaks['source']}"}
 
 
 def e2e_numpy_cfg2(dev, steps):
@@ -724,7 +742,7 @@ class MultiGPU:
             self.step = lambda: self.ex.run(self.A, self.B)
             self.launches_per_step = None
             self.ops_per_step = 49 * 2 * 4096 ** 3 + 18 * 8192 ** 2 + 7 * 18 * 4096 ** 2
-            self.dtype = "f32 (3xTF32)"
+            self.dtype = "f32 (bf16x3 leaves)" if S.LEAF_BF16X3 else "f32 (tf32 + 2 x bf16 leaves)"
             self.plan_desc = (f"{world} GPUs, strassen_paco_partition(16384, p={world}, base=4096, split_leftover): "
                               f"{len(self.ex.nodes)} node(s) + {len(self.ex.pieces)} leaf piece(s) on this rank; "
                               "signed partial C folded by the leaf epilogues, then one NCCL reduce-scatter")
@@ -748,14 +766,13 @@ class MultiGPU:
                     "frac": gbs / self.peaks["hbm_gbs"], "per": "GPU (rank 0's algorithmic bytes / step time)",
                     "peak_source": f"hbm_gbs {self.peaks['source']}"}
         from paper_2011_01441_b200 import strassen as S
-        passes = 2 if S.TF32B2 else 3   # tf32-equivalent products per leaf (tf32 + 2 x bf16 vs 3xTF32)
-        mma = passes * 49 * 2 * 4096 ** 3 / self.world
+        lw = leaf_work(S, self.peaks)
+        mma = 49 * lw["per_product"] / self.world
         tf = mma / (ms * 1e-3) / 1e12
-        peak = self.peaks["bf16_tflops"] / 2
-        return {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s (tf32-equivalent)",
-                "frac": tf / peak,
+        return {"bound": "tensor", "achieved": tf, "peak": lw["peak"], "unit": lw["unit"],
+                "frac": tf / lw["peak"], "frac_burst": tf / lw["peak_burst"],
                 "per": "GPU (leaf tensor work / N / step time, reduce-scatter included)",
-                "peak_source": f"TF32 dense = bf16_tflops / 2 {self.peaks['source']}"}
+                "peak_source": lw["peak_source"]}
 
     def e2e(self, steps):
         """The same step from pinned host operands, host wall clock, max over ranks."""

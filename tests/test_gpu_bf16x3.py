@@ -104,9 +104,12 @@ def test_bf16x3_rejects_misaligned():
     assert rc != 0
 
 
-def test_strassen_bf16x3_vs_tf32b2(monkeypatch):
-    """cfg5's shape at half size (8192, 2 levels): the bf16x3 leaves (default) and the
-    tf32 + 2 x bf16 leaves both within 1e-4 of the f64 product."""
+@pytest.mark.parametrize("overlap", [True, False])
+def test_strassen_bf16x3_vs_tf32b2(monkeypatch, overlap):
+    """cfg5's shape at half size (8192, 2 levels): the bf16x3 leaves (default; leaf
+    operands formed on the side stream or in line) and the tf32 + 2 x bf16 leaves
+    all within 1e-4 of the f64 product."""
+    monkeypatch.setattr(S, "B3_OVERLAP", overlap)
     n, base = 8192, 2048
     g = torch.Generator(device="cuda").manual_seed(8)
     a = torch.rand(n, n, device="cuda", generator=g) * 2 - 1

@@ -18,9 +18,9 @@ b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
 rows = torch.arange(0, n, n // 64, device="cuda")
 ref = a[rows].double() @ b.double()
 res = {}
-for name, b2, cv, raw, b3 in (("bf16x3", True, True, True, True), ("tf32b2_raw", True, True, True, False),
-                              ("bf16x3_again", True, True, True, True)):
-    S.TF32B2, S.TF32B2_CONVERT, S.TF32B2_RAW, S.LEAF_BF16X3 = b2, cv, raw, b3
+for name, b3, ov in (("bf16x3", True, True), ("bf16x3_inline", True, False), ("tf32b2_raw", False, False),
+                     ("bf16x3_again", True, True)):
+    S.LEAF_BF16X3, S.B3_OVERLAP = b3, ov
     for _ in range(2):
         c = S.strassen_seq(a, b, n, base=n // 4)
     torch.cuda.synchronize()
