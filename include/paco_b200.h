@@ -289,7 +289,8 @@ int paco_mm_tf32b2_multi(int device, void* stream, int count, const void* const*
                          const void* const* b_l16, int64_t ldb, const int32_t* ndst, void* const* dst,
                          const int32_t* sign, int64_t ldc, int64_t n, int64_t m, int64_t k);
 
-/* Strassen leaf operands in the bf16x3 format: like paco_lincomb_multi, but
+/* Strassen leaf operands in the bf16x3 format: like paco_lincomb_multi (but up
+ * to 8 inputs: a leaf node's operands straight from the level-0 blocks), and
  * output o is written as two bf16 planes his[o] = bf16_rn(x), los[o] =
  * bf16_rn(x - his[o]) (pitch ldo[o] elements, shared by both planes); a
  * one-term row is a split copy.  16-byte aligned views, m % 8 == 0. */

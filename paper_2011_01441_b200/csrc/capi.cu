@@ -314,7 +314,7 @@ int paco_lincomb_split(int device, void* stream, int64_t n, int64_t m, int nin, 
     set_error("paco_lincomb_split: null arrays");
     return PACO_ERR_ARG;
   }
-  for (int q = 0; q < nin && q < 4; ++q) PACO_TRY(check_view("in", ins[q], lds[q], n, m));
+  for (int q = 0; q < nin && q < 8; ++q) PACO_TRY(check_view("in", ins[q], lds[q], n, m));
   for (int o = 0; o < nout && o < 8; ++o) {
     PACO_TRY(check_view("hi", his[o], ldo[o], n, m));
     PACO_TRY(check_view("lo", los[o], ldo[o], n, m));

@@ -311,13 +311,17 @@ int launch_lincomb_multi(cudaStream_t st, int64_t n, int64_t m, int nin, const v
 // lo = bf16_rn(x - hi) (x = hi + lo to 2^-17 relative); a one-term row is a
 // split copy.  Eight columns per thread: 2 x 16-byte loads per input, one
 // 16-byte store per plane; 4 bytes written per output element, as an fp32 sum.
+// Up to 8 inputs: a leaf-level node's operands straight from the level-0 blocks
+// (S_r's quadrant q = sum of its terms' sub-quadrants q), skipping the
+// level-1 fp32 sums.
+constexpr int kSplitIn = 8;
 struct SplitArgs {
-  const float* in[kMultiIn];
-  int64_t ldi[kMultiIn];
+  const float* in[kSplitIn];
+  int64_t ldi[kSplitIn];
   __nv_bfloat16* hi[kMultiOut];
   __nv_bfloat16* lo[kMultiOut];
   int64_t ldo[kMultiOut];
-  int8_t coef[kMultiOut * kMultiIn];
+  int8_t coef[kMultiOut * kSplitIn];
   int32_t nin, nout;
 };
 
@@ -325,13 +329,14 @@ __device__ __forceinline__ uint32_t bf16x2_bits(__nv_bfloat16 a, __nv_bfloat16 b
   return uint32_t(__bfloat16_as_ushort(a)) | (uint32_t(__bfloat16_as_ushort(b)) << 16);
 }
 
+template <int NI>
 __global__ void __launch_bounds__(128) lincomb_split_kernel(const SplitArgs a, int64_t n, int64_t m) {
   const int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
   if (j >= m) return;
   for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
-    float x[kMultiIn][8];
+    float x[NI][8];
 #pragma unroll
-    for (int q = 0; q < kMultiIn; ++q)
+    for (int q = 0; q < NI; ++q)
       if (q < a.nin) {
         const float4* p = reinterpret_cast<const float4*>(a.in[q] + i * a.ldi[q] + j);
         const float4 u = __ldcs(p), w = __ldcs(p + 1);
@@ -343,9 +348,9 @@ __global__ void __launch_bounds__(128) lincomb_split_kernel(const SplitArgs a, i
       if (o >= a.nout) break;
       float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int q = 0; q < kMultiIn; ++q) {
+      for (int q = 0; q < NI; ++q) {
         if (q >= a.nin) break;
-        const int c = a.coef[o * kMultiIn + q];
+        const int c = a.coef[o * kSplitIn + q];
 #pragma unroll
         for (int e = 0; e < 8; ++e) v[e] = c > 0 ? v[e] + x[q][e] : (c < 0 ? v[e] - x[q][e] : v[e]);
       }
@@ -366,8 +371,8 @@ __global__ void __launch_bounds__(128) lincomb_split_kernel(const SplitArgs a, i
 int launch_lincomb_split(cudaStream_t st, int64_t n, int64_t m, int nin, const void* const* ins, const int64_t* lds,
                          int nout, void* const* his, void* const* los, const int64_t* ldo, const int32_t* coefs) {
   if (n <= 0 || m <= 0 || nout == 0) return PACO_OK;
-  if (nin < 1 || nin > kMultiIn || nout < 0 || nout > kMultiOut) {
-    set_error("paco_lincomb_split: %d inputs (1..%d), %d outputs (0..%d)", nin, kMultiIn, nout, kMultiOut);
+  if (nin < 1 || nin > kSplitIn || nout < 0 || nout > kMultiOut) {
+    set_error("paco_lincomb_split: %d inputs (1..%d), %d outputs (0..%d)", nin, kSplitIn, nout, kMultiOut);
     return PACO_ERR_ARG;
   }
   SplitArgs a{};
@@ -385,7 +390,7 @@ int launch_lincomb_split(cudaStream_t st, int64_t n, int64_t m, int nin, const v
     a.ldo[o] = ldo[o];
     ok = ok && ldo[o] % 8 == 0 && reinterpret_cast<uintptr_t>(his[o]) % 16 == 0 &&
          reinterpret_cast<uintptr_t>(los[o]) % 16 == 0;
-    for (int q = 0; q < nin; ++q) a.coef[o * kMultiIn + q] = int8_t(coefs[o * nin + q] > 0 ? 1 : (coefs[o * nin + q] < 0 ? -1 : 0));
+    for (int q = 0; q < nin; ++q) a.coef[o * kSplitIn + q] = int8_t(coefs[o * nin + q] > 0 ? 1 : (coefs[o * nin + q] < 0 ? -1 : 0));
   }
   if (!ok) {
     set_error("paco_lincomb_split: views need 16-byte aligned starts and pitches and a column count %% 8 == 0");
@@ -393,7 +398,11 @@ int launch_lincomb_split(cudaStream_t st, int64_t n, int64_t m, int nin, const v
   }
   KernelSpan ks(PACO_KT_LINCOMB, st);
   const int64_t xb = (m / 8 + 127) / 128, yb = n < 65535 ? n : 65535, ycap = 2368 / xb + 1;
-  lincomb_split_kernel<<<dim3(unsigned(xb), unsigned(yb < ycap ? yb : ycap)), 128, 0, st>>>(a, n, m);
+  const dim3 grid(unsigned(xb), unsigned(yb < ycap ? yb : ycap));
+  if (nin <= 4)
+    lincomb_split_kernel<4><<<grid, 128, 0, st>>>(a, n, m);
+  else
+    lincomb_split_kernel<8><<<grid, 128, 0, st>>>(a, n, m);
   PACO_CUDA_TRY(cudaGetLastError());
   return PACO_OK;
 }

@@ -661,47 +661,58 @@ def _leaf_level_b2raw(A: View, Bt: View, dests, stream) -> None:
         t.record_stream(stream)
 
 
-def _split_all(src: View, table, transpose: bool, stream, keep: list) -> list:
-    """The seven S_r (table = S_TERMS, from A) or T_r^T (T_TERMS, from B^T) of a
-    leaf-level node as bf16x3 (hi, lo) plane pairs, all written by ONE
-    ``paco_lincomb_split`` pass over the four quadrants (one-term formulas are
-    split copies).  Returns [(hi, lo)] views of pitch h."""
-    h = src.rows // 2
+def _split_terms(terms, table, transpose: bool, stream, keep: list) -> list:
+    """The seven S_r (table = S_TERMS) or T_r^T (T_TERMS, transposed quadrant
+    names) of a leaf-level node whose operand is the signed sum of ``terms``
+    [(coef, View)] (one view, or up to two level-0 blocks: the operand's
+    quadrant q is then the sum of the terms' quadrants q, so the level-1 fp32
+    sum is never materialised), as bf16x3 (hi, lo) plane pairs, all written by
+    ONE ``paco_lincomb_split`` pass over the terms' quadrants (one-term formulas
+    are split copies).  Returns [(hi, lo)] addresses of pitch h."""
+    h = terms[0][1].rows // 2
     names = ("00", "01", "10", "11")
-    quads = [_quad(src, _tquad(q) if transpose else q) for q in names]
-    planes = torch.empty((2, 7, h, h), dtype=torch.bfloat16, device=src.device)
+    ins = [_quad(v, _tquad(q) if transpose else q) for _, v in terms for q in names]
+    planes = torch.empty((2, 7, h, h), dtype=torch.bfloat16, device=terms[0][1].device)
     keep.append(planes)
     coefs = []
     for r in range(1, 8):
-        row = [0] * 4
-        for c, q in table[r]:
-            row[names.index(q)] = c
+        row = [0] * len(ins)
+        for t, (c, _) in enumerate(terms):
+            for c2, q in table[r]:
+                row[4 * t + names.index(q)] = c * c2
         coefs += row
     his = [planes[0, r].data_ptr() for r in range(7)]
     los = [planes[1, r].data_ptr() for r in range(7)]
+    ni = len(ins)
     nat.check(nat.load().paco_lincomb_split(
-        src.device, stream.cuda_stream, h, h, 4, (ctypes.c_void_p * 4)(*[v.ptr for v in quads]),
-        (ctypes.c_int64 * 4)(*[v.ld for v in quads]), 7, (ctypes.c_void_p * 7)(*his), (ctypes.c_void_p * 7)(*los),
-        (ctypes.c_int64 * 7)(*([h] * 7)), (ctypes.c_int32 * 28)(*coefs)))
+        terms[0][1].device, stream.cuda_stream, h, h, ni, (ctypes.c_void_p * ni)(*[v.ptr for v in ins]),
+        (ctypes.c_int64 * ni)(*[v.ld for v in ins]), 7, (ctypes.c_void_p * 7)(*his), (ctypes.c_void_p * 7)(*los),
+        (ctypes.c_int64 * 7)(*([h] * 7)), (ctypes.c_int32 * (7 * ni))(*coefs)))
     return list(zip(his, los))
 
 
-def _leaf_level_b3(A: View, Bt: View, dests, stream, pre=None) -> None:
+def _split_all(src: View, table, transpose: bool, stream, keep: list) -> list:
+    """``_split_terms`` of a node whose operand is the single view ``src``."""
+    return _split_terms([(1, src)], table, transpose, stream, keep)
+
+
+def _leaf_level_b3(A: View, Bt: View, dests, stream, pre=None, h: int | None = None, dev: int | None = None) -> None:
     """Leaf-level node, B given transposed, leaves in the bf16x3 format: the seven
     S_r and T_r^T are written as bf16 (hi, lo) planes by one
     ``paco_lincomb_split`` pass per side, and the seven products are one
     ``paco_mm_bf16x3_multi`` launch (hi*hi + hi*lo + lo*hi on kind::f16, fp32
     accumulation) whose epilogues reduce-add each product with its signs into
     its C blocks (M_DESTS)."""
-    h = A.rows // 2
-    dev = A.device
+    if A is not None:
+        h, dev = A.rows // 2, A.device
     if pre is None:
         keep = []
         S_ = _split_all(A, S_TERMS, False, stream, keep)
         T_ = _split_all(Bt, T_TERMS, True, stream, keep)
-    else:  # formed on the side stream (_preform_b3): wait for that pass only
+    else:  # formed already (_preform_b3 on the side stream, or from level-0 blocks)
         S_, T_, keep, ev = pre
-        stream.wait_event(ev)
+        if ev is not None:
+            stream.wait_event(ev)
     ndst = (ctypes.c_int32 * 7)()
     dst = (ctypes.c_void_p * 28)()
     sign = (ctypes.c_int32 * 28)()
@@ -785,6 +796,18 @@ def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream, leaf=None)
     h = n // 2
     dev = A.device
     keep = []
+    kids = {r: [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]] for r in range(1, 8)}
+    if (leaf is _leaf_level_b3 and B3_DIRECT and _leaf_level(h, base) and h % 2 == 0 and (h // 2) % 8 == 0
+            and all(len(c) <= 2 for c in kids.values())):
+        # leaf-level children: form each child's bf16x3 operands straight from this
+        # node's quadrants (no level-1 fp32 sums), then its seven products
+        for r in range(1, 8):
+            child = kids[r]
+            ck = []
+            S_ = _split_terms([(c, _quad(A, q)) for c, q in S_TERMS[r]], S_TERMS, False, stream, ck)
+            T_ = _split_terms([(c, _quad(Bt, _tquad(q))) for c, q in T_TERMS[r]], T_TERMS, True, stream, ck)
+            _leaf_level_b3(None, None, child, stream, pre=(S_, T_, ck, None), h=h // 2, dev=dev)
+        return
     S_all = _form_all(A, S_TERMS, False, stream, keep)
     T_all = _form_all(Bt, T_TERMS, True, stream, keep)
     children = {}
@@ -935,6 +958,10 @@ LEAF_BF16X3 = True
 # 17.2-18.5 ms in line; tools/cfg5_variants.py) -- the step runs under sw_power_cap, so
 # concurrent HBM passes only move the clock down while the leaves run
 B3_OVERLAP = False
+# ... with each leaf-level node's operands formed straight from the level-0 blocks (8-input
+# paco_lincomb_split: S_r's quadrant q = the sum of its terms' quadrants q), so the level-1
+# fp32 sums are never written or re-read
+B3_DIRECT = True
 
 
 def _pair_batch(n: int, m: int, count: int) -> bool:

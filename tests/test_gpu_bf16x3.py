@@ -57,6 +57,25 @@ def test_lincomb_split_exact(shape):
         assert float(((rec - x.double()).abs() / x.double().abs().clamp_min(1e-30)).max()) <= 2.0 ** -16
 
 
+def test_lincomb_split_eight_inputs():
+    """Eight inputs (two level-0 blocks' quadrants): a leaf node's operands straight
+    from the level-0 blocks, e.g. (A00 + A11)'s sub-quadrant sums."""
+    n = m = 520
+    lib = nat.load()
+    st = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(8, n, m, device="cuda", generator=g)
+    q = [x[i] for i in range(8)]
+    rows = [[1, 0, 0, 1, -1, 0, 0, -1], [0, 0, 1, 1, 0, 0, 1, 1], [1, 0, 0, 0, 1, 0, 0, 0],
+            [0, 0, 0, 1, 0, 0, 0, -1], [1, 1, 0, 0, 1, 1, 0, 0], [-1, 0, 1, 0, -1, 0, 1, 0], [0, 1, 0, -1, 0, 0, 0, 0]]
+    his, los = _split(lib, st, q, rows)
+    torch.cuda.synchronize()
+    for h, lo, r in zip(his, los, rows):
+        want = sum(c * v.double() for c, v in zip(r, q) if c)
+        rec = h.double() + lo.double()
+        assert float((rec - want).abs().max() / want.abs().max()) <= 2.0 ** -15
+
+
 @pytest.mark.parametrize("shape", [(2048, 2048, 512, 4), (2000, 1800, 336, 7), (256, 256, 32, 1)])
 def test_bf16x3_pair_kernel_accuracy(shape):
     """Products vs float64 of the fp32 operands: two signed destinations per
@@ -104,11 +123,13 @@ def test_bf16x3_rejects_misaligned():
     assert rc != 0
 
 
-@pytest.mark.parametrize("overlap", [True, False])
-def test_strassen_bf16x3_vs_tf32b2(monkeypatch, overlap):
-    """cfg5's shape at half size (8192, 2 levels): the bf16x3 leaves (default; leaf
-    operands formed on the side stream or in line) and the tf32 + 2 x bf16 leaves
-    all within 1e-4 of the f64 product."""
+@pytest.mark.parametrize("direct,overlap", [(True, False), (False, True), (False, False)])
+def test_strassen_bf16x3_vs_tf32b2(monkeypatch, direct, overlap):
+    """cfg5's shape at half size (8192, 2 levels): the bf16x3 leaves (default: leaf
+    operands straight from the level-0 blocks; or from level-1 fp32 sums, on the
+    side stream or in line) and the tf32 + 2 x bf16 leaves all within 1e-4 of the
+    f64 product."""
+    monkeypatch.setattr(S, "B3_DIRECT", direct)
     monkeypatch.setattr(S, "B3_OVERLAP", overlap)
     n, base = 8192, 2048
     g = torch.Generator(device="cuda").manual_seed(8)

@@ -18,9 +18,9 @@ b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
 rows = torch.arange(0, n, n // 64, device="cuda")
 ref = a[rows].double() @ b.double()
 res = {}
-for name, b3, ov in (("bf16x3", True, True), ("bf16x3_inline", True, False), ("tf32b2_raw", False, False),
-                     ("bf16x3_again", True, True)):
-    S.LEAF_BF16X3, S.B3_OVERLAP = b3, ov
+for name, b3, direct in (("bf16x3_direct", True, True), ("bf16x3_level1", True, False), ("tf32b2_raw", False, False),
+                         ("bf16x3_direct_again", True, True)):
+    S.LEAF_BF16X3, S.B3_DIRECT = b3, direct
     for _ in range(2):
         c = S.strassen_seq(a, b, n, base=n // 4)
     torch.cuda.synchronize()

@@ -43,5 +43,9 @@ for j, t in enumerate(ts):
           f" med {np.nanmedian(e1_first):.2f}"
           f" | last stores issued min {np.nanmin(last_e1):.2f} med {np.nanmedian(last_e1):.2f} max {np.nanmax(last_e1):.2f}"
           f" | exit min {np.nanmin(life[:, 2]):.2f} med {np.nanmedian(life[:, 2]):.2f} max {np.nanmax(life[:, 2]):.2f}")
+    print("   producer: first claim med %.2f, B issued med %.2f | tile0: P0 first A load %.2f, P1 last A load %.2f, "
+          "M0 stage ready %.2f, M1 mma issued %.2f, E0 acc ready %.2f, E1 stores issued %.2f (medians)"
+          % tuple([np.nanmedian(life[:, 3]), np.nanmedian(life[:, 4])] + [np.nanmedian(tiles[:, 0, f]) for f in range(6)]))
+    print("   tile1: " + " ".join("%.2f" % np.nanmedian(tiles[:, 1, f]) for f in range(6)))
     ntiles = np.sum(~np.isnan(tiles[:, :, 4]), axis=1)
     print("   tiles per CTA (first 15 traced):", np.bincount(ntiles))
