@@ -84,13 +84,14 @@ def _raw_worker(rank, world, port, q):
     from paper_2011_01441_b200 import strassen as S
     from paper_2011_01441_b200.distributed import CudaStrassenOps, DistributedStrassen
     calls = []
-    leaf = S._leaf_level_b2raw
+    name = "_leaf_level_b3" if S.LEAF_BF16X3 else "_leaf_level_b2raw"   # the single-GPU default leaves
+    leaf = getattr(S, name)
 
     def counted(*a, **k):
         calls.append(1)
         return leaf(*a, **k)
 
-    S._leaf_level_b2raw = counted
+    setattr(S, name, counted)
     try:
         n, base = 8192, 2048
         g = torch.Generator(device="cuda").manual_seed(7)
@@ -111,8 +112,9 @@ def _raw_worker(rank, world, port, q):
 
 
 def test_distributed_strassen_raw_leaves():
-    """Rank nodes big enough for the CTA-pair batch take the same raw-operand
-    tf32 + 2 x bf16 leaves as the single-GPU path (strassen.strassen_into)."""
+    """Rank nodes big enough for the CTA-pair batch take the same leaves as the
+    single-GPU path (strassen.strassen_into: bf16x3, or the raw-operand tf32 +
+    2 x bf16 format)."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
