@@ -308,6 +308,14 @@ int paco_mm_bf16x3_multi(int device, void* stream, int count, const void* const*
                          const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc, int64_t n,
                          int64_t m, int64_t k);
 
+/* The same batch with B[q] given in its own k x m layout (b_hi[q] + b_lo[q], pitch
+ * ldb; MN-major operand tiles): Strassen's T_r planes formed from B's quadrants
+ * with no transpose pass.  16-byte aligned planes and row pitches. */
+int paco_mm_bf16x3_multi_bn(int device, void* stream, int count, const void* const* a_hi, const void* const* a_lo,
+                            int64_t lda, const void* const* b_hi, const void* const* b_lo, int64_t ldb,
+                            const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc, int64_t n,
+                            int64_t m, int64_t k);
+
 /* dst (cols x rows, pitch ld_dst) = src^T (rows x cols, pitch ld_src); 4- or
  * 8-byte elements.  Strassen transposes B once so every T_r^T operand of the
  * fused leaves is a K-major view. */

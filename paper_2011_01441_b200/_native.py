@@ -101,6 +101,9 @@ SIGNATURES = {
     "paco_mm_bf16x3_multi": (_int, [_int, _vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64,
                                     ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, ctypes.POINTER(ctypes.c_int32),
                                     ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
+    "paco_mm_bf16x3_multi_bn": (_int, [_int, _vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64,
+                                       ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, ctypes.POINTER(ctypes.c_int32),
+                                       ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
     "paco_transpose": (_int, [_int, _vp, _int, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_copy2d": (_int, [_int, _vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "paco_host_register": (_int, [_vp, ctypes.c_size_t]),

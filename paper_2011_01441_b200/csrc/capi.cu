@@ -126,7 +126,7 @@ int launch_lincomb_split(cudaStream_t st, int64_t n, int64_t m, int nin, const v
 int launch_mm_bf16x3_multi(int device, cudaStream_t stream, int count, const void* const* a_hi,
                            const void* const* a_lo, int64_t lda, const void* const* b_hi, const void* const* b_lo,
                            int64_t ldb, const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc,
-                           int64_t n, int64_t m, int64_t k);
+                           int64_t n, int64_t m, int64_t k, int b_natural);
 int run_alu_probe(cudaStream_t st, int which, int iters, double* tpc, double* mhz);
 struct Box;
 }  // namespace paco
@@ -339,7 +339,25 @@ int paco_mm_bf16x3_multi(int device, void* stream, int count, const void* const*
   DeviceGuard dg;
   PACO_TRY(dg.use(device));
   return launch_mm_bf16x3_multi(device, static_cast<cudaStream_t>(stream), count, a_hi, a_lo, lda, b_hi, b_lo, ldb,
-                                ndst, dst, sign, ldc, n, m, k);
+                                ndst, dst, sign, ldc, n, m, k, 0);
+}
+
+int paco_mm_bf16x3_multi_bn(int device, void* stream, int count, const void* const* a_hi, const void* const* a_lo,
+                            int64_t lda, const void* const* b_hi, const void* const* b_lo, int64_t ldb,
+                            const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc, int64_t n,
+                            int64_t m, int64_t k) {
+  if (count >= 1 && count <= 8 && a_hi && a_lo && b_hi && b_lo && ndst && dst)
+    for (int q = 0; q < count; ++q) {
+      PACO_TRY(check_view("A_hi", a_hi[q], lda, n, k));
+      PACO_TRY(check_view("A_lo", a_lo[q], lda, n, k));
+      PACO_TRY(check_view("B_hi", b_hi[q], ldb, k, m));
+      PACO_TRY(check_view("B_lo", b_lo[q], ldb, k, m));
+      for (int d = 0; d < ndst[q] && d < 4; ++d) PACO_TRY(check_view("C", dst[4 * q + d], ldc, n, m));
+    }
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_mm_bf16x3_multi(device, static_cast<cudaStream_t>(stream), count, a_hi, a_lo, lda, b_hi, b_lo, ldb,
+                                ndst, dst, sign, ldc, n, m, k, 1);
 }
 
 int paco_mm_batch(int device, void* stream, int semiring, int count, const paco_mm_problem* problems) {

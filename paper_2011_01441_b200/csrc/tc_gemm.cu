@@ -1026,7 +1026,12 @@ __device__ __forceinline__ void pair_tile(const TcArgs& a, int32_t t, int& q, in
 // the leader issues hi*hi, hi*lo, lo*hi as kind::f16 MMAs: no converter warps, and
 // per CTA a stage is 32 KB of TMA writes + 48 KB of operand reads against 768
 // clocks of MMA -- the tensor pipe, not shared memory, bounds it.
-template <int ST, bool FA, bool B2, bool CV = false, bool RAW = false, bool B3 = false>
+//
+// BMN (with B3): B arrives in its own k x m layout (MN-major) instead of as B^T: a
+// stage's B tile per CTA is [32 k rows][128 n] as two SWIZZLE_128B boxes of 64
+// columns (128 B), read by the MMA through MN-major descriptors -- Strassen's T_r
+// planes are formed from B's quadrants directly, with no transpose pass.
+template <int ST, bool FA, bool B2, bool CV = false, bool RAW = false, bool B3 = false, bool BMN = false>
 __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
     tc_pair_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
   using L = PairLayout<ST, FA, B2, CV>;
@@ -1133,7 +1138,14 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
 #pragma unroll
             for (int o = 0; o < 2; ++o) {
               tma_load_2d_pair(smem + L::a_off(s, o), &P.a[o], fb, P.a_col0[o] + kb * KSTEP, arow);
-              tma_load_2d_pair(smem + L::b_off(s, o), &P.b[o], fb, P.b_col0[o] + kb * KSTEP, brow);
+              if constexpr (BMN) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j)  // [32 k][64 n] boxes: this CTA's 128 columns of B
+                  tma_load_2d_pair(smem + L::b_off(s, o) + j * (KSTEP * 128), &P.b[o], fb,
+                                   P.b_col0[o] + brow + 64 * j, kb * KSTEP);
+              } else {
+                tma_load_2d_pair(smem + L::b_off(s, o), &P.b[o], fb, P.b_col0[o] + kb * KSTEP, brow);
+              }
             }
           }
         }
@@ -1168,17 +1180,21 @@ __global__ void __launch_bounds__(PairLayout<ST, FA, B2, CV>::THREADS, 1)
           } else {
             const uint64_t ad[2] = {smem_desc_sw64(smem_u32(smem + L::a_off(s, 0))),
                                     smem_desc_sw64(smem_u32(smem + L::a_off(s, 1)))};
-            const uint64_t bd[2] = {smem_desc_sw64(smem_u32(smem + L::b_off(s, 0))),
-                                    smem_desc_sw64(smem_u32(smem + L::b_off(s, 1)))};
-            // 32 bytes of a 64-byte K-major row per step: 8 fp32 (tf32 K = 8) or 16 bf16 (f16 K = 16)
+            const uint64_t bd[2] = {BMN ? smem_desc_mn_sw128(smem_u32(smem + L::b_off(s, 0)), KSTEP)
+                                        : smem_desc_sw64(smem_u32(smem + L::b_off(s, 0))),
+                                    BMN ? smem_desc_mn_sw128(smem_u32(smem + L::b_off(s, 1)), KSTEP)
+                                        : smem_desc_sw64(smem_u32(smem + L::b_off(s, 1)))};
+            // 32 bytes of a 64-byte K-major row per step: 8 fp32 (tf32 K = 8) or 16 bf16 (f16 K = 16);
+            // MN-major B: 16 k rows of 128 B per step
+            constexpr uint64_t BADV = BMN ? 8 * 16 : 2;
+            constexpr uint32_t IDB3 = L::IDESC_BF16 | (BMN ? (1u << 16) : 0u);
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk)
 #pragma unroll
               for (int ps = 0; ps < 3; ++ps) {  // hi*hi, hi*lo, lo*hi
                 const int ao = ps == 2 ? 1 : 0, bo = ps == 1 ? 1 : 0;
                 if constexpr (B3)
-                  umma_pair_f16(d_tmem, ad[ao] + uint64_t(2 * kk), bd[bo] + uint64_t(2 * kk), L::IDESC_BF16,
-                                (kb | kk | ps) != 0);
+                  umma_pair_f16(d_tmem, ad[ao] + uint64_t(2 * kk), bd[bo] + BADV * kk, IDB3, (kb | kk | ps) != 0);
                 else
                   umma_pair(d_tmem, ad[ao] + uint64_t(2 * kk), bd[bo] + uint64_t(2 * kk), L::IDESC,
                             (kb | kk | ps) != 0);
@@ -2180,12 +2196,13 @@ int run_pair(int device, cudaStream_t stream, const tc::TcMaps& maps, int count,
   args.overwrite = (flags & PACO_MM_OVERWRITE) ? 1 : 0;
   args.tiles_rb = int32_t((n + 255) / 256);
   args.tiles_nb = int32_t((m + L::BN - 1) / L::BN);
-  const int kstep = mode == 5 ? 2 * L::BK : L::BK;
+  const int kstep = mode >= 5 ? 2 * L::BK : L::BK;
   args.kblocks = int32_t((k + kstep - 1) / kstep);
   args.groups = 1;
   const int64_t tiles = int64_t(args.tiles_rb) * args.tiles_nb * count;
   const int pairs = int(tiles < kNumSMs / 2 ? tiles : kNumSMs / 2);
-  auto kern = mode == 5   ? tc::tc_pair_kernel<PACO_PAIR_ST, false, false, false, false, true>
+  auto kern = mode == 6   ? tc::tc_pair_kernel<PACO_PAIR_ST, false, false, false, false, true, true>
+              : mode == 5 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, false, false, false, true>
               : mode == 1 ? tc::tc_pair_kernel<PACO_PAIR_ST, true, false>
               : mode == 2 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true>
               : mode == 3 ? tc::tc_pair_kernel<PACO_PAIR_ST, false, true, true>
@@ -2558,10 +2575,11 @@ int launch_mm_tf32b2_multi(int device, cudaStream_t stream, int count, const voi
 // bf16x3 batch on CTA pairs: C[q] (+/-)= A[q] B[q] with A[q] = a_hi + a_lo (bf16
 // planes, n x k, pitch lda elements) and B[q]^T = b_hi + b_lo (m x k, pitch ldb);
 // hi*hi + hi*lo + lo*hi accumulate in fp32 TMEM; destinations as _multi.
+// b_natural: B[q] given as k x m planes (pitch ldb) instead of B^T (MN-major tiles).
 int launch_mm_bf16x3_multi(int device, cudaStream_t stream, int count, const void* const* a_hi,
                            const void* const* a_lo, int64_t lda, const void* const* b_hi, const void* const* b_lo,
                            int64_t ldb, const int32_t* ndst, void* const* dst, const int32_t* sign, int64_t ldc,
-                           int64_t n, int64_t m, int64_t k) {
+                           int64_t n, int64_t m, int64_t k, int b_natural) {
   using L = tc::PairLayout<PACO_PAIR_ST>;
   constexpr int KSTEP = 2 * L::BK;  // 32 bf16 = one 64-byte swizzled row
   if (count < 1 || count > tc::kMaxBatch || !a_hi || !a_lo || !b_hi || !b_lo || !ndst || !dst || !sign) {
@@ -2592,10 +2610,16 @@ int launch_mm_bf16x3_multi(int device, cudaStream_t stream, int count, const voi
     }
     tc::TcProb& P = maps.p[q];
     if ((rc = make_map(&P.a[0], B16, 2, a_hi[q], n, k, lda, KSTEP, tc::BM, &P.a_col0[0], S64)) ||
-        (rc = make_map(&P.a[1], B16, 2, a_lo[q], n, k, lda, KSTEP, tc::BM, &P.a_col0[1], S64)) ||
-        (rc = make_map(&P.b[0], B16, 2, b_hi[q], m, k, ldb, KSTEP, L::BNH, &P.b_col0[0], S64)) ||
-        (rc = make_map(&P.b[1], B16, 2, b_lo[q], m, k, ldb, KSTEP, L::BNH, &P.b_col0[1], S64)))
+        (rc = make_map(&P.a[1], B16, 2, a_lo[q], n, k, lda, KSTEP, tc::BM, &P.a_col0[1], S64)))
       return rc;
+    if (b_natural) {
+      if ((rc = make_map(&P.b[0], B16, 2, b_hi[q], k, m, ldb, 64, KSTEP, &P.b_col0[0], CU_TENSOR_MAP_SWIZZLE_128B)) ||
+          (rc = make_map(&P.b[1], B16, 2, b_lo[q], k, m, ldb, 64, KSTEP, &P.b_col0[1], CU_TENSOR_MAP_SWIZZLE_128B)))
+        return rc;
+    } else if ((rc = make_map(&P.b[0], B16, 2, b_hi[q], m, k, ldb, KSTEP, L::BNH, &P.b_col0[0], S64)) ||
+               (rc = make_map(&P.b[1], B16, 2, b_lo[q], m, k, ldb, KSTEP, L::BNH, &P.b_col0[1], S64))) {
+      return rc;
+    }
     P.a2 = P.a[0];  // never loaded; valid maps for prefetch.tensormap
     P.b2 = P.b[0];
     P.ndst = ndst[q];
@@ -2613,7 +2637,7 @@ int launch_mm_bf16x3_multi(int device, cudaStream_t stream, int count, const voi
   }
   std::lock_guard<std::mutex> pl(g_pdl_mu);
   pdl_record(device, stream, count, ndst, dst, nullptr, ldc, n, m);
-  return run_pair(device, stream, maps, count, n, m, k, 0, 5);
+  return run_pair(device, stream, maps, count, n, m, k, 0, b_natural ? 6 : 5);
 }
 
 int launch_tf32b2_split(cudaStream_t stream, int nin, const void* const* ins, const int64_t* lds,

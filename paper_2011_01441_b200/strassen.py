@@ -696,7 +696,8 @@ def _split_all(src: View, table, transpose: bool, stream, keep: list) -> list:
     return _split_terms([(1, src)], table, transpose, stream, keep)
 
 
-def _leaf_level_b3(A: View, Bt: View, dests, stream, pre=None, h: int | None = None, dev: int | None = None) -> None:
+def _leaf_level_b3(A: View, Bt: View, dests, stream, pre=None, h: int | None = None, dev: int | None = None,
+                   bnat: bool = False) -> None:
     """Leaf-level node, B given transposed, leaves in the bf16x3 format: the seven
     S_r and T_r^T are written as bf16 (hi, lo) planes by one
     ``paco_lincomb_split`` pass per side, and the seven products are one
@@ -708,7 +709,7 @@ def _leaf_level_b3(A: View, Bt: View, dests, stream, pre=None, h: int | None = N
     if pre is None:
         keep = []
         S_ = _split_all(A, S_TERMS, False, stream, keep)
-        T_ = _split_all(Bt, T_TERMS, True, stream, keep)
+        T_ = _split_all(Bt, T_TERMS, not bnat, stream, keep)   # bnat: Bt is B itself (k x m)
     else:  # formed already (_preform_b3 on the side stream, or from level-0 blocks)
         S_, T_, keep, ev = pre
         if ev is not None:
@@ -729,9 +730,9 @@ def _leaf_level_b3(A: View, Bt: View, dests, stream, pre=None, h: int | None = N
             elif v.ld != ld:
                 raise ValueError("destinations must share one row pitch")
     arr = lambda vs: (ctypes.c_void_p * 7)(*vs)  # noqa: E731
-    nat.check(nat.load().paco_mm_bf16x3_multi(dev, stream.cuda_stream, 7, arr([a for a, _ in S_]),
-                                              arr([a for _, a in S_]), h, arr([b for b, _ in T_]),
-                                              arr([b for _, b in T_]), h, ndst, dst, sign, ld, h, h, h))
+    fn = nat.load().paco_mm_bf16x3_multi_bn if bnat else nat.load().paco_mm_bf16x3_multi
+    nat.check(fn(dev, stream.cuda_stream, 7, arr([a for a, _ in S_]), arr([a for _, a in S_]), h,
+                 arr([b for b, _ in T_]), arr([b for _, b in T_]), h, ndst, dst, sign, ld, h, h, h))
     for t in keep:
         t.record_stream(stream)
 
@@ -781,6 +782,36 @@ def _default_leaf(n: int, base: int):
             return _leaf_level_b3 if LEAF_BF16X3 and (n // 2) % 8 == 0 else _leaf_level_b2raw
         n //= 2
     return _leaf_level_b2raw
+
+
+def _b3n_ok(n: int, base: int, dests) -> bool:
+    """The bf16x3 leaves can take B in its own layout (no transpose): the node is a
+    leaf-level node, or its children are (direct formation from its quadrants)."""
+    if not (LEAF_BF16X3 and B3_NATURAL and B3_DIRECT) or n % 2:
+        return False
+    h = n // 2
+    if _leaf_level(n, base):
+        return h % 8 == 0 and len(dests) <= 2
+    if not (_leaf_level(h, base) and h % 2 == 0 and (h // 2) % 8 == 0):
+        return False
+    return all(len([1 for _ in dests for _c in M_DESTS[r]]) <= 2 for r in range(1, 8))
+
+
+def _strassen_b3n(A: View, B: View, dests, base: int, stream) -> None:
+    """dests (+/-)= A x B in bf16x3 with B in its own k x m layout (``_b3n_ok``):
+    T_r planes formed from B's quadrants and read by the MMA as MN-major tiles,
+    so B is never transposed."""
+    n = A.rows
+    if _leaf_level(n, base):
+        _leaf_level_b3(A, B, dests, stream, bnat=True)
+        return
+    h = n // 2
+    for r in range(1, 8):
+        child = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
+        ck = []
+        S_ = _split_terms([(c, _quad(A, q)) for c, q in S_TERMS[r]], S_TERMS, False, stream, ck)
+        T_ = _split_terms([(c, _quad(B, q)) for c, q in T_TERMS[r]], T_TERMS, False, stream, ck)
+        _leaf_level_b3(None, None, child, stream, pre=(S_, T_, ck, None), h=h // 2, dev=A.device, bnat=True)
 
 
 def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream, leaf=None) -> None:
@@ -910,8 +941,11 @@ def strassen_into(A: View, B: View, dests, base: int, stream) -> bool:
             return False
         _leaf_multi(A, B, dests, stream)
         return True
+    if A.ptr % 16 == 0 and A.ld % 4 == 0 and B.ptr % 16 == 0 and B.ld % 4 == 0 and _b3n_ok(n, base, dests):
+        _strassen_b3n(A, B, dests, base, stream)   # the default: bf16x3, B in its own layout
+        return True
     if TF32B2 and TF32B2_RAW and A.ptr % 16 == 0 and A.ld % 4 == 0 and _b2raw_ok(n, base):
-        # the default single-GPU leaves: plain fp32 operands, B transposed once
+        # the single-GPU leaves: plain fp32 operands, B transposed once
         _strassen_tc_fused_t(A, _transpose(B, stream), dests, base, stream, leaf=_default_leaf(n, base))
         return True
     if _leaf_level(n, base) and len(dests) > 2:
@@ -962,6 +996,9 @@ B3_OVERLAP = False
 # paco_lincomb_split: S_r's quadrant q = the sum of its terms' quadrants q), so the level-1
 # fp32 sums are never written or re-read
 B3_DIRECT = True
+# ... and B in its own k x m layout: T_r planes formed from B's quadrants, read by the MMA
+# as MN-major tiles (paco_mm_bf16x3_multi_bn), so B is never transposed
+B3_NATURAL = True
 
 
 def _pair_batch(n: int, m: int, count: int) -> bool:
@@ -979,7 +1016,9 @@ def _strassen_dev(A: View, B: View, C: View, base: int, dtype: torch.dtype, stre
     if kid == nat.SR_F32_TC and FUSED_COMBINE and (C.ld * 4) % 16 == 0 and C.ptr % 16 == 0:
         launch_fill(nat.SR_F32, stream, C)
         aligned = A.ptr % 16 == 0 and (A.ld * 4) % 16 == 0
-        if TF32B2 and TF32B2_RAW and aligned and _b2raw_ok(C.rows, base):
+        if aligned and B.ptr % 16 == 0 and (B.ld * 4) % 16 == 0 and _b3n_ok(C.rows, base, [(C, 1)]):
+            _strassen_b3n(A, B, [(C, 1)], base, stream)
+        elif TF32B2 and TF32B2_RAW and aligned and _b2raw_ok(C.rows, base):
             _strassen_tc_fused_t(A, _transpose(B, stream), [(C, 1)], base, stream, leaf=_default_leaf(C.rows, base))
         elif FUSED_PRODUCER and _fused_producer_ok(C.rows, base) and aligned:
             _strassen_tc_fused_t(A, _transpose(B, stream), [(C, 1)], base, stream)

@@ -76,10 +76,12 @@ def test_lincomb_split_eight_inputs():
         assert float((rec - want).abs().max() / want.abs().max()) <= 2.0 ** -15
 
 
-@pytest.mark.parametrize("shape", [(2048, 2048, 512, 4), (2000, 1800, 336, 7), (256, 256, 32, 1)])
-def test_bf16x3_pair_kernel_accuracy(shape):
+@pytest.mark.parametrize("bnat", [False, True])
+@pytest.mark.parametrize("shape", [(2048, 2048, 512, 4), (2000, 1800, 336, 7), (256, 256, 32, 1), (384, 200, 72, 2)])
+def test_bf16x3_pair_kernel_accuracy(shape, bnat):
     """Products vs float64 of the fp32 operands: two signed destinations per
-    product, ragged extents (TMA zero fill at tile edges), count 1..7."""
+    product, ragged extents (TMA zero fill at tile edges), count 1..7; B given
+    as B^T (K-major tiles) or in its own k x m layout (bnat: MN-major tiles)."""
     n, m, k, cnt = shape
     lib = nat.load()
     st = torch.cuda.current_stream().cuda_stream
@@ -87,7 +89,7 @@ def test_bf16x3_pair_kernel_accuracy(shape):
     a = [(torch.rand(n, k, device="cuda", generator=g) * 2 - 1) for _ in range(cnt)]
     b = [(torch.rand(m, k, device="cuda", generator=g) * 2 - 1) for _ in range(cnt)]
     sa = [_split(lib, st, [x], [[1]]) for x in a]
-    sb = [_split(lib, st, [x], [[1]]) for x in b]
+    sb = [_split(lib, st, [x.t().contiguous() if bnat else x], [[1]]) for x in b]
     lda, ldb = sa[0][0][0].stride(0), sb[0][0][0].stride(0)
     arr = lambda xs: (ctypes.c_void_p * cnt)(*[x.data_ptr() for x in xs])  # noqa: E731
     C = [torch.zeros(n, m, device="cuda") for _ in range(2)]
@@ -101,9 +103,9 @@ def test_bf16x3_pair_kernel_accuracy(shape):
         p = a[q].double() @ b[q].double().t()
         ref[q % 2] += p
         ref[(q + 1) % 2] += -p if q % 2 else p
-    nat.check(lib.paco_mm_bf16x3_multi(0, st, cnt, arr([x[0][0] for x in sa]), arr([x[1][0] for x in sa]), lda,
-                                       arr([x[0][0] for x in sb]), arr([x[1][0] for x in sb]), ldb, ndst, dst, sign,
-                                       m, n, m, k))
+    fn = lib.paco_mm_bf16x3_multi_bn if bnat else lib.paco_mm_bf16x3_multi
+    nat.check(fn(0, st, cnt, arr([x[0][0] for x in sa]), arr([x[1][0] for x in sa]), lda,
+                 arr([x[0][0] for x in sb]), arr([x[1][0] for x in sb]), ldb, ndst, dst, sign, m, n, m, k))
     torch.cuda.synchronize()
     for i in range(2):
         if cnt == 1 and i == 1:
@@ -123,13 +125,15 @@ def test_bf16x3_rejects_misaligned():
     assert rc != 0
 
 
-@pytest.mark.parametrize("direct,overlap", [(True, False), (False, True), (False, False)])
-def test_strassen_bf16x3_vs_tf32b2(monkeypatch, direct, overlap):
+@pytest.mark.parametrize("direct,overlap,natural", [(True, False, True), (True, False, False), (False, True, False),
+                                                    (False, False, False)])
+def test_strassen_bf16x3_vs_tf32b2(monkeypatch, direct, overlap, natural):
     """cfg5's shape at half size (8192, 2 levels): the bf16x3 leaves (default: leaf
-    operands straight from the level-0 blocks; or from level-1 fp32 sums, on the
-    side stream or in line) and the tf32 + 2 x bf16 leaves all within 1e-4 of the
-    f64 product."""
+    operands straight from the level-0 blocks, B in its own layout; or B transposed;
+    or from level-1 fp32 sums, on the side stream or in line) and the tf32 + 2 x
+    bf16 leaves all within 1e-4 of the f64 product."""
     monkeypatch.setattr(S, "B3_DIRECT", direct)
+    monkeypatch.setattr(S, "B3_NATURAL", natural)
     monkeypatch.setattr(S, "B3_OVERLAP", overlap)
     n, base = 8192, 2048
     g = torch.Generator(device="cuda").manual_seed(8)
@@ -143,3 +147,25 @@ def test_strassen_bf16x3_vs_tf32b2(monkeypatch, direct, overlap):
         c = S.strassen_seq(a, b, n, base=base)
         err[b3] = float((c[rows].double() - ref).norm() / ref.norm())
     assert err[True] < 1e-4 and err[False] < 1e-4, err
+
+
+def test_strassen_into_b3n_signed_placements():
+    """strassen_into on a leaf-level node and on a node whose children are
+    leaf-level, B in its own layout, folded +/- into two C blocks."""
+    from paper_2011_01441_b200.device import View
+    for n, base in ((4096, 2048), (8192, 2048)):
+        g = torch.Generator(device="cuda").manual_seed(n)
+        a = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+        b = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+        C = torch.rand(n, 2 * n, device="cuda", generator=g)
+        C0 = C.clone()
+        st = torch.cuda.current_stream()
+        assert S._b3n_ok(n, base, [(None, 1), (None, -1)]) == (n == 4096)
+        dests = [(View.of(C[:, :n]), 1)] if n == 8192 else [(View.of(C[:, :n]), 1), (View.of(C[:, n:]), -1)]
+        assert S.strassen_into(View.of(a), View.of(b), dests, base, st)
+        rows = torch.arange(0, n, 61, device="cuda")
+        ref = a[rows].double() @ b.double()
+        for half, sg in ((0, 1), (1, -1))[:len(dests)]:
+            got = C[rows, half * n:(half + 1) * n].double() - C0[rows, half * n:(half + 1) * n].double()
+            err = float((got - sg * ref).norm() / ref.norm())
+            assert err <= 1e-4, (n, half, err)
