@@ -397,9 +397,22 @@ int launch_lincomb_split(cudaStream_t st, int64_t n, int64_t m, int nin, const v
     return PACO_ERR_UNSUPPORTED;
   }
   KernelSpan ks(PACO_KT_LINCOMB, st);
-  const int64_t xb = (m / 8 + 127) / 128, yb = n < 65535 ? n : 65535, ycap = 2368 / xb + 1;
-  const dim3 grid(unsigned(xb), unsigned(yb < ycap ? yb : ycap));
-  if (nin <= 4)
+  const int64_t xb = (m / 8 + 127) / 128, yb = n < 65535 ? n : 65535;
+  // one wave: as many row-striding blocks as fit on the 148 SMs at once (a partial
+  // last wave of a fixed 2368-block grid cost ~5 %)
+  static int occ[2] = {0, 0};
+  const int w = nin <= 4 ? 0 : 1;
+  if (!occ[w]) {
+    int b = 0;
+    if (w == 0)
+      PACO_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, lincomb_split_kernel<4>, 128, 0));
+    else
+      PACO_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, lincomb_split_kernel<8>, 128, 0));
+    occ[w] = b > 0 ? b : 1;
+  }
+  const int64_t ywave = int64_t(occ[w]) * kNumSMs / xb;
+  const dim3 grid(unsigned(xb), unsigned(yb < ywave ? yb : (ywave > 0 ? ywave : 1)));
+  if (w == 0)
     lincomb_split_kernel<4><<<grid, 128, 0, st>>>(a, n, m);
   else
     lincomb_split_kernel<8><<<grid, 128, 0, st>>>(a, n, m);
