@@ -106,6 +106,7 @@ def test_strassen_fused_producer_matches_split_path(n, base, monkeypatch):
     calls = []
     real = S._leaf_level_fused
     monkeypatch.setattr(S, "_leaf_level_fused", lambda *x: calls.append(1) or real(*x))
+    monkeypatch.setattr(S, "LEAF_BF16X3", False)   # the 3xTF32 paths under test
     monkeypatch.setattr(S, "FUSED_PRODUCER", True)
     c1 = S.strassen_seq(a, b, n, base=base)
     assert calls, "fused-producer leaves not used"
@@ -269,6 +270,7 @@ def test_strassen_tf32b2_vs_3xtf32(monkeypatch, cv, raw):
     rows = torch.arange(0, n, 61, device="cuda")
     ref = a[rows].double() @ b.double()
     err = {}
+    monkeypatch.setattr(S, "LEAF_BF16X3", False)   # the formats under test, not the bf16x3 default
     monkeypatch.setattr(S, "TF32B2_CONVERT", cv)
     monkeypatch.setattr(S, "TF32B2_RAW", raw)
     for b2 in (True, False):
