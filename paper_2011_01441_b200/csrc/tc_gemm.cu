@@ -69,7 +69,7 @@ struct KindBF16T {
   static constexpr int RING_BYTES = ST * 48 * 1024, EPI_WARPS = EW, EPI_BUFS = EB, KB_MAX = 0, EPI_COLS = EC;
   static constexpr int SWZ = 128;  // operand swizzle (bytes per K-major row)
   static constexpr bool B_KMAJOR = false, B_RES = false, FUSED = false;
-  static constexpr int CONV_WARPS = 0, RAW_STAGES = 0, NT = 0, RAW_BYTES = 0, CPS = 1;
+  static constexpr int CONV_WARPS = 0, RAW_STAGES = 0, NT = 0, RAW_BYTES = 0;
   // F32 accumulate, BF16 A/B (format 1), A K-major, B MN-major (bit 16)
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -92,7 +92,7 @@ struct KindTF32x3T {
   static constexpr int RING_BYTES = ST * 2 * (128 + BN_) * BK * 4, EPI_WARPS = 4, EPI_BUFS = 2, KB_MAX = 0,
                        EPI_COLS = 32, SWZ = BK_ * 4;
   static constexpr bool B_KMAJOR = true, B_RES = false, FUSED = false;  // B^T tiles (the split writes B transposed)
-  static constexpr int CONV_WARPS = 0, RAW_STAGES = 0, NT = 0, RAW_BYTES = 0, CPS = 1;
+  static constexpr int CONV_WARPS = 0, RAW_STAGES = 0, NT = 0, RAW_BYTES = 0;
   // F32 accumulate, TF32 A/B (format 2), both K-major
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -121,7 +121,7 @@ struct KindTF32x3FT {
   static constexpr int BN = 256, BK = 16, UMMA_K = 8, STAGES = ST, ELEM = 4, NOPS = 2, PASSES = 3;
   static constexpr int EPI_WARPS = 4, EPI_BUFS = 2, KB_MAX = 0, EPI_COLS = 16, SWZ = 64;
   static constexpr bool B_KMAJOR = true, B_RES = false, FUSED = true;
-  static constexpr int CONV_WARPS = CW, RAW_STAGES = 0, NT = NT_, RAW_BYTES = 0, CPS = 1;
+  static constexpr int CONV_WARPS = CW, RAW_STAGES = 0, NT = NT_, RAW_BYTES = 0;
   static_assert(NT_ >= 1 && NT_ <= NOPS, "raw terms live in the hi / lo slots");
   static constexpr int RING_BYTES = ST * 2 * (128 + BN) * BK * 4;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
@@ -140,16 +140,13 @@ using KindTF32x3F = KindTF32x3FT<PACO_TF32F_ST, 2, PACO_TF32F_CW>;
 // 128 KB from L2 for every 128 KB of C it writes, which puts cfg3 on the L2
 // throughput cap instead of HBM.  A ring of AST stages, EB staging buffers
 // per epilogue warp.
-// CPS_ = 2: two CTAs per SM (BN = 128, a 2-stage A ring, <= 113 KB of shared memory
-// and 256 TMEM columns each), so a CTA of the next launch can start on an SM
-// while the other CTA there still drains its last tile.
-template <int AST, int EB, int EW = 8, int EC = 32, int BN_ = 256, int CPS_ = 1>
+template <int AST, int EB, int EW = 8, int EC = 32, int BN_ = 256>
 struct KindBF16Res {
   static constexpr int BN = BN_, BK = 64, UMMA_K = 16, STAGES = AST, ELEM = 2, NOPS = 1, PASSES = 1;
   static constexpr int KB_MAX = 4, EPI_WARPS = EW, EPI_BUFS = EB, EPI_COLS = EC, SWZ = 128;
   static constexpr int RING_BYTES = KB_MAX * BN * BK * 2 + AST * 128 * BK * 2;
   static constexpr bool B_KMAJOR = false, B_RES = true, FUSED = false;
-  static constexpr int CONV_WARPS = 0, RAW_STAGES = 0, NT = 0, RAW_BYTES = 0, CPS = CPS_;
+  static constexpr int CONV_WARPS = 0, RAW_STAGES = 0, NT = 0, RAW_BYTES = 0;
   // F32 accumulate, BF16 A/B, A K-major, B MN-major, N = BN
   static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -418,7 +415,7 @@ struct TcMaps {
 };
 
 template <class K>
-__global__ void __launch_bounds__(Layout<K>::THREADS, K::CPS) tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
+__global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcArgs args) {
   using L = Layout<K>;
   constexpr int STAGES = K::STAGES, BN = K::BN, BK = K::BK;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -2035,7 +2032,7 @@ int run_tc(int device, Scratch& sc, cudaStream_t stream, const tc::TcMaps& maps,
     set_error("tcgen05 path: too many tiles");
     return PACO_ERR_ARG;
   }
-  const int grid = int(tiles < kNumSMs * K::CPS ? tiles : kNumSMs * K::CPS);
+  const int grid = int(tiles < kNumSMs ? tiles : kNumSMs);
   // resident B: one group per column block, but only as many groups as divide
   // the grid evenly (148 = 4 x 37), else the groups' CTA counts differ and the
   // smaller groups finish last; a group then walks several column blocks.
@@ -2320,8 +2317,6 @@ int launch_mm_bf16_tc(int device, cudaStream_t stream, const void* A, int64_t ld
   // DESIGN.md section 6); PACO_TC_RESV=-1 forces the streaming kind.
   static const int resv = dev_knob("PACO_TC_RESV") ? atoi(dev_knob("PACO_TC_RESV")) : 7;
 #define PACO_TC_GO(KIND) return launch_tc<KIND>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags)
-  static const int res2 = dev_knob("PACO_TC_RES2") ? atoi(dev_knob("PACO_TC_RES2")) : 0;
-  if (k <= 256 && resv >= 0 && res2 == 1) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<2, 1, 4, 16, 128, 2>));
   if (k <= 256 && resv >= 0) PACO_TC_GO(PACO_TC_ARGS(tc::KindBF16Res<PACO_RES_AST, PACO_RES_EB, 8, PACO_RES_EC>));
 #undef PACO_TC_GO
   return launch_tc<tc::KindBF16>(device, stream, A, lda, B, ldb, C, ldc, n, m, k, pieces, n_pieces, flags);
