@@ -298,6 +298,15 @@ int paco_lincomb_split(int device, void* stream, int64_t n, int64_t m, int nin, 
                        const int64_t* lds, int nout, void* const* his, void* const* los, const int64_t* ldo,
                        const int32_t* coefs);
 
+/* All 49 leaf operands of one side of a 2-level Strassen in one pass: x is the
+ * 4h x 4h operand (A: side 0, S formulas; B in its own layout: side 1, T
+ * formulas), leaf (r, r') (r, r' = 1..7, output index 7 (r - 1) + r' - 1) is the
+ * signed sum of x's 4 x 4 blocks of size h given by formula r over the
+ * quadrants and r' over their sub-quadrants, written as
+ * bf16 hi / lo planes (pitch ldo).  Every element of x is read once. */
+int paco_strassen_split49(int device, void* stream, int side, const void* x, int64_t ldx, int64_t h,
+                          void* const* his, void* const* los, int64_t ldo);
+
 /* bf16x3 batch on tcgen05 CTA pairs -- cfg5's Strassen leaf products: C[q] (+/-)=
  * A[q] B[q] with A[q] = a_hi[q] + a_lo[q] (bf16 planes, n x k, pitch lda) and
  * B[q]^T = b_hi[q] + b_lo[q] (m x k, pitch ldb), computed as hi*hi + hi*lo +

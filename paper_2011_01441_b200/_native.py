@@ -101,6 +101,8 @@ SIGNATURES = {
     "paco_mm_bf16x3_multi": (_int, [_int, _vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64,
                                     ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, ctypes.POINTER(ctypes.c_int32),
                                     ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),
+    "paco_strassen_split49": (_int, [_int, _vp, _int, _vp, _i64, _i64, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                     _i64]),
     "paco_mm_bf16x3_multi_bn": (_int, [_int, _vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64,
                                        ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i64, ctypes.POINTER(ctypes.c_int32),
                                        ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int32), _i64, _i64, _i64, _i64]),

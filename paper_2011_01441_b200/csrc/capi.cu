@@ -121,6 +121,8 @@ int launch_transpose(cudaStream_t st, int elsize, void* dst, int64_t ldd, const 
                      int64_t cols);
 int launch_lincomb_multi(cudaStream_t st, int64_t n, int64_t m, int nin, const void* const* ins, const int64_t* lds,
                          int nout, void* const* outs, const int64_t* ldo, const int32_t* coefs);
+int launch_strassen_split49(cudaStream_t st, int side, const void* x, int64_t ldx, int64_t h, void* const* his,
+                            void* const* los, int64_t ldo);
 int launch_lincomb_split(cudaStream_t st, int64_t n, int64_t m, int nin, const void* const* ins, const int64_t* lds,
                          int nout, void* const* his, void* const* los, const int64_t* ldo, const int32_t* coefs);
 int launch_mm_bf16x3_multi(int device, cudaStream_t stream, int count, const void* const* a_hi,
@@ -322,6 +324,22 @@ int paco_lincomb_split(int device, void* stream, int64_t n, int64_t m, int nin, 
   DeviceGuard dg;
   PACO_TRY(dg.use(device));
   return launch_lincomb_split(static_cast<cudaStream_t>(stream), n, m, nin, ins, lds, nout, his, los, ldo, coefs);
+}
+
+int paco_strassen_split49(int device, void* stream, int side, const void* x, int64_t ldx, int64_t h,
+                          void* const* his, void* const* los, int64_t ldo) {
+  if (!x || !his || !los || (side != 0 && side != 1)) {
+    set_error("paco_strassen_split49: null arrays or side not 0 (S) / 1 (T)");
+    return PACO_ERR_ARG;
+  }
+  PACO_TRY(check_view("x", x, ldx, 4 * h, 4 * h));
+  for (int o = 0; o < 49; ++o) {
+    PACO_TRY(check_view("hi", his[o], ldo, h, h));
+    PACO_TRY(check_view("lo", los[o], ldo, h, h));
+  }
+  DeviceGuard dg;
+  PACO_TRY(dg.use(device));
+  return launch_strassen_split49(static_cast<cudaStream_t>(stream), side, x, ldx, h, his, los, ldo);
 }
 
 int paco_mm_bf16x3_multi(int device, void* stream, int count, const void* const* a_hi, const void* const* a_lo,

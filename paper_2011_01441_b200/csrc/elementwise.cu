@@ -420,6 +420,117 @@ int launch_lincomb_split(cudaStream_t st, int64_t n, int64_t m, int nin, const v
   return PACO_OK;
 }
 
+// All 49 leaf operands of a 2-level Strassen side in ONE pass over the 16
+// level-0 blocks X[q1][q2] (q = 00, 01, 10, 11; X = A for the S side, B for
+// the T side, both in natural orientation): leaf (r, r') = sum over the terms
+// (c1, q1) of formula r and (c2, q2) of formula r' of c1 c2 X[q1][q2]
+// (PAPER.md:1839-1852), written as bf16 hi / lo planes.  Each block is read
+// once (the per-node passes re-read a level-0 block once per term: 3 GB vs
+// 1 GB per side at cfg5).  The formulas are compile-time tables, so after
+// unrolling every input index is a register.
+struct Split49Args {
+  const float* x;      // the n x n operand, n = 4 h
+  int64_t ldx;
+  __nv_bfloat16* hi[49];
+  __nv_bfloat16* lo[49];
+  int64_t ldo;
+};
+struct StrassenTab {
+  int8_t q[7][2], c[7][2];
+};
+__host__ __device__ constexpr StrassenTab strassen_tab(bool t) {
+  // formula r (0..6) -> up to two terms: quadrant q (00, 01, 10, 11 = 0..3; -1 = none)
+  // with sign c -- strassen.py S_TERMS (A's terms) / T_TERMS (B's terms)
+  return t ? StrassenTab{{{0, 3}, {0, -1}, {1, 3}, {2, 0}, {3, -1}, {0, 1}, {2, 3}},
+                         {{1, 1}, {1, 0}, {1, -1}, {1, -1}, {1, 0}, {1, 1}, {1, 1}}}
+           : StrassenTab{{{0, 3}, {2, 3}, {0, -1}, {3, -1}, {0, 1}, {2, 0}, {1, 3}},
+                         {{1, 1}, {1, 1}, {1, 0}, {1, 0}, {1, 1}, {1, -1}, {1, -1}}};
+}
+
+template <bool T>
+__global__ void __launch_bounds__(128) strassen_split49_kernel(const Split49Args a, int64_t h) {
+  // four columns per thread: 64 input registers, so four CTAs fit per SM and the
+  // next row's loads of one warp overlap another warp's 98 plane stores
+  constexpr StrassenTab tab = strassen_tab(T);
+  const int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (j >= h) return;
+  for (int64_t i = blockIdx.y; i < h; i += gridDim.y) {
+    float x[16][4];  // [q1 * 4 + q2][column]
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+      const int q1 = b >> 2, q2 = b & 3;
+      const int64_t row = (q1 >> 1) * 2 * h + (q2 >> 1) * h + i, col = (q1 & 1) * 2 * h + (q2 & 1) * h + j;
+      const float4 u = __ldcs(reinterpret_cast<const float4*>(a.x + row * a.ldx + col));
+      x[b][0] = u.x; x[b][1] = u.y; x[b][2] = u.z; x[b][3] = u.w;
+    }
+#pragma unroll
+    for (int r = 0; r < 7; ++r)
+#pragma unroll
+      for (int r2 = 0; r2 < 7; ++r2) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int t1 = 0; t1 < 2; ++t1)
+#pragma unroll
+          for (int t2 = 0; t2 < 2; ++t2) {
+            const int q1 = tab.q[r][t1], q2 = tab.q[r2][t2];
+            if (q1 < 0 || q2 < 0) continue;
+            const int c = tab.c[r][t1] * tab.c[r2][t2];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = c > 0 ? v[e] + x[q1 * 4 + q2][e] : v[e] - x[q1 * 4 + q2][e];
+          }
+        uint32_t hh[2], ll[2];
+#pragma unroll
+        for (int e = 0; e < 4; e += 2) {
+          const __nv_bfloat16 h0 = __float2bfloat16_rn(v[e]), h1 = __float2bfloat16_rn(v[e + 1]);
+          hh[e / 2] = bf16x2_bits(h0, h1);
+          ll[e / 2] = bf16x2_bits(__float2bfloat16_rn(v[e] - __bfloat162float(h0)),
+                                  __float2bfloat16_rn(v[e + 1] - __bfloat162float(h1)));
+        }
+        const int o = r * 7 + r2;
+        __stcs(reinterpret_cast<uint2*>(a.hi[o] + i * a.ldo + j), make_uint2(hh[0], hh[1]));
+        __stcs(reinterpret_cast<uint2*>(a.lo[o] + i * a.ldo + j), make_uint2(ll[0], ll[1]));
+      }
+  }
+}
+
+int launch_strassen_split49(cudaStream_t st, int side, const void* x, int64_t ldx, int64_t h, void* const* his,
+                            void* const* los, int64_t ldo) {
+  if (h <= 0) return PACO_OK;
+  Split49Args a{};
+  a.x = static_cast<const float*>(x);
+  a.ldx = ldx;
+  a.ldo = ldo;
+  bool ok = h % 8 == 0 && ldx % 4 == 0 && ldo % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0;
+  for (int o = 0; o < 49; ++o) {
+    a.hi[o] = static_cast<__nv_bfloat16*>(his[o]);
+    a.lo[o] = static_cast<__nv_bfloat16*>(los[o]);
+    ok = ok && reinterpret_cast<uintptr_t>(his[o]) % 16 == 0 && reinterpret_cast<uintptr_t>(los[o]) % 16 == 0;
+  }
+  if (!ok) {
+    set_error("paco_strassen_split49: 16-byte aligned operand and planes, h %% 8 == 0");
+    return PACO_ERR_UNSUPPORTED;
+  }
+  KernelSpan ks(PACO_KT_LINCOMB, st);
+  static int occ[2] = {0, 0};
+  const int w = side ? 1 : 0;
+  if (!occ[w]) {
+    int b = 0;
+    if (w)
+      PACO_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, strassen_split49_kernel<true>, 128, 0));
+    else
+      PACO_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, strassen_split49_kernel<false>, 128, 0));
+    occ[w] = b > 0 ? b : 1;
+  }
+  const int64_t xb = (h / 4 + 127) / 128, ywave = int64_t(occ[w]) * kNumSMs / xb;
+  const dim3 grid(unsigned(xb), unsigned(h < ywave ? h : (ywave > 0 ? ywave : 1)));
+  if (w)
+    strassen_split49_kernel<true><<<grid, 128, 0, st>>>(a, h);
+  else
+    strassen_split49_kernel<false><<<grid, 128, 0, st>>>(a, h);
+  PACO_CUDA_TRY(cudaGetLastError());
+  return PACO_OK;
+}
+
 int launch_lincomb(int dtype, cudaStream_t st, void* out, int64_t ldo, int64_t n, int64_t m, int nin,
                    const void* const* ins, const int64_t* lds, const int32_t* coefs, int acc) {
   if (nin < 0 || nin > 4) {

@@ -806,12 +806,30 @@ def _strassen_b3n(A: View, B: View, dests, base: int, stream) -> None:
         _leaf_level_b3(A, B, dests, stream, bnat=True)
         return
     h = n // 2
+    hq = h // 2
+    if B3_ONEPASS and n % 4 == 0 and hq % 8 == 0:
+        # all 49 leaf operands of each side in one pass over the operand
+        planes = torch.empty((2, 2, 49, hq, hq), dtype=torch.bfloat16, device=A.device)
+        lib = nat.load()
+        for side, X in ((0, A), (1, B)):
+            his = (ctypes.c_void_p * 49)(*[planes[side, 0, o].data_ptr() for o in range(49)])
+            los = (ctypes.c_void_p * 49)(*[planes[side, 1, o].data_ptr() for o in range(49)])
+            nat.check(lib.paco_strassen_split49(A.device, stream.cuda_stream, side, X.ptr, X.ld, hq, his, los, hq))
+        addr = lambda side, part, o: planes[side, part, o].data_ptr()  # noqa: E731
+        for r in range(1, 8):
+            child = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
+            os_ = [7 * (r - 1) + r2 for r2 in range(7)]
+            S_ = [(addr(0, 0, o), addr(0, 1, o)) for o in os_]
+            T_ = [(addr(1, 0, o), addr(1, 1, o)) for o in os_]
+            _leaf_level_b3(None, None, child, stream, pre=(S_, T_, [], None), h=hq, dev=A.device, bnat=True)
+        planes.record_stream(stream)
+        return
     for r in range(1, 8):
         child = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
         ck = []
         S_ = _split_terms([(c, _quad(A, q)) for c, q in S_TERMS[r]], S_TERMS, False, stream, ck)
         T_ = _split_terms([(c, _quad(B, q)) for c, q in T_TERMS[r]], T_TERMS, False, stream, ck)
-        _leaf_level_b3(None, None, child, stream, pre=(S_, T_, ck, None), h=h // 2, dev=A.device, bnat=True)
+        _leaf_level_b3(None, None, child, stream, pre=(S_, T_, ck, None), h=hq, dev=A.device, bnat=True)
 
 
 def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream, leaf=None) -> None:
@@ -999,6 +1017,10 @@ B3_DIRECT = True
 # ... and B in its own k x m layout: T_r planes formed from B's quadrants, read by the MMA
 # as MN-major tiles (paco_mm_bf16x3_multi_bn), so B is never transposed
 B3_NATURAL = True
+# ... with all 49 leaf operands of each side formed in ONE pass over A / B
+# (paco_strassen_split49: every element read once, instead of once per term of its
+# level-1 formula)
+B3_ONEPASS = True
 
 
 def _pair_batch(n: int, m: int, count: int) -> bool:

@@ -125,15 +125,17 @@ def test_bf16x3_rejects_misaligned():
     assert rc != 0
 
 
-@pytest.mark.parametrize("direct,overlap,natural", [(True, False, True), (True, False, False), (False, True, False),
-                                                    (False, False, False)])
-def test_strassen_bf16x3_vs_tf32b2(monkeypatch, direct, overlap, natural):
+@pytest.mark.parametrize("direct,overlap,natural,onepass", [(True, False, True, True), (True, False, True, False),
+                                                            (True, False, False, False), (False, True, False, False),
+                                                            (False, False, False, False)])
+def test_strassen_bf16x3_vs_tf32b2(monkeypatch, direct, overlap, natural, onepass):
     """cfg5's shape at half size (8192, 2 levels): the bf16x3 leaves (default: leaf
     operands straight from the level-0 blocks, B in its own layout; or B transposed;
     or from level-1 fp32 sums, on the side stream or in line) and the tf32 + 2 x
     bf16 leaves all within 1e-4 of the f64 product."""
     monkeypatch.setattr(S, "B3_DIRECT", direct)
     monkeypatch.setattr(S, "B3_NATURAL", natural)
+    monkeypatch.setattr(S, "B3_ONEPASS", onepass)
     monkeypatch.setattr(S, "B3_OVERLAP", overlap)
     n, base = 8192, 2048
     g = torch.Generator(device="cuda").manual_seed(8)
@@ -169,3 +171,30 @@ def test_strassen_into_b3n_signed_placements():
             got = C[rows, half * n:(half + 1) * n].double() - C0[rows, half * n:(half + 1) * n].double()
             err = float((got - sg * ref).norm() / ref.norm())
             assert err <= 1e-4, (n, half, err)
+
+
+@pytest.mark.parametrize("side", [0, 1])
+def test_strassen_split49(side):
+    """paco_strassen_split49: leaf (r, r') = formula r over the quadrants and r' over
+    their sub-quadrants, as bf16 hi / lo planes (hi + lo within 2^-15 of the f64 sum)."""
+    h = 264
+    n = 4 * h
+    lib = nat.load()
+    st = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(side)
+    big = torch.rand(n, n + 8, device="cuda", generator=g) * 2 - 1
+    x = big[:, :n]
+    planes = torch.full((2, 49, h, h + 8), float("nan"), device="cuda").bfloat16()
+    his = (ctypes.c_void_p * 49)(*[planes[0, o].data_ptr() for o in range(49)])
+    los = (ctypes.c_void_p * 49)(*[planes[1, o].data_ptr() for o in range(49)])
+    nat.check(lib.paco_strassen_split49(0, st, side, x.data_ptr(), x.stride(0), h, his, los, h + 8))
+    torch.cuda.synchronize()
+    names = ("00", "01", "10", "11")
+    tab = S.T_TERMS if side else S.S_TERMS
+    blk = lambda q1, q2: x[(names.index(q1) >> 1) * 2 * h + (names.index(q2) >> 1) * h:][:h, (names.index(q1) & 1) * 2 * h + (names.index(q2) & 1) * h:][:, :h]  # noqa: E731
+    for r in range(1, 8):
+        for r2 in range(1, 8):
+            want = sum(c1 * c2 * blk(q1, q2).double() for c1, q1 in tab[r] for c2, q2 in tab[r2])
+            o = 7 * (r - 1) + r2 - 1
+            got = planes[0, o, :, :h].double() + planes[1, o, :, :h].double()
+            assert float((got - want).abs().max()) <= 2.0 ** -15 * float(want.abs().max()), (r, r2)
