@@ -576,6 +576,16 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
             raw = claim_issue(args);
           }
         }
+        // every claim of this CTA has returned (the last one said "no tile"): the
+        // last CTA to get here re-zeroes the counters for the next launch on this
+        // stream (no memset per launch; that launch claims only after
+        // griddepcontrol.wait, i.e. after this grid completed).  Done here, not at
+        // exit, so the atomic's round trip is off the CTA's exit path.
+        if (atomicAdd(&args.sched[args.groups], 1) == int32_t(gridDim.x) - 1) {
+          for (int g = 0; g < args.groups; ++g) args.sched[g] = 0;
+          args.sched[args.groups] = 0;
+          __threadfence();
+        }
       }
     }
   } else if (warp == 1) {
@@ -869,17 +879,7 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
   tc_fence_after();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(L::TMEM_COLS));
-  if (threadIdx.x == 0) {
-    tc_stamp(args, 15, 2);
-    // every claim of this CTA has returned; the last CTA out re-zeroes the
-    // counters for the next launch on this stream (no memset per launch)
-    __threadfence();
-    if (atomicAdd(&args.sched[args.groups], 1) == int32_t(gridDim.x) - 1) {
-      for (int g = 0; g < args.groups; ++g) args.sched[g] = 0;
-      args.sched[args.groups] = 0;
-      __threadfence();
-    }
-  }
+  if (threadIdx.x == 0) tc_stamp(args, 15, 2);
 }
 
 // ---------------------------------------------------------------------------
