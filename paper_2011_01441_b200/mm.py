@@ -236,6 +236,11 @@ _KP = (128, 2, 2048, 0.25, 16)
 # keeps the GPU fed) and each chunk's staging is cut into ~8 MiB row parts whose
 # DMAs start while the next part is being copied
 _KP_STAGED = (128, 1.5, 2048, 0.25, 16)
+# last-phase row blocks: None = _KP[4] uniform blocks, else geometric decay toward the end
+# (cfg2 end to end from NumPy: 32.02 ms at 0.6, 32.04-32.06 at 0.7, 32.21-32.24 uniform;
+# tools/e2e_rows_ab.py)
+_ROW_DECAY = 0.6
+_ROW_CAP = 2048
 _STAGE_PART_BYTES = 8 << 20
 
 
@@ -389,6 +394,30 @@ def _pipelined_host_mm(A, B, C, kid: int, semiring: Semiring, dev: int, st, over
     d2h.synchronize()
 
 
+def _row_edges(n: int) -> list[int]:
+    """Row blocks of the last phase.  Uniform: _KP[4] blocks.  Geometric
+    (_ROW_DECAY): the blocks shrink by _ROW_DECAY toward the end, from at most
+    _ROW_CAP rows down to 128, so block i's C download still hides behind block
+    i + 1's compute while only the last, smallest download is exposed, with
+    fewer, fuller launches at the front."""
+    if _ROW_DECAY is None or n < 4 * 128:
+        R = max(1, min(int(_KP[4]), n // _PIPE_MIN_ROWS))
+        return [((n * i // R) // 128) * 128 for i in range(R)] + [n]
+    sizes, s_, tot = [], 128.0, 0
+    while tot < n:
+        b = min(n - tot, max(128, int(-(-s_ // 128)) * 128))
+        sizes.append(b)
+        tot += b
+        s_ = min(float(_ROW_CAP), s_ / _ROW_DECAY)
+    if len(sizes) > 1 and sizes[-1] < sizes[-2] // 2:  # fold a small remainder into the first block
+        tail = sizes.pop()
+        sizes[-1] += tail
+    edges = [0]
+    for b in reversed(sizes):
+        edges.append(edges[-1] + b)
+    return edges
+
+
 def _kphased_edges(k: int, kp: tuple = _KP) -> tuple[list[int], int]:
     """k-chunk edges of the front phase (geometric growth from a small first
     chunk, capped) and the start of the row-blocked last phase."""
@@ -442,8 +471,7 @@ def _kphased_host_mm(A, B, C, kid: int, dev: int, st, overwrite: bool, front_sha
         edges, front = [0], 0
     else:
         edges, front = _kphased_edges(k, _KP_STAGED if staged else _KP)
-    R = max(1, min(int(_KP[4]), n // _PIPE_MIN_ROWS))
-    redges = [((n * i // R) // 128) * 128 for i in range(R)] + [n]
+    redges = _row_edges(n)
     h2d = torch.cuda.Stream(device=dev)
     d2h = torch.cuda.Stream(device=dev)
     h2d.wait_stream(st)
@@ -496,7 +524,7 @@ def _kphased_host_mm(A, B, C, kid: int, dev: int, st, overwrite: bool, front_sha
         launch_fold(kid, st, cv, View.of(c_in), reset=False)
     st.wait_event(last_ev)
     outs = []
-    for i in range(R):
+    for i in range(len(redges) - 1):
         r0, r1 = redges[i], redges[i + 1]
         if r1 <= r0:
             continue
