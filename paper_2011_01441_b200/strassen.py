@@ -710,7 +710,7 @@ def _leaf_level_b3(A: View, Bt: View, dests, stream, pre=None, h: int | None = N
         keep = []
         S_ = _split_all(A, S_TERMS, False, stream, keep)
         T_ = _split_all(Bt, T_TERMS, not bnat, stream, keep)   # bnat: Bt is B itself (k x m)
-    else:  # formed already (_preform_b3 on the side stream, or from level-0 blocks)
+    else:  # formed already (from the level-0 blocks: _strassen_tc_fused_t, _strassen_b3n)
         S_, T_, keep, ev = pre
         if ev is not None:
             stream.wait_event(ev)
@@ -735,42 +735,6 @@ def _leaf_level_b3(A: View, Bt: View, dests, stream, pre=None, h: int | None = N
                  arr([b for b, _ in T_]), arr([b for _, b in T_]), h, ndst, dst, sign, ld, h, h, h))
     for t in keep:
         t.record_stream(stream)
-
-
-_SIDE_STREAMS: dict = {}
-
-
-def _side_stream(dev: int):
-    """The per-device stream that forms leaf operands ahead of the leaf launches."""
-    st = _SIDE_STREAMS.get(dev)
-    if st is None:
-        st = _SIDE_STREAMS[dev] = torch.cuda.Stream(device=dev)
-    return st
-
-
-def _preform_b3(nodes, stream) -> dict:
-    """Form the bf16x3 operands of several leaf-level nodes on a side stream, in
-    order, so node r+1's HBM-bound formation pass runs while node r's
-    tensor-bound leaf launch does (the launches only wait for their own node's
-    event).  nodes: {r: (A, Bt)}; returns {r: (S_, T_, keep, event)}."""
-    if not nodes:
-        return {}
-    dev = next(iter(nodes.values()))[0].device
-    side = _side_stream(dev)
-    side.wait_stream(stream)
-    out = {}
-    with torch.cuda.stream(side):
-        for r, (A, Bt) in nodes.items():
-            keep = []
-            S_ = _split_all(A, S_TERMS, False, side, keep)
-            T_ = _split_all(Bt, T_TERMS, True, side, keep)
-            ev = torch.cuda.Event()
-            ev.record(side)
-            for t in keep:
-                t.record_stream(stream)
-            out[r] = (S_, T_, keep, ev)
-    # the node operands (S_all / T_all of the caller) are read on the side stream
-    return out
 
 
 def _default_leaf(n: int, base: int):
@@ -864,18 +828,9 @@ def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream, leaf=None)
         child = [(_quad(D, q), sd * c) for D, sd in dests for c, q in M_DESTS[r]]
         fits = len(child) <= (2 if _leaf_level(h, base) else 1)
         children[r] = (child, h > base and h % 2 == 0 and fits)
-    pre = {}
-    if leaf is _leaf_level_b3 and B3_OVERLAP and _leaf_level(h, base):
-        pre = _preform_b3({r: (S_all[r - 1], T_all[r - 1]) for r in range(1, 8) if children[r][1]}, stream)
-        side = _side_stream(dev)
-        for t in keep:  # the node sums are read by the side stream's formation passes
-            t.record_stream(side)
     for r in range(1, 8):
         S, Tt = S_all[r - 1], T_all[r - 1]
         child, down = children[r]
-        if down and r in pre:
-            _leaf_level_b3(S, Tt, child, stream, pre=pre[r])
-            continue
         if down:
             _strassen_tc_fused_t(S, Tt, child, base, stream, leaf)
             continue
@@ -1005,11 +960,6 @@ TF32B2_RAW = True
 # a 32-deep stage is 32 KB of TMA writes + 48 KB of MMA reads against 768 MMA clocks,
 # so the leaves are tensor-bound instead of shared-memory bound
 LEAF_BF16X3 = True
-# ... with the seven leaf-level nodes' formation passes on a side stream, overlapping the
-# (tensor-bound) leaf launches of the previous nodes.  Off: a wash on cfg5 (16.8-19.5 vs
-# 17.2-18.5 ms in line; tools/cfg5_variants.py) -- the step runs under sw_power_cap, so
-# concurrent HBM passes only move the clock down while the leaves run
-B3_OVERLAP = False
 # ... with each leaf-level node's operands formed straight from the level-0 blocks (8-input
 # paco_lincomb_split: S_r's quadrant q = the sum of its terms' quadrants q), so the level-1
 # fp32 sums are never written or re-read

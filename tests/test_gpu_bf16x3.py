@@ -125,18 +125,16 @@ def test_bf16x3_rejects_misaligned():
     assert rc != 0
 
 
-@pytest.mark.parametrize("direct,overlap,natural,onepass", [(True, False, True, True), (True, False, True, False),
-                                                            (True, False, False, False), (False, True, False, False),
-                                                            (False, False, False, False)])
-def test_strassen_bf16x3_vs_tf32b2(monkeypatch, direct, overlap, natural, onepass):
+@pytest.mark.parametrize("direct,natural,onepass", [(True, True, True), (True, True, False), (True, False, False),
+                                                    (False, False, False)])
+def test_strassen_bf16x3_vs_tf32b2(monkeypatch, direct, natural, onepass):
     """cfg5's shape at half size (8192, 2 levels): the bf16x3 leaves (default: leaf
-    operands straight from the level-0 blocks, B in its own layout; or B transposed;
-    or from level-1 fp32 sums, on the side stream or in line) and the tf32 + 2 x
+    operands of a side in one pass, or per node straight from the level-0 blocks, B
+    in its own layout or transposed; or from level-1 fp32 sums) and the tf32 + 2 x
     bf16 leaves all within 1e-4 of the f64 product."""
     monkeypatch.setattr(S, "B3_DIRECT", direct)
     monkeypatch.setattr(S, "B3_NATURAL", natural)
     monkeypatch.setattr(S, "B3_ONEPASS", onepass)
-    monkeypatch.setattr(S, "B3_OVERLAP", overlap)
     n, base = 8192, 2048
     g = torch.Generator(device="cuda").manual_seed(8)
     a = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
