@@ -319,7 +319,8 @@ struct TcArgs {
   int32_t tiles_rb;  // row blocks
   int32_t tiles_nb;  // column blocks
   int32_t kblocks;
-  int32_t ablate;    // diagnostics: 1 = no C stores, 2 = no MMAs, 4 = no smem staging, 8 = no A loads
+  int32_t ablate;    // diagnostics: 1 = no C stores, 2 = no MMAs, 4 = no smem staging, 8 = no A loads,
+                     // 16 = no resident-B loads
   long long* trace;  // diagnostics (paco_debug_trace): per CTA x 16 tiles x 6 globaltimer stamps
   int32_t* sched;    // per-group tile counters + a CTA-done counter at [groups]
                      // (zero at launch; the last CTA to finish zeroes them again)
@@ -513,6 +514,10 @@ __global__ void __launch_bounds__(Layout<K>::THREADS, 1) tc_gemm_kernel(const __
             if (nb != loaded_nb) {  // (re)load the resident B column block
               if (bloads > 0) mbar_wait(bempty, (bloads - 1) & 1);
               for (int kb = 0; kb < args.kblocks; ++kb) {  // per k block: the first MMA starts early
+                if (args.ablate & 16) {  // diagnostics: the resident B "lands" with no bytes
+                  mbar_arrive(&bfull[kb]);
+                  continue;
+                }
                 mbar_expect_tx_relaxed(&bfull[kb], L::B_BYTES);
 #pragma unroll
                 for (int j = 0; j < BN / L::BOX_N; ++j)
