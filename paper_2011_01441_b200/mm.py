@@ -403,15 +403,17 @@ def _row_edges(n: int) -> list[int]:
     if _ROW_DECAY is None or n < 4 * 128:
         R = max(1, min(int(_KP[4]), n // _PIPE_MIN_ROWS))
         return [((n * i // R) // 128) * 128 for i in range(R)] + [n]
+    n_al = n // 128 * 128  # blocks on tile boundaries; the last absorbs n % 128
     sizes, s_, tot = [], 128.0, 0
-    while tot < n:
-        b = min(n - tot, max(128, int(-(-s_ // 128)) * 128))
+    while tot < n_al:
+        b = min(n_al - tot, max(128, int(-(-s_ // 128)) * 128))
         sizes.append(b)
         tot += b
         s_ = min(float(_ROW_CAP), s_ / _ROW_DECAY)
     if len(sizes) > 1 and sizes[-1] < sizes[-2] // 2:  # fold a small remainder into the first block
         tail = sizes.pop()
         sizes[-1] += tail
+    sizes[0] += n - n_al
     edges = [0]
     for b in reversed(sizes):
         edges.append(edges[-1] + b)

@@ -276,3 +276,19 @@ def test_quantized_one_piece_plan(p):
             return max(-(-t.region.n // 128) * -(-t.region.m // 128) * t.region.k
                        for t in plan.tasks if t.kind == COMPUTE)
         assert worst(pl) <= worst(ref) * 1.02, (n, m, k, p, worst(pl), worst(ref))
+
+
+@pytest.mark.parametrize("n", [512, 1000, 4096, 8192, 16384, 65536])
+def test_host_pipeline_row_blocks(n):
+    """mm_seq's last-phase row blocks (host logic): they tile [0, n) in order, on
+    128-row boundaries except the end, shrink toward the end (geometric schedule)
+    and end with a small block, so only a small download is exposed."""
+    from paper_2011_01441_b200 import mm as MMmod
+    e = MMmod._row_edges(n)
+    assert e[0] == 0 and e[-1] == n and all(b > a for a, b in zip(e, e[1:]))
+    assert all(x % 128 == 0 for x in e[:-1])
+    sizes = [b - a for a, b in zip(e, e[1:])]
+    if MMmod._ROW_DECAY is not None and n >= 4096:
+        assert sizes[-1] == 128 + n % 128
+        assert all(a >= b for a, b in zip(sizes[1:], sizes[2:]))
+        assert max(sizes) <= 2 * MMmod._ROW_CAP
