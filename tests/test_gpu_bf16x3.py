@@ -196,3 +196,14 @@ def test_strassen_split49(side):
             o = 7 * (r - 1) + r2 - 1
             got = planes[0, o, :, :h].double() + planes[1, o, :, :h].double()
             assert float((got - want).abs().max()) <= 2.0 ** -15 * float(want.abs().max()), (r, r2)
+
+
+def test_strassen_split49_rejects_bad_arguments():
+    lib = nat.load()
+    st = torch.cuda.current_stream().cuda_stream
+    x = torch.zeros(4 * 64, 4 * 64, device="cuda")
+    p = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
+    planes = (ctypes.c_void_p * 49)(*([p.data_ptr()] * 49))
+    assert lib.paco_strassen_split49(0, st, 2, x.data_ptr(), 256, 64, planes, planes, 64) != 0      # side
+    assert lib.paco_strassen_split49(0, st, 0, x.data_ptr() + 4, 256, 64, planes, planes, 64) != 0  # misaligned
+    assert lib.paco_strassen_split49(0, st, 0, x.data_ptr(), 256, 60, planes, planes, 64) != 0      # h % 8
