@@ -300,6 +300,11 @@ class FusedDistributedMM:
             # the tcgen05 epilogue folds only into local C (TMA reduce-add): a
             # remote owner's share goes through a staged block
             self.fold_style = "stage"
+        if self.fold_style == "atomic" and self.exchange and not self._probe_remote(self.nat.MM_ATOMIC |
+                                                                                   self.nat.MM_REMOTE):
+            # the element atomics into a peer's IPC-mapped C did not land right on this
+            # fabric (checked once, on every rank): staged folds need only peer copies
+            self.fold_style = "stage"
         self.remote_bulk = self._probe_remote_bulk() if self.fold_style == "atomic" and remote_bulk else False
         # C rectangles of mine that another rank folds into over NVLink: the
         # owner's own folds there must be atomic w.r.t. the peer's at system
@@ -373,19 +378,24 @@ class FusedDistributedMM:
     def _probe_remote_bulk(self) -> bool:
         """Can the TMA bulk-reduce epilogue fold into a peer's IPC-mapped C?
 
-        Each rank folds a small known product into the next rank's buffer with
-        the bulk epilogue, every owner checks what landed against a local
-        computation, and the fused path uses bulk remote folds only if all
-        ranks agree; otherwise remote folds use element atomics (MM_REMOTE).
+        Off unless asked for (remote_bulk=True): a TMA bulk reduction that the
+        fabric rejected would leave a sticky CUDA error, and element atomics
+        over NVLink are always legal for peer-mapped memory.  If it fails,
+        remote folds use element atomics (MM_REMOTE)."""
+        return self._probe_remote(self.nat.MM_ATOMIC, small=False)
+
+    def _probe_remote(self, flags: int, small: bool = True) -> bool:
+        """Does a fold with ``flags`` into a peer's IPC-mapped C land right?
+
+        Each rank folds a small known product into the next rank's buffer,
+        every owner checks what landed against a local computation, and the
+        answer is True only if all ranks agree (collective: call on every rank).
         """
         from .device import View
         from .mm import launch_fill, launch_mm
 
-        # Off unless asked for (remote_bulk=True): a TMA bulk reduction that the
-        # fabric rejected would leave a sticky CUDA error, and element atomics
-        # over NVLink are always legal for peer-mapped memory.
         if self.world == 1 or self.n < 128 or self.m < 128:
-            return False
+            return self.world == 1 or small  # no room to probe: ``small`` is the answer
         dev = self.device
         st = torch.cuda.current_stream(dev)
         g = torch.Generator(device="cpu").manual_seed(1234)
@@ -400,7 +410,7 @@ class FusedDistributedMM:
         pv = View.raw(self.ptrs[peer], 128, 128, 4, dev, ld=self.m * self.itemsize // 4)
         ok = True
         try:
-            launch_mm(probe_sr, st, View.of(a), View.of(b), pv, flags=self.nat.MM_ATOMIC, device=dev)
+            launch_mm(probe_sr, st, View.of(a), View.of(b), pv, flags=flags, device=dev)
             torch.cuda.synchronize(dev)
         except Exception:
             ok = False
