@@ -705,6 +705,9 @@ class MultiGPU:
                                   f"reduction: local ones are fused into the kernels' epilogues, remote ones {how} "
                                   f"(CUDA IPC); fold handshake: {sync if self.ex.exchange else 'none (no k cut)'}; "
                                   "tile-grid CTA plan inside each rank")
+                if self.ex.fold_probe_ms:
+                    self.plan_desc += ("; fold style chosen by a start-up timing probe (1024^3 block, [fused, "
+                                       f"staged] ms per rank: {[[round(x, 3) for x in t] for t in self.ex.fold_probe_ms]})")
             else:
                 self.ex = DistributedMM(plan, sr, CudaOps(sr, kid, st))
                 self.C = torch.empty((n, n), dtype=torch.int32, device=dev)

@@ -243,7 +243,7 @@ class FusedDistributedMM:
     """
 
     def __init__(self, plan: Plan, semiring, kernel_id: int, device: int, *, group=None,
-                 fold_style: str = "atomic", remote_bulk: bool = False):
+                 fold_style: str = "atomic", remote_bulk: bool = False, fold_probe: bool = True):
         import ctypes
         import os
 
@@ -304,6 +304,9 @@ class FusedDistributedMM:
                                                                                    self.nat.MM_REMOTE):
             # the element atomics into a peer's IPC-mapped C did not land right on this
             # fabric (checked once, on every rank): staged folds need only peer copies
+            self.fold_style = "stage"
+        self.fold_probe_ms = None   # [[fused, staged] ms per rank] when the timing probe ran
+        if self.fold_style == "atomic" and self.exchange and fold_probe and not self._atomic_folds_pay():
             self.fold_style = "stage"
         self.remote_bulk = self._probe_remote_bulk() if self.fold_style == "atomic" and remote_bulk else False
         # C rectangles of mine that another rank folds into over NVLink: the
@@ -383,6 +386,60 @@ class FusedDistributedMM:
         over NVLink are always legal for peer-mapped memory.  If it fails,
         remote folds use element atomics (MM_REMOTE)."""
         return self._probe_remote(self.nat.MM_ATOMIC, small=False)
+
+    def _atomic_folds_pay(self, size: int = 1024, slack: float = 1.15) -> bool:
+        """Measure, don't guess: is a block computed with its fold fused into a
+        peer's C (element atomics over the fabric) faster than the staged form
+        (local product, one peer copy, a fold)?  Every rank times both on a
+        size x size x size block of its neighbour's C at the same time (so the
+        links carry the real pattern), best of 3; the fused form is kept unless
+        the slowest rank's fused time exceeds ``slack`` x its staged time."""
+        from .device import View
+        from .mm import launch_fill, launch_fold, launch_mm
+
+        if self.world == 1 or self.n < size or self.m < size or self.itemsize != 4:
+            return True
+        dev = self.device
+        st = torch.cuda.current_stream(dev)
+        kid = self.nat.SR_MINPLUS_SAT32
+        g = torch.Generator(device="cpu").manual_seed(4321)
+        a = torch.randint(0, 2**20, (size, size), generator=g, dtype=torch.int32).to(dev)
+        b = torch.randint(0, 2**20, (size, size), generator=g, dtype=torch.int32).to(dev)
+        tmp = torch.empty((size, size), dtype=torch.int32, device=dev)
+        ld = self.m * self.itemsize // 4
+        peer = (self.rank + 1) % self.world
+        pv = View.raw(self.ptrs[peer], size, size, 4, dev, ld=ld)
+        mine = View.raw(self.own_ptr, size, size, 4, dev, ld=ld)
+
+        def fused():
+            launch_mm(kid, st, View.of(a), View.of(b), pv, flags=self.nat.MM_ATOMIC | self.nat.MM_REMOTE, device=dev)
+
+        def staged():
+            launch_mm(kid, st, View.of(a), View.of(b), View.of(tmp), overwrite=True, device=dev)
+            self.nat.check(self.nat.load().paco_copy2d(dev, st.cuda_stream, self.ptrs[peer], ld * 4,
+                                                       tmp.data_ptr(), size * 4, size * 4, size))
+            launch_fold(kid, st, mine, View.of(tmp), False)   # the owner's fold, same size
+
+        times = []
+        for fn in (fused, staged):
+            best = float("inf")
+            for _ in range(4):
+                torch.cuda.synchronize(dev)
+                dist.barrier(group=self.group)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                fn()
+                e1.record(st)
+                e1.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            times.append(best)
+        launch_fill(kid, st, mine)   # leave this rank's probe block at the semiring zero
+        torch.cuda.synchronize(dev)
+        allt = [None] * self.world
+        dist.all_gather_object(allt, times, group=self.group)
+        dist.barrier(group=self.group)
+        self.fold_probe_ms = allt
+        return max(t[0] for t in allt) <= slack * max(t[1] for t in allt)
 
     def _probe_remote(self, flags: int, small: bool = True) -> bool:
         """Does a fold with ``flags`` into a peer's IPC-mapped C land right?
