@@ -698,22 +698,22 @@ def _split_all(src: View, table, transpose: bool, stream, keep: list) -> list:
 
 def _leaf_level_b3(A: View, Bt: View, dests, stream, pre=None, h: int | None = None, dev: int | None = None,
                    bnat: bool = False) -> None:
-    """Leaf-level node, B given transposed, leaves in the bf16x3 format: the seven
-    S_r and T_r^T are written as bf16 (hi, lo) planes by one
-    ``paco_lincomb_split`` pass per side, and the seven products are one
-    ``paco_mm_bf16x3_multi`` launch (hi*hi + hi*lo + lo*hi on kind::f16, fp32
-    accumulation) whose epilogues reduce-add each product with its signs into
-    its C blocks (M_DESTS)."""
+    """Leaf-level node, leaves in the bf16x3 format: the seven S_r and T_r^T (or,
+    with ``bnat``, T_r in B's own k x m layout) are written as bf16 (hi, lo)
+    planes by one ``paco_lincomb_split`` pass per side -- or arrive formed
+    already as ``pre`` = (S planes, T planes, buffers to keep alive), with ``h``
+    and ``dev`` -- and the seven products are one ``paco_mm_bf16x3_multi(_bn)``
+    launch (hi*hi + hi*lo + lo*hi on kind::f16, fp32 accumulation) whose
+    epilogues reduce-add each product with its signs into its C blocks
+    (M_DESTS; PAPER.md:1839-1852)."""
     if A is not None:
         h, dev = A.rows // 2, A.device
     if pre is None:
         keep = []
         S_ = _split_all(A, S_TERMS, False, stream, keep)
         T_ = _split_all(Bt, T_TERMS, not bnat, stream, keep)   # bnat: Bt is B itself (k x m)
-    else:  # formed already (from the level-0 blocks: _strassen_tc_fused_t, _strassen_b3n)
-        S_, T_, keep, ev = pre
-        if ev is not None:
-            stream.wait_event(ev)
+    else:  # formed already from the level-0 blocks (_strassen_tc_fused_t, _strassen_b3n)
+        S_, T_, keep = pre
     ndst = (ctypes.c_int32 * 7)()
     dst = (ctypes.c_void_p * 28)()
     sign = (ctypes.c_int32 * 28)()
@@ -785,7 +785,7 @@ def _strassen_b3n(A: View, B: View, dests, base: int, stream) -> None:
             os_ = [7 * (r - 1) + r2 for r2 in range(7)]
             S_ = [(addr(0, 0, o), addr(0, 1, o)) for o in os_]
             T_ = [(addr(1, 0, o), addr(1, 1, o)) for o in os_]
-            _leaf_level_b3(None, None, child, stream, pre=(S_, T_, [], None), h=hq, dev=A.device, bnat=True)
+            _leaf_level_b3(None, None, child, stream, pre=(S_, T_, []), h=hq, dev=A.device, bnat=True)
         planes.record_stream(stream)
         return
     for r in range(1, 8):
@@ -793,7 +793,7 @@ def _strassen_b3n(A: View, B: View, dests, base: int, stream) -> None:
         ck = []
         S_ = _split_terms([(c, _quad(A, q)) for c, q in S_TERMS[r]], S_TERMS, False, stream, ck)
         T_ = _split_terms([(c, _quad(B, q)) for c, q in T_TERMS[r]], T_TERMS, False, stream, ck)
-        _leaf_level_b3(None, None, child, stream, pre=(S_, T_, ck, None), h=hq, dev=A.device, bnat=True)
+        _leaf_level_b3(None, None, child, stream, pre=(S_, T_, ck), h=hq, dev=A.device, bnat=True)
 
 
 def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream, leaf=None) -> None:
@@ -819,7 +819,7 @@ def _strassen_tc_fused_t(A: View, Bt: View, dests, base: int, stream, leaf=None)
             ck = []
             S_ = _split_terms([(c, _quad(A, q)) for c, q in S_TERMS[r]], S_TERMS, False, stream, ck)
             T_ = _split_terms([(c, _quad(Bt, _tquad(q))) for c, q in T_TERMS[r]], T_TERMS, True, stream, ck)
-            _leaf_level_b3(None, None, child, stream, pre=(S_, T_, ck, None), h=h // 2, dev=dev)
+            _leaf_level_b3(None, None, child, stream, pre=(S_, T_, ck), h=h // 2, dev=dev)
         return
     S_all = _form_all(A, S_TERMS, False, stream, keep)
     T_all = _form_all(Bt, T_TERMS, True, stream, keep)
